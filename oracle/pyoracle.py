@@ -1,0 +1,321 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes bindings to the oracle.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs may import this module. It binds:
+  * oracle/_build/liboracle.so  — this repo's C restatement (emu_ref.c,
+    ckks_ref.c, mt19937.c): the checker for the product's residues;
+  * oracle/_ref/libshardnn_ref.so — the UNMODIFIED reference sources compiled
+    where they lie (plus ref_shim.cpp); present only where it was built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libshardnn_ref.so")
+
+u64p = C.POINTER(C.c_uint64)
+i64p = C.POINTER(C.c_int64)
+dp = C.POINTER(C.c_double)
+ip = C.POINTER(C.c_int)
+lp = C.POINTER(C.c_long)
+
+
+def build():
+    """Compile the oracle (and oracle/_ref when /root/reference exists)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        L.ck_create.restype = C.c_void_p
+        L.ck_create.argtypes = [C.c_int, C.c_int, ip, C.c_int, ip, C.c_int]
+        L.ck_destroy.argtypes = [C.c_void_p]
+        for name in ("ck_prime", "ck_root"):
+            getattr(L, name).restype = C.c_uint64
+            getattr(L, name).argtypes = [C.c_void_p, C.c_int]
+        L.ck_dnum.argtypes = [C.c_void_p]
+        L.ck_dnum_at.argtypes = [C.c_void_p, C.c_int]
+        L.ck_scale.restype = C.c_double
+        L.ck_scale.argtypes = [C.c_void_p]
+        L.ck_mulmod.restype = C.c_uint64
+        L.ck_mulmod.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.ck_is_prime.argtypes = [C.c_uint64]
+        L.ck_galois_elt.restype = C.c_uint64
+        L.ck_galois_elt.argtypes = [C.c_void_p, C.c_long]
+        L.ck_automorph_ntt.argtypes = [C.c_void_p, u64p, u64p, C.c_uint64]
+        L.ck_automorph_coef.argtypes = [C.c_void_p, C.c_int, u64p, u64p, C.c_uint64]
+        L.ck_ntt_fwd.argtypes = [C.c_void_p, C.c_int, u64p]
+        L.ck_ntt_inv.argtypes = [C.c_void_p, C.c_int, u64p]
+        L.ck_encode.argtypes = [C.c_void_p, dp, C.c_size_t, C.c_double, i64p]
+        L.ck_decode.argtypes = [C.c_void_p, dp, C.c_double, dp]
+        L.ck_encode_plain.argtypes = [C.c_void_p, dp, C.c_size_t, C.c_double, C.c_int, C.c_int, u64p]
+        L.ck_prng.restype = C.c_uint64
+        L.ck_prng.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.ck_keygen.argtypes = [C.c_void_p, C.c_uint64]
+        L.ck_secret_coef.argtypes = [C.c_void_p, i64p]
+        L.ck_galois_key.argtypes = [C.c_void_p, C.c_uint64, u64p]
+        L.ck_encrypt.argtypes = [C.c_void_p, u64p, C.c_int, C.c_uint64, u64p]
+        L.ck_decrypt_coef.argtypes = [C.c_void_p, u64p, C.c_int, dp]
+        L.ck_decrypt_decode.argtypes = [C.c_void_p, u64p, C.c_int, C.c_double, dp]
+        for name in ("ck_add", "ck_mul_plain", "ck_add_plain"):
+            getattr(L, name).argtypes = [C.c_void_p, u64p, u64p, C.c_int, u64p]
+        L.ck_rescale.argtypes = [C.c_void_p, u64p, C.c_int, u64p]
+        L.ck_modup.argtypes = [C.c_void_p, u64p, C.c_int, u64p]
+        L.ck_inner_product.argtypes = [C.c_void_p, u64p, C.c_int, u64p, C.c_uint64, u64p, u64p]
+        L.ck_moddown.argtypes = [C.c_void_p, u64p, C.c_int, u64p]
+        L.ck_rotate.argtypes = [C.c_void_p, u64p, C.c_int, C.c_long, u64p]
+        L.ck_rotate_hoisted.argtypes = [C.c_void_p, u64p, C.c_int, lp, C.c_int, u64p]
+        L.ck_conv.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp,
+                              C.c_int, u64p, dp]
+        L.emu_make_inputs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                      C.c_int, dp, dp]
+        L.emu_rotate.argtypes = [dp, dp, C.c_size_t, C.c_long]
+        L.emu_fused_plain.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, dp, C.c_int,
+                                      C.c_long, C.c_long, C.c_double, dp]
+        L.emu_conv_slots.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, dp, dp,
+                                     C.c_int, dp]
+        L.emu_oracle_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, dp]
+        L.emu_decompose.argtypes = [C.c_int, C.c_uint64, C.c_uint64, lp, C.c_int]
+        L.emu_min_lengths.argtypes = [C.c_uint64, C.c_uint64, u64p]
+        _lib = L
+    return _lib
+
+
+def ref_available():
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        R = C.CDLL(REF_SO)
+        R.ref_make_inputs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                      C.c_int, dp, dp]
+        R.ref_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, C.c_uint64, dp,
+                               dp, u64p, ip]
+        R.ref_oracle_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, dp]
+        R.ref_decompose.argtypes = [C.c_int, C.c_uint64, C.c_uint64, lp, C.c_int]
+        R.ref_min_lengths.argtypes = [C.c_uint64, C.c_uint64, u64p]
+        R.ref_plan_rotations.restype = C.c_long
+        R.ref_plan_rotations.argtypes = [lp, ip, C.c_int, C.c_uint64, C.c_int, lp, ip, ip, ip]
+        R.ref_time_conv.restype = C.c_double
+        R.ref_time_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, C.c_uint64,
+                                    C.c_int, C.c_int]
+        R.ref_time_rotations.restype = C.c_double
+        R.ref_time_rotations.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, u64p]
+        _ref = R
+    return _ref
+
+
+# ---------------------------------------------------------------- emulator
+
+def make_inputs(c, m, kappa, c_out, seed_img, seed_filt, weight_kind=0, use_ref=False):
+    img = np.zeros(c * m * m)
+    filt = np.zeros(c * c_out * kappa * kappa)
+    fn = ref().ref_make_inputs if use_ref else lib().emu_make_inputs
+    rc = fn(c, m, kappa, c_out, seed_img, seed_filt, weight_kind, _ptr(img, dp), _ptr(filt, dp))
+    assert rc in (0, None)
+    return img, filt
+
+
+def emu_conv_slots(c, m, kappa, c_out, s, img, filt, plan):
+    out = np.zeros(s)
+    img = np.ascontiguousarray(img, dtype=np.float64)
+    filt = np.ascontiguousarray(filt, dtype=np.float64)
+    rc = lib().emu_conv_slots(c, m, kappa, c_out, s, _ptr(img, dp), _ptr(filt, dp), plan, _ptr(out, dp))
+    assert rc == 0
+    return out
+
+
+def emu_oracle_conv(c, m, kappa, c_out, img, filt):
+    out = np.zeros(c_out * m * m)
+    lib().emu_oracle_conv(c, m, kappa, c_out, _ptr(np.ascontiguousarray(img), dp),
+                          _ptr(np.ascontiguousarray(filt), dp), _ptr(out, dp))
+    return out
+
+
+def emu_fused_plain(c, m, kappa, c_out, s, filt, r, kk, ll):
+    out = np.zeros(s)
+    ne = lib().emu_fused_plain(c, m, kappa, c_out, s, _ptr(np.ascontiguousarray(filt), dp), r, kk, ll,
+                               1.0, _ptr(out, dp))
+    return out if ne else None
+
+
+def emu_decompose(strategy, n, s):
+    buf = (C.c_long * 64)()
+    k = lib().emu_decompose(strategy, n, s, buf, 64)
+    assert k >= 0
+    return [buf[i] for i in range(k)]
+
+
+def emu_min_lengths(n_max, cap):
+    out = np.zeros(n_max + 1, dtype=np.uint64)
+    assert lib().emu_min_lengths(n_max, cap, _ptr(out, u64p)) == 0
+    return out
+
+
+def ref_conv(c, m, kappa, c_out, img, filt, plan, s):
+    out_slots = np.zeros(s)
+    out_img = np.zeros(c_out * m * m)
+    ledger = np.zeros(9, dtype=np.uint64)
+    drop = C.c_int(0)
+    rc = ref().ref_conv(c, m, kappa, c_out, _ptr(np.ascontiguousarray(img), dp),
+                        _ptr(np.ascontiguousarray(filt), dp), plan, s, _ptr(out_slots, dp),
+                        _ptr(out_img, dp), _ptr(ledger, u64p), C.byref(drop))
+    assert rc == 0
+    return out_slots, out_img, ledger, drop.value
+
+
+# ---------------------------------------------------------------- CKKS model
+
+class CKKS:
+    """Thin owner of a ck_ctx (the CPU golden model)."""
+
+    def __init__(self, logN, qbits, pbits, logscale):
+        L = lib()
+        self.logN, self.N = logN, 1 << logN
+        self.qbits, self.pbits = list(qbits), list(pbits)
+        self.L, self.K = len(qbits), len(pbits)
+        qa = (C.c_int * self.L)(*qbits)
+        pa = (C.c_int * self.K)(*pbits)
+        self.h = L.ck_create(logN, self.L, qa, self.K, pa, logscale)
+        assert self.h
+        self.np = self.L + self.K
+        self.primes = [L.ck_prime(self.h, i) for i in range(self.np)]
+        self.dnum = L.ck_dnum(self.h)
+        self.scale = L.ck_scale(self.h)
+
+    def __del__(self):
+        try:
+            lib().ck_destroy(self.h)
+        except Exception:
+            pass
+
+    def dnum_at(self, level):
+        return lib().ck_dnum_at(self.h, level)
+
+    def keygen(self, seed):
+        lib().ck_keygen(self.h, seed)
+
+    def secret(self):
+        s = np.zeros(self.N, dtype=np.int64)
+        lib().ck_secret_coef(self.h, _ptr(s, i64p))
+        return s
+
+    def galois(self, k):
+        return lib().ck_galois_elt(self.h, k)
+
+    def galois_key(self, g):
+        key = np.zeros((self.dnum, 2, self.np, self.N), dtype=np.uint64)
+        lib().ck_galois_key(self.h, g, _ptr(key, u64p))
+        return key
+
+    def ntt(self, idx, a, inverse=False):
+        a = np.ascontiguousarray(a, dtype=np.uint64).copy()
+        (lib().ck_ntt_inv if inverse else lib().ck_ntt_fwd)(self.h, idx, _ptr(a, u64p))
+        return a
+
+    def encode_coef(self, z, scale):
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        out = np.zeros(self.N, dtype=np.int64)
+        rc = lib().ck_encode(self.h, _ptr(z, dp), len(z), scale, _ptr(out, i64p))
+        assert rc == 0
+        return out
+
+    def decode(self, coef, scale):
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        z = np.zeros(self.N // 2)
+        lib().ck_decode(self.h, _ptr(coef, dp), scale, _ptr(z, dp))
+        return z
+
+    def encode(self, z, scale, level, with_p=False):
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        rows = level + 1 + (self.K if with_p else 0)
+        out = np.zeros((rows, self.N), dtype=np.uint64)
+        rc = lib().ck_encode_plain(self.h, _ptr(z, dp), len(z), scale, level, int(with_p), _ptr(out, u64p))
+        assert rc == 0
+        return out
+
+    def encrypt(self, pt, level, seed):
+        ct = np.zeros((2, level + 1, self.N), dtype=np.uint64)
+        lib().ck_encrypt(self.h, _ptr(np.ascontiguousarray(pt), u64p), level, seed, _ptr(ct, u64p))
+        return ct
+
+    def decrypt(self, ct, level, scale):
+        z = np.zeros(self.N // 2)
+        lib().ck_decrypt_decode(self.h, _ptr(np.ascontiguousarray(ct), u64p), level, scale, _ptr(z, dp))
+        return z
+
+    def decrypt_coef(self, ct, level):
+        z = np.zeros(self.N)
+        lib().ck_decrypt_coef(self.h, _ptr(np.ascontiguousarray(ct), u64p), level, _ptr(z, dp))
+        return z
+
+    def _binop(self, fn, a, b, level):
+        out = np.zeros((2, level + 1, self.N), dtype=np.uint64)
+        fn(self.h, _ptr(np.ascontiguousarray(a), u64p), _ptr(np.ascontiguousarray(b), u64p), level,
+           _ptr(out, u64p))
+        return out
+
+    def add(self, a, b, level):
+        return self._binop(lib().ck_add, a, b, level)
+
+    def mul_plain(self, ct, pt, level):
+        return self._binop(lib().ck_mul_plain, ct, pt, level)
+
+    def add_plain(self, ct, pt, level):
+        return self._binop(lib().ck_add_plain, ct, pt, level)
+
+    def rescale(self, ct, level):
+        out = np.zeros((2, level, self.N), dtype=np.uint64)
+        lib().ck_rescale(self.h, _ptr(np.ascontiguousarray(ct), u64p), level, _ptr(out, u64p))
+        return out
+
+    def modup(self, c1, level):
+        out = np.zeros((self.dnum_at(level), level + 1 + self.K, self.N), dtype=np.uint64)
+        lib().ck_modup(self.h, _ptr(np.ascontiguousarray(c1), u64p), level, _ptr(out, u64p))
+        return out
+
+    def moddown(self, acc, level):
+        out = np.zeros((level + 1, self.N), dtype=np.uint64)
+        lib().ck_moddown(self.h, _ptr(np.ascontiguousarray(acc), u64p), level, _ptr(out, u64p))
+        return out
+
+    def rotate(self, ct, level, k):
+        out = np.zeros((2, level + 1, self.N), dtype=np.uint64)
+        lib().ck_rotate(self.h, _ptr(np.ascontiguousarray(ct), u64p), level, k, _ptr(out, u64p))
+        return out
+
+    def rotate_hoisted(self, ct, level, ks):
+        out = np.zeros((len(ks), 2, level + 1, self.N), dtype=np.uint64)
+        ka = (C.c_long * len(ks))(*ks)
+        lib().ck_rotate_hoisted(self.h, _ptr(np.ascontiguousarray(ct), u64p), level, ka, len(ks),
+                                _ptr(out, u64p))
+        return out
+
+    def conv(self, ct, level, c, m, kappa, c_out, filt, plan):
+        out = np.zeros((2, level, self.N), dtype=np.uint64)
+        sc = C.c_double(0)
+        rc = lib().ck_conv(self.h, _ptr(np.ascontiguousarray(ct), u64p), level, c, m, kappa, c_out,
+                           _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), plan, _ptr(out, u64p),
+                           C.byref(sc))
+        assert rc == 0
+        return out, sc.value

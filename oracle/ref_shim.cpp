@@ -1,0 +1,239 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product (libfheconv).
+//
+// C-ABI shim over the UNMODIFIED reference library (shardnn, compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/). It lets the
+// Python tests and bench.py's reference arm drive the reference's own public
+// API through ctypes:
+//   * conv_plan / convolve  (reference conv.cpp:266-271, :364-371)
+//   * decompose_positive / decompose_signed / min_decomposition_length
+//     (reference rot.cpp:21-46, :84-94)
+//   * plan_rotations + execute_schedule (reference rot.cpp:96-156)
+//   * oracle_conv (reference oracle.cpp:7-31)
+// Inputs are generated with the reference's own test helpers
+// (tests/helpers.hpp:13-27: mt19937_64 + uniform_real_distribution), so the
+// golden vectors are exactly what the reference's tests would see.
+#include "shardnn/conv.hpp"
+#include "shardnn/oracle.hpp"
+#include "shardnn/pack.hpp"
+#include "shardnn/rot.hpp"
+#include "helpers.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+using namespace shardnn;
+using namespace shardnn::testing;
+
+namespace {
+
+// weight_kind: 0 = U[-1,1] (random_filter), 1 = U[-0.5,0.5], 2 = N(0,0.1^2) clipped to [-1,1]
+FilterTensor make_filter(std::mt19937_64& rng, int c_in, int c_out, int kappa, int weight_kind) {
+    if (weight_kind == 0) return random_filter(rng, c_in, c_out, kappa);
+    FilterTensor k(c_in, c_out, kappa);
+    if (weight_kind == 1) {
+        std::uniform_real_distribution<double> dist(-0.5, 0.5);
+        for (double& v : k.weights) v = dist(rng);
+    } else {
+        std::normal_distribution<double> dist(0.0, 0.1);
+        for (double& v : k.weights) v = std::clamp(dist(rng), -1.0, 1.0);
+    }
+    return k;
+}
+
+void fill_ledger(const CostLedger& l, uint64_t* out) {
+    if (!out) return;
+    out[0] = l.rotations.load();
+    out[1] = l.hoisted_rotations.load();
+    out[2] = l.hoist_groups.load();
+    out[3] = l.ct_pt_mults.load();
+    out[4] = l.ct_ct_mults.load();
+    out[5] = l.adds.load();
+    out[6] = l.bootstraps.load();
+    out[7] = static_cast<uint64_t>(l.max_depth_consumed.load());
+    out[8] = l.rotation_amounts().size();
+}
+
+PackedImage run_plan(Engine& eng, const PackedImage& p, const FilterTensor& k, int plan) {
+    if (plan == 1) return conv_plan(eng, p, k, ConvPlan::ChannelFirst);
+    if (plan == 2) return conv_plan(eng, p, k, ConvPlan::ShiftFirst);
+    return convolve(eng, p, k);
+}
+
+}  // namespace
+
+extern "C" {
+
+/// Generates the reference's random inputs and fills img (c*m*m) and filt
+/// (c_in*c_out*kappa^2, reference storage order tensor.hpp:53-58).
+int ref_make_inputs(int c, int m, int kappa, int c_out, uint64_t seed_img, uint64_t seed_filt,
+                    int weight_kind, double* img, double* filt) {
+    try {
+        std::mt19937_64 ri(seed_img);
+        ImageTensor t = random_tensor(ri, c, m);
+        std::mt19937_64 rf(seed_filt);
+        FilterTensor k = make_filter(rf, c, c_out, kappa, weight_kind);
+        std::memcpy(img, t.data.data(), t.data.size() * sizeof(double));
+        std::memcpy(filt, k.weights.data(), k.weights.size() * sizeof(double));
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// Runs pack + conv_plan(plan) on the emulator; writes the raw output shard
+/// slots (s = c*m*m for the single-shard configs), the unpacked image and
+/// the ledger [rot, hoisted, groups, ct_pt, ct_ct, adds, boots, depth, n_amounts].
+int ref_conv(int c, int m, int kappa, int c_out, const double* img, const double* filt,
+             int plan, uint64_t shard_size, double* out_slots, double* out_image,
+             uint64_t* ledger, int* out_level_drop) {
+    try {
+        ImageTensor t(c, m);
+        std::memcpy(t.data.data(), img, t.data.size() * sizeof(double));
+        FilterTensor k(c, c_out, kappa);
+        std::memcpy(k.weights.data(), filt, k.weights.size() * sizeof(double));
+        Engine eng;
+        PackedImage p = pack(eng, t, shard_size);
+        eng.ledger().reset();
+        PackedImage out = run_plan(eng, p, k, plan);
+        if (out_slots) {
+            size_t off = 0;
+            for (const auto& sh : out.shards) {
+                std::memcpy(out_slots + off, sh.slots.data(), sh.slots.size() * sizeof(double));
+                off += sh.slots.size();
+            }
+        }
+        if (out_image) {
+            ImageTensor u = unpack(out);
+            std::memcpy(out_image, u.data.data(), u.data.size() * sizeof(double));
+        }
+        fill_ledger(eng.ledger(), ledger);
+        if (out_level_drop) *out_level_drop = p.min_level() - out.min_level();
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// Textbook same-padding conv (reference oracle.cpp:7-31).
+int ref_oracle_conv(int c, int m, int kappa, int c_out, const double* img, const double* filt,
+                    int stride, double* out) {
+    try {
+        ImageTensor t(c, m);
+        std::memcpy(t.data.data(), img, t.data.size() * sizeof(double));
+        FilterTensor k(c, c_out, kappa);
+        std::memcpy(k.weights.data(), filt, k.weights.size() * sizeof(double));
+        ImageTensor o = oracle_conv(t, k, stride);
+        std::memcpy(out, o.data.data(), o.data.size() * sizeof(double));
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// strategy 0 = positive, 1 = signed. Returns the number of steps (or -1).
+int ref_decompose(int strategy, uint64_t n, uint64_t s, long* steps, int cap) {
+    try {
+        std::vector<long> v = strategy == 0 ? decompose_positive(n, s) : decompose_signed(n, s);
+        if (static_cast<int>(v.size()) > cap) return -1;
+        std::copy(v.begin(), v.end(), steps);
+        return static_cast<int>(v.size());
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// BFS minimal lengths for n in [0, n_max] (reference rot.cpp:84-94).
+int ref_min_lengths(uint64_t n_max, uint64_t cap, uint64_t* out) {
+    try {
+        auto v = min_decomposition_lengths(n_max, cap);
+        for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// plan_rotations (rot.cpp:96-129). strategy 0 positive, 1 signed, 2 exact.
+/// Writes per-request step lists (flattened, up to 64 steps each) and the
+/// group index of each request. Returns total_keyed_rotations.
+long ref_plan_rotations(const long* amounts, const int* same_source, int n, uint64_t s,
+                        int strategy, long* steps_flat, int* n_steps, int* group_of,
+                        int* group_hoisted) {
+    try {
+        std::vector<RotationRequest> req(n);
+        for (int i = 0; i < n; ++i) req[i] = {amounts[i], same_source[i] != 0};
+        DecompStrategy st = strategy == 0   ? DecompStrategy::Positive
+                            : strategy == 1 ? DecompStrategy::Signed
+                                            : DecompStrategy::Exact;
+        RotationSchedule sch = plan_rotations(req, s, st);
+        int r = 0;
+        for (size_t g = 0; g < sch.groups.size(); ++g) {
+            for (const auto& steps : sch.groups[g].steps) {
+                n_steps[r] = static_cast<int>(steps.size());
+                for (size_t k = 0; k < steps.size() && k < 64; ++k) steps_flat[r * 64 + k] = steps[k];
+                group_of[r] = static_cast<int>(g);
+                group_hoisted[r] = sch.groups[g].hoisted ? 1 : 0;
+                ++r;
+            }
+        }
+        return static_cast<long>(sch.total_keyed_rotations);
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// Reference CPU path timing: runs conv_plan(plan) `iters` times on each of
+/// `threads` independent Engines (the reference's Engine is not shared
+/// across threads, emu.hpp:181). Returns wall seconds for the whole batch.
+double ref_time_conv(int c, int m, int kappa, int c_out, const double* img, const double* filt,
+                     int plan, uint64_t shard_size, int iters, int threads) {
+    ImageTensor t(c, m);
+    std::memcpy(t.data.data(), img, t.data.size() * sizeof(double));
+    FilterTensor k(c, c_out, kappa);
+    std::memcpy(k.weights.data(), filt, k.weights.size() * sizeof(double));
+    auto work = [&]() {
+        Engine eng;
+        PackedImage p = pack(eng, t, shard_size);
+        for (int i = 0; i < iters; ++i) {
+            PackedImage out = run_plan(eng, p, k, plan);
+            (void)out;
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int i = 0; i < threads; ++i) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+/// Reference rotation microbenchmark leg (cfg2): executes the plan for
+/// amounts 1..n_amounts on `vectors` random vectors of s slots per thread.
+/// Returns wall seconds; writes total keyed steps per vector.
+double ref_time_rotations(uint64_t s, int strategy, int n_amounts, int vectors, int threads,
+                          uint64_t* keyed_per_vector) {
+    std::vector<RotationRequest> req;
+    for (int a = 1; a <= n_amounts; ++a) req.push_back({a, false});
+    DecompStrategy st = strategy == 0 ? DecompStrategy::Positive : DecompStrategy::Signed;
+    RotationSchedule sch = plan_rotations(req, s, st);
+    if (keyed_per_vector) *keyed_per_vector = sch.total_keyed_rotations;
+    auto work = [&](int tid) {
+        Engine eng;
+        std::mt19937_64 rng(1000 + tid);
+        for (int v = 0; v < vectors; ++v) {
+            SlotVector x = eng.encode(random_values(rng, s));
+            auto out = execute_schedule(eng, x, sch);
+            (void)out;
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int i = 0; i < threads; ++i) pool.emplace_back(work, i);
+    for (auto& th : pool) th.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // extern "C"
