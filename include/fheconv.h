@@ -1,0 +1,171 @@
+/*
+ * fheconv.h — C ABI of the B200-native RNS-CKKS encrypted-convolution hot path.
+ *
+ * Drop-in boundary. The reference has no FFI;
+ * its evaluator is the concrete C++ class shardnn::Engine
+ * (reference proj/include/shardnn/emu.hpp:132-183) passed as Engine& to the
+ * conv operators (conv.hpp:29-68). Each entry point below names the
+ * reference interface it replaces. include/fheconv.hpp wraps these calls in
+ * an Engine-shaped C++ class with the reference's method names and
+ * exception messages.
+ *
+ * Conventions
+ *   - All functions return 0 (FHE_OK) on success, a negative FHE_E* code on
+ *     failure; fhe_last_error(ctx) returns the message, using the
+ *     reference's exception text where one exists (e.g. "slot count
+ *     mismatch", "depth exhausted", "empty rotation batch",
+ *     "insufficient capacity").
+ *   - Handles own device memory on the context's GPU; one CUDA stream per
+ *     context; a context is not thread-safe (serialise per context, as the
+ *     reference's Engine RNG is unguarded, emu.hpp:181).
+ *   - Residues are uint64 in [0, q), NTT domain, laid out [poly][prime][N]
+ *     (ciphertext = 2 polys over q_0..q_level).
+ *   - There is NO CPU fallback: on a machine without a usable sm_100 GPU,
+ *     fhe_ctx_create fails with FHE_E_CUDA.
+ */
+#ifndef FHECONV_H
+#define FHECONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FHE_OK 0
+#define FHE_E_INVALID (-1)  /* std::invalid_argument in the reference */
+#define FHE_E_RUNTIME (-2)  /* std::runtime_error in the reference    */
+#define FHE_E_CUDA (-3)     /* device / driver failure                */
+#define FHE_E_NOKEY (-4)    /* required Galois key was not generated  */
+
+typedef struct fhe_ctx fhe_ctx;
+typedef struct fhe_ct fhe_ct;                 /* device ciphertext      */
+typedef struct fhe_pt fhe_pt;                 /* device plaintext       */
+typedef struct fhe_conv_layer fhe_conv_layer; /* pre-encoded conv layer */
+
+typedef struct {
+    int log_n;          /* ring degree N = 2^log_n, slots s = N/2            */
+    int n_q;            /* number of ciphertext primes (levels = n_q - 1)    */
+    const int* q_bits;  /* bit sizes of q_0..q_{n_q-1}                       */
+    int n_p;            /* number of special primes K (digit size alpha = K) */
+    const int* p_bits;  /* bit sizes of p_0..p_{K-1}                         */
+    int log_scale;      /* Delta = 2^log_scale                               */
+    int device;         /* CUDA device ordinal                               */
+} fhe_params;
+
+/* CostLedger counters (reference emu.hpp:39-122) + CKKS work counters. */
+typedef struct {
+    uint64_t rotations;          /* emu.hpp:41 */
+    uint64_t hoisted_rotations;  /* emu.hpp:42 */
+    uint64_t hoist_groups;       /* emu.hpp:43 */
+    uint64_t ct_pt_mults;        /* emu.hpp:44 */
+    uint64_t ct_ct_mults;        /* emu.hpp:45 */
+    uint64_t adds;               /* emu.hpp:46 */
+    uint64_t bootstraps;         /* emu.hpp:47 */
+    uint64_t max_depth_consumed; /* emu.hpp:48 */
+    uint64_t distinct_amounts;   /* |rotation_amounts()| emu.hpp:63-66 */
+    /* work actually performed on the GPU */
+    uint64_t key_switches;       /* Galois key inner products */
+    uint64_t modups;
+    uint64_t moddowns;
+    uint64_t rescales;
+    uint64_t kernel_launches;
+} fhe_ledger;
+
+/* ---------------------------------------------------------------- context */
+/* replaces: shardnn::Engine(EngineConfig) emu.hpp:134 */
+int fhe_ctx_create(const fhe_params* params, fhe_ctx** out);
+void fhe_ctx_destroy(fhe_ctx* ctx);
+const char* fhe_last_error(const fhe_ctx* ctx);
+/* N, slots, n_q, n_p, dnum, primes (n_q + n_p entries, q's then p's) */
+int fhe_ctx_info(const fhe_ctx* ctx, int* log_n, int* n_q, int* n_p, int* dnum, uint64_t* primes);
+int fhe_synchronize(fhe_ctx* ctx);
+/* replaces: Engine::ledger() emu.hpp:137-138, CostLedger::reset emu.hpp:77-88 */
+int fhe_ledger_get(const fhe_ctx* ctx, fhe_ledger* out);
+int fhe_ledger_reset(fhe_ctx* ctx);
+/* distinct requested rotation amounts (mod s, zero included), ascending */
+int fhe_ledger_amounts(const fhe_ctx* ctx, uint64_t* out, size_t cap, size_t* n);
+
+/* ------------------------------------------------------------------- keys */
+/* (CKKS-only; no reference counterpart — the emulator has no keys) */
+int fhe_keygen(fhe_ctx* ctx, uint64_t seed);
+/* Galois keys for left rotations by each step (mod s); 0 is ignored. */
+int fhe_gen_galois_keys(fhe_ctx* ctx, const int64_t* steps, size_t n);
+/* download the key for rotation `step`: [dnum][2][n_q+n_p][N] words */
+int fhe_galois_key_download(fhe_ctx* ctx, int64_t step, uint64_t* host, size_t words);
+
+/* ------------------------------------------------------------------- data */
+/* replaces: Engine::encode(std::vector<double>) emu.hpp:144-152 (+ CKKS
+ * encoding). n <= s real slots; level in [0, n_q-1]; with_special = 1 also
+ * encodes residues mod the special primes (needed by fused conv plaintexts). */
+int fhe_encode(fhe_ctx* ctx, const double* slots, size_t n, int level, double scale, int with_special,
+               fhe_pt** out);
+int fhe_encrypt(fhe_ctx* ctx, const fhe_pt* pt, uint64_t seed, fhe_ct** out);
+/* decrypt + decode to n <= s real slots (replaces reading SlotVector::slots) */
+int fhe_decrypt_decode(fhe_ctx* ctx, const fhe_ct* ct, double* out, size_t n);
+int fhe_ct_level(const fhe_ct* ct);
+double fhe_ct_scale(const fhe_ct* ct);
+/* residue transfer (parity tests, e2e benchmarks); words = 2 (level+1) N */
+int fhe_ct_download(fhe_ctx* ctx, const fhe_ct* ct, uint64_t* host, size_t words);
+int fhe_ct_upload(fhe_ctx* ctx, const uint64_t* host, int level, double scale, fhe_ct** out);
+/* overwrite an existing ciphertext of the same level in place */
+int fhe_ct_upload_into(fhe_ctx* ctx, const uint64_t* host, fhe_ct* ct);
+int fhe_pt_download(fhe_ctx* ctx, const fhe_pt* pt, uint64_t* host, size_t words);
+int fhe_pt_rows(const fhe_pt* pt);
+void fhe_ct_free(fhe_ct* ct);
+void fhe_pt_free(fhe_pt* pt);
+
+/* ---------------------------------------------------------------- ops */
+/* replaces: Engine::rotate emu.cpp:28-37 — left rotation out[i] = in[(i+k) mod s];
+ * k = 0 mod s is a free copy (amount still recorded). */
+int fhe_rotate(fhe_ctx* ctx, const fhe_ct* ct, int64_t k, fhe_ct** out);
+/* replaces: Engine::rotate_many emu.cpp:39-54 — one shared ModUp (hoisting);
+ * "empty rotation batch" when n == 0. outs[i] receives a new ciphertext. */
+int fhe_rotate_hoisted(fhe_ctx* ctx, const fhe_ct* ct, const int64_t* ks, size_t n, fhe_ct** outs);
+/* replaces: Engine::mul_plain emu.cpp:56-67 (no rescale; level bookkeeping by
+ * fhe_rescale) */
+int fhe_mul_plain(fhe_ctx* ctx, const fhe_ct* ct, const fhe_pt* pt, fhe_ct** out);
+/* replaces: Engine::add emu.cpp:82-91 / sub :93-102 / add_plain :104-111 */
+int fhe_add(fhe_ctx* ctx, const fhe_ct* a, const fhe_ct* b, fhe_ct** out);
+int fhe_sub(fhe_ctx* ctx, const fhe_ct* a, const fhe_ct* b, fhe_ct** out);
+int fhe_add_plain(fhe_ctx* ctx, const fhe_ct* ct, const fhe_pt* pt, fhe_ct** out);
+/* drop q_level with centered rounding (the level the reference only counts,
+ * emu.cpp:62-63) */
+int fhe_rescale(fhe_ctx* ctx, const fhe_ct* ct, fhe_ct** out);
+
+/* Rotation through power-of-two keys (replaces plan_rotations +
+ * execute_schedule, reference rot.cpp:96-156). strategy: 0 positive (binary,
+ * rot.cpp:21-29), 1 signed (nearest power of two, rot.cpp:31-46). Requires
+ * keys for the power-of-two steps used. */
+int fhe_rotate_decomposed(fhe_ctx* ctx, const fhe_ct* ct, int64_t k, int strategy, fhe_ct** out);
+/* keyed steps a decomposition uses (host-only planning) */
+int fhe_decompose(int strategy, uint64_t n, uint64_t s, int64_t* steps, int cap);
+
+/* ----------------------------------------------------------------- conv */
+/* Host-side layer preparation (replaces ImageConv::fused_plain conv.cpp:69-85
+ * + make_shift_plan :215-231): encodes the kappa^2 * c fused mask x weight
+ * plaintexts at `level` over Q_level u P with scale q_level, uploads them
+ * once. weights: (c_in, c_out, kappa, kappa) as FilterTensor::weights
+ * (tensor.hpp:41-58). Single image shard, c_in * m^2 == s. */
+int fhe_conv_layer_create(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
+                          int level, fhe_conv_layer** out);
+void fhe_conv_layer_free(fhe_conv_layer* layer);
+/* Galois steps a layer needs (channel rotations r m^2 and shifts kk m + ll) */
+int fhe_conv_layer_steps(const fhe_conv_layer* layer, int approach, int64_t* steps, size_t cap, size_t* n);
+/* replaces: conv_plan(eng, p, k, plan) conv.cpp:266-271.
+ * approach 1 = paper Approach 1 (ConvPlan::ChannelFirst: shifts first),
+ * approach 2 = paper Approach 2 (ConvPlan::ShiftFirst: channel rotations first,
+ * shifts hoisted). Output: one ciphertext at level - 1 (one rescale). */
+int fhe_conv2d(fhe_ctx* ctx, const fhe_ct* ct, const fhe_conv_layer* layer, int approach, fhe_ct** out);
+/* same, writing into a preallocated output ciphertext of level - 1 */
+int fhe_conv2d_into(fhe_ctx* ctx, const fhe_ct* ct, const fhe_conv_layer* layer, int approach, fhe_ct* out);
+/* batch: n independent ciphertexts through the same layer (keys and
+ * plaintexts shared; BASELINE cfg5) */
+int fhe_conv2d_batch(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* layer,
+                     int approach, fhe_ct** outs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FHECONV_H */

@@ -1,0 +1,1080 @@
+// C-ABI implementation (include/fheconv.h): context, keys, data movement,
+// ops and the fused encrypted convolution. Host C++ drives the sm_100a
+// kernels in kernels.cu on one CUDA stream per context. No CPU fallback.
+//
+// Reference interface mirrored: shardnn::Engine (reference
+// proj/include/shardnn/emu.hpp:132-183) and the conv entry points
+// conv_plan / conv_single_shard (proj/src/conv.cpp:254-271).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fheconv.h"
+#include "host_math.hpp"
+#include "kernels.cuh"
+
+using namespace fhe;
+
+namespace {
+
+struct FheError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& m) { throw FheError{code, m}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(FHE_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+uint64_t dev_words_alloc_count = 0;
+
+}  // namespace
+
+struct fhe_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    int logN = 0, N = 0, L = 0, K = 0, alpha = 0, dnum = 0, np = 0;
+    std::vector<uint64_t> primes;
+    double scale = 0;
+    DevCtx dc{};
+    Prime* d_primes = nullptr;
+    uint64_t *d_tw = nullptr, *d_tw_sh = nullptr, *d_itw = nullptr, *d_itw_sh = nullptr;
+    uint64_t *d_ninv = nullptr, *d_ninv_sh = nullptr;
+    ModUpDigit* d_modup = nullptr;  // [L][dnum]
+    ModDownTable* d_md = nullptr;
+    uint64_t *d_qlinv = nullptr, *d_qlinv_sh = nullptr;  // [L][L]
+    uint64_t* d_s = nullptr;                              // secret, [np][N] NTT
+    bool have_key = false;
+    uint64_t key_seed = 0;
+    std::map<uint32_t, uint64_t*> keys;
+    fhe_ledger ledger{};
+    std::set<uint64_t> amounts;
+    std::string err;
+    // pinned staging
+    void* h_stage = nullptr;
+    size_t h_stage_bytes = 0;
+
+    // ------------------------------------------------------------ helpers
+    uint64_t* alloc(size_t words) {
+        void* p = nullptr;
+        ck(cudaMallocAsync(&p, words * 8, st), "cudaMallocAsync");
+        dev_words_alloc_count += words;
+        return (uint64_t*)p;
+    }
+    void release(void* p) {
+        if (p) cudaFreeAsync(p, st);
+    }
+    void* stage(size_t bytes) {
+        if (bytes > h_stage_bytes) {
+            if (h_stage) {
+                cudaStreamSynchronize(st);
+                cudaFreeHost(h_stage);
+            }
+            ck(cudaMallocHost(&h_stage, bytes), "cudaMallocHost");
+            h_stage_bytes = bytes;
+        }
+        return h_stage;
+    }
+    size_t slots() const { return (size_t)N / 2; }
+    int dn_at(int level) const { return (level + 1 + alpha - 1) / alpha; }
+    int ne_at(int level) const { return level + 1 + K; }
+    uint32_t galois_of(uint64_t amount) const {
+        return (uint32_t)host::powmod(5, amount, 2 * (uint64_t)N);
+    }
+    uint64_t reduce_amount(int64_t k) const {
+        const int64_t s = (int64_t)slots();
+        int64_t m = k % s;
+        if (m < 0) m += s;
+        return (uint64_t)m;
+    }
+    void note_amount(uint64_t a) { amounts.insert(a); }
+    const uint64_t* key_for(uint32_t g) const {
+        auto it = keys.find(g);
+        if (it == keys.end()) fail(FHE_E_NOKEY, "missing Galois key for rotation");
+        return it->second;
+    }
+    void launched(int n = 1) { ledger.kernel_launches += n; }
+};
+
+struct fhe_ct {
+    fhe_ctx* ctx;
+    int level;
+    double scale;
+    int depth;
+    uint64_t* d;
+    size_t words() const { return (size_t)2 * (level + 1) * ctx->N; }
+    uint64_t* c0() const { return d; }
+    uint64_t* c1() const { return d + (size_t)(level + 1) * ctx->N; }
+};
+
+struct fhe_pt {
+    fhe_ctx* ctx;
+    int level;
+    int rows;
+    double scale;
+    uint64_t* d;
+};
+
+struct fhe_conv_layer {
+    fhe_ctx* ctx;
+    int c_in, c_out, m, kappa, level, nk;
+    std::vector<int> nonempty;  // [c_in][nk]
+    uint64_t* d_pts;            // [c_in][nk][ne][N]
+    size_t pt_words;
+};
+
+namespace {
+
+template <class F>
+int guard(const fhe_ctx* ctx, F&& f) {
+    try {
+        f();
+        return FHE_OK;
+    } catch (const FheError& e) {
+        if (ctx) const_cast<fhe_ctx*>(ctx)->err = e.msg;
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        if (ctx) const_cast<fhe_ctx*>(ctx)->err = e.what();
+        return FHE_E_INVALID;
+    } catch (const std::exception& e) {
+        if (ctx) const_cast<fhe_ctx*>(ctx)->err = e.what();
+        return FHE_E_RUNTIME;
+    }
+}
+
+RowMap qmap(const fhe_ctx* c, int level) { return RowMap{level + 1, level, c->L, 0}; }
+RowMap extmap(const fhe_ctx* c, int level) { return RowMap{level + 1 + c->K, level, c->L, 0}; }
+
+fhe_ct* new_ct(fhe_ctx* c, int level, double scale, int depth) {
+    fhe_ct* ct = new fhe_ct{c, level, scale, depth, nullptr};
+    ct->d = c->alloc(ct->words());
+    return ct;
+}
+
+// ------------------------------------------------------------ primitives
+
+// digits [dn][ne][N] of c1 (level+1 rows, NTT)
+void modup(fhe_ctx* c, const uint64_t* c1, int level, uint64_t* digits) {
+    const int nr = level + 1, dn = c->dn_at(level), ne = c->ne_at(level);
+    uint64_t* coef = c->alloc((size_t)nr * c->N);
+    ck(cudaMemcpyAsync(coef, c1, (size_t)nr * c->N * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    ntt_inverse(c->dc, coef, nr, qmap(c, level), c->st);
+    modup_bconv(c->dc, coef, c1, digits, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+    ntt_forward(c->dc, digits, dn * ne, RowMap{ne, level, c->L, c->alpha}, c->st);
+    c->release(coef);
+    c->ledger.modups++;
+    c->launched(6);
+}
+
+// out[p] = ModDown(acc[p]) (+ sigma_g(add_src) on poly 0)
+void moddown(fhe_ctx* c, const uint64_t* acc, int level, int npoly, uint64_t* out, const uint64_t* add_src,
+             uint32_t g) {
+    const int nr = level + 1;
+    uint64_t* pc = c->alloc((size_t)npoly * c->K * c->N);
+    uint64_t* conv = c->alloc((size_t)npoly * nr * c->N);
+    gather_special(c->dc, pc, acc, level, npoly, c->st);
+    ntt_inverse(c->dc, pc, npoly * c->K, RowMap{c->K, -1, c->L, 0}, c->st);
+    moddown_bconv(c->dc, pc, conv, c->d_md, level, npoly, c->st);
+    ntt_forward(c->dc, conv, npoly * nr, qmap(c, level), c->st);
+    moddown_finish(c->dc, out, acc, conv, c->d_md, level, npoly, add_src, g, c->st);
+    c->release(pc);
+    c->release(conv);
+    c->ledger.moddowns += npoly;
+    c->launched(7);
+}
+
+// out = rotation of ct by Galois g given the ModUp digits of ct.c1
+void rotate_from_digits(fhe_ctx* c, const fhe_ct* ct, const uint64_t* digits, uint32_t g, uint64_t* out) {
+    const int level = ct->level, ne = c->ne_at(level);
+    uint64_t* acc = c->alloc((size_t)2 * ne * c->N);
+    ks_inner_product(c->dc, digits, c->key_for(g), acc, acc + (size_t)ne * c->N, g, level, c->dn_at(level),
+                     c->st);
+    moddown(c, acc, level, 2, out, ct->c0(), g);
+    c->release(acc);
+    c->ledger.key_switches++;
+    c->launched();
+}
+
+void rescale_into(fhe_ctx* c, const uint64_t* in, int level, uint64_t* out) {
+    const size_t N = c->N;
+    uint64_t* tmp = c->alloc(2 * N);
+    uint64_t* spread = c->alloc((size_t)2 * level * N);
+    ck(cudaMemcpyAsync(tmp, in + (size_t)level * N, N * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    ck(cudaMemcpyAsync(tmp + N, in + ((size_t)level + 1 + level) * N, N * 8, cudaMemcpyDeviceToDevice, c->st),
+       "memcpy");
+    ntt_inverse(c->dc, tmp, 2, RowMap{1, -1, level, 0}, c->st);
+    rescale_spread(c->dc, tmp, spread, level, c->st);
+    ntt_forward(c->dc, spread, 2 * level, qmap(c, level - 1), c->st);
+    rescale_finish(c->dc, out, in, spread, level, c->d_qlinv + (size_t)level * c->L,
+                   c->d_qlinv_sh + (size_t)level * c->L, c->st);
+    c->release(tmp);
+    c->release(spread);
+    c->ledger.rescales++;
+    c->launched(6);
+}
+
+void gen_key(fhe_ctx* c, uint32_t g) {
+    if (c->keys.count(g)) return;
+    const size_t N = c->N;
+    const int np = c->np;
+    uint64_t* key = c->alloc((size_t)c->dnum * 2 * np * N);
+    int64_t* e = (int64_t*)c->alloc(N);
+    uint64_t* erows = c->alloc((size_t)np * N);
+    const RowMap all{np, c->L - 1, c->L, 0};
+    for (int j = 0; j < c->dnum; ++j) {
+        uint64_t* b = key + (size_t)(2 * j) * np * N;
+        uint64_t* a = key + (size_t)(2 * j + 1) * np * N;
+        sample_gauss(c->dc, e, stream_key(c->key_seed, stream_id(DOM_KEY_E, g, j)), c->st);
+        reduce_signed_rows(c->dc, e, erows, np, all, c->st);
+        ntt_forward(c->dc, erows, np, all, c->st);
+        sample_uniform_rows(c->dc, a, np, all, stream_key(c->key_seed, stream_id(DOM_KEY_A, g, j)), c->st);
+        const int lo = j * c->alpha, hi = std::min(lo + c->alpha, c->L);
+        keygen_combine(c->dc, b, a, erows, c->d_s, g, lo, hi, c->d_md, np, c->st);
+    }
+    c->release(e);
+    c->release(erows);
+    c->keys[g] = key;
+}
+
+void upload_tables(fhe_ctx* c) {
+    using namespace host;
+    const size_t N = c->N;
+    const int np = c->np, L = c->L, K = c->K;
+    std::vector<Prime> pr(np);
+    for (int i = 0; i < np; ++i) {
+        const uint64_t q = c->primes[i];
+        const u128 ratio = (~(u128)0) / q;  // floor((2^128 - 1) / q) == floor(2^128 / q) for odd q
+        pr[i] = Prime{q, (uint64_t)(ratio >> 64), (uint64_t)ratio, 0};
+    }
+    std::vector<uint64_t> tw((size_t)np * N), tws((size_t)np * N), itw((size_t)np * N), itws((size_t)np * N);
+    std::vector<uint64_t> ninv(np), ninvs(np);
+    std::vector<uint32_t> brv(N);
+    for (size_t k = 0; k < N; ++k) brv[k] = bitrev((uint32_t)k, c->logN);
+    std::vector<uint64_t> pw(N), ipw(N);
+    for (int i = 0; i < np; ++i) {
+        const uint64_t q = c->primes[i];
+        const uint64_t psi = find_root(q, N), ipsi = invmod(psi, q);
+        uint64_t p = 1, ip = 1;
+        for (size_t k = 0; k < N; ++k) {
+            pw[k] = p;
+            ipw[k] = ip;
+            p = mulmod(p, psi, q);
+            ip = mulmod(ip, ipsi, q);
+        }
+        for (size_t k = 0; k < N; ++k) {
+            const size_t o = (size_t)i * N + k;
+            tw[o] = pw[brv[k]];
+            itw[o] = ipw[brv[k]];
+            tws[o] = shoup(tw[o], q);
+            itws[o] = shoup(itw[o], q);
+        }
+        ninv[i] = invmod(N % q, q);
+        ninvs[i] = shoup(ninv[i], q);
+    }
+    // ModUp digit tables [L][dnum]
+    std::vector<ModUpDigit> mu((size_t)L * c->dnum);
+    for (int level = 0; level < L; ++level) {
+        const int nr = level + 1, ne = nr + K;
+        for (int j = 0; j < c->dnum; ++j) {
+            ModUpDigit& T = mu[(size_t)level * c->dnum + j];
+            std::memset(&T, 0, sizeof(T));
+            T.lo = j * c->alpha;
+            T.hi = std::min(T.lo + c->alpha, nr);
+            if (T.lo >= nr) continue;
+            for (int i = T.lo; i < T.hi; ++i) {
+                uint64_t h = 1;
+                for (int i2 = T.lo; i2 < T.hi; ++i2)
+                    if (i2 != i) h = mulmod(h, c->primes[i2] % c->primes[i], c->primes[i]);
+                T.inv[i - T.lo] = invmod(h, c->primes[i]);
+                T.inv_sh[i - T.lo] = shoup(T.inv[i - T.lo], c->primes[i]);
+            }
+            for (int u = 0; u < ne; ++u) {
+                const int p = u <= level ? u : L + (u - level - 1);
+                const uint64_t t = c->primes[p];
+                uint64_t QJ = 1;
+                for (int i = T.lo; i < T.hi; ++i) {
+                    uint64_t h = 1;
+                    for (int i2 = T.lo; i2 < T.hi; ++i2)
+                        if (i2 != i) h = mulmod(h, c->primes[i2] % t, t);
+                    T.hat[u][i - T.lo] = h;
+                    T.hat_sh[u][i - T.lo] = shoup(h, t);
+                    QJ = mulmod(QJ, c->primes[i] % t, t);
+                }
+                T.qj[u] = QJ;
+            }
+        }
+    }
+    // ModDown table
+    ModDownTable md;
+    std::memset(&md, 0, sizeof(md));
+    for (int k = 0; k < K; ++k) {
+        const uint64_t pk = c->primes[L + k];
+        uint64_t h = 1;
+        for (int k2 = 0; k2 < K; ++k2)
+            if (k2 != k) h = mulmod(h, c->primes[L + k2] % pk, pk);
+        md.pinv[k] = invmod(h, pk);
+        md.pinv_sh[k] = shoup(md.pinv[k], pk);
+    }
+    for (int t = 0; t < L; ++t) {
+        const uint64_t q = c->primes[t];
+        uint64_t P = 1;
+        for (int k = 0; k < K; ++k) {
+            uint64_t h = 1;
+            for (int k2 = 0; k2 < K; ++k2)
+                if (k2 != k) h = mulmod(h, c->primes[L + k2] % q, q);
+            md.hat[t][k] = h;
+            md.hat_sh[t][k] = shoup(h, q);
+            P = mulmod(P, c->primes[L + k] % q, q);
+        }
+        md.pmod[t] = P;
+        md.pmod_sh[t] = shoup(P, q);
+        md.pinvq[t] = invmod(P, q);
+        md.pinvq_sh[t] = shoup(md.pinvq[t], q);
+    }
+    // rescale: q_l^-1 mod q_i
+    std::vector<uint64_t> ql((size_t)L * L, 0), qls((size_t)L * L, 0);
+    for (int l = 1; l < L; ++l)
+        for (int i = 0; i < l; ++i) {
+            const uint64_t q = c->primes[i];
+            ql[(size_t)l * L + i] = invmod(c->primes[l] % q, q);
+            qls[(size_t)l * L + i] = shoup(ql[(size_t)l * L + i], q);
+        }
+    auto up = [&](void** dst, const void* src, size_t bytes) {
+        ck(cudaMalloc(dst, bytes), "cudaMalloc");
+        ck(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy");
+    };
+    up((void**)&c->d_primes, pr.data(), pr.size() * sizeof(Prime));
+    up((void**)&c->d_tw, tw.data(), tw.size() * 8);
+    up((void**)&c->d_tw_sh, tws.data(), tws.size() * 8);
+    up((void**)&c->d_itw, itw.data(), itw.size() * 8);
+    up((void**)&c->d_itw_sh, itws.data(), itws.size() * 8);
+    up((void**)&c->d_ninv, ninv.data(), ninv.size() * 8);
+    up((void**)&c->d_ninv_sh, ninvs.data(), ninvs.size() * 8);
+    up((void**)&c->d_modup, mu.data(), mu.size() * sizeof(ModUpDigit));
+    up((void**)&c->d_md, &md, sizeof(md));
+    up((void**)&c->d_qlinv, ql.data(), ql.size() * 8);
+    up((void**)&c->d_qlinv_sh, qls.data(), qls.size() * 8);
+    c->dc = DevCtx{c->logN, c->N, L, K, c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv,
+                   c->d_ninv_sh};
+}
+
+void require_key(const fhe_ctx* c) {
+    if (!c->have_key) fail(FHE_E_RUNTIME, "secret key not generated (call fhe_keygen)");
+}
+
+// ------------------------------------------------------------ conv layer
+
+// Fused plaintext of reference conv.cpp:69-85 for one image shard (t = 1,
+// n_out = 1, rep = 1, identity tau). Returns false when every entry is zero.
+bool fused_plain(int c_in, int c_out, int m, int kappa, size_t s, const double* w, int r, long kk, long ll,
+                 std::vector<double>& plain) {
+    const size_t block = (size_t)m * m, z = s / block;
+    const long h = kappa / 2;
+    plain.assign(s, 0.0);
+    bool any = false;
+    for (size_t b = 0; b < z; ++b) {
+        const size_t in_ch = ((b + (size_t)r) % z) % (size_t)c_in;
+        const size_t out_ch = b % (size_t)c_out;
+        const double wt =
+            w[((in_ch * c_out + out_ch) * kappa + (size_t)(kk + h)) * kappa + (size_t)(ll + h)] * 1.0;
+        if (wt == 0.0) continue;
+        any = true;
+        const long i_lo = std::max(0L, -kk), i_hi = std::min<long>(m, m - kk);
+        const long j_lo = std::max(0L, -ll), j_hi = std::min<long>(m, m - ll);
+        for (long i = i_lo; i < i_hi; ++i)
+            for (long j = j_lo; j < j_hi; ++j) plain[b * block + (size_t)(i * m + j)] = wt;
+    }
+    return any;
+}
+
+void encode_rows(fhe_ctx* c, const double* z, size_t n, int level, double scale, int rows, uint64_t* dst) {
+    const size_t N = c->N;
+    int64_t* h = (int64_t*)c->stage(N * 8);
+    ck(cudaStreamSynchronize(c->st), "sync");  // staging buffer reuse
+    host::encode(z, n, N, scale, h);
+    int64_t* dcoef = (int64_t*)c->alloc(N);
+    ck(cudaMemcpyAsync(dcoef, h, N * 8, cudaMemcpyHostToDevice, c->st), "H2D");
+    reduce_signed_rows(c->dc, dcoef, dst, rows, RowMap{rows, level, c->L, 0}, c->st);
+    ntt_forward(c->dc, dst, rows, RowMap{rows, level, c->L, 0}, c->st);
+    c->release(dcoef);
+}
+
+// Ledger replay of the reference schedule (conv.cpp:119-210) so the
+// operation-count laws (test_conv.cpp:244-276) hold for the CKKS path too.
+void ledger_conv(fhe_ctx* c, const fhe_conv_layer* ly, int approach) {
+    fhe_ledger& lg = c->ledger;
+    const long m = ly->m, h = ly->kappa / 2;
+    const uint64_t block = (uint64_t)m * m;
+    bool have_acc = false;
+    std::vector<int> shifted_done(ly->nk, 0);  // ChannelFirst caches shifted copies across r
+    for (int r = 0; r < ly->c_in; ++r) {
+        const uint64_t chan = c->reduce_amount((int64_t)r * block);
+        bool have_partial = false;
+        if (approach == 1) {
+            int i = 0;
+            for (long kk = -h; kk <= h; ++kk)
+                for (long ll = -h; ll <= h; ++ll, ++i) {
+                    if (!ly->nonempty[r * ly->nk + i]) continue;
+                    if (!shifted_done[i]) {
+                        const uint64_t a = c->reduce_amount(kk * m + ll);
+                        c->note_amount(a);
+                        if (a) lg.rotations++;
+                        shifted_done[i] = 1;
+                    }
+                    c->note_amount(chan);
+                    if (chan) lg.rotations++;
+                    lg.ct_pt_mults++;
+                    if (have_partial) lg.adds++;
+                    have_partial = true;
+                }
+        } else {
+            bool any = false;
+            for (int i = 0; i < ly->nk; ++i) any |= ly->nonempty[r * ly->nk + i] != 0;
+            if (!any) continue;
+            c->note_amount(chan);
+            if (chan) lg.rotations++;
+            int batch = 0, i = 0;
+            for (long kk = -h; kk <= h; ++kk)
+                for (long ll = -h; ll <= h; ++ll, ++i)
+                    if (ly->nonempty[r * ly->nk + i]) {
+                        c->note_amount(c->reduce_amount(kk * m + ll));
+                        ++batch;
+                    }
+            lg.hoist_groups++;
+            lg.hoisted_rotations += batch;
+            for (int k = 0; k < batch; ++k) {
+                lg.ct_pt_mults++;
+                if (have_partial) lg.adds++;
+                have_partial = true;
+            }
+        }
+        if (have_partial) {
+            if (have_acc) lg.adds++;
+            have_acc = true;
+        }
+    }
+    if (!have_acc) {
+        c->note_amount(0);
+        lg.ct_pt_mults++;
+    }
+}
+
+void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct* out) {
+    if (approach != 1 && approach != 2) fail(FHE_E_INVALID, "approach must be 1 or 2");
+    if (ct->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
+    if (out->level != ct->level - 1) fail(FHE_E_INVALID, "output level must be input level - 1");
+    const int level = ct->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N;
+    const int nk = ly->nk, cin = ly->c_in;
+    const long m = ly->m, h = ly->kappa / 2;
+    const int64_t block = (int64_t)m * m;
+
+    uint64_t* acc = c->alloc(2 * extw);
+    ck(cudaMemsetAsync(acc, 0, 2 * extw * 8, c->st), "memset");
+    uint64_t* dsrc = c->alloc((size_t)dn * extw);
+    uint64_t* dtmp = c->alloc((size_t)dn * extw);
+    fhe_ct X{c, level, ct->scale, ct->depth, c->alloc(ct->words())};
+    modup(c, ct->c1(), level, dsrc);
+
+    auto pt_of = [&](int r, int i) { return ly->d_pts + ((size_t)r * nk + i) * extw; };
+    auto run_terms = [&](MacTerms& t, const fhe_ct& src) {
+        if (t.n == 0) return;
+        conv_mac(c->dc, acc, dtmp, src.d, t, c->d_md, level, dn, c->st);
+        for (int i = 0; i < t.n; ++i)
+            if (t.galois[i] != 1) c->ledger.key_switches++;
+        c->launched();
+        t.n = 0;
+    };
+    auto push = [&](MacTerms& t, const fhe_ct& src, uint32_t g, const uint64_t* pt) {
+        if (t.n == kMaxTerms) run_terms(t, src);
+        t.galois[t.n] = g;
+        t.key[t.n] = g == 1 ? nullptr : c->key_for(g);
+        t.pt[t.n] = pt;
+        t.n++;
+    };
+
+    if (approach == 2) {
+        for (int r = 0; r < cin; ++r) {
+            bool any = false;
+            for (int i = 0; i < nk; ++i) any |= ly->nonempty[r * nk + i] != 0;
+            if (!any) continue;
+            const uint32_t gr = c->galois_of(c->reduce_amount((int64_t)r * block));
+            const fhe_ct* src = ct;
+            if (gr != 1) {
+                rotate_from_digits(c, ct, dsrc, gr, X.d);
+                src = &X;
+            }
+            modup(c, src->c1(), level, dtmp);
+            MacTerms t{};
+            int i = 0;
+            for (long kk = -h; kk <= h; ++kk)
+                for (long ll = -h; ll <= h; ++ll, ++i) {
+                    if (!ly->nonempty[r * nk + i]) continue;
+                    push(t, *src, c->galois_of(c->reduce_amount(kk * m + ll)), pt_of(r, i));
+                }
+            run_terms(t, *src);
+        }
+    } else {
+        int i = 0;
+        for (long kk = -h; kk <= h; ++kk)
+            for (long ll = -h; ll <= h; ++ll, ++i) {
+                bool any = false;
+                for (int r = 0; r < cin; ++r) any |= ly->nonempty[r * nk + i] != 0;
+                if (!any) continue;
+                const uint32_t gi = c->galois_of(c->reduce_amount(kk * m + ll));
+                const fhe_ct* src = ct;
+                if (gi != 1) {
+                    rotate_from_digits(c, ct, dsrc, gi, X.d);
+                    src = &X;
+                }
+                modup(c, src->c1(), level, dtmp);
+                MacTerms t{};
+                for (int r = 0; r < cin; ++r) {
+                    if (!ly->nonempty[r * nk + i]) continue;
+                    push(t, *src, c->galois_of(c->reduce_amount((int64_t)r * block)), pt_of(r, i));
+                }
+                run_terms(t, *src);
+            }
+    }
+    // one ModDown per component, then one rescale
+    uint64_t* md = c->alloc((size_t)2 * nr * N);
+    moddown(c, acc, level, 2, md, nullptr, 1);
+    rescale_into(c, md, level, out->d);
+    out->scale = (ct->scale * (double)c->primes[level]) / (double)c->primes[level];
+    out->depth = ct->depth + 1;
+    c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, out->depth);
+    c->release(md);
+    c->release(acc);
+    c->release(dsrc);
+    c->release(dtmp);
+    c->release(X.d);
+    ledger_conv(c, ly, approach);
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
+    if (!p || !out) return FHE_E_INVALID;
+    *out = nullptr;
+    fhe_ctx* c = new fhe_ctx();
+    const int rc = guard(c, [&] {
+        if (p->log_n < 12 || p->log_n > 16) fail(FHE_E_INVALID, "log_n must be in [12, 16]");
+        if (p->n_q < 1 || p->n_p < 1 || p->n_p > kMaxAlpha || p->n_q + p->n_p > kMaxPrimes)
+            fail(FHE_E_INVALID, "unsupported prime counts");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            fail(FHE_E_CUDA, "no CUDA device available (libfheconv has no CPU fallback)");
+        c->device = p->device;
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, c->device), "cudaGetDeviceProperties");
+        if (prop.major < 10) fail(FHE_E_CUDA, "libfheconv is built for sm_100a (B200)");
+        ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "cudaStreamCreate");
+        cudaMemPool_t pool;
+        ck(cudaDeviceGetDefaultMemPool(&pool, c->device), "mempool");
+        uint64_t thresh = ~0ULL;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+        c->logN = p->log_n;
+        c->N = 1 << p->log_n;
+        c->L = p->n_q;
+        c->K = p->n_p;
+        c->alpha = p->n_p;
+        c->dnum = (c->L + c->alpha - 1) / c->alpha;
+        c->np = c->L + c->K;
+        std::vector<int> bits(p->q_bits, p->q_bits + p->n_q);
+        bits.insert(bits.end(), p->p_bits, p->p_bits + p->n_p);
+        c->primes = host::generate_primes(bits, (uint64_t)c->N);
+        c->scale = std::ldexp(1.0, p->log_scale);
+        upload_tables(c);
+    });
+    if (rc != FHE_OK) {
+        // keep the context alive only to report the error? callers get rc.
+        fhe_ctx_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return FHE_OK;
+}
+
+void fhe_ctx_destroy(fhe_ctx* c) {
+    if (!c) return;
+    if (c->st) cudaStreamSynchronize(c->st);
+    for (auto& kv : c->keys) cudaFreeAsync(kv.second, c->st);
+    if (c->st) cudaStreamSynchronize(c->st);
+    void* bufs[] = {c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv, c->d_ninv_sh,
+                    c->d_modup, c->d_md, c->d_qlinv, c->d_qlinv_sh, c->d_s};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+const char* fhe_last_error(const fhe_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int fhe_ctx_info(const fhe_ctx* c, int* log_n, int* n_q, int* n_p, int* dnum, uint64_t* primes) {
+    if (!c) return FHE_E_INVALID;
+    if (log_n) *log_n = c->logN;
+    if (n_q) *n_q = c->L;
+    if (n_p) *n_p = c->K;
+    if (dnum) *dnum = c->dnum;
+    if (primes) std::copy(c->primes.begin(), c->primes.end(), primes);
+    return FHE_OK;
+}
+
+int fhe_synchronize(fhe_ctx* c) {
+    return guard(c, [&] { ck(cudaStreamSynchronize(c->st), "cudaStreamSynchronize"); });
+}
+
+int fhe_ledger_get(const fhe_ctx* c, fhe_ledger* out) {
+    if (!c || !out) return FHE_E_INVALID;
+    *out = c->ledger;
+    out->distinct_amounts = c->amounts.size();
+    return FHE_OK;
+}
+int fhe_ledger_reset(fhe_ctx* c) {
+    if (!c) return FHE_E_INVALID;
+    c->ledger = fhe_ledger{};
+    c->amounts.clear();
+    return FHE_OK;
+}
+int fhe_ledger_amounts(const fhe_ctx* c, uint64_t* out, size_t cap, size_t* n) {
+    if (!c) return FHE_E_INVALID;
+    size_t i = 0;
+    for (uint64_t a : c->amounts) {
+        if (i < cap && out) out[i] = a;
+        ++i;
+    }
+    if (n) *n = i;
+    return FHE_OK;
+}
+
+int fhe_keygen(fhe_ctx* c, uint64_t seed) {
+    return guard(c, [&] {
+        const size_t N = c->N;
+        if (!c->d_s) ck(cudaMalloc(&c->d_s, (size_t)c->np * N * 8), "cudaMalloc");
+        for (auto& kv : c->keys) c->release(kv.second);
+        c->keys.clear();
+        int64_t* s = (int64_t*)c->alloc(N);
+        sample_ternary(c->dc, s, stream_key(seed, stream_id(DOM_SECRET, 0, 0)), c->st);
+        const RowMap all{c->np, c->L - 1, c->L, 0};
+        reduce_signed_rows(c->dc, s, c->d_s, c->np, all, c->st);
+        ntt_forward(c->dc, c->d_s, c->np, all, c->st);
+        c->release(s);
+        c->key_seed = seed;
+        c->have_key = true;
+        ck(cudaStreamSynchronize(c->st), "keygen");
+    });
+}
+
+int fhe_gen_galois_keys(fhe_ctx* c, const int64_t* steps, size_t n) {
+    return guard(c, [&] {
+        require_key(c);
+        for (size_t i = 0; i < n; ++i) {
+            const uint64_t a = c->reduce_amount(steps[i]);
+            if (a == 0) continue;
+            const uint32_t g = c->galois_of(a);
+            if (c->keys.count(g)) continue;
+            // keys are allocated with cudaMalloc (long-lived) via a pool copy
+            gen_key(c, g);
+        }
+        ck(cudaStreamSynchronize(c->st), "galois keys");
+    });
+}
+
+int fhe_galois_key_download(fhe_ctx* c, int64_t step, uint64_t* host, size_t words) {
+    return guard(c, [&] {
+        const uint32_t g = c->galois_of(c->reduce_amount(step));
+        const size_t need = (size_t)c->dnum * 2 * c->np * c->N;
+        if (words < need) fail(FHE_E_INVALID, "buffer too small");
+        ck(cudaMemcpyAsync(host, c->key_for(g), need * 8, cudaMemcpyDeviceToHost, c->st), "D2H");
+        ck(cudaStreamSynchronize(c->st), "sync");
+    });
+}
+
+int fhe_encode(fhe_ctx* c, const double* z, size_t n, int level, double scale, int with_special, fhe_pt** out) {
+    return guard(c, [&] {
+        if (n == 0 || (n & (n - 1)) != 0 || n > c->slots())
+            fail(FHE_E_INVALID, "slot count must be a power of two");
+        if (level < 0 || level >= c->L) fail(FHE_E_INVALID, "level out of range");
+        const int rows = level + 1 + (with_special ? c->K : 0);
+        fhe_pt* pt = new fhe_pt{c, level, rows, scale, c->alloc((size_t)rows * c->N)};
+        try {
+            encode_rows(c, z, n, level, scale, rows, pt->d);
+        } catch (...) {
+            c->release(pt->d);
+            delete pt;
+            throw;
+        }
+        *out = pt;
+    });
+}
+
+int fhe_encrypt(fhe_ctx* c, const fhe_pt* pt, uint64_t seed, fhe_ct** out) {
+    return guard(c, [&] {
+        require_key(c);
+        const int level = pt->level, nr = level + 1;
+        const size_t N = c->N;
+        fhe_ct* ct = new_ct(c, level, pt->scale, 0);
+        int64_t* e = (int64_t*)c->alloc(N);
+        uint64_t* erows = c->alloc((size_t)nr * N);
+        sample_gauss(c->dc, e, stream_key(seed, stream_id(DOM_ENC_E, 0, 0)), c->st);
+        reduce_signed_rows(c->dc, e, erows, nr, qmap(c, level), c->st);
+        ntt_forward(c->dc, erows, nr, qmap(c, level), c->st);
+        sample_uniform_rows(c->dc, ct->c1(), nr, qmap(c, level), stream_key(seed, stream_id(DOM_ENC_A, 0, 0)),
+                            c->st);
+        encrypt_combine(c->dc, ct->c0(), ct->c1(), erows, c->d_s, pt->d, nr, c->st);
+        c->release(e);
+        c->release(erows);
+        *out = ct;
+    });
+}
+
+int fhe_decrypt_decode(fhe_ctx* c, const fhe_ct* ct, double* out, size_t n) {
+    return guard(c, [&] {
+        require_key(c);
+        if (n > c->slots()) fail(FHE_E_INVALID, "slot count mismatch");
+        const size_t N = c->N;
+        const int nr = ct->level + 1, use = std::min(nr, 2);
+        uint64_t* m = c->alloc((size_t)use * N);
+        decrypt_combine(c->dc, m, ct->c0(), ct->c1(), c->d_s, use, c->st);
+        ntt_inverse(c->dc, m, use, qmap(c, ct->level), c->st);
+        uint64_t* h = (uint64_t*)c->stage((size_t)use * N * 8);
+        ck(cudaMemcpyAsync(h, m, (size_t)use * N * 8, cudaMemcpyDeviceToHost, c->st), "D2H");
+        ck(cudaStreamSynchronize(c->st), "sync");
+        c->release(m);
+        std::vector<double> coef(N);
+        const uint64_t q0 = c->primes[0];
+        if (use == 1) {
+            for (size_t k = 0; k < N; ++k) coef[k] = h[k] > q0 / 2 ? -(double)(q0 - h[k]) : (double)h[k];
+        } else {
+            using host::u128;
+            const uint64_t q1 = c->primes[1];
+            const uint64_t inv = host::invmod(q0 % q1, q1);
+            const u128 Q = (u128)q0 * q1;
+            for (size_t k = 0; k < N; ++k) {
+                const uint64_t x0 = h[k], x1 = h[N + k];
+                const uint64_t x0m = x0 % q1;
+                const uint64_t d = x1 >= x0m ? x1 - x0m : x1 + q1 - x0m;
+                const uint64_t tq = host::mulmod(d, inv, q1);
+                const u128 X = (u128)x0 + (u128)q0 * tq;
+                coef[k] = X > Q / 2 ? -(double)(Q - X) : (double)X;
+            }
+        }
+        host::decode(coef.data(), N, ct->scale, out, n);
+    });
+}
+
+int fhe_ct_level(const fhe_ct* ct) { return ct ? ct->level : -1; }
+double fhe_ct_scale(const fhe_ct* ct) { return ct ? ct->scale : 0.0; }
+int fhe_pt_rows(const fhe_pt* pt) { return pt ? pt->rows : -1; }
+
+int fhe_ct_download(fhe_ctx* c, const fhe_ct* ct, uint64_t* host, size_t words) {
+    return guard(c, [&] {
+        if (words < ct->words()) fail(FHE_E_INVALID, "buffer too small");
+        ck(cudaMemcpyAsync(host, ct->d, ct->words() * 8, cudaMemcpyDeviceToHost, c->st), "D2H");
+        ck(cudaStreamSynchronize(c->st), "sync");
+    });
+}
+
+int fhe_ct_upload(fhe_ctx* c, const uint64_t* host, int level, double scale, fhe_ct** out) {
+    return guard(c, [&] {
+        if (level < 0 || level >= c->L) fail(FHE_E_INVALID, "level out of range");
+        fhe_ct* ct = new_ct(c, level, scale, 0);
+        ck(cudaMemcpyAsync(ct->d, host, ct->words() * 8, cudaMemcpyHostToDevice, c->st), "H2D");
+        *out = ct;
+    });
+}
+
+int fhe_ct_upload_into(fhe_ctx* c, const uint64_t* host, fhe_ct* ct) {
+    return guard(c, [&] {
+        ck(cudaMemcpyAsync(ct->d, host, ct->words() * 8, cudaMemcpyHostToDevice, c->st), "H2D");
+    });
+}
+
+int fhe_pt_download(fhe_ctx* c, const fhe_pt* pt, uint64_t* host, size_t words) {
+    return guard(c, [&] {
+        const size_t need = (size_t)pt->rows * c->N;
+        if (words < need) fail(FHE_E_INVALID, "buffer too small");
+        ck(cudaMemcpyAsync(host, pt->d, need * 8, cudaMemcpyDeviceToHost, c->st), "D2H");
+        ck(cudaStreamSynchronize(c->st), "sync");
+    });
+}
+
+void fhe_ct_free(fhe_ct* ct) {
+    if (!ct) return;
+    ct->ctx->release(ct->d);
+    delete ct;
+}
+void fhe_pt_free(fhe_pt* pt) {
+    if (!pt) return;
+    pt->ctx->release(pt->d);
+    delete pt;
+}
+
+int fhe_rotate_hoisted(fhe_ctx* c, const fhe_ct* ct, const int64_t* ks, size_t n, fhe_ct** outs) {
+    return guard(c, [&] {
+        if (n == 0) fail(FHE_E_INVALID, "empty rotation batch");
+        const int level = ct->level;
+        bool need = false;
+        for (size_t i = 0; i < n; ++i) need |= c->reduce_amount(ks[i]) != 0;
+        for (size_t i = 0; i < n; ++i)
+            if (c->reduce_amount(ks[i])) c->key_for(c->galois_of(c->reduce_amount(ks[i])));
+        uint64_t* digits = nullptr;
+        if (need) {
+            digits = c->alloc((size_t)c->dn_at(level) * c->ne_at(level) * c->N);
+            modup(c, ct->c1(), level, digits);
+        }
+        for (size_t i = 0; i < n; ++i) {
+            const uint64_t a = c->reduce_amount(ks[i]);
+            c->note_amount(a);
+            fhe_ct* o = new_ct(c, level, ct->scale, ct->depth);
+            if (a == 0)
+                ck(cudaMemcpyAsync(o->d, ct->d, ct->words() * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+            else
+                rotate_from_digits(c, ct, digits, c->galois_of(a), o->d);
+            outs[i] = o;
+        }
+        c->release(digits);
+        c->ledger.hoist_groups++;
+        c->ledger.hoisted_rotations += n;
+    });
+}
+
+int fhe_rotate(fhe_ctx* c, const fhe_ct* ct, int64_t k, fhe_ct** out) {
+    return guard(c, [&] {
+        const uint64_t a = c->reduce_amount(k);
+        c->note_amount(a);
+        fhe_ct* o = new_ct(c, ct->level, ct->scale, ct->depth);
+        if (a == 0) {
+            ck(cudaMemcpyAsync(o->d, ct->d, ct->words() * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+        } else {
+            const uint32_t g = c->galois_of(a);
+            c->key_for(g);
+            uint64_t* digits = c->alloc((size_t)c->dn_at(ct->level) * c->ne_at(ct->level) * c->N);
+            modup(c, ct->c1(), ct->level, digits);
+            rotate_from_digits(c, ct, digits, g, o->d);
+            c->release(digits);
+            c->ledger.rotations++;
+        }
+        *out = o;
+    });
+}
+
+int fhe_decompose(int strategy, uint64_t n, uint64_t s, int64_t* steps, int cap) {
+    // reference rot.cpp:21-46
+    if (n >= s) return FHE_E_INVALID;
+    auto floor_pow2 = [](uint64_t v) {
+        uint64_t p = 1;
+        while (p * 2 <= v) p *= 2;
+        return p;
+    };
+    int k = 0;
+    if (strategy == 0) {
+        for (uint64_t bit = floor_pow2(s); bit >= 1; bit /= 2) {
+            if (n & bit) {
+                if (k >= cap) return FHE_E_INVALID;
+                steps[k++] = (int64_t)bit;
+            }
+            if (bit == 1) break;
+        }
+        return k;
+    }
+    int64_t rest = (int64_t)n;
+    while (rest != 0) {
+        const uint64_t mag = (uint64_t)(rest < 0 ? -rest : rest);
+        const uint64_t lo = floor_pow2(mag), hi = lo * 2;
+        const uint64_t pick = (mag - lo <= hi - mag) ? lo : hi;
+        const int64_t step = rest < 0 ? -(int64_t)pick : (int64_t)pick;
+        if (k >= cap) return FHE_E_INVALID;
+        steps[k++] = step;
+        rest -= step;
+    }
+    return k;
+}
+
+int fhe_rotate_decomposed(fhe_ctx* c, const fhe_ct* ct, int64_t k, int strategy, fhe_ct** out) {
+    return guard(c, [&] {
+        const uint64_t a = c->reduce_amount(k);
+        int64_t steps[64];
+        const int ns = fhe_decompose(strategy, a, c->slots(), steps, 64);
+        if (ns < 0) fail(FHE_E_INVALID, "decomposition failed");
+        fhe_ct* cur = new_ct(c, ct->level, ct->scale, ct->depth);
+        ck(cudaMemcpyAsync(cur->d, ct->d, ct->words() * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+        uint64_t* digits = c->alloc((size_t)c->dn_at(ct->level) * c->ne_at(ct->level) * c->N);
+        fhe_ct* nxt = new_ct(c, ct->level, ct->scale, ct->depth);
+        for (int i = 0; i < ns; ++i) {
+            const uint64_t sa = c->reduce_amount(steps[i]);
+            c->note_amount(sa);
+            if (sa == 0) continue;  // a full-cycle step is the identity
+            modup(c, cur->c1(), ct->level, digits);
+            rotate_from_digits(c, cur, digits, c->galois_of(sa), nxt->d);
+            std::swap(cur, nxt);
+            c->ledger.rotations++;
+        }
+        c->release(digits);
+        fhe_ct_free(nxt);
+        *out = cur;
+    });
+}
+
+int fhe_mul_plain(fhe_ctx* c, const fhe_ct* ct, const fhe_pt* pt, fhe_ct** out) {
+    return guard(c, [&] {
+        if (pt->level < ct->level) fail(FHE_E_INVALID, "slot count mismatch");
+        if (ct->level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
+        fhe_ct* o = new_ct(c, ct->level, ct->scale * pt->scale, ct->depth + 1);
+        ew_mul_bcast(c->dc, o->d, ct->d, pt->d, 2 * (ct->level + 1), ct->level + 1, c->st);
+        c->ledger.ct_pt_mults++;
+        c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, o->depth);
+        *out = o;
+    });
+}
+
+int fhe_add(fhe_ctx* c, const fhe_ct* a, const fhe_ct* b, fhe_ct** out) {
+    return guard(c, [&] {
+        if (a->level != b->level) fail(FHE_E_INVALID, "level mismatch");
+        fhe_ct* o = new_ct(c, a->level, a->scale, std::max(a->depth, b->depth));
+        ew_add(c->dc, o->d, a->d, b->d, 2 * (a->level + 1), a->level + 1, c->st);
+        c->ledger.adds++;
+        *out = o;
+    });
+}
+
+int fhe_sub(fhe_ctx* c, const fhe_ct* a, const fhe_ct* b, fhe_ct** out) {
+    return guard(c, [&] {
+        if (a->level != b->level) fail(FHE_E_INVALID, "level mismatch");
+        fhe_ct* o = new_ct(c, a->level, a->scale, std::max(a->depth, b->depth));
+        ew_sub(c->dc, o->d, a->d, b->d, 2 * (a->level + 1), a->level + 1, c->st);
+        c->ledger.adds++;
+        *out = o;
+    });
+}
+
+int fhe_add_plain(fhe_ctx* c, const fhe_ct* ct, const fhe_pt* pt, fhe_ct** out) {
+    return guard(c, [&] {
+        if (pt->level < ct->level) fail(FHE_E_INVALID, "slot count mismatch");
+        const int nr = ct->level + 1;
+        fhe_ct* o = new_ct(c, ct->level, ct->scale, ct->depth);
+        ck(cudaMemcpyAsync(o->c1(), ct->c1(), (size_t)nr * c->N * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+        ew_add(c->dc, o->c0(), ct->c0(), pt->d, nr, nr, c->st);
+        c->ledger.adds++;
+        *out = o;
+    });
+}
+
+int fhe_rescale(fhe_ctx* c, const fhe_ct* ct, fhe_ct** out) {
+    return guard(c, [&] {
+        if (ct->level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
+        fhe_ct* o = new_ct(c, ct->level - 1, ct->scale / (double)c->primes[ct->level], ct->depth);
+        rescale_into(c, ct->d, ct->level, o->d);
+        *out = o;
+    });
+}
+
+int fhe_conv_layer_create(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights, int level,
+                          fhe_conv_layer** out) {
+    return guard(c, [&] {
+        if (kappa % 2 == 0) fail(FHE_E_INVALID, "kernel size must be odd");
+        if (c_out <= 0 || (c_out & (c_out - 1))) fail(FHE_E_INVALID, "output channel count must be a power of two");
+        const size_t s = c->slots(), block = (size_t)m * m;
+        if (m <= 0 || (m & (m - 1)) || block > s || (size_t)c_in * block > s)
+            fail(FHE_E_INVALID, "image does not fit one shard");
+        if ((size_t)c_out * block > s) fail(FHE_E_INVALID, "insufficient capacity");
+        if (kappa / 2 >= m) fail(FHE_E_INVALID, "kernel reach exceeds channel size");
+        if (level < 1 || level >= c->L) fail(FHE_E_INVALID, "level out of range");
+        fhe_conv_layer* ly = new fhe_conv_layer();
+        ly->ctx = c;
+        ly->c_in = c_in;
+        ly->c_out = c_out;
+        ly->m = m;
+        ly->kappa = kappa;
+        ly->level = level;
+        ly->nk = kappa * kappa;
+        const int ne = c->ne_at(level);
+        ly->pt_words = (size_t)c_in * ly->nk * ne * c->N;
+        ck(cudaMalloc(&ly->d_pts, ly->pt_words * 8), "cudaMalloc");
+        ly->nonempty.assign((size_t)c_in * ly->nk, 0);
+        const double pscale = (double)c->primes[level];
+        std::vector<double> plain;
+        const long h = kappa / 2;
+        for (int r = 0; r < c_in; ++r) {
+            int i = 0;
+            for (long kk = -h; kk <= h; ++kk)
+                for (long ll = -h; ll <= h; ++ll, ++i) {
+                    if (!fused_plain(c_in, c_out, m, kappa, s, weights, r, kk, ll, plain)) continue;
+                    ly->nonempty[(size_t)r * ly->nk + i] = 1;
+                    encode_rows(c, plain.data(), s, level, pscale, ne,
+                                ly->d_pts + ((size_t)r * ly->nk + i) * ne * c->N);
+                }
+        }
+        ck(cudaStreamSynchronize(c->st), "sync");
+        *out = ly;
+    });
+}
+
+void fhe_conv_layer_free(fhe_conv_layer* ly) {
+    if (!ly) return;
+    cudaStreamSynchronize(ly->ctx->st);
+    cudaFree(ly->d_pts);
+    delete ly;
+}
+
+int fhe_conv_layer_steps(const fhe_conv_layer* ly, int approach, int64_t* steps, size_t cap, size_t* n) {
+    (void)approach;  // both approaches use the same key set: r m^2 and kk m + ll
+    if (!ly) return FHE_E_INVALID;
+    std::set<int64_t> st;
+    const long h = ly->kappa / 2;
+    for (int r = 1; r < ly->c_in; ++r) st.insert((int64_t)r * ly->m * ly->m);
+    for (long kk = -h; kk <= h; ++kk)
+        for (long ll = -h; ll <= h; ++ll)
+            if (kk || ll) st.insert(kk * ly->m + ll);
+    size_t i = 0;
+    for (int64_t v : st) {
+        if (i < cap && steps) steps[i] = v;
+        ++i;
+    }
+    if (n) *n = i;
+    return FHE_OK;
+}
+
+int fhe_conv2d_into(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct* out) {
+    return guard(c, [&] { conv_impl(c, ct, ly, approach, out); });
+}
+
+int fhe_conv2d(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct** out) {
+    return guard(c, [&] {
+        if (ct->level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
+        fhe_ct* o = new_ct(c, ct->level - 1, ct->scale, ct->depth + 1);
+        try {
+            conv_impl(c, ct, ly, approach, o);
+        } catch (...) {
+            fhe_ct_free(o);
+            throw;
+        }
+        *out = o;
+    });
+}
+
+int fhe_conv2d_batch(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* ly, int approach,
+                     fhe_ct** outs) {
+    return guard(c, [&] {
+        for (size_t i = 0; i < n; ++i) {
+            fhe_ct* o = new_ct(c, cts[i]->level - 1, cts[i]->scale, cts[i]->depth + 1);
+            conv_impl(c, cts[i], ly, approach, o);
+            outs[i] = o;
+        }
+    });
+}
+
+}  // extern "C"

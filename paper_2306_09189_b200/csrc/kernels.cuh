@@ -1,0 +1,145 @@
+// Device data structures and kernel launchers of the encrypted-conv hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace fhe {
+
+constexpr int kMaxPrimes = 40;  // n_q + n_p
+constexpr int kMaxAlpha = 4;    // special primes / digit size
+constexpr int kMaxTerms = 32;   // rotation terms per fused MAC launch
+
+// Basis of a batch of residue rows. Row r belongs to poly r / rows_per_poly
+// and to extended row u = r % rows_per_poly, whose prime index is
+// u <= level ? u : L + (u - level - 1)   (q_0..q_level, then p_0..p_{K-1}).
+// With skip_alpha > 0, rows u in digit (r / rows_per_poly)'s own range
+// [j a, min(j a + a, level + 1)) are skipped (ModUp digits keep those rows
+// in the NTT domain already).
+struct RowMap {
+    int rows_per_poly;
+    int level;
+    int L;
+    int skip_alpha;
+};
+
+FHE_HD int row_prime(const RowMap& m, int u) { return u <= m.level ? u : m.L + (u - m.level - 1); }
+
+// Per-context device constants, passed to kernels by value.
+struct DevCtx {
+    int logN;
+    int N;
+    int L;  // ciphertext primes
+    int K;  // special primes
+    const Prime* primes;    // [L+K]
+    const uint64_t* tw;     // [L+K][N] psi^brv(k)
+    const uint64_t* tw_sh;  // Shoup companions
+    const uint64_t* itw;    // [L+K][N] psi^-brv(k)
+    const uint64_t* itw_sh;
+    const uint64_t* ninv;  // [L+K] N^-1 and Shoup
+    const uint64_t* ninv_sh;
+};
+
+// FastBConv constants of ModUp digit j at level l.
+struct ModUpDigit {
+    int lo, hi;                          // q indices of the digit
+    uint64_t inv[kMaxAlpha];             // [(Q_J/q_i)^-1]_{q_i}
+    uint64_t inv_sh[kMaxAlpha];
+    uint64_t hat[kMaxPrimes][kMaxAlpha];  // [Q_J/q_i]_{t_u}
+    uint64_t hat_sh[kMaxPrimes][kMaxAlpha];
+    uint64_t qj[kMaxPrimes];  // [Q_J]_{t_u}
+};
+
+// ModDown constants (level independent: rows are q_0..q_{L-1}).
+struct ModDownTable {
+    uint64_t pinv[kMaxAlpha];  // [(P/p_k)^-1]_{p_k}
+    uint64_t pinv_sh[kMaxAlpha];
+    uint64_t hat[kMaxPrimes][kMaxAlpha];  // [P/p_k]_{q_i}
+    uint64_t hat_sh[kMaxPrimes][kMaxAlpha];
+    uint64_t pmod[kMaxPrimes];  // [P]_{q_i}
+    uint64_t pmod_sh[kMaxPrimes];
+    uint64_t pinvq[kMaxPrimes];  // [P^-1]_{q_i}
+    uint64_t pinvq_sh[kMaxPrimes];
+};
+
+// Rotation terms of one fused multiply-accumulate launch.
+struct MacTerms {
+    int n;
+    uint32_t galois[kMaxTerms];           // 1 = identity term
+    const uint64_t* key[kMaxTerms];        // [dnum][2][L+K][N], null for identity
+    const uint64_t* pt[kMaxTerms];         // [level+1+K][N]
+};
+
+// --------------------------------------------------------------- launchers
+// All launchers enqueue on `st` and never synchronise.
+void ntt_forward(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);
+void ntt_inverse(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);
+
+void reduce_signed_rows(const DevCtx& c, const int64_t* coef, uint64_t* out, int nrows, const RowMap& rm,
+                        cudaStream_t st);
+void sample_uniform_rows(const DevCtx& c, uint64_t* out, int nrows, const RowMap& rm, uint64_t key,
+                         cudaStream_t st);
+void sample_gauss(const DevCtx& c, int64_t* out, uint64_t key, cudaStream_t st);
+void sample_ternary(const DevCtx& c, int64_t* out, uint64_t key, cudaStream_t st);
+
+// key[j][0][t] = e[t] - a[t] s[t] + [t in digit j] pmod[t] sigma_g(s)[t]; a already in key[j][1]
+void keygen_combine(const DevCtx& c, uint64_t* key_b, const uint64_t* key_a, const uint64_t* e,
+                    const uint64_t* s, uint32_t galois, int lo, int hi, const ModDownTable* md, int nrows,
+                    cudaStream_t st);
+// c0 = e - a s + pt (rows 0..level), a already in c1
+void encrypt_combine(const DevCtx& c, uint64_t* c0, const uint64_t* c1, const uint64_t* e,
+                     const uint64_t* s, const uint64_t* pt, int nrows, cudaStream_t st);
+// m = c0 + c1 s for rows 0..nrows-1
+void decrypt_combine(const DevCtx& c, uint64_t* m, const uint64_t* c0, const uint64_t* c1,
+                     const uint64_t* s, int nrows, cudaStream_t st);
+
+// elementwise over rows 0..nrows-1 of the Q basis (row r -> prime r % rows_per_poly)
+void ew_add(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b, int nrows, int rpp,
+            cudaStream_t st);
+void ew_sub(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b, int nrows, int rpp,
+            cudaStream_t st);
+// out[p][u] = a[p][u] * b[u] (b is one poly broadcast over the polys of a)
+void ew_mul_bcast(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b, int nrows,
+                  int rpp, cudaStream_t st);
+void automorph(const DevCtx& c, uint64_t* out, const uint64_t* in, int nrows, uint32_t galois,
+               cudaStream_t st);
+
+// rescale: tmp holds INTT'd last rows of both polys ([2][N]); writes
+// spread[2][level][N] = centered tmp mod q_i (coefficient domain)
+void rescale_spread(const DevCtx& c, const uint64_t* tmp, uint64_t* spread, int level, cudaStream_t st);
+// out[p][i] = (in[p][i] - spread[p][i]) * q_level^-1
+void rescale_finish(const DevCtx& c, uint64_t* out, const uint64_t* in, const uint64_t* spread, int level,
+                    const uint64_t* qlinv, const uint64_t* qlinv_sh, cudaStream_t st);
+
+// ModUp FastBConv: coef = INTT(c1) (level+1 rows); digits [dn][ne][N];
+// own rows copied from c1_ntt (NTT domain), others in the coefficient domain.
+void modup_bconv(const DevCtx& c, const uint64_t* coef, const uint64_t* c1_ntt, uint64_t* digits,
+                 const ModUpDigit* tables, int level, int dn, cudaStream_t st);
+
+// acc_c[u][k] = sum_j D[j][u][perm_g(k)] key[j][c][prime(u)][k], ne = level+1+K rows
+void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* key, uint64_t* acc0,
+                      uint64_t* acc1, uint32_t galois, int level, int dn, cudaStream_t st);
+
+// ModDown, batched over npoly polys of ne = level+1+K rows each:
+//  pcoef: [npoly][K][N] INTT'd special rows -> conv: [npoly][level+1][N]
+void moddown_bconv(const DevCtx& c, const uint64_t* pcoef, uint64_t* conv, const ModDownTable* md,
+                   int level, int npoly, cudaStream_t st);
+// out[p][i] = (acc[p][i] - conv[p][i]) P^-1 (+ sigma_g(add_src)[i] for p == 0 if add_src)
+void moddown_finish(const DevCtx& c, uint64_t* out, const uint64_t* acc, const uint64_t* conv,
+                    const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
+                    cudaStream_t st);
+// copy the K special rows of each poly's accumulator into [npoly][K][N]
+void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, int level, int npoly,
+                    cudaStream_t st);
+
+// Fused conv multiply-accumulate: for every term i
+//   ACC0 += pt_i * (IP_0(D, key_i, g_i) + [u<=l] P sigma_gi(X.c0))
+//   ACC1 += pt_i * IP_1(D, key_i, g_i)
+// identity terms (g = 1): ACC_c += pt_i * [u<=l] P X.c
+void conv_mac(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* x, const MacTerms& t,
+              const ModDownTable* md, int level, int dn, cudaStream_t st);
+
+}  // namespace fhe

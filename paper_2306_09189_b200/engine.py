@@ -1,0 +1,274 @@
+"""Python host API over the C ABI (include/fheconv.h).
+
+Mirrors the reference's evaluator surface (shardnn::Engine, reference
+proj/include/shardnn/emu.hpp:132-183) and conv entry point (conv_plan,
+proj/src/conv.cpp:266-271) so tests read like the reference's own tests:
+
+    ctx = Context.from_config("cfg3")
+    ctx.keygen(7)
+    layer = ctx.conv_layer(c_in=16, c_out=16, m=32, kappa=3, weights=w)
+    ctx.gen_galois_keys(layer.steps())
+    ct = ctx.encrypt(ctx.encode(image_slots), seed=9000)
+    out = ctx.conv2d(ct, layer, approach=2)       # ConvPlan::ShiftFirst
+    slots = ctx.decrypt(out)
+
+Every call goes to libfheconv.so on the GPU; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+
+# BASELINE.json configs (CKKS parameters of cfg1..cfg5)
+CONFIGS = {
+    "cfg1": dict(log_n=13, q_bits=[60] + [40] * 4, p_bits=[60], log_scale=40),
+    "cfg2": dict(log_n=14, q_bits=[50] * 8, p_bits=[60], log_scale=50),
+    "cfg3": dict(log_n=15, q_bits=[60] + [50] * 12, p_bits=[60, 60], log_scale=50),
+    "cfg4": dict(log_n=16, q_bits=[60] + [50] * 16, p_bits=[60, 60, 60], log_scale=50),
+    "cfg5": dict(log_n=15, q_bits=[60] + [50] * 12, p_bits=[60, 60], log_scale=50),
+}
+
+_L = None
+
+
+def lib():
+    global _L
+    if _L is None:
+        _L = _lib.load()
+    return _L
+
+
+class FheError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class InvalidArgument(FheError, ValueError):
+    pass
+
+
+def _u64(a):
+    return a.ctypes.data_as(_lib.u64p)
+
+
+class Plaintext:
+    def __init__(self, ctx: "Context", h):
+        self.ctx, self.h = ctx, h
+
+    @property
+    def rows(self) -> int:
+        return lib().fhe_pt_rows(self.h)
+
+    def residues(self) -> np.ndarray:
+        out = np.zeros((self.rows, self.ctx.N), dtype=np.uint64)
+        self.ctx._check(lib().fhe_pt_download(self.ctx.h, self.h, _u64(out), out.size))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            lib().fhe_pt_free(self.h)
+            self.h = None
+
+
+class Ciphertext:
+    def __init__(self, ctx: "Context", h):
+        self.ctx, self.h = ctx, h
+
+    @property
+    def level(self) -> int:
+        return lib().fhe_ct_level(self.h)
+
+    @property
+    def scale(self) -> float:
+        return lib().fhe_ct_scale(self.h)
+
+    def residues(self) -> np.ndarray:
+        out = np.zeros((2, self.level + 1, self.ctx.N), dtype=np.uint64)
+        self.ctx._check(lib().fhe_ct_download(self.ctx.h, self.h, _u64(out), out.size))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            lib().fhe_ct_free(self.h)
+            self.h = None
+
+
+class ConvLayer:
+    def __init__(self, ctx: "Context", h, c_in, c_out, m, kappa, level):
+        self.ctx, self.h = ctx, h
+        self.c_in, self.c_out, self.m, self.kappa, self.level = c_in, c_out, m, kappa, level
+
+    def steps(self, approach: int = 2) -> list[int]:
+        buf = (C.c_int64 * 1024)()
+        n = C.c_size_t(0)
+        self.ctx._check(lib().fhe_conv_layer_steps(self.h, approach, buf, 1024, C.byref(n)))
+        return [buf[i] for i in range(n.value)]
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            lib().fhe_conv_layer_free(self.h)
+            self.h = None
+
+
+class Context:
+    """One B200, one CUDA stream; owns keys and the cost ledger."""
+
+    def __init__(self, log_n: int, q_bits: Sequence[int], p_bits: Sequence[int], log_scale: int, device: int = 0):
+        self.log_n, self.N = log_n, 1 << log_n
+        self.slots = self.N // 2
+        self.q_bits, self.p_bits = list(q_bits), list(p_bits)
+        qa = (C.c_int * len(q_bits))(*q_bits)
+        pa = (C.c_int * len(p_bits))(*p_bits)
+        self._keep = (qa, pa)
+        p = _lib.FheParams(log_n, len(q_bits), qa, len(p_bits), pa, log_scale, device)
+        h = C.c_void_p()
+        rc = lib().fhe_ctx_create(C.byref(p), C.byref(h))
+        if rc != 0:
+            raise FheError(rc, f"fhe_ctx_create failed ({rc})")
+        self.h = h.value
+        nq, npp, dn = C.c_int(), C.c_int(), C.c_int()
+        primes = (C.c_uint64 * (len(q_bits) + len(p_bits)))()
+        lib().fhe_ctx_info(self.h, None, C.byref(nq), C.byref(npp), C.byref(dn), primes)
+        self.L, self.K, self.dnum = nq.value, npp.value, dn.value
+        self.primes = list(primes)
+        self.scale = 2.0 ** log_scale
+        self.max_level = self.L - 1
+
+    @classmethod
+    def from_config(cls, name: str, device: int = 0) -> "Context":
+        return cls(device=device, **CONFIGS[name])
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fhe_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    # ------------------------------------------------------------- helpers
+    def _check(self, rc: int):
+        if rc != 0:
+            msg = lib().fhe_last_error(self.h).decode()
+            if rc == _lib.FHE_E_INVALID:
+                raise InvalidArgument(rc, msg)
+            raise FheError(rc, msg)
+
+    def _new(self, fn, *args, cls=Ciphertext):
+        out = C.c_void_p()
+        self._check(fn(self.h, *args, C.byref(out)))
+        return cls(self, out.value)
+
+    def synchronize(self):
+        self._check(lib().fhe_synchronize(self.h))
+
+    # ---------------------------------------------------------------- keys
+    def keygen(self, seed: int):
+        self._check(lib().fhe_keygen(self.h, seed))
+
+    def gen_galois_keys(self, steps: Iterable[int]):
+        a = np.ascontiguousarray(list(steps), dtype=np.int64)
+        self._check(lib().fhe_gen_galois_keys(self.h, a.ctypes.data_as(_lib.i64p), len(a)))
+
+    def galois_key(self, step: int) -> np.ndarray:
+        out = np.zeros((self.dnum, 2, self.L + self.K, self.N), dtype=np.uint64)
+        self._check(lib().fhe_galois_key_download(self.h, step, _u64(out), out.size))
+        return out
+
+    # ---------------------------------------------------------------- data
+    def encode(self, slots, level: int | None = None, scale: float | None = None,
+               with_special: bool = False) -> Plaintext:
+        z = np.ascontiguousarray(slots, dtype=np.float64)
+        level = self.max_level if level is None else level
+        scale = self.scale if scale is None else scale
+        return self._new(lib().fhe_encode, z.ctypes.data_as(_lib.dp), len(z), level, scale, int(with_special),
+                         cls=Plaintext)
+
+    def encrypt(self, pt: Plaintext, seed: int) -> Ciphertext:
+        return self._new(lib().fhe_encrypt, pt.h, seed)
+
+    def decrypt(self, ct: Ciphertext, n: int | None = None) -> np.ndarray:
+        n = self.slots if n is None else n
+        out = np.zeros(n)
+        self._check(lib().fhe_decrypt_decode(self.h, ct.h, out.ctypes.data_as(_lib.dp), n))
+        return out
+
+    def upload(self, residues: np.ndarray, level: int, scale: float | None = None) -> Ciphertext:
+        r = np.ascontiguousarray(residues, dtype=np.uint64)
+        assert r.size == 2 * (level + 1) * self.N
+        return self._new(lib().fhe_ct_upload, _u64(r), level, self.scale if scale is None else scale)
+
+    # ----------------------------------------------------------------- ops
+    def rotate(self, ct: Ciphertext, k: int) -> Ciphertext:
+        return self._new(lib().fhe_rotate, ct.h, k)
+
+    def rotate_hoisted(self, ct: Ciphertext, ks: Sequence[int]) -> list[Ciphertext]:
+        a = np.ascontiguousarray(list(ks), dtype=np.int64)
+        outs = (C.c_void_p * max(1, len(a)))()
+        self._check(lib().fhe_rotate_hoisted(self.h, ct.h, a.ctypes.data_as(_lib.i64p), len(a), outs))
+        return [Ciphertext(self, outs[i]) for i in range(len(a))]
+
+    rotate_many = rotate_hoisted  # reference name (emu.hpp:164)
+
+    def rotate_decomposed(self, ct: Ciphertext, k: int, strategy: int) -> Ciphertext:
+        return self._new(lib().fhe_rotate_decomposed, ct.h, k, strategy)
+
+    def mul_plain(self, ct: Ciphertext, pt: Plaintext) -> Ciphertext:
+        return self._new(lib().fhe_mul_plain, ct.h, pt.h)
+
+    def add(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+        return self._new(lib().fhe_add, a.h, b.h)
+
+    def sub(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+        return self._new(lib().fhe_sub, a.h, b.h)
+
+    def add_plain(self, ct: Ciphertext, pt: Plaintext) -> Ciphertext:
+        return self._new(lib().fhe_add_plain, ct.h, pt.h)
+
+    def rescale(self, ct: Ciphertext) -> Ciphertext:
+        return self._new(lib().fhe_rescale, ct.h)
+
+    # ---------------------------------------------------------------- conv
+    def conv_layer(self, c_in: int, c_out: int, m: int, kappa: int, weights, level: int | None = None) -> ConvLayer:
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        assert w.size == c_in * c_out * kappa * kappa
+        level = self.max_level if level is None else level
+        out = C.c_void_p()
+        self._check(lib().fhe_conv_layer_create(self.h, c_in, c_out, m, kappa, w.ctypes.data_as(_lib.dp), level,
+                                                C.byref(out)))
+        return ConvLayer(self, out.value, c_in, c_out, m, kappa, level)
+
+    def conv2d(self, ct: Ciphertext, layer: ConvLayer, approach: int = 2) -> Ciphertext:
+        return self._new(lib().fhe_conv2d, ct.h, layer.h, approach)
+
+    def conv2d_into(self, ct: Ciphertext, layer: ConvLayer, approach: int, out: Ciphertext):
+        self._check(lib().fhe_conv2d_into(self.h, ct.h, layer.h, approach, out.h))
+
+    # -------------------------------------------------------------- ledger
+    def ledger(self) -> dict:
+        lg = _lib.FheLedger()
+        self._check(lib().fhe_ledger_get(self.h, C.byref(lg)))
+        return {f: getattr(lg, f) for f in _lib.LEDGER_FIELDS}
+
+    def ledger_reset(self):
+        self._check(lib().fhe_ledger_reset(self.h))
+
+    def rotation_amounts(self) -> list[int]:
+        buf = (C.c_uint64 * 4096)()
+        n = C.c_size_t(0)
+        self._check(lib().fhe_ledger_amounts(self.h, buf, 4096, C.byref(n)))
+        return [buf[i] for i in range(min(n.value, 4096))]
+
+
+def decompose(strategy: int, n: int, s: int) -> list[int]:
+    """reference rot.cpp:21-46 (0 = positive, 1 = signed)."""
+    buf = (C.c_int64 * 64)()
+    k = lib().fhe_decompose(strategy, n, s, buf, 64)
+    if k < 0:
+        raise InvalidArgument(k, "amount must satisfy 0 <= n < s")
+    return [buf[i] for i in range(k)]
