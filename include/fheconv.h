@@ -81,6 +81,14 @@ const char* fhe_last_error(const fhe_ctx* ctx);
 /* N, slots, n_q, n_p, dnum, primes (n_q + n_p entries, q's then p's) */
 int fhe_ctx_info(const fhe_ctx* ctx, int* log_n, int* n_q, int* n_p, int* dnum, uint64_t* primes);
 int fhe_synchronize(fhe_ctx* ctx);
+/* device-side timing on the context's stream (CUDA events) */
+int fhe_timer_start(fhe_ctx* ctx);
+int fhe_timer_stop(fhe_ctx* ctx, float* ms); /* synchronises; ms since fhe_timer_start */
+/* per-kernel-class CUDA-event profiling of the hot kernels (off by default).
+ * class names: "conv_mac", "ks_inner", "ntt", "modup_bconv", "moddown", "rescale" */
+int fhe_prof_enable(fhe_ctx* ctx, int on);
+int fhe_prof_get(fhe_ctx* ctx, const char* kernel_class, double* total_ms, uint64_t* launches);
+int fhe_prof_reset(fhe_ctx* ctx);
 /* replaces: Engine::ledger() emu.hpp:137-138, CostLedger::reset emu.hpp:77-88 */
 int fhe_ledger_get(const fhe_ctx* ctx, fhe_ledger* out);
 int fhe_ledger_reset(fhe_ctx* ctx);

@@ -43,6 +43,11 @@ SIGNATURES = [
     ("fhe_ctx_info", C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                C.POINTER(C.c_int), u64p]),
     ("fhe_synchronize", C.c_int, [vp]),
+    ("fhe_timer_start", C.c_int, [vp]),
+    ("fhe_timer_stop", C.c_int, [vp, C.POINTER(C.c_float)]),
+    ("fhe_prof_enable", C.c_int, [vp, C.c_int]),
+    ("fhe_prof_get", C.c_int, [vp, C.c_char_p, C.POINTER(C.c_double), u64p]),
+    ("fhe_prof_reset", C.c_int, [vp]),
     ("fhe_ledger_get", C.c_int, [vp, C.POINTER(FheLedger)]),
     ("fhe_ledger_reset", C.c_int, [vp]),
     ("fhe_ledger_amounts", C.c_int, [vp, u64p, C.c_size_t, C.POINTER(C.c_size_t)]),

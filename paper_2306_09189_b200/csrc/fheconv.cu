@@ -61,6 +61,53 @@ struct fhe_ctx {
     // pinned staging
     void* h_stage = nullptr;
     size_t h_stage_bytes = 0;
+    // timing / profiling (CUDA events on st)
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    bool prof_on = false;
+    struct ProfRec {
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+        double ms = 0;
+        uint64_t n = 0;
+    };
+    std::map<std::string, ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+
+    cudaEvent_t get_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        return e;
+    }
+    template <class F>
+    void timed(const char* cls, F&& f) {
+        if (!prof_on) {
+            f();
+            return;
+        }
+        cudaEvent_t a = get_event(), b = get_event();
+        cudaEventRecord(a, st);
+        f();
+        cudaEventRecord(b, st);
+        prof[cls].pending.emplace_back(a, b);
+    }
+    void prof_collect() {
+        ck(cudaStreamSynchronize(st), "sync");
+        for (auto& kv : prof) {
+            for (auto& pr : kv.second.pending) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, pr.first, pr.second);
+                kv.second.ms += ms;
+                kv.second.n++;
+                ev_pool.push_back(pr.first);
+                ev_pool.push_back(pr.second);
+            }
+            kv.second.pending.clear();
+        }
+    }
 
     // ------------------------------------------------------------ helpers
     uint64_t* alloc(size_t words) {
@@ -151,7 +198,6 @@ int guard(const fhe_ctx* ctx, F&& f) {
 }
 
 RowMap qmap(const fhe_ctx* c, int level) { return RowMap{level + 1, level, c->L, 0}; }
-RowMap extmap(const fhe_ctx* c, int level) { return RowMap{level + 1 + c->K, level, c->L, 0}; }
 
 fhe_ct* new_ct(fhe_ctx* c, int level, double scale, int depth) {
     fhe_ct* ct = new fhe_ct{c, level, scale, depth, nullptr};
@@ -166,9 +212,11 @@ void modup(fhe_ctx* c, const uint64_t* c1, int level, uint64_t* digits) {
     const int nr = level + 1, dn = c->dn_at(level), ne = c->ne_at(level);
     uint64_t* coef = c->alloc((size_t)nr * c->N);
     ck(cudaMemcpyAsync(coef, c1, (size_t)nr * c->N * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
-    ntt_inverse(c->dc, coef, nr, qmap(c, level), c->st);
-    modup_bconv(c->dc, coef, c1, digits, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
-    ntt_forward(c->dc, digits, dn * ne, RowMap{ne, level, c->L, c->alpha}, c->st);
+    c->timed("ntt", [&] { ntt_inverse(c->dc, coef, nr, qmap(c, level), c->st); });
+    c->timed("modup_bconv", [&] {
+        modup_bconv(c->dc, coef, c1, digits, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+    });
+    c->timed("ntt", [&] { ntt_forward(c->dc, digits, dn * ne, RowMap{ne, level, c->L, c->alpha}, c->st); });
     c->release(coef);
     c->ledger.modups++;
     c->launched(6);
@@ -180,11 +228,12 @@ void moddown(fhe_ctx* c, const uint64_t* acc, int level, int npoly, uint64_t* ou
     const int nr = level + 1;
     uint64_t* pc = c->alloc((size_t)npoly * c->K * c->N);
     uint64_t* conv = c->alloc((size_t)npoly * nr * c->N);
-    gather_special(c->dc, pc, acc, level, npoly, c->st);
-    ntt_inverse(c->dc, pc, npoly * c->K, RowMap{c->K, -1, c->L, 0}, c->st);
-    moddown_bconv(c->dc, pc, conv, c->d_md, level, npoly, c->st);
-    ntt_forward(c->dc, conv, npoly * nr, qmap(c, level), c->st);
-    moddown_finish(c->dc, out, acc, conv, c->d_md, level, npoly, add_src, g, c->st);
+    c->timed("moddown", [&] { gather_special(c->dc, pc, acc, level, npoly, c->st); });
+    c->timed("ntt", [&] { ntt_inverse(c->dc, pc, npoly * c->K, RowMap{c->K, -1, c->L, 0}, c->st); });
+    c->timed("moddown", [&] { moddown_bconv(c->dc, pc, conv, c->d_md, level, npoly, c->st); });
+    c->timed("ntt", [&] { ntt_forward(c->dc, conv, npoly * nr, qmap(c, level), c->st); });
+    c->timed("moddown",
+             [&] { moddown_finish(c->dc, out, acc, conv, c->d_md, level, npoly, add_src, g, c->st); });
     c->release(pc);
     c->release(conv);
     c->ledger.moddowns += npoly;
@@ -195,8 +244,10 @@ void moddown(fhe_ctx* c, const uint64_t* acc, int level, int npoly, uint64_t* ou
 void rotate_from_digits(fhe_ctx* c, const fhe_ct* ct, const uint64_t* digits, uint32_t g, uint64_t* out) {
     const int level = ct->level, ne = c->ne_at(level);
     uint64_t* acc = c->alloc((size_t)2 * ne * c->N);
-    ks_inner_product(c->dc, digits, c->key_for(g), acc, acc + (size_t)ne * c->N, g, level, c->dn_at(level),
-                     c->st);
+    const uint64_t* key = c->key_for(g);
+    c->timed("ks_inner", [&] {
+        ks_inner_product(c->dc, digits, key, acc, acc + (size_t)ne * c->N, g, level, c->dn_at(level), c->st);
+    });
     moddown(c, acc, level, 2, out, ct->c0(), g);
     c->release(acc);
     c->ledger.key_switches++;
@@ -210,11 +261,13 @@ void rescale_into(fhe_ctx* c, const uint64_t* in, int level, uint64_t* out) {
     ck(cudaMemcpyAsync(tmp, in + (size_t)level * N, N * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
     ck(cudaMemcpyAsync(tmp + N, in + ((size_t)level + 1 + level) * N, N * 8, cudaMemcpyDeviceToDevice, c->st),
        "memcpy");
-    ntt_inverse(c->dc, tmp, 2, RowMap{1, -1, level, 0}, c->st);
-    rescale_spread(c->dc, tmp, spread, level, c->st);
-    ntt_forward(c->dc, spread, 2 * level, qmap(c, level - 1), c->st);
-    rescale_finish(c->dc, out, in, spread, level, c->d_qlinv + (size_t)level * c->L,
-                   c->d_qlinv_sh + (size_t)level * c->L, c->st);
+    c->timed("ntt", [&] { ntt_inverse(c->dc, tmp, 2, RowMap{1, -1, level, 0}, c->st); });
+    c->timed("rescale", [&] { rescale_spread(c->dc, tmp, spread, level, c->st); });
+    c->timed("ntt", [&] { ntt_forward(c->dc, spread, 2 * level, qmap(c, level - 1), c->st); });
+    c->timed("rescale", [&] {
+        rescale_finish(c->dc, out, in, spread, level, c->d_qlinv + (size_t)level * c->L,
+                       c->d_qlinv_sh + (size_t)level * c->L, c->st);
+    });
     c->release(tmp);
     c->release(spread);
     c->ledger.rescales++;
@@ -487,7 +540,7 @@ void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
     auto pt_of = [&](int r, int i) { return ly->d_pts + ((size_t)r * nk + i) * extw; };
     auto run_terms = [&](MacTerms& t, const fhe_ct& src) {
         if (t.n == 0) return;
-        conv_mac(c->dc, acc, dtmp, src.d, t, c->d_md, level, dn, c->st);
+        c->timed("conv_mac", [&] { conv_mac(c->dc, acc, dtmp, src.d, t, c->d_md, level, dn, c->st); });
         for (int i = 0; i < t.n; ++i)
             if (t.galois[i] != 1) c->ledger.key_switches++;
         c->launched();
@@ -617,6 +670,14 @@ void fhe_ctx_destroy(fhe_ctx* c) {
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->t0) cudaEventDestroy(c->t0);
+    if (c->t1) cudaEventDestroy(c->t1);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (auto& kv : c->prof)
+        for (auto& pr : kv.second.pending) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
 }
@@ -635,6 +696,46 @@ int fhe_ctx_info(const fhe_ctx* c, int* log_n, int* n_q, int* n_p, int* dnum, ui
 
 int fhe_synchronize(fhe_ctx* c) {
     return guard(c, [&] { ck(cudaStreamSynchronize(c->st), "cudaStreamSynchronize"); });
+}
+
+int fhe_timer_start(fhe_ctx* c) {
+    return guard(c, [&] {
+        if (!c->t0) ck(cudaEventCreate(&c->t0), "cudaEventCreate");
+        if (!c->t1) ck(cudaEventCreate(&c->t1), "cudaEventCreate");
+        ck(cudaEventRecord(c->t0, c->st), "cudaEventRecord");
+    });
+}
+
+int fhe_timer_stop(fhe_ctx* c, float* ms) {
+    return guard(c, [&] {
+        if (!c->t0) fail(FHE_E_INVALID, "timer not started");
+        ck(cudaEventRecord(c->t1, c->st), "cudaEventRecord");
+        ck(cudaEventSynchronize(c->t1), "cudaEventSynchronize");
+        ck(cudaEventElapsedTime(ms, c->t0, c->t1), "cudaEventElapsedTime");
+    });
+}
+
+int fhe_prof_enable(fhe_ctx* c, int on) {
+    return guard(c, [&] {
+        c->prof_collect();
+        c->prof_on = on != 0;
+    });
+}
+
+int fhe_prof_get(fhe_ctx* c, const char* cls, double* total_ms, uint64_t* launches) {
+    return guard(c, [&] {
+        c->prof_collect();
+        auto it = c->prof.find(cls);
+        if (total_ms) *total_ms = it == c->prof.end() ? 0.0 : it->second.ms;
+        if (launches) *launches = it == c->prof.end() ? 0 : it->second.n;
+    });
+}
+
+int fhe_prof_reset(fhe_ctx* c) {
+    return guard(c, [&] {
+        c->prof_collect();
+        c->prof.clear();
+    });
 }
 
 int fhe_ledger_get(const fhe_ctx* c, fhe_ledger* out) {

@@ -167,6 +167,26 @@ class Context:
     def synchronize(self):
         self._check(lib().fhe_synchronize(self.h))
 
+    def timer_start(self):
+        self._check(lib().fhe_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_float(0)
+        self._check(lib().fhe_timer_stop(self.h, C.byref(ms)))
+        return ms.value
+
+    def prof_enable(self, on: bool = True):
+        self._check(lib().fhe_prof_enable(self.h, int(on)))
+
+    def prof_reset(self):
+        self._check(lib().fhe_prof_reset(self.h))
+
+    def prof_get(self, cls: str) -> tuple[float, int]:
+        ms = C.c_double(0)
+        n = C.c_uint64(0)
+        self._check(lib().fhe_prof_get(self.h, cls.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
     # ---------------------------------------------------------------- keys
     def keygen(self, seed: int):
         self._check(lib().fhe_keygen(self.h, seed))

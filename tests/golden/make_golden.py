@@ -1,0 +1,120 @@
+"""Generates tests/golden/golden.npz from the UNMODIFIED reference.
+
+Run in the container that has /root/reference (the GPU box does not):
+    make -C oracle && python tests/golden/make_golden.py
+
+Every value comes from the reference's own code compiled where it lies
+(oracle/_ref/libshardnn_ref.so built by oracle/Makefile; ref_shim.cpp only
+adapts calling conventions): inputs from its test helpers
+(tests/helpers.hpp:13-27), conv outputs and ledgers from conv_plan /
+convolve (conv.cpp:254-371), decompositions from rot.cpp:21-129.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "..", "..", "oracle"))
+import pyoracle as po  # noqa: E402
+
+# name: (c, m, kappa, c_out, seed_img, seed_filt, weight_kind, shard size s)
+CONV_CASES = {
+    "cfg1": (4, 32, 3, 4, 1000, 2000, 0, 4096),
+    "cfg3": (16, 32, 3, 16, 1001, 2001, 0, 16384),
+    "cfg4": (8, 64, 5, 8, 1002, 2002, 2, 32768),
+    "small_c4m4k3": (4, 4, 3, 4, 39, 139, 0, 64),
+    "small_c2m8k5": (2, 8, 5, 2, 94, 194, 0, 128),
+    "small_c4m4k1": (4, 4, 1, 4, 33, 133, 0, 64),
+    "small_c4to2": (4, 4, 3, 2, 34, 134, 0, 64),
+    "small_dup_c2m4k3": (2, 4, 3, 2, 35, 135, 0, 64),
+}
+CFG5 = dict(c=16, m=32, kappa=3, seed_img=1003, seed_filts=(2003, 2004, 2005), weight_kind=1, s=16384)
+
+
+def main():
+    R = po.ref()
+    out = {}
+    for name, (c, m, k, co, si, sf, wk, s) in CONV_CASES.items():
+        img, filt = po.make_inputs(c, m, k, co, si, sf, wk, use_ref=True)
+        res = {}
+        for plan in (0, 1, 2):
+            res[plan] = po.ref_conv(c, m, k, co, img, filt, plan, s)
+        assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[1][0], res[2][0])
+        oracle = np.zeros(co * m * m)
+        R.ref_oracle_conv(c, m, k, co, img.ctypes.data_as(po.dp), filt.ctypes.data_as(po.dp), 1,
+                          oracle.ctypes.data_as(po.dp))
+        out[f"{name}/params"] = np.array([c, m, k, co, si, sf, wk, s], dtype=np.int64)
+        out[f"{name}/img"] = img if img.size <= 4096 else img[:64]
+        out[f"{name}/img_sum"] = np.array([img.sum(), np.abs(img).sum()])
+        out[f"{name}/filt"] = filt
+        out[f"{name}/slots"] = res[2][0]
+        if not np.array_equal(res[2][1], res[2][0][: co * m * m]):
+            out[f"{name}/image"] = res[2][1]
+        # textbook oracle agrees to ~1e-14 (summation order differs); keep its max deviation
+        out[f"{name}/oracle_dev"] = np.array([np.abs(oracle - res[2][1]).max()])
+        if oracle.size <= 4096:
+            out[f"{name}/oracle_conv"] = oracle
+        for plan in (0, 1, 2):
+            out[f"{name}/ledger{plan}"] = res[plan][2]
+        out[f"{name}/level_drop"] = np.array([res[2][3]])
+    # cfg5: three stacked layers, each input = previous output image
+    x, _ = po.make_inputs(CFG5["c"], CFG5["m"], CFG5["kappa"], CFG5["c"], CFG5["seed_img"], 0, 0, use_ref=True)
+    out["cfg5/img_sum"] = np.array([x.sum(), np.abs(x).sum()])
+    for li, sf in enumerate(CFG5["seed_filts"]):
+        _, filt = po.make_inputs(CFG5["c"], CFG5["m"], CFG5["kappa"], CFG5["c"], 0, sf, CFG5["weight_kind"],
+                                 use_ref=True)
+        slots, image, ledger, drop = po.ref_conv(CFG5["c"], CFG5["m"], CFG5["kappa"], CFG5["c"], x, filt, 2,
+                                                 CFG5["s"])
+        out[f"cfg5/filt{li}"] = filt
+        out[f"cfg5/out{li}"] = slots
+        x = image
+    # rotation decompositions (rot.cpp:21-94)
+    import ctypes as C
+    for s in (4096, 8192):
+        lens = np.zeros((2, s), dtype=np.int8)
+        sums = np.zeros((2, s), dtype=np.int32)
+        first = np.zeros((2, 1024, 16), dtype=np.int16)
+        buf = (C.c_long * 64)()
+        for strat in (0, 1):
+            for n in range(s):
+                k = R.ref_decompose(strat, n, s, buf, 64)
+                lens[strat, n] = k
+                sums[strat, n] = sum(buf[i] for i in range(k))
+                if n < 1024:
+                    first[strat, n, :k] = [buf[i] for i in range(k)]
+        out[f"decomp{s}/lens"] = lens
+        out[f"decomp{s}/sums"] = sums
+        out[f"decomp{s}/steps_lt1024"] = first
+    ml = np.zeros(4096, dtype=np.uint64)
+    R.ref_min_lengths(4095, 4096, ml.ctypes.data_as(po.u64p))
+    out["minlen4096"] = ml.astype(np.int8)
+    # planner (rot.cpp:96-129): cfg2 amounts 1..127 and the 3x3 stencil (m = 32)
+    def plan(amounts, same, s, strat):
+        n = len(amounts)
+        a = (C.c_long * n)(*amounts)
+        ss = (C.c_int * n)(*same)
+        steps = (C.c_long * (64 * n))()
+        ns = (C.c_int * n)()
+        g = (C.c_int * n)()
+        gh = (C.c_int * n)()
+        tot = R.ref_plan_rotations(a, ss, n, s, strat, steps, ns, g, gh)
+        return tot, np.array(list(ns)), np.array(list(g)), np.array(list(gh))
+    amounts = list(range(1, 128))
+    stencil = [kk * 32 + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1)]
+    for strat in (0, 1, 2):
+        tot, ns, g, gh = plan(amounts, [0] * 127, 8192, strat)
+        out[f"plan_cfg2/strat{strat}/total"] = np.array([tot])
+        out[f"plan_cfg2/strat{strat}/nsteps"] = ns
+        tot, ns, g, gh = plan(stencil, [0] + [1] * 8, 8192, strat)
+        out[f"plan_stencil/strat{strat}/total"] = np.array([tot])
+        out[f"plan_stencil/strat{strat}/nsteps"] = ns
+        out[f"plan_stencil/strat{strat}/groups"] = g
+        out[f"plan_stencil/strat{strat}/hoisted"] = gh
+    path = os.path.join(HERE, "golden.npz")
+    np.savez_compressed(path, **out)
+    print(path, os.path.getsize(path), "bytes,", len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()

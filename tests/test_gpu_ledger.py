@@ -1,0 +1,94 @@
+"""Operation-count laws of the reference (test_conv.cpp:244-276,
+acceptance.cpp:205-243) hold for the CKKS path's ledger, plus error
+behaviour matching the reference's exception messages."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2306_09189_b200 import Context
+    c = Context.from_config("cfg1")
+    c.keygen(7)
+    return c
+
+
+def run(ctx, oracle, approach, name="cfg1"):
+    img, filt = oracle.make_inputs(4, 32, 3, 4, 1000, 2000, 0)
+    layer = ctx.conv_layer(4, 4, 32, 3, filt)
+    ctx.gen_galois_keys(layer.steps())
+    ct = ctx.encrypt(ctx.encode(img), 9000)
+    ctx.ledger_reset()
+    out = ctx.conv2d(ct, layer, approach)
+    return ctx.ledger(), out, ct
+
+
+@pytest.mark.parametrize("approach,plan", [(1, 1), (2, 2)])
+def test_ledger_matches_reference(ctx, oracle, golden, approach, plan):
+    lg, out, ct = run(ctx, oracle, approach)
+    ref = [int(x) for x in golden[f"cfg1/ledger{plan}"]]
+    got = [lg[f] for f in ("rotations", "hoisted_rotations", "hoist_groups", "ct_pt_mults", "ct_ct_mults", "adds",
+                           "bootstraps", "max_depth_consumed", "distinct_amounts")]
+    assert got == ref
+    assert out.level == ct.level - 1  # one level per conv (test_conv.cpp:210-223)
+
+
+def test_ckks_work_counts(ctx, oracle):
+    lg, _, _ = run(ctx, oracle, 2)
+    # Approach 2: one ModUp of src + one per channel-rotated copy; c-1 + c(k^2-1) key switches;
+    # one ModDown per channel rotation (2 polys) + one fused ModDown pair; one rescale
+    assert lg["modups"] == 1 + 4
+    assert lg["key_switches"] == 3 + 4 * 8
+    assert lg["moddowns"] == 2 * 3 + 2
+    assert lg["rescales"] == 1
+    lg, _, _ = run(ctx, oracle, 1)
+    assert lg["modups"] == 1 + 9
+    assert lg["key_switches"] == 8 + 9 * 3
+
+
+def test_error_messages(ctx):
+    from paper_2306_09189_b200 import FheError, InvalidArgument
+    z = np.zeros(ctx.slots)
+    ct = ctx.encrypt(ctx.encode(z), 1)
+    with pytest.raises(InvalidArgument, match="empty rotation batch"):
+        ctx.rotate_hoisted(ct, [])
+    with pytest.raises(InvalidArgument, match="slot count must be a power of two"):
+        ctx.encode(np.zeros(3))
+    low = ctx.encrypt(ctx.encode(z, level=0), 1)
+    with pytest.raises(FheError, match="depth exhausted"):
+        ctx.rescale(low)
+    with pytest.raises(InvalidArgument, match="insufficient capacity"):
+        ctx.conv_layer(4, 8, 32, 3, np.zeros(4 * 8 * 9))
+    with pytest.raises(InvalidArgument, match="kernel size must be odd"):
+        ctx.conv_layer(4, 4, 32, 2, np.zeros(4 * 4 * 4))
+    with pytest.raises(FheError, match="missing Galois key"):
+        ctx.rotate(ct, 12345)
+
+
+def test_zero_filter_and_identity(ctx, oracle):
+    """all-empty plaintexts (Acc::finish zero product, conv.cpp:25-28) and the identity filter."""
+    img, _ = oracle.make_inputs(4, 32, 3, 4, 1000, 2000, 0)
+    ct = ctx.encrypt(ctx.encode(img), 9000)
+    zero = ctx.conv_layer(4, 4, 32, 3, np.zeros(4 * 4 * 9))
+    assert np.abs(ctx.decrypt(ctx.conv2d(ct, zero, 2))).max() < 1e-6
+    ident = np.zeros((4, 4, 3, 3))
+    for f in range(4):
+        ident[f, f, 1, 1] = 1.0
+    layer = ctx.conv_layer(4, 4, 32, 3, ident.ravel())
+    for ap in (1, 2):
+        assert np.abs(ctx.decrypt(ctx.conv2d(ct, layer, ap)) - img).max() < 1e-6
+
+
+def test_cxx_engine_demo_runs():
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = "/tmp/fheconv_engine_demo_gpu"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cxx", "engine_demo.cpp"), "-o", exe,
+                    "-L", os.path.join(root, "paper_2306_09189_b200"), "-lfheconv",
+                    f"-Wl,-rpath,{os.path.join(root, 'paper_2306_09189_b200')}"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

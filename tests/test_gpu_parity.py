@@ -1,0 +1,237 @@
+"""GPU parity: every op of libfheconv (through the C ABI) is bit-exact with
+the CPU golden model (oracle/ckks_ref.c) on the same seeds, and decrypted
+conv outputs agree with the reference's conv_plan slots within 1e-6
+(BASELINE north star). Tolerance 1e-6 absolute on decrypted slots."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-6
+KEY_SEED, ENC_SEED = 7, 9000
+
+
+class Pair:
+    """GPU context + CPU golden model with the same parameters and keys."""
+
+    def __init__(self, oracle, name):
+        from paper_2306_09189_b200 import CONFIGS, Context
+        p = CONFIGS[name]
+        self.ctx = Context.from_config(name)
+        self.ck = oracle.CKKS(p["log_n"], p["q_bits"], p["p_bits"], p["log_scale"])
+        self.ctx.keygen(KEY_SEED)
+        self.ck.keygen(KEY_SEED)
+        self.top = self.ctx.max_level
+
+
+_pairs = {}
+
+
+def pair(oracle, name):
+    if name not in _pairs:
+        _pairs[name] = Pair(oracle, name)
+    return _pairs[name]
+
+
+@pytest.fixture(scope="module")
+def p1(oracle):
+    return pair(oracle, "cfg1")
+
+
+def rnd(n, seed):
+    return np.random.default_rng(seed).uniform(-1, 1, n)
+
+
+def test_primes_match_golden_model(oracle):
+    for name in ("cfg1", "cfg2", "cfg3", "cfg4"):
+        p = pair(oracle, name)
+        assert p.ctx.primes == p.ck.primes
+
+
+def test_encode_encrypt_bit_exact(p1):
+    z = rnd(p1.ctx.slots, 1)
+    pt = p1.ctx.encode(z)
+    ptr = p1.ck.encode(z, p1.ck.scale, p1.top)
+    assert np.array_equal(pt.residues(), ptr)
+    ptp = p1.ctx.encode(z, with_special=True)
+    assert np.array_equal(ptp.residues(), p1.ck.encode(z, p1.ck.scale, p1.top, with_p=True))
+    ct = p1.ctx.encrypt(pt, ENC_SEED)
+    assert np.array_equal(ct.residues(), p1.ck.encrypt(ptr, p1.top, ENC_SEED))
+    assert np.abs(p1.ctx.decrypt(ct) - z).max() < 1e-8
+    # lower level + short slot vector (Engine::encode accepts any power of two)
+    pt2 = p1.ctx.encode(z[:256], level=2)
+    assert np.array_equal(pt2.residues(), p1.ck.encode(z[:256], p1.ck.scale, 2))
+
+
+def test_galois_keys_bit_exact(p1):
+    p1.ctx.gen_galois_keys([1, 33, -1])
+    for k in (1, 33, -1):
+        assert np.array_equal(p1.ctx.galois_key(k), p1.ck.galois_key(p1.ck.galois(k)))
+
+
+@pytest.mark.parametrize("k", [1, -1, 33, 4095, -4096, 0, 8192])
+def test_rotate_bit_exact(p1, k):
+    p1.ctx.gen_galois_keys([k])
+    z = rnd(p1.ctx.slots, 2)
+    ct = p1.ctx.encrypt(p1.ctx.encode(z), ENC_SEED)
+    ctr = p1.ck.encrypt(p1.ck.encode(z, p1.ck.scale, p1.top), p1.top, ENC_SEED)
+    r = p1.ctx.rotate(ct, k)
+    assert np.array_equal(r.residues(), p1.ck.rotate(ctr, p1.top, k))
+    assert np.abs(p1.ctx.decrypt(r) - np.roll(z, -k)).max() < TOL
+
+
+def test_rotate_hoisted_bit_exact(p1):
+    ks = [1, -1, 32, -32, 33, -33, 31, -31, 0]
+    p1.ctx.gen_galois_keys(ks)
+    z = rnd(p1.ctx.slots, 3)
+    ct = p1.ctx.encrypt(p1.ctx.encode(z), ENC_SEED)
+    ctr = p1.ck.encrypt(p1.ck.encode(z, p1.ck.scale, p1.top), p1.top, ENC_SEED)
+    outs = p1.ctx.rotate_hoisted(ct, ks)
+    ref = p1.ck.rotate_hoisted(ctr, p1.top, ks)
+    for i, k in enumerate(ks):
+        assert np.array_equal(outs[i].residues(), ref[i])
+        assert np.abs(p1.ctx.decrypt(outs[i]) - np.roll(z, -k)).max() < TOL
+
+
+def test_elementwise_and_rescale_bit_exact(p1):
+    a, b, w = rnd(p1.ctx.slots, 4), rnd(p1.ctx.slots, 5), rnd(p1.ctx.slots, 6)
+    L = p1.top
+    ca, cb = p1.ctx.encrypt(p1.ctx.encode(a), 11), p1.ctx.encrypt(p1.ctx.encode(b), 12)
+    ra = p1.ck.encrypt(p1.ck.encode(a, p1.ck.scale, L), L, 11)
+    rb = p1.ck.encrypt(p1.ck.encode(b, p1.ck.scale, L), L, 12)
+    assert np.array_equal(p1.ctx.add(ca, cb).residues(), p1.ck.add(ra, rb, L))
+    sub = p1.ctx.sub(ca, cb)
+    assert np.abs(p1.ctx.decrypt(sub) - (a - b)).max() < 1e-8
+    ql = float(p1.ctx.primes[L])
+    pw, rw = p1.ctx.encode(w, scale=ql), p1.ck.encode(w, ql, L)
+    m = p1.ctx.mul_plain(ca, pw)
+    rm = p1.ck.mul_plain(ra, rw, L)
+    assert np.array_equal(m.residues(), rm)
+    rs = p1.ctx.rescale(m)
+    assert rs.level == L - 1
+    assert np.array_equal(rs.residues(), p1.ck.rescale(rm, L))
+    assert np.abs(p1.ctx.decrypt(rs) - a * w).max() < 1e-7
+    ap = p1.ctx.add_plain(ca, p1.ctx.encode(b))
+    assert np.array_equal(ap.residues(), p1.ck.add_plain(ra, p1.ck.encode(b, p1.ck.scale, L), L))
+
+
+def conv_case(oracle, golden, name):
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    return c, m, k, co, img, filt
+
+
+@pytest.mark.parametrize("approach", [1, 2])
+def test_conv_cfg1_bit_exact_and_within_tolerance(oracle, golden, p1, approach):
+    c, m, k, co, img, filt = conv_case(oracle, golden, "cfg1")
+    layer = p1.ctx.conv_layer(c, co, m, k, filt)
+    p1.ctx.gen_galois_keys(layer.steps())
+    ct = p1.ctx.encrypt(p1.ctx.encode(img), ENC_SEED)
+    ctr = p1.ck.encrypt(p1.ck.encode(img, p1.ck.scale, p1.top), p1.top, ENC_SEED)
+    out = p1.ctx.conv2d(ct, layer, approach)
+    ref, sc = p1.ck.conv(ctr, p1.top, c, m, k, co, filt, approach)
+    assert out.level == p1.top - 1 and out.scale == sc
+    assert np.array_equal(out.residues(), ref)
+    err = np.abs(p1.ctx.decrypt(out) - golden["cfg1/slots"]).max()
+    assert err < TOL, err
+
+
+@pytest.mark.parametrize("approach", [1, 2])
+def test_conv_cfg3_bit_exact_and_within_tolerance(oracle, golden, approach):
+    p = pair(oracle, "cfg3")
+    c, m, k, co, img, filt = conv_case(oracle, golden, "cfg3")
+    layer = p.ctx.conv_layer(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    ct = p.ctx.encrypt(p.ctx.encode(img), ENC_SEED)
+    out = p.ctx.conv2d(ct, layer, approach)
+    err = np.abs(p.ctx.decrypt(out) - golden["cfg3/slots"]).max()
+    assert err < TOL, err
+    ctr = p.ck.encrypt(p.ck.encode(img, p.ck.scale, p.top), p.top, ENC_SEED)
+    assert np.array_equal(ct.residues(), ctr)
+    ref, _ = p.ck.conv(ctr, p.top, c, m, k, co, filt, approach)
+    assert np.array_equal(out.residues(), ref)
+
+
+@pytest.mark.slow
+def test_conv_cfg4_bit_exact_and_within_tolerance(oracle, golden):
+    p = pair(oracle, "cfg4")
+    c, m, k, co, img, filt = conv_case(oracle, golden, "cfg4")
+    layer = p.ctx.conv_layer(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    ct = p.ctx.encrypt(p.ctx.encode(img), ENC_SEED)
+    out = p.ctx.conv2d(ct, layer, 2)
+    err = np.abs(p.ctx.decrypt(out) - golden["cfg4/slots"]).max()
+    assert err < TOL, err
+    ctr = p.ck.encrypt(p.ck.encode(img, p.ck.scale, p.top), p.top, ENC_SEED)
+    ref, _ = p.ck.conv(ctr, p.top, c, m, k, co, filt, 2)
+    assert np.array_equal(out.residues(), ref)
+
+
+def test_conv_cfg5_three_layer_stack(oracle, golden):
+    """cfg5: three 3x3 16->16 layers, one rescale each (13 -> 12 -> 11 -> 10 primes)."""
+    p = pair(oracle, "cfg3")  # cfg5 shares cfg3's parameters
+    x, _ = oracle.make_inputs(16, 32, 3, 16, 1003, 0, 0)
+    ct = p.ctx.encrypt(p.ctx.encode(x), ENC_SEED + 1)
+    for li, sf in enumerate((2003, 2004, 2005)):
+        _, filt = oracle.make_inputs(16, 32, 3, 16, 0, sf, 1)
+        layer = p.ctx.conv_layer(16, 16, 32, 3, filt, level=ct.level)
+        p.ctx.gen_galois_keys(layer.steps())
+        ct = p.ctx.conv2d(ct, layer, 2)
+        assert ct.level == p.top - 1 - li
+        err = np.abs(p.ctx.decrypt(ct) - golden[f"cfg5/out{li}"]).max()
+        assert err < TOL, (li, err)
+
+
+@pytest.mark.parametrize("name", ["small_c4to2", "small_c4m4k1"])
+def test_conv_geometry_variants(oracle, golden, name):
+    """c_out < c_in and kappa = 1, packed into cfg1's 4096 slots."""
+    p = pair(oracle, "cfg1")
+    c, m, k, co, img, filt = conv_case(oracle, golden, name)
+    # embed a 4-channel 4x4 image into 4096 slots by duplication (pack, d = 256)
+    s = p.ctx.slots
+    slots = np.tile(img, s // img.size)
+    layer = p.ctx.conv_layer(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    ct = p.ctx.encrypt(p.ctx.encode(slots), ENC_SEED)
+    out = p.ctx.decrypt(p.ctx.conv2d(ct, layer, 2))
+    want = oracle.emu_conv_slots(c, m, k, co, s, img, filt, 2)
+    assert np.abs(out - want).max() < TOL
+    assert np.array_equal(want[: 64], golden[f"{name}/slots"])  # oracle == reference at s = 64
+
+
+def test_cfg2_decomposed_rotations(oracle, golden):
+    """cfg2: rotations by 1..127 through power-of-two keys only, positive vs
+    signed decomposition (reference rot.cpp:21-46, :131-156)."""
+    from paper_2306_09189_b200 import decompose
+    p = pair(oracle, "cfg2")
+    s = p.ctx.slots
+    pow2 = [1 << i for i in range(8)]
+    p.ctx.gen_galois_keys(pow2 + [-x for x in pow2])
+    z = rnd(s, 9)
+    ct = p.ctx.encrypt(p.ctx.encode(z), ENC_SEED)
+    for k in (1, 5, 63, 96, 127):
+        for strat in (0, 1):
+            out = p.ctx.rotate_decomposed(ct, k, strat)
+            assert np.abs(p.ctx.decrypt(out) - np.roll(z, -k)).max() < TOL
+    # residues of the signed path equal sequential golden-model rotations
+    ctr = p.ck.encrypt(p.ck.encode(z, p.ck.scale, p.top), p.top, ENC_SEED)
+    cur = ctr
+    for st in decompose(1, 127, s):
+        cur = p.ck.rotate(cur, p.top, st)
+    assert np.array_equal(p.ctx.rotate_decomposed(ct, 127, 1).residues(), cur)
+    keyed = {strat: sum(len(decompose(strat, n, s)) for n in range(1, 128)) for strat in (0, 1)}
+    assert keyed == {0: int(golden["plan_cfg2/strat0/total"][0]), 1: int(golden["plan_cfg2/strat1/total"][0])}
+
+
+def test_cfg2_hoisted_stencil(oracle):
+    p = pair(oracle, "cfg2")
+    stencil = [kk * 32 + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1)]
+    p.ctx.gen_galois_keys(stencil)
+    z = rnd(p.ctx.slots, 10)
+    ct = p.ctx.encrypt(p.ctx.encode(z), ENC_SEED)
+    ctr = p.ck.encrypt(p.ck.encode(z, p.ck.scale, p.top), p.top, ENC_SEED)
+    outs = p.ctx.rotate_hoisted(ct, stencil)
+    ref = p.ck.rotate_hoisted(ctr, p.top, stencil)
+    for i, k in enumerate(stencil):
+        assert np.array_equal(outs[i].residues(), ref[i])
+        assert np.abs(p.ctx.decrypt(outs[i]) - np.roll(z, -k)).max() < TOL

@@ -1,0 +1,121 @@
+"""Pins the oracle's C restatement (oracle/emu_ref.c, mt19937.c) against the
+reference's own outputs: the committed golden fixtures (generated from the
+compiled, unmodified reference by tests/golden/make_golden.py) and, where
+oracle/_ref was built, the live reference library."""
+import numpy as np
+import pytest
+
+CASES = ["cfg1", "cfg3", "cfg4", "small_c4m4k3", "small_c2m8k5", "small_c4m4k1", "small_c4to2",
+         "small_dup_c2m4k3"]
+
+
+def params(golden, name):
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden[f"{name}/params"])
+    return c, m, k, co, si, sf, wk, s
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_inputs_regenerate_bit_exact(oracle, golden, name):
+    c, m, k, co, si, sf, wk, s = params(golden, name)
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    ref_img = golden[f"{name}/img"]
+    assert np.array_equal(img[: ref_img.size], ref_img)
+    assert np.array_equal(np.array([img.sum(), np.abs(img).sum()]), golden[f"{name}/img_sum"])
+    assert np.array_equal(filt, golden[f"{name}/filt"])
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("plan", [0, 1, 2])
+def test_emulator_conv_bit_exact_vs_reference(oracle, golden, name, plan):
+    """conv_plan / convolve slots (reference conv.cpp:109-211) reproduced bit for bit."""
+    c, m, k, co, si, sf, wk, s = params(golden, name)
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    if s > c * m * m:  # pack() duplicates the channel sequence (pack.cpp:19-33)
+        img = np.tile(img, s // (c * m * m))
+    out = oracle.emu_conv_slots(c, m, k, co, s, img[: c * m * m], filt, plan)
+    assert np.array_equal(out, golden[f"{name}/slots"])
+
+
+@pytest.mark.parametrize("name", ["small_c4m4k3", "small_c2m8k5", "small_c4m4k1", "small_c4to2", "cfg1"])
+def test_textbook_conv_matches_reference_oracle(oracle, golden, name):
+    c, m, k, co, si, sf, wk, s = params(golden, name)
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    out = oracle.emu_oracle_conv(c, m, k, co, img, filt)
+    assert np.array_equal(out, golden[f"{name}/oracle_conv"])
+    # and the slot schedule agrees with the textbook conv (reference test_conv.cpp:86)
+    image = golden.get(f"{name}/image", golden[f"{name}/slots"][: co * m * m])
+    assert np.abs(image - out).max() < 1e-12
+
+
+def test_cfg5_stack_bit_exact(oracle, golden):
+    x, _ = oracle.make_inputs(16, 32, 3, 16, 1003, 0, 0)
+    assert np.array_equal(np.array([x.sum(), np.abs(x).sum()]), golden["cfg5/img_sum"])
+    for li, sf in enumerate((2003, 2004, 2005)):
+        _, filt = oracle.make_inputs(16, 32, 3, 16, 0, sf, 1)
+        assert np.array_equal(filt, golden[f"cfg5/filt{li}"])
+        x = oracle.emu_conv_slots(16, 32, 3, 16, 16384, x, filt, 2)
+        assert np.array_equal(x, golden[f"cfg5/out{li}"])
+
+
+def test_rotation_kats(oracle):
+    """reference test_emu.cpp:13-26"""
+    v = np.array([1.0, 2, 3, 4])
+    out = np.zeros(4)
+    for k, want in [(1, [2, 3, 4, 1]), (-1, [4, 1, 2, 3]), (5, [2, 3, 4, 1]), (0, [1, 2, 3, 4])]:
+        oracle.lib().emu_rotate(v.ctypes.data_as(oracle.dp), out.ctypes.data_as(oracle.dp), 4, k)
+        assert out.tolist() == want
+
+
+def test_single_channel_kats(oracle):
+    """reference test_conv.cpp:60-79 (identity, x2 scale, all-ones -> {10,10,10,10})"""
+    ch = np.array([1.0, 2, 3, 4])
+    assert oracle.emu_conv_slots(1, 2, 1, 1, 4, ch, np.array([2.0]), 0).tolist() == [2, 4, 6, 8]
+    ident = np.zeros(9)
+    ident[4] = 1.0
+    assert oracle.emu_conv_slots(1, 2, 3, 1, 4, ch, ident, 0).tolist() == [1, 2, 3, 4]
+    assert oracle.emu_conv_slots(1, 2, 3, 1, 4, ch, np.ones(9), 0).tolist() == [10, 10, 10, 10]
+
+
+@pytest.mark.parametrize("s", [4096, 8192])
+def test_decompositions_vs_reference(oracle, golden, s):
+    lens, sums, first = golden[f"decomp{s}/lens"], golden[f"decomp{s}/sums"], golden[f"decomp{s}/steps_lt1024"]
+    for strat in (0, 1):
+        for n in range(s):
+            st = oracle.emu_decompose(strat, n, s)
+            assert len(st) == lens[strat, n] and sum(st) == sums[strat, n]
+            if n < 1024:
+                assert st == [int(x) for x in first[strat, n, : len(st)]]
+
+
+def test_decomposition_kats(oracle):
+    """reference test_rot.cpp:12-29"""
+    assert oracle.emu_decompose(0, 127, 4096) == [64, 32, 16, 8, 4, 2, 1]
+    assert oracle.emu_decompose(1, 127, 4096) == [128, -1]
+    assert oracle.emu_decompose(1, 96, 4096) == [64, 32]
+    assert oracle.emu_decompose(1, 5, 4096) == [4, 1]
+    assert oracle.emu_decompose(1, 0, 4096) == []
+
+
+def test_min_lengths_vs_reference(oracle, golden):
+    ml = oracle.emu_min_lengths(4095, 4096)
+    assert np.array_equal(ml.astype(np.int8), golden["minlen4096"])
+    # greedy signed is BFS-minimal for every n < 4096 (acceptance.cpp:245-259)
+    for n in range(4096):
+        assert len(oracle.emu_decompose(1, n, 4096)) == ml[n]
+
+
+def test_planner_counts_vs_reference(golden):
+    # survey-reported values of the reference planner
+    assert int(golden["plan_cfg2/strat0/total"][0]) == 448
+    assert int(golden["plan_cfg2/strat1/total"][0]) == 355
+    assert [int(golden[f"plan_stencil/strat{s}/total"][0]) for s in (0, 1, 2)] == [51, 16, 8]
+
+
+def test_live_reference_if_built(oracle, golden):
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built here (no /root/reference)")
+    c, m, k, co, si, sf, wk, s = params(golden, "cfg1")
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk, use_ref=True)
+    slots, _, ledger, drop = oracle.ref_conv(c, m, k, co, img, filt, 2, s)
+    assert np.array_equal(slots, golden["cfg1/slots"])
+    assert np.array_equal(ledger, golden["cfg1/ledger2"]) and drop == 1
