@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark of the encrypted-convolution hot path (BASELINE.json metric:
+homomorphic convs/sec and hoisted rotations/sec at N=2^15; % HBM roofline).
+
+Headline workload (config.workload): BASELINE cfg3 — CKKS N=2^15, primes
+60 + 12x50 | 2x60 special, Delta = 2^50; image 32x32x16 packed into 16384
+slots; 3x3 16->16 same-padding conv, paper Approach 2 (channel rotations
+first, shifts hoisted), one rescale. One step = one ciphertext through the
+whole conv layer. Inputs are seeded synthetic data with the BASELINE shapes
+and distributions (uniform [-1,1] image and weights); keys and plaintexts
+are resident in HBM and the key stream (23 keys x 55 MB = 1.27 GB per conv)
+is larger than L2, so no L2 flush is needed between steps.
+
+Arms
+  default            libfheconv on the GPU (N replicas under torchrun; no
+                     data-path collective — the path does not shard).
+  --impl reference   the reference's own CPU implementation (conv_plan on the
+                     shardnn emulator, compiled unmodified into oracle/_ref)
+                     on all host cores; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = "cfg3"
+C_IN = C_OUT = 16
+M = 32
+KAPPA = 3
+WORKLOAD = ("cfg3: CKKS N=2^15 (16384 slots), 60+12x50-bit q | 2x60-bit p, scale 2^50, dnum 7; image 32x32x16 "
+            "U[-1,1]; 3x3 conv 16->16 same padding, weights U[-1,1]; Approach 2 (hoisted shifts) + 1 rescale; "
+            "1 ciphertext per step")
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel_class):
+    """dram bytes per launch from the committed ncu --set full capture (profiles/)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(kernel_class)
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------- byte model
+def byte_model(ctx, level, approach):
+    """Algorithmic (compulsory) HBM bytes per launch, SURVEY.md §8(d)."""
+    N, L, K, dnum = ctx.N, ctx.L, ctx.K, ctx.dnum
+    key = 2 * dnum * (L + K) * N * 8
+    ct = 2 * (level + 1) * N * 8
+    pt_qp = (level + 1 + K) * N * 8
+    n_shift = KAPPA * KAPPA - 1
+    if approach == 2:  # one launch per channel-rotated source: 8 shift keys + 9 plaintexts + the source
+        mac = n_shift * key + KAPPA * KAPPA * pt_qp + ct
+    else:  # one launch per shifted source: 15 channel keys + 16 plaintexts + the source
+        mac = (C_IN - 1) * key + C_IN * pt_qp + ct
+    conv = ct + 2 * level * N * 8 + (C_IN - 1 + n_shift) * key + C_IN * KAPPA * KAPPA * pt_qp
+    return {"key": key, "ct": ct, "pt": pt_qp, "conv_mac": mac, "conv": conv}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2306_09189_b200 import Context
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    ctx = Context.from_config(CFG, device=local_rank)
+    ctx.keygen(7)
+    rng = np.random.default_rng(1234 + rank)
+    img = rng.uniform(-1, 1, C_IN * M * M)
+    w = rng.uniform(-1, 1, C_IN * C_OUT * KAPPA * KAPPA)
+    layer = ctx.conv_layer(C_IN, C_OUT, M, KAPPA, w)
+    ctx.gen_galois_keys(layer.steps())
+    ct = ctx.encrypt(ctx.encode(img), 9000 + rank)
+    out = ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1)
+    level = ctx.max_level
+    approach = args.approach
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # correctness gate before timing: decrypted output vs numpy conv
+    ctx.conv2d_into(ct, layer, approach, out)
+    x = img.reshape(C_IN, M, M)
+    wt = w.reshape(C_IN, C_OUT, KAPPA, KAPPA)
+    xp = np.pad(x, ((0, 0), (1, 1), (1, 1)))
+    ref = np.zeros((C_OUT, M, M))
+    for a in range(3):
+        for b in range(3):
+            ref += np.einsum("fg,fij->gij", wt[:, :, a, b], xp[:, a:a + M, b:b + M])
+    err = float(np.abs(ctx.decrypt(out)[: C_OUT * M * M] - ref.ravel()).max())
+
+    for _ in range(args.warmup):
+        ctx.conv2d_into(ct, layer, approach, out)
+    ctx.synchronize()
+    ctx.prof_reset()
+    ctx.prof_enable(True)
+    launches0 = ctx.ledger()["kernel_launches"]
+    barrier()
+    ctx.synchronize()
+    with ClockSampler(local_rank) as clk:
+        ctx.timer_start()
+        for _ in range(args.steps):
+            ctx.conv2d_into(ct, layer, approach, out)
+        ms = ctx.timer_stop()  # synchronises the stream
+    barrier()
+    ctx.prof_enable(False)
+    launches = ctx.ledger()["kernel_launches"] - launches0
+    classes = ["conv_mac", "ntt", "ks_inner", "modup_bconv", "moddown", "rescale"]
+    prof = {c: ctx.prof_get(c) for c in classes}
+    ms_max = max_over_ranks(ms)
+
+    # secondary metrics (device-timed, same context): the other approach and
+    # the hoisted 3x3 stencil group at N = 2^15 (8 non-identity rotations)
+    other = 1 if approach == 2 else 2
+    for _ in range(2):
+        ctx.conv2d_into(ct, layer, other, out)
+    ctx.timer_start()
+    k2 = max(2, args.steps // 2)
+    for _ in range(k2):
+        ctx.conv2d_into(ct, layer, other, out)
+    ms_other = max_over_ranks(ctx.timer_stop())
+    stencil = [kk * M + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1)]
+    for _ in range(2):
+        ctx.rotate_hoisted(ct, stencil)
+    ctx.synchronize()
+    ctx.timer_start()
+    kh = max(3, args.steps)
+    for _ in range(kh):
+        outs = ctx.rotate_hoisted(ct, stencil)
+    ms_hoist = max_over_ranks(ctx.timer_stop())
+    del outs
+
+    # e2e: the C ABI with host buffers, H2D + conv + D2H inside the timed region
+    N = ctx.N
+    h_in = torch.empty(2 * (level + 1) * N, dtype=torch.int64, pin_memory=True)
+    h_out = torch.empty(2 * level * N, dtype=torch.int64, pin_memory=True)
+    h_in.numpy().view(np.uint64)[:] = ct.residues().ravel()
+    import ctypes as C
+    from paper_2306_09189_b200 import _lib
+    from paper_2306_09189_b200.engine import lib
+    L_ = lib()
+    pin_in = C.cast(h_in.data_ptr(), _lib.u64p)
+    pin_out = C.cast(h_out.data_ptr(), _lib.u64p)
+    ct_dev = ctx.upload(ct.residues(), level)
+    for _ in range(2):
+        L_.fhe_ct_upload_into(ctx.h, pin_in, ct_dev.h)
+        ctx.conv2d_into(ct_dev, layer, approach, out)
+        L_.fhe_ct_download(ctx.h, out.h, pin_out, h_out.numel())
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        assert L_.fhe_ct_upload_into(ctx.h, pin_in, ct_dev.h) == 0
+        ctx.conv2d_into(ct_dev, layer, approach, out)
+        assert L_.fhe_ct_download(ctx.h, out.h, pin_out, h_out.numel()) == 0  # synchronises
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_err = float(np.abs(ctx.decrypt(out)[: C_OUT * M * M] - ref.ravel()).max())
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return None
+
+    bm = byte_model(ctx, level, approach)
+    step_s = ms_max / 1e3 / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+    # dominant kernel class by device time inside the timed region
+    dom = max(prof, key=lambda c: prof[c][0])
+    dom_ms, dom_n = prof[dom]
+    peak, peak_kind = measured_peak()
+    if dom == "conv_mac":
+        alg = bm["conv_mac"]
+        note = ("conv_mac: fused key-switch inner product + plaintext MAC + channel sum for one source; "
+                f"algorithmic bytes/launch = {KAPPA * KAPPA - 1 if approach == 2 else C_IN - 1} keys x "
+                f"{bm['key'] / 1e6:.2f} MB + plaintexts + source ciphertext")
+    else:
+        alg = None
+        note = f"dominant class {dom}"
+    avg_s = dom_ms / 1e3 / max(dom_n, 1)
+    achieved = alg / avg_s / 1e9 if alg else None
+    cpu = cpu_baseline(args) if not args.no_cpu else None
+    line = {
+        "metric": "homomorphic convs/sec at N=2^15 (cfg3, Approach 2)",
+        "value": round(value, 3),
+        "unit": "conv/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_s * 1e3, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64 (RNS residues mod 40-60-bit primes)",
+        "data": "synthetic (seeded U[-1,1] image/weights, BASELINE cfg3 shapes); no dataset involved",
+        "config": {"workload": WORKLOAD, "approach": approach, "batch_per_gpu": 1, "parallelism": f"replicas x{world}",
+                   "l2": "no flush: per-step key stream (1.27 GB) >> 126 MB L2", "key_seed": 7,
+                   "enc_seed": 9000, "decrypt_max_abs_err": err},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1) if achieved else None,
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
+                     "traffic": ncu_traffic(dom), "algorithmic_bytes_per_launch": alg,
+                     "avg_launch_ms": round(avg_s * 1e3, 4), "launches": dom_n, "peak_kind": peak_kind,
+                     "note": note},
+        "conv_roofline": {"algorithmic_bytes_per_conv": bm["conv"],
+                          "achieved_gbs": round(bm["conv"] / step_s / 1e9, 1),
+                          "frac": round(bm["conv"] / step_s / 1e9 / peak, 4)},
+        "kernel_ms_per_step": {c: round(prof[c][0] / args.steps, 4) for c in classes},
+        "approach1_conv_per_s" if approach == 2 else "approach2_conv_per_s":
+            round(world * k2 / (ms_other / 1e3), 3),
+        "hoisted_rot_per_s": round(world * kh * 8 / (ms_hoist / 1e3), 1),
+        "e2e": {"value": round(world * args.steps / e2e_s, 3), "unit": "conv/s",
+                "h2d_bytes_per_step": int(h_in.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
+                "api": "fhe_ct_upload_into + fhe_conv2d_into + fhe_ct_download (C ABI, pinned host buffers)",
+                "decrypt_max_abs_err": e2e_err},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return line
+
+
+# ------------------------------------------------------------ CPU baselines
+def _ref_inputs():
+    import pyoracle as po
+    img, filt = po.make_inputs(C_IN, M, KAPPA, C_OUT, 1001, 2001, 0)
+    return po, img, filt
+
+
+def cpu_baseline(args, seconds=10.0):
+    """The reference's own CPU path (conv_plan ShiftFirst on the shardnn
+    emulator, compiled unmodified) on all host cores, bounded to ~10 s."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        po, img, filt = _ref_inputs()
+        if not po.ref_available():
+            return {"unavailable": "oracle/_ref/libshardnn_ref.so not built"}
+        R = po.ref()
+        threads = os.cpu_count() or 1
+        dp = po.dp
+        ip, fp = img.ctypes.data_as(dp), filt.ctypes.data_as(dp)
+        t1 = R.ref_time_conv(C_IN, M, KAPPA, C_OUT, ip, fp, 2, C_IN * M * M, 1, 1)
+        iters = max(1, int(seconds / max(t1, 1e-4)))
+        dt = R.ref_time_conv(C_IN, M, KAPPA, C_OUT, ip, fp, 2, C_IN * M * M, iters, threads)
+        out = {"value": round(iters * threads / dt, 2), "unit": "conv/s", "cores": threads, "kind": "reference",
+               "sample": f"{iters * threads} conv_plan(ShiftFirst) runs at cfg3 geometry on {threads} independent "
+                         f"shardnn Engines ({dt:.1f} s); reference emulator, no cryptography",
+               "single_thread_conv_per_s": round(1.0 / t1, 2)}
+        if not args.no_golden:
+            out["golden_ckks"] = golden_ckks_baseline()
+        return out
+    except Exception as e:  # the baseline must never hide the GPU line
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
+def golden_ckks_baseline():
+    """This repo's CPU CKKS golden model (OpenMP, all cores): one cfg3 conv."""
+    po, img, filt = _ref_inputs()
+    ck = po.CKKS(15, [60] + [50] * 12, [60, 60], 50)
+    ck.keygen(7)
+    ct = ck.encrypt(ck.encode(img, ck.scale, 12), 12, 9000)
+    t = time.perf_counter()
+    ck.conv(ct, 12, C_IN, M, KAPPA, C_OUT, filt, 2)
+    dt = time.perf_counter() - t
+    return {"value": round(1.0 / dt, 4), "unit": "conv/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": "1 cfg3 Approach-2 conv incl. on-demand Galois keygen (23 keys), CPU RNS-CKKS golden model"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        po, img, filt = _ref_inputs()
+        if not po.ref_available():
+            raise RuntimeError("oracle/_ref/libshardnn_ref.so not built")
+        R = po.ref()
+    except Exception as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}), flush=True)
+        return None
+    threads = os.cpu_count() or 1
+    dp = po.dp
+    ip, fp = img.ctypes.data_as(dp), filt.ctypes.data_as(dp)
+    t1 = R.ref_time_conv(C_IN, M, KAPPA, C_OUT, ip, fp, 2, C_IN * M * M, 1, 1)
+    per_step = max(1, int(2.0 / max(t1, 1e-4)))  # ~2 s of work per thread per step
+    for _ in range(args.warmup):
+        R.ref_time_conv(C_IN, M, KAPPA, C_OUT, ip, fp, 2, C_IN * M * M, 1, threads)
+    total = 0.0
+    for _ in range(args.steps):
+        total += R.ref_time_conv(C_IN, M, KAPPA, C_OUT, ip, fp, 2, C_IN * M * M, per_step, threads)
+    n = args.steps * per_step * threads
+    value = n / total
+    line = {
+        "impl": "reference",
+        "metric": "homomorphic convs/sec at N=2^15 (cfg3, Approach 2)",
+        "value": round(value, 3), "unit": "conv/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (emulated slots)",
+        "data": "synthetic (reference test helpers: mt19937_64 U[-1,1], seeds 1001/2001)",
+        "config": {"workload": WORKLOAD, "approach": 2, "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "conv/s", "cores": threads, "kind": "reference",
+                         "sample": f"{per_step} conv_plan(ShiftFirst) per thread per step on {threads} threads; "
+                                   "shardnn emulator (no cryptography) compiled unmodified"},
+        "e2e": {"value": round(value, 3), "unit": "conv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--approach", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-golden", action="store_true", help="skip the golden-model CKKS CPU timing")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

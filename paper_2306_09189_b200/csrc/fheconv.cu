@@ -56,6 +56,7 @@ struct fhe_ctx {
     uint64_t key_seed = 0;
     std::map<uint32_t, uint64_t*> keys;
     fhe_ledger ledger{};
+    uint64_t launch_base = 0;
     std::set<uint64_t> amounts;
     std::string err;
     // pinned staging
@@ -148,7 +149,6 @@ struct fhe_ctx {
         if (it == keys.end()) fail(FHE_E_NOKEY, "missing Galois key for rotation");
         return it->second;
     }
-    void launched(int n = 1) { ledger.kernel_launches += n; }
 };
 
 struct fhe_ct {
@@ -219,7 +219,6 @@ void modup(fhe_ctx* c, const uint64_t* c1, int level, uint64_t* digits) {
     c->timed("ntt", [&] { ntt_forward(c->dc, digits, dn * ne, RowMap{ne, level, c->L, c->alpha}, c->st); });
     c->release(coef);
     c->ledger.modups++;
-    c->launched(6);
 }
 
 // out[p] = ModDown(acc[p]) (+ sigma_g(add_src) on poly 0)
@@ -237,7 +236,6 @@ void moddown(fhe_ctx* c, const uint64_t* acc, int level, int npoly, uint64_t* ou
     c->release(pc);
     c->release(conv);
     c->ledger.moddowns += npoly;
-    c->launched(7);
 }
 
 // out = rotation of ct by Galois g given the ModUp digits of ct.c1
@@ -251,7 +249,6 @@ void rotate_from_digits(fhe_ctx* c, const fhe_ct* ct, const uint64_t* digits, ui
     moddown(c, acc, level, 2, out, ct->c0(), g);
     c->release(acc);
     c->ledger.key_switches++;
-    c->launched();
 }
 
 void rescale_into(fhe_ctx* c, const uint64_t* in, int level, uint64_t* out) {
@@ -271,7 +268,6 @@ void rescale_into(fhe_ctx* c, const uint64_t* in, int level, uint64_t* out) {
     c->release(tmp);
     c->release(spread);
     c->ledger.rescales++;
-    c->launched(6);
 }
 
 void gen_key(fhe_ctx* c, uint32_t g) {
@@ -543,7 +539,6 @@ void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
         c->timed("conv_mac", [&] { conv_mac(c->dc, acc, dtmp, src.d, t, c->d_md, level, dn, c->st); });
         for (int i = 0; i < t.n; ++i)
             if (t.galois[i] != 1) c->ledger.key_switches++;
-        c->launched();
         t.n = 0;
     };
     auto push = [&](MacTerms& t, const fhe_ct& src, uint32_t g, const uint64_t* pt) {
@@ -741,6 +736,7 @@ int fhe_prof_reset(fhe_ctx* c) {
 int fhe_ledger_get(const fhe_ctx* c, fhe_ledger* out) {
     if (!c || !out) return FHE_E_INVALID;
     *out = c->ledger;
+    out->kernel_launches = launches_total() - c->launch_base;
     out->distinct_amounts = c->amounts.size();
     return FHE_OK;
 }
@@ -748,6 +744,7 @@ int fhe_ledger_reset(fhe_ctx* c) {
     if (!c) return FHE_E_INVALID;
     c->ledger = fhe_ledger{};
     c->amounts.clear();
+    c->launch_base = launches_total();
     return FHE_OK;
 }
 int fhe_ledger_amounts(const fhe_ctx* c, uint64_t* out, size_t cap, size_t* n) {

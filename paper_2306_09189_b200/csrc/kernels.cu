@@ -12,6 +12,8 @@ namespace fhe {
 
 namespace {
 
+uint64_t g_launches = 0;  // every kernel this library enqueues (host-side count)
+
 constexpr int kEwThreads = 256;
 
 inline int ew_blocks(size_t n) {
@@ -185,13 +187,17 @@ constexpr int kCols = 16;
 template <int LOG_N1, int LOG_B>
 void ntt_fwd_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st) {
     const int N1 = 1 << LOG_N1, B = 1 << LOG_B;
+    ++g_launches;
     k_ntt_fwd_a<LOG_N1, kCols><<<dim3(B / kCols, nrows), 256, 0, st>>>(c, data, rm);
+    ++g_launches;
     k_ntt_fwd_b<LOG_B><<<dim3(N1, nrows), 128, 0, st>>>(c, data, rm);
 }
 template <int LOG_N1, int LOG_B>
 void ntt_inv_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st) {
     const int N1 = 1 << LOG_N1, B = 1 << LOG_B;
+    ++g_launches;
     k_ntt_inv_b<LOG_B><<<dim3(N1, nrows), 128, 0, st>>>(c, data, rm);
+    ++g_launches;
     k_ntt_inv_a<LOG_N1, kCols><<<dim3(B / kCols, nrows), 256, 0, st>>>(c, data, rm);
 }
 
@@ -303,30 +309,37 @@ __global__ void k_decrypt_combine(DevCtx c, uint64_t* m, const uint64_t* c0, con
 
 void reduce_signed_rows(const DevCtx& c, const int64_t* coef, uint64_t* out, int nrows, const RowMap& rm,
                         cudaStream_t st) {
+    ++g_launches;
     k_reduce_signed_rows<<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, coef, out, nrows, rm);
 }
 void sample_uniform_rows(const DevCtx& c, uint64_t* out, int nrows, const RowMap& rm, uint64_t key,
                          cudaStream_t st) {
+    ++g_launches;
     k_sample_uniform<<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, out, nrows, rm, key);
 }
 void sample_gauss(const DevCtx& c, int64_t* out, uint64_t key, cudaStream_t st) {
+    ++g_launches;
     k_sample_gauss<<<ew_blocks(c.N), kEwThreads, 0, st>>>(c, out, key);
 }
 void sample_ternary(const DevCtx& c, int64_t* out, uint64_t key, cudaStream_t st) {
+    ++g_launches;
     k_sample_ternary<<<ew_blocks(c.N), kEwThreads, 0, st>>>(c, out, key);
 }
 void keygen_combine(const DevCtx& c, uint64_t* key_b, const uint64_t* key_a, const uint64_t* e,
                     const uint64_t* s, uint32_t galois, int lo, int hi, const ModDownTable* md, int nrows,
                     cudaStream_t st) {
+    ++g_launches;
     k_keygen_combine<<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, key_b, key_a, e, s, galois, lo,
                                                                               hi, md, nrows);
 }
 void encrypt_combine(const DevCtx& c, uint64_t* c0, const uint64_t* c1, const uint64_t* e,
                      const uint64_t* s, const uint64_t* pt, int nrows, cudaStream_t st) {
+    ++g_launches;
     k_encrypt_combine<<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, c0, c1, e, s, pt, nrows);
 }
 void decrypt_combine(const DevCtx& c, uint64_t* m, const uint64_t* c0, const uint64_t* c1,
                      const uint64_t* s, int nrows, cudaStream_t st) {
+    ++g_launches;
     k_decrypt_combine<<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, m, c0, c1, s, nrows);
 }
 
@@ -392,24 +405,30 @@ __global__ void k_rescale_finish(DevCtx c, uint64_t* out, const uint64_t* in, co
 
 void ew_add(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b, int nrows, int rpp,
             cudaStream_t st) {
+    ++g_launches;
     k_ew<0><<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, out, a, b, nrows, rpp);
 }
 void ew_sub(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b, int nrows, int rpp,
             cudaStream_t st) {
+    ++g_launches;
     k_ew<1><<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, out, a, b, nrows, rpp);
 }
 void ew_mul_bcast(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b, int nrows, int rpp,
                   cudaStream_t st) {
+    ++g_launches;
     k_ew<2><<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, out, a, b, nrows, rpp);
 }
 void automorph(const DevCtx& c, uint64_t* out, const uint64_t* in, int nrows, uint32_t galois, cudaStream_t st) {
+    ++g_launches;
     k_automorph<<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, out, in, nrows, galois);
 }
 void rescale_spread(const DevCtx& c, const uint64_t* tmp, uint64_t* spread, int level, cudaStream_t st) {
+    ++g_launches;
     k_rescale_spread<<<ew_blocks((size_t)2 * level * c.N), kEwThreads, 0, st>>>(c, tmp, spread, level);
 }
 void rescale_finish(const DevCtx& c, uint64_t* out, const uint64_t* in, const uint64_t* spread, int level,
                     const uint64_t* qlinv, const uint64_t* qlinv_sh, cudaStream_t st) {
+    ++g_launches;
     k_rescale_finish<<<ew_blocks((size_t)2 * level * c.N), kEwThreads, 0, st>>>(c, out, in, spread, level, qlinv,
                                                                                  qlinv_sh);
 }
@@ -589,30 +608,38 @@ __global__ void __launch_bounds__(256) k_conv_mac(DevCtx c, uint64_t* acc, const
 
 void modup_bconv(const DevCtx& c, const uint64_t* coef, const uint64_t* c1_ntt, uint64_t* digits,
                  const ModUpDigit* tables, int level, int dn, cudaStream_t st) {
+    ++g_launches;
     k_modup_bconv<<<ew_blocks((size_t)dn * c.N), kEwThreads, 0, st>>>(c, coef, c1_ntt, digits, tables, level, dn);
 }
 void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* key, uint64_t* acc0,
                       uint64_t* acc1, uint32_t galois, int level, int dn, cudaStream_t st) {
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
+    ++g_launches;
     k_ks_inner<<<ew_blocks(total), kEwThreads, 0, st>>>(c, digits, key, acc0, acc1, galois, level, dn);
 }
 void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, int level, int npoly, cudaStream_t st) {
+    ++g_launches;
     k_gather_special<<<ew_blocks((size_t)npoly * c.K * c.N), kEwThreads, 0, st>>>(c, dst, acc, level, npoly);
 }
 void moddown_bconv(const DevCtx& c, const uint64_t* pcoef, uint64_t* conv, const ModDownTable* md, int level,
                    int npoly, cudaStream_t st) {
+    ++g_launches;
     k_moddown_bconv<<<ew_blocks((size_t)npoly * c.N), kEwThreads, 0, st>>>(c, pcoef, conv, md, level, npoly);
 }
 void moddown_finish(const DevCtx& c, uint64_t* out, const uint64_t* acc, const uint64_t* conv,
                     const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
                     cudaStream_t st) {
+    ++g_launches;
     k_moddown_finish<<<ew_blocks((size_t)npoly * (level + 1) * c.N), kEwThreads, 0, st>>>(
         c, out, acc, conv, md, level, npoly, add_src, galois);
 }
 void conv_mac(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* x, const MacTerms& t,
               const ModDownTable* md, int level, int dn, cudaStream_t st) {
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
+    ++g_launches;
     k_conv_mac<<<ew_blocks(total), 256, 0, st>>>(c, acc, digits, x, t, md, level, dn);
 }
+
+uint64_t launches_total() { return g_launches; }
 
 }  // namespace fhe

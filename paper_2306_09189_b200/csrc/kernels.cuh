@@ -74,6 +74,9 @@ struct MacTerms {
 };
 
 // --------------------------------------------------------------- launchers
+// total number of kernels enqueued by this library (for the bench's gpu_launches)
+uint64_t launches_total();
+
 // All launchers enqueue on `st` and never synchronise.
 void ntt_forward(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);
 void ntt_inverse(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);
