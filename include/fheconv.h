@@ -89,6 +89,8 @@ int fhe_timer_stop(fhe_ctx* ctx, float* ms); /* synchronises; ms since fhe_timer
 int fhe_prof_enable(fhe_ctx* ctx, int on);
 int fhe_prof_get(fhe_ctx* ctx, const char* kernel_class, double* total_ms, uint64_t* launches);
 int fhe_prof_reset(fhe_ctx* ctx);
+/* cudaProfilerStart/Stop (scopes ncu --profile-from-start off captures) */
+int fhe_profiler_range(int on);
 /* replaces: Engine::ledger() emu.hpp:137-138, CostLedger::reset emu.hpp:77-88 */
 int fhe_ledger_get(const fhe_ctx* ctx, fhe_ledger* out);
 int fhe_ledger_reset(fhe_ctx* ctx);
@@ -164,7 +166,14 @@ int fhe_conv_layer_steps(const fhe_conv_layer* layer, int approach, int64_t* ste
 /* replaces: conv_plan(eng, p, k, plan) conv.cpp:266-271.
  * approach 1 = paper Approach 1 (ConvPlan::ChannelFirst: shifts first),
  * approach 2 = paper Approach 2 (ConvPlan::ShiftFirst: channel rotations first,
- * shifts hoisted). Output: one ciphertext at level - 1 (one rescale). */
+ *              shifts hoisted),
+ * approach 3 = baby-step/giant-step: channel rotations hoisted from one
+ *              decomposition, shifts applied once to aggregated sums
+ *              (rotated plaintexts),
+ * approach 4 = baby-step/giant-step with the roles swapped (shifts hoisted),
+ * approach 0 = 3 or 4, whichever needs fewer decompositions.
+ * All approaches decrypt to the same slots (within CKKS noise).
+ * Output: one ciphertext at level - 1 (one rescale). */
 int fhe_conv2d(fhe_ctx* ctx, const fhe_ct* ct, const fhe_conv_layer* layer, int approach, fhe_ct** out);
 /* same, writing into a preallocated output ciphertext of level - 1 */
 int fhe_conv2d_into(fhe_ctx* ctx, const fhe_ct* ct, const fhe_conv_layer* layer, int approach, fhe_ct* out);

@@ -913,10 +913,139 @@ static void conv_accumulate(const ck_ctx* ck, int level, const uint64_t* pt, con
     free(perm_c0);
 }
 
+/* Baby-step / giant-step conv with output aggregation.
+ * orient 3: baby steps = channel rotations r m^2 (hoisted from one ModUp of
+ *           the input), giant steps = shifts kk m + ll;
+ * orient 4: baby steps = shifts, giant steps = channel rotations.
+ * With X_b = rot_b(ct) kept in the QP basis (never ModDown'd),
+ *   Y_g = sum_b rot_{-g}(pt_{g,b}) * X_b                      (QP accumulators)
+ *   out = Rescale(ModDown(Y_0 + sum_{g != 0} KS_g(ModDown(Y_g))))
+ * where KS_g(Y) = IP(ModUp(Y.c1), key_g) + P sigma_g(Y.c0) (QP). */
+static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,
+                     const double* filt, int orient, uint64_t* out, double* out_scale) {
+    const size_t N = ck->N, s = N / 2, block = (size_t)m * m;
+    const int nr = level + 1, ne = nr + ck->K, dn = ck_dnum_at(ck, level);
+    const long h = kappa / 2;
+    const int nk = (int)((2 * h + 1) * (2 * h + 1));
+    const size_t extw = (size_t)ne * N, ctw = (size_t)2 * nr * N;
+    const uint64_t ql = ck->q[level];
+    const double pscale = (double)ql;
+    const int nb = orient == 3 ? c : nk, ngi = orient == 3 ? nk : c;
+    long* bamt = malloc((size_t)nb * sizeof(long));
+    long* gamt = malloc((size_t)ngi * sizeof(long));
+    for (int r = 0; r < c; r++) (orient == 3 ? bamt : gamt)[r] = (long)r * (long)block;
+    {
+        int i = 0;
+        for (long kk = -h; kk <= h; kk++)
+            for (long ll = -h; ll <= h; ll++, i++) (orient == 3 ? gamt : bamt)[i] = kk * m + ll;
+    }
+    uint64_t Pmod[CK_MAXP];
+    for (int u = 0; u < ne; u++) {
+        const uint64_t q = ck->q[ext_prime(ck, level, u)];
+        uint64_t P = 1;
+        for (int k = 0; k < ck->K; k++) P = ck_mulmod(P, ck->q[ck->L + k] % q, q);
+        Pmod[u] = u < nr ? P : 0;
+    }
+    /* rotated plaintexts pt'[g][b] = rot_{-g}(fused_plain(r, i)) */
+    uint64_t* pts = malloc((size_t)ngi * nb * extw * 8);
+    int* nonempty = calloc((size_t)ngi * nb, sizeof(int));
+    double* plain = malloc(s * sizeof(double));
+    double* rplain = malloc(s * sizeof(double));
+    for (int gi = 0; gi < ngi; gi++)
+        for (int bi = 0; bi < nb; bi++) {
+            const int r = orient == 3 ? bi : gi, i = orient == 3 ? gi : bi;
+            const long kk = i / (2 * h + 1) - h, ll = i % (2 * h + 1) - h;
+            if (!emu_fused_plain(c, m, kappa, c_out, s, filt, r, kk, ll, 1.0, plain)) continue;
+            nonempty[gi * nb + bi] = 1;
+            emu_rotate(plain, rplain, s, -gamt[gi]);
+            ck_encode_plain(ck, rplain, s, pscale, level, 1, pts + ((size_t)gi * nb + bi) * extw);
+        }
+    free(plain);
+    free(rplain);
+    key_cache kc = {.n = 0};
+    uint64_t* dsrc = malloc((size_t)dn * extw * 8);
+    uint64_t* ip0 = malloc(extw * 8);
+    uint64_t* ip1 = malloc(extw * 8);
+    uint64_t* Y = calloc((size_t)ngi * 2 * extw, 8); /* [g][2][ne][N] */
+    ck_modup(ck, ct + (size_t)nr * N, level, dsrc);
+    for (int bi = 0; bi < nb; bi++) {
+        int any = 0;
+        for (int gi = 0; gi < ngi; gi++) any |= nonempty[gi * nb + bi];
+        if (!any) continue;
+        const uint64_t g = ck_galois_elt(ck, bamt[bi]);
+        if (g != 1) ck_inner_product(ck, dsrc, level, cache_get(ck, &kc, g), g, ip0, ip1);
+        for (int gi = 0; gi < ngi; gi++) {
+            if (!nonempty[gi * nb + bi]) continue;
+            const uint64_t* pt = pts + ((size_t)gi * nb + bi) * extw;
+            uint64_t* y = Y + (size_t)gi * 2 * extw;
+            if (g == 1)
+                conv_accumulate(ck, level, pt, ct, 1, NULL, NULL, Pmod, y, y + extw);
+            else
+                conv_accumulate(ck, level, pt, ct, g, ip0, ip1, Pmod, y, y + extw);
+        }
+    }
+    uint64_t* acc0 = calloc(extw, 8);
+    uint64_t* acc1 = calloc(extw, 8);
+    uint64_t* yq = malloc(ctw * 8);
+    uint64_t* perm = malloc((size_t)nr * N * 8);
+    for (int gi = 0; gi < ngi; gi++) {
+        int any = 0;
+        for (int bi = 0; bi < nb; bi++) any |= nonempty[gi * nb + bi];
+        if (!any) continue;
+        const uint64_t* y = Y + (size_t)gi * 2 * extw;
+        const uint64_t g = ck_galois_elt(ck, gamt[gi]);
+        if (g == 1) {
+            for (int u = 0; u < ne; u++) {
+                const uint64_t q = ck->q[ext_prime(ck, level, u)];
+                for (size_t k = 0; k < N; k++) {
+                    acc0[(size_t)u * N + k] = addm(acc0[(size_t)u * N + k], y[(size_t)u * N + k], q);
+                    acc1[(size_t)u * N + k] = addm(acc1[(size_t)u * N + k], y[extw + (size_t)u * N + k], q);
+                }
+            }
+            continue;
+        }
+        ck_moddown(ck, y, level, yq);
+        ck_moddown(ck, y + extw, level, yq + (size_t)nr * N);
+        ck_modup(ck, yq + (size_t)nr * N, level, dsrc);
+        ck_inner_product(ck, dsrc, level, cache_get(ck, &kc, g), g, ip0, ip1);
+        for (int t = 0; t < nr; t++) ck_automorph_ntt(ck, yq + (size_t)t * N, perm + (size_t)t * N, g);
+        for (int u = 0; u < ne; u++) {
+            const uint64_t q = ck->q[ext_prime(ck, level, u)];
+            for (size_t k = 0; k < N; k++) {
+                uint64_t t0 = ip0[(size_t)u * N + k];
+                if (u < nr) t0 = addm(t0, ck_mulmod(Pmod[u], perm[(size_t)u * N + k], q), q);
+                acc0[(size_t)u * N + k] = addm(acc0[(size_t)u * N + k], t0, q);
+                acc1[(size_t)u * N + k] = addm(acc1[(size_t)u * N + k], ip1[(size_t)u * N + k], q);
+            }
+        }
+    }
+    cache_free(&kc);
+    uint64_t* md = malloc(ctw * 8);
+    ck_moddown(ck, acc0, level, md);
+    ck_moddown(ck, acc1, level, md + (size_t)nr * N);
+    ck_rescale(ck, md, level, out);
+    if (out_scale) *out_scale = (ck->scale * pscale) / (double)ql;
+    free(md);
+    free(acc0);
+    free(acc1);
+    free(yq);
+    free(perm);
+    free(Y);
+    free(dsrc);
+    free(ip0);
+    free(ip1);
+    free(pts);
+    free(nonempty);
+    free(bamt);
+    free(gamt);
+    return 0;
+}
+
 int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,
             const double* filt, int plan, uint64_t* out, double* out_scale) {
     const size_t N = ck->N, s = N / 2, block = (size_t)m * m;
     if ((size_t)c * block > s || s % block || (size_t)c_out * block > s || level < 1) return -1;
+    if (plan == 3 || plan == 4) return conv_bsgs(ck, ct, level, c, m, kappa, c_out, filt, plan, out, out_scale);
     const int nr = level + 1, ne = nr + ck->K, dn = ck_dnum_at(ck, level);
     const long h = kappa / 2;
     const int nk = (int)((2 * h + 1) * (2 * h + 1));

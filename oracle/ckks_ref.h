@@ -90,7 +90,9 @@ void ck_rotate_hoisted(const ck_ctx* ck, const uint64_t* ct, int level, const lo
                        uint64_t* outs);
 
 /* Fused single-shard encrypted convolution: plan 1 =
- * Approach 1 (shifts first), plan 2 = Approach 2 (channel rotations first).
+ * Approach 1 (shifts first), plan 2 = Approach 2 (channel rotations first),
+ * plan 3 = BSGS with hoisted channel rotations + aggregated shifts,
+ * plan 4 = BSGS with hoisted shifts + aggregated channel rotations.
  * Input ct at `level` (scale = ck_scale), output ct at level - 1 after one
  * rescale; *out_scale receives the output scale. */
 int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,

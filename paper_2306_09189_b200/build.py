@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfheconv.so")
-SOURCES = ["kernels.cu", "fheconv.cu"]
+SOURCES = ["ntt.cu", "kernels.cu", "fheconv.cu"]
 HEADERS = ["kernels.cuh", "modarith.cuh", "host_math.hpp", "cdt_table.h"]
 
 NVCC_FLAGS = [

@@ -5,6 +5,7 @@
 // Reference interface mirrored: shardnn::Engine (reference
 // proj/include/shardnn/emu.hpp:132-183) and the conv entry points
 // conv_plan / conv_single_shard (proj/src/conv.cpp:254-271).
+#include <cuda_profiler_api.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -176,6 +177,15 @@ struct fhe_conv_layer {
     std::vector<int> nonempty;  // [c_in][nk]
     uint64_t* d_pts;            // [c_in][nk][ne][N]
     size_t pt_words;
+    std::vector<double> weights;
+    // BSGS plaintext sets (approach 3: baby = channel rotations, 4: baby = shifts)
+    struct Bsgs {
+        bool ready = false;
+        int nb = 0, ngi = 0;
+        std::vector<int64_t> bamt, gamt;
+        std::vector<int> nonempty;  // [ngi][nb]
+        uint64_t* d_pts = nullptr;  // [ngi][nb][ne][N], pt'[g][b] = rot_{-g}(pt)
+    } bs[2];
 };
 
 namespace {
@@ -516,8 +526,153 @@ void ledger_conv(fhe_ctx* c, const fhe_conv_layer* ly, int approach) {
     }
 }
 
+// Rotated plaintexts of the BSGS schedules, encoded once.
+fhe_conv_layer::Bsgs& ensure_bsgs(fhe_ctx* c, const fhe_conv_layer* cly, int orient) {
+    fhe_conv_layer* ly = const_cast<fhe_conv_layer*>(cly);
+    fhe_conv_layer::Bsgs& B = ly->bs[orient - 3];
+    if (B.ready) return B;
+    const long m = ly->m, h = ly->kappa / 2;
+    const int64_t block = (int64_t)m * m;
+    std::vector<int64_t> chan, shift;
+    for (int r = 0; r < ly->c_in; ++r) chan.push_back((int64_t)r * block);
+    for (long kk = -h; kk <= h; ++kk)
+        for (long ll = -h; ll <= h; ++ll) shift.push_back(kk * m + ll);
+    B.bamt = orient == 3 ? chan : shift;
+    B.gamt = orient == 3 ? shift : chan;
+    B.nb = (int)B.bamt.size();
+    B.ngi = (int)B.gamt.size();
+    if (B.nb > kMaxBaby) fail(FHE_E_INVALID, "too many baby steps for the BSGS schedule");
+    const int ne = c->ne_at(ly->level);
+    const size_t extw = (size_t)ne * c->N, s = c->slots();
+    ck(cudaMalloc(&B.d_pts, (size_t)B.ngi * B.nb * extw * 8), "cudaMalloc");
+    B.nonempty.assign((size_t)B.ngi * B.nb, 0);
+    const double pscale = (double)c->primes[ly->level];
+    std::vector<double> plain, rot(s);
+    for (int gi = 0; gi < B.ngi; ++gi)
+        for (int bi = 0; bi < B.nb; ++bi) {
+            const int r = orient == 3 ? bi : gi, i = orient == 3 ? gi : bi;
+            const long kk = i / (2 * h + 1) - h, ll = i % (2 * h + 1) - h;
+            if (!fused_plain(ly->c_in, ly->c_out, ly->m, ly->kappa, s, ly->weights.data(), r, kk, ll, plain))
+                continue;
+            B.nonempty[(size_t)gi * B.nb + bi] = 1;
+            const uint64_t g = c->reduce_amount(B.gamt[gi]);
+            for (size_t j = 0; j < s; ++j) rot[j] = plain[(j + s - g) % s];  // rot_{-g}
+            encode_rows(c, rot.data(), s, ly->level, pscale, ne, B.d_pts + ((size_t)gi * B.nb + bi) * extw);
+        }
+    ck(cudaStreamSynchronize(c->st), "sync");
+    B.ready = true;
+    return B;
+}
+
+void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orient, fhe_ct* out) {
+    fhe_conv_layer::Bsgs& B = ensure_bsgs(c, ly, orient);
+    const int level = ct->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N;
+    uint64_t* dsrc = c->alloc((size_t)dn * extw);
+    uint64_t* Y = c->alloc((size_t)B.ngi * 2 * extw);
+    uint64_t* XT = c->alloc((size_t)B.nb * 2 * extw);
+    modup(c, ct->c1(), level, dsrc);
+    // baby steps: the hoisted key switches of the source, then the plaintext mat-vec
+    BabyTerms t{};
+    t.nb = B.nb;
+    t.nb_total = B.nb;
+    t.pts = B.d_pts;
+    for (int b = 0; b < B.nb; ++b) {
+        const uint32_t g = c->galois_of(c->reduce_amount(B.bamt[b]));
+        t.galois[b] = g;
+        t.key[b] = g == 1 ? nullptr : c->key_for(g);
+        uint32_t any = 0;
+        for (int gi = 0; gi < B.ngi; ++gi) any |= B.nonempty[(size_t)gi * B.nb + b] ? 1u : 0u;
+        t.gmask[b] = any;
+        if (g != 1 && any) c->ledger.key_switches++;
+    }
+    c->timed("ks_multi", [&] { ks_multi(c->dc, XT, dsrc, ct->d, t, c->d_md, level, dn, c->st); });
+    for (int g0 = 0; g0 < B.ngi; g0 += kMaxGiant) {
+        t.ngi = std::min(kMaxGiant, B.ngi - g0);
+        t.g0 = g0;
+        for (int b = 0; b < B.nb; ++b) {
+            uint32_t mask = 0;
+            for (int gi = 0; gi < t.ngi; ++gi)
+                if (B.nonempty[(size_t)(g0 + gi) * B.nb + b]) mask |= 1u << gi;
+            t.gmask[b] = mask;
+        }
+        c->timed("pt_matvec", [&] { pt_matvec(c->dc, Y + (size_t)g0 * 2 * extw, XT, t, level, c->st); });
+    }
+    // giant steps: ModDown each aggregated Y_g, ModUp, key-switch-accumulate
+    uint64_t* acc = c->alloc(2 * extw);
+    ck(cudaMemsetAsync(acc, 0, 2 * extw * 8, c->st), "memset");
+    std::vector<int> giants;
+    int id = -1;
+    for (int gi = 0; gi < B.ngi; ++gi) {
+        bool any = false;
+        for (int b = 0; b < B.nb; ++b) any |= B.nonempty[(size_t)gi * B.nb + b] != 0;
+        if (!any) continue;
+        if (c->reduce_amount(B.gamt[gi]) == 0)
+            id = gi;
+        else
+            giants.push_back(gi);
+    }
+    uint64_t* yq = c->alloc((size_t)B.ngi * 2 * nr * N);
+    // batched ModDown over contiguous runs of giant accumulators
+    for (size_t a = 0; a < giants.size();) {
+        size_t b = a;
+        while (b + 1 < giants.size() && giants[b + 1] == giants[b] + 1) ++b;
+        const int first = giants[a], cnt = giants[b] - giants[a] + 1;
+        moddown(c, Y + (size_t)first * 2 * extw, level, 2 * cnt, yq + (size_t)first * 2 * nr * N, nullptr, 1);
+        a = b + 1;
+    }
+    for (int gi : giants) {
+        const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[gi]));
+        const uint64_t* yc = yq + (size_t)gi * 2 * nr * N;
+        modup(c, yc + (size_t)nr * N, level, dsrc);
+        const uint64_t* key = c->key_for(g);
+        c->timed("ks_inner", [&] { ks_accumulate(c->dc, acc, dsrc, key, yc, g, c->d_md, level, dn, c->st); });
+        c->ledger.key_switches++;
+    }
+    if (id >= 0) qp_add(c->dc, acc, Y + (size_t)id * 2 * extw, level, c->st);
+    uint64_t* md = c->alloc((size_t)2 * nr * N);
+    moddown(c, acc, level, 2, md, nullptr, 1);
+    rescale_into(c, md, level, out->d);
+    out->scale = (ct->scale * (double)c->primes[level]) / (double)c->primes[level];
+    out->depth = ct->depth + 1;
+    c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, out->depth);
+    // ledger: one hoisted baby group + one rotation per giant step
+    fhe_ledger& lg = c->ledger;
+    lg.hoist_groups++;
+    for (int b = 0; b < B.nb; ++b) {
+        c->note_amount(c->reduce_amount(B.bamt[b]));
+        lg.hoisted_rotations++;
+    }
+    for (int gi : giants) {
+        c->note_amount(c->reduce_amount(B.gamt[gi]));
+        lg.rotations++;
+    }
+    uint64_t pairs = 0;
+    for (int v : B.nonempty) pairs += v;
+    lg.ct_pt_mults += pairs;
+    lg.adds += pairs ? pairs - 1 : 0;
+    c->release(md);
+    c->release(acc);
+    c->release(yq);
+    c->release(Y);
+    c->release(XT);
+    c->release(dsrc);
+}
+
+int auto_orient(const fhe_conv_layer* ly) {
+    // giant steps each cost a ModUp: take the smaller set as giant steps
+    return ly->kappa * ly->kappa <= ly->c_in ? 3 : 4;
+}
+
 void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct* out) {
-    if (approach != 1 && approach != 2) fail(FHE_E_INVALID, "approach must be 1 or 2");
+    if (approach < 0 || approach > 4) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3 or 4");
+    if (approach == 0) approach = auto_orient(ly);
+    if (approach >= 3) {
+        if (ct->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
+        if (out->level != ct->level - 1) fail(FHE_E_INVALID, "output level must be input level - 1");
+        conv_bsgs(c, ct, ly, approach, out);
+        return;
+    }
     if (ct->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
     if (out->level != ct->level - 1) fail(FHE_E_INVALID, "output level must be input level - 1");
     const int level = ct->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
@@ -725,6 +880,8 @@ int fhe_prof_get(fhe_ctx* c, const char* cls, double* total_ms, uint64_t* launch
         if (launches) *launches = it == c->prof.end() ? 0 : it->second.n;
     });
 }
+
+int fhe_profiler_range(int on) { return (on ? cudaProfilerStart() : cudaProfilerStop()) == cudaSuccess ? 0 : FHE_E_CUDA; }
 
 int fhe_prof_reset(fhe_ctx* c) {
     return guard(c, [&] {
@@ -1099,6 +1256,7 @@ int fhe_conv_layer_create(fhe_ctx* c, int c_in, int c_out, int m, int kappa, con
         ly->kappa = kappa;
         ly->level = level;
         ly->nk = kappa * kappa;
+        ly->weights.assign(weights, weights + (size_t)c_in * c_out * kappa * kappa);
         const int ne = c->ne_at(level);
         ly->pt_words = (size_t)c_in * ly->nk * ne * c->N;
         ck(cudaMalloc(&ly->d_pts, ly->pt_words * 8), "cudaMalloc");
@@ -1125,6 +1283,8 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
     if (!ly) return;
     cudaStreamSynchronize(ly->ctx->st);
     cudaFree(ly->d_pts);
+    for (auto& b : ly->bs)
+        if (b.d_pts) cudaFree(b.d_pts);
     delete ly;
 }
 

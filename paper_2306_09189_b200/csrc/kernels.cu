@@ -10,9 +10,10 @@
 
 namespace fhe {
 
-namespace {
-
 uint64_t g_launches = 0;  // every kernel this library enqueues (host-side count)
+void note_launch(int n) { g_launches += n; }
+
+namespace {
 
 constexpr int kEwThreads = 256;
 
@@ -31,201 +32,7 @@ __device__ __forceinline__ uint32_t perm_index(uint32_t k, uint32_t g, int logN)
     return brev_n((e2 - 1) >> 1, logN);
 }
 
-// ----------------------------------------------------------------- NTT
-// Forward negacyclic NTT split as N = N1 * B:
-//  phase A: the first log N1 Cooley-Tukey stages act on "columns" (stride B)
-//  phase B: the last log B stages act on contiguous blocks of B words.
-// The inverse runs the Gentleman-Sande stages in the mirrored order.
-
-template <int LOG_N1, int C>
-__global__ void __launch_bounds__(256) k_ntt_fwd_a(DevCtx c, uint64_t* data, RowMap rm) {
-    constexpr int N1 = 1 << LOG_N1;
-    __shared__ uint64_t s[N1 * C];
-    const int row = blockIdx.y;
-    const int u = row % rm.rows_per_poly;
-    if (rm.skip_alpha) {
-        const int j = row / rm.rows_per_poly, lo = j * rm.skip_alpha;
-        const int hi = min(lo + rm.skip_alpha, rm.level + 1);
-        if (u >= lo && u < hi) return;
-    }
-    const int p = row_prime(rm, u);
-    const uint64_t q = c.primes[p].q;
-    const uint64_t* tw = c.tw + (size_t)p * c.N;
-    const uint64_t* tws = c.tw_sh + (size_t)p * c.N;
-    const int B = c.N >> LOG_N1;
-    const int col0 = blockIdx.x * C;
-    uint64_t* a = data + (size_t)row * c.N;
-    for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-        const int r = i / C, cc = i % C;
-        s[i] = a[(size_t)r * B + col0 + cc];
-    }
-    __syncthreads();
-    for (int m = 1; m < N1; m <<= 1) {
-        const int tr = N1 / (2 * m);
-        for (int bf = threadIdx.x; bf < (N1 / 2) * C; bf += blockDim.x) {
-            const int cc = bf % C, b = bf / C;
-            const int g = b / tr;
-            const int r = g * 2 * tr + (b % tr);
-            const uint64_t w = tw[m + g], ws = tws[m + g];
-            const uint64_t U = s[r * C + cc];
-            const uint64_t V = mul_shoup(s[(r + tr) * C + cc], w, ws, q);
-            s[r * C + cc] = add_mod(U, V, q);
-            s[(r + tr) * C + cc] = sub_mod(U, V, q);
-        }
-        __syncthreads();
-    }
-    for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-        const int r = i / C, cc = i % C;
-        a[(size_t)r * B + col0 + cc] = s[i];
-    }
-}
-
-template <int LOG_B>
-__global__ void __launch_bounds__(128) k_ntt_fwd_b(DevCtx c, uint64_t* data, RowMap rm) {
-    constexpr int B = 1 << LOG_B;
-    __shared__ uint64_t s[B];
-    const int row = blockIdx.y;
-    const int u = row % rm.rows_per_poly;
-    if (rm.skip_alpha) {
-        const int j = row / rm.rows_per_poly, lo = j * rm.skip_alpha;
-        const int hi = min(lo + rm.skip_alpha, rm.level + 1);
-        if (u >= lo && u < hi) return;
-    }
-    const int p = row_prime(rm, u);
-    const uint64_t q = c.primes[p].q;
-    const uint64_t* tw = c.tw + (size_t)p * c.N;
-    const uint64_t* tws = c.tw_sh + (size_t)p * c.N;
-    const int blk = blockIdx.x;
-    uint64_t* a = data + (size_t)row * c.N + (size_t)blk * B;
-    for (int i = threadIdx.x; i < B; i += blockDim.x) s[i] = a[i];
-    __syncthreads();
-    const int N1 = c.N >> LOG_B;
-    int t = B / 2;
-    for (int m = N1; m < c.N; m <<= 1, t >>= 1) {
-        for (int bf = threadIdx.x; bf < B / 2; bf += blockDim.x) {
-            const int g = bf / t;
-            const int j = g * 2 * t + (bf % t);
-            const int widx = m + blk * (B / (2 * t)) + g;
-            const uint64_t U = s[j];
-            const uint64_t V = mul_shoup(s[j + t], tw[widx], tws[widx], q);
-            s[j] = add_mod(U, V, q);
-            s[j + t] = sub_mod(U, V, q);
-        }
-        __syncthreads();
-    }
-    for (int i = threadIdx.x; i < B; i += blockDim.x) a[i] = s[i];
-}
-
-template <int LOG_B>
-__global__ void __launch_bounds__(128) k_ntt_inv_b(DevCtx c, uint64_t* data, RowMap rm) {
-    constexpr int B = 1 << LOG_B;
-    __shared__ uint64_t s[B];
-    const int row = blockIdx.y;
-    const int u = row % rm.rows_per_poly;
-    const int p = row_prime(rm, u);
-    const uint64_t q = c.primes[p].q;
-    const uint64_t* tw = c.itw + (size_t)p * c.N;
-    const uint64_t* tws = c.itw_sh + (size_t)p * c.N;
-    const int blk = blockIdx.x;
-    uint64_t* a = data + (size_t)row * c.N + (size_t)blk * B;
-    for (int i = threadIdx.x; i < B; i += blockDim.x) s[i] = a[i];
-    __syncthreads();
-    int h = c.N / 2;
-    for (int t = 1; t <= B / 2; t <<= 1, h >>= 1) {
-        for (int bf = threadIdx.x; bf < B / 2; bf += blockDim.x) {
-            const int g = bf / t;
-            const int j = g * 2 * t + (bf % t);
-            const int widx = h + blk * (B / (2 * t)) + g;
-            const uint64_t U = s[j], V = s[j + t];
-            s[j] = add_mod(U, V, q);
-            s[j + t] = mul_shoup(sub_mod(U, V, q), tw[widx], tws[widx], q);
-        }
-        __syncthreads();
-    }
-    for (int i = threadIdx.x; i < B; i += blockDim.x) a[i] = s[i];
-}
-
-template <int LOG_N1, int C>
-__global__ void __launch_bounds__(256) k_ntt_inv_a(DevCtx c, uint64_t* data, RowMap rm) {
-    constexpr int N1 = 1 << LOG_N1;
-    __shared__ uint64_t s[N1 * C];
-    const int row = blockIdx.y;
-    const int u = row % rm.rows_per_poly;
-    const int p = row_prime(rm, u);
-    const uint64_t q = c.primes[p].q;
-    const uint64_t* tw = c.itw + (size_t)p * c.N;
-    const uint64_t* tws = c.itw_sh + (size_t)p * c.N;
-    const int B = c.N >> LOG_N1;
-    const int col0 = blockIdx.x * C;
-    uint64_t* a = data + (size_t)row * c.N;
-    for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-        const int r = i / C, cc = i % C;
-        s[i] = a[(size_t)r * B + col0 + cc];
-    }
-    __syncthreads();
-    for (int tr = 1; tr < N1; tr <<= 1) {
-        const int h = N1 / (2 * tr);
-        for (int bf = threadIdx.x; bf < (N1 / 2) * C; bf += blockDim.x) {
-            const int cc = bf % C, b = bf / C;
-            const int g = b / tr;
-            const int r = g * 2 * tr + (b % tr);
-            const uint64_t U = s[r * C + cc], V = s[(r + tr) * C + cc];
-            s[r * C + cc] = add_mod(U, V, q);
-            s[(r + tr) * C + cc] = mul_shoup(sub_mod(U, V, q), tw[h + g], tws[h + g], q);
-        }
-        __syncthreads();
-    }
-    const uint64_t ni = c.ninv[p], nis = c.ninv_sh[p];
-    for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-        const int r = i / C, cc = i % C;
-        a[(size_t)r * B + col0 + cc] = mul_shoup(s[i], ni, nis, q);
-    }
-}
-
-constexpr int kCols = 16;
-
-template <int LOG_N1, int LOG_B>
-void ntt_fwd_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st) {
-    const int N1 = 1 << LOG_N1, B = 1 << LOG_B;
-    ++g_launches;
-    k_ntt_fwd_a<LOG_N1, kCols><<<dim3(B / kCols, nrows), 256, 0, st>>>(c, data, rm);
-    ++g_launches;
-    k_ntt_fwd_b<LOG_B><<<dim3(N1, nrows), 128, 0, st>>>(c, data, rm);
-}
-template <int LOG_N1, int LOG_B>
-void ntt_inv_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st) {
-    const int N1 = 1 << LOG_N1, B = 1 << LOG_B;
-    ++g_launches;
-    k_ntt_inv_b<LOG_B><<<dim3(N1, nrows), 128, 0, st>>>(c, data, rm);
-    ++g_launches;
-    k_ntt_inv_a<LOG_N1, kCols><<<dim3(B / kCols, nrows), 256, 0, st>>>(c, data, rm);
-}
-
 }  // namespace
-
-void ntt_forward(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st) {
-    if (nrows <= 0) return;
-    switch (c.logN) {
-        case 12: ntt_fwd_dispatch<6, 6>(c, data, nrows, rm, st); break;
-        case 13: ntt_fwd_dispatch<6, 7>(c, data, nrows, rm, st); break;
-        case 14: ntt_fwd_dispatch<7, 7>(c, data, nrows, rm, st); break;
-        case 15: ntt_fwd_dispatch<7, 8>(c, data, nrows, rm, st); break;
-        case 16: ntt_fwd_dispatch<8, 8>(c, data, nrows, rm, st); break;
-        default: break;
-    }
-}
-
-void ntt_inverse(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st) {
-    if (nrows <= 0) return;
-    switch (c.logN) {
-        case 12: ntt_inv_dispatch<6, 6>(c, data, nrows, rm, st); break;
-        case 13: ntt_inv_dispatch<6, 7>(c, data, nrows, rm, st); break;
-        case 14: ntt_inv_dispatch<7, 7>(c, data, nrows, rm, st); break;
-        case 15: ntt_inv_dispatch<7, 8>(c, data, nrows, rm, st); break;
-        case 16: ntt_inv_dispatch<8, 8>(c, data, nrows, rm, st); break;
-        default: break;
-    }
-}
 
 // ------------------------------------------------------------ sampling
 namespace {
@@ -638,6 +445,259 @@ void conv_mac(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
     ++g_launches;
     k_conv_mac<<<ew_blocks(total), 256, 0, st>>>(c, acc, digits, x, t, md, level, dn);
+}
+
+namespace {
+
+// ---- key-switch inner products on coefficient pairs (k, k+1), k even.
+// In bit-reversed NTT order perm_g(k+1) = perm_g(k) ^ 1, so the gathered
+// digit pair is the aligned pair {2j, 2j+1} (possibly swapped): every access
+// below is a 16-byte vector load.
+__device__ __forceinline__ ulonglong2 ld2(const uint64_t* p) { return __ldg(reinterpret_cast<const ulonglong2*>(p)); }
+__device__ __forceinline__ ulonglong2 ld2cs(const uint64_t* p) {
+    return __ldcs(reinterpret_cast<const ulonglong2*>(p));
+}
+__device__ __forceinline__ void st2(uint64_t* p, uint64_t a, uint64_t b) {
+    *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(a, b);
+}
+
+template <int DN>
+__device__ __forceinline__ void ip_pair(const uint64_t* __restrict__ D, const uint64_t* __restrict__ key, int ne,
+                                        int np, int u, int p, uint32_t k, uint32_t pk, int N, U128 (&s0)[2],
+                                        U128 (&s1)[2]) {
+    const uint32_t base = pk & ~1u;
+    const bool swp = pk & 1u;
+    ulonglong2 d[DN], k0[DN], k1[DN];
+#pragma unroll
+    for (int j = 0; j < DN; ++j) {
+        d[j] = ld2(D + ((size_t)j * ne + u) * N + base);
+        k0[j] = ld2cs(key + (((size_t)j * 2 + 0) * np + p) * N + k);
+        k1[j] = ld2cs(key + (((size_t)j * 2 + 1) * np + p) * N + k);
+    }
+#pragma unroll
+    for (int j = 0; j < DN; ++j) {
+        const uint64_t da = swp ? d[j].y : d[j].x, db = swp ? d[j].x : d[j].y;
+        mac(s0[0], da, k0[j].x);
+        mac(s0[1], db, k0[j].y);
+        mac(s1[0], da, k1[j].x);
+        mac(s1[1], db, k1[j].y);
+    }
+}
+
+// XT[b][c] = (IP_0(D, key_b) + [u<=l] P sigma_b(X.c0), IP_1(D, key_b)); identity b: P X
+template <int DN>
+__global__ void __launch_bounds__(256) k_ks_multi(DevCtx c, uint64_t* XT, const uint64_t* D, const uint64_t* X,
+                                                  BabyTerms t, const ModDownTable* md, int level) {
+    const int nr = level + 1, ne = nr + c.K;
+    const int np = c.L + c.K;
+    const size_t total = (size_t)ne * c.N;
+    const size_t pairs = total / 2;
+    RowMap rm{ne, level, c.L, 0};
+    for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < pairs; ip += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = ip * 2;
+        const int u = (int)(i / c.N);
+        const uint32_t k = (uint32_t)(i % c.N);
+        const int p = row_prime(rm, u);
+        const Prime pr = c.primes[p];
+        const bool qrow = u < nr;
+        const uint64_t pm = qrow ? md->pmod[u] : 0, pms = qrow ? md->pmod_sh[u] : 0;
+        for (int b = 0; b < t.nb; ++b) {
+            uint64_t* xt = XT + (size_t)b * 2 * total;
+            const uint32_t gal = t.galois[b];
+            if (t.gmask[b] == 0) continue;
+            if (gal == 1) {
+                if (qrow) {
+                    const ulonglong2 a = ld2(X + (size_t)u * c.N + k);
+                    const ulonglong2 bb = ld2(X + ((size_t)nr + u) * c.N + k);
+                    st2(xt + i, mul_shoup(a.x, pm, pms, pr.q), mul_shoup(a.y, pm, pms, pr.q));
+                    st2(xt + total + i, mul_shoup(bb.x, pm, pms, pr.q), mul_shoup(bb.y, pm, pms, pr.q));
+                } else {
+                    st2(xt + i, 0, 0);
+                    st2(xt + total + i, 0, 0);
+                }
+                continue;
+            }
+            const uint32_t pk = perm_index(k, gal, c.logN);
+            U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
+            ip_pair<DN>(D, t.key[b], ne, np, u, p, k, pk, c.N, s0, s1);
+            if (qrow) {
+                const ulonglong2 x = ld2(X + (size_t)u * c.N + (pk & ~1u));
+                const bool swp = pk & 1u;
+                add128(s0[0], mul_shoup(swp ? x.y : x.x, pm, pms, pr.q));
+                add128(s0[1], mul_shoup(swp ? x.x : x.y, pm, pms, pr.q));
+            }
+            st2(xt + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
+            st2(xt + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
+        }
+    }
+}
+
+// Y[g][c] = sum_b pt[g][b] * XT[b][c]  (the plaintext "matrix-vector" of the baby steps)
+template <int NG>
+__global__ void __launch_bounds__(256) k_pt_matvec(DevCtx c, uint64_t* Y, const uint64_t* XT, BabyTerms t,
+                                                   int level) {
+    const int ne = level + 1 + c.K;
+    const size_t total = (size_t)ne * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int u = (int)(i / c.N);
+        const Prime pr = c.primes[row_prime(rm, u)];
+        U128 a0[NG], a1[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) a0[g] = a1[g] = U128{0, 0};
+        for (int b = 0; b < t.nb; ++b) {
+            const uint32_t mask = t.gmask[b];
+            if (mask == 0) continue;
+            const uint64_t x0 = __ldcs(XT + (size_t)b * 2 * total + i);
+            const uint64_t x1 = __ldcs(XT + (size_t)b * 2 * total + total + i);
+            uint64_t w[NG];
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+                w[g] = (g < t.ngi && ((mask >> g) & 1u))
+                           ? __ldcs(t.pts + (((size_t)(t.g0 + g) * t.nb_total + b) * ne) * c.N + i)
+                           : 0;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                mac(a0[g], w[g], x0);
+                mac(a1[g], w[g], x1);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            if (g < t.ngi) {
+                uint64_t* y = Y + (size_t)g * 2 * total;
+                y[i] = reduce128(a0[g].hi, a0[g].lo, pr);
+                y[total + i] = reduce128(a1[g].hi, a1[g].lo, pr);
+            }
+        }
+    }
+}
+
+template <int DN>
+__global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc, const uint64_t* D,
+                                                         const uint64_t* key, const uint64_t* c0, uint32_t g,
+                                                         const ModDownTable* md, int level) {
+    const int nr = level + 1, ne = nr + c.K;
+    const int np = c.L + c.K;
+    const size_t total = (size_t)ne * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < total / 2;
+         ip += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = ip * 2;
+        const int u = (int)(i / c.N);
+        const uint32_t k = (uint32_t)(i % c.N);
+        const int p = row_prime(rm, u);
+        const Prime pr = c.primes[p];
+        const uint32_t pk = perm_index(k, g, c.logN);
+        U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
+        ip_pair<DN>(D, key, ne, np, u, p, k, pk, c.N, s0, s1);
+        if (u < nr) {
+            const ulonglong2 x = ld2(c0 + (size_t)u * c.N + (pk & ~1u));
+            const bool swp = pk & 1u;
+            add128(s0[0], mul_shoup(swp ? x.y : x.x, md->pmod[u], md->pmod_sh[u], pr.q));
+            add128(s0[1], mul_shoup(swp ? x.x : x.y, md->pmod[u], md->pmod_sh[u], pr.q));
+        }
+        const ulonglong2 a0 = ld2(acc + i), a1 = ld2(acc + total + i);
+        add128(s0[0], a0.x);
+        add128(s0[1], a0.y);
+        add128(s1[0], a1.x);
+        add128(s1[1], a1.y);
+        st2(acc + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
+        st2(acc + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
+    }
+}
+
+__global__ void k_ks_accumulate(DevCtx c, uint64_t* acc, const uint64_t* D, const uint64_t* key, const uint64_t* c0,
+                                uint32_t g, const ModDownTable* md, int level, int dn) {
+    const int nr = level + 1, ne = nr + c.K;
+    const int np = c.L + c.K;
+    const size_t total = (size_t)ne * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int u = (int)(i / c.N);
+        const uint32_t k = (uint32_t)(i % c.N);
+        const int p = row_prime(rm, u);
+        const Prime pr = c.primes[p];
+        const uint32_t pk = perm_index(k, g, c.logN);
+        U128 s0{0, 0}, s1{0, 0};
+        for (int j = 0; j < dn; ++j) {
+            const uint64_t d = D[((size_t)j * ne + u) * c.N + pk];
+            mac(s0, d, key[(((size_t)j * 2 + 0) * np + p) * c.N + k]);
+            mac(s1, d, key[(((size_t)j * 2 + 1) * np + p) * c.N + k]);
+        }
+        if (u < nr) add128(s0, mul_shoup(c0[(size_t)u * c.N + pk], md->pmod[u], md->pmod_sh[u], pr.q));
+        add128(s0, acc[i]);
+        add128(s1, acc[total + i]);
+        acc[i] = reduce128(s0.hi, s0.lo, pr);
+        acc[total + i] = reduce128(s1.hi, s1.lo, pr);
+    }
+}
+
+__global__ void k_qp_add(DevCtx c, uint64_t* acc, const uint64_t* y, int level) {
+    const int ne = level + 1 + c.K;
+    const size_t total = (size_t)2 * ne * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int u = (int)((i / c.N) % ne);
+        acc[i] = add_mod(acc[i], y[i], c.primes[row_prime(rm, u)].q);
+    }
+}
+
+}  // namespace
+
+#define FHE_DN_SWITCH(dn, CALL) \
+    switch (dn) {                  \
+        case 1: CALL(1); break;    \
+        case 2: CALL(2); break;    \
+        case 3: CALL(3); break;    \
+        case 4: CALL(4); break;    \
+        case 5: CALL(5); break;    \
+        case 6: CALL(6); break;    \
+        case 7: CALL(7); break;    \
+        case 8: CALL(8); break;    \
+        default: break;            \
+    }
+
+void ks_multi(const DevCtx& c, uint64_t* XT, const uint64_t* digits, const uint64_t* ct, const BabyTerms& t,
+              const ModDownTable* md, int level, int dn, cudaStream_t st) {
+    const size_t total = (size_t)(level + 1 + c.K) * c.N;
+    const int blocks = ew_blocks(total / 2);
+#define FHE_KS_MULTI(D) k_ks_multi<D><<<blocks, 256, 0, st>>>(c, XT, digits, ct, t, md, level)
+    ++g_launches;
+    FHE_DN_SWITCH(dn, FHE_KS_MULTI)
+#undef FHE_KS_MULTI
+}
+
+void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms& t, int level, cudaStream_t st) {
+    const size_t total = (size_t)(level + 1 + c.K) * c.N;
+    const int blocks = ew_blocks(total);
+    ++g_launches;
+    if (t.ngi <= 4)
+        k_pt_matvec<4><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
+    else if (t.ngi <= 8)
+        k_pt_matvec<8><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
+    else if (t.ngi <= 9)
+        k_pt_matvec<9><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
+    else if (t.ngi <= 12)
+        k_pt_matvec<12><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
+    else
+        k_pt_matvec<16><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
+}
+
+void ks_accumulate(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* key, const uint64_t* c0,
+                   uint32_t galois, const ModDownTable* md, int level, int dn, cudaStream_t st) {
+    const size_t total = (size_t)(level + 1 + c.K) * c.N;
+    ++g_launches;
+    const int blocks = ew_blocks(total / 2);
+#define FHE_KS_ACC(D) k_ks_accumulate_t<D><<<blocks, 256, 0, st>>>(c, acc, digits, key, c0, galois, md, level)
+    FHE_DN_SWITCH(dn, FHE_KS_ACC)
+#undef FHE_KS_ACC
+}
+
+void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st) {
+    const size_t total = (size_t)2 * (level + 1 + c.K) * c.N;
+    ++g_launches;
+    k_qp_add<<<ew_blocks(total), kEwThreads, 0, st>>>(c, acc, y, level);
 }
 
 uint64_t launches_total() { return g_launches; }

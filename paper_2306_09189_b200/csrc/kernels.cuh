@@ -73,6 +73,21 @@ struct MacTerms {
     const uint64_t* pt[kMaxTerms];         // [level+1+K][N]
 };
 
+// Baby steps of the BSGS conv: rotations of one hoisted
+// source, each multiplied by up to kMaxGiant rotated plaintexts.
+constexpr int kMaxBaby = 32;
+constexpr int kMaxGiant = 16;
+struct BabyTerms {
+    int nb;                          // baby steps
+    int ngi;                         // giant accumulators in this launch
+    int nb_total;                    // plaintext matrix row length
+    int g0;                          // first giant index of this launch
+    uint32_t galois[kMaxBaby];       // 1 = identity
+    const uint64_t* key[kMaxBaby];
+    uint32_t gmask[kMaxBaby];        // bit (g - g0) set when pt[g][b] is non-empty
+    const uint64_t* pts;             // [ngi_total][nb_total][ne][N]
+};
+
 // --------------------------------------------------------------- launchers
 // total number of kernels enqueued by this library (for the bench's gpu_launches)
 uint64_t launches_total();
@@ -144,5 +159,18 @@ void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, int lev
 // identity terms (g = 1): ACC_c += pt_i * [u<=l] P X.c
 void conv_mac(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* x, const MacTerms& t,
               const ModDownTable* md, int level, int dn, cudaStream_t st);
+
+// Baby steps of the BSGS conv, in two streaming passes:
+// XT[b] = (IP_0(D, key_b) + [u<=l] P sigma_b(ct.c0), IP_1(D, key_b)) (identity b: P ct) over the
+// QP basis, XT = [nb][2][ne][N], for babies with gmask[b] != 0;
+void ks_multi(const DevCtx& c, uint64_t* XT, const uint64_t* digits, const uint64_t* ct, const BabyTerms& t,
+              const ModDownTable* md, int level, int dn, cudaStream_t st);
+// Y[g][c] = sum_b pt[g0 + g][b] * XT[b][c] for g < t.ngi, Y = [ngi][2][ne][N] (overwritten)
+void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms& t, int level, cudaStream_t st);
+// acc_0 += IP_0(D, key, g) + [u <= l] P sigma_g(c0);  acc_1 += IP_1(D, key, g)   (acc = [2][ne][N])
+void ks_accumulate(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* key, const uint64_t* c0,
+                   uint32_t galois, const ModDownTable* md, int level, int dn, cudaStream_t st);
+// acc += y over [2][ne][N] (QP basis)
+void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st);
 
 }  // namespace fhe

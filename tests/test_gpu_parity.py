@@ -121,7 +121,7 @@ def conv_case(oracle, golden, name):
     return c, m, k, co, img, filt
 
 
-@pytest.mark.parametrize("approach", [1, 2])
+@pytest.mark.parametrize("approach", [1, 2, 3, 4])
 def test_conv_cfg1_bit_exact_and_within_tolerance(oracle, golden, p1, approach):
     c, m, k, co, img, filt = conv_case(oracle, golden, "cfg1")
     layer = p1.ctx.conv_layer(c, co, m, k, filt)
@@ -136,7 +136,7 @@ def test_conv_cfg1_bit_exact_and_within_tolerance(oracle, golden, p1, approach):
     assert err < TOL, err
 
 
-@pytest.mark.parametrize("approach", [1, 2])
+@pytest.mark.parametrize("approach", [1, 2, 3, 4])
 def test_conv_cfg3_bit_exact_and_within_tolerance(oracle, golden, approach):
     p = pair(oracle, "cfg3")
     c, m, k, co, img, filt = conv_case(oracle, golden, "cfg3")
@@ -153,18 +153,30 @@ def test_conv_cfg3_bit_exact_and_within_tolerance(oracle, golden, approach):
 
 
 @pytest.mark.slow
-def test_conv_cfg4_bit_exact_and_within_tolerance(oracle, golden):
+@pytest.mark.parametrize("approach", [2, 4])
+def test_conv_cfg4_bit_exact_and_within_tolerance(oracle, golden, approach):
     p = pair(oracle, "cfg4")
     c, m, k, co, img, filt = conv_case(oracle, golden, "cfg4")
     layer = p.ctx.conv_layer(c, co, m, k, filt)
     p.ctx.gen_galois_keys(layer.steps())
     ct = p.ctx.encrypt(p.ctx.encode(img), ENC_SEED)
-    out = p.ctx.conv2d(ct, layer, 2)
+    out = p.ctx.conv2d(ct, layer, approach)
     err = np.abs(p.ctx.decrypt(out) - golden["cfg4/slots"]).max()
     assert err < TOL, err
     ctr = p.ck.encrypt(p.ck.encode(img, p.ck.scale, p.top), p.top, ENC_SEED)
-    ref, _ = p.ck.conv(ctr, p.top, c, m, k, co, filt, 2)
+    ref, _ = p.ck.conv(ctr, p.top, c, m, k, co, filt, approach)
     assert np.array_equal(out.residues(), ref)
+
+
+def test_conv_auto_schedule_picks_fewer_decompositions(oracle, golden):
+    p = pair(oracle, "cfg1")
+    c, m, k, co, img, filt = conv_case(oracle, golden, "cfg1")
+    layer = p.ctx.conv_layer(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    ct = p.ctx.encrypt(p.ctx.encode(img), ENC_SEED)
+    a = p.ctx.conv2d(ct, layer, 0)
+    b = p.ctx.conv2d(ct, layer, 4)  # c = 4 < kappa^2 = 9: shifts hoisted, 3 giant steps
+    assert np.array_equal(a.residues(), b.residues())
 
 
 def test_conv_cfg5_three_layer_stack(oracle, golden):
@@ -176,7 +188,7 @@ def test_conv_cfg5_three_layer_stack(oracle, golden):
         _, filt = oracle.make_inputs(16, 32, 3, 16, 0, sf, 1)
         layer = p.ctx.conv_layer(16, 16, 32, 3, filt, level=ct.level)
         p.ctx.gen_galois_keys(layer.steps())
-        ct = p.ctx.conv2d(ct, layer, 2)
+        ct = p.ctx.conv2d(ct, layer, (2, 3, 1)[li])
         assert ct.level == p.top - 1 - li
         err = np.abs(p.ctx.decrypt(ct) - golden[f"cfg5/out{li}"]).max()
         assert err < TOL, (li, err)
