@@ -217,19 +217,26 @@ fhe_ct* new_ct(fhe_ctx* c, int level, double scale, int depth) {
 
 // ------------------------------------------------------------ primitives
 
-// digits [dn][ne][N] of c1 (level+1 rows, NTT)
-void modup(fhe_ctx* c, const uint64_t* c1, int level, uint64_t* digits) {
+// digits [nsrc][dn][ne][N] of nsrc polynomials c1 + s * stride (level+1 rows each, NTT)
+void modup_batch(fhe_ctx* c, const uint64_t* c1, size_t stride, int nsrc, int level, uint64_t* digits) {
     const int nr = level + 1, dn = c->dn_at(level), ne = c->ne_at(level);
-    uint64_t* coef = c->alloc((size_t)nr * c->N);
-    ck(cudaMemcpyAsync(coef, c1, (size_t)nr * c->N * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
-    c->timed("ntt", [&] { ntt_inverse(c->dc, coef, nr, qmap(c, level), c->st); });
+    const size_t rowsw = (size_t)nr * c->N;
+    uint64_t* coef = c->alloc((size_t)nsrc * rowsw);
+    ck(cudaMemcpy2DAsync(coef, rowsw * 8, c1, stride * 8, rowsw * 8, nsrc, cudaMemcpyDeviceToDevice, c->st),
+       "memcpy2d");
+    c->timed("ntt", [&] { ntt_inverse(c->dc, coef, nsrc * nr, qmap(c, level), c->st); });
     c->timed("modup_bconv", [&] {
-        modup_bconv(c->dc, coef, c1, digits, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+        modup_bconv(c->dc, coef, c1, stride, nsrc, digits, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
     });
-    c->timed("ntt", [&] { ntt_forward(c->dc, digits, dn * ne, RowMap{ne, level, c->L, c->alpha}, c->st); });
+    c->timed("ntt", [&] {
+        ntt_forward(c->dc, digits, nsrc * dn * ne, RowMap{ne, level, c->L, c->alpha, dn}, c->st);
+    });
     c->release(coef);
-    c->ledger.modups++;
+    c->ledger.modups += nsrc;
 }
+
+// digits [dn][ne][N] of c1 (level+1 rows, NTT)
+void modup(fhe_ctx* c, const uint64_t* c1, int level, uint64_t* digits) { modup_batch(c, c1, 0, 1, level, digits); }
 
 // out[p] = ModDown(acc[p]) (+ sigma_g(add_src) on poly 0)
 void moddown(fhe_ctx* c, const uint64_t* acc, int level, int npoly, uint64_t* out, const uint64_t* add_src,
@@ -621,13 +628,35 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
         moddown(c, Y + (size_t)first * 2 * extw, level, 2 * cnt, yq + (size_t)first * 2 * nr * N, nullptr, 1);
         a = b + 1;
     }
-    for (int gi : giants) {
-        const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[gi]));
-        const uint64_t* yc = yq + (size_t)gi * 2 * nr * N;
-        modup(c, yc + (size_t)nr * N, level, dsrc);
-        const uint64_t* key = c->key_for(g);
-        c->timed("ks_inner", [&] { ks_accumulate(c->dc, acc, dsrc, key, yc, g, c->d_md, level, dn, c->st); });
-        c->ledger.key_switches++;
+    // all giant steps at once: one batched ModUp, one accumulate kernel
+    if (!giants.empty()) {
+        const size_t dw = (size_t)dn * extw;
+        const int per = std::min<int>((int)giants.size(), kMaxGiant);
+        uint64_t* dg = c->alloc((size_t)per * dw);
+        for (size_t a = 0; a < giants.size(); a += per) {
+            const int n = std::min<int>(per, (int)(giants.size() - a));
+            // sources must be equally spaced: giants[a..a+n) may skip the identity, so ModUp each run
+            for (int s = 0; s < n;) {
+                int e = s;
+                while (e + 1 < n && giants[a + e + 1] == giants[a + e] + 1) ++e;
+                const uint64_t* c1 = yq + (size_t)giants[a + s] * 2 * nr * N + (size_t)nr * N;
+                modup_batch(c, c1, (size_t)2 * nr * N, e - s + 1, level, dg + (size_t)s * dw);
+                s = e + 1;
+            }
+            GiantTerms gt{};
+            gt.n = n;
+            gt.digits = dg;
+            for (int s = 0; s < n; ++s) {
+                const int gi = giants[a + s];
+                const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[gi]));
+                gt.galois[s] = g;
+                gt.key[s] = c->key_for(g);
+                gt.c0[s] = yq + (size_t)gi * 2 * nr * N;
+                c->ledger.key_switches++;
+            }
+            c->timed("ks_inner", [&] { ks_accumulate_multi(c->dc, acc, gt, c->d_md, level, dn, c->st); });
+        }
+        c->release(dg);
     }
     if (id >= 0) qp_add(c->dc, acc, Y + (size_t)id * 2 * extw, level, c->st);
     uint64_t* md = c->alloc((size_t)2 * nr * N);

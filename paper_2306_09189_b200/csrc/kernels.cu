@@ -245,14 +245,18 @@ namespace {
 
 // one thread per (digit j, coefficient k): computes the centered
 // [x_i (Q_J/q_i)^-1]_{q_i} once and extends it to every target row.
-__global__ void k_modup_bconv(DevCtx c, const uint64_t* coef, const uint64_t* c1_ntt, uint64_t* digits,
-                              const ModUpDigit* tables, int level, int dn) {
-    const int ne = level + 1 + c.K;
-    const size_t total = (size_t)dn * c.N;
+__global__ void k_modup_bconv(DevCtx c, const uint64_t* coef_all, const uint64_t* c1_all, size_t src_stride,
+                              int nsrc, uint64_t* digits_all, const ModUpDigit* tables, int level, int dn) {
+    const int ne = level + 1 + c.K, nr = level + 1;
+    const size_t total = (size_t)nsrc * dn * c.N;
     RowMap rm{ne, level, c.L, 0};
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int j = (int)(i / c.N);
+        const int sj = (int)(i / c.N);
+        const int src = sj / dn, j = sj % dn;
         const int k = (int)(i % c.N);
+        const uint64_t* coef = coef_all + (size_t)src * nr * c.N;
+        const uint64_t* c1_ntt = c1_all + (size_t)src * src_stride;
+        uint64_t* digits = digits_all + (size_t)src * dn * ne * c.N;
         const ModUpDigit& T = tables[j];
         uint64_t v[kMaxAlpha];
         int neg = 0;
@@ -413,10 +417,11 @@ __global__ void __launch_bounds__(256) k_conv_mac(DevCtx c, uint64_t* acc, const
 
 }  // namespace
 
-void modup_bconv(const DevCtx& c, const uint64_t* coef, const uint64_t* c1_ntt, uint64_t* digits,
-                 const ModUpDigit* tables, int level, int dn, cudaStream_t st) {
+void modup_bconv(const DevCtx& c, const uint64_t* coef, const uint64_t* c1_ntt, size_t src_stride, int nsrc,
+                 uint64_t* digits, const ModUpDigit* tables, int level, int dn, cudaStream_t st) {
     ++g_launches;
-    k_modup_bconv<<<ew_blocks((size_t)dn * c.N), kEwThreads, 0, st>>>(c, coef, c1_ntt, digits, tables, level, dn);
+    k_modup_bconv<<<ew_blocks((size_t)nsrc * dn * c.N), kEwThreads, 0, st>>>(c, coef, c1_ntt, src_stride, nsrc,
+                                                                              digits, tables, level, dn);
 }
 void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* key, uint64_t* acc0,
                       uint64_t* acc1, uint32_t galois, int level, int dn, cudaStream_t st) {
@@ -607,29 +612,38 @@ __global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc
     }
 }
 
-__global__ void k_ks_accumulate(DevCtx c, uint64_t* acc, const uint64_t* D, const uint64_t* key, const uint64_t* c0,
-                                uint32_t g, const ModDownTable* md, int level, int dn) {
+template <int DN>
+__global__ void __launch_bounds__(256) k_ks_accumulate_multi(DevCtx c, uint64_t* acc, GiantTerms t,
+                                                             const ModDownTable* md, int level) {
     const int nr = level + 1, ne = nr + c.K;
     const int np = c.L + c.K;
     const size_t total = (size_t)ne * c.N;
     RowMap rm{ne, level, c.L, 0};
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < total / 2;
+         ip += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = ip * 2;
         const int u = (int)(i / c.N);
         const uint32_t k = (uint32_t)(i % c.N);
         const int p = row_prime(rm, u);
         const Prime pr = c.primes[p];
-        const uint32_t pk = perm_index(k, g, c.logN);
-        U128 s0{0, 0}, s1{0, 0};
-        for (int j = 0; j < dn; ++j) {
-            const uint64_t d = D[((size_t)j * ne + u) * c.N + pk];
-            mac(s0, d, key[(((size_t)j * 2 + 0) * np + p) * c.N + k]);
-            mac(s1, d, key[(((size_t)j * 2 + 1) * np + p) * c.N + k]);
+        U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
+        for (int g = 0; g < t.n; ++g) {
+            const uint32_t pk = perm_index(k, t.galois[g], c.logN);
+            ip_pair<DN>(t.digits + (size_t)g * DN * total, t.key[g], ne, np, u, p, k, pk, c.N, s0, s1);
+            if (u < nr) {
+                const ulonglong2 x = ld2(t.c0[g] + (size_t)u * c.N + (pk & ~1u));
+                const bool swp = pk & 1u;
+                add128(s0[0], mul_shoup(swp ? x.y : x.x, md->pmod[u], md->pmod_sh[u], pr.q));
+                add128(s0[1], mul_shoup(swp ? x.x : x.y, md->pmod[u], md->pmod_sh[u], pr.q));
+            }
         }
-        if (u < nr) add128(s0, mul_shoup(c0[(size_t)u * c.N + pk], md->pmod[u], md->pmod_sh[u], pr.q));
-        add128(s0, acc[i]);
-        add128(s1, acc[total + i]);
-        acc[i] = reduce128(s0.hi, s0.lo, pr);
-        acc[total + i] = reduce128(s1.hi, s1.lo, pr);
+        const ulonglong2 a0 = ld2(acc + i), a1 = ld2(acc + total + i);
+        add128(s0[0], a0.x);
+        add128(s0[1], a0.y);
+        add128(s1[0], a1.x);
+        add128(s1[1], a1.y);
+        st2(acc + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
+        st2(acc + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
     }
 }
 
@@ -692,6 +706,16 @@ void ks_accumulate(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const
 #define FHE_KS_ACC(D) k_ks_accumulate_t<D><<<blocks, 256, 0, st>>>(c, acc, digits, key, c0, galois, md, level)
     FHE_DN_SWITCH(dn, FHE_KS_ACC)
 #undef FHE_KS_ACC
+}
+
+void ks_accumulate_multi(const DevCtx& c, uint64_t* acc, const GiantTerms& t, const ModDownTable* md, int level,
+                         int dn, cudaStream_t st) {
+    const size_t total = (size_t)(level + 1 + c.K) * c.N;
+    ++g_launches;
+    const int blocks = ew_blocks(total / 2);
+#define FHE_KS_ACCM(D) k_ks_accumulate_multi<D><<<blocks, 256, 0, st>>>(c, acc, t, md, level)
+    FHE_DN_SWITCH(dn, FHE_KS_ACCM)
+#undef FHE_KS_ACCM
 }
 
 void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st) {

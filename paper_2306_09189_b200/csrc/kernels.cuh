@@ -24,6 +24,7 @@ struct RowMap {
     int level;
     int L;
     int skip_alpha;
+    int skip_dn;  // digits per source when several ModUps are batched (0: one source)
 };
 
 FHE_HD int row_prime(const RowMap& m, int u) { return u <= m.level ? u : m.L + (u - m.level - 1); }
@@ -132,10 +133,11 @@ void rescale_spread(const DevCtx& c, const uint64_t* tmp, uint64_t* spread, int 
 void rescale_finish(const DevCtx& c, uint64_t* out, const uint64_t* in, const uint64_t* spread, int level,
                     const uint64_t* qlinv, const uint64_t* qlinv_sh, cudaStream_t st);
 
-// ModUp FastBConv: coef = INTT(c1) (level+1 rows); digits [dn][ne][N];
-// own rows copied from c1_ntt (NTT domain), others in the coefficient domain.
-void modup_bconv(const DevCtx& c, const uint64_t* coef, const uint64_t* c1_ntt, uint64_t* digits,
-                 const ModUpDigit* tables, int level, int dn, cudaStream_t st);
+// ModUp FastBConv for nsrc sources: coef = INTT(c1) ([nsrc][level+1][N]);
+// digits [nsrc][dn][ne][N]; own rows copied from the NTT-domain c1 of each
+// source (c1_ntt + s * src_stride), the others in the coefficient domain.
+void modup_bconv(const DevCtx& c, const uint64_t* coef, const uint64_t* c1_ntt, size_t src_stride, int nsrc,
+                 uint64_t* digits, const ModUpDigit* tables, int level, int dn, cudaStream_t st);
 
 // acc_c[u][k] = sum_j D[j][u][perm_g(k)] key[j][c][prime(u)][k], ne = level+1+K rows
 void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* key, uint64_t* acc0,
@@ -170,6 +172,17 @@ void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms
 // acc_0 += IP_0(D, key, g) + [u <= l] P sigma_g(c0);  acc_1 += IP_1(D, key, g)   (acc = [2][ne][N])
 void ks_accumulate(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* key, const uint64_t* c0,
                    uint32_t galois, const ModDownTable* md, int level, int dn, cudaStream_t st);
+// Giant steps of the BSGS conv, one launch:
+// acc_0 += sum_g IP_0(D_g, key_g) + [u<=l] P sigma_g(c0_g);  acc_1 += sum_g IP_1(D_g, key_g)
+struct GiantTerms {
+    int n;
+    uint32_t galois[kMaxGiant];
+    const uint64_t* key[kMaxGiant];
+    const uint64_t* c0[kMaxGiant];  // [level+1][N] NTT
+    const uint64_t* digits;          // [n][dn][ne][N]
+};
+void ks_accumulate_multi(const DevCtx& c, uint64_t* acc, const GiantTerms& t, const ModDownTable* md, int level,
+                         int dn, cudaStream_t st);
 // acc += y over [2][ne][N] (QP basis)
 void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st);
 

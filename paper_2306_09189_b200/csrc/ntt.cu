@@ -33,6 +33,7 @@ __device__ __forceinline__ void fwd_pass(uint64_t (&v)[8], int G0, int logn, int
                                          const uint64_t* __restrict__ tw, const uint64_t* __restrict__ tws,
                                          uint64_t q) {
     constexpr int GS = 1 << R;
+    const uint64_t q2 = 2 * q;
     const int logt = logn - sigma0 - 1;  // distance of the first sub-stage is 2^logt
     const int logd = logt - (R - 1);     // element stride inside a group
 #pragma unroll
@@ -49,10 +50,12 @@ __device__ __forceinline__ void fwd_pass(uint64_t (&v)[8], int G0, int logn, int
                 if (k & half) continue;
                 const int widx = base + (k >> (R - rho));
                 const uint64_t w = __ldg(tw + widx), ws = __ldg(tws + widx);
-                const uint64_t U = v[g * GS + k];
-                const uint64_t V = mul_shoup(v[g * GS + k + half], w, ws, q);
-                v[g * GS + k] = add_mod(U, V, q);
-                v[g * GS + k + half] = sub_mod(U, V, q);
+                // Harvey's lazy CT butterfly: values live in [0, 4q) between stages
+                uint64_t U = v[g * GS + k];
+                U = U >= q2 ? U - q2 : U;
+                const uint64_t V = mul_shoup_lazy(v[g * GS + k + half], w, ws, q);  // [0, 2q)
+                v[g * GS + k] = U + V;
+                v[g * GS + k + half] = U - V + q2;
             }
         }
     }
@@ -76,6 +79,7 @@ __device__ __forceinline__ void inv_pass(uint64_t (&v)[8], int G0, int logt, int
                                          const uint64_t* __restrict__ tw, const uint64_t* __restrict__ tws,
                                          uint64_t q) {
     constexpr int GS = 1 << R;
+    const uint64_t q2 = 2 * q;
 #pragma unroll
     for (int g = 0; g < 8 / GS; ++g) {
         const int G = G0 + g;
@@ -90,9 +94,11 @@ __device__ __forceinline__ void inv_pass(uint64_t (&v)[8], int G0, int logt, int
                 if (k & half) continue;
                 const int widx = base + (k >> (rho + 1));
                 const uint64_t w = __ldg(tw + widx), ws = __ldg(tws + widx);
+                // Harvey's lazy GS butterfly: values live in [0, 2q) between stages
                 const uint64_t U = v[g * GS + k], V = v[g * GS + k + half];
-                v[g * GS + k] = add_mod(U, V, q);
-                v[g * GS + k + half] = mul_shoup(sub_mod(U, V, q), w, ws, q);
+                const uint64_t T = U + V;
+                v[g * GS + k] = T >= q2 ? T - q2 : T;
+                v[g * GS + k + half] = mul_shoup_lazy(U - V + q2, w, ws, q);
             }
         }
     }
@@ -163,7 +169,9 @@ __device__ __forceinline__ void inv_local(uint64_t* vec, int lt, int log_ntot, i
 
 __device__ __forceinline__ bool skip_row(const RowMap& rm, int row, int u) {
     if (!rm.skip_alpha) return false;
-    const int j = row / rm.rows_per_poly, lo = j * rm.skip_alpha;
+    int j = row / rm.rows_per_poly;
+    if (rm.skip_dn) j %= rm.skip_dn;
+    const int lo = j * rm.skip_alpha;
     const int hi = min(lo + rm.skip_alpha, rm.level + 1);
     return u >= lo && u < hi;
 }
@@ -237,7 +245,17 @@ __global__ void __launch_bounds__(256) k_ntt_rows(DevCtx c, uint64_t* data, RowM
                              c.itw_sh + (size_t)p * c.N, q);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < BPC * B; i += blockDim.x) a[i] = sm[(i / B) * PB + pad(i % B)];
+    if (!INVERSE) {
+        // forward transform ends here: normalise [0, 4q) -> [0, q)
+        const uint64_t q2 = 2 * q;
+        for (int i = threadIdx.x; i < BPC * B; i += blockDim.x) {
+            uint64_t x = sm[(i / B) * PB + pad(i % B)];
+            x = x >= q2 ? x - q2 : x;
+            a[i] = x >= q ? x - q : x;
+        }
+    } else {
+        for (int i = threadIdx.x; i < BPC * B; i += blockDim.x) a[i] = sm[(i / B) * PB + pad(i % B)];
+    }
 }
 
 template <int LOG_N1, int LOG_B>
