@@ -196,7 +196,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     ctx.prof_enable(False)
     launches = ctx.ledger()["kernel_launches"] - launches0
-    classes = ["conv_mac", "ks_multi", "pt_matvec", "ntt", "ks_inner", "modup_bconv", "moddown", "rescale"]
+    classes = ["conv_mac", "ks_multi", "pt_matvec", "ntt", "ntt_modup", "ntt_moddown", "ks_inner", "moddown", "rescale"]
     prof = {c: ctx.prof_get(c) for c in classes}
     ms_max = max_over_ranks(ms)
 

@@ -89,6 +89,9 @@ int fhe_timer_stop(fhe_ctx* ctx, float* ms); /* synchronises; ms since fhe_timer
 int fhe_prof_enable(fhe_ctx* ctx, int on);
 int fhe_prof_get(fhe_ctx* ctx, const char* kernel_class, double* total_ms, uint64_t* launches);
 int fhe_prof_reset(fhe_ctx* ctx);
+/* micro-benchmark of the NTT kernels: nrows rows at the top level's primes,
+ * `iters` transforms; *ms = device time per transform launch */
+int fhe_bench_ntt(fhe_ctx* ctx, int nrows, int inverse, int iters, float* ms);
 /* cudaProfilerStart/Stop (scopes ncu --profile-from-start off captures) */
 int fhe_profiler_range(int on);
 /* replaces: Engine::ledger() emu.hpp:137-138, CostLedger::reset emu.hpp:77-88 */

@@ -49,6 +49,7 @@ SIGNATURES = [
     ("fhe_prof_get", C.c_int, [vp, C.c_char_p, C.POINTER(C.c_double), u64p]),
     ("fhe_prof_reset", C.c_int, [vp]),
     ("fhe_profiler_range", C.c_int, [C.c_int]),
+    ("fhe_bench_ntt", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     ("fhe_ledger_get", C.c_int, [vp, C.POINTER(FheLedger)]),
     ("fhe_ledger_reset", C.c_int, [vp]),
     ("fhe_ledger_amounts", C.c_int, [vp, u64p, C.c_size_t, C.POINTER(C.c_size_t)]),

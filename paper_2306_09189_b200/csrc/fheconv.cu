@@ -225,11 +225,9 @@ void modup_batch(fhe_ctx* c, const uint64_t* c1, size_t stride, int nsrc, int le
     ck(cudaMemcpy2DAsync(coef, rowsw * 8, c1, stride * 8, rowsw * 8, nsrc, cudaMemcpyDeviceToDevice, c->st),
        "memcpy2d");
     c->timed("ntt", [&] { ntt_inverse(c->dc, coef, nsrc * nr, qmap(c, level), c->st); });
-    c->timed("modup_bconv", [&] {
-        modup_bconv(c->dc, coef, c1, stride, nsrc, digits, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
-    });
-    c->timed("ntt", [&] {
-        ntt_forward(c->dc, digits, nsrc * dn * ne, RowMap{ne, level, c->L, c->alpha, dn}, c->st);
+    (void)ne;
+    c->timed("ntt_modup", [&] {
+        ntt_modup(c->dc, digits, coef, c1, stride, nsrc, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
     });
     c->release(coef);
     c->ledger.modups += nsrc;
@@ -246,10 +244,8 @@ void moddown(fhe_ctx* c, const uint64_t* acc, int level, int npoly, uint64_t* ou
     uint64_t* conv = c->alloc((size_t)npoly * nr * c->N);
     c->timed("moddown", [&] { gather_special(c->dc, pc, acc, level, npoly, c->st); });
     c->timed("ntt", [&] { ntt_inverse(c->dc, pc, npoly * c->K, RowMap{c->K, -1, c->L, 0}, c->st); });
-    c->timed("moddown", [&] { moddown_bconv(c->dc, pc, conv, c->d_md, level, npoly, c->st); });
-    c->timed("ntt", [&] { ntt_forward(c->dc, conv, npoly * nr, qmap(c, level), c->st); });
-    c->timed("moddown",
-             [&] { moddown_finish(c->dc, out, acc, conv, c->d_md, level, npoly, add_src, g, c->st); });
+    c->timed("ntt_moddown",
+             [&] { ntt_moddown(c->dc, conv, pc, acc, out, c->d_md, level, npoly, add_src, g, c->st); });
     c->release(pc);
     c->release(conv);
     c->ledger.moddowns += npoly;
@@ -593,7 +589,25 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
         t.gmask[b] = any;
         if (g != 1 && any) c->ledger.key_switches++;
     }
-    c->timed("ks_multi", [&] { ks_multi(c->dc, XT, dsrc, ct->d, t, c->d_md, level, dn, c->st); });
+    {
+        KsStream ks{};
+        ks.digits = dsrc;
+        ks.digit_stride = 0;
+        ks.out = XT;
+        for (int b = 0; b < B.nb; ++b) {
+            if (!t.gmask[b]) continue;
+            if (t.galois[b] == 1) {
+                c->timed("ks_multi", [&] { identity_term(c->dc, XT + (size_t)b * 2 * extw, ct->d, c->d_md, level, c->st); });
+                continue;
+            }
+            ks.galois[ks.n] = t.galois[b];
+            ks.key[ks.n] = t.key[b];
+            ks.c0[ks.n] = ct->c0();
+            ks.slot[ks.n] = b;
+            ks.n++;
+        }
+        c->timed("ks_multi", [&] { ks_stream(c->dc, ks, 0, c->d_md, level, dn, c->st); });
+    }
     for (int g0 = 0; g0 < B.ngi; g0 += kMaxGiant) {
         t.ngi = std::min(kMaxGiant, B.ngi - g0);
         t.g0 = g0;
@@ -643,18 +657,20 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
                 modup_batch(c, c1, (size_t)2 * nr * N, e - s + 1, level, dg + (size_t)s * dw);
                 s = e + 1;
             }
-            GiantTerms gt{};
-            gt.n = n;
-            gt.digits = dg;
+            KsStream ks{};
+            ks.n = n;
+            ks.digits = dg;
+            ks.digit_stride = dw;
+            ks.out = acc;
             for (int s = 0; s < n; ++s) {
                 const int gi = giants[a + s];
                 const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[gi]));
-                gt.galois[s] = g;
-                gt.key[s] = c->key_for(g);
-                gt.c0[s] = yq + (size_t)gi * 2 * nr * N;
+                ks.galois[s] = g;
+                ks.key[s] = c->key_for(g);
+                ks.c0[s] = yq + (size_t)gi * 2 * nr * N;
                 c->ledger.key_switches++;
             }
-            c->timed("ks_inner", [&] { ks_accumulate_multi(c->dc, acc, gt, c->d_md, level, dn, c->st); });
+            c->timed("ks_inner", [&] { ks_stream(c->dc, ks, 1, c->d_md, level, dn, c->st); });
         }
         c->release(dg);
     }
@@ -907,6 +923,29 @@ int fhe_prof_get(fhe_ctx* c, const char* cls, double* total_ms, uint64_t* launch
         auto it = c->prof.find(cls);
         if (total_ms) *total_ms = it == c->prof.end() ? 0.0 : it->second.ms;
         if (launches) *launches = it == c->prof.end() ? 0 : it->second.n;
+    });
+}
+
+int fhe_bench_ntt(fhe_ctx* c, int nrows, int inverse, int iters, float* ms) {
+    return guard(c, [&] {
+        const int level = c->L - 1;
+        uint64_t* d = c->alloc((size_t)nrows * c->N);
+        ck(cudaMemsetAsync(d, 0, (size_t)nrows * c->N * 8, c->st), "memset");
+        const RowMap rm{level + 1, level, c->L, 0};
+        for (int i = 0; i < 2; ++i)
+            inverse ? ntt_inverse(c->dc, d, nrows, rm, c->st) : ntt_forward(c->dc, d, nrows, rm, c->st);
+        cudaEvent_t a = c->get_event(), b = c->get_event();
+        cudaEventRecord(a, c->st);
+        for (int i = 0; i < iters; ++i)
+            inverse ? ntt_inverse(c->dc, d, nrows, rm, c->st) : ntt_forward(c->dc, d, nrows, rm, c->st);
+        cudaEventRecord(b, c->st);
+        ck(cudaEventSynchronize(b), "sync");
+        float t = 0;
+        cudaEventElapsedTime(&t, a, b);
+        *ms = t / iters;
+        c->ev_pool.push_back(a);
+        c->ev_pool.push_back(b);
+        c->release(d);
     });
 }
 

@@ -462,6 +462,23 @@ __device__ __forceinline__ ulonglong2 ld2(const uint64_t* p) { return __ldg(rein
 __device__ __forceinline__ ulonglong2 ld2cs(const uint64_t* p) {
     return __ldcs(reinterpret_cast<const ulonglong2*>(p));
 }
+// volatile (non-reorderable) 16-byte loads: issued in program order so that a
+// whole batch of independent loads is in flight before the first use
+__device__ __forceinline__ ulonglong2 vld2_nc(const uint64_t* p) {
+    ulonglong2 r;
+    asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ ulonglong2 vld2_cs(const uint64_t* p) {
+    ulonglong2 r;
+    asm volatile("ld.global.cs.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint64_t vld_cs(const uint64_t* p) {
+    uint64_t r;
+    asm volatile("ld.global.cs.u64 %0, [%1];" : "=l"(r) : "l"(p));
+    return r;
+}
 __device__ __forceinline__ void st2(uint64_t* p, uint64_t a, uint64_t b) {
     *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(a, b);
 }
@@ -475,10 +492,11 @@ __device__ __forceinline__ void ip_pair(const uint64_t* __restrict__ D, const ui
     ulonglong2 d[DN], k0[DN], k1[DN];
 #pragma unroll
     for (int j = 0; j < DN; ++j) {
-        d[j] = ld2(D + ((size_t)j * ne + u) * N + base);
-        k0[j] = ld2cs(key + (((size_t)j * 2 + 0) * np + p) * N + k);
-        k1[j] = ld2cs(key + (((size_t)j * 2 + 1) * np + p) * N + k);
+        k0[j] = vld2_cs(key + (((size_t)j * 2 + 0) * np + p) * N + k);
+        k1[j] = vld2_cs(key + (((size_t)j * 2 + 1) * np + p) * N + k);
     }
+#pragma unroll
+    for (int j = 0; j < DN; ++j) d[j] = vld2_nc(D + ((size_t)j * ne + u) * N + base);
 #pragma unroll
     for (int j = 0; j < DN; ++j) {
         const uint64_t da = swp ? d[j].y : d[j].x, db = swp ? d[j].x : d[j].y;
@@ -486,6 +504,119 @@ __device__ __forceinline__ void ip_pair(const uint64_t* __restrict__ D, const ui
         mac(s0[1], db, k0[j].y);
         mac(s1[0], da, k1[j].x);
         mac(s1[1], db, k1[j].y);
+    }
+}
+
+// ---- cp.async (LDGSTS) helpers: per-thread asynchronous 16-byte copies to smem
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Streaming key switch. Each thread owns a coefficient pair
+// of one extended row and walks the term list; the 2*DN key words and DN
+// gathered digit words of term t+1 are copied into a per-thread shared-memory
+// stage with cp.async while term t is multiplied out, so every thread keeps
+// ~700 bytes of the key stream in flight without holding them in registers.
+// MODE 0 (baby steps): XT[slot_t] = (IP_0 + [u<=l] P sigma_t(c0), IP_1) per term.
+// MODE 1 (giant steps): acc += sum_t (IP_0 + [u<=l] P sigma_t(c0_t), IP_1).
+constexpr int kStreamThreads = 128;
+template <int DN, int MODE>
+__global__ void __launch_bounds__(kStreamThreads) k_ks_stream(DevCtx c, KsStream a, const ModDownTable* md,
+                                                              int level) {
+    extern __shared__ ulonglong2 sbuf[];  // [2 stages][3*DN][kStreamThreads]
+    const int nr = level + 1, ne = nr + c.K;
+    const int np = c.L + c.K;
+    const size_t total = (size_t)ne * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    const int tid = threadIdx.x;
+    auto slot = [&](int stage, int w) -> ulonglong2* { return sbuf + ((size_t)stage * 3 * DN + w) * kStreamThreads + tid; };
+    for (size_t ip = blockIdx.x * (size_t)blockDim.x + tid; ip < total / 2; ip += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = ip * 2;
+        const int u = (int)(i / c.N);
+        const uint32_t k = (uint32_t)(i % c.N);
+        const int p = row_prime(rm, u);
+        const Prime pr = c.primes[p];
+        const bool qrow = u < nr;
+        const uint64_t pm = qrow ? md->pmod[u] : 0, pms = qrow ? md->pmod_sh[u] : 0;
+        auto issue = [&](int t, int stage) {
+            const uint32_t pk = perm_index(k, a.galois[t], c.logN);
+            const uint64_t* key = a.key[t];
+            const uint64_t* D = a.digits + (size_t)t * a.digit_stride;
+#pragma unroll
+            for (int j = 0; j < DN; ++j) {
+                cp_async16(slot(stage, 3 * j + 0), key + (((size_t)j * 2 + 0) * np + p) * c.N + k);
+                cp_async16(slot(stage, 3 * j + 1), key + (((size_t)j * 2 + 1) * np + p) * c.N + k);
+                cp_async16(slot(stage, 3 * j + 2), D + ((size_t)j * ne + u) * c.N + (pk & ~1u));
+            }
+            cp_async_commit();
+        };
+        U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
+        issue(0, 0);
+        for (int t = 0; t < a.n; ++t) {
+            if (t + 1 < a.n)
+                issue(t + 1, (t + 1) & 1);
+            else
+                cp_async_commit();  // empty group keeps the wait count uniform
+            cp_async_wait<1>();
+            const int st = t & 1;
+            const uint32_t pk = perm_index(k, a.galois[t], c.logN);
+            const bool swp = pk & 1u;
+            if (MODE == 0) {
+                s0[0] = s0[1] = s1[0] = s1[1] = U128{0, 0};
+            }
+#pragma unroll
+            for (int j = 0; j < DN; ++j) {
+                const ulonglong2 k0 = *slot(st, 3 * j + 0), k1 = *slot(st, 3 * j + 1), d = *slot(st, 3 * j + 2);
+                const uint64_t da = swp ? d.y : d.x, db = swp ? d.x : d.y;
+                mac(s0[0], da, k0.x);
+                mac(s0[1], db, k0.y);
+                mac(s1[0], da, k1.x);
+                mac(s1[1], db, k1.y);
+            }
+            if (qrow) {
+                const ulonglong2 x = ld2(a.c0[t] + (size_t)u * c.N + (pk & ~1u));
+                add128(s0[0], mul_shoup(swp ? x.y : x.x, pm, pms, pr.q));
+                add128(s0[1], mul_shoup(swp ? x.x : x.y, pm, pms, pr.q));
+            }
+            if (MODE == 0) {
+                uint64_t* xt = a.out + (size_t)a.slot[t] * 2 * total;
+                st2(xt + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
+                st2(xt + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
+            }
+        }
+        if (MODE == 1) {
+            const ulonglong2 a0 = ld2(a.out + i), a1 = ld2(a.out + total + i);
+            add128(s0[0], a0.x);
+            add128(s0[1], a0.y);
+            add128(s1[0], a1.x);
+            add128(s1[1], a1.y);
+            st2(a.out + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
+            st2(a.out + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
+        }
+    }
+}
+
+// XT[slot] = P ct (identity baby step) for q rows, 0 for the special rows
+__global__ void k_identity_term(DevCtx c, uint64_t* xt, const uint64_t* X, const ModDownTable* md, int level) {
+    const int nr = level + 1, ne = nr + c.K;
+    const size_t total = (size_t)ne * c.N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int u = (int)(i / c.N);
+        const size_t k = i % c.N;
+        if (u < nr) {
+            const uint64_t q = c.primes[u].q;
+            xt[i] = mul_shoup(X[(size_t)u * c.N + k], md->pmod[u], md->pmod_sh[u], q);
+            xt[total + i] = mul_shoup(X[((size_t)nr + u) * c.N + k], md->pmod[u], md->pmod_sh[u], q);
+        } else {
+            xt[i] = 0;
+            xt[total + i] = 0;
+        }
     }
 }
 
@@ -553,14 +684,14 @@ __global__ void __launch_bounds__(256) k_pt_matvec(DevCtx c, uint64_t* Y, const 
         for (int b = 0; b < t.nb; ++b) {
             const uint32_t mask = t.gmask[b];
             if (mask == 0) continue;
-            const uint64_t x0 = __ldcs(XT + (size_t)b * 2 * total + i);
-            const uint64_t x1 = __ldcs(XT + (size_t)b * 2 * total + total + i);
             uint64_t w[NG];
 #pragma unroll
             for (int g = 0; g < NG; ++g)
                 w[g] = (g < t.ngi && ((mask >> g) & 1u))
-                           ? __ldcs(t.pts + (((size_t)(t.g0 + g) * t.nb_total + b) * ne) * c.N + i)
+                           ? vld_cs(t.pts + (((size_t)(t.g0 + g) * t.nb_total + b) * ne) * c.N + i)
                            : 0;
+            const uint64_t x0 = vld_cs(XT + (size_t)b * 2 * total + i);
+            const uint64_t x1 = vld_cs(XT + (size_t)b * 2 * total + total + i);
 #pragma unroll
             for (int g = 0; g < NG; ++g) {
                 mac(a0[g], w[g], x0);
@@ -613,7 +744,7 @@ __global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc
 }
 
 template <int DN>
-__global__ void __launch_bounds__(256) k_ks_accumulate_multi(DevCtx c, uint64_t* acc, GiantTerms t,
+__global__ void __launch_bounds__(256, 1) k_ks_accumulate_multi(DevCtx c, uint64_t* acc, GiantTerms t,
                                                              const ModDownTable* md, int level) {
     const int nr = level + 1, ne = nr + c.K;
     const int np = c.L + c.K;
@@ -680,6 +811,34 @@ void ks_multi(const DevCtx& c, uint64_t* XT, const uint64_t* digits, const uint6
     ++g_launches;
     FHE_DN_SWITCH(dn, FHE_KS_MULTI)
 #undef FHE_KS_MULTI
+}
+
+void ks_stream(const DevCtx& c, const KsStream& a, int mode, const ModDownTable* md, int level, int dn,
+               cudaStream_t st) {
+    if (a.n <= 0) return;
+    const size_t total = (size_t)(level + 1 + c.K) * c.N;
+    const size_t smem = (size_t)2 * 3 * dn * kStreamThreads * sizeof(ulonglong2);
+    int blocks = (int)((total / 2 + kStreamThreads - 1) / kStreamThreads);
+    blocks = blocks < 148 * 8 ? blocks : 148 * 8;
+    ++g_launches;
+#define FHE_KSS(D)                                                                                             \
+    do {                                                                                                       \
+        if (mode == 0) {                                                                                       \
+            cudaFuncSetAttribute(k_ks_stream<D, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+            k_ks_stream<D, 0><<<blocks, kStreamThreads, smem, st>>>(c, a, md, level);                          \
+        } else {                                                                                               \
+            cudaFuncSetAttribute(k_ks_stream<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+            k_ks_stream<D, 1><<<blocks, kStreamThreads, smem, st>>>(c, a, md, level);                          \
+        }                                                                                                      \
+    } while (0)
+    FHE_DN_SWITCH(dn, FHE_KSS)
+#undef FHE_KSS
+}
+
+void identity_term(const DevCtx& c, uint64_t* xt, const uint64_t* ct, const ModDownTable* md, int level,
+                   cudaStream_t st) {
+    ++g_launches;
+    k_identity_term<<<ew_blocks((size_t)(level + 1 + c.K) * c.N), kEwThreads, 0, st>>>(c, xt, ct, md, level);
 }
 
 void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms& t, int level, cudaStream_t st) {

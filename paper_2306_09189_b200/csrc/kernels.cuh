@@ -89,6 +89,23 @@ struct BabyTerms {
     const uint64_t* pts;             // [ngi_total][nb_total][ne][N]
 };
 
+// Operands of the fused NTT modes (ntt.cu)
+struct NttFuse {
+    // ModUp: digits of nsrc sources from their INTT'd rows
+    const uint64_t* coef;   // [nsrc][level+1][N] coefficient domain
+    const uint64_t* c1;     // NTT-domain input of source s at c1 + s * c1_stride
+    size_t c1_stride;
+    const ModUpDigit* mu;   // [dnum] tables of the level
+    int dn;
+    // ModDown
+    const uint64_t* pc;     // [npoly][K][N] INTT'd special-prime rows
+    const ModDownTable* md;
+    const uint64_t* acc;    // [npoly][ne][N]
+    uint64_t* out;          // [npoly][level+1][N]
+    const uint64_t* add_src;
+    uint32_t galois;
+};
+
 // --------------------------------------------------------------- launchers
 // total number of kernels enqueued by this library (for the bench's gpu_launches)
 uint64_t launches_total();
@@ -96,6 +113,14 @@ uint64_t launches_total();
 // All launchers enqueue on `st` and never synchronise.
 void ntt_forward(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);
 void ntt_inverse(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);
+// ModUp FastBConv fused into the forward NTT: digits = [nsrc][dn][ne][N]
+void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const uint64_t* c1, size_t c1_stride,
+               int nsrc, const ModUpDigit* tables, int level, int dn, cudaStream_t st);
+// ModDown FastBConv + finish fused into the forward NTT of conv (scratch [npoly][level+1][N]):
+// out[p] = (acc[p] - NTT(FastBConv_P->Q(pcoef[p]))) P^-1 (+ sigma_g(add_src) on poly 0)
+void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, uint64_t* out,
+                 const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
+                 cudaStream_t st);
 
 void reduce_signed_rows(const DevCtx& c, const int64_t* coef, uint64_t* out, int nrows, const RowMap& rm,
                         cudaStream_t st);
@@ -183,6 +208,24 @@ struct GiantTerms {
 };
 void ks_accumulate_multi(const DevCtx& c, uint64_t* acc, const GiantTerms& t, const ModDownTable* md, int level,
                          int dn, cudaStream_t st);
+// Streaming key-switch term list (k_ks_stream): term t uses Galois element
+// galois[t], key[t], digits + t * digit_stride and the NTT-domain c0[t].
+struct KsStream {
+    int n;
+    uint32_t galois[kMaxBaby];
+    const uint64_t* key[kMaxBaby];
+    const uint64_t* c0[kMaxBaby];
+    int slot[kMaxBaby];        // mode 0: output slot in out = [slots][2][ne][N]
+    const uint64_t* digits;
+    size_t digit_stride;
+    uint64_t* out;             // mode 0: XT; mode 1: acc [2][ne][N]
+};
+// mode 0: XT[slot_t] = key switch of term t; mode 1: acc += sum_t key switch of term t
+void ks_stream(const DevCtx& c, const KsStream& a, int mode, const ModDownTable* md, int level, int dn,
+               cudaStream_t st);
+// xt = P ct (q rows), 0 (special rows): the identity baby step
+void identity_term(const DevCtx& c, uint64_t* xt, const uint64_t* ct, const ModDownTable* md, int level,
+                   cudaStream_t st);
 // acc += y over [2][ne][N] (QP basis)
 void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st);
 

@@ -10,7 +10,7 @@ img = rng.uniform(-1,1,c*m*m); w = rng.uniform(-1,1,c*c*k*k)
 layer = ctx.conv_layer(c,c,m,k,w); ctx.gen_galois_keys(layer.steps())
 ct = ctx.encrypt(ctx.encode(img), 9000)
 out = ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level-1), 1)
-classes = ["conv_mac", "ks_multi", "pt_matvec", "ntt", "ks_inner", "modup_bconv", "moddown", "rescale"]
+classes = ["conv_mac", "ks_multi", "pt_matvec", "ntt", "ntt_modup", "ntt_moddown", "ks_inner", "moddown", "rescale"]
 for ap in (1,2,3,4):
     for _ in range(3): ctx.conv2d_into(ct, layer, ap, out)
     ctx.synchronize()
