@@ -328,28 +328,31 @@ __global__ void __launch_bounds__(256) k_ntt_cols_bconv(DevCtx c, uint64_t* data
         u_begin = blockIdx.z * tg_size;
         u_end = min(u_begin + tg_size, nr);
     }
-    // load + first half of the conversion (once per tile)
-    uint64_t v[EPT][KA];
-    int neg[EPT];
+    // load + first half of the conversion (once per tile), kept in shared
+    // memory (per-thread private slots) so the NTT passes keep a low register count
+    extern __shared__ uint64_t dyn[];
+    uint64_t(*sv)[EPT][256] = reinterpret_cast<uint64_t(*)[EPT][256]>(dyn);  // [KA][EPT][256]
+    uint8_t(*sneg)[256] = reinterpret_cast<uint8_t(*)[256]>(dyn + KA * EPT * 256);
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
         const int i = threadIdx.x + e * 256;
         const size_t pos = (size_t)(i / C) * B + col0 + i % C;
-        neg[e] = 0;
+        int neg = 0;
 #pragma unroll
         for (int a = 0; a < KA; ++a) {
+            uint64_t v = 0;
             if (a < nsrc_rows) {
                 const int qi = MODE == FUSE_MODUP ? lo + a : c.L + a;
                 const uint64_t q = c.primes[qi].q;
                 const uint64_t x = srcrows[(size_t)a * c.N + pos];
                 const uint64_t w = MODE == FUSE_MODUP ? T->inv[a] : fz.md->pinv[a];
                 const uint64_t ws = MODE == FUSE_MODUP ? T->inv_sh[a] : fz.md->pinv_sh[a];
-                v[e][a] = mul_shoup(x, w, ws, q);
-                neg[e] += v[e][a] > (q >> 1);
-            } else {
-                v[e][a] = 0;
+                v = mul_shoup(x, w, ws, q);
+                neg += v > (q >> 1);
             }
+            sv[a][e][threadIdx.x] = v;
         }
+        sneg[e][threadIdx.x] = (uint8_t)neg;
     }
     const int cc = threadIdx.x / TPC, lt = threadIdx.x % TPC;
     for (int u = u_begin; u < u_end; ++u) {
@@ -375,14 +378,15 @@ __global__ void __launch_bounds__(256) k_ntt_cols_bconv(DevCtx c, uint64_t* data
             hats[a] = MODE == FUSE_MODUP ? T->hat_sh[u][a] : fz.md->hat_sh[p][a];
         }
         const uint64_t corr = MODE == FUSE_MODUP ? T->qj[u] : fz.md->pmod[p];
-#pragma unroll
+#pragma unroll 2
         for (int e = 0; e < EPT; ++e) {
             const int i = threadIdx.x + e * 256;
             uint64_t y = 0;
 #pragma unroll
             for (int a = 0; a < KA; ++a)
-                if (a < nsrc_rows) y = add_mod(y, mul_shoup(v[e][a], hat[a], hats[a], t), t);
-            for (int n = 0; n < neg[e]; ++n) y = sub_mod(y, corr, t);  // centered lift
+                if (a < nsrc_rows) y = add_mod(y, mul_shoup(sv[a][e][threadIdx.x], hat[a], hats[a], t), t);
+            const int neg = sneg[e][threadIdx.x];
+            for (int n = 0; n < neg; ++n) y = sub_mod(y, corr, t);  // centered lift
             sm[(i % C) * PN + pad(i / C)] = y;
         }
         __syncthreads();
@@ -474,12 +478,18 @@ void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, 
             // target groups: enough CTAs to fill the GPU, few enough to amortise the conversion
             const int ngroups_src = nrows / rm.rows_per_poly;
             const int tiles = B / C;
-            int tg = 1;
-            while (tiles * ngroups_src * tg < 2 * 148 && tg < rm.rows_per_poly) ++tg;
-            const int tg_size = (rm.rows_per_poly + tg - 1) / tg;
-            tg = (rm.rows_per_poly + tg_size - 1) / tg_size;
+            // ~4 target rows per CTA: enough CTAs to overlap, the conversion amortised 4x
+            const int tg_size = rm.rows_per_poly < 4 ? rm.rows_per_poly : 4;
+            const int tg = (rm.rows_per_poly + tg_size - 1) / tg_size;
+            (void)tiles;
             const dim3 gc(tiles, ngroups_src, tg);
-#define FHE_BCONV(MODE, KA) k_ntt_cols_bconv<LOG_N1, C, MODE, KA><<<gc, 256, 0, st>>>(c, data, rm, fz, tg_size)
+#define FHE_BCONV(MODE, KA)                                                                              \
+    do {                                                                                                 \
+        const int dsm = (KA) * (N1 * C / 256) * 256 * 8 + (N1 * C / 256) * 256;                          \
+        cudaFuncSetAttribute(k_ntt_cols_bconv<LOG_N1, C, MODE, KA>,                                      \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);                          \
+        k_ntt_cols_bconv<LOG_N1, C, MODE, KA><<<gc, 256, dsm, st>>>(c, data, rm, fz, tg_size);           \
+    } while (0)
 #define FHE_BCONV_K(MODE)             \
     switch (c.K) {                    \
         case 1: FHE_BCONV(MODE, 1); break; \
