@@ -919,8 +919,8 @@ static void conv_accumulate(const ck_ctx* ck, int level, const uint64_t* pt, con
  * orient 4: baby steps = shifts, giant steps = channel rotations.
  * With X_b = rot_b(ct) kept in the QP basis (never ModDown'd),
  *   Y_g = sum_b rot_{-g}(pt_{g,b}) * X_b                      (QP accumulators)
- *   out = Rescale(ModDown(Y_0 + sum_{g != 0} KS_g(ModDown(Y_g))))
- * where KS_g(Y) = IP(ModUp(Y.c1), key_g) + P sigma_g(Y.c0) (QP). */
+ *   out = Rescale(ModDown(Y_0 + sum_{g != 0} KS_g(Y_g)))
+ * where KS_g(Y) = (IP_0(ModUp(ModDown(Y.c1)), key_g) + sigma_g(Y.c0), IP_1(...)) in QP. */
 static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,
                      const double* filt, int orient, uint64_t* out, double* out_scale) {
     const size_t N = ck->N, s = N / 2, block = (size_t)m * m;
@@ -987,7 +987,7 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
     uint64_t* acc0 = calloc(extw, 8);
     uint64_t* acc1 = calloc(extw, 8);
     uint64_t* yq = malloc(ctw * 8);
-    uint64_t* perm = malloc((size_t)nr * N * 8);
+    uint64_t* perm = malloc(extw * 8);
     for (int gi = 0; gi < ngi; gi++) {
         int any = 0;
         for (int bi = 0; bi < nb; bi++) any |= nonempty[gi * nb + bi];
@@ -1004,16 +1004,17 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
             }
             continue;
         }
-        ck_moddown(ck, y, level, yq);
+        /* only Y.c1 is brought down to Q for the decomposition; Y.c0 is already
+         * P-scaled in the QP basis and enters the accumulator directly (the final
+         * ModDown performs its rounding), saving a ModDown per giant step */
         ck_moddown(ck, y + extw, level, yq + (size_t)nr * N);
         ck_modup(ck, yq + (size_t)nr * N, level, dsrc);
         ck_inner_product(ck, dsrc, level, cache_get(ck, &kc, g), g, ip0, ip1);
-        for (int t = 0; t < nr; t++) ck_automorph_ntt(ck, yq + (size_t)t * N, perm + (size_t)t * N, g);
+        for (int t = 0; t < ne; t++) ck_automorph_ntt(ck, y + (size_t)t * N, perm + (size_t)t * N, g);
         for (int u = 0; u < ne; u++) {
             const uint64_t q = ck->q[ext_prime(ck, level, u)];
             for (size_t k = 0; k < N; k++) {
-                uint64_t t0 = ip0[(size_t)u * N + k];
-                if (u < nr) t0 = addm(t0, ck_mulmod(Pmod[u], perm[(size_t)u * N + k], q), q);
+                const uint64_t t0 = addm(ip0[(size_t)u * N + k], perm[(size_t)u * N + k], q);
                 acc0[(size_t)u * N + k] = addm(acc0[(size_t)u * N + k], t0, q);
                 acc1[(size_t)u * N + k] = addm(acc1[(size_t)u * N + k], ip1[(size_t)u * N + k], q);
             }

@@ -237,18 +237,24 @@ void modup_batch(fhe_ctx* c, const uint64_t* c1, size_t stride, int nsrc, int le
 void modup(fhe_ctx* c, const uint64_t* c1, int level, uint64_t* digits) { modup_batch(c, c1, 0, 1, level, digits); }
 
 // out[p] = ModDown(acc[p]) (+ sigma_g(add_src) on poly 0)
-void moddown(fhe_ctx* c, const uint64_t* acc, int level, int npoly, uint64_t* out, const uint64_t* add_src,
-             uint32_t g) {
+void moddown_strided(fhe_ctx* c, const uint64_t* acc, size_t acc_stride, int level, int npoly, uint64_t* out,
+                     const uint64_t* add_src, uint32_t g) {
     const int nr = level + 1;
     uint64_t* pc = c->alloc((size_t)npoly * c->K * c->N);
     uint64_t* conv = c->alloc((size_t)npoly * nr * c->N);
-    c->timed("moddown", [&] { gather_special(c->dc, pc, acc, level, npoly, c->st); });
+    c->timed("moddown", [&] { gather_special(c->dc, pc, acc, acc_stride, level, npoly, c->st); });
     c->timed("ntt", [&] { ntt_inverse(c->dc, pc, npoly * c->K, RowMap{c->K, -1, c->L, 0}, c->st); });
     c->timed("ntt_moddown",
-             [&] { ntt_moddown(c->dc, conv, pc, acc, out, c->d_md, level, npoly, add_src, g, c->st); });
+             [&] { ntt_moddown(c->dc, conv, pc, acc, acc_stride, out, c->d_md, level, npoly, add_src, g, c->st); });
     c->release(pc);
     c->release(conv);
     c->ledger.moddowns += npoly;
+}
+
+// out[p] = ModDown(acc[p]) for contiguous [npoly][ne][N] accumulators
+void moddown(fhe_ctx* c, const uint64_t* acc, int level, int npoly, uint64_t* out, const uint64_t* add_src,
+             uint32_t g) {
+    moddown_strided(c, acc, (size_t)c->ne_at(level) * c->N, level, npoly, out, add_src, g);
 }
 
 // out = rotation of ct by Galois g given the ModUp digits of ct.c1
@@ -633,13 +639,15 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
         else
             giants.push_back(gi);
     }
-    uint64_t* yq = c->alloc((size_t)B.ngi * 2 * nr * N);
-    // batched ModDown over contiguous runs of giant accumulators
+    // giant steps: only Y_g.c1 is brought down to Q (for the decomposition);
+    // Y_g.c0 stays P-scaled in QP and enters the accumulator directly
+    uint64_t* yq = c->alloc((size_t)B.ngi * nr * N);  // [ngi][nr][N] = ModDown(Y_g.c1)
     for (size_t a = 0; a < giants.size();) {
         size_t b = a;
         while (b + 1 < giants.size() && giants[b + 1] == giants[b] + 1) ++b;
         const int first = giants[a], cnt = giants[b] - giants[a] + 1;
-        moddown(c, Y + (size_t)first * 2 * extw, level, 2 * cnt, yq + (size_t)first * 2 * nr * N, nullptr, 1);
+        moddown_strided(c, Y + (size_t)first * 2 * extw + extw, 2 * extw, level, cnt, yq + (size_t)first * nr * N,
+                        nullptr, 1);
         a = b + 1;
     }
     // all giant steps at once: one batched ModUp, one accumulate kernel
@@ -653,8 +661,8 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
             for (int s = 0; s < n;) {
                 int e = s;
                 while (e + 1 < n && giants[a + e + 1] == giants[a + e] + 1) ++e;
-                const uint64_t* c1 = yq + (size_t)giants[a + s] * 2 * nr * N + (size_t)nr * N;
-                modup_batch(c, c1, (size_t)2 * nr * N, e - s + 1, level, dg + (size_t)s * dw);
+                const uint64_t* c1 = yq + (size_t)giants[a + s] * nr * N;
+                modup_batch(c, c1, (size_t)nr * N, e - s + 1, level, dg + (size_t)s * dw);
                 s = e + 1;
             }
             KsStream ks{};
@@ -662,12 +670,13 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
             ks.digits = dg;
             ks.digit_stride = dw;
             ks.out = acc;
+            ks.c0_qp = 1;
             for (int s = 0; s < n; ++s) {
                 const int gi = giants[a + s];
                 const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[gi]));
                 ks.galois[s] = g;
                 ks.key[s] = c->key_for(g);
-                ks.c0[s] = yq + (size_t)gi * 2 * nr * N;
+                ks.c0[s] = Y + (size_t)gi * 2 * extw;
                 c->ledger.key_switches++;
             }
             c->timed("ks_inner", [&] { ks_stream(c->dc, ks, 1, c->d_md, level, dn, c->st); });

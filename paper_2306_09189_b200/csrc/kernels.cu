@@ -311,13 +311,13 @@ __global__ void k_ks_inner(DevCtx c, const uint64_t* D, const uint64_t* key, uin
     }
 }
 
-__global__ void k_gather_special(DevCtx c, uint64_t* dst, const uint64_t* acc, int level, int npoly) {
-    const int ne = level + 1 + c.K;
+__global__ void k_gather_special(DevCtx c, uint64_t* dst, const uint64_t* acc, size_t acc_stride, int level,
+                                 int npoly) {
     const size_t total = (size_t)npoly * c.K * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / c.N);
         const int p = r / c.K, kk = r % c.K;
-        dst[i] = acc[((size_t)p * ne + level + 1 + kk) * c.N + (i % c.N)];
+        dst[i] = acc[(size_t)p * acc_stride + ((size_t)level + 1 + kk) * c.N + (i % c.N)];
     }
 }
 
@@ -429,9 +429,11 @@ void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* k
     ++g_launches;
     k_ks_inner<<<ew_blocks(total), kEwThreads, 0, st>>>(c, digits, key, acc0, acc1, galois, level, dn);
 }
-void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, int level, int npoly, cudaStream_t st) {
+void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, size_t acc_stride, int level, int npoly,
+                    cudaStream_t st) {
     ++g_launches;
-    k_gather_special<<<ew_blocks((size_t)npoly * c.K * c.N), kEwThreads, 0, st>>>(c, dst, acc, level, npoly);
+    k_gather_special<<<ew_blocks((size_t)npoly * c.K * c.N), kEwThreads, 0, st>>>(c, dst, acc, acc_stride, level,
+                                                                                   npoly);
 }
 void moddown_bconv(const DevCtx& c, const uint64_t* pcoef, uint64_t* conv, const ModDownTable* md, int level,
                    int npoly, cudaStream_t st) {
@@ -579,7 +581,11 @@ __global__ void __launch_bounds__(kStreamThreads) k_ks_stream(DevCtx c, KsStream
                 mac(s1[0], da, k1.x);
                 mac(s1[1], db, k1.y);
             }
-            if (qrow) {
+            if (a.c0_qp) {  // P-scaled QP-basis c0: added unscaled on every row
+                const ulonglong2 x = ld2(a.c0[t] + (size_t)u * c.N + (pk & ~1u));
+                add128(s0[0], swp ? x.y : x.x);
+                add128(s0[1], swp ? x.x : x.y);
+            } else if (qrow) {
                 const ulonglong2 x = ld2(a.c0[t] + (size_t)u * c.N + (pk & ~1u));
                 add128(s0[0], mul_shoup(swp ? x.y : x.x, pm, pms, pr.q));
                 add128(s0[1], mul_shoup(swp ? x.x : x.y, pm, pms, pr.q));

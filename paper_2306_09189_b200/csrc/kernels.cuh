@@ -100,7 +100,8 @@ struct NttFuse {
     // ModDown
     const uint64_t* pc;     // [npoly][K][N] INTT'd special-prime rows
     const ModDownTable* md;
-    const uint64_t* acc;    // [npoly][ne][N]
+    const uint64_t* acc;    // poly pp at acc + pp * acc_stride, [ne][N] each
+    size_t acc_stride;
     uint64_t* out;          // [npoly][level+1][N]
     const uint64_t* add_src;
     uint32_t galois;
@@ -118,9 +119,9 @@ void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const ui
                int nsrc, const ModUpDigit* tables, int level, int dn, cudaStream_t st);
 // ModDown FastBConv + finish fused into the forward NTT of conv (scratch [npoly][level+1][N]):
 // out[p] = (acc[p] - NTT(FastBConv_P->Q(pcoef[p]))) P^-1 (+ sigma_g(add_src) on poly 0)
-void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, uint64_t* out,
-                 const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
-                 cudaStream_t st);
+void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, size_t acc_stride,
+                 uint64_t* out, const ModDownTable* md, int level, int npoly, const uint64_t* add_src,
+                 uint32_t galois, cudaStream_t st);
 
 void reduce_signed_rows(const DevCtx& c, const int64_t* coef, uint64_t* out, int nrows, const RowMap& rm,
                         cudaStream_t st);
@@ -177,7 +178,7 @@ void moddown_finish(const DevCtx& c, uint64_t* out, const uint64_t* acc, const u
                     const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
                     cudaStream_t st);
 // copy the K special rows of each poly's accumulator into [npoly][K][N]
-void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, int level, int npoly,
+void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, size_t acc_stride, int level, int npoly,
                     cudaStream_t st);
 
 // Fused conv multiply-accumulate: for every term i
@@ -216,6 +217,7 @@ struct KsStream {
     const uint64_t* key[kMaxBaby];
     const uint64_t* c0[kMaxBaby];
     int slot[kMaxBaby];        // mode 0: output slot in out = [slots][2][ne][N]
+    int c0_qp;                 // c0[t] is a P-scaled QP-basis poly [ne][N], added unscaled
     const uint64_t* digits;
     size_t digit_stride;
     uint64_t* out;             // mode 0: XT; mode 1: acc [2][ne][N]

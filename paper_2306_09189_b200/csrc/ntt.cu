@@ -24,12 +24,18 @@ namespace {
 // padded shared-memory index (2-way bank conflicts at worst for 8-byte words)
 __device__ __forceinline__ int pad(int x) { return x + (x >> 4); }
 
-// One radix-2^R pass of forward CT butterflies on 8 register values that
-// form 8 / 2^R groups. Local vector of n = 2^logn elements, local stage of
+#ifndef FHE_NTT_EPT
+#define FHE_NTT_EPT 16
+#endif
+constexpr int EPT = FHE_NTT_EPT;         // residues per thread in a pass
+constexpr int LOG_EPT = EPT == 16 ? 4 : 3;
+
+// One radix-2^R pass of forward CT butterflies on EPT register values that
+// form EPT / 2^R groups. Local vector of n = 2^logn elements, local stage of
 // the pass sigma0, global stage offset s0, block index blk:
 //   twiddle(stage sigma, x) = 2^(s0+sigma) + blk 2^sigma + x / (2 t_sigma)
 template <int R>
-__device__ __forceinline__ void fwd_pass(uint64_t (&v)[8], int G0, int logn, int sigma0, int s0, int blk,
+__device__ __forceinline__ void fwd_pass(uint64_t (&v)[EPT], int G0, int logn, int sigma0, int s0, int blk,
                                          const uint64_t* __restrict__ tw, const uint64_t* __restrict__ tws,
                                          uint64_t q) {
     constexpr int GS = 1 << R;
@@ -37,7 +43,7 @@ __device__ __forceinline__ void fwd_pass(uint64_t (&v)[8], int G0, int logn, int
     const int logt = logn - sigma0 - 1;  // distance of the first sub-stage is 2^logt
     const int logd = logt - (R - 1);     // element stride inside a group
 #pragma unroll
-    for (int g = 0; g < 8 / GS; ++g) {
+    for (int g = 0; g < EPT / GS; ++g) {
         const int G = G0 + g;
         const int j0 = ((G >> logd) << (logd + R)) | (G & ((1 << logd) - 1));
 #pragma unroll
@@ -45,11 +51,13 @@ __device__ __forceinline__ void fwd_pass(uint64_t (&v)[8], int G0, int logn, int
             const int half = 1 << (R - 1 - rho);
             const int sig = sigma0 + rho;
             const int base = (1 << (s0 + sig)) + (blk << sig) + (j0 >> (logt + 1 - rho));
+            const uint64_t* twb = tw + base;
+            const uint64_t* twsb = tws + base;
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
-                const int widx = base + (k >> (R - rho));
-                const uint64_t w = __ldg(tw + widx), ws = __ldg(tws + widx);
+                const int off = k >> (R - rho);
+                const uint64_t w = __ldg(twb + off), ws = __ldg(twsb + off);
                 // Harvey's lazy CT butterfly: values live in [0, 4q) between stages
                 uint64_t U = v[g * GS + k];
                 U = U >= q2 ? U - q2 : U;
@@ -75,13 +83,13 @@ __device__ __forceinline__ int fwd_pos(int G0, int e, int logn, int sigma0) {
 // Inverse GS pass of R stages starting at distance 2^logt (t grows):
 //   twiddle(t', x) = n_tot / (2 t') + blk n_loc / (2 t') + x / (2 t')
 template <int R>
-__device__ __forceinline__ void inv_pass(uint64_t (&v)[8], int G0, int logt, int log_ntot, int log_nloc, int blk,
+__device__ __forceinline__ void inv_pass(uint64_t (&v)[EPT], int G0, int logt, int log_ntot, int log_nloc, int blk,
                                          const uint64_t* __restrict__ tw, const uint64_t* __restrict__ tws,
                                          uint64_t q) {
     constexpr int GS = 1 << R;
     const uint64_t q2 = 2 * q;
 #pragma unroll
-    for (int g = 0; g < 8 / GS; ++g) {
+    for (int g = 0; g < EPT / GS; ++g) {
         const int G = G0 + g;
         const int j0 = ((G >> logt) << (logt + R)) | (G & ((1 << logt) - 1));
 #pragma unroll
@@ -89,11 +97,13 @@ __device__ __forceinline__ void inv_pass(uint64_t (&v)[8], int G0, int logt, int
             const int half = 1 << rho;
             const int lt = logt + rho;  // current distance 2^lt
             const int base = (1 << (log_ntot - lt - 1)) + (blk << (log_nloc - lt - 1)) + (j0 >> (lt + 1));
+            const uint64_t* twb = tw + base;
+            const uint64_t* twsb = tws + base;
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
-                const int widx = base + (k >> (rho + 1));
-                const uint64_t w = __ldg(tw + widx), ws = __ldg(tws + widx);
+                const int off = k >> (rho + 1);
+                const uint64_t w = __ldg(twb + off), ws = __ldg(twsb + off);
                 // Harvey's lazy GS butterfly: values live in [0, 2q) between stages
                 const uint64_t U = v[g * GS + k], V = v[g * GS + k + half];
                 const uint64_t T = U + V;
@@ -113,17 +123,17 @@ __device__ __forceinline__ int inv_pos(int G0, int e, int logt) {
 }
 
 // Run all forward stages of a local vector of 2^LOGN elements held in smem
-// (element x at vec[pad(x)]); 2^LOGN / 8 cooperating threads, lt = lane.
+// (element x at vec[pad(x)]); 2^LOGN / EPT cooperating threads, lt = lane.
 template <int R, int LOGN, int SIGMA0, bool WARP_SYNC>
 __device__ __forceinline__ void fwd_step(uint64_t* vec, int lt, int s0, int blk, const uint64_t* tw,
                                          const uint64_t* tws, uint64_t q) {
-    uint64_t v[8];
-    const int G0 = lt * (8 >> R);
+    uint64_t v[EPT];
+    const int G0 = lt * (EPT >> R);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))];
+    for (int e = 0; e < EPT; ++e) v[e] = vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))];
     fwd_pass<R>(v, G0, LOGN, SIGMA0, s0, blk, tw, tws, q);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))] = v[e];
+    for (int e = 0; e < EPT; ++e) vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))] = v[e];
     if (WARP_SYNC)
         __syncwarp();
     else
@@ -134,7 +144,7 @@ template <int LOGN, int SIGMA0, bool WARP_SYNC>
 __device__ __forceinline__ void fwd_local(uint64_t* vec, int lt, int s0, int blk, const uint64_t* tw,
                                           const uint64_t* tws, uint64_t q) {
     if constexpr (SIGMA0 < LOGN) {
-        constexpr int R = (LOGN - SIGMA0) >= 3 ? 3 : (LOGN - SIGMA0);
+        constexpr int R = (LOGN - SIGMA0) >= LOG_EPT ? LOG_EPT : (LOGN - SIGMA0);
         fwd_step<R, LOGN, SIGMA0, WARP_SYNC>(vec, lt, s0, blk, tw, tws, q);
         fwd_local<LOGN, SIGMA0 + R, WARP_SYNC>(vec, lt, s0, blk, tw, tws, q);
     }
@@ -143,25 +153,25 @@ __device__ __forceinline__ void fwd_local(uint64_t* vec, int lt, int s0, int blk
 template <int R, int LOGN, int LOGT, bool WARP_SYNC>
 __device__ __forceinline__ void inv_step(uint64_t* vec, int lt, int log_ntot, int blk, const uint64_t* tw,
                                          const uint64_t* tws, uint64_t q) {
-    uint64_t v[8];
-    const int G0 = lt * (8 >> R);
+    uint64_t v[EPT];
+    const int G0 = lt * (EPT >> R);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = vec[pad(inv_pos<R>(G0, e, LOGT))];
+    for (int e = 0; e < EPT; ++e) v[e] = vec[pad(inv_pos<R>(G0, e, LOGT))];
     inv_pass<R>(v, G0, LOGT, log_ntot, LOGN, blk, tw, tws, q);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) vec[pad(inv_pos<R>(G0, e, LOGT))] = v[e];
+    for (int e = 0; e < EPT; ++e) vec[pad(inv_pos<R>(G0, e, LOGT))] = v[e];
     if (WARP_SYNC)
         __syncwarp();
     else
         __syncthreads();
 }
 
-// inverse passes in growing distance; the first pass takes LOGN mod 3 stages
+// inverse passes in growing distance; the first pass takes LOGN mod LOG_EPT stages
 template <int LOGN, int LOGT, bool WARP_SYNC>
 __device__ __forceinline__ void inv_local(uint64_t* vec, int lt, int log_ntot, int blk, const uint64_t* tw,
                                           const uint64_t* tws, uint64_t q) {
     if constexpr (LOGT < LOGN) {
-        constexpr int R = (LOGT == 0 && LOGN % 3 != 0) ? LOGN % 3 : 3;
+        constexpr int R = (LOGT == 0 && LOGN % LOG_EPT != 0) ? LOGN % LOG_EPT : LOG_EPT;
         inv_step<R, LOGN, LOGT, WARP_SYNC>(vec, lt, log_ntot, blk, tw, tws, q);
         inv_local<LOGN, LOGT + R, WARP_SYNC>(vec, lt, log_ntot, blk, tw, tws, q);
     }
@@ -190,7 +200,7 @@ enum { FUSE_NONE = 0, FUSE_MODUP = 1, FUSE_MODDOWN = 2 };
 template <int LOG_N1, int C, bool INVERSE, int FUSE>
 __global__ void __launch_bounds__(256) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
     constexpr int N1 = 1 << LOG_N1;
-    constexpr int TPC = N1 / 8;               // threads per column
+    constexpr int TPC = N1 / EPT;             // threads per column
     constexpr int PN = N1 + (N1 >> 4) + 1;    // padded column length (odd in words)
     __shared__ uint64_t sm[C * PN];            // column-major: column cc at sm + cc * PN
     const int row = blockIdx.y;
@@ -302,9 +312,9 @@ template <int LOG_N1, int C, int MODE, int KA>
 __global__ void __launch_bounds__(256) k_ntt_cols_bconv(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz,
                                                         int tg_size) {
     constexpr int N1 = 1 << LOG_N1;
-    constexpr int TPC = N1 / 8;
+    constexpr int TPC = N1 / EPT;
     constexpr int PN = N1 + (N1 >> 4) + 1;
-    constexpr int EPT = N1 * C / 256;  // elements per thread in the load phase (= 8)
+    static_assert(N1 * C / 256 == EPT, "load phase: EPT elements per thread");
     __shared__ uint64_t sm[C * PN];
     const int B = c.N >> LOG_N1;
     const int col0 = blockIdx.x * C;
@@ -410,7 +420,7 @@ __device__ __forceinline__ uint32_t perm_index_n(uint32_t k, uint32_t g, int log
 template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE>
 __global__ void __launch_bounds__(256) k_ntt_rows(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
     constexpr int B = 1 << LOG_B;
-    constexpr int TPB = B / 8;
+    constexpr int TPB = B / EPT;
     constexpr int BPC = 256 / TPB;
     constexpr int PB = B + (B >> 4);
     __shared__ uint64_t sm[BPC * PB];
@@ -439,7 +449,8 @@ __global__ void __launch_bounds__(256) k_ntt_rows(DevCtx c, uint64_t* data, RowM
         if (FUSE == FUSE_MODDOWN) {
             const int pp = row / rm.rows_per_poly;
             const int nr = rm.level + 1, ne = nr + c.K;
-            const uint64_t* acc = fz.acc + ((size_t)pp * ne + u) * c.N + (size_t)blk0 * B;
+            (void)ne;
+            const uint64_t* acc = fz.acc + (size_t)pp * fz.acc_stride + (size_t)u * c.N + (size_t)blk0 * B;
             uint64_t* out = fz.out + ((size_t)pp * nr + u) * c.N + (size_t)blk0 * B;
             const uint64_t pi = fz.md->pinvq[u], pis = fz.md->pinvq_sh[u];
             const bool add = fz.add_src && pp == 0;
@@ -470,8 +481,8 @@ template <int LOG_N1, int LOG_B>
 void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, bool inverse, int fuse,
                   const NttFuse& fz, cudaStream_t st) {
     constexpr int N1 = 1 << LOG_N1, B = 1 << LOG_B;
-    constexpr int C = 256 / (N1 / 8);
-    constexpr int BPC = 256 / (B / 8);
+    constexpr int C = 256 / (N1 / EPT);
+    constexpr int BPC = 256 / (B / EPT);
     const dim3 ga(B / C, nrows), gb((N1 + BPC - 1) / BPC, nrows);
     if (!inverse) {
         if (fuse == FUSE_MODUP || fuse == FUSE_MODDOWN) {
@@ -485,7 +496,7 @@ void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, 
             const dim3 gc(tiles, ngroups_src, tg);
 #define FHE_BCONV(MODE, KA)                                                                              \
     do {                                                                                                 \
-        const int dsm = (KA) * (N1 * C / 256) * 256 * 8 + (N1 * C / 256) * 256;                          \
+        const int dsm = (KA) * EPT * 256 * 8 + EPT * 256;                                                \
         cudaFuncSetAttribute(k_ntt_cols_bconv<LOG_N1, C, MODE, KA>,                                      \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);                          \
         k_ntt_cols_bconv<LOG_N1, C, MODE, KA><<<gc, 256, dsm, st>>>(c, data, rm, fz, tg_size);           \
@@ -552,14 +563,15 @@ void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const ui
     ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, c.K, dn}, false, FUSE_MODUP, fz, st);
 }
 
-void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, uint64_t* out,
-                 const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
-                 cudaStream_t st) {
+void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, size_t acc_stride,
+                 uint64_t* out, const ModDownTable* md, int level, int npoly, const uint64_t* add_src,
+                 uint32_t galois, cudaStream_t st) {
     const int nr = level + 1;
     NttFuse fz{};
     fz.pc = pcoef;
     fz.md = md;
     fz.acc = acc;
+    fz.acc_stride = acc_stride;
     fz.out = out;
     fz.add_src = add_src;
     fz.galois = galois;
