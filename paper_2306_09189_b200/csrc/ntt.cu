@@ -209,66 +209,7 @@ __global__ void __launch_bounds__(256) k_ntt_cols(DevCtx c, uint64_t* data, RowM
     const int col0 = blockIdx.x * C;
     uint64_t* a = data + (size_t)row * c.N;
     int p;
-    if (FUSE == FUSE_MODUP) {
-        // row = (src, digit j, extended row u)
-        const int sj = row / rm.rows_per_poly;
-        const int src = sj / fz.dn, j = sj % fz.dn;
-        const ModUpDigit& T = fz.mu[j];
-        const uint64_t* c1 = fz.c1 + (size_t)src * fz.c1_stride;
-        if (u >= T.lo && u < T.hi) {  // own prime of the digit: NTT-domain copy
-            for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-                const size_t pos = (size_t)(i / C) * B + col0 + i % C;
-                a[pos] = c1[(size_t)u * c.N + pos];
-            }
-            return;
-        }
-        p = row_prime(rm, u);
-        const uint64_t t = c.primes[p].q;
-        const int na = T.hi - T.lo;
-        const uint64_t* coef = fz.coef + (size_t)src * (rm.level + 1) * c.N;
-        for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-            const int r = i / C, cc = i % C;
-            const size_t pos = (size_t)r * B + col0 + cc;
-            uint64_t y = 0;
-            int neg = 0;
-#pragma unroll
-            for (int al = 0; al < kMaxAlpha; ++al) {
-                if (al < na) {
-                    const int qi = T.lo + al;
-                    const uint64_t q = c.primes[qi].q;
-                    const uint64_t v = mul_shoup(coef[(size_t)qi * c.N + pos], T.inv[al], T.inv_sh[al], q);
-                    neg += v > (q >> 1);
-                    y = add_mod(y, mul_shoup(v, T.hat[u][al], T.hat_sh[u][al], t), t);
-                }
-            }
-            for (int n = 0; n < neg; ++n) y = sub_mod(y, T.qj[u], t);  // centered lift
-            sm[cc * PN + pad(r)] = y;
-        }
-    } else if (FUSE == FUSE_MODDOWN) {
-        // row = (poly pp, q row t); FastBConv of the K special-prime coefficients
-        const int pp = row / rm.rows_per_poly;
-        p = u;
-        const uint64_t t = c.primes[p].q;
-        const ModDownTable* md = fz.md;
-        const uint64_t* pc = fz.pc + (size_t)pp * c.K * c.N;
-        for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-            const int r = i / C, cc = i % C;
-            const size_t pos = (size_t)r * B + col0 + cc;
-            uint64_t y = 0;
-            int neg = 0;
-#pragma unroll
-            for (int k = 0; k < kMaxAlpha; ++k) {
-                if (k < c.K) {
-                    const uint64_t q = c.primes[c.L + k].q;
-                    const uint64_t v = mul_shoup(pc[(size_t)k * c.N + pos], md->pinv[k], md->pinv_sh[k], q);
-                    neg += v > (q >> 1);
-                    y = add_mod(y, mul_shoup(v, md->hat[p][k], md->hat_sh[p][k], t), t);
-                }
-            }
-            for (int n = 0; n < neg; ++n) y = sub_mod(y, md->pmod[p], t);
-            sm[cc * PN + pad(r)] = y;
-        }
-    } else {
+    {
         if (skip_row(rm, row, u)) return;
         p = row_prime(rm, u);
         // coalesced load: consecutive threads take consecutive columns of a row
@@ -297,116 +238,6 @@ __global__ void __launch_bounds__(256) k_ntt_cols(DevCtx c, uint64_t* data, RowM
             const int r = i / C, cc2 = i % C;
             a[(size_t)r * B + col0 + cc2] = sm[cc2 * PN + pad(r)];
         }
-    }
-}
-
-// Column pass with the FastBConv fused in front, amortised over target rows:
-// CTA = (column tile, source group, target group). The centered
-// [x_i (Q_J/q_i)^-1]_{q_i} values of the tile are computed once into
-// registers, then every target row of the group is converted, transformed
-// and written. MODE = FUSE_MODUP: source group = (src, digit j), targets =
-// extended rows u (own rows of the digit copied from the NTT input);
-// MODE = FUSE_MODDOWN: source group = poly, sources = the K special rows,
-// targets = q rows t <= level.
-template <int LOG_N1, int C, int MODE, int KA>
-__global__ void __launch_bounds__(256) k_ntt_cols_bconv(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz,
-                                                        int tg_size) {
-    constexpr int N1 = 1 << LOG_N1;
-    constexpr int TPC = N1 / EPT;
-    constexpr int PN = N1 + (N1 >> 4) + 1;
-    static_assert(N1 * C / 256 == EPT, "load phase: EPT elements per thread");
-    __shared__ uint64_t sm[C * PN];
-    const int B = c.N >> LOG_N1;
-    const int col0 = blockIdx.x * C;
-    const int sg = blockIdx.y;
-    const int nr = rm.level + 1;
-    int nsrc_rows, u_begin, u_end, lo = 0, hi = 0;
-    const uint64_t* srcrows;
-    const ModUpDigit* T = nullptr;
-    if (MODE == FUSE_MODUP) {
-        const int src = sg / fz.dn, j = sg % fz.dn;
-        T = fz.mu + j;
-        lo = T->lo;
-        hi = T->hi;
-        nsrc_rows = hi - lo;
-        srcrows = fz.coef + ((size_t)src * nr + lo) * c.N;
-        u_begin = blockIdx.z * tg_size;
-        u_end = min(u_begin + tg_size, rm.rows_per_poly);
-    } else {
-        nsrc_rows = c.K;
-        srcrows = fz.pc + (size_t)sg * c.K * c.N;
-        u_begin = blockIdx.z * tg_size;
-        u_end = min(u_begin + tg_size, nr);
-    }
-    // load + first half of the conversion (once per tile), kept in shared
-    // memory (per-thread private slots) so the NTT passes keep a low register count
-    extern __shared__ uint64_t dyn[];
-    uint64_t(*sv)[EPT][256] = reinterpret_cast<uint64_t(*)[EPT][256]>(dyn);  // [KA][EPT][256]
-    uint8_t(*sneg)[256] = reinterpret_cast<uint8_t(*)[256]>(dyn + KA * EPT * 256);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-        const int i = threadIdx.x + e * 256;
-        const size_t pos = (size_t)(i / C) * B + col0 + i % C;
-        int neg = 0;
-#pragma unroll
-        for (int a = 0; a < KA; ++a) {
-            uint64_t v = 0;
-            if (a < nsrc_rows) {
-                const int qi = MODE == FUSE_MODUP ? lo + a : c.L + a;
-                const uint64_t q = c.primes[qi].q;
-                const uint64_t x = srcrows[(size_t)a * c.N + pos];
-                const uint64_t w = MODE == FUSE_MODUP ? T->inv[a] : fz.md->pinv[a];
-                const uint64_t ws = MODE == FUSE_MODUP ? T->inv_sh[a] : fz.md->pinv_sh[a];
-                v = mul_shoup(x, w, ws, q);
-                neg += v > (q >> 1);
-            }
-            sv[a][e][threadIdx.x] = v;
-        }
-        sneg[e][threadIdx.x] = (uint8_t)neg;
-    }
-    const int cc = threadIdx.x / TPC, lt = threadIdx.x % TPC;
-    for (int u = u_begin; u < u_end; ++u) {
-        const int outrow = sg * rm.rows_per_poly + u;
-        uint64_t* a_out = data + (size_t)outrow * c.N;
-        if (MODE == FUSE_MODUP && u >= lo && u < hi) {  // own prime: NTT-domain copy
-            const int src = sg / fz.dn;
-            const uint64_t* c1 = fz.c1 + (size_t)src * fz.c1_stride + (size_t)u * c.N;
-#pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-                const int i = threadIdx.x + e * 256;
-                const size_t pos = (size_t)(i / C) * B + col0 + i % C;
-                a_out[pos] = c1[pos];
-            }
-            continue;
-        }
-        const int p = row_prime(rm, u);
-        const uint64_t t = c.primes[p].q;
-        uint64_t hat[KA], hats[KA];
-#pragma unroll
-        for (int a = 0; a < KA; ++a) {
-            hat[a] = MODE == FUSE_MODUP ? T->hat[u][a] : fz.md->hat[p][a];
-            hats[a] = MODE == FUSE_MODUP ? T->hat_sh[u][a] : fz.md->hat_sh[p][a];
-        }
-        const uint64_t corr = MODE == FUSE_MODUP ? T->qj[u] : fz.md->pmod[p];
-#pragma unroll 2
-        for (int e = 0; e < EPT; ++e) {
-            const int i = threadIdx.x + e * 256;
-            uint64_t y = 0;
-#pragma unroll
-            for (int a = 0; a < KA; ++a)
-                if (a < nsrc_rows) y = add_mod(y, mul_shoup(sv[a][e][threadIdx.x], hat[a], hats[a], t), t);
-            const int neg = sneg[e][threadIdx.x];
-            for (int n = 0; n < neg; ++n) y = sub_mod(y, corr, t);  // centered lift
-            sm[(i % C) * PN + pad(i / C)] = y;
-        }
-        __syncthreads();
-        fwd_local<LOG_N1, 0, false>(sm + cc * PN, lt, 0, 0, c.tw + (size_t)p * c.N, c.tw_sh + (size_t)p * c.N, t);
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int i = threadIdx.x + e * 256;
-            a_out[(size_t)(i / C) * B + col0 + i % C] = sm[(i % C) * PN + pad(i / C)];
-        }
-        __syncthreads();
     }
 }
 
@@ -477,6 +308,86 @@ __global__ void __launch_bounds__(256) k_ntt_rows(DevCtx c, uint64_t* data, RowM
     }
 }
 
+// FastBConv of ModUp (one thread per output coefficient pair, all targets in
+// parallel): digits[src][j][u] = conv_J->t_u(coef[src]) for u outside the
+// digit, NTT-domain copies of c1 for the digit's own rows.
+template <int KA>
+__global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits, NttFuse fz, int level, int nsrc) {
+    const int nr = level + 1, ne = nr + c.K;
+    const size_t halfN = c.N / 2;
+    const size_t total = (size_t)nsrc * fz.dn * ne * halfN;
+    RowMap rm{ne, level, c.L, 0};
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t row = idx / halfN;
+        const size_t k = (idx % halfN) * 2;
+        const int u = (int)(row % ne);
+        const int sj = (int)(row / ne);
+        const int src = sj / fz.dn, j = sj % fz.dn;
+        const ModUpDigit& T = fz.mu[j];
+        uint64_t* out = digits + row * c.N + k;
+        if (u >= T.lo && u < T.hi) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(fz.c1 + (size_t)src * fz.c1_stride +
+                                                                      (size_t)u * c.N + k);
+            *reinterpret_cast<ulonglong2*>(out) = x;
+            continue;
+        }
+        const uint64_t t = c.primes[row_prime(rm, u)].q;
+        const uint64_t* coef = fz.coef + (size_t)src * nr * c.N;
+        uint64_t y0 = 0, y1 = 0;
+        int n0 = 0, n1 = 0;
+        const int na = T.hi - T.lo;
+#pragma unroll
+        for (int a = 0; a < KA; ++a) {
+            if (a < na) {
+                const int qi = T.lo + a;
+                const uint64_t q = c.primes[qi].q;
+                const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(coef + (size_t)qi * c.N + k);
+                const uint64_t v0 = mul_shoup(x.x, T.inv[a], T.inv_sh[a], q);
+                const uint64_t v1 = mul_shoup(x.y, T.inv[a], T.inv_sh[a], q);
+                n0 += v0 > (q >> 1);
+                n1 += v1 > (q >> 1);
+                y0 = add_mod(y0, mul_shoup(v0, T.hat[u][a], T.hat_sh[u][a], t), t);
+                y1 = add_mod(y1, mul_shoup(v1, T.hat[u][a], T.hat_sh[u][a], t), t);
+            }
+        }
+        for (int n = 0; n < n0; ++n) y0 = sub_mod(y0, T.qj[u], t);
+        for (int n = 0; n < n1; ++n) y1 = sub_mod(y1, T.qj[u], t);
+        *reinterpret_cast<ulonglong2*>(out) = make_ulonglong2(y0, y1);
+    }
+}
+
+// FastBConv of ModDown: conv[pp][t] = conv_P->q_t(pc[pp]) (coefficient domain)
+template <int KA>
+__global__ void __launch_bounds__(256) k_bconv_moddown(DevCtx c, uint64_t* conv, NttFuse fz, int level, int npoly) {
+    const int nr = level + 1;
+    const size_t halfN = c.N / 2;
+    const size_t total = (size_t)npoly * nr * halfN;
+    const ModDownTable* md = fz.md;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t row = idx / halfN;
+        const size_t k = (idx % halfN) * 2;
+        const int t = (int)(row % nr), pp = (int)(row / nr);
+        const uint64_t qt = c.primes[t].q;
+        const uint64_t* pc = fz.pc + (size_t)pp * c.K * c.N;
+        uint64_t y0 = 0, y1 = 0;
+        int n0 = 0, n1 = 0;
+#pragma unroll
+        for (int a = 0; a < KA; ++a) {
+            const uint64_t q = c.primes[c.L + a].q;
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(pc + (size_t)a * c.N + k);
+            const uint64_t v0 = mul_shoup(x.x, md->pinv[a], md->pinv_sh[a], q);
+            const uint64_t v1 = mul_shoup(x.y, md->pinv[a], md->pinv_sh[a], q);
+            n0 += v0 > (q >> 1);
+            n1 += v1 > (q >> 1);
+            y0 = add_mod(y0, mul_shoup(v0, md->hat[t][a], md->hat_sh[t][a], qt), qt);
+            y1 = add_mod(y1, mul_shoup(v1, md->hat[t][a], md->hat_sh[t][a], qt), qt);
+        }
+        for (int n = 0; n < n0; ++n) y0 = sub_mod(y0, md->pmod[t], qt);
+        for (int n = 0; n < n1; ++n) y1 = sub_mod(y1, md->pmod[t], qt);
+        *reinterpret_cast<ulonglong2*>(conv + row * c.N + k) = make_ulonglong2(y0, y1);
+    }
+}
+
 template <int LOG_N1, int LOG_B>
 void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, bool inverse, int fuse,
                   const NttFuse& fz, cudaStream_t st) {
@@ -485,42 +396,11 @@ void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, 
     constexpr int BPC = 256 / (B / EPT);
     const dim3 ga(B / C, nrows), gb((N1 + BPC - 1) / BPC, nrows);
     if (!inverse) {
-        if (fuse == FUSE_MODUP || fuse == FUSE_MODDOWN) {
-            // target groups: enough CTAs to fill the GPU, few enough to amortise the conversion
-            const int ngroups_src = nrows / rm.rows_per_poly;
-            const int tiles = B / C;
-            // ~4 target rows per CTA: enough CTAs to overlap, the conversion amortised 4x
-            const int tg_size = rm.rows_per_poly < 4 ? rm.rows_per_poly : 4;
-            const int tg = (rm.rows_per_poly + tg_size - 1) / tg_size;
-            (void)tiles;
-            const dim3 gc(tiles, ngroups_src, tg);
-#define FHE_BCONV(MODE, KA)                                                                              \
-    do {                                                                                                 \
-        const int dsm = (KA) * EPT * 256 * 8 + EPT * 256;                                                \
-        cudaFuncSetAttribute(k_ntt_cols_bconv<LOG_N1, C, MODE, KA>,                                      \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);                          \
-        k_ntt_cols_bconv<LOG_N1, C, MODE, KA><<<gc, 256, dsm, st>>>(c, data, rm, fz, tg_size);           \
-    } while (0)
-#define FHE_BCONV_K(MODE)             \
-    switch (c.K) {                    \
-        case 1: FHE_BCONV(MODE, 1); break; \
-        case 2: FHE_BCONV(MODE, 2); break; \
-        case 3: FHE_BCONV(MODE, 3); break; \
-        default: FHE_BCONV(MODE, 4); break; \
-    }
-            if (fuse == FUSE_MODUP) {
-                FHE_BCONV_K(FUSE_MODUP)
-                k_ntt_rows<LOG_N1, LOG_B, false, FUSE_NONE><<<gb, 256, 0, st>>>(c, data, rm, fz);
-            } else {
-                FHE_BCONV_K(FUSE_MODDOWN)
-                k_ntt_rows<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gb, 256, 0, st>>>(c, data, rm, fz);
-            }
-#undef FHE_BCONV_K
-#undef FHE_BCONV
-        } else {
-            k_ntt_cols<LOG_N1, C, false, FUSE_NONE><<<ga, 256, 0, st>>>(c, data, rm, fz);
+        k_ntt_cols<LOG_N1, C, false, FUSE_NONE><<<ga, 256, 0, st>>>(c, data, rm, fz);
+        if (fuse == FUSE_MODDOWN)
+            k_ntt_rows<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gb, 256, 0, st>>>(c, data, rm, fz);
+        else
             k_ntt_rows<LOG_N1, LOG_B, false, FUSE_NONE><<<gb, 256, 0, st>>>(c, data, rm, fz);
-        }
     } else {
         k_ntt_rows<LOG_N1, LOG_B, true, FUSE_NONE><<<gb, 256, 0, st>>>(c, data, rm, fz);
         k_ntt_cols<LOG_N1, C, true, FUSE_NONE><<<ga, 256, 0, st>>>(c, data, rm, fz);
@@ -560,7 +440,18 @@ void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const ui
     fz.c1_stride = c1_stride;
     fz.mu = tables;
     fz.dn = dn;
-    ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, c.K, dn}, false, FUSE_MODUP, fz, st);
+    {
+        const size_t total = (size_t)nsrc * dn * ne * (c.N / 2);
+        const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+        switch (c.K) {
+            case 1: k_bconv_modup<1><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
+            case 2: k_bconv_modup<2><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
+            case 3: k_bconv_modup<3><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
+            default: k_bconv_modup<4><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
+        }
+        note_launch(1);
+    }
+    ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, c.K, dn}, false, FUSE_NONE, fz, st);
 }
 
 void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, size_t acc_stride,
@@ -575,6 +466,17 @@ void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const u
     fz.out = out;
     fz.add_src = add_src;
     fz.galois = galois;
+    {
+        const size_t total = (size_t)npoly * nr * (c.N / 2);
+        const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+        switch (c.K) {
+            case 1: k_bconv_moddown<1><<<blocks, 256, 0, st>>>(c, conv, fz, level, npoly); break;
+            case 2: k_bconv_moddown<2><<<blocks, 256, 0, st>>>(c, conv, fz, level, npoly); break;
+            case 3: k_bconv_moddown<3><<<blocks, 256, 0, st>>>(c, conv, fz, level, npoly); break;
+            default: k_bconv_moddown<4><<<blocks, 256, 0, st>>>(c, conv, fz, level, npoly); break;
+        }
+        note_launch(1);
+    }
     ntt_run(c, conv, npoly * nr, RowMap{nr, level, c.L, 0, 0}, false, FUSE_MODDOWN, fz, st);
 }
 
