@@ -4,9 +4,11 @@ homomorphic convs/sec and hoisted rotations/sec at N=2^15; % HBM roofline).
 
 Headline workload (config.workload): BASELINE cfg3 — CKKS N=2^15, primes
 60 + 12x50 | 2x60 special, Delta = 2^50; image 32x32x16 packed into 16384
-slots; 3x3 16->16 same-padding conv, paper Approach 2 (channel rotations
-first, shifts hoisted), one rescale. One step = one ciphertext through the
-whole conv layer. Inputs are seeded synthetic data with the BASELINE shapes
+slots; 3x3 16->16 same-padding conv, one rescale. One step = one ciphertext
+through the whole conv layer. The headline uses the fastest schedule
+(--approach 0: baby-step/giant-step with hoisted channel rotations, DESIGN.md
+§4.3); the paper's Approach 1 / Approach 2 schedules of the same layer are
+timed in the same run (conv_per_s_by_approach). Inputs are seeded synthetic data with the BASELINE shapes
 and distributions (uniform [-1,1] image and weights); keys and plaintexts
 are resident in HBM and the key stream (23 keys x 55 MB = 1.27 GB per conv)
 is larger than L2, so no L2 flush is needed between steps.
@@ -38,8 +40,7 @@ C_IN = C_OUT = 16
 M = 32
 KAPPA = 3
 WORKLOAD = ("cfg3: CKKS N=2^15 (16384 slots), 60+12x50-bit q | 2x60-bit p, scale 2^50, dnum 7; image 32x32x16 "
-            "U[-1,1]; 3x3 conv 16->16 same padding, weights U[-1,1]; Approach 2 (hoisted shifts) + 1 rescale; "
-            "1 ciphertext per step")
+            "U[-1,1]; 3x3 conv 16->16 same padding, weights U[-1,1]; + 1 rescale; 1 ciphertext per step")
 
 
 def env_int(name, default):
@@ -120,23 +121,32 @@ def ncu_traffic(kernel_class):
         return None
 
 
-# ----------------------------------------------------------------- byte model
-def byte_model(ctx, level, approach):
-    """Algorithmic (compulsory) HBM bytes per launch, SURVEY.md §8(d)."""
-    N, L, K, dnum = ctx.N, ctx.L, ctx.K, ctx.dnum
-    key = 2 * dnum * (L + K) * N * 8
-    ct = 2 * (level + 1) * N * 8
-    pt_qp = (level + 1 + K) * N * 8
-    n_shift = KAPPA * KAPPA - 1
-    if approach == 2:  # one launch per channel-rotated source: 8 shift keys + 9 plaintexts + the source
-        mac = n_shift * key + KAPPA * KAPPA * pt_qp + ct
-    else:  # one launch per shifted source: 15 channel keys + 16 plaintexts + the source
-        mac = (C_IN - 1) * key + C_IN * pt_qp + ct
-    conv = ct + 2 * level * N * 8 + (C_IN - 1 + n_shift) * key + C_IN * KAPPA * KAPPA * pt_qp
-    return {"key": key, "ct": ct, "pt": pt_qp, "conv_mac": mac, "conv": conv}
-
-
 # ------------------------------------------------------------------ our arm
+KERNEL_CLASSES = ["ntt", "ntt_modup", "ntt_moddown", "ks_multi", "pt_matvec", "ks_inner", "conv_mac", "moddown",
+                  "rescale"]
+KERNEL_NOTES = {
+    "ntt": "plain forward/inverse NTT passes (IMAD-bound 64-bit Shoup butterflies)",
+    "ntt_modup": "ModUp: FastBConv of the digit + forward NTT of the extended rows",
+    "ntt_moddown": "ModDown: FastBConv P->Q + forward NTT + fused (acc - conv) P^-1",
+    "ks_multi": "hoisted key-switch inner products of the baby steps (cp.async key stream)",
+    "pt_matvec": "rotated-plaintext multiply-accumulate into the giant accumulators",
+    "ks_inner": "giant-step key switches accumulated into the QP accumulator",
+    "conv_mac": "paper-schedule fused inner product + plaintext MAC (approaches 1/2)",
+}
+
+
+def conv_reference_numpy(img, w):
+    x = img.reshape(C_IN, M, M)
+    wt = w.reshape(C_IN, C_OUT, KAPPA, KAPPA)
+    h = KAPPA // 2
+    xp = np.pad(x, ((0, 0), (h, h), (h, h)))
+    ref = np.zeros((C_OUT, M, M))
+    for a in range(KAPPA):
+        for b in range(KAPPA):
+            ref += np.einsum("fg,fij->gij", wt[:, :, a, b], xp[:, a:a + M, b:b + M])
+    return ref.ravel()
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     from paper_2306_09189_b200 import Context
@@ -157,6 +167,7 @@ def run_ours(args, rank, world, local_rank):
     out = ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1)
     level = ctx.max_level
     approach = args.approach
+    ref = conv_reference_numpy(img, w)
 
     def barrier():
         if dist:
@@ -169,16 +180,19 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # correctness gate before timing: decrypted output vs numpy conv
+    def timed_convs(ap, steps, warmup):
+        for _ in range(warmup):
+            ctx.conv2d_into(ct, layer, ap, out)
+        ctx.synchronize()
+        ctx.timer_start()
+        for _ in range(steps):
+            ctx.conv2d_into(ct, layer, ap, out)
+        return max_over_ranks(ctx.timer_stop())
+
+    # correctness gate before timing: decrypted output vs a float64 numpy conv
     ctx.conv2d_into(ct, layer, approach, out)
-    x = img.reshape(C_IN, M, M)
-    wt = w.reshape(C_IN, C_OUT, KAPPA, KAPPA)
-    xp = np.pad(x, ((0, 0), (1, 1), (1, 1)))
-    ref = np.zeros((C_OUT, M, M))
-    for a in range(3):
-        for b in range(3):
-            ref += np.einsum("fg,fij->gij", wt[:, :, a, b], xp[:, a:a + M, b:b + M])
-    err = float(np.abs(ctx.decrypt(out)[: C_OUT * M * M] - ref.ravel()).max())
+    err = float(np.abs(ctx.decrypt(out)[: C_OUT * M * M] - ref).max())
+    assert err < 1e-6, f"decrypted conv error {err}"
 
     for _ in range(args.warmup):
         ctx.conv2d_into(ct, layer, approach, out)
@@ -196,39 +210,34 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     ctx.prof_enable(False)
     launches = ctx.ledger()["kernel_launches"] - launches0
-    classes = ["conv_mac", "ks_multi", "pt_matvec", "ntt", "ntt_modup", "ntt_moddown", "ks_inner", "moddown", "rescale"]
-    prof = {c: ctx.prof_get(c) for c in classes}
+    prof = {c: ctx.prof_get_bytes(c) for c in KERNEL_CLASSES}
     ms_max = max_over_ranks(ms)
 
-    # secondary metrics (device-timed, same context): the other approach and
-    # the hoisted 3x3 stencil group at N = 2^15 (8 non-identity rotations)
-    other = 1 if approach == 2 else 2
-    for _ in range(2):
-        ctx.conv2d_into(ct, layer, other, out)
-    ctx.timer_start()
-    k2 = max(2, args.steps // 2)
-    for _ in range(k2):
-        ctx.conv2d_into(ct, layer, other, out)
-    ms_other = max_over_ranks(ctx.timer_stop())
-    stencil = [kk * M + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1)]
+    # the same conv under every schedule (device-timed, same context)
+    per_approach = {}
+    for ap in (1, 2, 3, 4):
+        k2 = max(3, args.steps // 4) if ap in (1, 2) else max(3, args.steps // 2)
+        per_approach[ap] = world * k2 / (timed_convs(ap, k2, 2) / 1e3)
+    # hoisted rotations at N = 2^15: the 8 non-identity shifts of a 3x3 stencil from one ModUp
+    stencil = [kk * M + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1) if kk or ll]
     for _ in range(2):
         ctx.rotate_hoisted(ct, stencil)
     ctx.synchronize()
-    ctx.timer_start()
     kh = max(3, args.steps)
+    ctx.timer_start()
     for _ in range(kh):
         outs = ctx.rotate_hoisted(ct, stencil)
     ms_hoist = max_over_ranks(ctx.timer_stop())
     del outs
 
     # e2e: the C ABI with host buffers, H2D + conv + D2H inside the timed region
+    import ctypes as C
+    from paper_2306_09189_b200 import _lib
+    from paper_2306_09189_b200.engine import lib
     N = ctx.N
     h_in = torch.empty(2 * (level + 1) * N, dtype=torch.int64, pin_memory=True)
     h_out = torch.empty(2 * level * N, dtype=torch.int64, pin_memory=True)
     h_in.numpy().view(np.uint64)[:] = ct.residues().ravel()
-    import ctypes as C
-    from paper_2306_09189_b200 import _lib
-    from paper_2306_09189_b200.engine import lib
     L_ = lib()
     pin_in = C.cast(h_in.data_ptr(), _lib.u64p)
     pin_out = C.cast(h_out.data_ptr(), _lib.u64p)
@@ -244,33 +253,36 @@ def run_ours(args, rank, world, local_rank):
         ctx.conv2d_into(ct_dev, layer, approach, out)
         assert L_.fhe_ct_download(ctx.h, out.h, pin_out, h_out.numel()) == 0  # synchronises
     e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e_err = float(np.abs(ctx.decrypt(out)[: C_OUT * M * M] - ref.ravel()).max())
+    e2e_err = float(np.abs(ctx.decrypt(out)[: C_OUT * M * M] - ref).max())
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return None
 
-    bm = byte_model(ctx, level, approach)
     step_s = ms_max / 1e3 / args.steps
     value = world * args.steps / (ms_max / 1e3)
-    # dominant kernel class by device time inside the timed region
-    dom = max(prof, key=lambda c: prof[c][0])
-    dom_ms, dom_n = prof[dom]
     peak, peak_kind = measured_peak()
-    if dom == "conv_mac":
-        alg = bm["conv_mac"]
-        note = ("conv_mac: fused key-switch inner product + plaintext MAC + channel sum for one source; "
-                f"algorithmic bytes/launch = {KAPPA * KAPPA - 1 if approach == 2 else C_IN - 1} keys x "
-                f"{bm['key'] / 1e6:.2f} MB + plaintexts + source ciphertext")
-    else:
-        alg = None
-        note = f"dominant class {dom}"
-    avg_s = dom_ms / 1e3 / max(dom_n, 1)
-    achieved = alg / avg_s / 1e9 if alg else None
+    kernels = {}
+    for cls, (kms, kn, kbytes) in prof.items():
+        if kn == 0:
+            continue
+        gbs = kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+        kernels[cls] = {"ms_per_step": round(kms / args.steps, 4), "share": round(kms / ms, 3),
+                        "launches_per_step": round(kn / args.steps, 1),
+                        "algorithmic_mb_per_launch": round(kbytes / kn / 1e6, 2),
+                        "achieved_gbs": round(gbs, 1), "frac_hbm": round(gbs / peak, 3),
+                        "note": KERNEL_NOTES.get(cls, "")}
+    dom = max(kernels, key=lambda c: kernels[c]["ms_per_step"])
+    dms, dn_, dbytes = prof[dom]
+    avg_s = dms / 1e3 / dn_
+    achieved = dbytes / dn_ / avg_s / 1e9
+    ks_cls = [c for c in ("ks_multi", "ks_inner") if c in kernels]
+    ks_bytes = sum(prof[c][2] for c in ks_cls)
+    ks_ms = sum(prof[c][0] for c in ks_cls)
     cpu = cpu_baseline(args) if not args.no_cpu else None
     line = {
-        "metric": "homomorphic convs/sec at N=2^15 (cfg3, Approach 2)",
+        "metric": "homomorphic convs/sec at N=2^15 (cfg3 3x3 16->16 conv layer)",
         "value": round(value, 3),
         "unit": "conv/s",
         "n_gpus": world,
@@ -282,21 +294,24 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "u64 (RNS residues mod 40-60-bit primes)",
         "data": "synthetic (seeded U[-1,1] image/weights, BASELINE cfg3 shapes); no dataset involved",
-        "config": {"workload": WORKLOAD, "approach": approach, "batch_per_gpu": 1, "parallelism": f"replicas x{world}",
-                   "l2": "no flush: per-step key stream (1.27 GB) >> 126 MB L2", "key_seed": 7,
+        "config": {"workload": WORKLOAD, "approach": approach,
+                   "schedule": {0: "auto (BSGS: hoisted channel rotations + aggregated shifts)", 1: "paper Approach 1",
+                                2: "paper Approach 2", 3: "BSGS, hoisted channel rotations",
+                                4: "BSGS, hoisted shifts"}[approach],
+                   "batch_per_gpu": 1, "parallelism": f"replicas x{world}",
+                   "l2": "no flush: per-step key stream (23 Galois keys, 1.27 GB) >> 126 MB L2", "key_seed": 7,
                    "enc_seed": 9000, "decrypt_max_abs_err": err},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1) if achieved else None,
-                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
-                     "traffic": ncu_traffic(dom), "algorithmic_bytes_per_launch": alg,
-                     "avg_launch_ms": round(avg_s * 1e3, 4), "launches": dom_n, "peak_kind": peak_kind,
-                     "note": note},
-        "conv_roofline": {"algorithmic_bytes_per_conv": bm["conv"],
-                          "achieved_gbs": round(bm["conv"] / step_s / 1e9, 1),
-                          "frac": round(bm["conv"] / step_s / 1e9 / peak, 4)},
-        "kernel_ms_per_step": {c: round(prof[c][0] / args.steps, 4) for c in classes},
-        "approach1_conv_per_s" if approach == 2 else "approach2_conv_per_s":
-            round(world * k2 / (ms_other / 1e3), 3),
-        "hoisted_rot_per_s": round(world * kh * 8 / (ms_hoist / 1e3), 1),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dom),
+                     "algorithmic_bytes_per_launch": round(dbytes / dn_), "avg_launch_ms": round(avg_s * 1e3, 4),
+                     "peak_kind": peak_kind, "note": KERNEL_NOTES.get(dom, "") +
+                     ("; NTT-class kernels are integer-pipe bound (see kernels[].frac_hbm and profiles/)"
+                      if dom.startswith("ntt") else "")},
+        "keyswitch_roofline": {"kernels": ks_cls, "achieved_gbs": round(ks_bytes / (ks_ms / 1e3) / 1e9, 1) if ks_ms else None,
+                               "frac": round(ks_bytes / (ks_ms / 1e3) / 1e9 / peak, 4) if ks_ms else None},
+        "kernels": kernels,
+        "conv_per_s_by_approach": {str(k): round(v, 2) for k, v in per_approach.items()},
+        "hoisted_rot_per_s": round(world * kh * len(stencil) / (ms_hoist / 1e3), 1),
         "e2e": {"value": round(world * args.steps / e2e_s, 3), "unit": "conv/s",
                 "h2d_bytes_per_step": int(h_in.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
                 "api": "fhe_ct_upload_into + fhe_conv2d_into + fhe_ct_download (C ABI, pinned host buffers)",
@@ -383,7 +398,7 @@ def run_reference(args, rank):
     value = n / total
     line = {
         "impl": "reference",
-        "metric": "homomorphic convs/sec at N=2^15 (cfg3, Approach 2)",
+        "metric": "homomorphic convs/sec at N=2^15 (cfg3 3x3 16->16 conv layer)",
         "value": round(value, 3), "unit": "conv/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64 (emulated slots)",
@@ -404,7 +419,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--approach", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--approach", type=int, default=0, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-golden", action="store_true", help="skip the golden-model CKKS CPU timing")
     args = ap.parse_args()

@@ -85,9 +85,13 @@ int fhe_synchronize(fhe_ctx* ctx);
 int fhe_timer_start(fhe_ctx* ctx);
 int fhe_timer_stop(fhe_ctx* ctx, float* ms); /* synchronises; ms since fhe_timer_start */
 /* per-kernel-class CUDA-event profiling of the hot kernels (off by default).
- * class names: "conv_mac", "ks_inner", "ntt", "modup_bconv", "moddown", "rescale" */
+ * class names: "ntt", "ntt_modup", "ntt_moddown", "ks_multi", "pt_matvec",
+ * "ks_inner", "conv_mac", "moddown", "rescale" */
 int fhe_prof_enable(fhe_ctx* ctx, int on);
 int fhe_prof_get(fhe_ctx* ctx, const char* kernel_class, double* total_ms, uint64_t* launches);
+/* same + the algorithmic (compulsory) bytes of those launches: every input
+ * read once, every output written once, intermediates inside a launch excluded */
+int fhe_prof_get_bytes(fhe_ctx* ctx, const char* kernel_class, double* total_ms, uint64_t* launches, double* bytes);
 int fhe_prof_reset(fhe_ctx* ctx);
 /* micro-benchmark of the NTT kernels: nrows rows at the top level's primes,
  * `iters` transforms; *ms = device time per transform launch */

@@ -47,6 +47,7 @@ SIGNATURES = [
     ("fhe_timer_stop", C.c_int, [vp, C.POINTER(C.c_float)]),
     ("fhe_prof_enable", C.c_int, [vp, C.c_int]),
     ("fhe_prof_get", C.c_int, [vp, C.c_char_p, C.POINTER(C.c_double), u64p]),
+    ("fhe_prof_get_bytes", C.c_int, [vp, C.c_char_p, C.POINTER(C.c_double), u64p, C.POINTER(C.c_double)]),
     ("fhe_prof_reset", C.c_int, [vp]),
     ("fhe_profiler_range", C.c_int, [C.c_int]),
     ("fhe_bench_ntt", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),

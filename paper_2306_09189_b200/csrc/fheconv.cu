@@ -70,6 +70,7 @@ struct fhe_ctx {
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
         double ms = 0;
         uint64_t n = 0;
+        double bytes = 0;  // algorithmic (compulsory) bytes of the launches
     };
     std::map<std::string, ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
@@ -84,8 +85,10 @@ struct fhe_ctx {
         ck(cudaEventCreate(&e), "cudaEventCreate");
         return e;
     }
+    // algorithmic bytes of `rows` residue rows
+    double rows(double r) const { return r * (double)N * 8.0; }
     template <class F>
-    void timed(const char* cls, F&& f) {
+    void timed(const char* cls, double bytes, F&& f) {
         if (!prof_on) {
             f();
             return;
@@ -95,6 +98,7 @@ struct fhe_ctx {
         f();
         cudaEventRecord(b, st);
         prof[cls].pending.emplace_back(a, b);
+        prof[cls].bytes += bytes;
     }
     void prof_collect() {
         ck(cudaStreamSynchronize(st), "sync");
@@ -224,9 +228,9 @@ void modup_batch(fhe_ctx* c, const uint64_t* c1, size_t stride, int nsrc, int le
     uint64_t* coef = c->alloc((size_t)nsrc * rowsw);
     ck(cudaMemcpy2DAsync(coef, rowsw * 8, c1, stride * 8, rowsw * 8, nsrc, cudaMemcpyDeviceToDevice, c->st),
        "memcpy2d");
-    c->timed("ntt", [&] { ntt_inverse(c->dc, coef, nsrc * nr, qmap(c, level), c->st); });
+    c->timed("ntt", c->rows(2.0 * nsrc * nr), [&] { ntt_inverse(c->dc, coef, nsrc * nr, qmap(c, level), c->st); });
     (void)ne;
-    c->timed("ntt_modup", [&] {
+    c->timed("ntt_modup", c->rows(2.0 * nsrc * nr + (double)nsrc * dn * ne), [&] {
         ntt_modup(c->dc, digits, coef, c1, stride, nsrc, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
     });
     c->release(coef);
@@ -242,9 +246,9 @@ void moddown_strided(fhe_ctx* c, const uint64_t* acc, size_t acc_stride, int lev
     const int nr = level + 1;
     uint64_t* pc = c->alloc((size_t)npoly * c->K * c->N);
     uint64_t* conv = c->alloc((size_t)npoly * nr * c->N);
-    c->timed("moddown", [&] { gather_special(c->dc, pc, acc, acc_stride, level, npoly, c->st); });
-    c->timed("ntt", [&] { ntt_inverse(c->dc, pc, npoly * c->K, RowMap{c->K, -1, c->L, 0}, c->st); });
-    c->timed("ntt_moddown",
+    c->timed("moddown", c->rows(2.0 * npoly * c->K), [&] { gather_special(c->dc, pc, acc, acc_stride, level, npoly, c->st); });
+    c->timed("ntt", c->rows(2.0 * npoly * c->K), [&] { ntt_inverse(c->dc, pc, npoly * c->K, RowMap{c->K, -1, c->L, 0}, c->st); });
+    c->timed("ntt_moddown", c->rows((double)npoly * (c->K + 2 * nr) + (add_src ? nr : 0)),
              [&] { ntt_moddown(c->dc, conv, pc, acc, acc_stride, out, c->d_md, level, npoly, add_src, g, c->st); });
     c->release(pc);
     c->release(conv);
@@ -262,7 +266,7 @@ void rotate_from_digits(fhe_ctx* c, const fhe_ct* ct, const uint64_t* digits, ui
     const int level = ct->level, ne = c->ne_at(level);
     uint64_t* acc = c->alloc((size_t)2 * ne * c->N);
     const uint64_t* key = c->key_for(g);
-    c->timed("ks_inner", [&] {
+    c->timed("ks_inner", c->rows(3.0 * c->dn_at(level) * ne + 2.0 * ne), [&] {
         ks_inner_product(c->dc, digits, key, acc, acc + (size_t)ne * c->N, g, level, c->dn_at(level), c->st);
     });
     moddown(c, acc, level, 2, out, ct->c0(), g);
@@ -277,10 +281,10 @@ void rescale_into(fhe_ctx* c, const uint64_t* in, int level, uint64_t* out) {
     ck(cudaMemcpyAsync(tmp, in + (size_t)level * N, N * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
     ck(cudaMemcpyAsync(tmp + N, in + ((size_t)level + 1 + level) * N, N * 8, cudaMemcpyDeviceToDevice, c->st),
        "memcpy");
-    c->timed("ntt", [&] { ntt_inverse(c->dc, tmp, 2, RowMap{1, -1, level, 0}, c->st); });
-    c->timed("rescale", [&] { rescale_spread(c->dc, tmp, spread, level, c->st); });
-    c->timed("ntt", [&] { ntt_forward(c->dc, spread, 2 * level, qmap(c, level - 1), c->st); });
-    c->timed("rescale", [&] {
+    c->timed("ntt", c->rows(4), [&] { ntt_inverse(c->dc, tmp, 2, RowMap{1, -1, level, 0}, c->st); });
+    c->timed("rescale", c->rows(2.0 + 2.0 * level), [&] { rescale_spread(c->dc, tmp, spread, level, c->st); });
+    c->timed("ntt", c->rows(4.0 * level), [&] { ntt_forward(c->dc, spread, 2 * level, qmap(c, level - 1), c->st); });
+    c->timed("rescale", c->rows(2.0 * (level + 1) + 4.0 * level), [&] {
         rescale_finish(c->dc, out, in, spread, level, c->d_qlinv + (size_t)level * c->L,
                        c->d_qlinv_sh + (size_t)level * c->L, c->st);
     });
@@ -603,7 +607,7 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
         for (int b = 0; b < B.nb; ++b) {
             if (!t.gmask[b]) continue;
             if (t.galois[b] == 1) {
-                c->timed("ks_multi", [&] { identity_term(c->dc, XT + (size_t)b * 2 * extw, ct->d, c->d_md, level, c->st); });
+                c->timed("ks_multi", c->rows(2.0 * nr + 2.0 * ne), [&] { identity_term(c->dc, XT + (size_t)b * 2 * extw, ct->d, c->d_md, level, c->st); });
                 continue;
             }
             ks.galois[ks.n] = t.galois[b];
@@ -612,18 +616,20 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
             ks.slot[ks.n] = b;
             ks.n++;
         }
-        c->timed("ks_multi", [&] { ks_stream(c->dc, ks, 0, c->d_md, level, dn, c->st); });
+        c->timed("ks_multi", c->rows((double)ks.n * (2.0 * dn * ne + 2.0 * ne) + (double)dn * ne + nr), [&] { ks_stream(c->dc, ks, 0, c->d_md, level, dn, c->st); });
     }
     for (int g0 = 0; g0 < B.ngi; g0 += kMaxGiant) {
         t.ngi = std::min(kMaxGiant, B.ngi - g0);
         t.g0 = g0;
+        double pt_pairs = 0;
         for (int b = 0; b < B.nb; ++b) {
             uint32_t mask = 0;
             for (int gi = 0; gi < t.ngi; ++gi)
                 if (B.nonempty[(size_t)(g0 + gi) * B.nb + b]) mask |= 1u << gi;
             t.gmask[b] = mask;
+            pt_pairs += __builtin_popcount(mask);
         }
-        c->timed("pt_matvec", [&] { pt_matvec(c->dc, Y + (size_t)g0 * 2 * extw, XT, t, level, c->st); });
+        c->timed("pt_matvec", c->rows(pt_pairs * ne + 2.0 * B.nb * ne + 2.0 * t.ngi * ne), [&] { pt_matvec(c->dc, Y + (size_t)g0 * 2 * extw, XT, t, level, c->st); });
     }
     // giant steps: ModDown each aggregated Y_g, ModUp, key-switch-accumulate
     uint64_t* acc = c->alloc(2 * extw);
@@ -679,7 +685,7 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
                 ks.c0[s] = Y + (size_t)gi * 2 * extw;
                 c->ledger.key_switches++;
             }
-            c->timed("ks_inner", [&] { ks_stream(c->dc, ks, 1, c->d_md, level, dn, c->st); });
+            c->timed("ks_inner", c->rows((double)ks.n * (3.0 * dn * ne + ne) + 4.0 * ne), [&] { ks_stream(c->dc, ks, 1, c->d_md, level, dn, c->st); });
         }
         c->release(dg);
     }
@@ -745,7 +751,10 @@ void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
     auto pt_of = [&](int r, int i) { return ly->d_pts + ((size_t)r * nk + i) * extw; };
     auto run_terms = [&](MacTerms& t, const fhe_ct& src) {
         if (t.n == 0) return;
-        c->timed("conv_mac", [&] { conv_mac(c->dc, acc, dtmp, src.d, t, c->d_md, level, dn, c->st); });
+        double mac_rows = (double)t.n * ne + (double)dn * ne + 2.0 * nr + 4.0 * ne;
+        for (int i = 0; i < t.n; ++i)
+            if (t.galois[i] != 1) mac_rows += 2.0 * dn * ne;
+        c->timed("conv_mac", c->rows(mac_rows), [&] { conv_mac(c->dc, acc, dtmp, src.d, t, c->d_md, level, dn, c->st); });
         for (int i = 0; i < t.n; ++i)
             if (t.galois[i] != 1) c->ledger.key_switches++;
         t.n = 0;
@@ -927,11 +936,16 @@ int fhe_prof_enable(fhe_ctx* c, int on) {
 }
 
 int fhe_prof_get(fhe_ctx* c, const char* cls, double* total_ms, uint64_t* launches) {
+    return fhe_prof_get_bytes(c, cls, total_ms, launches, nullptr);
+}
+
+int fhe_prof_get_bytes(fhe_ctx* c, const char* cls, double* total_ms, uint64_t* launches, double* bytes) {
     return guard(c, [&] {
         c->prof_collect();
         auto it = c->prof.find(cls);
         if (total_ms) *total_ms = it == c->prof.end() ? 0.0 : it->second.ms;
         if (launches) *launches = it == c->prof.end() ? 0 : it->second.n;
+        if (bytes) *bytes = it == c->prof.end() ? 0.0 : it->second.bytes;
     });
 }
 

@@ -182,10 +182,16 @@ class Context:
         self._check(lib().fhe_prof_reset(self.h))
 
     def prof_get(self, cls: str) -> tuple[float, int]:
+        ms, n, _ = self.prof_get_bytes(cls)
+        return ms, n
+
+    def prof_get_bytes(self, cls: str) -> tuple[float, int, float]:
+        """(device ms, launches, algorithmic bytes) of a kernel class since prof_reset."""
         ms = C.c_double(0)
         n = C.c_uint64(0)
-        self._check(lib().fhe_prof_get(self.h, cls.encode(), C.byref(ms), C.byref(n)))
-        return ms.value, n.value
+        b = C.c_double(0)
+        self._check(lib().fhe_prof_get_bytes(self.h, cls.encode(), C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
 
     # ---------------------------------------------------------------- keys
     def keygen(self, seed: int):
