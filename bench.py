@@ -43,6 +43,22 @@ WORKLOAD = ("cfg3: CKKS N=2^15 (16384 slots), 60+12x50-bit q | 2x60-bit p, scale
             "U[-1,1]; 3x3 conv 16->16 same padding, weights U[-1,1]; + 1 rescale; 1 ciphertext per step")
 
 
+def job_value(world, units_per_rank, max_elapsed_s):
+    """Whole-job throughput: every rank processed units_per_rank units; the job
+    took as long as the slowest rank (device time, max over ranks)."""
+    return world * units_per_rank / max_elapsed_s
+
+
+def reduce_max(value, dist, device=None):
+    """Max of a per-rank float over the process group (identity without one)."""
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -174,11 +190,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     def max_over_ranks(v):
-        if not dist:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(v, dist, "cuda")
 
     def timed_convs(ap, steps, warmup):
         for _ in range(warmup):
@@ -261,7 +273,7 @@ def run_ours(args, rank, world, local_rank):
         return None
 
     step_s = ms_max / 1e3 / args.steps
-    value = world * args.steps / (ms_max / 1e3)
+    value = job_value(world, args.steps, ms_max / 1e3)
     peak, peak_kind = measured_peak()
     kernels = {}
     for cls, (kms, kn, kbytes) in prof.items():
@@ -416,7 +428,7 @@ def run_reference(args, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--approach", type=int, default=0, choices=[0, 1, 2, 3, 4])
