@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libfheconv.so")
+LIB_PATH = os.environ.get("FHECONV_LIB") or os.path.join(PKG, "libfheconv.so")
 
 u64p = C.POINTER(C.c_uint64)
 i64p = C.POINTER(C.c_int64)

@@ -42,8 +42,8 @@ __constant__ uint64_t c_cdt[FHE_CDT_LEN] = {FHE_CDT_VALUES};
 __global__ void k_reduce_signed_rows(DevCtx c, const int64_t* coef, uint64_t* out, int nrows, RowMap rm) {
     const size_t total = (size_t)nrows * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / c.N);
-        const int k = (int)(i % c.N);
+        const int r = (int)(i >> c.logN);
+        const int k = (int)(i & (size_t)(c.N - 1));
         const Prime pr = c.primes[row_prime(rm, r % rm.rows_per_poly)];
         out[i] = reduce_signed(coef[k], pr);
     }
@@ -52,8 +52,8 @@ __global__ void k_reduce_signed_rows(DevCtx c, const int64_t* coef, uint64_t* ou
 __global__ void k_sample_uniform(DevCtx c, uint64_t* out, int nrows, RowMap rm, uint64_t key) {
     const size_t total = (size_t)nrows * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / c.N);
-        const int k = (int)(i % c.N);
+        const int r = (int)(i >> c.logN);
+        const int k = (int)(i & (size_t)(c.N - 1));
         const int p = row_prime(rm, r % rm.rows_per_poly);
         const uint64_t ctr = 2 * ((uint64_t)p * c.N + k);
         out[i] = uniform_mod(prng_k(key, ctr), prng_k(key, ctr + 1), c.primes[p]);
@@ -81,8 +81,8 @@ __global__ void k_keygen_combine(DevCtx c, uint64_t* b, const uint64_t* a, const
                                  uint32_t galois, int lo, int hi, const ModDownTable* md, int nrows) {
     const size_t total = (size_t)nrows * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int t = (int)(i / c.N);
-        const uint32_t k = (uint32_t)(i % c.N);
+        const int t = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         const Prime pr = c.primes[t];
         uint64_t v = sub_mod(e[i], mul_mod(a[i], s[i], pr), pr.q);
         if (t >= lo && t < hi) {
@@ -97,7 +97,7 @@ __global__ void k_encrypt_combine(DevCtx c, uint64_t* c0, const uint64_t* c1, co
                                   const uint64_t* s, const uint64_t* pt, int nrows) {
     const size_t total = (size_t)nrows * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const Prime pr = c.primes[i / c.N];
+        const Prime pr = c.primes[(i >> c.logN)];
         const uint64_t v = sub_mod(e[i], mul_mod(c1[i], s[i], pr), pr.q);
         c0[i] = add_mod(v, pt[i], pr.q);
     }
@@ -107,7 +107,7 @@ __global__ void k_decrypt_combine(DevCtx c, uint64_t* m, const uint64_t* c0, con
                                   const uint64_t* s, int nrows) {
     const size_t total = (size_t)nrows * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const Prime pr = c.primes[i / c.N];
+        const Prime pr = c.primes[(i >> c.logN)];
         m[i] = add_mod(c0[i], mul_mod(c1[i], s[i], pr), pr.q);
     }
 }
@@ -158,7 +158,7 @@ __global__ void k_ew(DevCtx c, uint64_t* out, const uint64_t* a, const uint64_t*
     const size_t total = (size_t)nrows * c.N;
     const size_t polyw = (size_t)rpp * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int u = (int)((i / c.N) % rpp);
+        const int u = (int)((i >> c.logN) % rpp);
         const Prime pr = c.primes[u];
         if (OP == 0) out[i] = add_mod(a[i], b[i], pr.q);
         if (OP == 1) out[i] = sub_mod(a[i], b[i], pr.q);
@@ -169,8 +169,8 @@ __global__ void k_ew(DevCtx c, uint64_t* out, const uint64_t* a, const uint64_t*
 __global__ void k_automorph(DevCtx c, uint64_t* out, const uint64_t* in, int nrows, uint32_t g) {
     const size_t total = (size_t)nrows * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const size_t r = i / c.N;
-        const uint32_t k = (uint32_t)(i % c.N);
+        const size_t r = i >> c.logN;
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         out[i] = in[r * c.N + perm_index(k, g, c.logN)];
     }
 }
@@ -179,9 +179,9 @@ __global__ void k_rescale_spread(DevCtx c, const uint64_t* tmp, uint64_t* spread
     const size_t total = (size_t)2 * level * c.N;
     const uint64_t ql = c.primes[level].q;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / c.N);
+        const int r = (int)(i >> c.logN);
         const int p = r / level, t = r % level;
-        const int k = (int)(i % c.N);
+        const int k = (int)(i & (size_t)(c.N - 1));
         const uint64_t v = tmp[(size_t)p * c.N + k];
         const Prime pr = c.primes[t];
         uint64_t o;
@@ -199,9 +199,9 @@ __global__ void k_rescale_finish(DevCtx c, uint64_t* out, const uint64_t* in, co
                                  const uint64_t* qlinv, const uint64_t* qlinv_sh) {
     const size_t total = (size_t)2 * level * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / c.N);
+        const int r = (int)(i >> c.logN);
         const int p = r / level, t = r % level;
-        const int k = (int)(i % c.N);
+        const int k = (int)(i & (size_t)(c.N - 1));
         const uint64_t q = c.primes[t].q;
         const uint64_t x = in[((size_t)p * (level + 1) + t) * c.N + k];
         out[i] = mul_shoup(sub_mod(x, spread[i], q), qlinv[t], qlinv_sh[t], q);
@@ -251,9 +251,9 @@ __global__ void k_modup_bconv(DevCtx c, const uint64_t* coef_all, const uint64_t
     const size_t total = (size_t)nsrc * dn * c.N;
     RowMap rm{ne, level, c.L, 0};
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int sj = (int)(i / c.N);
+        const int sj = (int)(i >> c.logN);
         const int src = sj / dn, j = sj % dn;
-        const int k = (int)(i % c.N);
+        const int k = (int)(i & (size_t)(c.N - 1));
         const uint64_t* coef = coef_all + (size_t)src * nr * c.N;
         const uint64_t* c1_ntt = c1_all + (size_t)src * src_stride;
         uint64_t* digits = digits_all + (size_t)src * dn * ne * c.N;
@@ -295,8 +295,8 @@ __global__ void k_ks_inner(DevCtx c, const uint64_t* D, const uint64_t* key, uin
     const size_t total = (size_t)ne * c.N;
     RowMap rm{ne, level, c.L, 0};
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int u = (int)(i / c.N);
-        const uint32_t k = (uint32_t)(i % c.N);
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         const int p = row_prime(rm, u);
         const Prime pr = c.primes[p];
         const uint32_t pk = perm_index(k, g, c.logN);
@@ -315,9 +315,9 @@ __global__ void k_gather_special(DevCtx c, uint64_t* dst, const uint64_t* acc, s
                                  int npoly) {
     const size_t total = (size_t)npoly * c.K * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / c.N);
+        const int r = (int)(i >> c.logN);
         const int p = r / c.K, kk = r % c.K;
-        dst[i] = acc[(size_t)p * acc_stride + ((size_t)level + 1 + kk) * c.N + (i % c.N)];
+        dst[i] = acc[(size_t)p * acc_stride + ((size_t)level + 1 + kk) * c.N + (i & (size_t)(c.N - 1))];
     }
 }
 
@@ -326,8 +326,8 @@ __global__ void k_moddown_bconv(DevCtx c, const uint64_t* pcoef, uint64_t* conv,
     const int nr = level + 1;
     const size_t total = (size_t)npoly * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int p = (int)(i / c.N);
-        const int k = (int)(i % c.N);
+        const int p = (int)(i >> c.logN);
+        const int k = (int)(i & (size_t)(c.N - 1));
         uint64_t v[kMaxAlpha];
         int neg = 0;
 #pragma unroll
@@ -356,9 +356,9 @@ __global__ void k_moddown_finish(DevCtx c, uint64_t* out, const uint64_t* acc, c
     const int nr = level + 1, ne = nr + c.K;
     const size_t total = (size_t)npoly * nr * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / c.N);
+        const int r = (int)(i >> c.logN);
         const int p = r / nr, t = r % nr;
-        const uint32_t k = (uint32_t)(i % c.N);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         const uint64_t q = c.primes[t].q;
         const uint64_t x = acc[((size_t)p * ne + t) * c.N + k];
         uint64_t o = mul_shoup(sub_mod(x, conv[i], q), md->pinvq[t], md->pinvq_sh[t], q);
@@ -376,8 +376,8 @@ __global__ void __launch_bounds__(256) k_conv_mac(DevCtx c, uint64_t* acc, const
     const size_t plane = total;  // ACC = [2][ne][N]
     RowMap rm{ne, level, c.L, 0};
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int u = (int)(i / c.N);
-        const uint32_t k = (uint32_t)(i % c.N);
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         const int p = row_prime(rm, u);
         const Prime pr = c.primes[p];
         const bool qrow = u < nr;
@@ -540,8 +540,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_ks_stream(DevCtx c, KsStream
     auto slot = [&](int stage, int w) -> ulonglong2* { return sbuf + ((size_t)stage * 3 * DN + w) * kStreamThreads + tid; };
     for (size_t ip = blockIdx.x * (size_t)blockDim.x + tid; ip < total / 2; ip += (size_t)gridDim.x * blockDim.x) {
         const size_t i = ip * 2;
-        const int u = (int)(i / c.N);
-        const uint32_t k = (uint32_t)(i % c.N);
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         const int p = row_prime(rm, u);
         const Prime pr = c.primes[p];
         const bool qrow = u < nr;
@@ -613,8 +613,8 @@ __global__ void k_identity_term(DevCtx c, uint64_t* xt, const uint64_t* X, const
     const int nr = level + 1, ne = nr + c.K;
     const size_t total = (size_t)ne * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int u = (int)(i / c.N);
-        const size_t k = i % c.N;
+        const int u = (int)(i >> c.logN);
+        const size_t k = i & (size_t)(c.N - 1);
         if (u < nr) {
             const uint64_t q = c.primes[u].q;
             xt[i] = mul_shoup(X[(size_t)u * c.N + k], md->pmod[u], md->pmod_sh[u], q);
@@ -637,8 +637,8 @@ __global__ void __launch_bounds__(256) k_ks_multi(DevCtx c, uint64_t* XT, const 
     RowMap rm{ne, level, c.L, 0};
     for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < pairs; ip += (size_t)gridDim.x * blockDim.x) {
         const size_t i = ip * 2;
-        const int u = (int)(i / c.N);
-        const uint32_t k = (uint32_t)(i % c.N);
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         const int p = row_prime(rm, u);
         const Prime pr = c.primes[p];
         const bool qrow = u < nr;
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(256) k_pt_matvec(DevCtx c, uint64_t* Y, const 
     const size_t total = (size_t)ne * c.N;
     RowMap rm{ne, level, c.L, 0};
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int u = (int)(i / c.N);
+        const int u = (int)(i >> c.logN);
         const Prime pr = c.primes[row_prime(rm, u)];
         U128 a0[NG], a1[NG];
 #pragma unroll
@@ -715,6 +715,62 @@ __global__ void __launch_bounds__(256) k_pt_matvec(DevCtx c, uint64_t* Y, const 
     }
 }
 
+// Plaintext mat-vec on coefficient pairs: the baby-step terms X~_b of the
+// thread's pair are staged once in private shared-memory slots, then every
+// giant accumulator streams its plaintexts with 16-byte loads.
+constexpr int kMatvecThreads = 128;
+__global__ void __launch_bounds__(kMatvecThreads) k_pt_matvec2(DevCtx c, uint64_t* Y, const uint64_t* XT,
+                                                               BabyTerms t, int level) {
+    extern __shared__ ulonglong2 xs[];  // [nb][2][kMatvecThreads]
+    const int ne = level + 1 + c.K;
+    const size_t total = (size_t)ne * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    const int tid = threadIdx.x;
+    for (size_t ip = blockIdx.x * (size_t)blockDim.x + tid; ip < total / 2; ip += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = ip * 2;
+        const int u = (int)(i >> c.logN);
+        const Prime pr = c.primes[row_prime(rm, u)];
+        for (int b = 0; b < t.nb; ++b) {
+            if (t.gmask[b] == 0) continue;
+            xs[(b * 2 + 0) * kMatvecThreads + tid] = vld2_cs(XT + (size_t)b * 2 * total + i);
+            xs[(b * 2 + 1) * kMatvecThreads + tid] = vld2_cs(XT + (size_t)b * 2 * total + total + i);
+        }
+        for (int g = 0; g < t.ngi; ++g) {
+            U128 a0[2] = {{0, 0}, {0, 0}}, a1[2] = {{0, 0}, {0, 0}};
+            const uint64_t* pg = t.pts + ((size_t)(t.g0 + g) * t.nb_total) * total + i;
+            int b = 0;
+            for (; b + 4 <= t.nb; b += 4) {
+                ulonglong2 w[4];
+#pragma unroll
+                for (int d = 0; d < 4; ++d)
+                    w[d] = ((t.gmask[b + d] >> g) & 1u) ? vld2_cs(pg + (size_t)(b + d) * total) : make_ulonglong2(0, 0);
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const ulonglong2 x0 = xs[((b + d) * 2 + 0) * kMatvecThreads + tid];
+                    const ulonglong2 x1 = xs[((b + d) * 2 + 1) * kMatvecThreads + tid];
+                    mac(a0[0], w[d].x, x0.x);
+                    mac(a0[1], w[d].y, x0.y);
+                    mac(a1[0], w[d].x, x1.x);
+                    mac(a1[1], w[d].y, x1.y);
+                }
+            }
+            for (; b < t.nb; ++b) {
+                if (!((t.gmask[b] >> g) & 1u)) continue;
+                const ulonglong2 w = vld2_cs(pg + (size_t)b * total);
+                const ulonglong2 x0 = xs[(b * 2 + 0) * kMatvecThreads + tid];
+                const ulonglong2 x1 = xs[(b * 2 + 1) * kMatvecThreads + tid];
+                mac(a0[0], w.x, x0.x);
+                mac(a0[1], w.y, x0.y);
+                mac(a1[0], w.x, x1.x);
+                mac(a1[1], w.y, x1.y);
+            }
+            uint64_t* y = Y + (size_t)g * 2 * total;
+            st2(y + i, reduce128(a0[0].hi, a0[0].lo, pr), reduce128(a0[1].hi, a0[1].lo, pr));
+            st2(y + total + i, reduce128(a1[0].hi, a1[0].lo, pr), reduce128(a1[1].hi, a1[1].lo, pr));
+        }
+    }
+}
+
 template <int DN>
 __global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc, const uint64_t* D,
                                                          const uint64_t* key, const uint64_t* c0, uint32_t g,
@@ -726,8 +782,8 @@ __global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc
     for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < total / 2;
          ip += (size_t)gridDim.x * blockDim.x) {
         const size_t i = ip * 2;
-        const int u = (int)(i / c.N);
-        const uint32_t k = (uint32_t)(i % c.N);
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         const int p = row_prime(rm, u);
         const Prime pr = c.primes[p];
         const uint32_t pk = perm_index(k, g, c.logN);
@@ -759,8 +815,8 @@ __global__ void __launch_bounds__(256, 1) k_ks_accumulate_multi(DevCtx c, uint64
     for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < total / 2;
          ip += (size_t)gridDim.x * blockDim.x) {
         const size_t i = ip * 2;
-        const int u = (int)(i / c.N);
-        const uint32_t k = (uint32_t)(i % c.N);
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
         const int p = row_prime(rm, u);
         const Prime pr = c.primes[p];
         U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
@@ -789,7 +845,7 @@ __global__ void k_qp_add(DevCtx c, uint64_t* acc, const uint64_t* y, int level) 
     const size_t total = (size_t)2 * ne * c.N;
     RowMap rm{ne, level, c.L, 0};
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int u = (int)((i / c.N) % ne);
+        const int u = (int)((i >> c.logN) % ne);
         acc[i] = add_mod(acc[i], y[i], c.primes[row_prime(rm, u)].q);
     }
 }
@@ -849,18 +905,12 @@ void identity_term(const DevCtx& c, uint64_t* xt, const uint64_t* ct, const ModD
 
 void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms& t, int level, cudaStream_t st) {
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
-    const int blocks = ew_blocks(total);
+    const size_t smem = (size_t)t.nb * 2 * kMatvecThreads * sizeof(ulonglong2);
+    int blocks = (int)((total / 2 + kMatvecThreads - 1) / kMatvecThreads);
+    blocks = blocks < 148 * 12 ? blocks : 148 * 12;
     ++g_launches;
-    if (t.ngi <= 4)
-        k_pt_matvec<4><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
-    else if (t.ngi <= 8)
-        k_pt_matvec<8><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
-    else if (t.ngi <= 9)
-        k_pt_matvec<9><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
-    else if (t.ngi <= 12)
-        k_pt_matvec<12><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
-    else
-        k_pt_matvec<16><<<blocks, 256, 0, st>>>(c, Y, XT, t, level);
+    cudaFuncSetAttribute(k_pt_matvec2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_pt_matvec2<<<blocks, kMatvecThreads, smem, st>>>(c, Y, XT, t, level);
 }
 
 void ks_accumulate(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* key, const uint64_t* c0,

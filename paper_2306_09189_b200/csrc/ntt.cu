@@ -27,7 +27,11 @@ __device__ __forceinline__ int pad(int x) { return x + (x >> 4); }
 #ifndef FHE_NTT_EPT
 #define FHE_NTT_EPT 16
 #endif
+#ifndef FHE_NTT_THREADS
+#define FHE_NTT_THREADS 128
+#endif
 constexpr int EPT = FHE_NTT_EPT;         // residues per thread in a pass
+constexpr int NTT_THREADS = FHE_NTT_THREADS;
 constexpr int LOG_EPT = EPT == 16 ? 4 : 3;
 
 // One radix-2^R pass of forward CT butterflies on EPT register values that
@@ -198,7 +202,7 @@ enum { FUSE_NONE = 0, FUSE_MODUP = 1, FUSE_MODDOWN = 2 };
 
 // Phase A (columns). CTA = C columns x N1 rows; N1/8 threads per column.
 template <int LOG_N1, int C, bool INVERSE, int FUSE>
-__global__ void __launch_bounds__(256) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
+__global__ void __launch_bounds__(NTT_THREADS) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
     constexpr int N1 = 1 << LOG_N1;
     constexpr int TPC = N1 / EPT;             // threads per column
     constexpr int PN = N1 + (N1 >> 4) + 1;    // padded column length (odd in words)
@@ -249,10 +253,10 @@ __device__ __forceinline__ uint32_t perm_index_n(uint32_t k, uint32_t g, int log
 
 // Phase B (contiguous blocks of B). CTA = BPC blocks; B/8 threads per block.
 template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE>
-__global__ void __launch_bounds__(256) k_ntt_rows(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
+__global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
     constexpr int B = 1 << LOG_B;
     constexpr int TPB = B / EPT;
-    constexpr int BPC = 256 / TPB;
+    constexpr int BPC = NTT_THREADS / TPB;
     constexpr int PB = B + (B >> 4);
     __shared__ uint64_t sm[BPC * PB];
     const int row = blockIdx.y;
@@ -308,51 +312,59 @@ __global__ void __launch_bounds__(256) k_ntt_rows(DevCtx c, uint64_t* data, RowM
     }
 }
 
-// FastBConv of ModUp (one thread per output coefficient pair, all targets in
-// parallel): digits[src][j][u] = conv_J->t_u(coef[src]) for u outside the
-// digit, NTT-domain copies of c1 for the digit's own rows.
+// FastBConv of ModUp: one thread per (source, digit, coefficient pair); the
+// centered [x_i (Q_J/q_i)^-1]_{q_i} values are computed once and extended to
+// every target row of the digit (16-byte loads/stores); the digit's own rows
+// are NTT-domain copies of c1.
 template <int KA>
 __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits, NttFuse fz, int level, int nsrc) {
     const int nr = level + 1, ne = nr + c.K;
-    const size_t halfN = c.N / 2;
-    const size_t total = (size_t)nsrc * fz.dn * ne * halfN;
+    const int halfN = c.N / 2;
+    const int total = nsrc * fz.dn * halfN;
     RowMap rm{ne, level, c.L, 0};
-    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-        const size_t row = idx / halfN;
-        const size_t k = (idx % halfN) * 2;
-        const int u = (int)(row % ne);
-        const int sj = (int)(row / ne);
-        const int src = sj / fz.dn, j = sj % fz.dn;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int sj = idx >> (c.logN - 1);
+        const size_t k = (size_t)(idx & (halfN - 1)) * 2;
+        const int src = sj / fz.dn, j = sj - src * fz.dn;
         const ModUpDigit& T = fz.mu[j];
-        uint64_t* out = digits + row * c.N + k;
-        if (u >= T.lo && u < T.hi) {
-            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(fz.c1 + (size_t)src * fz.c1_stride +
-                                                                      (size_t)u * c.N + k);
-            *reinterpret_cast<ulonglong2*>(out) = x;
-            continue;
-        }
-        const uint64_t t = c.primes[row_prime(rm, u)].q;
-        const uint64_t* coef = fz.coef + (size_t)src * nr * c.N;
-        uint64_t y0 = 0, y1 = 0;
-        int n0 = 0, n1 = 0;
         const int na = T.hi - T.lo;
+        const uint64_t* coef = fz.coef + (size_t)src * nr * c.N;
+        const uint64_t* c1 = fz.c1 + (size_t)src * fz.c1_stride;
+        uint64_t* out = digits + (size_t)sj * ne * c.N + k;
+        uint64_t v0[KA], v1[KA];
+        int n0 = 0, n1 = 0;
 #pragma unroll
         for (int a = 0; a < KA; ++a) {
+            v0[a] = v1[a] = 0;
             if (a < na) {
                 const int qi = T.lo + a;
                 const uint64_t q = c.primes[qi].q;
-                const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(coef + (size_t)qi * c.N + k);
-                const uint64_t v0 = mul_shoup(x.x, T.inv[a], T.inv_sh[a], q);
-                const uint64_t v1 = mul_shoup(x.y, T.inv[a], T.inv_sh[a], q);
-                n0 += v0 > (q >> 1);
-                n1 += v1 > (q >> 1);
-                y0 = add_mod(y0, mul_shoup(v0, T.hat[u][a], T.hat_sh[u][a], t), t);
-                y1 = add_mod(y1, mul_shoup(v1, T.hat[u][a], T.hat_sh[u][a], t), t);
+                const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(coef + (size_t)qi * c.N + k));
+                v0[a] = mul_shoup(x.x, T.inv[a], T.inv_sh[a], q);
+                v1[a] = mul_shoup(x.y, T.inv[a], T.inv_sh[a], q);
+                n0 += v0[a] > (q >> 1);
+                n1 += v1[a] > (q >> 1);
+                // own row of the digit: NTT-domain copy
+                *reinterpret_cast<ulonglong2*>(out + (size_t)qi * c.N) =
+                    __ldcs(reinterpret_cast<const ulonglong2*>(c1 + (size_t)qi * c.N + k));
             }
         }
-        for (int n = 0; n < n0; ++n) y0 = sub_mod(y0, T.qj[u], t);
-        for (int n = 0; n < n1; ++n) y1 = sub_mod(y1, T.qj[u], t);
-        *reinterpret_cast<ulonglong2*>(out) = make_ulonglong2(y0, y1);
+        for (int u = 0; u < ne; ++u) {
+            if (u >= T.lo && u < T.hi) continue;
+            const uint64_t t = c.primes[row_prime(rm, u)].q;
+            uint64_t y0 = 0, y1 = 0;
+#pragma unroll
+            for (int a = 0; a < KA; ++a) {
+                if (a < na) {
+                    y0 = add_mod(y0, mul_shoup(v0[a], T.hat[u][a], T.hat_sh[u][a], t), t);
+                    y1 = add_mod(y1, mul_shoup(v1[a], T.hat[u][a], T.hat_sh[u][a], t), t);
+                }
+            }
+            const uint64_t qj = T.qj[u];
+            for (int n = 0; n < n0; ++n) y0 = sub_mod(y0, qj, t);  // centered lift
+            for (int n = 0; n < n1; ++n) y1 = sub_mod(y1, qj, t);
+            *reinterpret_cast<ulonglong2*>(out + (size_t)u * c.N) = make_ulonglong2(y0, y1);
+        }
     }
 }
 
@@ -364,8 +376,8 @@ __global__ void __launch_bounds__(256) k_bconv_moddown(DevCtx c, uint64_t* conv,
     const size_t total = (size_t)npoly * nr * halfN;
     const ModDownTable* md = fz.md;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-        const size_t row = idx / halfN;
-        const size_t k = (idx % halfN) * 2;
+        const int row = (int)(idx >> (c.logN - 1));
+        const size_t k = (idx & (halfN - 1)) * 2;
         const int t = (int)(row % nr), pp = (int)(row / nr);
         const uint64_t qt = c.primes[t].q;
         const uint64_t* pc = fz.pc + (size_t)pp * c.K * c.N;
@@ -384,7 +396,7 @@ __global__ void __launch_bounds__(256) k_bconv_moddown(DevCtx c, uint64_t* conv,
         }
         for (int n = 0; n < n0; ++n) y0 = sub_mod(y0, md->pmod[t], qt);
         for (int n = 0; n < n1; ++n) y1 = sub_mod(y1, md->pmod[t], qt);
-        *reinterpret_cast<ulonglong2*>(conv + row * c.N + k) = make_ulonglong2(y0, y1);
+        *reinterpret_cast<ulonglong2*>(conv + (size_t)row * c.N + k) = make_ulonglong2(y0, y1);
     }
 }
 
@@ -392,18 +404,18 @@ template <int LOG_N1, int LOG_B>
 void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, bool inverse, int fuse,
                   const NttFuse& fz, cudaStream_t st) {
     constexpr int N1 = 1 << LOG_N1, B = 1 << LOG_B;
-    constexpr int C = 256 / (N1 / EPT);
-    constexpr int BPC = 256 / (B / EPT);
+    constexpr int C = NTT_THREADS / (N1 / EPT);
+    constexpr int BPC = NTT_THREADS / (B / EPT);
     const dim3 ga(B / C, nrows), gb((N1 + BPC - 1) / BPC, nrows);
     if (!inverse) {
-        k_ntt_cols<LOG_N1, C, false, FUSE_NONE><<<ga, 256, 0, st>>>(c, data, rm, fz);
+        k_ntt_cols<LOG_N1, C, false, FUSE_NONE><<<ga, NTT_THREADS, 0, st>>>(c, data, rm, fz);
         if (fuse == FUSE_MODDOWN)
-            k_ntt_rows<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gb, 256, 0, st>>>(c, data, rm, fz);
+            k_ntt_rows<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
         else
-            k_ntt_rows<LOG_N1, LOG_B, false, FUSE_NONE><<<gb, 256, 0, st>>>(c, data, rm, fz);
+            k_ntt_rows<LOG_N1, LOG_B, false, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
     } else {
-        k_ntt_rows<LOG_N1, LOG_B, true, FUSE_NONE><<<gb, 256, 0, st>>>(c, data, rm, fz);
-        k_ntt_cols<LOG_N1, C, true, FUSE_NONE><<<ga, 256, 0, st>>>(c, data, rm, fz);
+        k_ntt_rows<LOG_N1, LOG_B, true, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
+        k_ntt_cols<LOG_N1, C, true, FUSE_NONE><<<ga, NTT_THREADS, 0, st>>>(c, data, rm, fz);
     }
     note_launch(2);
 }
@@ -441,7 +453,7 @@ void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const ui
     fz.mu = tables;
     fz.dn = dn;
     {
-        const size_t total = (size_t)nsrc * dn * ne * (c.N / 2);
+        const size_t total = (size_t)nsrc * dn * (c.N / 2);
         const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
         switch (c.K) {
             case 1: k_bconv_modup<1><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
