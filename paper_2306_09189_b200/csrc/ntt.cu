@@ -216,10 +216,18 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_cols(DevCtx c, uint64_t* da
     {
         if (skip_row(rm, row, u)) return;
         p = row_prime(rm, u);
-        // coalesced load: consecutive threads take consecutive columns of a row
-        for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-            const int r = i / C, cc = i % C;
-            sm[cc * PN + pad(r)] = a[(size_t)r * B + col0 + cc];
+        // coalesced load: consecutive threads take consecutive columns of a row;
+        // all EPT loads are issued before the shared-memory stores
+        uint64_t tmp[EPT];
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int i = threadIdx.x + e * NTT_THREADS;
+            tmp[e] = __ldcs(a + (size_t)(i / C) * B + col0 + i % C);
+        }
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int i = threadIdx.x + e * NTT_THREADS;
+            sm[(i % C) * PN + pad(i / C)] = tmp[e];
         }
     }
     const uint64_t q = c.primes[p].q;
@@ -233,14 +241,16 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_cols(DevCtx c, uint64_t* da
     }
     if (INVERSE) {
         const uint64_t ni = c.ninv[p], nis = c.ninv_sh[p];
-        for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-            const int r = i / C, cc2 = i % C;
-            a[(size_t)r * B + col0 + cc2] = mul_shoup(sm[cc2 * PN + pad(r)], ni, nis, q);
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int i = threadIdx.x + e * NTT_THREADS;
+            a[(size_t)(i / C) * B + col0 + i % C] = mul_shoup(sm[(i % C) * PN + pad(i / C)], ni, nis, q);
         }
     } else {
-        for (int i = threadIdx.x; i < N1 * C; i += blockDim.x) {
-            const int r = i / C, cc2 = i % C;
-            a[(size_t)r * B + col0 + cc2] = sm[cc2 * PN + pad(r)];
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int i = threadIdx.x + e * NTT_THREADS;
+            a[(size_t)(i / C) * B + col0 + i % C] = sm[(i % C) * PN + pad(i / C)];
         }
     }
 }
@@ -266,7 +276,16 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
     const uint64_t q = c.primes[p].q;
     const int blk0 = blockIdx.x * BPC;
     uint64_t* a = data + (size_t)row * c.N + (size_t)blk0 * B;
-    for (int i = threadIdx.x; i < BPC * B; i += blockDim.x) sm[(i / B) * PB + pad(i % B)] = a[i];
+    {
+        uint64_t tmp[EPT];
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) tmp[e] = __ldcs(a + threadIdx.x + e * NTT_THREADS);
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int i = threadIdx.x + e * NTT_THREADS;
+            sm[(i / B) * PB + pad(i % B)] = tmp[e];
+        }
+    }
     __syncthreads();
     const int bi = threadIdx.x / TPB, lt = threadIdx.x % TPB;
     constexpr bool WS = TPB <= 32;
@@ -289,26 +308,40 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
             uint64_t* out = fz.out + ((size_t)pp * nr + u) * c.N + (size_t)blk0 * B;
             const uint64_t pi = fz.md->pinvq[u], pis = fz.md->pinvq_sh[u];
             const bool add = fz.add_src && pp == 0;
-            for (int i = threadIdx.x; i < BPC * B; i += blockDim.x) {
+            uint64_t av[EPT], sv[EPT];
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) {
+                const int i = threadIdx.x + e * NTT_THREADS;
+                av[e] = __ldcs(acc + i);
+                sv[e] = add ? __ldg(fz.add_src + (size_t)u * c.N +
+                                    perm_index_n((uint32_t)(blk0 * B + i), fz.galois, c.logN))
+                            : 0;
+            }
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) {
+                const int i = threadIdx.x + e * NTT_THREADS;
                 uint64_t x = sm[(i / B) * PB + pad(i % B)];
                 x = x >= q2 ? x - q2 : x;
                 x = x >= q ? x - q : x;
-                uint64_t o = mul_shoup(sub_mod(acc[i], x, q), pi, pis, q);
-                if (add) {
-                    const uint32_t k = (uint32_t)(blk0 * B + i);
-                    o = add_mod(o, fz.add_src[(size_t)u * c.N + perm_index_n(k, fz.galois, c.logN)], q);
-                }
+                uint64_t o = mul_shoup(sub_mod(av[e], x, q), pi, pis, q);
+                if (add) o = add_mod(o, sv[e], q);
                 out[i] = o;
             }
         } else {
-            for (int i = threadIdx.x; i < BPC * B; i += blockDim.x) {
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) {
+                const int i = threadIdx.x + e * NTT_THREADS;
                 uint64_t x = sm[(i / B) * PB + pad(i % B)];
                 x = x >= q2 ? x - q2 : x;
                 a[i] = x >= q ? x - q : x;
             }
         }
     } else {
-        for (int i = threadIdx.x; i < BPC * B; i += blockDim.x) a[i] = sm[(i / B) * PB + pad(i % B)];
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int i = threadIdx.x + e * NTT_THREADS;
+            a[i] = sm[(i / B) * PB + pad(i % B)];
+        }
     }
 }
 
