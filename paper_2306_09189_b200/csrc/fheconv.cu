@@ -646,48 +646,52 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
             giants.push_back(gi);
     }
     // giant steps: only Y_g.c1 is brought down to Q (for the decomposition);
-    // Y_g.c0 stays P-scaled in QP and enters the accumulator directly
-    uint64_t* yq = c->alloc((size_t)B.ngi * nr * N);  // [ngi][nr][N] = ModDown(Y_g.c1)
-    for (size_t a = 0; a < giants.size();) {
-        size_t b = a;
-        while (b + 1 < giants.size() && giants[b + 1] == giants[b] + 1) ++b;
-        const int first = giants[a], cnt = giants[b] - giants[a] + 1;
-        moddown_strided(c, Y + (size_t)first * 2 * extw + extw, 2 * extw, level, cnt, yq + (size_t)first * nr * N,
-                        nullptr, 1);
-        a = b + 1;
-    }
-    // all giant steps at once: one batched ModUp, one accumulate kernel
+    // Y_g.c0 stays P-scaled in QP and enters the accumulator directly.
+    // ModDown(Y_g.c1) is evaluated in the coefficient domain, which is exactly
+    // what the ModUp that follows consumes:
+    //   coef(ModDown(y)) = (INTT(y_Q) - conv_P->Q(INTT(y_P))) P^-1,
+    // so all giants go through one INTT, one conversion kernel, one ModUp
+    // conversion and one forward NTT (the own-digit rows are transformed too).
     if (!giants.empty()) {
+        const int G = (int)giants.size();
         const size_t dw = (size_t)dn * extw;
-        const int per = std::min<int>((int)giants.size(), kMaxGiant);
-        uint64_t* dg = c->alloc((size_t)per * dw);
-        for (size_t a = 0; a < giants.size(); a += per) {
-            const int n = std::min<int>(per, (int)(giants.size() - a));
-            // sources must be equally spaced: giants[a..a+n) may skip the identity, so ModUp each run
-            for (int s = 0; s < n;) {
-                int e = s;
-                while (e + 1 < n && giants[a + e + 1] == giants[a + e] + 1) ++e;
-                const uint64_t* c1 = yq + (size_t)giants[a + s] * nr * N;
-                modup_batch(c, c1, (size_t)nr * N, e - s + 1, level, dg + (size_t)s * dw);
-                s = e + 1;
-            }
+        uint64_t* yc = c->alloc((size_t)G * extw);       // [G][ne][N] Y_g.c1, then its INTT
+        uint64_t* yq = c->alloc((size_t)G * nr * N);     // [G][nr][N] coef(ModDown(Y_g.c1))
+        uint64_t* dg = c->alloc((size_t)G * dw);         // [G][dn][ne][N] ModUp digits
+        for (int s = 0; s < G; ++s)
+            ck(cudaMemcpyAsync(yc + (size_t)s * extw, Y + (size_t)giants[s] * 2 * extw + extw, extw * 8,
+                               cudaMemcpyDeviceToDevice, c->st),
+               "memcpy");
+        c->timed("ntt", c->rows(2.0 * G * ne), [&] { ntt_inverse(c->dc, yc, G * ne, RowMap{ne, level, c->L, 0}, c->st); });
+        c->timed("moddown", c->rows((double)G * (ne + nr)),
+                 [&] { moddown_coef(c->dc, yq, yc, c->d_md, level, G, c->st); });
+        c->ledger.moddowns += G;
+        c->timed("ntt_modup", c->rows((double)G * nr + (double)G * dn * ne), [&] {
+            ntt_modup_coef(c->dc, dg, yq, G, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+        });
+        c->ledger.modups += G;
+        for (int a0 = 0; a0 < G; a0 += kMaxBaby) {
+            const int n = std::min(kMaxBaby, G - a0);
             KsStream ks{};
             ks.n = n;
-            ks.digits = dg;
+            ks.digits = dg + (size_t)a0 * dw;
             ks.digit_stride = dw;
             ks.out = acc;
             ks.c0_qp = 1;
             for (int s = 0; s < n; ++s) {
-                const int gi = giants[a + s];
+                const int gi = giants[a0 + s];
                 const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[gi]));
                 ks.galois[s] = g;
                 ks.key[s] = c->key_for(g);
                 ks.c0[s] = Y + (size_t)gi * 2 * extw;
                 c->ledger.key_switches++;
             }
-            c->timed("ks_inner", c->rows((double)ks.n * (3.0 * dn * ne + ne) + 4.0 * ne), [&] { ks_stream(c->dc, ks, 1, c->d_md, level, dn, c->st); });
+            c->timed("ks_inner", c->rows((double)ks.n * (3.0 * dn * ne + ne) + 4.0 * ne),
+                     [&] { ks_stream(c->dc, ks, 1, c->d_md, level, dn, c->st); });
         }
         c->release(dg);
+        c->release(yq);
+        c->release(yc);
     }
     if (id >= 0) qp_add(c->dc, acc, Y + (size_t)id * 2 * extw, level, c->st);
     uint64_t* md = c->alloc((size_t)2 * nr * N);
@@ -713,7 +717,6 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
     lg.adds += pairs ? pairs - 1 : 0;
     c->release(md);
     c->release(acc);
-    c->release(yq);
     c->release(Y);
     c->release(XT);
     c->release(dsrc);

@@ -117,6 +117,13 @@ void ntt_inverse(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, c
 // ModUp FastBConv fused into the forward NTT: digits = [nsrc][dn][ne][N]
 void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const uint64_t* c1, size_t c1_stride,
                int nsrc, const ModUpDigit* tables, int level, int dn, cudaStream_t st);
+// ModUp of nsrc coefficient-domain sources coef = [nsrc][level+1][N]: every
+// digit row (own rows included) = conversion of coef, then the forward NTT
+void ntt_modup_coef(const DevCtx& c, uint64_t* digits, const uint64_t* coef, int nsrc, const ModUpDigit* tables,
+                    int level, int dn, cudaStream_t st);
+// coefficient-domain ModDown: out[p][t] = (y[p][t] - conv_P->q_t(y[p][P rows])) P^-1, y = [npoly][ne][N]
+void moddown_coef(const DevCtx& c, uint64_t* out, const uint64_t* y, const ModDownTable* md, int level, int npoly,
+                  cudaStream_t st);
 // ModDown FastBConv + finish fused into the forward NTT of conv (scratch [npoly][level+1][N]):
 // out[p] = (acc[p] - NTT(FastBConv_P->Q(pcoef[p]))) P^-1 (+ sigma_g(add_src) on poly 0)
 void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, size_t acc_stride,

@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
         const ModUpDigit& T = fz.mu[j];
         const int na = T.hi - T.lo;
         const uint64_t* coef = fz.coef + (size_t)src * nr * c.N;
-        const uint64_t* c1 = fz.c1 + (size_t)src * fz.c1_stride;
+        const uint64_t* c1 = fz.c1 ? fz.c1 + (size_t)src * fz.c1_stride : nullptr;
         uint64_t* out = digits + (size_t)sj * ne * c.N + k;
         uint64_t v0[KA], v1[KA];
         int n0 = 0, n1 = 0;
@@ -377,9 +377,10 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
                 v1[a] = mul_shoup(x.y, T.inv[a], T.inv_sh[a], q);
                 n0 += v0[a] > (q >> 1);
                 n1 += v1[a] > (q >> 1);
-                // own row of the digit: NTT-domain copy
+                // own row of the digit: NTT-domain copy of c1, or (coefficient-domain
+                // sources, c1 == nullptr) the coefficients themselves, transformed later
                 *reinterpret_cast<ulonglong2*>(out + (size_t)qi * c.N) =
-                    __ldcs(reinterpret_cast<const ulonglong2*>(c1 + (size_t)qi * c.N + k));
+                    c1 ? __ldcs(reinterpret_cast<const ulonglong2*>(c1 + (size_t)qi * c.N + k)) : x;
             }
         }
         for (int u = 0; u < ne; ++u) {
@@ -497,6 +498,74 @@ void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const ui
         note_launch(1);
     }
     ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, c.K, dn}, false, FUSE_NONE, fz, st);
+}
+
+// coefficient-domain ModDown (one thread per coefficient pair and q row)
+template <int KA>
+__global__ void __launch_bounds__(256) k_moddown_coef(DevCtx c, uint64_t* out, const uint64_t* y,
+                                                      const ModDownTable* md, int level, int npoly) {
+    const int nr = level + 1, ne = nr + c.K;
+    const int halfN = c.N / 2;
+    const int total = npoly * nr * halfN;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int row = idx >> (c.logN - 1);
+        const size_t k = (size_t)(idx & (halfN - 1)) * 2;
+        const int pp = row / nr, t = row - pp * nr;
+        const uint64_t qt = c.primes[t].q;
+        const uint64_t* yp = y + (size_t)pp * ne * c.N;
+        uint64_t c0 = 0, c1 = 0;
+        int n0 = 0, n1 = 0;
+#pragma unroll
+        for (int a = 0; a < KA; ++a) {
+            const uint64_t q = c.primes[c.L + a].q;
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(yp + (size_t)(nr + a) * c.N + k);
+            const uint64_t v0 = mul_shoup(x.x, md->pinv[a], md->pinv_sh[a], q);
+            const uint64_t v1 = mul_shoup(x.y, md->pinv[a], md->pinv_sh[a], q);
+            n0 += v0 > (q >> 1);
+            n1 += v1 > (q >> 1);
+            c0 = add_mod(c0, mul_shoup(v0, md->hat[t][a], md->hat_sh[t][a], qt), qt);
+            c1 = add_mod(c1, mul_shoup(v1, md->hat[t][a], md->hat_sh[t][a], qt), qt);
+        }
+        for (int n = 0; n < n0; ++n) c0 = sub_mod(c0, md->pmod[t], qt);
+        for (int n = 0; n < n1; ++n) c1 = sub_mod(c1, md->pmod[t], qt);
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(yp + (size_t)t * c.N + k);
+        const uint64_t o0 = mul_shoup(sub_mod(x.x, c0, qt), md->pinvq[t], md->pinvq_sh[t], qt);
+        const uint64_t o1 = mul_shoup(sub_mod(x.y, c1, qt), md->pinvq[t], md->pinvq_sh[t], qt);
+        *reinterpret_cast<ulonglong2*>(out + (size_t)row * c.N + k) = make_ulonglong2(o0, o1);
+    }
+}
+
+void moddown_coef(const DevCtx& c, uint64_t* out, const uint64_t* y, const ModDownTable* md, int level, int npoly,
+                  cudaStream_t st) {
+    const size_t total = (size_t)npoly * (level + 1) * (c.N / 2);
+    const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+    switch (c.K) {
+        case 1: k_moddown_coef<1><<<blocks, 256, 0, st>>>(c, out, y, md, level, npoly); break;
+        case 2: k_moddown_coef<2><<<blocks, 256, 0, st>>>(c, out, y, md, level, npoly); break;
+        case 3: k_moddown_coef<3><<<blocks, 256, 0, st>>>(c, out, y, md, level, npoly); break;
+        default: k_moddown_coef<4><<<blocks, 256, 0, st>>>(c, out, y, md, level, npoly); break;
+    }
+    note_launch(1);
+}
+
+void ntt_modup_coef(const DevCtx& c, uint64_t* digits, const uint64_t* coef, int nsrc, const ModUpDigit* tables,
+                    int level, int dn, cudaStream_t st) {
+    const int ne = level + 1 + c.K;
+    NttFuse fz{};
+    fz.coef = coef;
+    fz.c1 = nullptr;
+    fz.mu = tables;
+    fz.dn = dn;
+    const size_t total = (size_t)nsrc * dn * (c.N / 2);
+    const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+    switch (c.K) {
+        case 1: k_bconv_modup<1><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
+        case 2: k_bconv_modup<2><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
+        case 3: k_bconv_modup<3><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
+        default: k_bconv_modup<4><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
+    }
+    note_launch(1);
+    ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, 0, dn}, false, FUSE_NONE, fz, st);
 }
 
 void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, size_t acc_stride,
