@@ -188,6 +188,9 @@ int fhe_conv2d_into(fhe_ctx* ctx, const fhe_ct* ct, const fhe_conv_layer* layer,
  * plaintexts shared; BASELINE cfg5) */
 int fhe_conv2d_batch(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* layer,
                      int approach, fhe_ct** outs);
+/* same, into preallocated outputs of level - 1 */
+int fhe_conv2d_batch_into(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* layer,
+                          int approach, fhe_ct* const* outs);
 
 #ifdef __cplusplus
 }

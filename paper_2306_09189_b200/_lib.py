@@ -84,6 +84,7 @@ SIGNATURES = [
     ("fhe_conv2d", C.c_int, [vp, vp, vp, C.c_int, vpp]),
     ("fhe_conv2d_into", C.c_int, [vp, vp, vp, C.c_int, vp]),
     ("fhe_conv2d_batch", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, vp, C.c_int, vpp]),
+    ("fhe_conv2d_batch_into", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, vp, C.c_int, C.POINTER(C.c_void_p)]),
 ]
 
 EXPORTED = [s[0] for s in SIGNATURES]

@@ -722,6 +722,174 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
     c->release(dsrc);
 }
 
+// Batched BSGS conv of S ciphertexts through one layer: every key and every
+// plaintext is streamed once per batch (the lanes of a warp that share a
+// coefficient pair share the loads), ModUps/NTTs run over the whole batch.
+void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv_layer* ly, int orient,
+                     fhe_ct* const* outs) {
+    fhe_conv_layer::Bsgs& B = ensure_bsgs(c, ly, orient);
+    const int level = cts[0]->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
+    for (int s = 0; s < S; ++s) {
+        if (cts[s]->level != level || outs[s]->level != level - 1)
+            fail(FHE_E_INVALID, "batched conv: all inputs must share the layer level");
+    }
+    uint64_t* buf = c->alloc((size_t)S * ctw);
+    for (int s = 0; s < S; ++s)
+        ck(cudaMemcpyAsync(buf + (size_t)s * ctw, cts[s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    uint64_t* dsrc = c->alloc((size_t)S * dw);
+    modup_batch(c, buf + (size_t)nr * N, ctw, S, level, dsrc);
+    // baby steps
+    const size_t xts = (size_t)B.nb * 2 * extw, ys = (size_t)B.ngi * 2 * extw;
+    uint64_t* XT = c->alloc((size_t)S * xts);
+    BabyTerms t{};
+    t.nb = B.nb;
+    t.nb_total = B.nb;
+    t.pts = B.d_pts;
+    KsBatch kb{};
+    kb.nsrc = S;
+    kb.digits = dsrc;
+    kb.digit_src_stride = dw;
+    kb.c0 = buf;
+    kb.c0_src_stride = ctw;
+    kb.out = XT;
+    kb.out_src_stride = xts;
+    for (int b = 0; b < B.nb; ++b) {
+        const uint32_t g = c->galois_of(c->reduce_amount(B.bamt[b]));
+        t.galois[b] = g;
+        t.key[b] = g == 1 ? nullptr : c->key_for(g);
+        uint32_t any = 0;
+        for (int gi = 0; gi < B.ngi; ++gi) any |= B.nonempty[(size_t)gi * B.nb + b] ? 1u : 0u;
+        t.gmask[b] = any;
+        if (!any) continue;
+        if (g == 1) {
+            c->timed("ks_multi", c->rows((2.0 * nr + 2.0 * ne) * S), [&] {
+                identity_batch(c->dc, XT + (size_t)b * 2 * extw, xts, buf, ctw, c->d_md, level, S, c->st);
+            });
+            continue;
+        }
+        kb.galois[kb.n] = g;
+        kb.key[kb.n] = t.key[b];
+        kb.slot[kb.n] = b;
+        kb.n++;
+        c->ledger.key_switches += S;
+    }
+    c->timed("ks_multi", c->rows((double)kb.n * (2.0 * dn * ne + 2.0 * ne * S) + ((double)dn * ne + nr) * S),
+             [&] { ks_batch(c->dc, kb, 0, c->d_md, level, dn, c->st); });
+    uint64_t* Y = c->alloc((size_t)S * ys);
+    for (int g0 = 0; g0 < B.ngi; g0 += kMaxGiant) {
+        t.ngi = std::min(kMaxGiant, B.ngi - g0);
+        t.g0 = g0;
+        double pt_pairs = 0;
+        for (int b = 0; b < B.nb; ++b) {
+            uint32_t mask = 0;
+            for (int gi = 0; gi < t.ngi; ++gi)
+                if (B.nonempty[(size_t)(g0 + gi) * B.nb + b]) mask |= 1u << gi;
+            t.gmask[b] = mask;
+            pt_pairs += __builtin_popcount(mask);
+        }
+        c->timed("pt_matvec", c->rows(pt_pairs * ne + (2.0 * B.nb * ne + 2.0 * t.ngi * ne) * S), [&] {
+            pt_matvec_batch(c->dc, Y + (size_t)g0 * 2 * extw, ys, XT, xts, t, level, S, c->st);
+        });
+    }
+    c->release(XT);
+    c->release(dsrc);
+    // giant steps, in source chunks (bounds the digit buffers)
+    std::vector<int> giants;
+    int id = -1;
+    for (int gi = 0; gi < B.ngi; ++gi) {
+        bool any = false;
+        for (int b = 0; b < B.nb; ++b) any |= B.nonempty[(size_t)gi * B.nb + b] != 0;
+        if (!any) continue;
+        if (c->reduce_amount(B.gamt[gi]) == 0)
+            id = gi;
+        else
+            giants.push_back(gi);
+    }
+    uint64_t* acc = c->alloc((size_t)S * 2 * extw);
+    ck(cudaMemsetAsync(acc, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
+    const int G = (int)giants.size();
+    if (G > 0) {
+        const int SC = std::max(1, std::min(S, 8));
+        uint64_t* yc = c->alloc((size_t)SC * G * extw);
+        uint64_t* yq = c->alloc((size_t)SC * G * nr * N);
+        uint64_t* dg = c->alloc((size_t)SC * G * dw);
+        for (int s0 = 0; s0 < S; s0 += SC) {
+            const int sc = std::min(SC, S - s0);
+            for (int s = 0; s < sc; ++s)
+                for (int gi = 0; gi < G; ++gi)
+                    ck(cudaMemcpyAsync(yc + ((size_t)s * G + gi) * extw,
+                                       Y + (size_t)(s0 + s) * ys + (size_t)giants[gi] * 2 * extw + extw, extw * 8,
+                                       cudaMemcpyDeviceToDevice, c->st),
+                       "memcpy");
+            const int np_ = sc * G;
+            c->timed("ntt", c->rows(2.0 * np_ * ne),
+                     [&] { ntt_inverse(c->dc, yc, np_ * ne, RowMap{ne, level, c->L, 0}, c->st); });
+            c->timed("moddown", c->rows((double)np_ * (ne + nr)),
+                     [&] { moddown_coef(c->dc, yq, yc, c->d_md, level, np_, c->st); });
+            c->timed("ntt_modup", c->rows((double)np_ * nr + (double)np_ * dn * ne), [&] {
+                ntt_modup_coef(c->dc, dg, yq, np_, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+            });
+            c->ledger.moddowns += np_;
+            c->ledger.modups += np_;
+            KsBatch kg{};
+            kg.nsrc = sc;
+            kg.n = G;
+            kg.digits = dg;
+            kg.digit_src_stride = (size_t)G * dw;
+            kg.digit_term_stride = dw;
+            kg.c0 = Y + (size_t)s0 * ys;
+            kg.c0_src_stride = ys;
+            kg.c0_qp = 1;
+            kg.out = acc + (size_t)s0 * 2 * extw;
+            kg.out_src_stride = 2 * extw;
+            for (int gi = 0; gi < G; ++gi) {
+                const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[giants[gi]]));
+                kg.galois[gi] = g;
+                kg.key[gi] = c->key_for(g);
+                kg.c0_off[gi] = (size_t)giants[gi] * 2 * extw;
+            }
+            c->ledger.key_switches += (uint64_t)G * sc;
+            c->timed("ks_inner", c->rows((double)G * 2.0 * dn * ne + (double)sc * G * (dn * ne + ne) + 4.0 * ne * sc),
+                     [&] { ks_batch(c->dc, kg, 1, c->d_md, level, dn, c->st); });
+        }
+        c->release(dg);
+        c->release(yq);
+        c->release(yc);
+    }
+    if (id >= 0)
+        for (int s = 0; s < S; ++s)
+            qp_add(c->dc, acc + (size_t)s * 2 * extw, Y + (size_t)s * ys + (size_t)id * 2 * extw, level, c->st);
+    uint64_t* md = c->alloc((size_t)S * ctw);
+    moddown(c, acc, level, 2 * S, md, nullptr, 1);
+    for (int s = 0; s < S; ++s) {
+        rescale_into(c, md + (size_t)s * ctw, level, outs[s]->d);
+        outs[s]->scale = (cts[s]->scale * (double)c->primes[level]) / (double)c->primes[level];
+        outs[s]->depth = cts[s]->depth + 1;
+        c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[s]->depth);
+    }
+    fhe_ledger& lg = c->ledger;
+    uint64_t pairs = 0;
+    for (int v : B.nonempty) pairs += v;
+    for (int s = 0; s < S; ++s) {
+        lg.hoist_groups++;
+        for (int b = 0; b < B.nb; ++b) {
+            c->note_amount(c->reduce_amount(B.bamt[b]));
+            lg.hoisted_rotations++;
+        }
+        for (int gi : giants) {
+            c->note_amount(c->reduce_amount(B.gamt[gi]));
+            lg.rotations++;
+        }
+        lg.ct_pt_mults += pairs;
+        lg.adds += pairs ? pairs - 1 : 0;
+    }
+    c->release(md);
+    c->release(acc);
+    c->release(Y);
+    c->release(buf);
+}
+
 int auto_orient(const fhe_conv_layer* ly) {
     // giant steps each cost a ModUp: take the smaller set as giant steps
     return ly->kappa * ly->kappa <= ly->c_in ? 3 : 4;
@@ -826,6 +994,22 @@ void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
     c->release(dtmp);
     c->release(X.d);
     ledger_conv(c, ly, approach);
+}
+
+void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* ly, int approach,
+                fhe_ct* const* outs) {
+    if (n == 0) return;
+    if (approach < 0 || approach > 4) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3 or 4");
+    if (approach == 0) approach = auto_orient(ly);
+    if (approach >= 3 && n > 1) {
+        if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
+        for (size_t s0 = 0; s0 < n; s0 += 32) {
+            const int S = (int)std::min<size_t>(32, n - s0);
+            conv_bsgs_batch(c, cts + s0, S, ly, approach, outs + s0);
+        }
+        return;
+    }
+    for (size_t i = 0; i < n; ++i) conv_impl(c, cts[i], ly, approach, outs[i]);
 }
 
 }  // namespace
@@ -1421,12 +1605,21 @@ int fhe_conv2d(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
 int fhe_conv2d_batch(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* ly, int approach,
                      fhe_ct** outs) {
     return guard(c, [&] {
-        for (size_t i = 0; i < n; ++i) {
-            fhe_ct* o = new_ct(c, cts[i]->level - 1, cts[i]->scale, cts[i]->depth + 1);
-            conv_impl(c, cts[i], ly, approach, o);
-            outs[i] = o;
+        std::vector<fhe_ct*> o(n, nullptr);
+        try {
+            for (size_t i = 0; i < n; ++i) o[i] = new_ct(c, cts[i]->level - 1, cts[i]->scale, cts[i]->depth + 1);
+            batch_impl(c, cts, n, ly, approach, o.data());
+        } catch (...) {
+            for (fhe_ct* x : o) fhe_ct_free(x);
+            throw;
         }
+        for (size_t i = 0; i < n; ++i) outs[i] = o[i];
     });
+}
+
+int fhe_conv2d_batch_into(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* ly, int approach,
+                          fhe_ct* const* outs) {
+    return guard(c, [&] { batch_impl(c, cts, n, ly, approach, outs); });
 }
 
 }  // extern "C"

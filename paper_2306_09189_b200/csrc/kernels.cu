@@ -608,6 +608,155 @@ __global__ void __launch_bounds__(kStreamThreads) k_ks_stream(DevCtx c, KsStream
     }
 }
 
+// ---- batched key switching: work item = (coefficient pair, source), source
+// fastest, so the lanes of a warp that share a pair issue identical key
+// addresses (one transaction serves all sources of the batch).
+template <int DN, int MODE>
+__global__ void __launch_bounds__(256) k_ks_batch(DevCtx c, KsBatch a, const ModDownTable* md, int level) {
+    const int nr = level + 1, ne = nr + c.K;
+    const int np = c.L + c.K;
+    const size_t total = (size_t)ne * c.N;
+    const size_t items = (total / 2) * a.nsrc;
+    RowMap rm{ne, level, c.L, 0};
+    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < items; it += (size_t)gridDim.x * blockDim.x) {
+        const int s = (int)(it % a.nsrc);
+        const size_t i = (it / a.nsrc) * 2;
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
+        const int p = row_prime(rm, u);
+        const Prime pr = c.primes[p];
+        const bool qrow = u < nr;
+        const uint64_t pm = qrow ? md->pmod[u] : 0, pms = qrow ? md->pmod_sh[u] : 0;
+        U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
+        for (int t = 0; t < a.n; ++t) {
+            const uint32_t pk = perm_index(k, a.galois[t], c.logN);
+            const bool swp = pk & 1u;
+            const uint64_t* key = a.key[t];
+            const uint64_t* D = a.digits + (size_t)s * a.digit_src_stride + (size_t)t * a.digit_term_stride;
+            const uint64_t* c0 = a.c0 + (size_t)s * a.c0_src_stride + a.c0_off[t];
+            ulonglong2 k0[DN], k1[DN], d[DN];
+#pragma unroll
+            for (int j = 0; j < DN; ++j) {
+                k0[j] = vld2_nc(key + (((size_t)j * 2 + 0) * np + p) * c.N + k);
+                k1[j] = vld2_nc(key + (((size_t)j * 2 + 1) * np + p) * c.N + k);
+                d[j] = vld2_nc(D + ((size_t)j * ne + u) * c.N + (pk & ~1u));
+            }
+            const ulonglong2 x = (a.c0_qp || qrow) ? vld2_nc(c0 + (size_t)u * c.N + (pk & ~1u)) : make_ulonglong2(0, 0);
+            if (MODE == 0) s0[0] = s0[1] = s1[0] = s1[1] = U128{0, 0};
+#pragma unroll
+            for (int j = 0; j < DN; ++j) {
+                const uint64_t da = swp ? d[j].y : d[j].x, db = swp ? d[j].x : d[j].y;
+                mac(s0[0], da, k0[j].x);
+                mac(s0[1], db, k0[j].y);
+                mac(s1[0], da, k1[j].x);
+                mac(s1[1], db, k1[j].y);
+            }
+            if (a.c0_qp) {
+                add128(s0[0], swp ? x.y : x.x);
+                add128(s0[1], swp ? x.x : x.y);
+            } else if (qrow) {
+                add128(s0[0], mul_shoup(swp ? x.y : x.x, pm, pms, pr.q));
+                add128(s0[1], mul_shoup(swp ? x.x : x.y, pm, pms, pr.q));
+            }
+            if (MODE == 0) {
+                uint64_t* xt = a.out + (size_t)s * a.out_src_stride + (size_t)a.slot[t] * 2 * total;
+                st2(xt + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
+                st2(xt + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
+            }
+        }
+        if (MODE == 1) {
+            uint64_t* acc = a.out + (size_t)s * a.out_src_stride;
+            const ulonglong2 a0 = ld2(acc + i), a1 = ld2(acc + total + i);
+            add128(s0[0], a0.x);
+            add128(s0[1], a0.y);
+            add128(s1[0], a1.x);
+            add128(s1[1], a1.y);
+            st2(acc + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
+            st2(acc + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
+        }
+    }
+}
+
+// batched plaintext mat-vec: Y[s][g] = sum_b pt[g][b] * XT[s][b] (item = (pair, source),
+// the sources of a pair share every plaintext load)
+__global__ void __launch_bounds__(128) k_pt_matvec_b(DevCtx c, uint64_t* Y, size_t y_src_stride, const uint64_t* XT,
+                                                     size_t xt_src_stride, BabyTerms t, int level, int nsrc) {
+    extern __shared__ ulonglong2 xs[];  // [nb][2][128]
+    const int ne = level + 1 + c.K;
+    const size_t total = (size_t)ne * c.N;
+    const size_t items = (total / 2) * nsrc;
+    RowMap rm{ne, level, c.L, 0};
+    const int tid = threadIdx.x;
+    for (size_t it = blockIdx.x * (size_t)blockDim.x + tid; it < items; it += (size_t)gridDim.x * blockDim.x) {
+        const int s = (int)(it % nsrc);
+        const size_t i = (it / nsrc) * 2;
+        const int u = (int)(i >> c.logN);
+        const Prime pr = c.primes[row_prime(rm, u)];
+        const uint64_t* xts = XT + (size_t)s * xt_src_stride;
+        for (int b = 0; b < t.nb; ++b) {
+            if (t.gmask[b] == 0) continue;
+            xs[(b * 2 + 0) * 128 + tid] = vld2_cs(xts + (size_t)b * 2 * total + i);
+            xs[(b * 2 + 1) * 128 + tid] = vld2_cs(xts + (size_t)b * 2 * total + total + i);
+        }
+        for (int g = 0; g < t.ngi; ++g) {
+            U128 a0[2] = {{0, 0}, {0, 0}}, a1[2] = {{0, 0}, {0, 0}};
+            const uint64_t* pg = t.pts + ((size_t)(t.g0 + g) * t.nb_total) * total + i;
+            int b = 0;
+            for (; b + 4 <= t.nb; b += 4) {
+                ulonglong2 w[4];
+#pragma unroll
+                for (int d = 0; d < 4; ++d)
+                    w[d] = ((t.gmask[b + d] >> g) & 1u) ? vld2_nc(pg + (size_t)(b + d) * total) : make_ulonglong2(0, 0);
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const ulonglong2 x0 = xs[((b + d) * 2 + 0) * 128 + tid];
+                    const ulonglong2 x1 = xs[((b + d) * 2 + 1) * 128 + tid];
+                    mac(a0[0], w[d].x, x0.x);
+                    mac(a0[1], w[d].y, x0.y);
+                    mac(a1[0], w[d].x, x1.x);
+                    mac(a1[1], w[d].y, x1.y);
+                }
+            }
+            for (; b < t.nb; ++b) {
+                if (!((t.gmask[b] >> g) & 1u)) continue;
+                const ulonglong2 w = vld2_nc(pg + (size_t)b * total);
+                const ulonglong2 x0 = xs[(b * 2 + 0) * 128 + tid];
+                const ulonglong2 x1 = xs[(b * 2 + 1) * 128 + tid];
+                mac(a0[0], w.x, x0.x);
+                mac(a0[1], w.y, x0.y);
+                mac(a1[0], w.x, x1.x);
+                mac(a1[1], w.y, x1.y);
+            }
+            uint64_t* y = Y + (size_t)s * y_src_stride + (size_t)g * 2 * total;
+            st2(y + i, reduce128(a0[0].hi, a0[0].lo, pr), reduce128(a0[1].hi, a0[1].lo, pr));
+            st2(y + total + i, reduce128(a1[0].hi, a1[0].lo, pr), reduce128(a1[1].hi, a1[1].lo, pr));
+        }
+    }
+}
+
+// XT[s][slot] = P ct_s (identity baby step) for nsrc sources
+__global__ void k_identity_batch(DevCtx c, uint64_t* xt, size_t xt_src_stride, const uint64_t* X, size_t x_src_stride,
+                                 const ModDownTable* md, int level, int nsrc) {
+    const int nr = level + 1, ne = nr + c.K;
+    const size_t total = (size_t)ne * c.N;
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < total * nsrc; j += (size_t)gridDim.x * blockDim.x) {
+        const int s = (int)(j / total);
+        const size_t i = j - (size_t)s * total;
+        const int u = (int)(i >> c.logN);
+        const size_t k = i & (size_t)(c.N - 1);
+        uint64_t* o = xt + (size_t)s * xt_src_stride;
+        const uint64_t* x = X + (size_t)s * x_src_stride;
+        if (u < nr) {
+            const uint64_t q = c.primes[u].q;
+            o[i] = mul_shoup(x[(size_t)u * c.N + k], md->pmod[u], md->pmod_sh[u], q);
+            o[total + i] = mul_shoup(x[((size_t)nr + u) * c.N + k], md->pmod[u], md->pmod_sh[u], q);
+        } else {
+            o[i] = 0;
+            o[total + i] = 0;
+        }
+    }
+}
+
 // XT[slot] = P ct (identity baby step) for q rows, 0 for the special rows
 __global__ void k_identity_term(DevCtx c, uint64_t* xt, const uint64_t* X, const ModDownTable* md, int level) {
     const int nr = level + 1, ne = nr + c.K;
@@ -895,6 +1044,40 @@ void ks_stream(const DevCtx& c, const KsStream& a, int mode, const ModDownTable*
     } while (0)
     FHE_DN_SWITCH(dn, FHE_KSS)
 #undef FHE_KSS
+}
+
+void ks_batch(const DevCtx& c, const KsBatch& a, int mode, const ModDownTable* md, int level, int dn,
+              cudaStream_t st) {
+    if (a.n <= 0 || a.nsrc <= 0) return;
+    const size_t items = (size_t)(level + 1 + c.K) * c.N / 2 * a.nsrc;
+    const int blocks = (int)((items + 255) / 256 < 148 * 8 ? (items + 255) / 256 : 148 * 8);
+    ++g_launches;
+#define FHE_KSB(D)                                                                     \
+    do {                                                                               \
+        if (mode == 0)                                                                 \
+            k_ks_batch<D, 0><<<blocks, 256, 0, st>>>(c, a, md, level);                 \
+        else                                                                           \
+            k_ks_batch<D, 1><<<blocks, 256, 0, st>>>(c, a, md, level);                 \
+    } while (0)
+    FHE_DN_SWITCH(dn, FHE_KSB)
+#undef FHE_KSB
+}
+
+void pt_matvec_batch(const DevCtx& c, uint64_t* Y, size_t y_src_stride, const uint64_t* XT, size_t xt_src_stride,
+                     const BabyTerms& t, int level, int nsrc, cudaStream_t st) {
+    const size_t items = (size_t)(level + 1 + c.K) * c.N / 2 * nsrc;
+    const size_t smem = (size_t)t.nb * 2 * 128 * sizeof(ulonglong2);
+    const int blocks = (int)((items + 127) / 128 < 148 * 12 ? (items + 127) / 128 : 148 * 12);
+    ++g_launches;
+    cudaFuncSetAttribute(k_pt_matvec_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_pt_matvec_b<<<blocks, 128, smem, st>>>(c, Y, y_src_stride, XT, xt_src_stride, t, level, nsrc);
+}
+
+void identity_batch(const DevCtx& c, uint64_t* xt, size_t xt_src_stride, const uint64_t* ct, size_t ct_src_stride,
+                    const ModDownTable* md, int level, int nsrc, cudaStream_t st) {
+    ++g_launches;
+    k_identity_batch<<<ew_blocks((size_t)(level + 1 + c.K) * c.N * nsrc), kEwThreads, 0, st>>>(
+        c, xt, xt_src_stride, ct, ct_src_stride, md, level, nsrc);
 }
 
 void identity_term(const DevCtx& c, uint64_t* xt, const uint64_t* ct, const ModDownTable* md, int level,

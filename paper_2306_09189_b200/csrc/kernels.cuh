@@ -235,6 +235,28 @@ void ks_stream(const DevCtx& c, const KsStream& a, int mode, const ModDownTable*
 // xt = P ct (q rows), 0 (special rows): the identity baby step
 void identity_term(const DevCtx& c, uint64_t* xt, const uint64_t* ct, const ModDownTable* md, int level,
                    cudaStream_t st);
+// Batched key switching over nsrc sources (k_ks_batch): term t of source s uses
+// digits + s * digit_src_stride + t * digit_term_stride and c0 + s * c0_src_stride + c0_off[t].
+struct KsBatch {
+    int n, nsrc;
+    uint32_t galois[kMaxBaby];
+    const uint64_t* key[kMaxBaby];
+    size_t c0_off[kMaxBaby];
+    int slot[kMaxBaby];
+    const uint64_t* digits;
+    size_t digit_src_stride, digit_term_stride;
+    const uint64_t* c0;
+    size_t c0_src_stride;
+    int c0_qp;
+    uint64_t* out;  // mode 0: XT of source s at out + s * out_src_stride; mode 1: acc of source s
+    size_t out_src_stride;
+};
+void ks_batch(const DevCtx& c, const KsBatch& a, int mode, const ModDownTable* md, int level, int dn,
+              cudaStream_t st);
+void pt_matvec_batch(const DevCtx& c, uint64_t* Y, size_t y_src_stride, const uint64_t* XT, size_t xt_src_stride,
+                     const BabyTerms& t, int level, int nsrc, cudaStream_t st);
+void identity_batch(const DevCtx& c, uint64_t* xt, size_t xt_src_stride, const uint64_t* ct, size_t ct_src_stride,
+                    const ModDownTable* md, int level, int nsrc, cudaStream_t st);
 // acc += y over [2][ne][N] (QP basis)
 void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st);
 

@@ -275,6 +275,20 @@ class Context:
     def conv2d_into(self, ct: Ciphertext, layer: ConvLayer, approach: int, out: Ciphertext):
         self._check(lib().fhe_conv2d_into(self.h, ct.h, layer.h, approach, out.h))
 
+    def conv2d_batch(self, cts: Sequence[Ciphertext], layer: ConvLayer, approach: int = 0) -> list[Ciphertext]:
+        """n independent ciphertexts through one layer; keys and plaintexts are
+        streamed once per batch (BSGS schedules)."""
+        ins = (C.c_void_p * len(cts))(*[x.h for x in cts])
+        outs = (C.c_void_p * len(cts))()
+        self._check(lib().fhe_conv2d_batch(self.h, ins, len(cts), layer.h, approach, outs))
+        return [Ciphertext(self, outs[i]) for i in range(len(cts))]
+
+    def conv2d_batch_into(self, cts: Sequence[Ciphertext], layer: ConvLayer, approach: int,
+                          outs: Sequence[Ciphertext]):
+        ins = (C.c_void_p * len(cts))(*[x.h for x in cts])
+        o = (C.c_void_p * len(outs))(*[x.h for x in outs])
+        self._check(lib().fhe_conv2d_batch_into(self.h, ins, len(cts), layer.h, approach, o))
+
     # -------------------------------------------------------------- ledger
     def ledger(self) -> dict:
         lg = _lib.FheLedger()

@@ -247,3 +247,18 @@ def test_cfg2_hoisted_stencil(oracle):
     for i, k in enumerate(stencil):
         assert np.array_equal(outs[i].residues(), ref[i])
         assert np.abs(p.ctx.decrypt(outs[i]) - np.roll(z, -k)).max() < TOL
+
+
+@pytest.mark.parametrize("name,approach", [("cfg1", 4), ("cfg3", 3), ("cfg3", 0)])
+def test_batched_conv_equals_single(oracle, golden, name, approach):
+    """fhe_conv2d_batch (keys/plaintexts streamed once per batch) = per-ciphertext conv, bit for bit."""
+    p = pair(oracle, name)
+    c, m, k, co, img, filt = conv_case(oracle, golden, name)
+    layer = p.ctx.conv_layer(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    cts = [p.ctx.encrypt(p.ctx.encode(np.roll(img, 37 * i)), ENC_SEED + i) for i in range(5)]
+    outs = p.ctx.conv2d_batch(cts, layer, approach)
+    for i, ct in enumerate(cts):
+        assert np.array_equal(outs[i].residues(), p.ctx.conv2d(ct, layer, approach).residues())
+    err = np.abs(p.ctx.decrypt(outs[0]) - golden[f"{name}/slots"]).max()
+    assert err < TOL, err
