@@ -348,19 +348,46 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
 // FastBConv of ModUp: one thread per (source, digit, coefficient pair); the
 // centered [x_i (Q_J/q_i)^-1]_{q_i} values are computed once and extended to
 // every target row of the digit (16-byte loads/stores); the digit's own rows
-// are NTT-domain copies of c1.
+// are NTT-domain copies of c1 (or the coefficients, for coefficient-domain
+// sources). The per-target constants of all digits are staged in shared memory.
 template <int KA>
 __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits, NttFuse fz, int level, int nsrc) {
     const int nr = level + 1, ne = nr + c.K;
     const int halfN = c.N / 2;
     const int total = nsrc * fz.dn * halfN;
-    RowMap rm{ne, level, c.L, 0};
+    // smem: per digit j, per target u: t, hat[KA], hat_sh[KA], n * Q_J mod t for n = 0..KA
+    constexpr int W = 1 + 2 * KA + (KA + 1);
+    __shared__ uint64_t tab[8 * 24 * W];
+    __shared__ int lohi[8][2];
+    for (int x = threadIdx.x; x < fz.dn * ne; x += blockDim.x) {
+        const int j = x / ne, u = x - j * ne;
+        const ModUpDigit& T = fz.mu[j];
+        uint64_t* e = tab + (size_t)x * W;
+        const uint64_t t = c.primes[u <= level ? u : c.L + (u - level - 1)].q;
+        e[0] = t;
+#pragma unroll
+        for (int a = 0; a < KA; ++a) {
+            e[1 + a] = T.hat[u][a];
+            e[1 + KA + a] = T.hat_sh[u][a];
+        }
+        uint64_t m = 0;
+        for (int n = 0; n <= KA; ++n) {
+            e[1 + 2 * KA + n] = m;
+            m = add_mod(m, T.qj[u], t);
+        }
+        if (u == 0) {
+            lohi[j][0] = T.lo;
+            lohi[j][1] = T.hi;
+        }
+    }
+    __syncthreads();
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
         const int sj = idx >> (c.logN - 1);
         const size_t k = (size_t)(idx & (halfN - 1)) * 2;
         const int src = sj / fz.dn, j = sj - src * fz.dn;
         const ModUpDigit& T = fz.mu[j];
-        const int na = T.hi - T.lo;
+        const int lo = lohi[j][0], hi = lohi[j][1];
+        const int na = hi - lo;
         const uint64_t* coef = fz.coef + (size_t)src * nr * c.N;
         const uint64_t* c1 = fz.c1 ? fz.c1 + (size_t)src * fz.c1_stride : nullptr;
         uint64_t* out = digits + (size_t)sj * ne * c.N + k;
@@ -370,8 +397,8 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
         for (int a = 0; a < KA; ++a) {
             v0[a] = v1[a] = 0;
             if (a < na) {
-                const int qi = T.lo + a;
-                const uint64_t q = c.primes[qi].q;
+                const int qi = lo + a;
+                const uint64_t q = tab[((size_t)j * ne + qi) * W];  // own prime q_qi
                 const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(coef + (size_t)qi * c.N + k));
                 v0[a] = mul_shoup(x.x, T.inv[a], T.inv_sh[a], q);
                 v1[a] = mul_shoup(x.y, T.inv[a], T.inv_sh[a], q);
@@ -383,21 +410,32 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
                     c1 ? __ldcs(reinterpret_cast<const ulonglong2*>(c1 + (size_t)qi * c.N + k)) : x;
             }
         }
-        for (int u = 0; u < ne; ++u) {
-            if (u >= T.lo && u < T.hi) continue;
-            const uint64_t t = c.primes[row_prime(rm, u)].q;
-            uint64_t y0 = 0, y1 = 0;
+        const uint64_t* tj = tab + (size_t)j * ne * W;
+        // targets outside [lo, hi): two branch-free runs
+#pragma unroll 1
+        for (int run = 0; run < 2; ++run) {
+            const int ub = run == 0 ? 0 : hi, ue = run == 0 ? lo : ne;
+#pragma unroll 4
+            for (int u = ub; u < ue; ++u) {
+                const uint64_t* e = tj + (size_t)u * W;
+                const uint64_t t = e[0];
+                // lazy sum of na < KA + 1 products, each in [0, 2t)
+                uint64_t y0 = 0, y1 = 0;
 #pragma unroll
-            for (int a = 0; a < KA; ++a) {
-                if (a < na) {
-                    y0 = add_mod(y0, mul_shoup(v0[a], T.hat[u][a], T.hat_sh[u][a], t), t);
-                    y1 = add_mod(y1, mul_shoup(v1[a], T.hat[u][a], T.hat_sh[u][a], t), t);
+                for (int a = 0; a < KA; ++a) {
+                    y0 += mul_shoup_lazy(v0[a], e[1 + a], e[1 + KA + a], t);
+                    y1 += mul_shoup_lazy(v1[a], e[1 + a], e[1 + KA + a], t);
                 }
+#pragma unroll
+                for (int r = (KA >= 3 ? 4 : (KA >= 2 ? 2 : 1)); r >= 1; r >>= 1) {
+                    y0 = y0 >= r * t ? y0 - r * t : y0;
+                    y1 = y1 >= r * t ? y1 - r * t : y1;
+                }
+                // centered lift: each of the n0 (n1) negative terms stands for -Q_J
+                y0 = sub_mod(y0, e[1 + 2 * KA + n0], t);
+                y1 = sub_mod(y1, e[1 + 2 * KA + n1], t);
+                *reinterpret_cast<ulonglong2*>(out + (size_t)u * c.N) = make_ulonglong2(y0, y1);
             }
-            const uint64_t qj = T.qj[u];
-            for (int n = 0; n < n0; ++n) y0 = sub_mod(y0, qj, t);  // centered lift
-            for (int n = 0; n < n1; ++n) y1 = sub_mod(y1, qj, t);
-            *reinterpret_cast<ulonglong2*>(out + (size_t)u * c.N) = make_ulonglong2(y0, y1);
         }
     }
 }
