@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -58,6 +59,7 @@ struct fhe_ctx {
     std::map<uint32_t, uint64_t*> keys;
     fhe_ledger ledger{};
     uint64_t launch_base = 0;
+    int giant_chunk = 8;  // giant steps per ModUp batch (FHECONV_GIANT_CHUNK)
     std::set<uint64_t> amounts;
     std::string err;
     // pinned staging
@@ -653,33 +655,37 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
     // so all giants go through one INTT, one conversion kernel, one ModUp
     // conversion and one forward NTT (the own-digit rows are transformed too).
     if (!giants.empty()) {
-        const int G = (int)giants.size();
+        const int Gall = (int)giants.size();
         const size_t dw = (size_t)dn * extw;
-        uint64_t* yc = c->alloc((size_t)G * extw);       // [G][ne][N] Y_g.c1, then its INTT
-        uint64_t* yq = c->alloc((size_t)G * nr * N);     // [G][nr][N] coef(ModDown(Y_g.c1))
-        uint64_t* dg = c->alloc((size_t)G * dw);         // [G][dn][ne][N] ModUp digits
-        for (int s = 0; s < G; ++s)
-            ck(cudaMemcpyAsync(yc + (size_t)s * extw, Y + (size_t)giants[s] * 2 * extw + extw, extw * 8,
-                               cudaMemcpyDeviceToDevice, c->st),
-               "memcpy");
-        c->timed("ntt", c->rows(2.0 * G * ne), [&] { ntt_inverse(c->dc, yc, G * ne, RowMap{ne, level, c->L, 0}, c->st); });
-        c->timed("moddown", c->rows((double)G * (ne + nr)),
-                 [&] { moddown_coef(c->dc, yq, yc, c->d_md, level, G, c->st); });
-        c->ledger.moddowns += G;
-        c->timed("ntt_modup", c->rows((double)G * nr + (double)G * dn * ne), [&] {
-            ntt_modup_coef(c->dc, dg, yq, G, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
-        });
-        c->ledger.modups += G;
-        for (int a0 = 0; a0 < G; a0 += kMaxBaby) {
-            const int n = std::min(kMaxBaby, G - a0);
+        // giants in chunks sized so that a chunk's digits stay L2-resident
+        // between the ModUp NTT passes and the key-switch accumulation
+        const int GC = std::max(1, std::min(Gall, c->giant_chunk));
+        uint64_t* yc = c->alloc((size_t)GC * extw);       // [G][ne][N] Y_g.c1, then its INTT
+        uint64_t* yq = c->alloc((size_t)GC * nr * N);     // [G][nr][N] coef(ModDown(Y_g.c1))
+        uint64_t* dg = c->alloc((size_t)GC * dw);         // [G][dn][ne][N] ModUp digits
+        for (int g0 = 0; g0 < Gall; g0 += GC) {
+            const int G = std::min(GC, Gall - g0);
+            for (int s = 0; s < G; ++s)
+                ck(cudaMemcpyAsync(yc + (size_t)s * extw, Y + (size_t)giants[g0 + s] * 2 * extw + extw, extw * 8,
+                                   cudaMemcpyDeviceToDevice, c->st),
+                   "memcpy");
+            c->timed("ntt", c->rows(2.0 * G * ne),
+                     [&] { ntt_inverse(c->dc, yc, G * ne, RowMap{ne, level, c->L, 0}, c->st); });
+            c->timed("moddown", c->rows((double)G * (ne + nr)),
+                     [&] { moddown_coef(c->dc, yq, yc, c->d_md, level, G, c->st); });
+            c->ledger.moddowns += G;
+            c->timed("ntt_modup", c->rows((double)G * nr + (double)G * dn * ne), [&] {
+                ntt_modup_coef(c->dc, dg, yq, G, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+            });
+            c->ledger.modups += G;
             KsStream ks{};
-            ks.n = n;
-            ks.digits = dg + (size_t)a0 * dw;
+            ks.n = G;
+            ks.digits = dg;
             ks.digit_stride = dw;
             ks.out = acc;
             ks.c0_qp = 1;
-            for (int s = 0; s < n; ++s) {
-                const int gi = giants[a0 + s];
+            for (int s = 0; s < G; ++s) {
+                const int gi = giants[g0 + s];
                 const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[gi]));
                 ks.galois[s] = g;
                 ks.key[s] = c->key_for(g);
@@ -1049,6 +1055,7 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
         bits.insert(bits.end(), p->p_bits, p->p_bits + p->n_p);
         c->primes = host::generate_primes(bits, (uint64_t)c->N);
         c->scale = std::ldexp(1.0, p->log_scale);
+        if (const char* e = std::getenv("FHECONV_GIANT_CHUNK")) c->giant_chunk = std::max(1, std::atoi(e));
         upload_tables(c);
     });
     if (rc != FHE_OK) {
