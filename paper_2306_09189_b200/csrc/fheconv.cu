@@ -42,7 +42,10 @@ uint64_t dev_words_alloc_count = 0;
 
 struct fhe_ctx {
     int device = 0;
-    cudaStream_t st = nullptr;
+    cudaStream_t st = nullptr;       // stream the internals enqueue on (main or a lane)
+    cudaStream_t main_st = nullptr;  // the context's stream
+    std::vector<cudaStream_t> lanes; // extra streams: independent ciphertexts of a batch overlap
+    bool fused_batch = false;        // FHECONV_BATCH_FUSED=1: batched kernels instead of lanes
     int logN = 0, N = 0, L = 0, K = 0, alpha = 0, dnum = 0, np = 0;
     std::vector<uint64_t> primes;
     double scale = 0;
@@ -76,6 +79,7 @@ struct fhe_ctx {
     };
     std::map<std::string, ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
+    std::vector<cudaEvent_t> pending_events;  // recycled at the next prof_collect / sync
 
     cudaEvent_t get_event() {
         if (!ev_pool.empty()) {
@@ -104,6 +108,9 @@ struct fhe_ctx {
     }
     void prof_collect() {
         ck(cudaStreamSynchronize(st), "sync");
+        for (cudaStream_t l : lanes) ck(cudaStreamSynchronize(l), "sync");
+        for (cudaEvent_t e : pending_events) ev_pool.push_back(e);
+        pending_events.clear();
         for (auto& kv : prof) {
             for (auto& pr : kv.second.pending) {
                 float ms = 0;
@@ -1007,7 +1014,7 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
     if (n == 0) return;
     if (approach < 0 || approach > 4) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3 or 4");
     if (approach == 0) approach = auto_orient(ly);
-    if (approach >= 3 && n > 1) {
+    if (approach >= 3 && n > 1 && c->fused_batch) {
         if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
         for (size_t s0 = 0; s0 < n; s0 += 32) {
             const int S = (int)std::min<size_t>(32, n - s0);
@@ -1015,7 +1022,41 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
         }
         return;
     }
-    for (size_t i = 0; i < n; ++i) conv_impl(c, cts[i], ly, approach, outs[i]);
+    if (approach >= 3) ensure_bsgs(c, ly, approach);  // layer constants are built on the main stream
+    if (n == 1 || c->lanes.size() <= 1) {
+        for (size_t i = 0; i < n; ++i) conv_impl(c, cts[i], ly, approach, outs[i]);
+        return;
+    }
+    // independent ciphertexts on independent lanes: the memory-bound key/plaintext
+    // streams of one conv overlap the integer-bound NTTs of another
+    if (c->pending_events.size() > 256) {
+        ck(cudaStreamSynchronize(c->main_st), "sync");
+        for (cudaEvent_t e : c->pending_events) c->ev_pool.push_back(e);
+        c->pending_events.clear();
+    }
+    cudaEvent_t start = c->get_event();
+    ck(cudaEventRecord(start, c->main_st), "cudaEventRecord");
+    for (cudaStream_t l : c->lanes) ck(cudaStreamWaitEvent(l, start, 0), "cudaStreamWaitEvent");
+    try {
+        for (size_t i = 0; i < n; ++i) {
+            c->st = c->lanes[i % c->lanes.size()];
+            conv_impl(c, cts[i], ly, approach, outs[i]);
+        }
+    } catch (...) {
+        c->st = c->main_st;
+        throw;
+    }
+    c->st = c->main_st;
+    std::vector<cudaEvent_t> done;
+    for (cudaStream_t l : c->lanes) {
+        cudaEvent_t e = c->get_event();
+        ck(cudaEventRecord(e, l), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->main_st, e, 0), "cudaStreamWaitEvent");
+        done.push_back(e);
+    }
+    // events can be recycled once the main stream has passed them
+    c->pending_events.push_back(start);
+    for (cudaEvent_t e : done) c->pending_events.push_back(e);
 }
 
 }  // namespace
@@ -1040,6 +1081,15 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
         ck(cudaGetDeviceProperties(&prop, c->device), "cudaGetDeviceProperties");
         if (prop.major < 10) fail(FHE_E_CUDA, "libfheconv is built for sm_100a (B200)");
         ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "cudaStreamCreate");
+        c->main_st = c->st;
+        int nl = 4;
+        if (const char* e = std::getenv("FHECONV_LANES")) nl = std::max(1, std::atoi(e));
+        for (int i = 0; i < nl; ++i) {
+            cudaStream_t l;
+            ck(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking), "cudaStreamCreate");
+            c->lanes.push_back(l);
+        }
+        if (const char* e = std::getenv("FHECONV_BATCH_FUSED")) c->fused_batch = std::atoi(e) != 0;
         cudaMemPool_t pool;
         ck(cudaDeviceGetDefaultMemPool(&pool, c->device), "mempool");
         uint64_t thresh = ~0ULL;
@@ -1085,7 +1135,11 @@ void fhe_ctx_destroy(fhe_ctx* c) {
             cudaEventDestroy(pr.first);
             cudaEventDestroy(pr.second);
         }
-    if (c->st) cudaStreamDestroy(c->st);
+    for (cudaStream_t l : c->lanes) {
+        cudaStreamSynchronize(l);
+        cudaStreamDestroy(l);
+    }
+    if (c->main_st) cudaStreamDestroy(c->main_st);
     delete c;
 }
 
@@ -1102,7 +1156,10 @@ int fhe_ctx_info(const fhe_ctx* c, int* log_n, int* n_q, int* n_p, int* dnum, ui
 }
 
 int fhe_synchronize(fhe_ctx* c) {
-    return guard(c, [&] { ck(cudaStreamSynchronize(c->st), "cudaStreamSynchronize"); });
+    return guard(c, [&] {
+        ck(cudaStreamSynchronize(c->main_st), "cudaStreamSynchronize");
+        for (cudaStream_t l : c->lanes) ck(cudaStreamSynchronize(l), "cudaStreamSynchronize");
+    });
 }
 
 int fhe_timer_start(fhe_ctx* c) {
