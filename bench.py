@@ -40,7 +40,7 @@ C_IN = C_OUT = 16
 M = 32
 KAPPA = 3
 WORKLOAD = ("cfg3: CKKS N=2^15 (16384 slots), 60+12x50-bit q | 2x60-bit p, scale 2^50, dnum 7; image 32x32x16 "
-            "U[-1,1]; 3x3 conv 16->16 same padding, weights U[-1,1]; + 1 rescale; 1 ciphertext per step")
+            "U[-1,1]; 3x3 conv 16->16 same padding, weights U[-1,1]; + 1 rescale; step = batch of --batch ciphertexts")
 
 
 def job_value(world, units_per_rank, max_elapsed_s):
@@ -164,26 +164,29 @@ def conv_reference_numpy(img, w):
 
 
 def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
     import torch
-    from paper_2306_09189_b200 import Context
+    from paper_2306_09189_b200 import Context, _lib
+    from paper_2306_09189_b200.engine import lib
 
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    B = args.batch
     ctx = Context.from_config(CFG, device=local_rank)
     ctx.keygen(7)
     rng = np.random.default_rng(1234 + rank)
-    img = rng.uniform(-1, 1, C_IN * M * M)
+    imgs = [rng.uniform(-1, 1, C_IN * M * M) for _ in range(B)]
     w = rng.uniform(-1, 1, C_IN * C_OUT * KAPPA * KAPPA)
     layer = ctx.conv_layer(C_IN, C_OUT, M, KAPPA, w)
     ctx.gen_galois_keys(layer.steps())
-    ct = ctx.encrypt(ctx.encode(img), 9000 + rank)
-    out = ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1)
+    cts = [ctx.encrypt(ctx.encode(x), 9000 + rank * 1000 + i) for i, x in enumerate(imgs)]
+    outs = [ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1) for _ in range(B)]
     level = ctx.max_level
     approach = args.approach
-    ref = conv_reference_numpy(img, w)
 
     def barrier():
         if dist:
@@ -191,6 +194,40 @@ def run_ours(args, rank, world, local_rank):
 
     def max_over_ranks(v):
         return reduce_max(v, dist, "cuda")
+
+    # correctness gate before timing: every decrypted output vs a float64 numpy conv
+    ctx.conv2d_batch_into(cts, layer, approach, outs)
+    err = max(float(np.abs(ctx.decrypt(o)[: C_OUT * M * M] - conv_reference_numpy(x, w)).max())
+              for o, x in zip(outs, imgs))
+    assert err < 1e-6, f"decrypted conv error {err}"
+
+    # ---- timed region: K steps, each = the batch of B ciphertexts through the layer
+    for _ in range(args.warmup):
+        ctx.conv2d_batch_into(cts, layer, approach, outs)
+    ctx.synchronize()
+    launches0 = ctx.ledger()["kernel_launches"]
+    barrier()
+    ctx.synchronize()
+    with ClockSampler(local_rank) as clk:
+        ctx.timer_start()
+        for _ in range(args.steps):
+            ctx.conv2d_batch_into(cts, layer, approach, outs)
+        ms = ctx.timer_stop()  # synchronises the context stream (which joins the lanes)
+    barrier()
+    launches = ctx.ledger()["kernel_launches"] - launches0
+    ms_max = max_over_ranks(ms)
+
+    # ---- per-kernel profile: one ciphertext per conv, no lane overlap, CUDA events per launch
+    ct, out = cts[0], outs[0]
+    kp = max(10, args.steps // 4)
+    ctx.prof_reset()
+    ctx.prof_enable(True)
+    ctx.timer_start()
+    for _ in range(kp):
+        ctx.conv2d_into(ct, layer, approach, out)
+    ms1 = ctx.timer_stop()
+    ctx.prof_enable(False)
+    prof = {cl: ctx.prof_get_bytes(cl) for cl in KERNEL_CLASSES}
 
     def timed_convs(ap, steps, warmup):
         for _ in range(warmup):
@@ -201,71 +238,53 @@ def run_ours(args, rank, world, local_rank):
             ctx.conv2d_into(ct, layer, ap, out)
         return max_over_ranks(ctx.timer_stop())
 
-    # correctness gate before timing: decrypted output vs a float64 numpy conv
-    ctx.conv2d_into(ct, layer, approach, out)
-    err = float(np.abs(ctx.decrypt(out)[: C_OUT * M * M] - ref).max())
-    assert err < 1e-6, f"decrypted conv error {err}"
-
-    for _ in range(args.warmup):
-        ctx.conv2d_into(ct, layer, approach, out)
-    ctx.synchronize()
-    ctx.prof_reset()
-    ctx.prof_enable(True)
-    launches0 = ctx.ledger()["kernel_launches"]
-    barrier()
-    ctx.synchronize()
-    with ClockSampler(local_rank) as clk:
-        ctx.timer_start()
-        for _ in range(args.steps):
-            ctx.conv2d_into(ct, layer, approach, out)
-        ms = ctx.timer_stop()  # synchronises the stream
-    barrier()
-    ctx.prof_enable(False)
-    launches = ctx.ledger()["kernel_launches"] - launches0
-    prof = {c: ctx.prof_get_bytes(c) for c in KERNEL_CLASSES}
-    ms_max = max_over_ranks(ms)
-
-    # the same conv under every schedule (device-timed, same context)
     per_approach = {}
     for ap in (1, 2, 3, 4):
-        k2 = max(3, args.steps // 4) if ap in (1, 2) else max(3, args.steps // 2)
+        k2 = max(3, args.steps // 8) if ap in (1, 2) else max(5, args.steps // 4)
         per_approach[ap] = world * k2 / (timed_convs(ap, k2, 2) / 1e3)
     # hoisted rotations at N = 2^15: the 8 non-identity shifts of a 3x3 stencil from one ModUp
     stencil = [kk * M + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1) if kk or ll]
     for _ in range(2):
         ctx.rotate_hoisted(ct, stencil)
     ctx.synchronize()
-    kh = max(3, args.steps)
+    kh = max(10, args.steps // 2)
     ctx.timer_start()
     for _ in range(kh):
-        outs = ctx.rotate_hoisted(ct, stencil)
+        hs = ctx.rotate_hoisted(ct, stencil)
     ms_hoist = max_over_ranks(ctx.timer_stop())
-    del outs
+    del hs
 
-    # e2e: the C ABI with host buffers, H2D + conv + D2H inside the timed region
-    import ctypes as C
-    from paper_2306_09189_b200 import _lib
-    from paper_2306_09189_b200.engine import lib
+    # ---- e2e: the C ABI with pinned host buffers; H2D of the batch, conv, D2H of the results
     N = ctx.N
-    h_in = torch.empty(2 * (level + 1) * N, dtype=torch.int64, pin_memory=True)
-    h_out = torch.empty(2 * level * N, dtype=torch.int64, pin_memory=True)
-    h_in.numpy().view(np.uint64)[:] = ct.residues().ravel()
+    in_words, out_words = 2 * (level + 1) * N, 2 * level * N
+    h_in = torch.empty(B * in_words, dtype=torch.int64, pin_memory=True)
+    h_out = torch.empty(B * out_words, dtype=torch.int64, pin_memory=True)
+    hv = h_in.numpy().view(np.uint64)
+    for i, x in enumerate(cts):
+        hv[i * in_words:(i + 1) * in_words] = x.residues().ravel()
     L_ = lib()
-    pin_in = C.cast(h_in.data_ptr(), _lib.u64p)
-    pin_out = C.cast(h_out.data_ptr(), _lib.u64p)
-    ct_dev = ctx.upload(ct.residues(), level)
+    dev_in = [ctx.upload(x.residues(), level) for x in cts]
+    u64 = _lib.u64p
+
+    def e2e_step():
+        for i in range(B):
+            assert L_.fhe_ct_upload_into(ctx.h, C.cast(h_in.data_ptr() + i * in_words * 8, u64), dev_in[i].h) == 0
+        ctx.conv2d_batch_into(dev_in, layer, approach, outs)
+        for i in range(B):
+            assert L_.fhe_ct_download(ctx.h, outs[i].h, C.cast(h_out.data_ptr() + i * out_words * 8, u64),
+                                      out_words) == 0
+
     for _ in range(2):
-        L_.fhe_ct_upload_into(ctx.h, pin_in, ct_dev.h)
-        ctx.conv2d_into(ct_dev, layer, approach, out)
-        L_.fhe_ct_download(ctx.h, out.h, pin_out, h_out.numel())
+        e2e_step()
     barrier()
+    ke = max(5, args.steps // 2)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        assert L_.fhe_ct_upload_into(ctx.h, pin_in, ct_dev.h) == 0
-        ctx.conv2d_into(ct_dev, layer, approach, out)
-        assert L_.fhe_ct_download(ctx.h, out.h, pin_out, h_out.numel()) == 0  # synchronises
+    for _ in range(ke):
+        e2e_step()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e_err = float(np.abs(ctx.decrypt(out)[: C_OUT * M * M] - ref).max())
+    e2e_err = float(np.abs(ctx.decrypt(outs[0])[: C_OUT * M * M] - conv_reference_numpy(imgs[0], w)).max())
+
+    cfg2 = cfg2_rotations(world) if (rank == 0 and not args.no_cfg2) else None
 
     if rank != 0:
         if dist:
@@ -273,19 +292,19 @@ def run_ours(args, rank, world, local_rank):
         return None
 
     step_s = ms_max / 1e3 / args.steps
-    value = job_value(world, args.steps, ms_max / 1e3)
+    value = job_value(world, args.steps * B, ms_max / 1e3)
     peak, peak_kind = measured_peak()
     kernels = {}
     for cls, (kms, kn, kbytes) in prof.items():
         if kn == 0:
             continue
         gbs = kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
-        kernels[cls] = {"ms_per_step": round(kms / args.steps, 4), "share": round(kms / ms, 3),
-                        "launches_per_step": round(kn / args.steps, 1),
+        kernels[cls] = {"ms_per_conv": round(kms / kp, 4), "share": round(kms / ms1, 3),
+                        "launches_per_conv": round(kn / kp, 1),
                         "algorithmic_mb_per_launch": round(kbytes / kn / 1e6, 2),
                         "achieved_gbs": round(gbs, 1), "frac_hbm": round(gbs / peak, 3),
                         "note": KERNEL_NOTES.get(cls, "")}
-    dom = max(kernels, key=lambda c: kernels[c]["ms_per_step"])
+    dom = max(kernels, key=lambda c: kernels[c]["ms_per_conv"])
     dms, dn_, dbytes = prof[dom]
     avg_s = dms / 1e3 / dn_
     achieved = dbytes / dn_ / avg_s / 1e9
@@ -305,28 +324,34 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u64 (RNS residues mod 40-60-bit primes)",
-        "data": "synthetic (seeded U[-1,1] image/weights, BASELINE cfg3 shapes); no dataset involved",
+        "data": "synthetic (seeded U[-1,1] images/weights, BASELINE cfg3 shapes); no dataset involved",
         "config": {"workload": WORKLOAD, "approach": approach,
                    "schedule": {0: "auto (BSGS: hoisted channel rotations + aggregated shifts)", 1: "paper Approach 1",
                                 2: "paper Approach 2", 3: "BSGS, hoisted channel rotations",
                                 4: "BSGS, hoisted shifts"}[approach],
-                   "batch_per_gpu": 1, "parallelism": f"replicas x{world}",
+                   "batch_per_gpu": B, "step": f"{B} independent ciphertexts through the layer "
+                   "(fhe_conv2d_batch_into; 4 CUDA-stream lanes)", "parallelism": f"replicas x{world}",
                    "l2": "no flush: per-step key stream (23 Galois keys, 1.27 GB) >> 126 MB L2", "key_seed": 7,
-                   "enc_seed": 9000, "decrypt_max_abs_err": err},
+                   "enc_seed": 9000, "decrypt_max_abs_err": err,
+                   "latency_ms_single_conv": round(ms1 / kp, 4)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dom),
                      "algorithmic_bytes_per_launch": round(dbytes / dn_), "avg_launch_ms": round(avg_s * 1e3, 4),
-                     "peak_kind": peak_kind, "note": KERNEL_NOTES.get(dom, "") +
+                     "peak_kind": peak_kind, "measured_on": "profiled single-ciphertext pass right after the timed region",
+                     "note": KERNEL_NOTES.get(dom, "") +
                      ("; NTT-class kernels are integer-pipe bound (see kernels[].frac_hbm and profiles/)"
                       if dom.startswith("ntt") else "")},
-        "keyswitch_roofline": {"kernels": ks_cls, "achieved_gbs": round(ks_bytes / (ks_ms / 1e3) / 1e9, 1) if ks_ms else None,
+        "keyswitch_roofline": {"kernels": ks_cls,
+                               "achieved_gbs": round(ks_bytes / (ks_ms / 1e3) / 1e9, 1) if ks_ms else None,
                                "frac": round(ks_bytes / (ks_ms / 1e3) / 1e9 / peak, 4) if ks_ms else None},
         "kernels": kernels,
-        "conv_per_s_by_approach": {str(k): round(v, 2) for k, v in per_approach.items()},
+        "conv_per_s_by_approach_batch1": {str(k): round(v, 2) for k, v in per_approach.items()},
         "hoisted_rot_per_s": round(world * kh * len(stencil) / (ms_hoist / 1e3), 1),
-        "e2e": {"value": round(world * args.steps / e2e_s, 3), "unit": "conv/s",
-                "h2d_bytes_per_step": int(h_in.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
-                "api": "fhe_ct_upload_into + fhe_conv2d_into + fhe_ct_download (C ABI, pinned host buffers)",
+        "cfg2_rotations": cfg2,
+        "e2e": {"value": round(world * ke * B / e2e_s, 3), "unit": "conv/s",
+                "h2d_bytes_per_step": int(B * in_words * 8), "d2h_bytes_per_step": int(B * out_words * 8),
+                "api": "fhe_ct_upload_into x B + fhe_conv2d_batch_into + fhe_ct_download x B "
+                       "(C ABI, pinned host buffers)",
                 "decrypt_max_abs_err": e2e_err},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -336,6 +361,42 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.destroy_process_group()
     return line
+
+
+def cfg2_rotations(world):
+    """BASELINE cfg2 (N=2^14, 8x50-bit q | 1x60-bit p): rotations by every amount
+    1..127 through power-of-two keys only, positive vs signed decomposition
+    (reference rot.cpp:21-46), and the hoisted 3x3 stencil (m = 32)."""
+    from paper_2306_09189_b200 import Context, decompose
+    ctx = Context.from_config("cfg2")
+    ctx.keygen(7)
+    pow2 = [1 << i for i in range(8)]
+    stencil = [kk * 32 + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1) if kk or ll]
+    ctx.gen_galois_keys(pow2 + [-x for x in pow2] + stencil)
+    z = np.random.default_rng(5).uniform(-1, 1, ctx.slots)
+    ct = ctx.encrypt(ctx.encode(z), 1)
+    res = {}
+    for strat, name in ((0, "positive"), (1, "signed")):
+        keyed = sum(len(decompose(strat, n, ctx.slots)) for n in range(1, 128))
+        ctx.rotate_decomposed(ct, 127, strat)
+        ctx.synchronize()
+        ctx.timer_start()
+        for n in range(1, 128):
+            r = ctx.rotate_decomposed(ct, n, strat)
+        ms = ctx.timer_stop()
+        res[name] = {"requested_rot_per_s": round(world * 127 / (ms / 1e3), 1),
+                     "keyed_switches_per_s": round(world * keyed / (ms / 1e3), 1), "keyed_per_vector": keyed}
+    del r
+    ctx.rotate_hoisted(ct, stencil)
+    ctx.synchronize()
+    ctx.timer_start()
+    for _ in range(20):
+        hs = ctx.rotate_hoisted(ct, stencil)
+    ms = ctx.timer_stop()
+    del hs
+    res["hoisted_stencil_rot_per_s"] = round(world * 20 * len(stencil) / (ms / 1e3), 1)
+    res["note"] = "one ciphertext, amounts 1..127 sequentially; hoisted = 8 stencil shifts from one ModUp"
+    return res
 
 
 # ------------------------------------------------------------ CPU baselines
@@ -428,12 +489,14 @@ def run_reference(args, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--approach", type=int, default=0, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-golden", action="store_true", help="skip the golden-model CKKS CPU timing")
+    ap.add_argument("--batch", type=int, default=8, help="ciphertexts per step (independent images)")
+    ap.add_argument("--no-cfg2", action="store_true", help="skip the cfg2 rotation microbenchmark")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
