@@ -285,6 +285,7 @@ def run_ours(args, rank, world, local_rank):
     e2e_err = float(np.abs(ctx.decrypt(outs[0])[: C_OUT * M * M] - conv_reference_numpy(imgs[0], w)).max())
 
     cfg2 = cfg2_rotations(world) if (rank == 0 and not args.no_cfg2) else None
+    other_cfgs = other_configs(world, local_rank) if (rank == 0 and not args.no_cfg2) else None
 
     if rank != 0:
         if dist:
@@ -348,6 +349,7 @@ def run_ours(args, rank, world, local_rank):
         "conv_per_s_by_approach_batch1": {str(k): round(v, 2) for k, v in per_approach.items()},
         "hoisted_rot_per_s": round(world * kh * len(stencil) / (ms_hoist / 1e3), 1),
         "cfg2_rotations": cfg2,
+        "other_configs": other_cfgs,
         "e2e": {"value": round(world * ke * B / e2e_s, 3), "unit": "conv/s",
                 "h2d_bytes_per_step": int(B * in_words * 8), "d2h_bytes_per_step": int(B * out_words * 8),
                 "api": "fhe_ct_upload_into x B + fhe_conv2d_batch_into + fhe_ct_download x B "
@@ -361,6 +363,73 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.destroy_process_group()
     return line
+
+
+def other_configs(world, device):
+    """BASELINE cfg1 (N=2^13 4->4 3x3), cfg4 (N=2^16 8->8 5x5) and cfg5 (three
+    3x3 16->16 layers at cfg3 parameters, batch 32): conv/s of the fastest
+    schedule, each checked against a float64 numpy conv before timing."""
+    from paper_2306_09189_b200 import Context
+    res = {}
+    for name, (c, m, k, wk, batch) in {"cfg1": (4, 32, 3, 0, 8), "cfg4": (8, 64, 5, 2, 4)}.items():
+        ctx = Context.from_config(name, device=device)
+        ctx.keygen(7)
+        rng = np.random.default_rng(77)
+        w = rng.uniform(-1, 1, c * c * k * k) if wk == 0 else np.clip(rng.normal(0, 0.1, c * c * k * k), -1, 1)
+        imgs = [rng.uniform(-1, 1, c * m * m) for _ in range(batch)]
+        layer = ctx.conv_layer(c, c, m, k, w)
+        ctx.gen_galois_keys(layer.steps())
+        cts = [ctx.encrypt(ctx.encode(x), 100 + i) for i, x in enumerate(imgs)]
+        outs = [ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1) for _ in range(batch)]
+        ctx.conv2d_batch_into(cts, layer, 0, outs)
+        x = imgs[0].reshape(c, m, m)
+        wt = w.reshape(c, c, k, k)
+        h = k // 2
+        xp = np.pad(x, ((0, 0), (h, h), (h, h)))
+        ref = sum(np.einsum("fg,fij->gij", wt[:, :, a, b], xp[:, a:a + m, b:b + m]) for a in range(k) for b in range(k))
+        err = float(np.abs(ctx.decrypt(outs[0])[: c * m * m] - ref.ravel()).max())
+        reps = 5
+        ctx.synchronize()
+        ctx.timer_start()
+        for _ in range(reps):
+            ctx.conv2d_batch_into(cts, layer, 0, outs)
+        ms = ctx.timer_stop()
+        ctx.timer_start()
+        for _ in range(reps):
+            ctx.conv2d_into(cts[0], layer, 0, outs[0])
+        ms1 = ctx.timer_stop()
+        res[name] = {"conv_per_s": round(world * reps * batch / (ms / 1e3), 1), "batch": batch,
+                     "latency_ms": round(ms1 / reps, 4), "decrypt_max_abs_err": err}
+        ctx.close()
+    # cfg5: 3 stacked 3x3 16->16 layers (weights U[-0.5,0.5]), one rescale each, batch 32
+    ctx = Context.from_config("cfg5", device=device)
+    ctx.keygen(7)
+    rng = np.random.default_rng(55)
+    layers, lv = [], ctx.max_level
+    for li in range(3):
+        layers.append(ctx.conv_layer(16, 16, 32, 3, rng.uniform(-0.5, 0.5, 16 * 16 * 9), level=lv))
+        lv -= 1
+    ctx.gen_galois_keys(layers[0].steps())
+    B5 = 32
+    cts = [ctx.encrypt(ctx.encode(rng.uniform(-1, 1, 16 * 32 * 32)), 500 + i) for i in range(B5)]
+    bufs = [[ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1 - li), 1) for _ in range(B5)]
+            for li in range(3)]
+
+    def stack():
+        src = cts
+        for li in range(3):
+            ctx.conv2d_batch_into(src, layers[li], 0, bufs[li])
+            src = bufs[li]
+
+    stack()
+    ctx.synchronize()
+    ctx.timer_start()
+    stack()
+    ms = ctx.timer_stop()
+    res["cfg5"] = {"three_layer_passes_per_s": round(world * B5 / (ms / 1e3), 2),
+                   "conv_per_s": round(world * 3 * B5 / (ms / 1e3), 1), "batch": B5, "levels_consumed": 3}
+    ctx.close()
+    return res
 
 
 def cfg2_rotations(world):
