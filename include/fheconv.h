@@ -168,7 +168,8 @@ int fhe_decompose(int strategy, uint64_t n, uint64_t s, int64_t* steps, int cap)
 int fhe_conv_layer_create(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
                           int level, fhe_conv_layer** out);
 void fhe_conv_layer_free(fhe_conv_layer* layer);
-/* Galois steps a layer needs (channel rotations r m^2 and shifts kk m + ll) */
+/* Galois steps a layer needs for `approach`: 1-4 channel rotations r m^2 and
+ * shifts kk m + ll; 5 r m^2 + ll and kk m; 0 the union (any approach runs) */
 int fhe_conv_layer_steps(const fhe_conv_layer* layer, int approach, int64_t* steps, size_t cap, size_t* n);
 /* replaces: conv_plan(eng, p, k, plan) conv.cpp:266-271.
  * approach 1 = paper Approach 1 (ConvPlan::ChannelFirst: shifts first),
@@ -178,7 +179,10 @@ int fhe_conv_layer_steps(const fhe_conv_layer* layer, int approach, int64_t* ste
  *              decomposition, shifts applied once to aggregated sums
  *              (rotated plaintexts),
  * approach 4 = baby-step/giant-step with the roles swapped (shifts hoisted),
- * approach 0 = 3 or 4, whichever needs fewer decompositions.
+ * approach 5 = fused baby-step/giant-step: the c kappa rotations r m^2 + ll are
+ *              hoisted and multiplied out in one kernel without materialising
+ *              the rotated copies, the kappa row shifts kk m are giant steps,
+ * approach 0 = 5 when c_in kappa <= 96 baby steps, else 3 or 4 (fewer giants).
  * All approaches decrypt to the same slots (within CKKS noise).
  * Output: one ciphertext at level - 1 (one rescale). */
 int fhe_conv2d(fhe_ctx* ctx, const fhe_ct* ct, const fhe_conv_layer* layer, int approach, fhe_ct** out);

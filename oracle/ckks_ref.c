@@ -916,7 +916,11 @@ static void conv_accumulate(const ck_ctx* ck, int level, const uint64_t* pt, con
 /* Baby-step / giant-step conv with output aggregation.
  * orient 3: baby steps = channel rotations r m^2 (hoisted from one ModUp of
  *           the input), giant steps = shifts kk m + ll;
- * orient 4: baby steps = shifts, giant steps = channel rotations.
+ * orient 4: baby steps = shifts, giant steps = channel rotations;
+ * orient 5: baby steps = channel rotations combined with column shifts
+ *           r m^2 + ll (c kappa of them), giant steps = row shifts kk m
+ *           (kappa of them): more (cheap) hoisted baby steps for fewer
+ *           giant steps, each of which costs a ModDown + ModUp.
  * With X_b = rot_b(ct) kept in the QP basis (never ModDown'd),
  *   Y_g = sum_b rot_{-g}(pt_{g,b}) * X_b                      (QP accumulators)
  *   out = Rescale(ModDown(Y_0 + sum_{g != 0} KS_g(Y_g)))
@@ -930,11 +934,17 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
     const size_t extw = (size_t)ne * N, ctw = (size_t)2 * nr * N;
     const uint64_t ql = ck->q[level];
     const double pscale = (double)ql;
-    const int nb = orient == 3 ? c : nk, ngi = orient == 3 ? nk : c;
+    const int kap = (int)(2 * h + 1);
+    const int nb = orient == 3 ? c : orient == 4 ? nk : c * kap;
+    const int ngi = orient == 3 ? nk : orient == 4 ? c : kap;
     long* bamt = malloc((size_t)nb * sizeof(long));
     long* gamt = malloc((size_t)ngi * sizeof(long));
-    for (int r = 0; r < c; r++) (orient == 3 ? bamt : gamt)[r] = (long)r * (long)block;
-    {
+    if (orient == 5) {
+        for (int r = 0; r < c; r++)
+            for (long ll = -h; ll <= h; ll++) bamt[r * kap + (ll + h)] = (long)r * (long)block + ll;
+        for (long kk = -h; kk <= h; kk++) gamt[kk + h] = kk * m;
+    } else {
+        for (int r = 0; r < c; r++) (orient == 3 ? bamt : gamt)[r] = (long)r * (long)block;
         int i = 0;
         for (long kk = -h; kk <= h; kk++)
             for (long ll = -h; ll <= h; ll++, i++) (orient == 3 ? gamt : bamt)[i] = kk * m + ll;
@@ -953,8 +963,18 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
     double* rplain = malloc(s * sizeof(double));
     for (int gi = 0; gi < ngi; gi++)
         for (int bi = 0; bi < nb; bi++) {
-            const int r = orient == 3 ? bi : gi, i = orient == 3 ? gi : bi;
-            const long kk = i / (2 * h + 1) - h, ll = i % (2 * h + 1) - h;
+            int r;
+            long kk, ll;
+            if (orient == 5) {
+                r = bi / kap;
+                ll = bi % kap - h;
+                kk = gi - h;
+            } else {
+                r = orient == 3 ? bi : gi;
+                const int i = orient == 3 ? gi : bi;
+                kk = i / kap - h;
+                ll = i % kap - h;
+            }
             if (!emu_fused_plain(c, m, kappa, c_out, s, filt, r, kk, ll, 1.0, plain)) continue;
             nonempty[gi * nb + bi] = 1;
             emu_rotate(plain, rplain, s, -gamt[gi]);
@@ -1046,7 +1066,7 @@ int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int k
             const double* filt, int plan, uint64_t* out, double* out_scale) {
     const size_t N = ck->N, s = N / 2, block = (size_t)m * m;
     if ((size_t)c * block > s || s % block || (size_t)c_out * block > s || level < 1) return -1;
-    if (plan == 3 || plan == 4) return conv_bsgs(ck, ct, level, c, m, kappa, c_out, filt, plan, out, out_scale);
+    if (plan >= 3 && plan <= 5) return conv_bsgs(ck, ct, level, c, m, kappa, c_out, filt, plan, out, out_scale);
     const int nr = level + 1, ne = nr + ck->K, dn = ck_dnum_at(ck, level);
     const long h = kappa / 2;
     const int nk = (int)((2 * h + 1) * (2 * h + 1));

@@ -92,7 +92,9 @@ void ck_rotate_hoisted(const ck_ctx* ck, const uint64_t* ct, int level, const lo
 /* Fused single-shard encrypted convolution: plan 1 =
  * Approach 1 (shifts first), plan 2 = Approach 2 (channel rotations first),
  * plan 3 = BSGS with hoisted channel rotations + aggregated shifts,
- * plan 4 = BSGS with hoisted shifts + aggregated channel rotations.
+ * plan 4 = BSGS with hoisted shifts + aggregated channel rotations,
+ * plan 5 = BSGS with hoisted channel+column rotations r m^2 + ll and
+ *          aggregated row shifts kk m.
  * Input ct at `level` (scale = ck_scale), output ct at level - 1 after one
  * rescale; *out_scale receives the output scale. */
 int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,

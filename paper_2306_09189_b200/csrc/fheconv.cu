@@ -46,6 +46,7 @@ struct fhe_ctx {
     cudaStream_t main_st = nullptr;  // the context's stream
     std::vector<cudaStream_t> lanes; // extra streams: independent ciphertexts of a batch overlap
     bool fused_batch = false;        // FHECONV_BATCH_FUSED=1: batched kernels instead of lanes
+    bool batch5 = true;              // approach 5: sources batched through one fused launch (FHECONV_BATCH5=0: lanes)
     int logN = 0, N = 0, L = 0, K = 0, alpha = 0, dnum = 0, np = 0;
     std::vector<uint64_t> primes;
     double scale = 0;
@@ -191,14 +192,15 @@ struct fhe_conv_layer {
     uint64_t* d_pts;            // [c_in][nk][ne][N]
     size_t pt_words;
     std::vector<double> weights;
-    // BSGS plaintext sets (approach 3: baby = channel rotations, 4: baby = shifts)
+    // BSGS plaintext sets (approach 3: baby = channel rotations, 4: baby = shifts,
+    // 5: baby = channel rotation + column shift r m^2 + ll, giant = row shift kk m)
     struct Bsgs {
         bool ready = false;
         int nb = 0, ngi = 0;
         std::vector<int64_t> bamt, gamt;
         std::vector<int> nonempty;  // [ngi][nb]
         uint64_t* d_pts = nullptr;  // [ngi][nb][ne][N], pt'[g][b] = rot_{-g}(pt)
-    } bs[2];
+    } bs[3];
 };
 
 namespace {
@@ -333,7 +335,9 @@ void upload_tables(fhe_ctx* c) {
     for (int i = 0; i < np; ++i) {
         const uint64_t q = c->primes[i];
         const u128 ratio = (~(u128)0) / q;  // floor((2^128 - 1) / q) == floor(2^128 / q) for odd q
-        pr[i] = Prime{q, (uint64_t)(ratio >> 64), (uint64_t)ratio, 0};
+        uint64_t inv = q;  // Newton: q^-1 mod 2^64 (q odd), 6 doublings of precision
+        for (int it = 0; it < 6; ++it) inv *= 2 - q * inv;
+        pr[i] = Prime{q, (uint64_t)(ratio >> 64), (uint64_t)ratio, (uint64_t)0 - inv};
     }
     std::vector<uint64_t> tw((size_t)np * N), tws((size_t)np * N), itw((size_t)np * N), itws((size_t)np * N);
     std::vector<uint64_t> ninv(np), ninvs(np);
@@ -559,11 +563,20 @@ fhe_conv_layer::Bsgs& ensure_bsgs(fhe_ctx* c, const fhe_conv_layer* cly, int ori
     for (int r = 0; r < ly->c_in; ++r) chan.push_back((int64_t)r * block);
     for (long kk = -h; kk <= h; ++kk)
         for (long ll = -h; ll <= h; ++ll) shift.push_back(kk * m + ll);
-    B.bamt = orient == 3 ? chan : shift;
-    B.gamt = orient == 3 ? shift : chan;
+    const int kap = (int)(2 * h + 1);
+    if (orient == 5) {
+        B.bamt.clear();
+        B.gamt.clear();
+        for (int r = 0; r < ly->c_in; ++r)
+            for (long ll = -h; ll <= h; ++ll) B.bamt.push_back((int64_t)r * block + ll);
+        for (long kk = -h; kk <= h; ++kk) B.gamt.push_back(kk * m);
+    } else {
+        B.bamt = orient == 3 ? chan : shift;
+        B.gamt = orient == 3 ? shift : chan;
+    }
     B.nb = (int)B.bamt.size();
     B.ngi = (int)B.gamt.size();
-    if (B.nb > kMaxBaby) fail(FHE_E_INVALID, "too many baby steps for the BSGS schedule");
+    if (B.nb > (orient == 5 ? kMaxFused : kMaxBaby)) fail(FHE_E_INVALID, "too many baby steps for the BSGS schedule");
     const int ne = c->ne_at(ly->level);
     const size_t extw = (size_t)ne * c->N, s = c->slots();
     ck(cudaMalloc(&B.d_pts, (size_t)B.ngi * B.nb * extw * 8), "cudaMalloc");
@@ -572,8 +585,18 @@ fhe_conv_layer::Bsgs& ensure_bsgs(fhe_ctx* c, const fhe_conv_layer* cly, int ori
     std::vector<double> plain, rot(s);
     for (int gi = 0; gi < B.ngi; ++gi)
         for (int bi = 0; bi < B.nb; ++bi) {
-            const int r = orient == 3 ? bi : gi, i = orient == 3 ? gi : bi;
-            const long kk = i / (2 * h + 1) - h, ll = i % (2 * h + 1) - h;
+            int r;
+            long kk, ll;
+            if (orient == 5) {
+                r = bi / kap;
+                ll = bi % kap - h;
+                kk = gi - h;
+            } else {
+                r = orient == 3 ? bi : gi;
+                const int i = orient == 3 ? gi : bi;
+                kk = i / kap - h;
+                ll = i % kap - h;
+            }
             if (!fused_plain(ly->c_in, ly->c_out, ly->m, ly->kappa, s, ly->weights.data(), r, kk, ll, plain))
                 continue;
             B.nonempty[(size_t)gi * B.nb + bi] = 1;
@@ -586,20 +609,70 @@ fhe_conv_layer::Bsgs& ensure_bsgs(fhe_ctx* c, const fhe_conv_layer* cly, int ori
     return B;
 }
 
+// Baby steps of the fused BSGS schedule for nsrc sources: Y_g(s) for every
+// giant g (chunks of kFusedMaxG giants per launch), X~_b never materialised.
+void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const uint64_t* digits, size_t dstride,
+                  const uint64_t* cts, size_t ctstride, int nsrc, uint64_t* Y, size_t ystride) {
+    const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t extw = (size_t)ne * c->N;
+    FusedBsgs f{};
+    f.nsrc = nsrc;
+    f.digits = digits;
+    f.digit_src_stride = dstride;
+    f.ct = cts;
+    f.ct_src_stride = ctstride;
+    f.pt_g_stride = (size_t)B.nb * extw;
+    f.y_src_stride = ystride;
+    f.y_g_stride = 2 * extw;
+    for (int b = 0; b < B.nb; ++b) {
+        bool any = false;
+        for (int g = 0; g < B.ngi; ++g) any |= B.nonempty[(size_t)g * B.nb + b] != 0;
+        if (any && c->reduce_amount(B.bamt[b]) != 0) c->ledger.key_switches += nsrc;
+    }
+    if (B.nb > kMaxFused) fail(FHE_E_INVALID, "too many baby steps for the fused BSGS schedule");
+    for (int g0 = 0; g0 < B.ngi; g0 += kFusedMaxG) {
+        const int ng = std::min(kFusedMaxG, B.ngi - g0);
+        f.ng = ng;
+        f.nb = 0;
+        double pt_words = 0, keyed = 0;
+        for (int b = 0; b < B.nb; ++b) {
+            uint32_t mask = 0;
+            for (int g = 0; g < ng; ++g)
+                if (B.nonempty[(size_t)(g0 + g) * B.nb + b]) mask |= 1u << g;
+            if (!mask) continue;
+            const uint32_t gal = c->galois_of(c->reduce_amount(B.bamt[b]));
+            f.galois[f.nb] = gal;
+            f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+            f.gmask[f.nb] = mask;
+            f.pt[f.nb] = B.d_pts + ((size_t)g0 * B.nb + b) * extw;
+            pt_words += __builtin_popcount(mask);
+            if (gal != 1) keyed += 1;
+            f.nb++;
+        }
+        f.Y = Y + (size_t)g0 * 2 * extw;
+        c->timed("bsgs_fused",
+                 c->rows(keyed * 2.0 * dn * ne + pt_words * ne +
+                         nsrc * ((double)dn * ne + 2.0 * nr + 2.0 * ng * ne)),
+                 [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+    }
+}
+
 void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orient, fhe_ct* out) {
     fhe_conv_layer::Bsgs& B = ensure_bsgs(c, ly, orient);
     const int level = ct->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
     const size_t N = c->N, extw = (size_t)ne * N;
     uint64_t* dsrc = c->alloc((size_t)dn * extw);
     uint64_t* Y = c->alloc((size_t)B.ngi * 2 * extw);
-    uint64_t* XT = c->alloc((size_t)B.nb * 2 * extw);
+    const bool fused = orient == 5;
+    uint64_t* XT = fused ? nullptr : c->alloc((size_t)B.nb * 2 * extw);
     modup(c, ct->c1(), level, dsrc);
+    if (fused) fused_babies(c, B, level, dsrc, 0, ct->d, 0, 1, Y, 0);
     // baby steps: the hoisted key switches of the source, then the plaintext mat-vec
     BabyTerms t{};
     t.nb = B.nb;
     t.nb_total = B.nb;
     t.pts = B.d_pts;
-    for (int b = 0; b < B.nb; ++b) {
+    for (int b = 0; !fused && b < B.nb; ++b) {
         const uint32_t g = c->galois_of(c->reduce_amount(B.bamt[b]));
         t.galois[b] = g;
         t.key[b] = g == 1 ? nullptr : c->key_for(g);
@@ -608,7 +681,7 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
         t.gmask[b] = any;
         if (g != 1 && any) c->ledger.key_switches++;
     }
-    {
+    if (!fused) {
         KsStream ks{};
         ks.digits = dsrc;
         ks.digit_stride = 0;
@@ -627,7 +700,7 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
         }
         c->timed("ks_multi", c->rows((double)ks.n * (2.0 * dn * ne + 2.0 * ne) + (double)dn * ne + nr), [&] { ks_stream(c->dc, ks, 0, c->d_md, level, dn, c->st); });
     }
-    for (int g0 = 0; g0 < B.ngi; g0 += kMaxGiant) {
+    for (int g0 = 0; !fused && g0 < B.ngi; g0 += kMaxGiant) {
         t.ngi = std::min(kMaxGiant, B.ngi - g0);
         t.g0 = g0;
         double pt_pairs = 0;
@@ -731,7 +804,7 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
     c->release(md);
     c->release(acc);
     c->release(Y);
-    c->release(XT);
+    if (XT) c->release(XT);
     c->release(dsrc);
 }
 
@@ -754,7 +827,10 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
     modup_batch(c, buf + (size_t)nr * N, ctw, S, level, dsrc);
     // baby steps
     const size_t xts = (size_t)B.nb * 2 * extw, ys = (size_t)B.ngi * 2 * extw;
-    uint64_t* XT = c->alloc((size_t)S * xts);
+    const bool fused = orient == 5;
+    uint64_t* Y = c->alloc((size_t)S * ys);
+    uint64_t* XT = fused ? nullptr : c->alloc((size_t)S * xts);
+    if (fused) fused_babies(c, B, level, dsrc, dw, buf, ctw, S, Y, ys);
     BabyTerms t{};
     t.nb = B.nb;
     t.nb_total = B.nb;
@@ -767,7 +843,7 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
     kb.c0_src_stride = ctw;
     kb.out = XT;
     kb.out_src_stride = xts;
-    for (int b = 0; b < B.nb; ++b) {
+    for (int b = 0; !fused && b < B.nb; ++b) {
         const uint32_t g = c->galois_of(c->reduce_amount(B.bamt[b]));
         t.galois[b] = g;
         t.key[b] = g == 1 ? nullptr : c->key_for(g);
@@ -787,10 +863,10 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
         kb.n++;
         c->ledger.key_switches += S;
     }
-    c->timed("ks_multi", c->rows((double)kb.n * (2.0 * dn * ne + 2.0 * ne * S) + ((double)dn * ne + nr) * S),
-             [&] { ks_batch(c->dc, kb, 0, c->d_md, level, dn, c->st); });
-    uint64_t* Y = c->alloc((size_t)S * ys);
-    for (int g0 = 0; g0 < B.ngi; g0 += kMaxGiant) {
+    if (!fused)
+        c->timed("ks_multi", c->rows((double)kb.n * (2.0 * dn * ne + 2.0 * ne * S) + ((double)dn * ne + nr) * S),
+                 [&] { ks_batch(c->dc, kb, 0, c->d_md, level, dn, c->st); });
+    for (int g0 = 0; !fused && g0 < B.ngi; g0 += kMaxGiant) {
         t.ngi = std::min(kMaxGiant, B.ngi - g0);
         t.g0 = g0;
         double pt_pairs = 0;
@@ -805,7 +881,7 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
             pt_matvec_batch(c->dc, Y + (size_t)g0 * 2 * extw, ys, XT, xts, t, level, S, c->st);
         });
     }
-    c->release(XT);
+    if (XT) c->release(XT);
     c->release(dsrc);
     // giant steps, in source chunks (bounds the digit buffers)
     std::vector<int> giants;
@@ -904,12 +980,16 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
 }
 
 int auto_orient(const fhe_conv_layer* ly) {
-    // giant steps each cost a ModUp: take the smaller set as giant steps
+    // giant steps each cost a ModDown + ModUp (~120 NTT rows at cfg3) while a
+    // fused baby step costs one key stream: the fused schedule (kappa giant
+    // steps) whenever its c kappa baby steps fit one launch, else the smaller
+    // of the two classic sets as giant steps
+    if (ly->c_in * ly->kappa <= kMaxFused) return 5;
     return ly->kappa * ly->kappa <= ly->c_in ? 3 : 4;
 }
 
 void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct* out) {
-    if (approach < 0 || approach > 4) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3 or 4");
+    if (approach < 0 || approach > 5) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3, 4 or 5");
     if (approach == 0) approach = auto_orient(ly);
     if (approach >= 3) {
         if (ct->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
@@ -1012,9 +1092,9 @@ void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
 void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* ly, int approach,
                 fhe_ct* const* outs) {
     if (n == 0) return;
-    if (approach < 0 || approach > 4) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3 or 4");
+    if (approach < 0 || approach > 5) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3, 4 or 5");
     if (approach == 0) approach = auto_orient(ly);
-    if (approach >= 3 && n > 1 && c->fused_batch) {
+    if (approach >= 3 && n > 1 && (c->fused_batch || (approach == 5 && c->batch5))) {
         if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
         for (size_t s0 = 0; s0 < n; s0 += 32) {
             const int S = (int)std::min<size_t>(32, n - s0);
@@ -1090,6 +1170,7 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
             c->lanes.push_back(l);
         }
         if (const char* e = std::getenv("FHECONV_BATCH_FUSED")) c->fused_batch = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FHECONV_BATCH5")) c->batch5 = std::atoi(e) != 0;
         cudaMemPool_t pool;
         ck(cudaDeviceGetDefaultMemPool(&pool, c->device), "mempool");
         uint64_t thresh = ~0ULL;
@@ -1631,14 +1712,25 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
 }
 
 int fhe_conv_layer_steps(const fhe_conv_layer* ly, int approach, int64_t* steps, size_t cap, size_t* n) {
-    (void)approach;  // both approaches use the same key set: r m^2 and kk m + ll
-    if (!ly) return FHE_E_INVALID;
+    // approaches 1-4 rotate by r m^2 and kk m + ll; approach 5 by r m^2 + ll and
+    // kk m; approach 0 (auto) lists the union so that every schedule can run
+    if (!ly || approach < 0 || approach > 5) return FHE_E_INVALID;
     std::set<int64_t> st;
     const long h = ly->kappa / 2;
-    for (int r = 1; r < ly->c_in; ++r) st.insert((int64_t)r * ly->m * ly->m);
-    for (long kk = -h; kk <= h; ++kk)
-        for (long ll = -h; ll <= h; ++ll)
-            if (kk || ll) st.insert(kk * ly->m + ll);
+    const int64_t block = (int64_t)ly->m * ly->m;
+    if (approach != 5) {
+        for (int r = 1; r < ly->c_in; ++r) st.insert((int64_t)r * block);
+        for (long kk = -h; kk <= h; ++kk)
+            for (long ll = -h; ll <= h; ++ll)
+                if (kk || ll) st.insert(kk * ly->m + ll);
+    }
+    if (approach == 0 || approach == 5) {
+        for (int r = 0; r < ly->c_in; ++r)
+            for (long ll = -h; ll <= h; ++ll)
+                if (r || ll) st.insert((int64_t)r * block + ll);
+        for (long kk = -h; kk <= h; ++kk)
+            if (kk) st.insert(kk * ly->m);
+    }
     size_t i = 0;
     for (int64_t v : st) {
         if (i < cap && steps) steps[i] = v;

@@ -920,6 +920,172 @@ __global__ void __launch_bounds__(kMatvecThreads) k_pt_matvec2(DevCtx c, uint64_
     }
 }
 
+// Fused BSGS baby steps. A CTA owns P = 128/SG consecutive coefficient pairs
+// of one extended row and SG sources (thread = (pair, source), pair fastest).
+// Per baby step the CTA stages, with cp.async, the 2*DN key words and NG
+// plaintext words of its pairs ONCE (shared by the SG sources) plus every
+// source's DN gathered digit words and gathered c0 word; the stage of baby
+// b+1 is in flight while baby b is multiplied out. The key-switched X~_b lives
+// only in registers; the NG giant accumulators are 128-bit lazy sums.
+template <int DN, int NG, int SG>
+struct FusedLayout {
+    static constexpr int P = 128 / SG;
+    static constexpr int KW = 2 * DN * P;   // key words      [2*DN][P]
+    static constexpr int PW = NG * P;       // plaintexts     [NG][P]
+    static constexpr int DW = SG * DN * P;  // digits         [SG][DN][P]
+    static constexpr int CW = SG * P;       // gathered c0    [SG][P]
+    static constexpr int STAGE = KW + PW + DW + CW;
+};
+
+template <int DN, int NG, int SG>
+__global__ void __launch_bounds__(128, 4) k_bsgs_fused(DevCtx c, FusedBsgs a, const ModDownTable* md, int level) {
+    using LY = FusedLayout<DN, NG, SG>;
+    constexpr int P = LY::P;
+    extern __shared__ ulonglong2 sb[];  // [2 stages][STAGE]
+    const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
+    const int tid = threadIdx.x, p = tid % P, sl = tid / P;
+    const size_t total = (size_t)ne * c.N;
+    const size_t chunks = total / 2 / P;
+    const int ngroups = (a.nsrc + SG - 1) / SG;
+    const size_t items = chunks * (size_t)ngroups;
+    const size_t keyrow = (size_t)np * c.N;  // stride between key rows j and j+1
+    RowMap rm{ne, level, c.L, 0};
+    // per-thread smem slots (stage 0); stage 1 is + STAGE
+    ulonglong2* const s_key = sb + p;                                   // + j * P
+    ulonglong2* const s_pt = sb + LY::KW + p;                           // + g * P
+    ulonglong2* const s_dig = sb + LY::KW + LY::PW + sl * DN * P + p;   // + j * P
+    ulonglong2* const s_c0 = sb + LY::KW + LY::PW + LY::DW + sl * P + p;
+    for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const size_t chunk = it / (size_t)ngroups;
+        const int s = (int)(it % (size_t)ngroups) * SG + sl;
+        const bool active = s < a.nsrc;
+        const size_t i = (chunk * P + p) * 2;
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
+        const int pi = row_prime(rm, u);
+        const Prime pr = c.primes[pi];
+        const bool qrow = u < nr;
+        const uint64_t pm = qrow ? md->pmod[u] : 0, pms = qrow ? md->pmod_sh[u] : 0;
+        const uint64_t* Du = a.digits + (size_t)(active ? s : 0) * a.digit_src_stride + (size_t)u * c.N;
+        const uint64_t* C = a.ct + (size_t)(active ? s : 0) * a.ct_src_stride;
+        const uint64_t* C0u = C + (size_t)u * c.N;
+        const uint64_t* C1u = C + ((size_t)nr + u) * c.N;
+        const size_t kofs = (size_t)pi * c.N + k, pofs = (size_t)u * c.N + k;
+        // bit-reversed exponent of this pair, reused for every baby's permutation
+        const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
+        auto pidx = [&](uint32_t g) { return brev_n((((e * g) & nmask) - 1) >> 1, c.logN); };
+        auto issue = [&](int b, int stg, uint32_t pk) {
+            const size_t so = (size_t)stg * LY::STAGE;
+            const uint64_t* key = a.key[b];
+            const uint32_t gm = a.gmask[b];
+#pragma unroll
+            for (int g = sl; g < NG; g += SG)
+                if ((gm >> g) & 1u) cp_async16(s_pt + so + g * P, a.pt[b] + (size_t)g * a.pt_g_stride + pofs);
+            if (key) {
+                const uint64_t* kp = key + kofs;
+#pragma unroll
+                for (int j = sl; j < 2 * DN; j += SG) cp_async16(s_key + so + j * P, kp + (size_t)j * keyrow);
+                if (active) {
+                    const uint64_t* dp = Du + (pk & ~1u);
+#pragma unroll
+                    for (int j = 0; j < DN; ++j) cp_async16(s_dig + so + j * P, dp + (size_t)j * total);
+                    if (qrow) cp_async16(s_c0 + so, C0u + (pk & ~1u));
+                }
+            } else if (active && qrow) {  // identity: c0, c1 unpermuted
+                cp_async16(s_dig + so, C1u + k);
+                cp_async16(s_c0 + so, C0u + k);
+            }
+            cp_async_commit();
+        };
+        U128 y[NG][2][2];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) y[g][0][0] = y[g][0][1] = y[g][1][0] = y[g][1][1] = U128{0, 0};
+        uint32_t pk_next = pidx(a.galois[0]);
+        issue(0, 0, pk_next);
+        for (int b = 0; b < a.nb; ++b) {
+            const uint32_t pk = pk_next;
+            cp_async_wait<0>();
+            __syncthreads();  // stage b visible to all; everyone is past baby b-1
+            if (b + 1 < a.nb) {
+                pk_next = pidx(a.galois[b + 1]);
+                issue(b + 1, (b + 1) & 1, pk_next);
+            }
+            const size_t so = (size_t)(b & 1) * LY::STAGE;
+            uint64_t x0a = 0, x0b = 0, x1a = 0, x1b = 0;
+            if (a.key[b]) {
+                // the gathered pair is (perm(k), perm(k)^1) in some order: read the two
+                // words with 8-byte loads at the swapped offsets instead of selecting
+                const int swp = (int)(pk & 1u);
+                const uint64_t* dw = reinterpret_cast<const uint64_t*>(s_dig + so);
+                Acc3 s0a{0, 0, 0, 0}, s0b{0, 0, 0, 0}, s1a{0, 0, 0, 0}, s1b{0, 0, 0, 0};
+#pragma unroll
+                for (int j = 0; j < DN; ++j) {
+                    const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
+                    const uint64_t da = dw[2 * j * P + swp], db = dw[2 * j * P + (swp ^ 1)];
+                    mac3(s0a, da, k0.x);
+                    mac3(s0b, db, k0.y);
+                    mac3(s1a, da, k1.x);
+                    mac3(s1b, db, k1.y);
+                }
+                if (qrow) {
+                    const uint64_t* cw = reinterpret_cast<const uint64_t*>(s_c0 + so);
+                    if (DN < 8) {  // P c0 as one more product term (s1 holds 8 terms)
+                        mac3(s0a, cw[swp], pm);
+                        mac3(s0b, cw[swp ^ 1], pm);
+                    } else {
+                        add3(s0a, mul_shoup(cw[swp], pm, pms, pr.q));
+                        add3(s0b, mul_shoup(cw[swp ^ 1], pm, pms, pr.q));
+                    }
+                }
+                // X~ 2^-64 in [0, 2q): the factor 2^64 is restored once per output
+                const U128 t0a = fold3(s0a), t0b = fold3(s0b), t1a = fold3(s1a), t1b = fold3(s1b);
+                x0a = redc_lazy(t0a.hi, t0a.lo, pr);
+                x0b = redc_lazy(t0b.hi, t0b.lo, pr);
+                x1a = redc_lazy(t1a.hi, t1a.lo, pr);
+                x1b = redc_lazy(t1b.hi, t1b.lo, pr);
+            } else if (qrow) {
+                const ulonglong2 c1 = s_dig[so], c0 = s_c0[so];
+                x0a = redc_lazy(0, mul_shoup(c0.x, pm, pms, pr.q), pr);
+                x0b = redc_lazy(0, mul_shoup(c0.y, pm, pms, pr.q), pr);
+                x1a = redc_lazy(0, mul_shoup(c1.x, pm, pms, pr.q), pr);
+                x1b = redc_lazy(0, mul_shoup(c1.y, pm, pms, pr.q), pr);
+            }
+            const uint32_t gm = a.gmask[b];
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                if (!((gm >> g) & 1u)) continue;
+                const ulonglong2 w = s_pt[so + g * P];
+                mac_small(y[g][0][0], w.x, x0a);
+                mac_small(y[g][0][1], w.y, x0b);
+                mac_small(y[g][1][0], w.x, x1a);
+                mac_small(y[g][1][1], w.y, x1b);
+            }
+            if ((b & 31) == 31) {  // keep the lazy sums far from 2^128 for any prime size
+#pragma unroll
+                for (int g = 0; g < NG; ++g)
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2)
+                            y[g][q2][e2] = U128{reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), 0};
+            }
+        }
+        if (active) {
+            uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
+            const uint64_t r64 = reduce64((uint64_t)0 - pr.q, pr);  // 2^64 mod q
+            auto out = [&](const U128& v) { return mul_mod(reduce128(v.hi, v.lo, pr), r64, pr); };
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                if (g >= a.ng) break;
+                uint64_t* yg = Ys + (size_t)g * a.y_g_stride;
+                st2(yg + i, out(y[g][0][0]), out(y[g][0][1]));
+                st2(yg + total + i, out(y[g][1][0]), out(y[g][1][1]));
+            }
+        }
+        __syncthreads();  // the next item's first stage reuses stage 0
+    }
+}
+
 template <int DN>
 __global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc, const uint64_t* D,
                                                          const uint64_t* key, const uint64_t* c0, uint32_t g,
@@ -1024,13 +1190,29 @@ void ks_multi(const DevCtx& c, uint64_t* XT, const uint64_t* digits, const uint6
 #undef FHE_KS_MULTI
 }
 
+// CTA caps of the HBM-streaming kernels (per SM). Smaller grids leave SM room
+// for the integer-bound NTT CTAs of other lanes to co-reside.
+static int env_cap(const char* name, int dflt) {
+    const char* v = getenv(name);
+    const int x = v ? atoi(v) : 0;
+    return x > 0 ? x : dflt;
+}
+static int ks_cap() {
+    static const int cap = env_cap("FHECONV_KS_CTAS", 148 * 8);
+    return cap;
+}
+static int mv_cap() {
+    static const int cap = env_cap("FHECONV_MV_CTAS", 148 * 12);
+    return cap;
+}
+
 void ks_stream(const DevCtx& c, const KsStream& a, int mode, const ModDownTable* md, int level, int dn,
                cudaStream_t st) {
     if (a.n <= 0) return;
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
     const size_t smem = (size_t)2 * 3 * dn * kStreamThreads * sizeof(ulonglong2);
     int blocks = (int)((total / 2 + kStreamThreads - 1) / kStreamThreads);
-    blocks = blocks < 148 * 8 ? blocks : 148 * 8;
+    blocks = blocks < ks_cap() ? blocks : ks_cap();
     ++g_launches;
 #define FHE_KSS(D)                                                                                             \
     do {                                                                                                       \
@@ -1090,10 +1272,53 @@ void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
     const size_t smem = (size_t)t.nb * 2 * kMatvecThreads * sizeof(ulonglong2);
     int blocks = (int)((total / 2 + kMatvecThreads - 1) / kMatvecThreads);
-    blocks = blocks < 148 * 12 ? blocks : 148 * 12;
+    blocks = blocks < mv_cap() ? blocks : mv_cap();
     ++g_launches;
     cudaFuncSetAttribute(k_pt_matvec2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_pt_matvec2<<<blocks, kMatvecThreads, smem, st>>>(c, Y, XT, t, level);
+}
+
+static int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <int DN, int NG, int SG>
+static void launch_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, cudaStream_t st) {
+    using LY = FusedLayout<DN, NG, SG>;
+    const int ne = level + 1 + c.K;
+    const size_t smem = (size_t)2 * LY::STAGE * sizeof(ulonglong2);
+    const size_t items = (size_t)ne * c.N / 2 / LY::P * (size_t)((a.nsrc + SG - 1) / SG);
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_bsgs_fused<DN, NG, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_fused<DN, NG, SG>, 128, smem);
+    if (per_sm < 1) per_sm = 1;
+    const size_t cap = (size_t)sm_count() * per_sm;
+    const int blocks = (int)(items < cap ? items : cap);
+    k_bsgs_fused<DN, NG, SG><<<blocks, 128, smem, st>>>(c, a, md, level);
+}
+
+void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, int dn, cudaStream_t st) {
+    if (a.nb <= 0 || a.nsrc <= 0 || a.ng <= 0) return;
+    ++g_launches;
+    const bool multi = a.nsrc > 1;
+#define FHE_FUSED(D)                                                          \
+    do {                                                                      \
+        if (a.ng <= 3) {                                                      \
+            if (multi) launch_fused<D, 3, 4>(c, a, md, level, st);            \
+            else launch_fused<D, 3, 1>(c, a, md, level, st);                  \
+        } else {                                                              \
+            if (multi) launch_fused<D, kFusedMaxG, 4>(c, a, md, level, st);   \
+            else launch_fused<D, kFusedMaxG, 1>(c, a, md, level, st);         \
+        }                                                                     \
+    } while (0)
+    FHE_DN_SWITCH(dn, FHE_FUSED)
+#undef FHE_FUSED
 }
 
 void ks_accumulate(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* key, const uint64_t* c0,

@@ -257,6 +257,29 @@ void pt_matvec_batch(const DevCtx& c, uint64_t* Y, size_t y_src_stride, const ui
                      const BabyTerms& t, int level, int nsrc, cudaStream_t st);
 void identity_batch(const DevCtx& c, uint64_t* xt, size_t xt_src_stride, const uint64_t* ct, size_t ct_src_stride,
                     const ModDownTable* md, int level, int nsrc, cudaStream_t st);
+// Fused BSGS baby steps (k_bsgs_fused): for every source s and
+// giant g of the launch,
+//   Y_g(s) = sum_b pt'[g][b] * X~_b(s),
+//   X~_b(s) = (IP_0(D(s), key_b, g_b) + [u<=l] P sigma_b(c0(s)), IP_1(...))   (QP basis)
+// with X~_b never written to memory; the identity baby (key null) is P ct(s).
+// Keys and plaintexts are staged once per CTA and shared by its sources.
+constexpr int kMaxFused = 96;
+constexpr int kFusedMaxG = 5;
+struct FusedBsgs {
+    int nb, ng, nsrc;
+    uint32_t galois[kMaxFused];
+    const uint64_t* key[kMaxFused];  // [dnum][2][L+K][N], null: identity baby
+    uint32_t gmask[kMaxFused];       // bit g: pt'[g][b] is non-empty
+    const uint64_t* pt[kMaxFused];   // pt'[g][b] = pt[b] + g * pt_g_stride, [ne][N]
+    size_t pt_g_stride;
+    const uint64_t* digits;          // source s: digits + s * digit_src_stride, [dn][ne][N]
+    size_t digit_src_stride;
+    const uint64_t* ct;              // source s: ct + s * ct_src_stride, [2][level+1][N]
+    size_t ct_src_stride;
+    uint64_t* Y;                     // Y_g(s) = Y + s * y_src_stride + g * y_g_stride, [2][ne][N]
+    size_t y_src_stride, y_g_stride;
+};
+void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, int dn, cudaStream_t st);
 // acc += y over [2][ne][N] (QP basis)
 void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st);
 

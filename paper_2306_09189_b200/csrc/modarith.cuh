@@ -22,7 +22,7 @@ struct Prime {
     uint64_t q;
     uint64_t bar_hi;  // floor(2^128 / q) high word
     uint64_t bar_lo;  // floor(2^128 / q) low word
-    uint64_t pad;
+    uint64_t qinv;    // -q^-1 mod 2^64 (Montgomery)
 };
 
 FHE_HD uint64_t mulhi64(uint64_t a, uint64_t b) {
@@ -69,6 +69,12 @@ FHE_HD uint64_t reduce128(uint64_t hi, uint64_t lo, const Prime& p) {
     return r;
 }
 
+// Montgomery reduction of T = (hi, lo) < q 2^64: T 2^-64 mod q, in [0, 2q).
+FHE_HD uint64_t redc_lazy(uint64_t hi, uint64_t lo, const Prime& p) {
+    const uint64_t m = lo * p.qinv;
+    return hi + mulhi64(m, p.q) + (lo != 0);
+}
+
 FHE_HD uint64_t mul_mod(uint64_t a, uint64_t b, const Prime& p) {
     return reduce128(mulhi64(a, b), a * b, p);
 }
@@ -89,6 +95,59 @@ FHE_HD void mac(U128& acc, uint64_t a, uint64_t b) {
 FHE_HD void add128(U128& acc, uint64_t v) {
     acc.lo += v;
     acc.hi += (acc.lo < v);
+}
+
+// Carry-deferred sum of products of operands < 2^60 (every prime is < 2^60):
+// with a = a1 2^32 + a0, b = b1 2^32 + b0 (a1, b1 < 2^28)
+//   sum a b = s0 + c 2^64 + s1 2^32 + s2 2^64,
+// s0 += a0 b0 (carries counted in c), s1 += a0 b1 + a1 b0 (< 2^61 per term),
+// s2 += a1 b1 (< 2^56 per term): four 32x32->64 multiply-adds and one 64-bit
+// add-with-carry per term instead of a full 128-bit product. s1 cannot
+// overflow for up to 8 terms (8 * 2^61 = 2^64), s2 for up to 2^8.
+struct Acc3 {
+    uint64_t s0, s1, s2;
+    uint32_t c;
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ void mac3(Acc3& A, uint64_t a, uint64_t b) {
+    const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+    asm("{\n\t.reg .u64 t;\n\t"
+        "mul.wide.u32 t, %4, %6;\n\t"
+        "add.cc.u64 %0, %0, t;\n\t"
+        "addc.u32 %3, %3, 0;\n\t"
+        "mad.wide.u32 %1, %4, %7, %1;\n\t"
+        "mad.wide.u32 %1, %5, %6, %1;\n\t"
+        "mad.wide.u32 %2, %5, %7, %2;\n\t}"
+        : "+l"(A.s0), "+l"(A.s1), "+l"(A.s2), "+r"(A.c)
+        : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+}
+// acc += a b for a, b < 2^62 (the middle sum a0 b1 + a1 b0 < 2^63 cannot carry):
+// four 32x32->64 products and two 128-bit additions
+__device__ __forceinline__ void mac_small(U128& acc, uint64_t a, uint64_t b) {
+    const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+    asm("{\n\t.reg .u64 p00, p11, mid, ml, mh;\n\t"
+        "mul.wide.u32 p00, %2, %4;\n\t"
+        "mul.wide.u32 mid, %2, %5;\n\t"
+        "mad.wide.u32 mid, %3, %4, mid;\n\t"
+        "mul.wide.u32 p11, %3, %5;\n\t"
+        "shl.b64 ml, mid, 32;\n\t"
+        "shr.u64 mh, mid, 32;\n\t"
+        "add.cc.u64 p00, p00, ml;\n\t"
+        "addc.u64 p11, p11, mh;\n\t"
+        "add.cc.u64 %0, %0, p00;\n\t"
+        "addc.u64 %1, %1, p11;\n\t}"
+        : "+l"(acc.lo), "+l"(acc.hi)
+        : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void add3(Acc3& A, uint64_t v) {
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+l"(A.s0), "+r"(A.c) : "l"(v));
+}
+#endif
+// (hi, lo) of the accumulated 128-bit value
+FHE_HD U128 fold3(const Acc3& A) {
+    const uint64_t lo = A.s0 + (A.s1 << 32);
+    const uint64_t hi = (uint64_t)A.c + (A.s1 >> 32) + A.s2 + (lo < A.s0);
+    return U128{lo, hi};
 }
 
 // ------------------------------------------------------------------ PRNG

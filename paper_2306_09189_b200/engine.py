@@ -103,7 +103,8 @@ class ConvLayer:
         self.ctx, self.h = ctx, h
         self.c_in, self.c_out, self.m, self.kappa, self.level = c_in, c_out, m, kappa, level
 
-    def steps(self, approach: int = 2) -> list[int]:
+    def steps(self, approach: int = 0) -> list[int]:
+        """Galois steps for `approach` (0: the union, so every schedule can run)."""
         buf = (C.c_int64 * 1024)()
         n = C.c_size_t(0)
         self.ctx._check(lib().fhe_conv_layer_steps(self.h, approach, buf, 1024, C.byref(n)))

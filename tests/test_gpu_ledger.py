@@ -46,6 +46,13 @@ def test_ckks_work_counts(ctx, oracle):
     lg, _, _ = run(ctx, oracle, 1)
     assert lg["modups"] == 1 + 9
     assert lg["key_switches"] == 8 + 9 * 3
+    # fused BSGS (approach 5): c kappa - 1 = 11 hoisted baby key switches from one
+    # ModUp, kappa - 1 = 2 giant steps (ModDown + ModUp + key switch each)
+    lg, _, _ = run(ctx, oracle, 5)
+    assert lg["modups"] == 1 + 2
+    assert lg["key_switches"] == 11 + 2
+    assert lg["hoist_groups"] == 1 and lg["hoisted_rotations"] == 12 and lg["rotations"] == 2
+    assert lg["rescales"] == 1
 
 
 def test_error_messages(ctx):
@@ -77,8 +84,10 @@ def test_zero_filter_and_identity(ctx, oracle):
     for f in range(4):
         ident[f, f, 1, 1] = 1.0
     layer = ctx.conv_layer(4, 4, 32, 3, ident.ravel())
-    for ap in (1, 2):
+    for ap in (1, 2, 3, 4, 5):
         assert np.abs(ctx.decrypt(ctx.conv2d(ct, layer, ap)) - img).max() < 1e-6
+    for ap in (3, 4, 5):
+        assert np.abs(ctx.decrypt(ctx.conv2d(ct, zero, ap))).max() < 1e-6
 
 
 def test_cxx_engine_demo_runs():

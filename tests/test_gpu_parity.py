@@ -121,7 +121,7 @@ def conv_case(oracle, golden, name):
     return c, m, k, co, img, filt
 
 
-@pytest.mark.parametrize("approach", [1, 2, 3, 4])
+@pytest.mark.parametrize("approach", [1, 2, 3, 4, 5])
 def test_conv_cfg1_bit_exact_and_within_tolerance(oracle, golden, p1, approach):
     c, m, k, co, img, filt = conv_case(oracle, golden, "cfg1")
     layer = p1.ctx.conv_layer(c, co, m, k, filt)
@@ -136,7 +136,7 @@ def test_conv_cfg1_bit_exact_and_within_tolerance(oracle, golden, p1, approach):
     assert err < TOL, err
 
 
-@pytest.mark.parametrize("approach", [1, 2, 3, 4])
+@pytest.mark.parametrize("approach", [1, 2, 3, 4, 5])
 def test_conv_cfg3_bit_exact_and_within_tolerance(oracle, golden, approach):
     p = pair(oracle, "cfg3")
     c, m, k, co, img, filt = conv_case(oracle, golden, "cfg3")
@@ -153,7 +153,7 @@ def test_conv_cfg3_bit_exact_and_within_tolerance(oracle, golden, approach):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("approach", [2, 4])
+@pytest.mark.parametrize("approach", [2, 4, 5])
 def test_conv_cfg4_bit_exact_and_within_tolerance(oracle, golden, approach):
     p = pair(oracle, "cfg4")
     c, m, k, co, img, filt = conv_case(oracle, golden, "cfg4")
@@ -175,8 +175,23 @@ def test_conv_auto_schedule_picks_fewer_decompositions(oracle, golden):
     p.ctx.gen_galois_keys(layer.steps())
     ct = p.ctx.encrypt(p.ctx.encode(img), ENC_SEED)
     a = p.ctx.conv2d(ct, layer, 0)
-    b = p.ctx.conv2d(ct, layer, 4)  # c = 4 < kappa^2 = 9: shifts hoisted, 3 giant steps
+    b = p.ctx.conv2d(ct, layer, 5)  # c kappa = 12 fused baby steps, kappa = 3 giant steps
     assert np.array_equal(a.residues(), b.residues())
+
+
+def test_conv_fused_schedule_runs_on_its_own_key_set(oracle, golden):
+    """approach 5 needs exactly the rotations r m^2 + ll and kk m."""
+    from paper_2306_09189_b200 import Context
+    c, m, k, co, img, filt = conv_case(oracle, golden, "cfg1")
+    ctx = Context.from_config("cfg1")
+    ctx.keygen(7)
+    layer = ctx.conv_layer(c, co, m, k, filt)
+    steps = layer.steps(5)
+    want = sorted(({r * m * m + ll for r in range(c) for ll in (-1, 0, 1)} | {-m, m}) - {0})
+    assert sorted(steps) == want
+    ctx.gen_galois_keys(steps)
+    out = ctx.conv2d(ctx.encrypt(ctx.encode(img), ENC_SEED), layer, 5)
+    assert np.abs(ctx.decrypt(out) - golden["cfg1/slots"]).max() < TOL
 
 
 def test_conv_cfg5_three_layer_stack(oracle, golden):
@@ -249,7 +264,7 @@ def test_cfg2_hoisted_stencil(oracle):
         assert np.abs(p.ctx.decrypt(outs[i]) - np.roll(z, -k)).max() < TOL
 
 
-@pytest.mark.parametrize("name,approach", [("cfg1", 4), ("cfg3", 3), ("cfg3", 0)])
+@pytest.mark.parametrize("name,approach", [("cfg1", 4), ("cfg3", 3), ("cfg3", 0), ("cfg1", 5), ("cfg3", 5)])
 def test_batched_conv_equals_single(oracle, golden, name, approach):
     """fhe_conv2d_batch (keys/plaintexts streamed once per batch) = per-ciphertext conv, bit for bit."""
     p = pair(oracle, name)

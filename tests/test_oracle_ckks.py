@@ -148,7 +148,7 @@ def test_mul_plain_rescale(cfg1):
     assert np.abs(cfg1.decrypt(s, 4, cfg1.scale) - 2 * z).max() < 1e-8
 
 
-@pytest.mark.parametrize("plan", [1, 2])
+@pytest.mark.parametrize("plan", [1, 2, 3, 4, 5])
 def test_conv_cfg1_decrypts_to_reference(cfg1, oracle, golden, plan):
     """decrypt(conv) vs the reference conv_plan slots, <= 1e-6 (north star)."""
     c, m, k = 4, 32, 3
