@@ -927,9 +927,10 @@ __global__ void __launch_bounds__(kMatvecThreads) k_pt_matvec2(DevCtx c, uint64_
 // source's DN gathered digit words and gathered c0 word; the stage of baby
 // b+1 is in flight while baby b is multiplied out. The key-switched X~_b lives
 // only in registers; the NG giant accumulators are 128-bit lazy sums.
-template <int DN, int NG, int SG>
+template <int DN, int NG, int SG, int NST_>
 struct FusedLayout {
     static constexpr int P = 128 / SG;
+    static constexpr int NST = NST_;        // pipeline stages
     static constexpr int KW = 2 * DN * P;   // key words      [2*DN][P]
     static constexpr int PW = NG * P;       // plaintexts     [NG][P]
     static constexpr int DW = SG * DN * P;  // digits         [SG][DN][P]
@@ -937,11 +938,11 @@ struct FusedLayout {
     static constexpr int STAGE = KW + PW + DW + CW;
 };
 
-template <int DN, int NG, int SG>
-__global__ void __launch_bounds__(128, 4) k_bsgs_fused(DevCtx c, FusedBsgs a, const ModDownTable* md, int level) {
-    using LY = FusedLayout<DN, NG, SG>;
+template <int DN, int NG, int SG, int NST, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a, const ModDownTable* md, int level) {
+    using LY = FusedLayout<DN, NG, SG, NST>;
     constexpr int P = LY::P;
-    extern __shared__ ulonglong2 sb[];  // [2 stages][STAGE]
+    extern __shared__ ulonglong2 sb[];  // [NST stages][STAGE]
     const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
     const int tid = threadIdx.x, p = tid % P, sl = tid / P;
     const size_t total = (size_t)ne * c.N;
@@ -974,8 +975,13 @@ __global__ void __launch_bounds__(128, 4) k_bsgs_fused(DevCtx c, FusedBsgs a, co
         // bit-reversed exponent of this pair, reused for every baby's permutation
         const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
         auto pidx = [&](uint32_t g) { return brev_n((((e * g) & nmask) - 1) >> 1, c.logN); };
-        auto issue = [&](int b, int stg, uint32_t pk) {
-            const size_t so = (size_t)stg * LY::STAGE;
+        auto issue = [&](int b) {
+            if (b >= a.nb) {
+                cp_async_commit();  // empty group keeps the wait count uniform
+                return;
+            }
+            const uint32_t pk = pidx(a.galois[b]);
+            const size_t so = (size_t)(b % NST) * LY::STAGE;
             const uint64_t* key = a.key[b];
             const uint32_t gm = a.gmask[b];
 #pragma unroll
@@ -1000,17 +1006,14 @@ __global__ void __launch_bounds__(128, 4) k_bsgs_fused(DevCtx c, FusedBsgs a, co
         U128 y[NG][2][2];
 #pragma unroll
         for (int g = 0; g < NG; ++g) y[g][0][0] = y[g][0][1] = y[g][1][0] = y[g][1][1] = U128{0, 0};
-        uint32_t pk_next = pidx(a.galois[0]);
-        issue(0, 0, pk_next);
+#pragma unroll
+        for (int b = 0; b < NST - 1; ++b) issue(b);
         for (int b = 0; b < a.nb; ++b) {
-            const uint32_t pk = pk_next;
-            cp_async_wait<0>();
+            cp_async_wait<NST - 2>();
             __syncthreads();  // stage b visible to all; everyone is past baby b-1
-            if (b + 1 < a.nb) {
-                pk_next = pidx(a.galois[b + 1]);
-                issue(b + 1, (b + 1) & 1, pk_next);
-            }
-            const size_t so = (size_t)(b & 1) * LY::STAGE;
+            issue(b + NST - 1);
+            const uint32_t pk = pidx(a.galois[b]);
+            const size_t so = (size_t)(b % NST) * LY::STAGE;
             uint64_t x0a = 0, x0b = 0, x1a = 0, x1b = 0;
             if (a.key[b]) {
                 // the gathered pair is (perm(k), perm(k)^1) in some order: read the two
@@ -1070,6 +1073,7 @@ __global__ void __launch_bounds__(128, 4) k_bsgs_fused(DevCtx c, FusedBsgs a, co
                             y[g][q2][e2] = U128{reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), 0};
             }
         }
+        cp_async_wait<0>();
         if (active) {
             uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
             const uint64_t r64 = reduce64((uint64_t)0 - pr.q, pr);  // 2^64 mod q
@@ -1288,19 +1292,25 @@ static int sm_count() {
     return n;
 }
 
-template <int DN, int NG, int SG>
+#ifndef FHE_FUSED_NST
+#define FHE_FUSED_NST 2
+#endif
+#ifndef FHE_FUSED_MINB
+#define FHE_FUSED_MINB 3
+#endif
+template <int DN, int NG, int SG, int NST = 2, int MINB = 4>
 static void launch_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, cudaStream_t st) {
-    using LY = FusedLayout<DN, NG, SG>;
+    using LY = FusedLayout<DN, NG, SG, NST>;
     const int ne = level + 1 + c.K;
-    const size_t smem = (size_t)2 * LY::STAGE * sizeof(ulonglong2);
+    const size_t smem = (size_t)NST * LY::STAGE * sizeof(ulonglong2);
     const size_t items = (size_t)ne * c.N / 2 / LY::P * (size_t)((a.nsrc + SG - 1) / SG);
     int per_sm = 0;
-    cudaFuncSetAttribute(k_bsgs_fused<DN, NG, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_fused<DN, NG, SG>, 128, smem);
+    cudaFuncSetAttribute(k_bsgs_fused<DN, NG, SG, NST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_fused<DN, NG, SG, NST, MINB>, 128, smem);
     if (per_sm < 1) per_sm = 1;
     const size_t cap = (size_t)sm_count() * per_sm;
     const int blocks = (int)(items < cap ? items : cap);
-    k_bsgs_fused<DN, NG, SG><<<blocks, 128, smem, st>>>(c, a, md, level);
+    k_bsgs_fused<DN, NG, SG, NST, MINB><<<blocks, 128, smem, st>>>(c, a, md, level);
 }
 
 void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, int dn, cudaStream_t st) {
@@ -1310,7 +1320,7 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
 #define FHE_FUSED(D)                                                          \
     do {                                                                      \
         if (a.ng <= 3) {                                                      \
-            if (multi) launch_fused<D, 3, 4>(c, a, md, level, st);            \
+            if (multi) launch_fused<D, 3, 4, FHE_FUSED_NST, FHE_FUSED_MINB>(c, a, md, level, st); \
             else launch_fused<D, 3, 1>(c, a, md, level, st);                  \
         } else {                                                              \
             if (multi) launch_fused<D, kFusedMaxG, 4>(c, a, md, level, st);   \
