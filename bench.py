@@ -138,14 +138,16 @@ def ncu_traffic(kernel_class):
 
 
 # ------------------------------------------------------------------ our arm
-KERNEL_CLASSES = ["ntt", "ntt_modup", "ntt_moddown", "ks_multi", "pt_matvec", "ks_inner", "conv_mac", "moddown",
-                  "rescale"]
+KERNEL_CLASSES = ["ntt", "ntt_modup", "ntt_moddown", "ks_multi", "pt_matvec", "bsgs_fused", "ks_inner", "conv_mac",
+                  "moddown", "rescale"]
 KERNEL_NOTES = {
     "ntt": "plain forward/inverse NTT passes (IMAD-bound 64-bit Shoup butterflies)",
     "ntt_modup": "ModUp: FastBConv of the digit + forward NTT of the extended rows",
     "ntt_moddown": "ModDown: FastBConv P->Q + forward NTT + fused (acc - conv) P^-1",
     "ks_multi": "hoisted key-switch inner products of the baby steps (cp.async key stream)",
     "pt_matvec": "rotated-plaintext multiply-accumulate into the giant accumulators",
+    "bsgs_fused": "fused baby steps (approach 5): hoisted key switches r m^2 + ll multiplied by the rotated "
+                  "plaintexts in registers, keys/plaintexts staged once per CTA (cp.async)",
     "ks_inner": "giant-step key switches accumulated into the QP accumulator",
     "conv_mac": "paper-schedule fused inner product + plaintext MAC (approaches 1/2)",
 }
@@ -239,7 +241,7 @@ def run_ours(args, rank, world, local_rank):
         return max_over_ranks(ctx.timer_stop())
 
     per_approach = {}
-    for ap in (1, 2, 3, 4):
+    for ap in (1, 2, 3, 4, 5):
         k2 = max(3, args.steps // 8) if ap in (1, 2) else max(5, args.steps // 4)
         per_approach[ap] = world * k2 / (timed_convs(ap, k2, 2) / 1e3)
     # hoisted rotations at N = 2^15: the 8 non-identity shifts of a 3x3 stencil from one ModUp
@@ -309,7 +311,7 @@ def run_ours(args, rank, world, local_rank):
     dms, dn_, dbytes = prof[dom]
     avg_s = dms / 1e3 / dn_
     achieved = dbytes / dn_ / avg_s / 1e9
-    ks_cls = [c for c in ("ks_multi", "ks_inner") if c in kernels]
+    ks_cls = [c for c in ("ks_multi", "ks_inner", "bsgs_fused") if c in kernels]
     ks_bytes = sum(prof[c][2] for c in ks_cls)
     ks_ms = sum(prof[c][0] for c in ks_cls)
     cpu = cpu_baseline(args) if not args.no_cpu else None
@@ -327,12 +329,14 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "u64 (RNS residues mod 40-60-bit primes)",
         "data": "synthetic (seeded U[-1,1] images/weights, BASELINE cfg3 shapes); no dataset involved",
         "config": {"workload": WORKLOAD, "approach": approach,
-                   "schedule": {0: "auto (BSGS: hoisted channel rotations + aggregated shifts)", 1: "paper Approach 1",
-                                2: "paper Approach 2", 3: "BSGS, hoisted channel rotations",
-                                4: "BSGS, hoisted shifts"}[approach],
+                   "schedule": {0: "auto (fused BSGS: 48 hoisted rotations r m^2 + ll, 3 giant row shifts)",
+                                1: "paper Approach 1", 2: "paper Approach 2", 3: "BSGS, hoisted channel rotations",
+                                4: "BSGS, hoisted shifts", 5: "fused BSGS"}[approach],
                    "batch_per_gpu": B, "step": f"{B} independent ciphertexts through the layer "
-                   "(fhe_conv2d_batch_into; 4 CUDA-stream lanes)", "parallelism": f"replicas x{world}",
-                   "l2": "no flush: per-step key stream (23 Galois keys, 1.27 GB) >> 126 MB L2", "key_seed": 7,
+                   "(fhe_conv2d_batch_into: one fused baby-step launch for the batch)",
+                   "parallelism": f"replicas x{world}",
+                   "l2": "no flush: per-step key stream (49 Galois keys, 2.7 GB) + rotated plaintexts (0.57 GB) "
+                         ">> 126 MB L2", "key_seed": 7,
                    "enc_seed": 9000, "decrypt_max_abs_err": err,
                    "latency_ms_single_conv": round(ms1 / kp, 4)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -389,15 +393,19 @@ def other_configs(world, device):
         ref = sum(np.einsum("fg,fij->gij", wt[:, :, a, b], xp[:, a:a + m, b:b + m]) for a in range(k) for b in range(k))
         err = float(np.abs(ctx.decrypt(outs[0])[: c * m * m] - ref.ravel()).max())
         reps = 5
-        ctx.synchronize()
-        ctx.timer_start()
-        for _ in range(reps):
-            ctx.conv2d_batch_into(cts, layer, 0, outs)
-        ms = ctx.timer_stop()
-        ctx.timer_start()
-        for _ in range(reps):
-            ctx.conv2d_into(cts[0], layer, 0, outs[0])
-        ms1 = ctx.timer_stop()
+        ctx.conv2d_batch_into(cts, layer, 0, outs)
+        ctx.conv2d_into(cts[0], layer, 0, outs[0])
+        ms, ms1 = float("inf"), float("inf")
+        for _ in range(3):  # best of three device-timed runs (first-call pool growth excluded)
+            ctx.synchronize()
+            ctx.timer_start()
+            for _ in range(reps):
+                ctx.conv2d_batch_into(cts, layer, 0, outs)
+            ms = min(ms, ctx.timer_stop())
+            ctx.timer_start()
+            for _ in range(reps):
+                ctx.conv2d_into(cts[0], layer, 0, outs[0])
+            ms1 = min(ms1, ctx.timer_stop())
         res[name] = {"conv_per_s": round(world * reps * batch / (ms / 1e3), 1), "batch": batch,
                      "latency_ms": round(ms1 / reps, 4), "decrypt_max_abs_err": err}
         ctx.close()
@@ -422,10 +430,13 @@ def other_configs(world, device):
             src = bufs[li]
 
     stack()
-    ctx.synchronize()
-    ctx.timer_start()
     stack()
-    ms = ctx.timer_stop()
+    ms = float("inf")
+    for _ in range(3):
+        ctx.synchronize()
+        ctx.timer_start()
+        stack()
+        ms = min(ms, ctx.timer_stop())
     res["cfg5"] = {"three_layer_passes_per_s": round(world * B5 / (ms / 1e3), 2),
                    "conv_per_s": round(world * 3 * B5 / (ms / 1e3), 1), "batch": B5, "levels_consumed": 3}
     ctx.close()
@@ -561,7 +572,7 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--approach", type=int, default=0, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--approach", type=int, default=0, choices=[0, 1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-golden", action="store_true", help="skip the golden-model CKKS CPU timing")
     ap.add_argument("--batch", type=int, default=8, help="ciphertexts per step (independent images)")
