@@ -195,6 +195,14 @@ int fhe_conv2d_batch(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, const fhe
 /* same, into preallocated outputs of level - 1 */
 int fhe_conv2d_batch_into(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* layer,
                           int approach, fhe_ct* const* outs);
+/* host-resident batch: n input ciphertexts at host_in ([n][2][level+1][N]
+ * words, level = the layer's level, scale `scale` or the context scale if
+ * <= 0) are uploaded, convolved and downloaded to host_out ([n][2][level][N])
+ * in chunks of `chunk` (0: 4) with uploads, convs and downloads of
+ * neighbouring chunks overlapped on three streams. Returns when host_out is
+ * complete. Pinned (page-locked) host buffers give asynchronous copies. */
+int fhe_conv2d_batch_host(fhe_ctx* ctx, const uint64_t* host_in, size_t n, double scale,
+                          const fhe_conv_layer* layer, int approach, size_t chunk, uint64_t* host_out);
 
 #ifdef __cplusplus
 }

@@ -85,6 +85,7 @@ SIGNATURES = [
     ("fhe_conv2d_into", C.c_int, [vp, vp, vp, C.c_int, vp]),
     ("fhe_conv2d_batch", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, vp, C.c_int, vpp]),
     ("fhe_conv2d_batch_into", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, vp, C.c_int, C.POINTER(C.c_void_p)]),
+    ("fhe_conv2d_batch_host", C.c_int, [vp, u64p, C.c_size_t, C.c_double, vp, C.c_int, C.c_size_t, u64p]),
 ]
 
 EXPORTED = [s[0] for s in SIGNATURES]

@@ -45,6 +45,8 @@ struct fhe_ctx {
     cudaStream_t st = nullptr;       // stream the internals enqueue on (main or a lane)
     cudaStream_t main_st = nullptr;  // the context's stream
     std::vector<cudaStream_t> lanes; // extra streams: independent ciphertexts of a batch overlap
+    cudaStream_t h2d_st = nullptr;   // host-pipelined batches: uploads
+    cudaStream_t d2h_st = nullptr;   // host-pipelined batches: downloads
     bool fused_batch = false;        // FHECONV_BATCH_FUSED=1: batched kernels instead of lanes
     bool batch5 = true;              // approach 5: sources batched through one fused launch (FHECONV_BATCH5=0: lanes)
     int logN = 0, N = 0, L = 0, K = 0, alpha = 0, dnum = 0, np = 0;
@@ -1162,6 +1164,8 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
         if (prop.major < 10) fail(FHE_E_CUDA, "libfheconv is built for sm_100a (B200)");
         ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "cudaStreamCreate");
         c->main_st = c->st;
+        ck(cudaStreamCreateWithFlags(&c->h2d_st, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&c->d2h_st, cudaStreamNonBlocking), "cudaStreamCreate");
         int nl = 4;
         if (const char* e = std::getenv("FHECONV_LANES")) nl = std::max(1, std::atoi(e));
         for (int i = 0; i < nl; ++i) {
@@ -1220,6 +1224,11 @@ void fhe_ctx_destroy(fhe_ctx* c) {
         cudaStreamSynchronize(l);
         cudaStreamDestroy(l);
     }
+    for (cudaStream_t x : {c->h2d_st, c->d2h_st})
+        if (x) {
+            cudaStreamSynchronize(x);
+            cudaStreamDestroy(x);
+        }
     if (c->main_st) cudaStreamDestroy(c->main_st);
     delete c;
 }
@@ -1776,6 +1785,72 @@ int fhe_conv2d_batch(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_c
 int fhe_conv2d_batch_into(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* ly, int approach,
                           fhe_ct* const* outs) {
     return guard(c, [&] { batch_impl(c, cts, n, ly, approach, outs); });
+}
+
+// Host-resident batch: chunks of `chunk` ciphertexts flow through three streams
+// (upload | conv | download) with double-buffered device ciphertexts, so the
+// PCIe/C2C copies of chunk j+1 and j-1 overlap the conv of chunk j.
+int fhe_conv2d_batch_host(fhe_ctx* c, const uint64_t* host_in, size_t n, double scale, const fhe_conv_layer* ly,
+                          int approach, size_t chunk, uint64_t* host_out) {
+    return guard(c, [&] {
+        if (!ly || (n && (!host_in || !host_out))) fail(FHE_E_INVALID, "null argument");
+        if (n == 0) return;
+        const int level = ly->level;
+        const size_t N = c->N, inw = (size_t)2 * (level + 1) * N, outw = (size_t)2 * level * N;
+        const size_t S = std::max<size_t>(1, std::min(chunk ? chunk : (size_t)4, n));
+        const double sc = scale > 0 ? scale : c->scale;
+        std::vector<fhe_ct*> din[2], dout[2];
+        for (int b = 0; b < 2; ++b)
+            for (size_t s = 0; s < S; ++s) {
+                din[b].push_back(new_ct(c, level, sc, 0));
+                dout[b].push_back(new_ct(c, level - 1, sc, 1));
+            }
+        cudaEvent_t ready = c->get_event(), ev_h2d[2] = {c->get_event(), c->get_event()},
+                    ev_comp[2] = {c->get_event(), c->get_event()}, ev_d2h[2] = {c->get_event(), c->get_event()};
+        ck(cudaEventRecord(ready, c->main_st), "cudaEventRecord");  // allocations done
+        ck(cudaStreamWaitEvent(c->h2d_st, ready, 0), "cudaStreamWaitEvent");
+        ck(cudaStreamWaitEvent(c->d2h_st, ready, 0), "cudaStreamWaitEvent");
+        auto cleanup = [&] {
+            cudaStreamSynchronize(c->h2d_st);
+            cudaStreamSynchronize(c->main_st);
+            cudaStreamSynchronize(c->d2h_st);
+            for (int b = 0; b < 2; ++b)
+                for (size_t s = 0; s < S; ++s) {
+                    fhe_ct_free(din[b][s]);
+                    fhe_ct_free(dout[b][s]);
+                }
+            for (cudaEvent_t e : {ready, ev_h2d[0], ev_h2d[1], ev_comp[0], ev_comp[1], ev_d2h[0], ev_d2h[1]})
+                c->ev_pool.push_back(e);
+        };
+        try {
+            const size_t nch = (n + S - 1) / S;
+            for (size_t j = 0; j < nch; ++j) {
+                const int b = (int)(j & 1);
+                const size_t s0 = j * S, sn = std::min(S, n - s0);
+                if (j >= 2) ck(cudaStreamWaitEvent(c->h2d_st, ev_comp[b], 0), "cudaStreamWaitEvent");
+                for (size_t s = 0; s < sn; ++s) {
+                    din[b][s]->scale = sc;
+                    ck(cudaMemcpyAsync(din[b][s]->d, host_in + (s0 + s) * inw, inw * 8, cudaMemcpyHostToDevice,
+                                       c->h2d_st), "H2D");
+                }
+                ck(cudaEventRecord(ev_h2d[b], c->h2d_st), "cudaEventRecord");
+                ck(cudaStreamWaitEvent(c->main_st, ev_h2d[b], 0), "cudaStreamWaitEvent");
+                if (j >= 2) ck(cudaStreamWaitEvent(c->main_st, ev_d2h[b], 0), "cudaStreamWaitEvent");
+                batch_impl(c, din[b].data(), sn, ly, approach, dout[b].data());
+                ck(cudaEventRecord(ev_comp[b], c->main_st), "cudaEventRecord");
+                ck(cudaStreamWaitEvent(c->d2h_st, ev_comp[b], 0), "cudaStreamWaitEvent");
+                for (size_t s = 0; s < sn; ++s)
+                    ck(cudaMemcpyAsync(host_out + (s0 + s) * outw, dout[b][s]->d, outw * 8, cudaMemcpyDeviceToHost,
+                                       c->d2h_st), "D2H");
+                ck(cudaEventRecord(ev_d2h[b], c->d2h_st), "cudaEventRecord");
+            }
+            ck(cudaStreamSynchronize(c->d2h_st), "sync");
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
 }
 
 }  // extern "C"

@@ -1316,16 +1316,19 @@ static void launch_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable
 void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, int dn, cudaStream_t st) {
     if (a.nb <= 0 || a.nsrc <= 0 || a.ng <= 0) return;
     ++g_launches;
-    const bool multi = a.nsrc > 1;
-#define FHE_FUSED(D)                                                          \
-    do {                                                                      \
-        if (a.ng <= 3) {                                                      \
-            if (multi) launch_fused<D, 3, 4, FHE_FUSED_NST, FHE_FUSED_MINB>(c, a, md, level, st); \
-            else launch_fused<D, 3, 1>(c, a, md, level, st);                  \
-        } else {                                                              \
-            if (multi) launch_fused<D, kFusedMaxG, 4>(c, a, md, level, st);   \
-            else launch_fused<D, kFusedMaxG, 1>(c, a, md, level, st);         \
-        }                                                                     \
+    // sources per CTA: 4 (keys/plaintexts shared 4 ways), 2 for pairs, 1 alone
+    const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
+#define FHE_FUSED(D)                                                                                \
+    do {                                                                                            \
+        if (a.ng <= 3) {                                                                            \
+            if (sg == 4) launch_fused<D, 3, 4, FHE_FUSED_NST, FHE_FUSED_MINB>(c, a, md, level, st); \
+            else if (sg == 2) launch_fused<D, 3, 2, 2, 3>(c, a, md, level, st);                     \
+            else launch_fused<D, 3, 1, 2, 2>(c, a, md, level, st);                                  \
+        } else {                                                                                    \
+            if (sg == 4) launch_fused<D, kFusedMaxG, 4, 2, 2>(c, a, md, level, st);                 \
+            else if (sg == 2) launch_fused<D, kFusedMaxG, 2, 2, 2>(c, a, md, level, st);            \
+            else launch_fused<D, kFusedMaxG, 1, 2, 2>(c, a, md, level, st);                         \
+        }                                                                                           \
     } while (0)
     FHE_DN_SWITCH(dn, FHE_FUSED)
 #undef FHE_FUSED

@@ -290,6 +290,24 @@ class Context:
         o = (C.c_void_p * len(outs))(*[x.h for x in outs])
         self._check(lib().fhe_conv2d_batch_into(self.h, ins, len(cts), layer.h, approach, o))
 
+    def conv2d_batch_host(self, host_in, n: int, layer: ConvLayer, approach: int = 0, host_out=None,
+                          chunk: int = 0, scale: float = 0.0):
+        """fhe_conv2d_batch_host: n host-resident ciphertexts (uint64 array [n, 2, level+1, N] or a raw
+        pointer to one, e.g. a pinned torch tensor's data_ptr()) -> host_out ([n, 2, level, N]); uploads,
+        convs and downloads of neighbouring chunks overlap."""
+        lv = layer.level
+        if host_out is None:
+            host_out = np.empty((n, 2, lv, self.N), dtype=np.uint64)
+
+        def ptr(x):
+            if isinstance(x, int):
+                return C.cast(x, _lib.u64p)
+            assert x.dtype == np.uint64 and x.flags["C_CONTIGUOUS"]
+            return x.ctypes.data_as(_lib.u64p)
+        self._check(lib().fhe_conv2d_batch_host(self.h, ptr(host_in), n, scale, layer.h, approach, chunk,
+                                                ptr(host_out)))
+        return host_out
+
     # -------------------------------------------------------------- ledger
     def ledger(self) -> dict:
         lg = _lib.FheLedger()

@@ -277,3 +277,18 @@ def test_batched_conv_equals_single(oracle, golden, name, approach):
         assert np.array_equal(outs[i].residues(), p.ctx.conv2d(ct, layer, approach).residues())
     err = np.abs(p.ctx.decrypt(outs[0]) - golden[f"{name}/slots"]).max()
     assert err < TOL, err
+
+
+@pytest.mark.parametrize("approach,chunk", [(5, 2), (3, 0)])
+def test_host_pipelined_batch_equals_device_batch(oracle, golden, approach, chunk):
+    """fhe_conv2d_batch_host (upload | conv | download overlapped) = per-ciphertext conv, bit for bit."""
+    p = pair(oracle, "cfg1")
+    c, m, k, co, img, filt = conv_case(oracle, golden, "cfg1")
+    layer = p.ctx.conv_layer(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    cts = [p.ctx.encrypt(p.ctx.encode(np.roll(img, 11 * i)), ENC_SEED + i) for i in range(5)]
+    host_in = np.stack([x.residues() for x in cts]).astype(np.uint64)
+    out = p.ctx.conv2d_batch_host(host_in, len(cts), layer, approach, chunk=chunk)
+    for i, ct in enumerate(cts):
+        assert np.array_equal(out[i], p.ctx.conv2d(ct, layer, approach).residues())
+    assert np.abs(p.ctx.decrypt(p.ctx.upload(out[0], p.top - 1)) - golden["cfg1/slots"]).max() < TOL
