@@ -1024,7 +1024,8 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
 #pragma unroll
                 for (int j = 0; j < DN; ++j) {
                     const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
-                    const uint64_t da = dw[2 * j * P + swp], db = dw[2 * j * P + (swp ^ 1)];
+                    const ulonglong2 dv = s_dig[so + j * P];  // one conflict-free 16-byte load
+                    const uint64_t da = swp ? dv.y : dv.x, db = swp ? dv.x : dv.y;
                     mac3(s0a, da, k0.x);
                     mac3(s0b, db, k0.y);
                     mac3(s1a, da, k1.x);
