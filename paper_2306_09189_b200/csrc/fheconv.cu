@@ -1822,11 +1822,31 @@ int fhe_conv2d_batch_host(fhe_ctx* c, const uint64_t* host_in, size_t n, double 
             for (cudaEvent_t e : {ready, ev_h2d[0], ev_h2d[1], ev_comp[0], ev_comp[1], ev_d2h[0], ev_d2h[1]})
                 c->ev_pool.push_back(e);
         };
+        // chunk sizes: half-size first and last chunks shorten the exposed
+        // upload of the first chunk and download of the last one
+        std::vector<size_t> sizes;
+        {
+            const size_t h = std::max<size_t>(1, S / 2);
+            size_t rem = n;
+            if (n > S) {
+                sizes.push_back(h);
+                rem -= h;
+                while (rem > S + h) {
+                    sizes.push_back(S);
+                    rem -= S;
+                }
+                if (rem > h) {
+                    sizes.push_back(rem - h);
+                    rem = h;
+                }
+            }
+            sizes.push_back(rem);
+        }
         try {
-            const size_t nch = (n + S - 1) / S;
-            for (size_t j = 0; j < nch; ++j) {
+            size_t s0 = 0;
+            for (size_t j = 0; j < sizes.size(); s0 += sizes[j], ++j) {
                 const int b = (int)(j & 1);
-                const size_t s0 = j * S, sn = std::min(S, n - s0);
+                const size_t sn = sizes[j];
                 if (j >= 2) ck(cudaStreamWaitEvent(c->h2d_st, ev_comp[b], 0), "cudaStreamWaitEvent");
                 for (size_t s = 0; s < sn; ++s) {
                     din[b][s]->scale = sc;
