@@ -760,22 +760,24 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
                 ntt_modup_coef(c->dc, dg, yq, G, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
             });
             c->ledger.modups += G;
-            KsStream ks{};
+            KsBatch ks{};
             ks.n = G;
+            ks.nsrc = 1;
             ks.digits = dg;
-            ks.digit_stride = dw;
-            ks.out = acc;
+            ks.digit_term_stride = dw;
+            ks.c0 = Y;
             ks.c0_qp = 1;
+            ks.out = acc;
             for (int s = 0; s < G; ++s) {
                 const int gi = giants[g0 + s];
                 const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[gi]));
                 ks.galois[s] = g;
                 ks.key[s] = c->key_for(g);
-                ks.c0[s] = Y + (size_t)gi * 2 * extw;
+                ks.c0_off[s] = (size_t)gi * 2 * extw;
                 c->ledger.key_switches++;
             }
             c->timed("ks_inner", c->rows((double)ks.n * (3.0 * dn * ne + ne) + 4.0 * ne),
-                     [&] { ks_stream(c->dc, ks, 1, c->d_md, level, dn, c->st); });
+                     [&] { ks_batch(c->dc, ks, 1, c->d_md, level, dn, c->st); });
         }
         c->release(dg);
         c->release(yq);

@@ -1091,6 +1091,100 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
     }
 }
 
+// Giant-step key switches of a batch, accumulated into each source's QP
+// accumulator: acc(s) += sum_t (IP_0(D(s,t), key_t) + sigma_t(Y(s,t).c0), IP_1(...)),
+// Y.c0 P-scaled in QP (added unscaled on every row). Same staging as
+// k_bsgs_fused: thread = (coefficient pair, source), the key rows of a term
+// are staged once per CTA for its SG sources, digits/c0 are per source.
+template <int DN, int SG>
+__global__ void __launch_bounds__(128, 3) k_ks_giant(DevCtx c, KsBatch a, int level) {
+    constexpr int P = 128 / SG;
+    constexpr int KW = 2 * DN * P, DW = SG * DN * P, CW = SG * P, STAGE = KW + DW + CW;
+    extern __shared__ ulonglong2 sb[];  // [2][STAGE]
+    const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
+    const int tid = threadIdx.x, p = tid % P, sl = tid / P;
+    const size_t total = (size_t)ne * c.N;
+    const size_t chunks = total / 2 / P;
+    const int ngroups = (a.nsrc + SG - 1) / SG;
+    const size_t items = chunks * (size_t)ngroups;
+    const size_t keyrow = (size_t)np * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    ulonglong2* const s_key = sb + p;
+    ulonglong2* const s_dig = sb + KW + sl * DN * P + p;
+    ulonglong2* const s_c0 = sb + KW + DW + sl * P + p;
+    for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const size_t chunk = it / (size_t)ngroups;
+        const int s = (int)(it % (size_t)ngroups) * SG + sl;
+        const bool active = s < a.nsrc;
+        const size_t i = (chunk * P + p) * 2;
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
+        const int pi = row_prime(rm, u);
+        const size_t kofs = (size_t)pi * c.N + k;
+        const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
+        auto pidx = [&](uint32_t g) { return brev_n((((e * g) & nmask) - 1) >> 1, c.logN); };
+        auto issue = [&](int t) {
+            const size_t so = (size_t)(t & 1) * STAGE;
+            const uint64_t* kp = a.key[t] + kofs;
+#pragma unroll
+            for (int j = sl; j < 2 * DN; j += SG) cp_async16(s_key + so + j * P, kp + (size_t)j * keyrow);
+            if (active) {
+                const uint32_t pk = pidx(a.galois[t]) & ~1u;
+                const uint64_t* D = a.digits + (size_t)s * a.digit_src_stride + (size_t)t * a.digit_term_stride +
+                                    (size_t)u * c.N + pk;
+#pragma unroll
+                for (int j = 0; j < DN; ++j) cp_async16(s_dig + so + j * P, D + (size_t)j * total);
+                cp_async16(s_c0 + so, a.c0 + (size_t)s * a.c0_src_stride + a.c0_off[t] + (size_t)u * c.N + pk);
+            }
+            cp_async_commit();
+        };
+        U128 r0a{0, 0}, r0b{0, 0}, r1a{0, 0}, r1b{0, 0};
+        issue(0);
+        for (int t = 0; t < a.n; ++t) {
+            cp_async_wait<0>();
+            __syncthreads();
+            if (t + 1 < a.n) issue(t + 1);
+            const size_t so = (size_t)(t & 1) * STAGE;
+            const int swp = (int)(pidx(a.galois[t]) & 1u);
+            Acc3 s0a{0, 0, 0, 0}, s0b{0, 0, 0, 0}, s1a{0, 0, 0, 0}, s1b{0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < DN; ++j) {
+                const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
+                const ulonglong2 dv = s_dig[so + j * P];
+                const uint64_t da = swp ? dv.y : dv.x, db = swp ? dv.x : dv.y;
+                mac3(s0a, da, k0.x);
+                mac3(s0b, db, k0.y);
+                mac3(s1a, da, k1.x);
+                mac3(s1b, db, k1.y);
+            }
+            const ulonglong2 cv = s_c0[so];
+            add3(s0a, swp ? cv.y : cv.x);
+            add3(s0b, swp ? cv.x : cv.y);
+            auto acc = [](U128& r, const Acc3& x) {
+                const U128 f = fold3(x);
+                r.lo += f.lo;
+                r.hi += f.hi + (r.lo < f.lo);
+            };
+            acc(r0a, s0a);
+            acc(r0b, s0b);
+            acc(r1a, s1a);
+            acc(r1b, s1b);
+        }
+        if (active) {
+            const Prime pr = c.primes[pi];
+            uint64_t* out = a.out + (size_t)s * a.out_src_stride;
+            const ulonglong2 a0 = ld2(out + i), a1 = ld2(out + total + i);
+            add128(r0a, a0.x);
+            add128(r0b, a0.y);
+            add128(r1a, a1.x);
+            add128(r1b, a1.y);
+            st2(out + i, reduce128(r0a.hi, r0a.lo, pr), reduce128(r0b.hi, r0b.lo, pr));
+            st2(out + total + i, reduce128(r1a.hi, r1a.lo, pr), reduce128(r1b.hi, r1b.lo, pr));
+        }
+        __syncthreads();
+    }
+}
+
 template <int DN>
 __global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc, const uint64_t* D,
                                                          const uint64_t* key, const uint64_t* c0, uint32_t g,
@@ -1233,9 +1327,44 @@ void ks_stream(const DevCtx& c, const KsStream& a, int mode, const ModDownTable*
 #undef FHE_KSS
 }
 
+static int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <int DN, int SG>
+static void launch_giant(const DevCtx& c, const KsBatch& a, int level, cudaStream_t st) {
+    constexpr int P = 128 / SG;
+    const size_t smem = (size_t)2 * (2 * DN * P + SG * DN * P + SG * P) * sizeof(ulonglong2);
+    const size_t items = (size_t)(level + 1 + c.K) * c.N / 2 / P * (size_t)((a.nsrc + SG - 1) / SG);
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_ks_giant<DN, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ks_giant<DN, SG>, 128, smem);
+    const size_t cap = (size_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+    k_ks_giant<DN, SG><<<(int)(items < cap ? items : cap), 128, smem, st>>>(c, a, level);
+}
+
 void ks_batch(const DevCtx& c, const KsBatch& a, int mode, const ModDownTable* md, int level, int dn,
               cudaStream_t st) {
     if (a.n <= 0 || a.nsrc <= 0) return;
+    if (mode == 1 && a.c0_qp) {  // giant steps: staged, key rows shared by the sources of a CTA
+        ++g_launches;
+        const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
+#define FHE_GIANT(D)                                                 \
+    do {                                                             \
+        if (sg == 4) launch_giant<D, 4>(c, a, level, st);            \
+        else if (sg == 2) launch_giant<D, 2>(c, a, level, st);       \
+        else launch_giant<D, 1>(c, a, level, st);                    \
+    } while (0)
+        FHE_DN_SWITCH(dn, FHE_GIANT)
+#undef FHE_GIANT
+        return;
+    }
     const size_t items = (size_t)(level + 1 + c.K) * c.N / 2 * a.nsrc;
     const int blocks = (int)((items + 255) / 256 < 148 * 8 ? (items + 255) / 256 : 148 * 8);
     ++g_launches;
@@ -1283,15 +1412,6 @@ void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms
     k_pt_matvec2<<<blocks, kMatvecThreads, smem, st>>>(c, Y, XT, t, level);
 }
 
-static int sm_count() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
-}
 
 #ifndef FHE_FUSED_NST
 #define FHE_FUSED_NST 2
