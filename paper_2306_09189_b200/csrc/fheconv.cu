@@ -59,6 +59,7 @@ struct fhe_ctx {
     ModUpDigit* d_modup = nullptr;  // [L][dnum]
     ModDownTable* d_md = nullptr;
     uint64_t *d_qlinv = nullptr, *d_qlinv_sh = nullptr;  // [L][L]
+    uint64_t *d_pqlinv = nullptr, *d_pqlinv_sh = nullptr;  // [L][L] (P q_l)^-1 mod q_i (fused ModDown+rescale)
     uint64_t* d_s = nullptr;                              // secret, [np][N] NTT
     bool have_key = false;
     uint64_t key_seed = 0;
@@ -287,6 +288,36 @@ void rotate_from_digits(fhe_ctx* c, const fhe_ct* ct, const uint64_t* digits, ui
     c->ledger.key_switches++;
 }
 
+// out[p] = Rescale(ModDown(acc[p])) for npoly QP accumulators at `level`,
+// out = [npoly][level][N], bit-identical to moddown() followed by
+// rescale_into() but with 3 inverse + `level` forward row transforms per
+// polynomial instead of 28: the rescale's INTT of row q_l is
+// taken from the coefficient-domain ModDown of that row, and
+//   out_i = (acc_i - NTT(conv_i + P spread_i(c_l))) (P q_l)^-1.
+void moddown_rescale(fhe_ctx* c, const uint64_t* acc, size_t acc_stride, int level, int npoly, uint64_t* out) {
+    const size_t N = c->N;
+    const int K = c->K;
+    uint64_t* pc = c->alloc((size_t)npoly * (K + 1) * N);  // [npoly][K] special rows, then [npoly] q_l rows
+    uint64_t* w = c->alloc((size_t)npoly * level * N);
+    uint64_t* qlc = pc + (size_t)npoly * K * N;
+    c->timed("moddown", c->rows(2.0 * npoly * (K + 1)), [&] {
+        gather_special(c->dc, pc, acc, acc_stride, level, npoly, c->st);
+        gather_row(c->dc, qlc, acc + (size_t)level * N, acc_stride, npoly, c->st);
+    });
+    c->timed("ntt", c->rows(2.0 * npoly * (K + 1)), [&] {
+        ntt_inverse(c->dc, pc, npoly * K, RowMap{K, -1, c->L, 0}, c->st);
+        ntt_inverse(c->dc, qlc, npoly, RowMap{1, -1, level, 0}, c->st);
+    });
+    c->timed("ntt_moddown", c->rows((double)npoly * (K + 1 + 3.0 * level)), [&] {
+        ntt_moddown_rescale(c->dc, w, pc, qlc, acc, acc_stride, out, c->d_md, c->d_pqlinv + (size_t)level * c->L,
+                            c->d_pqlinv_sh + (size_t)level * c->L, level, npoly, c->st);
+    });
+    c->release(pc);
+    c->release(w);
+    c->ledger.moddowns += npoly;
+    c->ledger.rescales += npoly / 2;
+}
+
 void rescale_into(fhe_ctx* c, const uint64_t* in, int level, uint64_t* out) {
     const size_t N = c->N;
     uint64_t* tmp = c->alloc(2 * N);
@@ -426,13 +457,15 @@ void upload_tables(fhe_ctx* c) {
         md.pinvq[t] = invmod(P, q);
         md.pinvq_sh[t] = shoup(md.pinvq[t], q);
     }
-    // rescale: q_l^-1 mod q_i
-    std::vector<uint64_t> ql((size_t)L * L, 0), qls((size_t)L * L, 0);
+    // rescale: q_l^-1 mod q_i; fused ModDown+rescale: (P q_l)^-1 mod q_i
+    std::vector<uint64_t> ql((size_t)L * L, 0), qls((size_t)L * L, 0), pql((size_t)L * L, 0), pqls((size_t)L * L, 0);
     for (int l = 1; l < L; ++l)
         for (int i = 0; i < l; ++i) {
             const uint64_t q = c->primes[i];
             ql[(size_t)l * L + i] = invmod(c->primes[l] % q, q);
             qls[(size_t)l * L + i] = shoup(ql[(size_t)l * L + i], q);
+            pql[(size_t)l * L + i] = mulmod(ql[(size_t)l * L + i], md.pinvq[i], q);
+            pqls[(size_t)l * L + i] = shoup(pql[(size_t)l * L + i], q);
         }
     auto up = [&](void** dst, const void* src, size_t bytes) {
         ck(cudaMalloc(dst, bytes), "cudaMalloc");
@@ -449,6 +482,8 @@ void upload_tables(fhe_ctx* c) {
     up((void**)&c->d_md, &md, sizeof(md));
     up((void**)&c->d_qlinv, ql.data(), ql.size() * 8);
     up((void**)&c->d_qlinv_sh, qls.data(), qls.size() * 8);
+    up((void**)&c->d_pqlinv, pql.data(), pql.size() * 8);
+    up((void**)&c->d_pqlinv_sh, pqls.data(), pqls.size() * 8);
     c->dc = DevCtx{c->logN, c->N, L, K, c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv,
                    c->d_ninv_sh};
 }
@@ -784,9 +819,8 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
         c->release(yc);
     }
     if (id >= 0) qp_add(c->dc, acc, Y + (size_t)id * 2 * extw, level, c->st);
-    uint64_t* md = c->alloc((size_t)2 * nr * N);
-    moddown(c, acc, level, 2, md, nullptr, 1);
-    rescale_into(c, md, level, out->d);
+    uint64_t* md = nullptr;
+    moddown_rescale(c, acc, extw, level, 2, out->d);
     out->scale = (ct->scale * (double)c->primes[level]) / (double)c->primes[level];
     out->depth = ct->depth + 1;
     c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, out->depth);
@@ -953,10 +987,11 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
     if (id >= 0)
         for (int s = 0; s < S; ++s)
             qp_add(c->dc, acc + (size_t)s * 2 * extw, Y + (size_t)s * ys + (size_t)id * 2 * extw, level, c->st);
-    uint64_t* md = c->alloc((size_t)S * ctw);
-    moddown(c, acc, level, 2 * S, md, nullptr, 1);
+    const size_t otw = (size_t)2 * level * N;
+    uint64_t* md = c->alloc((size_t)S * otw);
+    moddown_rescale(c, acc, extw, level, 2 * S, md);
     for (int s = 0; s < S; ++s) {
-        rescale_into(c, md + (size_t)s * ctw, level, outs[s]->d);
+        ck(cudaMemcpyAsync(outs[s]->d, md + (size_t)s * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
         outs[s]->scale = (cts[s]->scale * (double)c->primes[level]) / (double)c->primes[level];
         outs[s]->depth = cts[s]->depth + 1;
         c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[s]->depth);
@@ -1079,13 +1114,10 @@ void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
             }
     }
     // one ModDown per component, then one rescale
-    uint64_t* md = c->alloc((size_t)2 * nr * N);
-    moddown(c, acc, level, 2, md, nullptr, 1);
-    rescale_into(c, md, level, out->d);
+    moddown_rescale(c, acc, extw, level, 2, out->d);
     out->scale = (ct->scale * (double)c->primes[level]) / (double)c->primes[level];
     out->depth = ct->depth + 1;
     c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, out->depth);
-    c->release(md);
     c->release(acc);
     c->release(dsrc);
     c->release(dtmp);
@@ -1210,7 +1242,7 @@ void fhe_ctx_destroy(fhe_ctx* c) {
     for (auto& kv : c->keys) cudaFreeAsync(kv.second, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
     void* bufs[] = {c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv, c->d_ninv_sh,
-                    c->d_modup, c->d_md, c->d_qlinv, c->d_qlinv_sh, c->d_s};
+                    c->d_modup, c->d_md, c->d_qlinv, c->d_qlinv_sh, c->d_pqlinv, c->d_pqlinv_sh, c->d_s};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stage) cudaFreeHost(c->h_stage);

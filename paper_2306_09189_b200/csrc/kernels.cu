@@ -311,6 +311,12 @@ __global__ void k_ks_inner(DevCtx c, const uint64_t* D, const uint64_t* key, uin
     }
 }
 
+__global__ void k_gather_row(DevCtx c, uint64_t* dst, const uint64_t* src, size_t stride, int npoly) {
+    const size_t total = (size_t)npoly * c.N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[(i >> c.logN) * stride + (i & (size_t)(c.N - 1))];
+}
+
 __global__ void k_gather_special(DevCtx c, uint64_t* dst, const uint64_t* acc, size_t acc_stride, int level,
                                  int npoly) {
     const size_t total = (size_t)npoly * c.K * c.N;
@@ -428,6 +434,10 @@ void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* k
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
     ++g_launches;
     k_ks_inner<<<ew_blocks(total), kEwThreads, 0, st>>>(c, digits, key, acc0, acc1, galois, level, dn);
+}
+void gather_row(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t stride, int npoly, cudaStream_t st) {
+    ++g_launches;
+    k_gather_row<<<ew_blocks((size_t)npoly * c.N), kEwThreads, 0, st>>>(c, dst, src, stride, npoly);
 }
 void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, size_t acc_stride, int level, int npoly,
                     cudaStream_t st) {

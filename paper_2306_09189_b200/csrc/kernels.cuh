@@ -105,6 +105,9 @@ struct NttFuse {
     uint64_t* out;          // [npoly][level+1][N]
     const uint64_t* add_src;
     uint32_t galois;
+    // fused ModDown+rescale: output multiplier (P q_l)^-1 per row instead of P^-1
+    const uint64_t* outmul;
+    const uint64_t* outmul_sh;
 };
 
 // --------------------------------------------------------------- launchers
@@ -185,6 +188,13 @@ void moddown_finish(const DevCtx& c, uint64_t* out, const uint64_t* acc, const u
                     const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
                     cudaStream_t st);
 // copy the K special rows of each poly's accumulator into [npoly][K][N]
+// dst[p] = src[p * stride] row (N words) for p < npoly
+void gather_row(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t stride, int npoly, cudaStream_t st);
+// fused ModDown + rescale (fheconv.cu moddown_rescale): pcoef = INTT'd special rows
+// [npoly][K][N], qlc = INTT'd q_l rows [npoly][N], w scratch [npoly][level][N]
+void ntt_moddown_rescale(const DevCtx& c, uint64_t* w, const uint64_t* pcoef, const uint64_t* qlc, const uint64_t* acc,
+                         size_t acc_stride, uint64_t* out, const ModDownTable* md, const uint64_t* pqlinv,
+                         const uint64_t* pqlinv_sh, int level, int npoly, cudaStream_t st);
 void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, size_t acc_stride, int level, int npoly,
                     cudaStream_t st);
 

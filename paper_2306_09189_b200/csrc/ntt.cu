@@ -306,7 +306,8 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
             (void)ne;
             const uint64_t* acc = fz.acc + (size_t)pp * fz.acc_stride + (size_t)u * c.N + (size_t)blk0 * B;
             uint64_t* out = fz.out + ((size_t)pp * nr + u) * c.N + (size_t)blk0 * B;
-            const uint64_t pi = fz.md->pinvq[u], pis = fz.md->pinvq_sh[u];
+            const uint64_t pi = fz.outmul ? fz.outmul[u] : fz.md->pinvq[u];
+            const uint64_t pis = fz.outmul ? fz.outmul_sh[u] : fz.md->pinvq_sh[u];
             const bool add = fz.add_src && pp == 0;
             uint64_t av[EPT], sv[EPT];
 #pragma unroll
@@ -472,6 +473,78 @@ __global__ void __launch_bounds__(256) k_bconv_moddown(DevCtx c, uint64_t* conv,
     }
 }
 
+// Fused ModDown + rescale, coefficient domain: for each polynomial and pair
+// position, v_a = x_a [(P/p_a)^-1]_{p_a} (centred count n), conv_t =
+// sum_a v_a [P/p_a]_{q_t} - n [P]_{q_t} (as k_bconv_moddown), then the
+// rescale's input c_l = (x_{q_l} - conv_l) P^-1 mod q_l and
+//   w_i = conv_i + P * centred(c_l) mod q_i      (i < l).
+template <int KA>
+__global__ void __launch_bounds__(256) k_bconv_mdr(DevCtx c, uint64_t* w, const uint64_t* pcoef, const uint64_t* qlc,
+                                                   const ModDownTable* md, int level, int npoly) {
+    const size_t halfN = c.N / 2;
+    const size_t total = (size_t)npoly * halfN;
+    const uint64_t ql = c.primes[level].q;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const int pp = (int)(idx >> (c.logN - 1));
+        const size_t k = (idx & (halfN - 1)) * 2;
+        const uint64_t* pc = pcoef + (size_t)pp * c.K * c.N;
+        uint64_t v0[KA], v1[KA];
+        int n0 = 0, n1 = 0;
+#pragma unroll
+        for (int a = 0; a < KA; ++a) {
+            const uint64_t q = c.primes[c.L + a].q;
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(pc + (size_t)a * c.N + k);
+            v0[a] = mul_shoup(x.x, md->pinv[a], md->pinv_sh[a], q);
+            v1[a] = mul_shoup(x.y, md->pinv[a], md->pinv_sh[a], q);
+            n0 += v0[a] > (q >> 1);
+            n1 += v1[a] > (q >> 1);
+        }
+        auto conv = [&](int t, uint64_t& y0, uint64_t& y1) {
+            const uint64_t qt = c.primes[t].q;
+            y0 = 0;
+            y1 = 0;
+#pragma unroll
+            for (int a = 0; a < KA; ++a) {
+                y0 = add_mod(y0, mul_shoup(v0[a], md->hat[t][a], md->hat_sh[t][a], qt), qt);
+                y1 = add_mod(y1, mul_shoup(v1[a], md->hat[t][a], md->hat_sh[t][a], qt), qt);
+            }
+            for (int n = 0; n < n0; ++n) y0 = sub_mod(y0, md->pmod[t], qt);
+            for (int n = 0; n < n1; ++n) y1 = sub_mod(y1, md->pmod[t], qt);
+        };
+        uint64_t cl0, cl1;
+        {
+            uint64_t y0, y1;
+            conv(level, y0, y1);
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(qlc + (size_t)pp * c.N + k);
+            cl0 = mul_shoup(sub_mod(x.x, y0, ql), md->pinvq[level], md->pinvq_sh[level], ql);
+            cl1 = mul_shoup(sub_mod(x.y, y1, ql), md->pinvq[level], md->pinvq_sh[level], ql);
+        }
+        const bool neg0 = cl0 > (ql >> 1), neg1 = cl1 > (ql >> 1);
+        for (int t = 0; t < level; ++t) {
+            const Prime pr = c.primes[t];
+            // centred lift of c_l into q_t (the rescale's spread)
+            uint64_t s0, s1;
+            if (neg0) {
+                const uint64_t m = reduce64(ql - cl0, pr);
+                s0 = m ? pr.q - m : 0;
+            } else {
+                s0 = reduce64(cl0, pr);
+            }
+            if (neg1) {
+                const uint64_t m = reduce64(ql - cl1, pr);
+                s1 = m ? pr.q - m : 0;
+            } else {
+                s1 = reduce64(cl1, pr);
+            }
+            uint64_t y0, y1;
+            conv(t, y0, y1);
+            y0 = add_mod(y0, mul_shoup(s0, md->pmod[t], md->pmod_sh[t], pr.q), pr.q);
+            y1 = add_mod(y1, mul_shoup(s1, md->pmod[t], md->pmod_sh[t], pr.q), pr.q);
+            *reinterpret_cast<ulonglong2*>(w + ((size_t)pp * level + t) * c.N + k) = make_ulonglong2(y0, y1);
+        }
+    }
+}
+
 template <int LOG_N1, int LOG_B>
 void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, bool inverse, int fuse,
                   const NttFuse& fz, cudaStream_t st) {
@@ -630,6 +703,30 @@ void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const u
         note_launch(1);
     }
     ntt_run(c, conv, npoly * nr, RowMap{nr, level, c.L, 0, 0}, false, FUSE_MODDOWN, fz, st);
+}
+
+void ntt_moddown_rescale(const DevCtx& c, uint64_t* w, const uint64_t* pcoef, const uint64_t* qlc, const uint64_t* acc,
+                         size_t acc_stride, uint64_t* out, const ModDownTable* md, const uint64_t* pqlinv,
+                         const uint64_t* pqlinv_sh, int level, int npoly, cudaStream_t st) {
+    NttFuse fz{};
+    fz.md = md;
+    fz.acc = acc;
+    fz.acc_stride = acc_stride;
+    fz.out = out;
+    fz.outmul = pqlinv;
+    fz.outmul_sh = pqlinv_sh;
+    {
+        const size_t total = (size_t)npoly * (c.N / 2);
+        const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+        switch (c.K) {
+            case 1: k_bconv_mdr<1><<<blocks, 256, 0, st>>>(c, w, pcoef, qlc, md, level, npoly); break;
+            case 2: k_bconv_mdr<2><<<blocks, 256, 0, st>>>(c, w, pcoef, qlc, md, level, npoly); break;
+            case 3: k_bconv_mdr<3><<<blocks, 256, 0, st>>>(c, w, pcoef, qlc, md, level, npoly); break;
+            default: k_bconv_mdr<4><<<blocks, 256, 0, st>>>(c, w, pcoef, qlc, md, level, npoly); break;
+        }
+        note_launch(1);
+    }
+    ntt_run(c, w, npoly * level, RowMap{level, level - 1, c.L, 0, 0}, false, FUSE_MODDOWN, fz, st);
 }
 
 }  // namespace fhe
