@@ -209,8 +209,23 @@ def test_conv_cfg5_three_layer_stack(oracle, golden):
         assert err < TOL, (li, err)
 
 
+def test_conv_cfg5_three_layer_stack_fused(oracle, golden):
+    """cfg5 through the fused schedule at levels 12, 11, 10 (digit counts 7, 6, 6)."""
+    p = pair(oracle, "cfg3")
+    x, _ = oracle.make_inputs(16, 32, 3, 16, 1003, 0, 0)
+    ct = p.ctx.encrypt(p.ctx.encode(x), ENC_SEED + 1)
+    for li, sf in enumerate((2003, 2004, 2005)):
+        _, filt = oracle.make_inputs(16, 32, 3, 16, 0, sf, 1)
+        layer = p.ctx.conv_layer(16, 16, 32, 3, filt, level=ct.level)
+        p.ctx.gen_galois_keys(layer.steps(5))
+        ct = p.ctx.conv2d(ct, layer, 5)
+        err = np.abs(p.ctx.decrypt(ct) - golden[f"cfg5/out{li}"]).max()
+        assert err < TOL, (li, err)
+
+
 @pytest.mark.parametrize("name", ["small_c4to2", "small_c4m4k1"])
-def test_conv_geometry_variants(oracle, golden, name):
+@pytest.mark.parametrize("approach", [2, 3, 4, 5])
+def test_conv_geometry_variants(oracle, golden, name, approach):
     """c_out < c_in and kappa = 1, packed into cfg1's 4096 slots."""
     p = pair(oracle, "cfg1")
     c, m, k, co, img, filt = conv_case(oracle, golden, name)
@@ -220,7 +235,7 @@ def test_conv_geometry_variants(oracle, golden, name):
     layer = p.ctx.conv_layer(c, co, m, k, filt)
     p.ctx.gen_galois_keys(layer.steps())
     ct = p.ctx.encrypt(p.ctx.encode(slots), ENC_SEED)
-    out = p.ctx.decrypt(p.ctx.conv2d(ct, layer, 2))
+    out = p.ctx.decrypt(p.ctx.conv2d(ct, layer, approach))
     want = oracle.emu_conv_slots(c, m, k, co, s, img, filt, 2)
     assert np.abs(out - want).max() < TOL
     assert np.array_equal(want[: 64], golden[f"{name}/slots"])  # oracle == reference at s = 64
@@ -264,14 +279,15 @@ def test_cfg2_hoisted_stencil(oracle):
         assert np.abs(p.ctx.decrypt(outs[i]) - np.roll(z, -k)).max() < TOL
 
 
-@pytest.mark.parametrize("name,approach", [("cfg1", 4), ("cfg3", 3), ("cfg3", 0), ("cfg1", 5), ("cfg3", 5)])
-def test_batched_conv_equals_single(oracle, golden, name, approach):
+@pytest.mark.parametrize("name,approach,n", [("cfg1", 4, 5), ("cfg3", 3, 5), ("cfg3", 0, 5), ("cfg1", 5, 5),
+                                             ("cfg3", 5, 5), ("cfg1", 5, 2), ("cfg1", 5, 3), ("cfg1", 5, 9)])
+def test_batched_conv_equals_single(oracle, golden, name, approach, n):
     """fhe_conv2d_batch (keys/plaintexts streamed once per batch) = per-ciphertext conv, bit for bit."""
     p = pair(oracle, name)
     c, m, k, co, img, filt = conv_case(oracle, golden, name)
     layer = p.ctx.conv_layer(c, co, m, k, filt)
     p.ctx.gen_galois_keys(layer.steps())
-    cts = [p.ctx.encrypt(p.ctx.encode(np.roll(img, 37 * i)), ENC_SEED + i) for i in range(5)]
+    cts = [p.ctx.encrypt(p.ctx.encode(np.roll(img, 37 * i)), ENC_SEED + i) for i in range(n)]
     outs = p.ctx.conv2d_batch(cts, layer, approach)
     for i, ct in enumerate(cts):
         assert np.array_equal(outs[i].residues(), p.ctx.conv2d(ct, layer, approach).residues())
