@@ -1026,10 +1026,9 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
             const size_t so = (size_t)(b % NST) * LY::STAGE;
             uint64_t x0a = 0, x0b = 0, x1a = 0, x1b = 0;
             if (a.key[b]) {
-                // the gathered pair is (perm(k), perm(k)^1) in some order: read the two
-                // words with 8-byte loads at the swapped offsets instead of selecting
+                // the gathered pair is (perm(k), perm(k)^1) in some order: one 16-byte
+                // load (thread-linear slot, conflict-free), then select the order
                 const int swp = (int)(pk & 1u);
-                const uint64_t* dw = reinterpret_cast<const uint64_t*>(s_dig + so);
                 Acc3 s0a{0, 0, 0, 0}, s0b{0, 0, 0, 0}, s1a{0, 0, 0, 0}, s1b{0, 0, 0, 0};
 #pragma unroll
                 for (int j = 0; j < DN; ++j) {
@@ -1042,13 +1041,14 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
                     mac3(s1b, db, k1.y);
                 }
                 if (qrow) {
-                    const uint64_t* cw = reinterpret_cast<const uint64_t*>(s_c0 + so);
+                    const ulonglong2 cv = s_c0[so];
+                    const uint64_t ca = swp ? cv.y : cv.x, cb = swp ? cv.x : cv.y;
                     if (DN < 8) {  // P c0 as one more product term (s1 holds 8 terms)
-                        mac3(s0a, cw[swp], pm);
-                        mac3(s0b, cw[swp ^ 1], pm);
+                        mac3(s0a, ca, pm);
+                        mac3(s0b, cb, pm);
                     } else {
-                        add3(s0a, mul_shoup(cw[swp], pm, pms, pr.q));
-                        add3(s0b, mul_shoup(cw[swp ^ 1], pm, pms, pr.q));
+                        add3(s0a, mul_shoup(ca, pm, pms, pr.q));
+                        add3(s0b, mul_shoup(cb, pm, pms, pr.q));
                     }
                 }
                 // X~ 2^-64 in [0, 2q): the factor 2^64 is restored once per output
