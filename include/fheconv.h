@@ -203,6 +203,14 @@ int fhe_conv2d_batch_into(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, cons
  * complete. Pinned (page-locked) host buffers give asynchronous copies. */
 int fhe_conv2d_batch_host(fhe_ctx* ctx, const uint64_t* host_in, size_t n, double scale,
                           const fhe_conv_layer* layer, int approach, size_t chunk, uint64_t* host_out);
+/* asynchronous form: enqueues the uploads, convs and downloads and returns;
+ * consecutive calls pipeline into one another (the upload of call j+1 runs
+ * under the convs of call j). host_in / host_out must stay valid and
+ * untouched until fhe_host_wait returns. */
+int fhe_conv2d_batch_host_async(fhe_ctx* ctx, const uint64_t* host_in, size_t n, double scale,
+                                const fhe_conv_layer* layer, int approach, size_t chunk, uint64_t* host_out);
+/* waits for every enqueued host-resident batch (and all other work of ctx) */
+int fhe_host_wait(fhe_ctx* ctx);
 
 #ifdef __cplusplus
 }

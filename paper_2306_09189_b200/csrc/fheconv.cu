@@ -1283,6 +1283,8 @@ int fhe_synchronize(fhe_ctx* c) {
     return guard(c, [&] {
         ck(cudaStreamSynchronize(c->main_st), "cudaStreamSynchronize");
         for (cudaStream_t l : c->lanes) ck(cudaStreamSynchronize(l), "cudaStreamSynchronize");
+        ck(cudaStreamSynchronize(c->h2d_st), "cudaStreamSynchronize");
+        ck(cudaStreamSynchronize(c->d2h_st), "cudaStreamSynchronize");
     });
 }
 
@@ -1821,90 +1823,125 @@ int fhe_conv2d_batch_into(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const 
     return guard(c, [&] { batch_impl(c, cts, n, ly, approach, outs); });
 }
 
-// Host-resident batch: chunks of `chunk` ciphertexts flow through three streams
-// (upload | conv | download) with double-buffered device ciphertexts, so the
-// PCIe/C2C copies of chunk j+1 and j-1 overlap the conv of chunk j.
+// Host-resident batches: chunks of `chunk` ciphertexts flow through three
+// streams (upload on h2d_st | conv on the context stream | download on
+// d2h_st) with double-buffered device ciphertexts, so the PCIe/C2C copies of
+// chunk j+1 and j-1 overlap the conv of chunk j. Nothing here synchronises
+// the host: the device buffers are freed stream-ordered after their last use
+// and the events are recycled at the next fhe_host_wait / fhe_synchronize.
+static void batch_host_enqueue(fhe_ctx* c, const uint64_t* host_in, size_t n, double scale, const fhe_conv_layer* ly,
+                               int approach, size_t chunk, uint64_t* host_out, bool short_ends) {
+    if (!ly || (n && (!host_in || !host_out))) fail(FHE_E_INVALID, "null argument");
+    if (n == 0) return;
+    const int level = ly->level;
+    if (level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
+    const size_t N = c->N, inw = (size_t)2 * (level + 1) * N, outw = (size_t)2 * level * N;
+    const size_t S = std::max<size_t>(1, std::min(chunk ? chunk : (size_t)4, n));
+    const double sc = scale > 0 ? scale : c->scale;
+    // inputs live in the upload stream's order, outputs in the conv stream's
+    std::vector<fhe_ct*> din[2], dout[2];
+    auto mk = [&](int lv, int depth, cudaStream_t st) {
+        fhe_ct* ct = new fhe_ct{c, lv, sc, depth, nullptr};
+        ck(cudaMallocAsync(&ct->d, ct->words() * 8, st), "cudaMallocAsync");
+        return ct;
+    };
+    for (int b = 0; b < 2; ++b)
+        for (size_t s = 0; s < S; ++s) {
+            din[b].push_back(mk(level, 0, c->h2d_st));
+            dout[b].push_back(mk(level - 1, 1, c->main_st));
+        }
+    cudaEvent_t ev_h2d[2] = {c->get_event(), c->get_event()}, ev_comp[2] = {c->get_event(), c->get_event()},
+                ev_d2h[2] = {c->get_event(), c->get_event()}, out_ready = c->get_event();
+    ck(cudaEventRecord(out_ready, c->main_st), "cudaEventRecord");  // output buffers allocated
+    ck(cudaStreamWaitEvent(c->d2h_st, out_ready, 0), "cudaStreamWaitEvent");
+    // chunk sizes (short_ends: half-size first and last chunks shorten the
+    // exposed upload of the first chunk and download of the last one)
+    std::vector<size_t> sizes;
+    {
+        const size_t h = short_ends ? std::max<size_t>(1, S / 2) : S;
+        size_t rem = n;
+        if (n > S) {
+            sizes.push_back(h);
+            rem -= h;
+            while (rem > S + h) {
+                sizes.push_back(S);
+                rem -= S;
+            }
+            if (rem > h) {
+                sizes.push_back(rem - h);
+                rem = h;
+            }
+        }
+        sizes.push_back(rem);
+    }
+    size_t s0 = 0;
+    for (size_t j = 0; j < sizes.size(); s0 += sizes[j], ++j) {
+        const int b = (int)(j & 1);
+        const size_t sn = sizes[j];
+        if (j >= 2) ck(cudaStreamWaitEvent(c->h2d_st, ev_comp[b], 0), "cudaStreamWaitEvent");
+        for (size_t s = 0; s < sn; ++s)
+            ck(cudaMemcpyAsync(din[b][s]->d, host_in + (s0 + s) * inw, inw * 8, cudaMemcpyHostToDevice, c->h2d_st),
+               "H2D");
+        ck(cudaEventRecord(ev_h2d[b], c->h2d_st), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->main_st, ev_h2d[b], 0), "cudaStreamWaitEvent");
+        if (j >= 2) ck(cudaStreamWaitEvent(c->main_st, ev_d2h[b], 0), "cudaStreamWaitEvent");
+        batch_impl(c, din[b].data(), sn, ly, approach, dout[b].data());
+        ck(cudaEventRecord(ev_comp[b], c->main_st), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->d2h_st, ev_comp[b], 0), "cudaStreamWaitEvent");
+        for (size_t s = 0; s < sn; ++s)
+            ck(cudaMemcpyAsync(host_out + (s0 + s) * outw, dout[b][s]->d, outw * 8, cudaMemcpyDeviceToHost, c->d2h_st),
+               "D2H");
+        ck(cudaEventRecord(ev_d2h[b], c->d2h_st), "cudaEventRecord");
+    }
+    // stream-ordered frees after the last use: inputs after the last conv,
+    // outputs after the last download
+    for (int b = 0; b < 2; ++b)
+        for (size_t s = 0; s < S; ++s) {
+            ck(cudaFreeAsync(din[b][s]->d, c->main_st), "cudaFreeAsync");
+            ck(cudaFreeAsync(dout[b][s]->d, c->d2h_st), "cudaFreeAsync");
+            delete din[b][s];
+            delete dout[b][s];
+        }
+    for (cudaEvent_t e : {ev_h2d[0], ev_h2d[1], ev_comp[0], ev_comp[1], ev_d2h[0], ev_d2h[1], out_ready})
+        c->pending_events.push_back(e);
+}
+
+static void host_wait(fhe_ctx* c) {
+    ck(cudaStreamSynchronize(c->h2d_st), "sync");
+    ck(cudaStreamSynchronize(c->main_st), "sync");
+    ck(cudaStreamSynchronize(c->d2h_st), "sync");
+    for (cudaStream_t l : c->lanes) ck(cudaStreamSynchronize(l), "sync");
+    for (cudaEvent_t e : c->pending_events) c->ev_pool.push_back(e);
+    c->pending_events.clear();
+}
+
 int fhe_conv2d_batch_host(fhe_ctx* c, const uint64_t* host_in, size_t n, double scale, const fhe_conv_layer* ly,
                           int approach, size_t chunk, uint64_t* host_out) {
     return guard(c, [&] {
-        if (!ly || (n && (!host_in || !host_out))) fail(FHE_E_INVALID, "null argument");
-        if (n == 0) return;
-        const int level = ly->level;
-        const size_t N = c->N, inw = (size_t)2 * (level + 1) * N, outw = (size_t)2 * level * N;
-        const size_t S = std::max<size_t>(1, std::min(chunk ? chunk : (size_t)4, n));
-        const double sc = scale > 0 ? scale : c->scale;
-        std::vector<fhe_ct*> din[2], dout[2];
-        for (int b = 0; b < 2; ++b)
-            for (size_t s = 0; s < S; ++s) {
-                din[b].push_back(new_ct(c, level, sc, 0));
-                dout[b].push_back(new_ct(c, level - 1, sc, 1));
-            }
-        cudaEvent_t ready = c->get_event(), ev_h2d[2] = {c->get_event(), c->get_event()},
-                    ev_comp[2] = {c->get_event(), c->get_event()}, ev_d2h[2] = {c->get_event(), c->get_event()};
-        ck(cudaEventRecord(ready, c->main_st), "cudaEventRecord");  // allocations done
-        ck(cudaStreamWaitEvent(c->h2d_st, ready, 0), "cudaStreamWaitEvent");
-        ck(cudaStreamWaitEvent(c->d2h_st, ready, 0), "cudaStreamWaitEvent");
-        auto cleanup = [&] {
-            cudaStreamSynchronize(c->h2d_st);
-            cudaStreamSynchronize(c->main_st);
-            cudaStreamSynchronize(c->d2h_st);
-            for (int b = 0; b < 2; ++b)
-                for (size_t s = 0; s < S; ++s) {
-                    fhe_ct_free(din[b][s]);
-                    fhe_ct_free(dout[b][s]);
-                }
-            for (cudaEvent_t e : {ready, ev_h2d[0], ev_h2d[1], ev_comp[0], ev_comp[1], ev_d2h[0], ev_d2h[1]})
-                c->ev_pool.push_back(e);
-        };
-        // chunk sizes: half-size first and last chunks shorten the exposed
-        // upload of the first chunk and download of the last one
-        std::vector<size_t> sizes;
-        {
-            const size_t h = std::max<size_t>(1, S / 2);
-            size_t rem = n;
-            if (n > S) {
-                sizes.push_back(h);
-                rem -= h;
-                while (rem > S + h) {
-                    sizes.push_back(S);
-                    rem -= S;
-                }
-                if (rem > h) {
-                    sizes.push_back(rem - h);
-                    rem = h;
-                }
-            }
-            sizes.push_back(rem);
-        }
         try {
-            size_t s0 = 0;
-            for (size_t j = 0; j < sizes.size(); s0 += sizes[j], ++j) {
-                const int b = (int)(j & 1);
-                const size_t sn = sizes[j];
-                if (j >= 2) ck(cudaStreamWaitEvent(c->h2d_st, ev_comp[b], 0), "cudaStreamWaitEvent");
-                for (size_t s = 0; s < sn; ++s) {
-                    din[b][s]->scale = sc;
-                    ck(cudaMemcpyAsync(din[b][s]->d, host_in + (s0 + s) * inw, inw * 8, cudaMemcpyHostToDevice,
-                                       c->h2d_st), "H2D");
-                }
-                ck(cudaEventRecord(ev_h2d[b], c->h2d_st), "cudaEventRecord");
-                ck(cudaStreamWaitEvent(c->main_st, ev_h2d[b], 0), "cudaStreamWaitEvent");
-                if (j >= 2) ck(cudaStreamWaitEvent(c->main_st, ev_d2h[b], 0), "cudaStreamWaitEvent");
-                batch_impl(c, din[b].data(), sn, ly, approach, dout[b].data());
-                ck(cudaEventRecord(ev_comp[b], c->main_st), "cudaEventRecord");
-                ck(cudaStreamWaitEvent(c->d2h_st, ev_comp[b], 0), "cudaStreamWaitEvent");
-                for (size_t s = 0; s < sn; ++s)
-                    ck(cudaMemcpyAsync(host_out + (s0 + s) * outw, dout[b][s]->d, outw * 8, cudaMemcpyDeviceToHost,
-                                       c->d2h_st), "D2H");
-                ck(cudaEventRecord(ev_d2h[b], c->d2h_st), "cudaEventRecord");
-            }
-            ck(cudaStreamSynchronize(c->d2h_st), "sync");
+            batch_host_enqueue(c, host_in, n, scale, ly, approach, chunk, host_out, true);
         } catch (...) {
-            cleanup();
+            host_wait(c);
             throw;
         }
-        cleanup();
+        host_wait(c);
     });
+}
+
+int fhe_conv2d_batch_host_async(fhe_ctx* c, const uint64_t* host_in, size_t n, double scale,
+                                const fhe_conv_layer* ly, int approach, size_t chunk, uint64_t* host_out) {
+    return guard(c, [&] {
+        try {
+            batch_host_enqueue(c, host_in, n, scale, ly, approach, chunk, host_out, false);
+        } catch (...) {
+            host_wait(c);
+            throw;
+        }
+    });
+}
+
+int fhe_host_wait(fhe_ctx* c) {
+    return guard(c, [&] { host_wait(c); });
 }
 
 }  // extern "C"

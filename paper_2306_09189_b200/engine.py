@@ -291,7 +291,7 @@ class Context:
         self._check(lib().fhe_conv2d_batch_into(self.h, ins, len(cts), layer.h, approach, o))
 
     def conv2d_batch_host(self, host_in, n: int, layer: ConvLayer, approach: int = 0, host_out=None,
-                          chunk: int = 0, scale: float = 0.0):
+                          chunk: int = 0, scale: float = 0.0, asynchronous: bool = False):
         """fhe_conv2d_batch_host: n host-resident ciphertexts (uint64 array [n, 2, level+1, N] or a raw
         pointer to one, e.g. a pinned torch tensor's data_ptr()) -> host_out ([n, 2, level, N]); uploads,
         convs and downloads of neighbouring chunks overlap."""
@@ -304,9 +304,13 @@ class Context:
                 return C.cast(x, _lib.u64p)
             assert x.dtype == np.uint64 and x.flags["C_CONTIGUOUS"]
             return x.ctypes.data_as(_lib.u64p)
-        self._check(lib().fhe_conv2d_batch_host(self.h, ptr(host_in), n, scale, layer.h, approach, chunk,
-                                                ptr(host_out)))
+        fn = lib().fhe_conv2d_batch_host_async if asynchronous else lib().fhe_conv2d_batch_host
+        self._check(fn(self.h, ptr(host_in), n, scale, layer.h, approach, chunk, ptr(host_out)))
         return host_out
+
+    def host_wait(self):
+        """fhe_host_wait: completes every conv2d_batch_host(..., asynchronous=True)."""
+        self._check(lib().fhe_host_wait(self.h))
 
     # -------------------------------------------------------------- ledger
     def ledger(self) -> dict:

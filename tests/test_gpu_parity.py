@@ -308,3 +308,21 @@ def test_host_pipelined_batch_equals_device_batch(oracle, golden, approach, chun
     for i, ct in enumerate(cts):
         assert np.array_equal(out[i], p.ctx.conv2d(ct, layer, approach).residues())
     assert np.abs(p.ctx.decrypt(p.ctx.upload(out[0], p.top - 1)) - golden["cfg1/slots"]).max() < TOL
+
+
+def test_host_pipelined_async_calls_chain(oracle, golden):
+    """consecutive fhe_conv2d_batch_host_async calls pipeline into one another and
+    produce the same residues as the synchronous call."""
+    p = pair(oracle, "cfg1")
+    c, m, k, co, img, filt = conv_case(oracle, golden, "cfg1")
+    layer = p.ctx.conv_layer(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    cts = [p.ctx.encrypt(p.ctx.encode(np.roll(img, 5 * i)), ENC_SEED + i) for i in range(6)]
+    host_in = np.stack([x.residues() for x in cts]).astype(np.uint64)
+    want = p.ctx.conv2d_batch_host(host_in, 6, layer, 5, chunk=2)
+    outs = [np.zeros_like(want) for _ in range(3)]
+    for o in outs:
+        p.ctx.conv2d_batch_host(host_in, 6, layer, 5, host_out=o, chunk=2, asynchronous=True)
+    p.ctx.host_wait()
+    for o in outs:
+        assert np.array_equal(o, want)
