@@ -47,6 +47,16 @@ struct fhe_ctx {
     std::vector<cudaStream_t> lanes; // extra streams: independent ciphertexts of a batch overlap
     cudaStream_t h2d_st = nullptr;   // host-pipelined batches: uploads
     cudaStream_t d2h_st = nullptr;   // host-pipelined batches: downloads
+    // host-pipelined batches: two persistent device chunk buffers (inputs in the
+    // upload stream's order, outputs in the conv stream's) and their events;
+    // consecutive calls keep alternating them, so the pipeline runs across calls
+    struct HostPipe {
+        int level = -1;
+        size_t S = 0;
+        std::vector<uint64_t*> din[2], dout[2];
+        cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+        uint64_t chunks = 0;
+    } hp;
     bool fused_batch = false;        // FHECONV_BATCH_FUSED=1: batched kernels instead of lanes
     bool batch5 = true;              // approach 5: sources batched through one fused launch (FHECONV_BATCH5=0: lanes)
     int logN = 0, N = 0, L = 0, K = 0, alpha = 0, dnum = 0, np = 0;
@@ -1236,6 +1246,8 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
     return FHE_OK;
 }
 
+static void host_pipe_free(fhe_ctx* c);
+
 void fhe_ctx_destroy(fhe_ctx* c) {
     if (!c) return;
     if (c->st) cudaStreamSynchronize(c->st);
@@ -1263,6 +1275,10 @@ void fhe_ctx_destroy(fhe_ctx* c) {
             cudaStreamSynchronize(x);
             cudaStreamDestroy(x);
         }
+    host_pipe_free(c);
+    for (int b = 0; b < 2; ++b)
+        for (cudaEvent_t e : {c->hp.ev_h2d[b], c->hp.ev_comp[b], c->hp.ev_d2h[b]})
+            if (e) cudaEventDestroy(e);
     if (c->main_st) cudaStreamDestroy(c->main_st);
     delete c;
 }
@@ -1829,6 +1845,19 @@ int fhe_conv2d_batch_into(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const 
 // chunk j+1 and j-1 overlap the conv of chunk j. Nothing here synchronises
 // the host: the device buffers are freed stream-ordered after their last use
 // and the events are recycled at the next fhe_host_wait / fhe_synchronize.
+static void host_pipe_free(fhe_ctx* c) {
+    auto& h = c->hp;
+    for (int b = 0; b < 2; ++b) {
+        for (uint64_t* p : h.din[b]) cudaFree(p);
+        for (uint64_t* p : h.dout[b]) cudaFree(p);
+        h.din[b].clear();
+        h.dout[b].clear();
+    }
+    h.level = -1;
+    h.S = 0;
+    h.chunks = 0;
+}
+
 static void batch_host_enqueue(fhe_ctx* c, const uint64_t* host_in, size_t n, double scale, const fhe_conv_layer* ly,
                                int approach, size_t chunk, uint64_t* host_out, bool short_ends) {
     if (!ly || (n && (!host_in || !host_out))) fail(FHE_E_INVALID, "null argument");
@@ -1838,72 +1867,74 @@ static void batch_host_enqueue(fhe_ctx* c, const uint64_t* host_in, size_t n, do
     const size_t N = c->N, inw = (size_t)2 * (level + 1) * N, outw = (size_t)2 * level * N;
     const size_t S = std::max<size_t>(1, std::min(chunk ? chunk : (size_t)4, n));
     const double sc = scale > 0 ? scale : c->scale;
-    // inputs live in the upload stream's order, outputs in the conv stream's
-    std::vector<fhe_ct*> din[2], dout[2];
-    auto mk = [&](int lv, int depth, cudaStream_t st) {
-        fhe_ct* ct = new fhe_ct{c, lv, sc, depth, nullptr};
-        ck(cudaMallocAsync(&ct->d, ct->words() * 8, st), "cudaMallocAsync");
-        return ct;
-    };
-    for (int b = 0; b < 2; ++b)
-        for (size_t s = 0; s < S; ++s) {
-            din[b].push_back(mk(level, 0, c->h2d_st));
-            dout[b].push_back(mk(level - 1, 1, c->main_st));
+    auto& h = c->hp;
+    if (h.level != level || h.S < S) {  // (re)build the persistent chunk buffers
+        ck(cudaStreamSynchronize(c->h2d_st), "sync");
+        ck(cudaStreamSynchronize(c->main_st), "sync");
+        ck(cudaStreamSynchronize(c->d2h_st), "sync");
+        host_pipe_free(c);
+        for (int b = 0; b < 2; ++b) {
+            for (size_t s = 0; s < S; ++s) {
+                uint64_t *pi = nullptr, *po = nullptr;
+                ck(cudaMalloc(&pi, inw * 8), "cudaMalloc");
+                ck(cudaMalloc(&po, outw * 8), "cudaMalloc");
+                h.din[b].push_back(pi);
+                h.dout[b].push_back(po);
+            }
+            for (cudaEvent_t* e : {&h.ev_h2d[b], &h.ev_comp[b], &h.ev_d2h[b]})
+                if (!*e) ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
         }
-    cudaEvent_t ev_h2d[2] = {c->get_event(), c->get_event()}, ev_comp[2] = {c->get_event(), c->get_event()},
-                ev_d2h[2] = {c->get_event(), c->get_event()}, out_ready = c->get_event();
-    ck(cudaEventRecord(out_ready, c->main_st), "cudaEventRecord");  // output buffers allocated
-    ck(cudaStreamWaitEvent(c->d2h_st, out_ready, 0), "cudaStreamWaitEvent");
+        h.level = level;
+        h.S = S;
+    }
     // chunk sizes (short_ends: half-size first and last chunks shorten the
     // exposed upload of the first chunk and download of the last one)
     std::vector<size_t> sizes;
     {
-        const size_t h = short_ends ? std::max<size_t>(1, S / 2) : S;
+        const size_t hs = short_ends ? std::max<size_t>(1, S / 2) : S;
         size_t rem = n;
         if (n > S) {
-            sizes.push_back(h);
-            rem -= h;
-            while (rem > S + h) {
+            sizes.push_back(hs);
+            rem -= hs;
+            while (rem > S + hs) {
                 sizes.push_back(S);
                 rem -= S;
             }
-            if (rem > h) {
-                sizes.push_back(rem - h);
-                rem = h;
+            if (rem > hs) {
+                sizes.push_back(rem - hs);
+                rem = hs;
             }
         }
         sizes.push_back(rem);
     }
+    std::vector<fhe_ct> vin(S), vout(S);
+    std::vector<fhe_ct*> pin(S), pout(S);
     size_t s0 = 0;
     for (size_t j = 0; j < sizes.size(); s0 += sizes[j], ++j) {
-        const int b = (int)(j & 1);
+        const int b = (int)(h.chunks & 1);
         const size_t sn = sizes[j];
-        if (j >= 2) ck(cudaStreamWaitEvent(c->h2d_st, ev_comp[b], 0), "cudaStreamWaitEvent");
+        if (h.chunks >= 2) ck(cudaStreamWaitEvent(c->h2d_st, h.ev_comp[b], 0), "cudaStreamWaitEvent");
         for (size_t s = 0; s < sn; ++s)
-            ck(cudaMemcpyAsync(din[b][s]->d, host_in + (s0 + s) * inw, inw * 8, cudaMemcpyHostToDevice, c->h2d_st),
+            ck(cudaMemcpyAsync(h.din[b][s], host_in + (s0 + s) * inw, inw * 8, cudaMemcpyHostToDevice, c->h2d_st),
                "H2D");
-        ck(cudaEventRecord(ev_h2d[b], c->h2d_st), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(c->main_st, ev_h2d[b], 0), "cudaStreamWaitEvent");
-        if (j >= 2) ck(cudaStreamWaitEvent(c->main_st, ev_d2h[b], 0), "cudaStreamWaitEvent");
-        batch_impl(c, din[b].data(), sn, ly, approach, dout[b].data());
-        ck(cudaEventRecord(ev_comp[b], c->main_st), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(c->d2h_st, ev_comp[b], 0), "cudaStreamWaitEvent");
-        for (size_t s = 0; s < sn; ++s)
-            ck(cudaMemcpyAsync(host_out + (s0 + s) * outw, dout[b][s]->d, outw * 8, cudaMemcpyDeviceToHost, c->d2h_st),
-               "D2H");
-        ck(cudaEventRecord(ev_d2h[b], c->d2h_st), "cudaEventRecord");
-    }
-    // stream-ordered frees after the last use: inputs after the last conv,
-    // outputs after the last download
-    for (int b = 0; b < 2; ++b)
-        for (size_t s = 0; s < S; ++s) {
-            ck(cudaFreeAsync(din[b][s]->d, c->main_st), "cudaFreeAsync");
-            ck(cudaFreeAsync(dout[b][s]->d, c->d2h_st), "cudaFreeAsync");
-            delete din[b][s];
-            delete dout[b][s];
+        ck(cudaEventRecord(h.ev_h2d[b], c->h2d_st), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->main_st, h.ev_h2d[b], 0), "cudaStreamWaitEvent");
+        if (h.chunks >= 2) ck(cudaStreamWaitEvent(c->main_st, h.ev_d2h[b], 0), "cudaStreamWaitEvent");
+        for (size_t s = 0; s < sn; ++s) {
+            vin[s] = fhe_ct{c, level, sc, 0, h.din[b][s]};
+            vout[s] = fhe_ct{c, level - 1, sc, 1, h.dout[b][s]};
+            pin[s] = &vin[s];
+            pout[s] = &vout[s];
         }
-    for (cudaEvent_t e : {ev_h2d[0], ev_h2d[1], ev_comp[0], ev_comp[1], ev_d2h[0], ev_d2h[1], out_ready})
-        c->pending_events.push_back(e);
+        batch_impl(c, pin.data(), sn, ly, approach, pout.data());
+        ck(cudaEventRecord(h.ev_comp[b], c->main_st), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->d2h_st, h.ev_comp[b], 0), "cudaStreamWaitEvent");
+        for (size_t s = 0; s < sn; ++s)
+            ck(cudaMemcpyAsync(host_out + (s0 + s) * outw, h.dout[b][s], outw * 8, cudaMemcpyDeviceToHost, c->d2h_st),
+               "D2H");
+        ck(cudaEventRecord(h.ev_d2h[b], c->d2h_st), "cudaEventRecord");
+        ++h.chunks;
+    }
 }
 
 static void host_wait(fhe_ctx* c) {
