@@ -1575,16 +1575,45 @@ int fhe_rotate_hoisted(fhe_ctx* c, const fhe_ct* ct, const int64_t* ks, size_t n
             digits = c->alloc((size_t)c->dn_at(level) * c->ne_at(level) * c->N);
             modup(c, ct->c1(), level, digits);
         }
+        // all keyed outputs at once: one streaming key-switch launch writes
+        // (IP_0 + P sigma(c0), IP_1) per output in the QP basis, then one batched
+        // ModDown (ModDown(P x + y) = x + ModDown(y) exactly)
+        const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+        const size_t extw = (size_t)ne * c->N, ctw = (size_t)2 * nr * c->N;
+        std::vector<size_t> keyed;
+        for (size_t i = 0; i < n; ++i)
+            if (c->reduce_amount(ks[i])) keyed.push_back(i);
+        uint64_t* XT = keyed.empty() ? nullptr : c->alloc(keyed.size() * 2 * extw);
+        uint64_t* md = keyed.empty() ? nullptr : c->alloc(keyed.size() * ctw);
+        for (size_t t0 = 0; t0 < keyed.size(); t0 += kMaxBaby) {
+            KsStream kss{};
+            kss.digits = digits;
+            kss.digit_stride = 0;
+            kss.out = XT;
+            for (size_t t = t0; t < keyed.size() && kss.n < kMaxBaby; ++t) {
+                const uint32_t g = c->galois_of(c->reduce_amount(ks[keyed[t]]));
+                kss.galois[kss.n] = g;
+                kss.key[kss.n] = c->key_for(g);
+                kss.c0[kss.n] = ct->c0();
+                kss.slot[kss.n] = (int)t;
+                kss.n++;
+            }
+            c->timed("ks_multi", c->rows((double)kss.n * (2.0 * dn * ne + 2.0 * ne) + (double)dn * ne + nr),
+                     [&] { ks_stream(c->dc, kss, 0, c->d_md, level, dn, c->st); });
+        }
+        c->ledger.key_switches += keyed.size();
+        if (!keyed.empty()) moddown(c, XT, level, (int)(2 * keyed.size()), md, nullptr, 1);
+        size_t kt = 0;
         for (size_t i = 0; i < n; ++i) {
             const uint64_t a = c->reduce_amount(ks[i]);
             c->note_amount(a);
             fhe_ct* o = new_ct(c, level, ct->scale, ct->depth);
-            if (a == 0)
-                ck(cudaMemcpyAsync(o->d, ct->d, ct->words() * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
-            else
-                rotate_from_digits(c, ct, digits, c->galois_of(a), o->d);
+            const uint64_t* src = a == 0 ? ct->d : md + (kt++) * ctw;
+            ck(cudaMemcpyAsync(o->d, src, ct->words() * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
             outs[i] = o;
         }
+        c->release(md);
+        c->release(XT);
         c->release(digits);
         c->ledger.hoist_groups++;
         c->ledger.hoisted_rotations += n;
