@@ -246,17 +246,25 @@ def run_ours(args, rank, world, local_rank):
     for ap in (1, 2, 3, 4, 5):
         k2 = max(3, args.steps // 8) if ap in (1, 2) else max(5, args.steps // 4)
         per_approach[ap] = world * k2 / (timed_convs(ap, k2, 2) / 1e3)
-    # hoisted rotations at N = 2^15: the 8 non-identity shifts of a 3x3 stencil from one ModUp
+    # hoisted rotations at N = 2^15: the 8 non-identity shifts of a 3x3 stencil from one ModUp,
+    # for the step's B ciphertexts at once (keys shared) and for one ciphertext; outputs are
+    # preallocated (fhe_rotate_hoisted_batch_into), so the allocator stays out of the timed region
     stencil = [kk * M + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1) if kk or ll]
-    for _ in range(2):
-        ctx.rotate_hoisted(ct, stencil)
-    ctx.synchronize()
+    hout = [ctx.encrypt(ctx.encode(np.zeros(8)), 1) for _ in range(B * len(stencil))]
     kh = max(10, args.steps // 2)
-    ctx.timer_start()
-    for _ in range(kh):
-        hs = ctx.rotate_hoisted(ct, stencil)
-    ms_hoist = max_over_ranks(ctx.timer_stop())
-    del hs
+
+    def time_hoist(srcs):
+        outs_h = hout[: len(srcs) * len(stencil)]
+        for _ in range(2):
+            ctx.rotate_hoisted_batch_into(srcs, stencil, outs_h)
+        ctx.synchronize()
+        ctx.timer_start()
+        for _ in range(kh):
+            ctx.rotate_hoisted_batch_into(srcs, stencil, outs_h)
+        return max_over_ranks(ctx.timer_stop())
+
+    ms_hoist = time_hoist(cts)
+    ms_hoist1 = time_hoist([ct])
 
     # ---- e2e: the C ABI with pinned host buffers; H2D of the batch, conv, D2H of the results
     N = ctx.N
@@ -359,7 +367,10 @@ def run_ours(args, rank, world, local_rank):
                                "frac": round(ks_bytes / (ks_ms / 1e3) / 1e9 / peak, 4) if ks_ms else None},
         "kernels": kernels,
         "conv_per_s_by_approach_batch1": {str(k): round(v, 2) for k, v in per_approach.items()},
-        "hoisted_rot_per_s": round(world * kh * len(stencil) / (ms_hoist / 1e3), 1),
+        "hoisted_rot_per_s": round(world * kh * B * len(stencil) / (ms_hoist / 1e3), 1),
+        "hoisted_rot": {"batch": B, "single_ct_per_s": round(world * kh * len(stencil) / (ms_hoist1 / 1e3), 1),
+                        "api": "fhe_rotate_hoisted_batch_into: one ModUp per ciphertext, every stencil key "
+                               "streamed once per 16 ciphertexts, one batched ModDown"},
         "cfg2_rotations": cfg2,
         "other_configs": other_cfgs,
         "e2e": {"value": round(world * ke * B / e2e_s, 3), "unit": "conv/s",
@@ -453,39 +464,52 @@ def other_configs(world, device):
     return res
 
 
-def cfg2_rotations(world):
-    """BASELINE cfg2 (N=2^14, 8x50-bit q | 1x60-bit p): rotations by every amount
-    1..127 through power-of-two keys only, positive vs signed decomposition
-    (reference rot.cpp:21-46), and the hoisted 3x3 stencil (m = 32)."""
+def cfg2_rotations(world, nct=256):
+    """BASELINE cfg2 (N=2^14, 8x50-bit q | 1x60-bit p): `nct` seeded ciphertexts, each rotated
+    by every amount 1..127 through power-of-two keys only, positive vs signed decomposition
+    (reference rot.cpp:21-46), and the hoisted 3x3 stencil (m = 32). Every decomposition step
+    is one batched keyed rotation of all ciphertexts (fhe_rotate_hoisted_batch_into, keys
+    shared), outputs ping-pong between two preallocated sets."""
     from paper_2306_09189_b200 import Context, decompose
     ctx = Context.from_config("cfg2")
     ctx.keygen(7)
     pow2 = [1 << i for i in range(8)]
     stencil = [kk * 32 + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1) if kk or ll]
     ctx.gen_galois_keys(pow2 + [-x for x in pow2] + stencil)
-    z = np.random.default_rng(5).uniform(-1, 1, ctx.slots)
-    ct = ctx.encrypt(ctx.encode(z), 1)
-    res = {}
+    rng = np.random.default_rng(5)
+    cts = [ctx.encrypt(ctx.encode(rng.uniform(-1, 1, ctx.slots)), 100 + i) for i in range(nct)]
+    bufs = [[ctx.encrypt(ctx.encode(np.zeros(8)), 1) for _ in range(nct)] for _ in range(2)]
+    res = {"ciphertexts": nct}
     for strat, name in ((0, "positive"), (1, "signed")):
-        keyed = sum(len(decompose(strat, n, ctx.slots)) for n in range(1, 128))
-        ctx.rotate_decomposed(ct, 127, strat)
+        plans = {n: decompose(strat, n, ctx.slots) for n in range(1, 128)}
+        keyed = sum(len(p) for p in plans.values())
+
+        def rotate_all(n):
+            src = cts
+            for i, step in enumerate(plans[n]):
+                dst = bufs[i & 1]
+                ctx.rotate_hoisted_batch_into(src, [step], dst)
+                src = dst
+
+        rotate_all(127)
         ctx.synchronize()
         ctx.timer_start()
         for n in range(1, 128):
-            r = ctx.rotate_decomposed(ct, n, strat)
+            rotate_all(n)
         ms = ctx.timer_stop()
-        res[name] = {"requested_rot_per_s": round(world * 127 / (ms / 1e3), 1),
-                     "keyed_switches_per_s": round(world * keyed / (ms / 1e3), 1), "keyed_per_vector": keyed}
-    del r
-    ctx.rotate_hoisted(ct, stencil)
+        res[name] = {"requested_rot_per_s": round(world * nct * 127 / (ms / 1e3), 1),
+                     "keyed_switches_per_s": round(world * nct * keyed / (ms / 1e3), 1), "keyed_per_vector": keyed}
+    hb = [ctx.encrypt(ctx.encode(np.zeros(8)), 1) for _ in range(nct * len(stencil))]
+    ctx.rotate_hoisted_batch_into(cts, stencil, hb)
     ctx.synchronize()
     ctx.timer_start()
-    for _ in range(20):
-        hs = ctx.rotate_hoisted(ct, stencil)
+    for _ in range(3):
+        ctx.rotate_hoisted_batch_into(cts, stencil, hb)
     ms = ctx.timer_stop()
-    del hs
-    res["hoisted_stencil_rot_per_s"] = round(world * 20 * len(stencil) / (ms / 1e3), 1)
-    res["note"] = "one ciphertext, amounts 1..127 sequentially; hoisted = 8 stencil shifts from one ModUp"
+    res["hoisted_stencil_rot_per_s"] = round(world * 3 * nct * len(stencil) / (ms / 1e3), 1)
+    res["note"] = (f"{nct} ciphertexts, amounts 1..127 sequentially, each decomposition step one batched keyed "
+                   "rotation of all ciphertexts; hoisted = 8 stencil shifts from one ModUp per ciphertext")
+    ctx.close()
     return res
 
 

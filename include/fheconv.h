@@ -140,6 +140,14 @@ int fhe_rotate(fhe_ctx* ctx, const fhe_ct* ct, int64_t k, fhe_ct** out);
 /* replaces: Engine::rotate_many emu.cpp:39-54 — one shared ModUp (hoisting);
  * "empty rotation batch" when n == 0. outs[i] receives a new ciphertext. */
 int fhe_rotate_hoisted(fhe_ctx* ctx, const fhe_ct* ct, const int64_t* ks, size_t n, fhe_ct** outs);
+/* hoisted rotations of a batch: outs[i * k + j] = rot_{ks[j]}(cts[i]) (n * k
+ * outputs); one ModUp per ciphertext, each Galois key streamed once per chunk
+ * of up to 16 ciphertexts */
+int fhe_rotate_hoisted_batch(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, const int64_t* ks, size_t k,
+                             fhe_ct** outs);
+/* same into n * k preallocated ciphertexts at the inputs' level (no allocation) */
+int fhe_rotate_hoisted_batch_into(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, const int64_t* ks, size_t k,
+                                  fhe_ct* const* outs);
 /* replaces: Engine::mul_plain emu.cpp:56-67 (no rescale; level bookkeeping by
  * fhe_rescale) */
 int fhe_mul_plain(fhe_ctx* ctx, const fhe_ct* ct, const fhe_pt* pt, fhe_ct** out);

@@ -71,6 +71,8 @@ SIGNATURES = [
     ("fhe_pt_free", None, [vp]),
     ("fhe_rotate", C.c_int, [vp, vp, C.c_int64, vpp]),
     ("fhe_rotate_hoisted", C.c_int, [vp, vp, i64p, C.c_size_t, vpp]),
+    ("fhe_rotate_hoisted_batch", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, i64p, C.c_size_t, vpp]),
+    ("fhe_rotate_hoisted_batch_into", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, i64p, C.c_size_t, vpp]),
     ("fhe_mul_plain", C.c_int, [vp, vp, vp, vpp]),
     ("fhe_add", C.c_int, [vp, vp, vp, vpp]),
     ("fhe_sub", C.c_int, [vp, vp, vp, vpp]),

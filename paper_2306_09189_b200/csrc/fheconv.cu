@@ -1620,6 +1620,100 @@ int fhe_rotate_hoisted(fhe_ctx* c, const fhe_ct* ct, const int64_t* ks, size_t n
     });
 }
 
+// Hoisted rotations of a batch: outs[i * k + j] = rot_{ks[j]}(cts[i]). One
+// batched ModUp, one staged key-switch launch per chunk of sources (each key
+// row staged once per CTA for up to 4 ciphertexts), one batched ModDown.
+static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const int64_t* ks, size_t k,
+                                      fhe_ct** outs, bool into) {
+    {
+        if (k == 0) fail(FHE_E_INVALID, "empty rotation batch");
+        if (n == 0) return;
+        const int level = cts[0]->level;
+        for (size_t i = 0; i < n; ++i)
+            if (cts[i]->level != level) fail(FHE_E_INVALID, "batched rotation: all inputs must share one level");
+        std::vector<size_t> keyed;
+        for (size_t j = 0; j < k; ++j)
+            if (c->reduce_amount(ks[j])) {
+                c->key_for(c->galois_of(c->reduce_amount(ks[j])));  // fails early on a missing key
+                keyed.push_back(j);
+            }
+        const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+        const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
+        const size_t KK = keyed.size();
+        const size_t SC = std::max<size_t>(1, std::min<size_t>(n, 16));  // sources per chunk
+        uint64_t *buf = nullptr, *dig = nullptr, *XT = nullptr, *md = nullptr;
+        if (KK) {
+            buf = c->alloc(SC * ctw);
+            dig = c->alloc(SC * dw);
+            XT = c->alloc(SC * KK * 2 * extw);
+            md = c->alloc(SC * KK * ctw);
+        }
+        for (size_t s0 = 0; s0 < n; s0 += SC) {
+            const size_t sn = std::min(SC, n - s0);
+            if (KK) {
+                for (size_t s = 0; s < sn; ++s)
+                    ck(cudaMemcpyAsync(buf + s * ctw, cts[s0 + s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st),
+                       "memcpy");
+                modup_batch(c, buf + (size_t)nr * N, ctw, (int)sn, level, dig);
+                for (size_t t0 = 0; t0 < KK; t0 += kMaxBaby) {
+                    KsBatch kb{};
+                    kb.nsrc = (int)sn;
+                    kb.digits = dig;
+                    kb.digit_src_stride = dw;
+                    kb.c0 = buf;
+                    kb.c0_src_stride = ctw;
+                    kb.out = XT;
+                    kb.out_src_stride = KK * 2 * extw;
+                    for (size_t t = t0; t < KK && kb.n < kMaxBaby; ++t) {
+                        const uint32_t g = c->galois_of(c->reduce_amount(ks[keyed[t]]));
+                        kb.galois[kb.n] = g;
+                        kb.key[kb.n] = c->key_for(g);
+                        kb.slot[kb.n] = (int)t;
+                        kb.n++;
+                    }
+                    c->timed("ks_multi",
+                             c->rows((double)kb.n * 2.0 * dn * ne + sn * ((double)dn * ne + nr + 2.0 * kb.n * ne)),
+                             [&] { ks_batch(c->dc, kb, 0, c->d_md, level, dn, c->st); });
+                }
+                c->ledger.key_switches += sn * KK;
+                moddown(c, XT, level, (int)(2 * sn * KK), md, nullptr, 1);
+            }
+            for (size_t s = 0; s < sn; ++s) {
+                size_t kt = 0;
+                for (size_t j = 0; j < k; ++j) {
+                    const uint64_t a = c->reduce_amount(ks[j]);
+                    c->note_amount(a);
+                    fhe_ct* o = into ? outs[(s0 + s) * k + j] : new_ct(c, level, cts[s0 + s]->scale, cts[s0 + s]->depth);
+                    if (into) {
+                        if (!o || o->level != level) fail(FHE_E_INVALID, "output ciphertext level mismatch");
+                        o->scale = cts[s0 + s]->scale;
+                        o->depth = cts[s0 + s]->depth;
+                    }
+                    const uint64_t* src = a == 0 ? cts[s0 + s]->d : md + (s * KK + kt++) * ctw;
+                    ck(cudaMemcpyAsync(o->d, src, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+                    outs[(s0 + s) * k + j] = o;
+                }
+            }
+            c->ledger.hoist_groups += sn;
+            c->ledger.hoisted_rotations += sn * k;
+        }
+        c->release(md);
+        c->release(XT);
+        c->release(dig);
+        c->release(buf);
+    }
+}
+
+int fhe_rotate_hoisted_batch(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const int64_t* ks, size_t k,
+                             fhe_ct** outs) {
+    return guard(c, [&] { rotate_hoisted_batch_impl(c, cts, n, ks, k, outs, false); });
+}
+
+int fhe_rotate_hoisted_batch_into(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const int64_t* ks, size_t k,
+                                  fhe_ct* const* outs) {
+    return guard(c, [&] { rotate_hoisted_batch_impl(c, cts, n, ks, k, const_cast<fhe_ct**>(outs), true); });
+}
+
 int fhe_rotate(fhe_ctx* c, const fhe_ct* ct, int64_t k, fhe_ct** out) {
     return guard(c, [&] {
         const uint64_t a = c->reduce_amount(k);

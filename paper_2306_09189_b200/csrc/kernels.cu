@@ -1195,6 +1195,95 @@ __global__ void __launch_bounds__(128, 3) k_ks_giant(DevCtx c, KsBatch a, int le
     }
 }
 
+// Hoisted key switches of a batch, one output per (source, term):
+// XT(s, slot_t) = (IP_0(D(s), key_t) + [u<=l] P sigma_t(c0(s)), IP_1(D(s), key_t))
+// in the QP basis (a ModDown turns it into the rotated ciphertext). Staging
+// as k_ks_giant: the key rows of a term are shared by the CTA's SG sources.
+template <int DN, int SG>
+__global__ void __launch_bounds__(128, 3) k_ks_hoist(DevCtx c, KsBatch a, const ModDownTable* md, int level) {
+    constexpr int P = 128 / SG;
+    constexpr int KW = 2 * DN * P, DW = SG * DN * P, CW = SG * P, STAGE = KW + DW + CW;
+    extern __shared__ ulonglong2 sb[];  // [2][STAGE]
+    const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
+    const int tid = threadIdx.x, p = tid % P, sl = tid / P;
+    const size_t total = (size_t)ne * c.N;
+    const size_t chunks = total / 2 / P;
+    const int ngroups = (a.nsrc + SG - 1) / SG;
+    const size_t items = chunks * (size_t)ngroups;
+    const size_t keyrow = (size_t)np * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    ulonglong2* const s_key = sb + p;
+    ulonglong2* const s_dig = sb + KW + sl * DN * P + p;
+    ulonglong2* const s_c0 = sb + KW + DW + sl * P + p;
+    for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const size_t chunk = it / (size_t)ngroups;
+        const int s = (int)(it % (size_t)ngroups) * SG + sl;
+        const bool active = s < a.nsrc;
+        const size_t i = (chunk * P + p) * 2;
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
+        const int pi = row_prime(rm, u);
+        const bool qrow = u < nr;
+        const uint64_t pm = qrow ? md->pmod[u] : 0;
+        const size_t kofs = (size_t)pi * c.N + k;
+        const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
+        auto pidx = [&](uint32_t g) { return brev_n((((e * g) & nmask) - 1) >> 1, c.logN); };
+        const uint64_t* Ds = a.digits + (size_t)(active ? s : 0) * a.digit_src_stride + (size_t)u * c.N;
+        const uint64_t* C0 = a.c0 + (size_t)(active ? s : 0) * a.c0_src_stride + (size_t)u * c.N;
+        auto issue = [&](int t) {
+            const size_t so = (size_t)(t & 1) * STAGE;
+            const uint64_t* kp = a.key[t] + kofs;
+#pragma unroll
+            for (int j = sl; j < 2 * DN; j += SG) cp_async16(s_key + so + j * P, kp + (size_t)j * keyrow);
+            if (active) {
+                const uint32_t pk = pidx(a.galois[t]) & ~1u;
+#pragma unroll
+                for (int j = 0; j < DN; ++j) cp_async16(s_dig + so + j * P, Ds + (size_t)j * total + pk);
+                if (qrow) cp_async16(s_c0 + so, C0 + pk);
+            }
+            cp_async_commit();
+        };
+        const Prime pr = c.primes[pi];
+        issue(0);
+        for (int t = 0; t < a.n; ++t) {
+            cp_async_wait<0>();
+            __syncthreads();
+            if (t + 1 < a.n) issue(t + 1);
+            const size_t so = (size_t)(t & 1) * STAGE;
+            const int swp = (int)(pidx(a.galois[t]) & 1u);
+            Acc3 s0a{0, 0, 0, 0}, s0b{0, 0, 0, 0}, s1a{0, 0, 0, 0}, s1b{0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < DN; ++j) {
+                const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
+                const ulonglong2 dv = s_dig[so + j * P];
+                const uint64_t da = swp ? dv.y : dv.x, db = swp ? dv.x : dv.y;
+                mac3(s0a, da, k0.x);
+                mac3(s0b, db, k0.y);
+                mac3(s1a, da, k1.x);
+                mac3(s1b, db, k1.y);
+            }
+            if (qrow) {
+                const ulonglong2 cv = s_c0[so];
+                const uint64_t ca = swp ? cv.y : cv.x, cb = swp ? cv.x : cv.y;
+                if (DN < 8) {
+                    mac3(s0a, ca, pm);
+                    mac3(s0b, cb, pm);
+                } else {
+                    add3(s0a, mul_shoup(ca, pm, md->pmod_sh[u], pr.q));
+                    add3(s0b, mul_shoup(cb, pm, md->pmod_sh[u], pr.q));
+                }
+            }
+            if (active) {
+                uint64_t* xt = a.out + (size_t)s * a.out_src_stride + (size_t)a.slot[t] * 2 * total;
+                const U128 t0a = fold3(s0a), t0b = fold3(s0b), t1a = fold3(s1a), t1b = fold3(s1b);
+                st2(xt + i, reduce128(t0a.hi, t0a.lo, pr), reduce128(t0b.hi, t0b.lo, pr));
+                st2(xt + total + i, reduce128(t1a.hi, t1a.lo, pr), reduce128(t1b.hi, t1b.lo, pr));
+            }
+        }
+        __syncthreads();
+    }
+}
+
 template <int DN>
 __global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc, const uint64_t* D,
                                                          const uint64_t* key, const uint64_t* c0, uint32_t g,
@@ -1359,9 +1448,34 @@ static void launch_giant(const DevCtx& c, const KsBatch& a, int level, cudaStrea
     k_ks_giant<DN, SG><<<(int)(items < cap ? items : cap), 128, smem, st>>>(c, a, level);
 }
 
+template <int DN, int SG>
+static void launch_hoist(const DevCtx& c, const KsBatch& a, const ModDownTable* md, int level, cudaStream_t st) {
+    constexpr int P = 128 / SG;
+    const size_t smem = (size_t)2 * (2 * DN * P + SG * DN * P + SG * P) * sizeof(ulonglong2);
+    const size_t items = (size_t)(level + 1 + c.K) * c.N / 2 / P * (size_t)((a.nsrc + SG - 1) / SG);
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_ks_hoist<DN, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ks_hoist<DN, SG>, 128, smem);
+    const size_t cap = (size_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+    k_ks_hoist<DN, SG><<<(int)(items < cap ? items : cap), 128, smem, st>>>(c, a, md, level);
+}
+
 void ks_batch(const DevCtx& c, const KsBatch& a, int mode, const ModDownTable* md, int level, int dn,
               cudaStream_t st) {
     if (a.n <= 0 || a.nsrc <= 0) return;
+    if (mode == 0 && !a.c0_qp) {  // hoisted rotations of a batch: one output per (source, term)
+        ++g_launches;
+        const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
+#define FHE_HOIST(D)                                                  \
+    do {                                                              \
+        if (sg == 4) launch_hoist<D, 4>(c, a, md, level, st);         \
+        else if (sg == 2) launch_hoist<D, 2>(c, a, md, level, st);    \
+        else launch_hoist<D, 1>(c, a, md, level, st);                 \
+    } while (0)
+        FHE_DN_SWITCH(dn, FHE_HOIST)
+#undef FHE_HOIST
+        return;
+    }
     if (mode == 1 && a.c0_qp) {  // giant steps: staged, key rows shared by the sources of a CTA
         ++g_launches;
         const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;

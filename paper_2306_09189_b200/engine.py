@@ -242,6 +242,21 @@ class Context:
 
     rotate_many = rotate_hoisted  # reference name (emu.hpp:164)
 
+    def rotate_hoisted_batch(self, cts: Sequence[Ciphertext], ks: Sequence[int]) -> list[list[Ciphertext]]:
+        """fhe_rotate_hoisted_batch: [[rot_k(ct) for k in ks] for ct in cts], keys shared by the batch."""
+        a = np.ascontiguousarray(list(ks), dtype=np.int64)
+        ins = (C.c_void_p * max(1, len(cts)))(*[x.h for x in cts])
+        outs = (C.c_void_p * max(1, len(cts) * len(a)))()
+        self._check(lib().fhe_rotate_hoisted_batch(self.h, ins, len(cts), a.ctypes.data_as(_lib.i64p), len(a), outs))
+        return [[Ciphertext(self, outs[i * len(a) + j]) for j in range(len(a))] for i in range(len(cts))]
+
+    def rotate_hoisted_batch_into(self, cts: Sequence[Ciphertext], ks: Sequence[int], outs: Sequence[Ciphertext]):
+        """fhe_rotate_hoisted_batch_into: outs[i * len(ks) + j] = rot_{ks[j]}(cts[i]) (preallocated)."""
+        a = np.ascontiguousarray(list(ks), dtype=np.int64)
+        ins = (C.c_void_p * max(1, len(cts)))(*[x.h for x in cts])
+        o = (C.c_void_p * max(1, len(outs)))(*[x.h for x in outs])
+        self._check(lib().fhe_rotate_hoisted_batch_into(self.h, ins, len(cts), a.ctypes.data_as(_lib.i64p), len(a), o))
+
     def rotate_decomposed(self, ct: Ciphertext, k: int, strategy: int) -> Ciphertext:
         return self._new(lib().fhe_rotate_decomposed, ct.h, k, strategy)
 

@@ -326,3 +326,16 @@ def test_host_pipelined_async_calls_chain(oracle, golden):
     p.ctx.host_wait()
     for o in outs:
         assert np.array_equal(o, want)
+
+
+def test_rotate_hoisted_batch_equals_single(p1):
+    """fhe_rotate_hoisted_batch (keys shared by the ciphertexts of a batch) = per-ciphertext hoisting."""
+    ks = [1, -1, 0, 32, -33, 1000]
+    p1.ctx.gen_galois_keys([k for k in ks if k])
+    rng = np.random.default_rng(21)
+    cts = [p1.ctx.encrypt(p1.ctx.encode(rng.uniform(-1, 1, p1.ctx.slots)), ENC_SEED + i) for i in range(5)]
+    outs = p1.ctx.rotate_hoisted_batch(cts, ks)
+    for i, ct in enumerate(cts):
+        single = p1.ctx.rotate_hoisted(ct, ks)
+        for j in range(len(ks)):
+            assert np.array_equal(outs[i][j].residues(), single[j].residues())
