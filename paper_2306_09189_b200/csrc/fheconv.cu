@@ -1028,6 +1028,139 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
     c->release(buf);
 }
 
+// The paper's schedules for a batch of S ciphertexts:
+// approach 2 rotates every input by the channel amounts r m^2 first, approach
+// 1 by the stencil shifts first (the first-level rotations, hoisted from one
+// ModUp, keys shared by the batch, ModDown'd to ciphertexts); every rotated
+// copy is ModUp'd and its second-level rotations are key-switched and
+// multiplied by the layer's plaintexts inside the fused baby-step kernel
+// (one accumulator, no giant step), so the per-copy key switches never touch
+// memory. One fused ModDown + rescale per output.
+void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv_layer* ly, int approach,
+                      fhe_ct* const* outs) {
+    const int level = cts[0]->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
+    for (int s = 0; s < S; ++s)
+        if (cts[s]->level != level || outs[s]->level != level - 1)
+            fail(FHE_E_INVALID, "batched conv: all inputs must share the layer level");
+    const int nk = ly->nk, cin = ly->c_in;
+    const long m = ly->m, h = ly->kappa / 2;
+    const int64_t block = (int64_t)m * m;
+    auto shift_amt = [&](int i) { return (int64_t)(i / (2 * h + 1) - h) * m + (i % (2 * h + 1) - h); };
+    auto nonempty = [&](int r, int i) { return ly->nonempty[(size_t)r * nk + i] != 0; };
+    // first level: approach 2 -> channels r (amount r m^2), approach 1 -> shifts i
+    const int nfirst = approach == 2 ? cin : nk, nsecond = approach == 2 ? nk : cin;
+    auto rpos = [&](int f, int x) { return approach == 2 ? std::make_pair(f, x) : std::make_pair(x, f); };
+    auto first_amt = [&](int f) { return approach == 2 ? (int64_t)f * block : shift_amt(f); };
+    auto second_amt = [&](int x) { return approach == 2 ? shift_amt(x) : (int64_t)x * block; };
+    std::vector<int> fl;  // first-level members used (identity first)
+    int fid = -1;
+    for (int f = 0; f < nfirst; ++f) {
+        bool any = false;
+        for (int x = 0; x < nsecond; ++x) any |= nonempty(rpos(f, x).first, rpos(f, x).second);
+        if (!any) continue;
+        if (c->reduce_amount(first_amt(f)) == 0) fid = f;
+        else fl.push_back(f);
+    }
+    const int NF = (int)fl.size() + 1;  // slot 0: the input itself
+    uint64_t* X = c->alloc((size_t)S * NF * ctw);
+    for (int s = 0; s < S; ++s)
+        ck(cudaMemcpyAsync(X + (size_t)s * NF * ctw, cts[s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    uint64_t* acc = c->alloc((size_t)S * 2 * extw);
+    ck(cudaMemsetAsync(acc, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
+    if (!fl.empty()) {  // first-level rotations of every input, hoisted, keys shared by the batch
+        uint64_t* dig0 = c->alloc((size_t)S * dw);
+        modup_batch(c, X + (size_t)nr * N, (size_t)NF * ctw, S, level, dig0);
+        const size_t F = fl.size();
+        uint64_t* XT = c->alloc((size_t)S * F * 2 * extw);
+        for (size_t t0 = 0; t0 < F; t0 += kMaxBaby) {
+            KsBatch kb{};
+            kb.nsrc = S;
+            kb.digits = dig0;
+            kb.digit_src_stride = dw;
+            kb.c0 = X;
+            kb.c0_src_stride = (size_t)NF * ctw;
+            kb.out = XT;
+            kb.out_src_stride = F * 2 * extw;
+            for (size_t t = t0; t < F && kb.n < kMaxBaby; ++t) {
+                const uint32_t g = c->galois_of(c->reduce_amount(first_amt(fl[t])));
+                kb.galois[kb.n] = g;
+                kb.key[kb.n] = c->key_for(g);
+                kb.slot[kb.n] = (int)t;
+                kb.n++;
+            }
+            c->timed("ks_multi", c->rows((double)kb.n * 2.0 * dn * ne + S * ((double)dn * ne + nr + 2.0 * kb.n * ne)),
+                     [&] { ks_batch(c->dc, kb, 0, c->d_md, level, dn, c->st); });
+        }
+        c->ledger.key_switches += (uint64_t)S * F;
+        for (int s = 0; s < S; ++s)
+            moddown(c, XT + (size_t)s * F * 2 * extw, level, (int)(2 * F), X + ((size_t)s * NF + 1) * ctw, nullptr, 1);
+        c->release(XT);
+        c->release(dig0);
+    }
+    // every copy's ModUp, then the fused second-level key switches + MAC
+    uint64_t* dig = c->alloc((size_t)S * NF * dw);
+    modup_batch(c, X + (size_t)nr * N, ctw, S * NF, level, dig);
+    FusedBsgs fb{};
+    fb.nsrc = S;
+    fb.ng = 1;
+    fb.digits = dig;
+    fb.digit_src_stride = (size_t)NF * dw;
+    fb.digit_slot_stride = dw;
+    fb.ct = X;
+    fb.ct_src_stride = (size_t)NF * ctw;
+    fb.ct_slot_stride = ctw;
+    fb.pt_g_stride = 0;
+    fb.Y = acc;
+    fb.y_src_stride = 2 * extw;
+    fb.y_g_stride = 2 * extw;
+    fb.accumulate = 1;
+    double keyed = 0, pts = 0;
+    auto flush = [&] {
+        if (!fb.nb) return;
+        c->timed("bsgs_fused", c->rows(keyed * 2.0 * dn * ne + pts * ne + S * (NF * (double)dn * ne + 2.0 * nr + 4.0 * ne)),
+                 [&] { bsgs_fused(c->dc, fb, c->d_md, level, dn, c->st); });
+        fb.nb = 0;
+        keyed = pts = 0;
+    };
+    for (int slot = 0; slot < NF; ++slot) {
+        const int f = slot == 0 ? fid : fl[slot - 1];
+        if (f < 0) continue;
+        for (int x = 0; x < nsecond; ++x) {
+            const auto rp = rpos(f, x);
+            if (!nonempty(rp.first, rp.second)) continue;
+            if (fb.nb == kMaxFused) flush();
+            const uint32_t g = c->galois_of(c->reduce_amount(second_amt(x)));
+            fb.galois[fb.nb] = g;
+            fb.key[fb.nb] = g == 1 ? nullptr : c->key_for(g);
+            fb.gmask[fb.nb] = 1;
+            fb.pt[fb.nb] = ly->d_pts + ((size_t)rp.first * nk + rp.second) * extw;
+            fb.srcslot[fb.nb] = (uint16_t)slot;
+            fb.nb++;
+            pts += 1;
+            if (g != 1) {
+                keyed += 1;
+                c->ledger.key_switches += S;
+            }
+        }
+    }
+    flush();
+    c->release(dig);
+    const size_t otw = (size_t)2 * level * N;
+    uint64_t* md = c->alloc((size_t)S * otw);
+    moddown_rescale(c, acc, extw, level, 2 * S, md);
+    for (int s = 0; s < S; ++s) {
+        ck(cudaMemcpyAsync(outs[s]->d, md + (size_t)s * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+        outs[s]->scale = (cts[s]->scale * (double)c->primes[level]) / (double)c->primes[level];
+        outs[s]->depth = cts[s]->depth + 1;
+        c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[s]->depth);
+        ledger_conv(c, ly, approach);
+    }
+    c->release(md);
+    c->release(acc);
+    c->release(X);
+}
+
 int auto_orient(const fhe_conv_layer* ly) {
     // giant steps each cost a ModDown + ModUp (~120 NTT rows at cfg3) while a
     // fused baby step costs one key stream: the fused schedule (kappa giant
@@ -1140,6 +1273,14 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
     if (n == 0) return;
     if (approach < 0 || approach > 5) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3, 4 or 5");
     if (approach == 0) approach = auto_orient(ly);
+    if ((approach == 1 || approach == 2) && n > 1 && c->batch5) {
+        if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
+        for (size_t s0 = 0; s0 < n; s0 += 8) {
+            const int S = (int)std::min<size_t>(8, n - s0);
+            conv_paper_batch(c, cts + s0, S, ly, approach, outs + s0);
+        }
+        return;
+    }
     if (approach >= 3 && n > 1 && (c->fused_batch || (approach == 5 && c->batch5))) {
         if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
         for (size_t s0 = 0; s0 < n; s0 += 32) {

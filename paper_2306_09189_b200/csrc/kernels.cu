@@ -948,7 +948,7 @@ struct FusedLayout {
     static constexpr int STAGE = KW + PW + DW + CW;
 };
 
-template <int DN, int NG, int SG, int NST, int MINB>
+template <int DN, int NG, int SG, int NST, int MINB, bool SLOTS>
 __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a, const ModDownTable* md, int level) {
     using LY = FusedLayout<DN, NG, SG, NST>;
     constexpr int P = LY::P;
@@ -977,10 +977,8 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
         const Prime pr = c.primes[pi];
         const bool qrow = u < nr;
         const uint64_t pm = qrow ? md->pmod[u] : 0, pms = qrow ? md->pmod_sh[u] : 0;
-        const uint64_t* Du = a.digits + (size_t)(active ? s : 0) * a.digit_src_stride + (size_t)u * c.N;
-        const uint64_t* C = a.ct + (size_t)(active ? s : 0) * a.ct_src_stride;
-        const uint64_t* C0u = C + (size_t)u * c.N;
-        const uint64_t* C1u = C + ((size_t)nr + u) * c.N;
+        const uint64_t* Du0 = a.digits + (size_t)(active ? s : 0) * a.digit_src_stride + (size_t)u * c.N;
+        const uint64_t* C00 = a.ct + (size_t)(active ? s : 0) * a.ct_src_stride;
         const size_t kofs = (size_t)pi * c.N + k, pofs = (size_t)u * c.N + k;
         // bit-reversed exponent of this pair, reused for every baby's permutation
         const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
@@ -994,6 +992,10 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
             const size_t so = (size_t)(b % NST) * LY::STAGE;
             const uint64_t* key = a.key[b];
             const uint32_t gm = a.gmask[b];
+            const uint64_t* Du = SLOTS ? Du0 + (size_t)a.srcslot[b] * a.digit_slot_stride : Du0;
+            const uint64_t* C = SLOTS ? C00 + (size_t)a.srcslot[b] * a.ct_slot_stride : C00;
+            const uint64_t* C0u = C + (size_t)u * c.N;
+            const uint64_t* C1u = C + ((size_t)nr + u) * c.N;
 #pragma unroll
             for (int g = sl; g < NG; g += SG)
                 if ((gm >> g) & 1u) cp_async16(s_pt + so + g * P, a.pt[b] + (size_t)g * a.pt_g_stride + pofs);
@@ -1016,6 +1018,19 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
         U128 y[NG][2][2];
 #pragma unroll
         for (int g = 0; g < NG; ++g) y[g][0][0] = y[g][0][1] = y[g][1][0] = y[g][1][1] = U128{0, 0};
+        if (SLOTS && a.accumulate && active) {  // continue earlier partial sums, in the kernel's 2^-64 domain
+            const uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                if (g >= a.ng) break;
+                const ulonglong2 v0 = ld2(Ys + (size_t)g * a.y_g_stride + i);
+                const ulonglong2 v1 = ld2(Ys + (size_t)g * a.y_g_stride + total + i);
+                y[g][0][0] = U128{redc_lazy(0, v0.x, pr), 0};
+                y[g][0][1] = U128{redc_lazy(0, v0.y, pr), 0};
+                y[g][1][0] = U128{redc_lazy(0, v1.x, pr), 0};
+                y[g][1][1] = U128{redc_lazy(0, v1.y, pr), 0};
+            }
+        }
 #pragma unroll
         for (int b = 0; b < NST - 1; ++b) issue(b);
         for (int b = 0; b < a.nb; ++b) {
@@ -1543,29 +1558,35 @@ void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms
 #ifndef FHE_FUSED_MINB
 #define FHE_FUSED_MINB 3
 #endif
-template <int DN, int NG, int SG, int NST = 2, int MINB = 4>
+template <int DN, int NG, int SG, int NST = 2, int MINB = 4, bool SLOTS = false>
 static void launch_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, cudaStream_t st) {
     using LY = FusedLayout<DN, NG, SG, NST>;
     const int ne = level + 1 + c.K;
     const size_t smem = (size_t)NST * LY::STAGE * sizeof(ulonglong2);
     const size_t items = (size_t)ne * c.N / 2 / LY::P * (size_t)((a.nsrc + SG - 1) / SG);
     int per_sm = 0;
-    cudaFuncSetAttribute(k_bsgs_fused<DN, NG, SG, NST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_fused<DN, NG, SG, NST, MINB>, 128, smem);
+    cudaFuncSetAttribute(k_bsgs_fused<DN, NG, SG, NST, MINB, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_fused<DN, NG, SG, NST, MINB, SLOTS>, 128, smem);
     if (per_sm < 1) per_sm = 1;
     const size_t cap = (size_t)sm_count() * per_sm;
     const int blocks = (int)(items < cap ? items : cap);
-    k_bsgs_fused<DN, NG, SG, NST, MINB><<<blocks, 128, smem, st>>>(c, a, md, level);
+    k_bsgs_fused<DN, NG, SG, NST, MINB, SLOTS><<<blocks, 128, smem, st>>>(c, a, md, level);
 }
 
 void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, int dn, cudaStream_t st) {
     if (a.nb <= 0 || a.nsrc <= 0 || a.ng <= 0) return;
     ++g_launches;
-    // sources per CTA: 4 (keys/plaintexts shared 4 ways), 2 for pairs, 1 alone
+    // sources per CTA: 4 (keys/plaintexts shared 4 ways), 2 for pairs, 1 alone;
+    // per-baby source slots (paper schedules; the host passes <= 3 giant accumulators)
     const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
+    const bool slots = a.accumulate || a.digit_slot_stride || a.ct_slot_stride;
 #define FHE_FUSED(D)                                                                                \
     do {                                                                                            \
-        if (a.ng <= 3) {                                                                            \
+        if (slots) {                                                                                \
+            if (sg == 4) launch_fused<D, 3, 4, FHE_FUSED_NST, FHE_FUSED_MINB, true>(c, a, md, level, st); \
+            else if (sg == 2) launch_fused<D, 3, 2, 2, 3, true>(c, a, md, level, st);               \
+            else launch_fused<D, 3, 1, 2, 2, true>(c, a, md, level, st);                            \
+        } else if (a.ng <= 3) {                                                                     \
             if (sg == 4) launch_fused<D, 3, 4, FHE_FUSED_NST, FHE_FUSED_MINB>(c, a, md, level, st); \
             else if (sg == 2) launch_fused<D, 3, 2, 2, 3>(c, a, md, level, st);                     \
             else launch_fused<D, 3, 1, 2, 2>(c, a, md, level, st);                                  \

@@ -288,6 +288,11 @@ struct FusedBsgs {
     size_t ct_src_stride;
     uint64_t* Y;                     // Y_g(s) = Y + s * y_src_stride + g * y_g_stride, [2][ne][N]
     size_t y_src_stride, y_g_stride;
+    // paper schedules: baby b reads its digits / ciphertext from slot srcslot[b]
+    // (digits + srcslot * digit_slot_stride, ct + srcslot * ct_slot_stride)
+    uint16_t srcslot[kMaxFused];
+    size_t digit_slot_stride, ct_slot_stride;
+    int accumulate;                  // Y_g += (instead of =)
 };
 void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, int dn, cudaStream_t st);
 // acc += y over [2][ne][N] (QP basis)

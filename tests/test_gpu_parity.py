@@ -280,7 +280,9 @@ def test_cfg2_hoisted_stencil(oracle):
 
 
 @pytest.mark.parametrize("name,approach,n", [("cfg1", 4, 5), ("cfg3", 3, 5), ("cfg3", 0, 5), ("cfg1", 5, 5),
-                                             ("cfg3", 5, 5), ("cfg1", 5, 2), ("cfg1", 5, 3), ("cfg1", 5, 9)])
+                                             ("cfg3", 5, 5), ("cfg1", 5, 2), ("cfg1", 5, 3), ("cfg1", 5, 9),
+                                             ("cfg1", 1, 5), ("cfg1", 2, 5), ("cfg3", 1, 3), ("cfg3", 2, 3),
+                                             ("cfg1", 2, 10)])
 def test_batched_conv_equals_single(oracle, golden, name, approach, n):
     """fhe_conv2d_batch (keys/plaintexts streamed once per batch) = per-ciphertext conv, bit for bit."""
     p = pair(oracle, name)
