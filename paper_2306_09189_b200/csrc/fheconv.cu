@@ -85,6 +85,19 @@ struct fhe_ctx {
     // timing / profiling (CUDA events on st)
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     bool prof_on = false;
+    // CUDA graphs of batched convs (FHECONV_GRAPHS=0 disables): captured once per
+    // (layer, approach, input/output ciphertexts) and replayed; the ledger and
+    // launch counters of the capture are re-applied on every replay
+    struct GraphEntry {
+        std::vector<const void*> key;
+        cudaGraphExec_t exec = nullptr;
+        fhe_ledger delta{};
+        uint64_t launches = 0;
+        uint64_t last_use = 0;
+    };
+    std::vector<GraphEntry> graphs;
+    bool use_graphs = true;
+    uint64_t graph_clock = 0;
     struct ProfRec {
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
         double ms = 0;
@@ -1273,20 +1286,86 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
     if (n == 0) return;
     if (approach < 0 || approach > 5) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3, 4 or 5");
     if (approach == 0) approach = auto_orient(ly);
-    if ((approach == 1 || approach == 2) && n > 1 && c->batch5) {
+    const bool paper_batch = (approach == 1 || approach == 2) && n > 1 && c->batch5;
+    const bool bsgs_batch = approach >= 3 && n > 1 && (c->fused_batch || (approach == 5 && c->batch5));
+    if (paper_batch || bsgs_batch) {
         if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
-        for (size_t s0 = 0; s0 < n; s0 += 8) {
-            const int S = (int)std::min<size_t>(8, n - s0);
-            conv_paper_batch(c, cts + s0, S, ly, approach, outs + s0);
+        for (size_t s = 0; s < n; ++s)
+            if (outs[s]->level != ly->level - 1) fail(FHE_E_INVALID, "output level must be input level - 1");
+        auto body = [&] {
+            if (paper_batch) {
+                for (size_t s0 = 0; s0 < n; s0 += 8)
+                    conv_paper_batch(c, cts + s0, (int)std::min<size_t>(8, n - s0), ly, approach, outs + s0);
+            } else {
+                for (size_t s0 = 0; s0 < n; s0 += 32)
+                    conv_bsgs_batch(c, cts + s0, (int)std::min<size_t>(32, n - s0), ly, approach, outs + s0);
+            }
+        };
+        if (!c->use_graphs || c->prof_on || c->st != c->main_st) {
+            body();
+            return;
         }
-        return;
-    }
-    if (approach >= 3 && n > 1 && (c->fused_batch || (approach == 5 && c->batch5))) {
-        if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
-        for (size_t s0 = 0; s0 < n; s0 += 32) {
-            const int S = (int)std::min<size_t>(32, n - s0);
-            conv_bsgs_batch(c, cts + s0, S, ly, approach, outs + s0);
+        if (approach >= 3) ensure_bsgs(c, ly, approach);  // host encoding + sync: never inside a capture
+        std::vector<const void*> key{ly, (const void*)(uintptr_t)approach, (const void*)(uintptr_t)n};
+        for (size_t s = 0; s < n; ++s) {
+            key.push_back(cts[s]->d);
+            key.push_back(outs[s]->d);
         }
+        auto replay_host_state = [&](const fhe_ctx::GraphEntry& g) {
+            fhe_ledger& lg = c->ledger;
+            uint64_t* dst = reinterpret_cast<uint64_t*>(&lg);
+            const uint64_t* del = reinterpret_cast<const uint64_t*>(&g.delta);
+            for (size_t f = 0; f < sizeof(fhe_ledger) / sizeof(uint64_t); ++f) dst[f] += del[f];
+            note_launch((int)g.launches);
+            for (size_t s = 0; s < n; ++s) {
+                outs[s]->scale = (cts[s]->scale * (double)c->primes[ly->level]) / (double)c->primes[ly->level];
+                outs[s]->depth = cts[s]->depth + 1;
+                lg.max_depth_consumed = std::max<uint64_t>(lg.max_depth_consumed, outs[s]->depth);
+            }
+        };
+        for (auto& g : c->graphs)
+            if (g.key == key) {
+                ck(cudaGraphLaunch(g.exec, c->st), "cudaGraphLaunch");
+                g.last_use = ++c->graph_clock;
+                replay_host_state(g);
+                return;
+            }
+        // capture once: kernels, copies and stream-ordered allocations become graph nodes
+        const fhe_ledger before = c->ledger;
+        const uint64_t l0 = launches_total();
+        cudaGraph_t graph = nullptr;
+        ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        try {
+            body();
+        } catch (...) {
+            cudaStreamEndCapture(c->st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        ck(cudaStreamEndCapture(c->st, &graph), "cudaStreamEndCapture");
+        fhe_ctx::GraphEntry g;
+        g.key = key;
+        ck(cudaGraphInstantiate(&g.exec, graph, 0), "cudaGraphInstantiate");
+        cudaGraphDestroy(graph);
+        g.launches = launches_total() - l0;
+        {
+            uint64_t* d = reinterpret_cast<uint64_t*>(&g.delta);
+            const uint64_t* a = reinterpret_cast<const uint64_t*>(&c->ledger);
+            const uint64_t* b = reinterpret_cast<const uint64_t*>(&before);
+            for (size_t f = 0; f < sizeof(fhe_ledger) / sizeof(uint64_t); ++f) d[f] = a[f] - b[f];
+            g.delta.max_depth_consumed = 0;  // a maximum, re-applied by replay_host_state
+            g.delta.distinct_amounts = 0;
+        }
+        ck(cudaGraphLaunch(g.exec, c->st), "cudaGraphLaunch");
+        g.last_use = ++c->graph_clock;
+        if (c->graphs.size() >= 16) {  // evict the least recently used graph
+            auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                        [](const auto& x, const auto& y) { return x.last_use < y.last_use; });
+            ck(cudaStreamSynchronize(c->st), "sync");
+            cudaGraphExecDestroy(lru->exec);
+            c->graphs.erase(lru);
+        }
+        c->graphs.push_back(std::move(g));
         return;
     }
     if (approach >= 3) ensure_bsgs(c, ly, approach);  // layer constants are built on the main stream
@@ -1360,6 +1439,7 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
         }
         if (const char* e = std::getenv("FHECONV_BATCH_FUSED")) c->fused_batch = std::atoi(e) != 0;
         if (const char* e = std::getenv("FHECONV_BATCH5")) c->batch5 = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FHECONV_GRAPHS")) c->use_graphs = std::atoi(e) != 0;
         cudaMemPool_t pool;
         ck(cudaDeviceGetDefaultMemPool(&pool, c->device), "mempool");
         uint64_t thresh = ~0ULL;
@@ -1417,6 +1497,8 @@ void fhe_ctx_destroy(fhe_ctx* c) {
             cudaStreamDestroy(x);
         }
     host_pipe_free(c);
+    for (auto& g : c->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     for (int b = 0; b < 2; ++b)
         for (cudaEvent_t e : {c->hp.ev_h2d[b], c->hp.ev_comp[b], c->hp.ev_d2h[b]})
             if (e) cudaEventDestroy(e);

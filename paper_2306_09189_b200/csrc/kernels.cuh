@@ -113,6 +113,7 @@ struct NttFuse {
 // --------------------------------------------------------------- launchers
 // total number of kernels enqueued by this library (for the bench's gpu_launches)
 uint64_t launches_total();
+void note_launch(int n);
 
 // All launchers enqueue on `st` and never synchronise.
 void ntt_forward(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);

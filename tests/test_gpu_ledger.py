@@ -101,3 +101,28 @@ def test_cxx_engine_demo_runs():
                     f"-Wl,-rpath,{os.path.join(root, 'paper_2306_09189_b200')}"], check=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_graph_replay_keeps_ledger_and_results(ctx, oracle):
+    """batched convs are captured into a CUDA graph once and replayed; the replay re-applies
+    the capture's ledger counters and produces the same residues."""
+    img, filt = oracle.make_inputs(4, 32, 3, 4, 1000, 2000, 0)
+    layer = ctx.conv_layer(4, 4, 32, 3, filt)
+    ctx.gen_galois_keys(layer.steps())
+    cts = [ctx.encrypt(ctx.encode(np.roll(img, i)), 9000 + i) for i in range(3)]
+    outs = [ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1) for _ in range(3)]
+    deltas, results = [], []
+    for _ in range(3):  # capture, replay, replay
+        ctx.ledger_reset()
+        ctx.conv2d_batch_into(cts, layer, 5, outs)
+        lg = ctx.ledger()
+        deltas.append({k: lg[k] for k in ("rotations", "hoisted_rotations", "ct_pt_mults", "key_switches", "modups",
+                                          "moddowns", "rescales", "kernel_launches")})
+        results.append([o.residues() for o in outs])
+    launches = [d.pop("kernel_launches") for d in deltas]
+    assert deltas[0] == deltas[1] == deltas[2] and deltas[0]["key_switches"] > 0
+    # the first call also encodes the layer's rotated plaintexts (one-time setup)
+    assert launches[1] == launches[2] > 0 and launches[0] >= launches[1]
+    for r in results[1:]:
+        for a, b in zip(results[0], r):
+            assert np.array_equal(a, b)
