@@ -1288,12 +1288,14 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
     if (approach == 0) approach = auto_orient(ly);
     const bool paper_batch = (approach == 1 || approach == 2) && n > 1 && c->batch5;
     const bool bsgs_batch = approach >= 3 && n > 1 && (c->fused_batch || (approach == 5 && c->batch5));
-    if (paper_batch || bsgs_batch) {
+    if (paper_batch || bsgs_batch || n == 1) {
         if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
         for (size_t s = 0; s < n; ++s)
             if (outs[s]->level != ly->level - 1) fail(FHE_E_INVALID, "output level must be input level - 1");
         auto body = [&] {
-            if (paper_batch) {
+            if (n == 1) {
+                conv_impl(c, cts[0], ly, approach, outs[0]);
+            } else if (paper_batch) {
                 for (size_t s0 = 0; s0 < n; s0 += 8)
                     conv_paper_batch(c, cts + s0, (int)std::min<size_t>(8, n - s0), ly, approach, outs + s0);
             } else {
@@ -2148,7 +2150,7 @@ int fhe_conv_layer_steps(const fhe_conv_layer* ly, int approach, int64_t* steps,
 }
 
 int fhe_conv2d_into(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct* out) {
-    return guard(c, [&] { conv_impl(c, ct, ly, approach, out); });
+    return guard(c, [&] { batch_impl(c, &ct, 1, ly, approach, &out); });
 }
 
 int fhe_conv2d(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct** out) {
