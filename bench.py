@@ -549,6 +549,7 @@ def _ref_inputs():
 def cpu_baseline(args, seconds=10.0):
     """The reference's own CPU path (conv_plan ShiftFirst on the shardnn
     emulator, compiled unmodified) on all host cores, bounded to ~10 s."""
+    import ctypes as C
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
         po, img, filt = _ref_inputs()
@@ -564,12 +565,35 @@ def cpu_baseline(args, seconds=10.0):
         out = {"value": round(iters * threads / dt, 2), "unit": "conv/s", "cores": threads, "kind": "reference",
                "sample": f"{iters * threads} conv_plan(ShiftFirst) runs at cfg3 geometry on {threads} independent "
                          f"shardnn Engines ({dt:.1f} s); reference emulator, no cryptography",
-               "single_thread_conv_per_s": round(1.0 / t1, 2)}
+               "single_thread_conv_per_s": round(1.0 / t1, 2), "cpu_model": _cpu_model()}
+        # Approach 1 (ChannelFirst) on the same cores, a shorter sample
+        t1a = R.ref_time_conv(C_IN, M, KAPPA, C_OUT, ip, fp, 1, C_IN * M * M, 1, 1)
+        it1 = max(1, int(seconds / 3 / max(t1a, 1e-4)))
+        dt1 = R.ref_time_conv(C_IN, M, KAPPA, C_OUT, ip, fp, 1, C_IN * M * M, it1, threads)
+        out["approach1_conv_per_s"] = round(it1 * threads / dt1, 2)
+        # BASELINE cfg2 on the reference: execute_schedule of amounts 1..127, s = 8192
+        kp = (C.c_uint64 * 1)()
+        for strat, name in ((0, "positive"), (1, "signed")):
+            tr = R.ref_time_rotations(8192, strat, 127, 1, 1, kp)
+            vec = max(1, int(seconds / 6 / max(tr, 1e-4)))
+            dtr = R.ref_time_rotations(8192, strat, 127, vec, threads, kp)
+            out[f"cfg2_{name}_requested_rot_per_s"] = round(127 * vec * threads / dtr, 1)
+            out[f"cfg2_{name}_keyed_per_vector"] = int(kp[0])
         if not args.no_golden:
             out["golden_ckks"] = golden_ckks_baseline()
         return out
     except Exception as e:  # the baseline must never hide the GPU line
         return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def golden_ckks_baseline():
