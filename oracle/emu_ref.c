@@ -116,6 +116,106 @@ int emu_conv_slots(int c, int m, int kappa, int c_out, size_t s, const double* i
     return 0;
 }
 
+/* Multi-shard image-mode geometry (conv.cpp:37-67 with t >= 2, d = 1,
+ * rep = 1, tau = identity): shard u holds channels [u z, (u+1) z),
+ *   in_channel(u, r, b) = u z + (b + r) % z,  out_channel(v, b) = (v z + b) % c_out. */
+int emu_fused_plain_ms(int c, int m, int kappa, int c_out, size_t s, const double* filt, int v, int u,
+                       int r, long kk, long ll, double scale, double* plain) {
+    const size_t block = (size_t)m * m;
+    const size_t z = s / block;
+    int any = 0;
+    (void)c;
+    for (size_t i = 0; i < s; i++) plain[i] = 0.0;
+    for (size_t b = 0; b < z; b++) {
+        const int in_ch = (int)((size_t)u * z + (b + (size_t)r) % z);
+        const int out_ch = (int)(((size_t)v * z + b) % (size_t)c_out);
+        const double w = filt_centered(filt, c_out, kappa, in_ch, out_ch, kk, ll) * scale;
+        if (w == 0.0) continue;
+        any = 1;
+        const long i_lo = kk < 0 ? -kk : 0, i_hi = kk > 0 ? m - kk : m;
+        const long j_lo = ll < 0 ? -ll : 0, j_hi = ll > 0 ? m - ll : m;
+        for (long i = i_lo; i < i_hi; i++)
+            for (long j = j_lo; j < j_hi; j++) plain[b * block + (size_t)(i * m + j)] = w;
+    }
+    return any;
+}
+
+/* conv_image_shards (conv.cpp:261-264 -> conv_image_mode, plan = nullopt,
+ * conv.cpp:146-199 without hoisting): t = c m^2 / s input shards, n_out =
+ * c_out m^2 / s output shards (c_out > z) or 1. out = [n_out][s]. */
+int emu_conv_shards_slots(int c, int m, int kappa, int c_out, size_t s, const double* img, const double* filt,
+                          double* out) {
+    const size_t block = (size_t)m * m;
+    if (s % block || (size_t)c * block < s) return -1; /* image mode without duplication (d = 1) */
+    const size_t z = s / block, t = (size_t)c * block / s;
+    const size_t n_out = (size_t)c_out <= z ? 1 : (size_t)c_out / z;
+    const long h = kappa / 2;
+    const int nk = (int)((2 * h + 1) * (2 * h + 1));
+    double* acc = calloc(n_out * s, sizeof(double));
+    int* have_acc = calloc(n_out, sizeof(int));
+    double* partial = malloc(n_out * s * sizeof(double));
+    int* have_partial = malloc(n_out * sizeof(int));
+    double* x = malloc(s * sizeof(double));
+    double* y = malloc(s * sizeof(double));
+    double* plains = malloc(n_out * (size_t)nk * s * sizeof(double));
+    int* nonempty = malloc(n_out * (size_t)nk * sizeof(int));
+    for (size_t u = 0; u < t; u++) {
+        const double* src = img + u * s; /* pack(): shard u = flat slots [u s, (u+1) s) */
+        for (size_t r = 0; r < z; r++) {
+            int any = 0;
+            for (size_t v = 0; v < n_out; v++) {
+                int idx = 0;
+                for (long kk = -h; kk <= h; kk++)
+                    for (long ll = -h; ll <= h; ll++, idx++) {
+                        nonempty[v * nk + idx] = emu_fused_plain_ms(c, m, kappa, c_out, s, filt, (int)v, (int)u,
+                                                                    (int)r, kk, ll, 1.0,
+                                                                    plains + (v * nk + idx) * s);
+                        any |= nonempty[v * nk + idx];
+                    }
+            }
+            if (!any) continue;                       /* conv.cpp:172 */
+            emu_rotate(src, x, s, (long)(r * block)); /* conv.cpp:174 */
+            for (size_t v = 0; v < n_out; v++) have_partial[v] = 0;
+            int idx = 0;
+            for (long kk = -h; kk <= h; kk++)
+                for (long ll = -h; ll <= h; ll++, idx++) {
+                    int rotated = 0;
+                    for (size_t v = 0; v < n_out; v++) {
+                        if (!nonempty[v * nk + idx]) continue;
+                        if (!rotated) {
+                            emu_rotate(x, y, s, kk * m + ll); /* conv.cpp:192 */
+                            rotated = 1;
+                        }
+                        const double* p = plains + (v * nk + idx) * s;
+                        double* pv = partial + v * s;
+                        if (!have_partial[v]) {
+                            for (size_t i = 0; i < s; i++) pv[i] = y[i] * p[i];
+                            have_partial[v] = 1;
+                        } else {
+                            for (size_t i = 0; i < s; i++) pv[i] = pv[i] + y[i] * p[i];
+                        }
+                    }
+                }
+            for (size_t v = 0; v < n_out; v++) {
+                if (!have_partial[v]) continue;
+                double* av = acc + v * s;
+                if (!have_acc[v]) {
+                    memcpy(av, partial + v * s, s * sizeof(double));
+                    have_acc[v] = 1;
+                } else {
+                    for (size_t i = 0; i < s; i++) av[i] = av[i] + partial[v * s + i];
+                }
+            }
+        }
+    }
+    for (size_t v = 0; v < n_out; v++)
+        if (!have_acc[v]) /* Acc::finish zero product against shard 0 */
+            for (size_t i = 0; i < s; i++) acc[v * s + i] = img[i] * 0.0;
+    memcpy(out, acc, n_out * s * sizeof(double));
+    free(acc); free(have_acc); free(partial); free(have_partial); free(x); free(y); free(plains); free(nonempty);
+    return (int)n_out;
+}
+
 void emu_oracle_conv(int c, int m, int kappa, int c_out, const double* img, const double* filt,
                      double* out) { /* oracle.cpp:7-31, stride 1 */
     const long h = kappa / 2;

@@ -44,6 +44,13 @@ int emu_fused_plain(int c, int m, int kappa, int c_out, size_t s, const double* 
  * 2 ShiftFirst (paper Approach 2). out has s slots. */
 int emu_conv_slots(int c, int m, int kappa, int c_out, size_t s, const double* img,
                    const double* filt, int plan, double* out);
+/* multi-shard image mode (conv.cpp:37-67, 146-199 with t >= 2): the fused
+ * plaintext of output shard v vs rotation r of input shard u, and the full
+ * conv_image_shards slots; returns the output shard count n_out */
+int emu_fused_plain_ms(int c, int m, int kappa, int c_out, size_t s, const double* filt, int v, int u,
+                       int r, long kk, long ll, double scale, double* plain);
+int emu_conv_shards_slots(int c, int m, int kappa, int c_out, size_t s, const double* img, const double* filt,
+                          double* out);
 
 /* Textbook same-padding cross-correlation, stride 1 (oracle.cpp:7-31). */
 void emu_oracle_conv(int c, int m, int kappa, int c_out, const double* img, const double* filt,

@@ -93,6 +93,9 @@ def lib():
         L.emu_conv_slots.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, dp, dp,
                                      C.c_int, dp]
         L.emu_oracle_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, dp]
+        L.emu_fused_plain_ms.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, dp, C.c_int, C.c_int,
+                                         C.c_int, C.c_long, C.c_long, C.c_double, dp]
+        L.emu_conv_shards_slots.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, dp, dp, dp]
         L.emu_decompose.argtypes = [C.c_int, C.c_uint64, C.c_uint64, lp, C.c_int]
         L.emu_min_lengths.argtypes = [C.c_uint64, C.c_uint64, u64p]
         _lib = L
@@ -145,6 +148,17 @@ def emu_conv_slots(c, m, kappa, c_out, s, img, filt, plan):
     return out
 
 
+def emu_conv_shards_slots(c, m, kappa, c_out, s, img, filt):
+    """conv_image_shards slots ([n_out][s]) of a multi-shard image (t = c m^2 / s shards)."""
+    z = s // (m * m)
+    n_out = 1 if c_out <= z else c_out // z
+    out = np.zeros(n_out * s)
+    rc = lib().emu_conv_shards_slots(c, m, kappa, c_out, s, _ptr(np.ascontiguousarray(img, dtype=np.float64), dp),
+                                     _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), _ptr(out, dp))
+    assert rc == n_out, rc
+    return out.reshape(n_out, s)
+
+
 def emu_oracle_conv(c, m, kappa, c_out, img, filt):
     out = np.zeros(c_out * m * m)
     lib().emu_oracle_conv(c, m, kappa, c_out, _ptr(np.ascontiguousarray(img), dp),
@@ -182,6 +196,20 @@ def ref_conv(c, m, kappa, c_out, img, filt, plan, s):
                         _ptr(out_img, dp), _ptr(ledger, u64p), C.byref(drop))
     assert rc == 0
     return out_slots, out_img, ledger, drop.value
+
+
+def ref_conv_shards(c, m, kappa, c_out, img, filt, s):
+    """the reference's convolve() on a multi-shard image: conv_image_shards slots [n_out][s]."""
+    z = s // (m * m)
+    n_out = 1 if c_out <= z else c_out // z
+    out_slots = np.zeros(n_out * s)
+    out_img = np.zeros(c_out * m * m)
+    ledger = np.zeros(9, dtype=np.uint64)
+    drop = C.c_int(0)
+    rc = ref().ref_conv(c, m, kappa, c_out, _ptr(np.ascontiguousarray(img), dp), _ptr(np.ascontiguousarray(filt), dp),
+                        0, s, _ptr(out_slots, dp), _ptr(out_img, dp), _ptr(ledger, u64p), C.byref(drop))
+    assert rc == 0
+    return out_slots.reshape(n_out, s), out_img, ledger, drop.value
 
 
 # ---------------------------------------------------------------- CKKS model

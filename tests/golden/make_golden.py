@@ -30,6 +30,14 @@ CONV_CASES = {
     "small_dup_c2m4k3": (2, 4, 3, 2, 35, 135, 0, 64),
 }
 CFG5 = dict(c=16, m=32, kappa=3, seed_img=1003, seed_filts=(2003, 2004, 2005), weight_kind=1, s=16384)
+# multi-shard image mode (conv_image_shards conv.cpp:261-264): t = c m^2 / s input
+# shards, n_out = c_out m^2 / s output shards
+MS_CASES = {
+    "ms_cfg1_c8": (8, 32, 3, 8, 1010, 2010, 0, 4096),       # t = 2, n_out = 2
+    "ms_cfg1_c8to4": (8, 32, 3, 4, 1011, 2011, 0, 4096),    # t = 2, n_out = 1
+    "ms_cfg1_c4to8": (4, 32, 3, 8, 1012, 2012, 0, 4096),    # t = 1, n_out = 2
+    "ms_cfg3_c32": (32, 32, 3, 32, 1013, 2013, 0, 16384),   # t = 2, n_out = 2
+}
 
 
 def main():
@@ -58,6 +66,13 @@ def main():
         for plan in (0, 1, 2):
             out[f"{name}/ledger{plan}"] = res[plan][2]
         out[f"{name}/level_drop"] = np.array([res[2][3]])
+    for name, (c, m, k, co, si, sf, wk, s) in MS_CASES.items():
+        img, filt = po.make_inputs(c, m, k, co, si, sf, wk, use_ref=True)
+        slots, image, ledger, drop = po.ref_conv_shards(c, m, k, co, img, filt, s)
+        out[f"{name}/params"] = np.array([c, m, k, co, si, sf, wk, s], dtype=np.int64)
+        out[f"{name}/img_sum"] = np.array([img.sum(), np.abs(img).sum()])
+        out[f"{name}/slots"] = slots
+        out[f"{name}/ledger"] = ledger
     # cfg5: three stacked layers, each input = previous output image
     x, _ = po.make_inputs(CFG5["c"], CFG5["m"], CFG5["kappa"], CFG5["c"], CFG5["seed_img"], 0, 0, use_ref=True)
     out["cfg5/img_sum"] = np.array([x.sum(), np.abs(x).sum()])

@@ -119,3 +119,17 @@ def test_live_reference_if_built(oracle, golden):
     slots, _, ledger, drop = oracle.ref_conv(c, m, k, co, img, filt, 2, s)
     assert np.array_equal(slots, golden["cfg1/slots"])
     assert np.array_equal(ledger, golden["cfg1/ledger2"]) and drop == 1
+
+
+@pytest.mark.parametrize("name", ["ms_cfg1_c8", "ms_cfg1_c8to4", "ms_cfg1_c4to8", "ms_cfg3_c32"])
+def test_multishard_restatement_bit_exact(oracle, golden, name):
+    """emu_conv_shards_slots (conv_image_mode with t input shards / n_out output shards,
+    SURVEY §8(f) 1) == the reference's conv_image_shards slots, bit for bit."""
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    assert np.isclose(img.sum(), golden[f"{name}/img_sum"][0])
+    got = oracle.emu_conv_shards_slots(c, m, k, co, s, img, filt)
+    assert np.array_equal(got, golden[f"{name}/slots"])
+    # and it is the textbook same-padding conv of the image
+    want = oracle.emu_oracle_conv(c, m, k, co, img, filt)
+    assert np.abs(got.ravel()[: co * m * m] - want).max() < 1e-12
