@@ -1062,6 +1062,117 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
     return 0;
 }
 
+/* Multi-shard image-mode conv (slots as conv_image_shards,
+ * conv.cpp:146-199 with t input shards, n_out output shards) through the
+ * fused BSGS schedule: for output shard v,
+ *   Y_{v,kk} = sum_u sum_(r, ll) rot_{-kk m}(pt(v, u, r, kk, ll)) * X~_{u, r m^2 + ll},
+ *   out_v    = Rescale(ModDown(Y_{v,0} + sum_{kk != 0} KS_{kk m}(Y_{v,kk}))),
+ * X~ the QP-basis key switch of input shard u (P sigma(c0) folded in), the
+ * giant steps as in conv_bsgs. cts = [t][2][level+1][N], outs = [n_out][2][level][N]. */
+int ck_conv_shards(const ck_ctx* ck, const uint64_t* cts, int t, int level, int c, int m, int kappa, int c_out,
+                   const double* filt, uint64_t* outs, double* out_scale) {
+    const size_t N = ck->N, s = N / 2, block = (size_t)m * m;
+    if (s % block || (size_t)c * block != (size_t)t * s || level < 1) return -1;
+    const size_t z = s / block;
+    const int n_out = (size_t)c_out <= z ? 1 : (int)((size_t)c_out / z);
+    const int nr = level + 1, ne = nr + ck->K, dn = ck_dnum_at(ck, level);
+    const long h = kappa / 2;
+    const int kap = (int)(2 * h + 1);
+    const size_t extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, octw = (size_t)2 * level * N;
+    const uint64_t ql = ck->q[level];
+    uint64_t Pmod[CK_MAXP];
+    for (int u = 0; u < ne; u++) {
+        const uint64_t q = ck->q[ext_prime(ck, level, u)];
+        uint64_t P = 1;
+        for (int k = 0; k < ck->K; k++) P = ck_mulmod(P, ck->q[ck->L + k] % q, q);
+        Pmod[u] = u < nr ? P : 0;
+    }
+    key_cache kc = {.n = 0};
+    uint64_t* dsrc = malloc((size_t)t * dn * extw * 8);
+    for (int u = 0; u < t; u++)
+        ck_modup(ck, cts + (size_t)u * ctw + (size_t)nr * N, level, dsrc + (size_t)u * dn * extw);
+    uint64_t* ip0 = malloc(extw * 8);
+    uint64_t* ip1 = malloc(extw * 8);
+    uint64_t* Y = calloc((size_t)n_out * kap * 2 * extw, 8); /* [v][kk][2][ne][N] */
+    int* nonempty_g = calloc((size_t)n_out * kap, sizeof(int));
+    double* plain = malloc(s * sizeof(double));
+    double* rplain = malloc(s * sizeof(double));
+    uint64_t* pt = malloc(extw * 8);
+    for (int u = 0; u < t; u++)
+        for (size_t r = 0; r < z; r++)
+            for (long ll = -h; ll <= h; ll++) {
+                const long bamt = (long)(r * block) + ll;
+                const uint64_t g = ck_galois_elt(ck, bamt);
+                int have_ip = 0;
+                for (int v = 0; v < n_out; v++)
+                    for (long kk = -h; kk <= h; kk++) {
+                        if (!emu_fused_plain_ms(c, m, kappa, c_out, s, filt, v, u, (int)r, kk, ll, 1.0, plain))
+                            continue;
+                        if (g != 1 && !have_ip) {
+                            ck_inner_product(ck, dsrc + (size_t)u * dn * extw, level, cache_get(ck, &kc, g), g, ip0,
+                                             ip1);
+                            have_ip = 1;
+                        }
+                        emu_rotate(plain, rplain, s, -kk * m);
+                        ck_encode_plain(ck, rplain, s, (double)ql, level, 1, pt);
+                        uint64_t* y = Y + ((size_t)v * kap + (size_t)(kk + h)) * 2 * extw;
+                        nonempty_g[v * kap + (kk + h)] = 1;
+                        if (g == 1)
+                            conv_accumulate(ck, level, pt, cts + (size_t)u * ctw, 1, NULL, NULL, Pmod, y, y + extw);
+                        else
+                            conv_accumulate(ck, level, pt, cts + (size_t)u * ctw, g, ip0, ip1, Pmod, y, y + extw);
+                    }
+            }
+    free(plain);
+    free(rplain);
+    free(pt);
+    uint64_t* acc0 = malloc(extw * 8);
+    uint64_t* acc1 = malloc(extw * 8);
+    uint64_t* yq = malloc(ctw * 8);
+    uint64_t* perm = malloc(extw * 8);
+    uint64_t* dg = malloc((size_t)dn * extw * 8);
+    uint64_t* md = malloc(ctw * 8);
+    for (int v = 0; v < n_out; v++) {
+        memset(acc0, 0, extw * 8);
+        memset(acc1, 0, extw * 8);
+        for (long kk = -h; kk <= h; kk++) {
+            if (!nonempty_g[v * kap + (kk + h)]) continue;
+            const uint64_t* y = Y + ((size_t)v * kap + (size_t)(kk + h)) * 2 * extw;
+            const uint64_t g = ck_galois_elt(ck, kk * m);
+            if (g == 1) {
+                for (int u = 0; u < ne; u++) {
+                    const uint64_t q = ck->q[ext_prime(ck, level, u)];
+                    for (size_t k = 0; k < N; k++) {
+                        acc0[(size_t)u * N + k] = addm(acc0[(size_t)u * N + k], y[(size_t)u * N + k], q);
+                        acc1[(size_t)u * N + k] = addm(acc1[(size_t)u * N + k], y[extw + (size_t)u * N + k], q);
+                    }
+                }
+                continue;
+            }
+            ck_moddown(ck, y + extw, level, yq + (size_t)nr * N);
+            ck_modup(ck, yq + (size_t)nr * N, level, dg);
+            ck_inner_product(ck, dg, level, cache_get(ck, &kc, g), g, ip0, ip1);
+            for (int u = 0; u < ne; u++) ck_automorph_ntt(ck, y + (size_t)u * N, perm + (size_t)u * N, g);
+            for (int u = 0; u < ne; u++) {
+                const uint64_t q = ck->q[ext_prime(ck, level, u)];
+                for (size_t k = 0; k < N; k++) {
+                    const uint64_t t0 = addm(ip0[(size_t)u * N + k], perm[(size_t)u * N + k], q);
+                    acc0[(size_t)u * N + k] = addm(acc0[(size_t)u * N + k], t0, q);
+                    acc1[(size_t)u * N + k] = addm(acc1[(size_t)u * N + k], ip1[(size_t)u * N + k], q);
+                }
+            }
+        }
+        ck_moddown(ck, acc0, level, md);
+        ck_moddown(ck, acc1, level, md + (size_t)nr * N);
+        ck_rescale(ck, md, level, outs + (size_t)v * octw);
+    }
+    if (out_scale) *out_scale = (ck->scale * (double)ql) / (double)ql;
+    cache_free(&kc);
+    free(dsrc); free(ip0); free(ip1); free(Y); free(nonempty_g);
+    free(acc0); free(acc1); free(yq); free(perm); free(dg); free(md);
+    return n_out;
+}
+
 int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,
             const double* filt, int plan, uint64_t* out, double* out_scale) {
     const size_t N = ck->N, s = N / 2, block = (size_t)m * m;

@@ -100,6 +100,11 @@ void ck_rotate_hoisted(const ck_ctx* ck, const uint64_t* ct, int level, const lo
 int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,
             const double* filt, int plan, uint64_t* out, double* out_scale);
 
+/* Multi-shard image-mode conv (fused BSGS, see ckks_ref.c): t input shards
+ * [t][2][level+1][N] -> n_out output shards [n_out][2][level][N]; returns n_out. */
+int ck_conv_shards(const ck_ctx* ck, const uint64_t* cts, int t, int level, int c, int m, int kappa, int c_out,
+                   const double* filt, uint64_t* outs, double* out_scale);
+
 #ifdef __cplusplus
 }
 #endif

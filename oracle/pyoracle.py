@@ -85,6 +85,8 @@ def lib():
         L.ck_rotate_hoisted.argtypes = [C.c_void_p, u64p, C.c_int, lp, C.c_int, u64p]
         L.ck_conv.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp,
                               C.c_int, u64p, dp]
+        L.ck_conv_shards.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp,
+                                     u64p, dp]
         L.emu_make_inputs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
                                       C.c_int, dp, dp]
         L.emu_rotate.argtypes = [dp, dp, C.c_size_t, C.c_long]
@@ -346,4 +348,18 @@ class CKKS:
                            _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), plan, _ptr(out, u64p),
                            C.byref(sc))
         assert rc == 0
+        return out, sc.value
+
+    def conv_shards(self, cts, level, c, m, kappa, c_out, filt):
+        """multi-shard image-mode conv: cts [t][2][level+1][N] -> [n_out][2][level][N]."""
+        cts = np.ascontiguousarray(cts, dtype=np.uint64)
+        t = cts.shape[0]
+        z = (self.N // 2) // (m * m)
+        n_out = 1 if c_out <= z else c_out // z
+        out = np.zeros((n_out, 2, level, self.N), dtype=np.uint64)
+        sc = C.c_double(0)
+        rc = lib().ck_conv_shards(self.h, _ptr(cts, u64p), t, level, c, m, kappa, c_out,
+                                  _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), _ptr(out, u64p),
+                                  C.byref(sc))
+        assert rc == n_out, rc
         return out, sc.value

@@ -158,3 +158,16 @@ def test_conv_cfg1_decrypts_to_reference(cfg1, oracle, golden, plan):
     assert sc == cfg1.scale
     err = np.abs(cfg1.decrypt(out, 3, sc) - golden["cfg1/slots"]).max()
     assert err < 1e-6, err
+
+
+@pytest.mark.parametrize("name", ["ms_cfg1_c8", "ms_cfg1_c8to4", "ms_cfg1_c4to8"])
+def test_multishard_conv_decrypts_to_reference(cfg1, oracle, golden, name):
+    """the golden model's multi-shard conv (fused BSGS over t input / n_out output shards)
+    decrypts to the reference's conv_image_shards slots, <= 1e-6."""
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    t = c * m * m // s
+    cts = np.stack([cfg1.encrypt(cfg1.encode(img[u * s:(u + 1) * s], cfg1.scale, 4), 4, 9000 + u) for u in range(t)])
+    out, sc = cfg1.conv_shards(cts, 4, c, m, k, co, filt)
+    dec = np.stack([cfg1.decrypt(out[v], 3, sc) for v in range(out.shape[0])])
+    assert np.abs(dec - golden[f"{name}/slots"]).max() < 1e-6
