@@ -176,6 +176,20 @@ int fhe_decompose(int strategy, uint64_t n, uint64_t s, int64_t* steps, int cap)
 int fhe_conv_layer_create(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
                           int level, fhe_conv_layer** out);
 void fhe_conv_layer_free(fhe_conv_layer* layer);
+/* multi-shard image mode (reference conv_image_shards, conv.cpp:261-264 via
+ * conv_image_mode with t >= 2): an image of c_in channels
+ * with c_in m^2 = t * slots is packed into t ciphertexts (shard u = channels
+ * [u z, (u+1) z), z = slots / m^2, as pack() does); the c_out output channels
+ * land in n_out = max(1, c_out / z) ciphertexts (shard v block b = channel
+ * (v z + b) mod c_out). Runs the fused BSGS schedule. */
+int fhe_conv_layer_create_shards(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
+                                 int level, fhe_conv_layer** out);
+/* input / output shard counts of a layer (1 / 1 for single-shard layers) */
+int fhe_conv_layer_shards(const fhe_conv_layer* layer, int* t, int* n_out);
+/* n_images multi-shard convs: in = [n_images][t] ciphertexts at the layer level,
+ * outs = [n_images][n_out] preallocated ciphertexts at level - 1 */
+int fhe_conv2d_shards_into(fhe_ctx* ctx, const fhe_ct* const* in, size_t n_images, const fhe_conv_layer* layer,
+                           fhe_ct* const* outs);
 /* Galois steps a layer needs for `approach`: 1-4 channel rotations r m^2 and
  * shifts kk m + ll; 5 r m^2 + ll and kk m; 0 the union (any approach runs) */
 int fhe_conv_layer_steps(const fhe_conv_layer* layer, int approach, int64_t* steps, size_t cap, size_t* n);

@@ -227,6 +227,13 @@ struct fhe_conv_layer {
         std::vector<int> nonempty;  // [ngi][nb]
         uint64_t* d_pts = nullptr;  // [ngi][nb][ne][N], pt'[g][b] = rot_{-g}(pt)
     } bs[3];
+    // multi-shard image mode (fhe_conv_layer_create_shards): t input shards of z
+    // channels, n_out output shards; fused-BSGS plaintexts
+    // pt'[v][kk][b = (u, r, ll)] = rot_{-kk m}(fused_plain_ms(v, u, r, kk, ll))
+    bool ms = false;
+    int t = 1, z = 0, n_out = 1, nb_ms = 0;
+    std::vector<uint8_t> ms_nonempty;  // [n_out][kappa][nb_ms]
+    uint64_t* d_pts_ms = nullptr;
 };
 
 namespace {
@@ -528,6 +535,29 @@ bool fused_plain(int c_in, int c_out, int m, int kappa, size_t s, const double* 
     for (size_t b = 0; b < z; ++b) {
         const size_t in_ch = ((b + (size_t)r) % z) % (size_t)c_in;
         const size_t out_ch = b % (size_t)c_out;
+        const double wt =
+            w[((in_ch * c_out + out_ch) * kappa + (size_t)(kk + h)) * kappa + (size_t)(ll + h)] * 1.0;
+        if (wt == 0.0) continue;
+        any = true;
+        const long i_lo = std::max(0L, -kk), i_hi = std::min<long>(m, m - kk);
+        const long j_lo = std::max(0L, -ll), j_hi = std::min<long>(m, m - ll);
+        for (long i = i_lo; i < i_hi; ++i)
+            for (long j = j_lo; j < j_hi; ++j) plain[b * block + (size_t)(i * m + j)] = wt;
+    }
+    return any;
+}
+
+// multi-shard image mode (reference conv.cpp:37-85 with d = 1, rep = 1, tau = identity):
+//   in_channel(u, r, b) = u z + (b + r) % z,  out_channel(v, b) = (v z + b) % c_out
+bool fused_plain_ms(int c_out, int m, int kappa, size_t s, const double* w, int v, int u, int r, long kk, long ll,
+                    std::vector<double>& plain) {
+    const size_t block = (size_t)m * m, z = s / block;
+    const long h = kappa / 2;
+    plain.assign(s, 0.0);
+    bool any = false;
+    for (size_t b = 0; b < z; ++b) {
+        const size_t in_ch = (size_t)u * z + (b + (size_t)r) % z;
+        const size_t out_ch = ((size_t)v * z + b) % (size_t)c_out;
         const double wt =
             w[((in_ch * c_out + out_ch) * kappa + (size_t)(kk + h)) * kappa + (size_t)(ll + h)] * 1.0;
         if (wt == 0.0) continue;
@@ -869,6 +899,73 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
     c->release(dsrc);
 }
 
+// Giant steps and the final fused ModDown + rescale for S accumulator sets
+// Y = [S][ngi][2][ne][N] (source stride ys): giant gi of `giants` (amount
+// gamt[gi]) is key-switched as KS(Y.c1) + sigma(Y.c0) into the source's QP
+// accumulator (ModDown(Y.c1) in the coefficient domain feeding a batched
+// ModUp), the identity giant `id` is added as is; md = [S][2][level][N].
+void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, const std::vector<int>& giants,
+                   const std::vector<int64_t>& gamt, int id, uint64_t* md) {
+    const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N, dw = (size_t)dn * extw;
+    uint64_t* acc = c->alloc((size_t)S * 2 * extw);
+    ck(cudaMemsetAsync(acc, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
+    const int G = (int)giants.size();
+    if (G > 0) {
+        const int SC = std::max(1, std::min(S, 8));
+        uint64_t* yc = c->alloc((size_t)SC * G * extw);
+        uint64_t* yq = c->alloc((size_t)SC * G * nr * N);
+        uint64_t* dg = c->alloc((size_t)SC * G * dw);
+        for (int s0 = 0; s0 < S; s0 += SC) {
+            const int sc = std::min(SC, S - s0);
+            for (int s = 0; s < sc; ++s)
+                for (int gi = 0; gi < G; ++gi)
+                    ck(cudaMemcpyAsync(yc + ((size_t)s * G + gi) * extw,
+                                       Y + (size_t)(s0 + s) * ys + (size_t)giants[gi] * 2 * extw + extw, extw * 8,
+                                       cudaMemcpyDeviceToDevice, c->st),
+                       "memcpy");
+            const int np_ = sc * G;
+            c->timed("ntt", c->rows(2.0 * np_ * ne),
+                     [&] { ntt_inverse(c->dc, yc, np_ * ne, RowMap{ne, level, c->L, 0}, c->st); });
+            c->timed("moddown", c->rows((double)np_ * (ne + nr)),
+                     [&] { moddown_coef(c->dc, yq, yc, c->d_md, level, np_, c->st); });
+            c->timed("ntt_modup", c->rows((double)np_ * nr + (double)np_ * dn * ne), [&] {
+                ntt_modup_coef(c->dc, dg, yq, np_, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+            });
+            c->ledger.moddowns += np_;
+            c->ledger.modups += np_;
+            KsBatch kg{};
+            kg.nsrc = sc;
+            kg.n = G;
+            kg.digits = dg;
+            kg.digit_src_stride = (size_t)G * dw;
+            kg.digit_term_stride = dw;
+            kg.c0 = Y + (size_t)s0 * ys;
+            kg.c0_src_stride = ys;
+            kg.c0_qp = 1;
+            kg.out = acc + (size_t)s0 * 2 * extw;
+            kg.out_src_stride = 2 * extw;
+            for (int gi = 0; gi < G; ++gi) {
+                const uint32_t g = c->galois_of(c->reduce_amount(gamt[giants[gi]]));
+                kg.galois[gi] = g;
+                kg.key[gi] = c->key_for(g);
+                kg.c0_off[gi] = (size_t)giants[gi] * 2 * extw;
+            }
+            c->ledger.key_switches += (uint64_t)G * sc;
+            c->timed("ks_inner", c->rows((double)G * 2.0 * dn * ne + (double)sc * G * (dn * ne + ne) + 4.0 * ne * sc),
+                     [&] { ks_batch(c->dc, kg, 1, c->d_md, level, dn, c->st); });
+        }
+        c->release(dg);
+        c->release(yq);
+        c->release(yc);
+    }
+    if (id >= 0)
+        for (int s = 0; s < S; ++s)
+            qp_add(c->dc, acc + (size_t)s * 2 * extw, Y + (size_t)s * ys + (size_t)id * 2 * extw, level, c->st);
+    moddown_rescale(c, acc, extw, level, 2 * S, md);
+    c->release(acc);
+}
+
 // Batched BSGS conv of S ciphertexts through one layer: every key and every
 // plaintext is streamed once per batch (the lanes of a warp that share a
 // coefficient pair share the loads), ModUps/NTTs run over the whole batch.
@@ -956,63 +1053,9 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
         else
             giants.push_back(gi);
     }
-    uint64_t* acc = c->alloc((size_t)S * 2 * extw);
-    ck(cudaMemsetAsync(acc, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
-    const int G = (int)giants.size();
-    if (G > 0) {
-        const int SC = std::max(1, std::min(S, 8));
-        uint64_t* yc = c->alloc((size_t)SC * G * extw);
-        uint64_t* yq = c->alloc((size_t)SC * G * nr * N);
-        uint64_t* dg = c->alloc((size_t)SC * G * dw);
-        for (int s0 = 0; s0 < S; s0 += SC) {
-            const int sc = std::min(SC, S - s0);
-            for (int s = 0; s < sc; ++s)
-                for (int gi = 0; gi < G; ++gi)
-                    ck(cudaMemcpyAsync(yc + ((size_t)s * G + gi) * extw,
-                                       Y + (size_t)(s0 + s) * ys + (size_t)giants[gi] * 2 * extw + extw, extw * 8,
-                                       cudaMemcpyDeviceToDevice, c->st),
-                       "memcpy");
-            const int np_ = sc * G;
-            c->timed("ntt", c->rows(2.0 * np_ * ne),
-                     [&] { ntt_inverse(c->dc, yc, np_ * ne, RowMap{ne, level, c->L, 0}, c->st); });
-            c->timed("moddown", c->rows((double)np_ * (ne + nr)),
-                     [&] { moddown_coef(c->dc, yq, yc, c->d_md, level, np_, c->st); });
-            c->timed("ntt_modup", c->rows((double)np_ * nr + (double)np_ * dn * ne), [&] {
-                ntt_modup_coef(c->dc, dg, yq, np_, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
-            });
-            c->ledger.moddowns += np_;
-            c->ledger.modups += np_;
-            KsBatch kg{};
-            kg.nsrc = sc;
-            kg.n = G;
-            kg.digits = dg;
-            kg.digit_src_stride = (size_t)G * dw;
-            kg.digit_term_stride = dw;
-            kg.c0 = Y + (size_t)s0 * ys;
-            kg.c0_src_stride = ys;
-            kg.c0_qp = 1;
-            kg.out = acc + (size_t)s0 * 2 * extw;
-            kg.out_src_stride = 2 * extw;
-            for (int gi = 0; gi < G; ++gi) {
-                const uint32_t g = c->galois_of(c->reduce_amount(B.gamt[giants[gi]]));
-                kg.galois[gi] = g;
-                kg.key[gi] = c->key_for(g);
-                kg.c0_off[gi] = (size_t)giants[gi] * 2 * extw;
-            }
-            c->ledger.key_switches += (uint64_t)G * sc;
-            c->timed("ks_inner", c->rows((double)G * 2.0 * dn * ne + (double)sc * G * (dn * ne + ne) + 4.0 * ne * sc),
-                     [&] { ks_batch(c->dc, kg, 1, c->d_md, level, dn, c->st); });
-        }
-        c->release(dg);
-        c->release(yq);
-        c->release(yc);
-    }
-    if (id >= 0)
-        for (int s = 0; s < S; ++s)
-            qp_add(c->dc, acc + (size_t)s * 2 * extw, Y + (size_t)s * ys + (size_t)id * 2 * extw, level, c->st);
     const size_t otw = (size_t)2 * level * N;
     uint64_t* md = c->alloc((size_t)S * otw);
-    moddown_rescale(c, acc, extw, level, 2 * S, md);
+    giants_finish(c, Y, ys, S, level, giants, B.gamt, id, md);
     for (int s = 0; s < S; ++s) {
         ck(cudaMemcpyAsync(outs[s]->d, md + (size_t)s * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
         outs[s]->scale = (cts[s]->scale * (double)c->primes[level]) / (double)c->primes[level];
@@ -1036,7 +1079,6 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
         lg.adds += pairs ? pairs - 1 : 0;
     }
     c->release(md);
-    c->release(acc);
     c->release(Y);
     c->release(buf);
 }
@@ -1174,6 +1216,104 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
     c->release(X);
 }
 
+// Multi-shard image-mode conv of B images (B x t input shards -> B x n_out
+// output shards) through the fused BSGS schedule: babies (u, r, ll) read
+// input shard u through the fused kernel's source slots, giants kk m are
+// the row shifts, one accumulator set per (image, output shard).
+void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_layer* ly, fhe_ct* const* outs) {
+    const int level = ly->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
+    const int T = ly->t, NO = ly->n_out, kap = ly->kappa, nb = ly->nb_ms;
+    const long m = ly->m, h = kap / 2;
+    const int64_t block = (int64_t)m * m;
+    for (int i = 0; i < B * T; ++i)
+        if (in[i]->level != level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
+    for (int i = 0; i < B * NO; ++i)
+        if (outs[i]->level != level - 1) fail(FHE_E_INVALID, "output level must be input level - 1");
+    uint64_t* buf = c->alloc((size_t)B * T * ctw);
+    for (int i = 0; i < B * T; ++i)
+        ck(cudaMemcpyAsync(buf + (size_t)i * ctw, in[i]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    uint64_t* dig = c->alloc((size_t)B * T * dw);
+    modup_batch(c, buf + (size_t)nr * N, ctw, B * T, level, dig);
+    const size_t ys = (size_t)kap * 2 * extw;
+    uint64_t* Y = c->alloc((size_t)B * NO * ys);  // [B][n_out][kappa][2][ne][N]
+    ck(cudaMemsetAsync(Y, 0, (size_t)B * NO * ys * 8, c->st), "memset");
+    for (int v = 0; v < NO; ++v)
+        for (int g0 = 0; g0 < kap; g0 += 3) {
+            const int ng = std::min(3, kap - g0);
+            FusedBsgs f{};
+            f.nsrc = B;
+            f.ng = ng;
+            f.digits = dig;
+            f.digit_src_stride = (size_t)T * dw;
+            f.digit_slot_stride = dw;
+            f.ct = buf;
+            f.ct_src_stride = (size_t)T * ctw;
+            f.ct_slot_stride = ctw;
+            f.pt_g_stride = (size_t)nb * extw;
+            f.Y = Y + (size_t)v * ys + (size_t)g0 * 2 * extw;
+            f.y_src_stride = (size_t)NO * ys;
+            f.y_g_stride = 2 * extw;
+            f.accumulate = 1;
+            double keyed = 0, pts = 0;
+            auto flush = [&] {
+                if (!f.nb) return;
+                c->timed("bsgs_fused",
+                         c->rows(keyed * 2.0 * dn * ne + pts * ne + B * (T * (double)dn * ne + 2.0 * nr + 4.0 * ng * ne)),
+                         [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+                f.nb = 0;
+                keyed = pts = 0;
+            };
+            for (int b = 0; b < nb; ++b) {
+                uint32_t mask = 0;
+                for (int g = 0; g < ng; ++g)
+                    if (ly->ms_nonempty[((size_t)v * kap + g0 + g) * nb + b]) mask |= 1u << g;
+                if (!mask) continue;
+                if (f.nb == kMaxFused) flush();
+                const int u = b / (ly->z * kap), r = (b / kap) % ly->z;
+                const long ll = b % kap - h;
+                const uint32_t gal = c->galois_of(c->reduce_amount((int64_t)r * block + ll));
+                f.galois[f.nb] = gal;
+                f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+                f.gmask[f.nb] = mask;
+                f.pt[f.nb] = ly->d_pts_ms + (((size_t)v * kap + g0) * nb + b) * extw;
+                f.srcslot[f.nb] = (uint16_t)u;
+                f.nb++;
+                pts += __builtin_popcount(mask);
+                if (gal != 1) {
+                    keyed += 1;
+                    c->ledger.key_switches += B;
+                }
+            }
+            flush();
+        }
+    c->release(dig);
+    std::vector<int> giants;
+    std::vector<int64_t> gamt;
+    int id = -1;
+    for (long kk = -h; kk <= h; ++kk) {
+        gamt.push_back(kk * m);
+        if (kk == 0)
+            id = (int)(kk + h);
+        else
+            giants.push_back((int)(kk + h));
+    }
+    const size_t otw = (size_t)2 * level * N;
+    uint64_t* md = c->alloc((size_t)B * NO * otw);
+    giants_finish(c, Y, ys, B * NO, level, giants, gamt, id, md);
+    for (int i = 0; i < B * NO; ++i) {
+        ck(cudaMemcpyAsync(outs[i]->d, md + (size_t)i * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+        const fhe_ct* src = in[(i / NO) * T];
+        outs[i]->scale = (src->scale * (double)c->primes[level]) / (double)c->primes[level];
+        outs[i]->depth = src->depth + 1;
+        c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[i]->depth);
+    }
+    c->ledger.hoist_groups += (uint64_t)B * T;
+    c->release(md);
+    c->release(Y);
+    c->release(buf);
+}
+
 int auto_orient(const fhe_conv_layer* ly) {
     // giant steps each cost a ModDown + ModUp (~120 NTT rows at cfg3) while a
     // fused baby step costs one key stream: the fused schedule (kappa giant
@@ -1184,6 +1324,7 @@ int auto_orient(const fhe_conv_layer* ly) {
 }
 
 void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct* out) {
+    if (ly->ms) fail(FHE_E_INVALID, "multi-shard layer: use fhe_conv2d_shards_into");
     if (approach < 0 || approach > 5) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3, 4 or 5");
     if (approach == 0) approach = auto_orient(ly);
     if (approach >= 3) {
@@ -1284,6 +1425,7 @@ void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
 void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_layer* ly, int approach,
                 fhe_ct* const* outs) {
     if (n == 0) return;
+    if (ly->ms) fail(FHE_E_INVALID, "multi-shard layer: use fhe_conv2d_shards_into");
     if (approach < 0 || approach > 5) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3, 4 or 5");
     if (approach == 0) approach = auto_orient(ly);
     const bool paper_batch = (approach == 1 || approach == 2) && n > 1 && c->batch5;
@@ -2115,9 +2257,82 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
     if (!ly) return;
     cudaStreamSynchronize(ly->ctx->st);
     cudaFree(ly->d_pts);
+    if (ly->d_pts_ms) cudaFree(ly->d_pts_ms);
     for (auto& b : ly->bs)
         if (b.d_pts) cudaFree(b.d_pts);
     delete ly;
+}
+
+int fhe_conv_layer_create_shards(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights, int level,
+                                 fhe_conv_layer** out) {
+    return guard(c, [&] {
+        if (kappa % 2 == 0) fail(FHE_E_INVALID, "kernel size must be odd");
+        if (c_out <= 0 || (c_out & (c_out - 1))) fail(FHE_E_INVALID, "output channel count must be a power of two");
+        if (c_in <= 0 || (c_in & (c_in - 1))) fail(FHE_E_INVALID, "channel count must be a power of two");
+        const size_t s = c->slots(), block = (size_t)m * m;
+        if (m <= 0 || (m & (m - 1)) || block > s) fail(FHE_E_INVALID, "channel side must be a power of two");
+        if ((size_t)c_in * block < s)
+            fail(FHE_E_INVALID, "multi-shard convolution needs c_in m^2 >= slots (no duplication)");
+        if (kappa / 2 >= m) fail(FHE_E_INVALID, "kernel reach exceeds channel size");
+        if (level < 1 || level >= c->L) fail(FHE_E_INVALID, "level out of range");
+        const int z = (int)(s / block), T = (int)((size_t)c_in * block / s);
+        const int NO = c_out <= z ? 1 : c_out / z;
+        if (T > 64) fail(FHE_E_INVALID, "too many input shards");
+        fhe_conv_layer* ly = new fhe_conv_layer();
+        ly->ctx = c;
+        ly->c_in = c_in;
+        ly->c_out = c_out;
+        ly->m = m;
+        ly->kappa = kappa;
+        ly->level = level;
+        ly->nk = kappa * kappa;
+        ly->d_pts = nullptr;
+        ly->weights.assign(weights, weights + (size_t)c_in * c_out * kappa * kappa);
+        ly->ms = true;
+        ly->t = T;
+        ly->z = z;
+        ly->n_out = NO;
+        ly->nb_ms = T * z * kappa;
+        const int ne = c->ne_at(level), nb = ly->nb_ms;
+        const size_t extw = (size_t)ne * c->N;
+        const long h = kappa / 2;
+        ly->ms_nonempty.assign((size_t)NO * kappa * nb, 0);
+        ck(cudaMalloc(&ly->d_pts_ms, (size_t)NO * kappa * nb * extw * 8), "cudaMalloc");
+        const double pscale = (double)c->primes[level];
+        std::vector<double> plain, rot(s);
+        for (int v = 0; v < NO; ++v)
+            for (int gi = 0; gi < kappa; ++gi)
+                for (int b = 0; b < nb; ++b) {
+                    const int u = b / (z * kappa), r = (b / kappa) % z;
+                    const long ll = b % kappa - h, kk = gi - h;
+                    if (!fused_plain_ms(c_out, m, kappa, s, weights, v, u, r, kk, ll, plain)) continue;
+                    ly->ms_nonempty[((size_t)v * kappa + gi) * nb + b] = 1;
+                    const uint64_t g = c->reduce_amount(kk * m);
+                    for (size_t j = 0; j < s; ++j) rot[j] = plain[(j + s - g) % s];  // rot_{-kk m}
+                    encode_rows(c, rot.data(), s, level, pscale, ne,
+                                ly->d_pts_ms + (((size_t)v * kappa + gi) * nb + b) * extw);
+                }
+        ck(cudaStreamSynchronize(c->st), "sync");
+        *out = ly;
+    });
+}
+
+int fhe_conv_layer_shards(const fhe_conv_layer* ly, int* t, int* n_out) {
+    if (!ly) return FHE_E_INVALID;
+    if (t) *t = ly->ms ? ly->t : 1;
+    if (n_out) *n_out = ly->ms ? ly->n_out : 1;
+    return FHE_OK;
+}
+
+int fhe_conv2d_shards_into(fhe_ctx* c, const fhe_ct* const* in, size_t n_images, const fhe_conv_layer* ly,
+                           fhe_ct* const* outs) {
+    return guard(c, [&] {
+        if (!ly || !ly->ms) fail(FHE_E_INVALID, "layer was not created by fhe_conv_layer_create_shards");
+        for (size_t i0 = 0; i0 < n_images; i0 += 8) {
+            const int B = (int)std::min<size_t>(8, n_images - i0);
+            conv_ms_batch(c, in + i0 * ly->t, B, ly, outs + i0 * ly->n_out);
+        }
+    });
 }
 
 int fhe_conv_layer_steps(const fhe_conv_layer* ly, int approach, int64_t* steps, size_t cap, size_t* n) {
@@ -2127,7 +2342,15 @@ int fhe_conv_layer_steps(const fhe_conv_layer* ly, int approach, int64_t* steps,
     std::set<int64_t> st;
     const long h = ly->kappa / 2;
     const int64_t block = (int64_t)ly->m * ly->m;
-    if (approach != 5) {
+    if (ly->ms) {  // multi-shard layers run the fused schedule: r m^2 + ll (r < z) and kk m
+        for (int r = 0; r < ly->z; ++r)
+            for (long ll = -h; ll <= h; ++ll)
+                if (r || ll) st.insert((int64_t)r * block + ll);
+        for (long kk = -h; kk <= h; ++kk)
+            if (kk) st.insert(kk * ly->m);
+        approach = -1;
+    }
+    if (approach >= 0 && approach != 5) {
         for (int r = 1; r < ly->c_in; ++r) st.insert((int64_t)r * block);
         for (long kk = -h; kk <= h; ++kk)
             for (long ll = -h; ll <= h; ++ll)

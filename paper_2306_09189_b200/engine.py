@@ -285,6 +285,34 @@ class Context:
                                                 C.byref(out)))
         return ConvLayer(self, out.value, c_in, c_out, m, kappa, level)
 
+    def conv_layer_shards(self, c_in: int, c_out: int, m: int, kappa: int, weights,
+                          level: int | None = None) -> ConvLayer:
+        """fhe_conv_layer_create_shards: multi-shard image-mode layer (c_in m^2 = t * slots)."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        assert w.size == c_in * c_out * kappa * kappa
+        level = self.max_level if level is None else level
+        out = C.c_void_p()
+        self._check(lib().fhe_conv_layer_create_shards(self.h, c_in, c_out, m, kappa, w.ctypes.data_as(_lib.dp),
+                                                       level, C.byref(out)))
+        ly = ConvLayer(self, out.value, c_in, c_out, m, kappa, level)
+        t, no = C.c_int(0), C.c_int(0)
+        self._check(lib().fhe_conv_layer_shards(ly.h, C.byref(t), C.byref(no)))
+        ly.t, ly.n_out = t.value, no.value
+        return ly
+
+    def conv2d_shards(self, in_shards: Sequence[Ciphertext], layer: ConvLayer) -> list[Ciphertext]:
+        """one or more images ([n_images * t] shards) -> [n_images * n_out] output shards."""
+        n_img = len(in_shards) // layer.t
+        assert n_img * layer.t == len(in_shards)
+        outs = [self.encrypt(self.encode(np.zeros(8), level=layer.level - 1), 1) for _ in range(n_img * layer.n_out)]
+        self.conv2d_shards_into(in_shards, layer, outs)
+        return outs
+
+    def conv2d_shards_into(self, in_shards: Sequence[Ciphertext], layer: ConvLayer, outs: Sequence[Ciphertext]):
+        ins = (C.c_void_p * len(in_shards))(*[x.h for x in in_shards])
+        o = (C.c_void_p * len(outs))(*[x.h for x in outs])
+        self._check(lib().fhe_conv2d_shards_into(self.h, ins, len(in_shards) // layer.t, layer.h, o))
+
     def conv2d(self, ct: Ciphertext, layer: ConvLayer, approach: int = 2) -> Ciphertext:
         return self._new(lib().fhe_conv2d, ct.h, layer.h, approach)
 

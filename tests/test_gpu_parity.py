@@ -341,3 +341,40 @@ def test_rotate_hoisted_batch_equals_single(p1):
         single = p1.ctx.rotate_hoisted(ct, ks)
         for j in range(len(ks)):
             assert np.array_equal(outs[i][j].residues(), single[j].residues())
+
+
+@pytest.mark.parametrize("name", ["ms_cfg1_c8", "ms_cfg1_c8to4", "ms_cfg1_c4to8"])
+def test_multishard_conv_bit_exact_and_within_tolerance(oracle, golden, p1, name):
+    """multi-shard image mode: t input / n_out output ciphertexts, bit-exact vs
+    the golden model's ck_conv_shards, decrypted within 1e-6 of the reference's conv_image_shards."""
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    t = c * m * m // s
+    layer = p1.ctx.conv_layer_shards(c, co, m, k, filt)
+    assert layer.t == t and layer.n_out == golden[f"{name}/slots"].shape[0]
+    p1.ctx.gen_galois_keys(layer.steps())
+    cts = [p1.ctx.encrypt(p1.ctx.encode(img[u * s:(u + 1) * s]), ENC_SEED + u) for u in range(t)]
+    outs = p1.ctx.conv2d_shards(cts, layer)
+    ctr = np.stack([p1.ck.encrypt(p1.ck.encode(img[u * s:(u + 1) * s], p1.ck.scale, p1.top), p1.top, ENC_SEED + u)
+                    for u in range(t)])
+    ref, sc = p1.ck.conv_shards(ctr, p1.top, c, m, k, co, filt)
+    for v, o in enumerate(outs):
+        assert np.array_equal(o.residues(), ref[v])
+        assert np.abs(p1.ctx.decrypt(o) - golden[f"{name}/slots"][v]).max() < TOL
+    # two images at once = one at a time
+    outs2 = p1.ctx.conv2d_shards(cts + cts[::-1], layer)
+    for v in range(layer.n_out):
+        assert np.array_equal(outs2[v].residues(), outs[v].residues())
+
+
+def test_multishard_conv_cfg3(oracle, golden):
+    """cfg3 parameters, 32 channels of 32x32 (t = 2 input, n_out = 2 output ciphertexts)."""
+    p = pair(oracle, "cfg3")
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden["ms_cfg3_c32/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    layer = p.ctx.conv_layer_shards(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    cts = [p.ctx.encrypt(p.ctx.encode(img[u * s:(u + 1) * s]), ENC_SEED + u) for u in range(layer.t)]
+    outs = p.ctx.conv2d_shards(cts, layer)
+    for v, o in enumerate(outs):
+        assert np.abs(p.ctx.decrypt(o) - golden["ms_cfg3_c32/slots"][v]).max() < TOL
