@@ -216,6 +216,69 @@ int emu_conv_shards_slots(int c, int m, int kappa, int c_out, size_t s, const do
     return (int)n_out;
 }
 
+/* Channel-shard mode (conv_channel_shards, conv.cpp:273-362): m^2 > s, each
+ * channel spans pc = m^2 / s shards of rows = s / m rows; input shard
+ * (f, u) = image rows [u rows, (u+1) rows) of channel f. Output shard
+ * (g, v) sums, per (f, kk, ll) with w != 0, the in-shard term
+ * mask_in . rot(in[f][v], kk m + ll) and (kk != 0) the spill term from the
+ * neighbour shard v + sign(kk). out = [c_out][pc][s]. */
+int emu_conv_channel_slots(int c, int m, int kappa, int c_out, size_t s, const double* img, const double* filt,
+                           double* out) {
+    const size_t block = (size_t)m * m;
+    if (block <= s || block % s || s % (size_t)m) return -1;
+    const size_t pc = block / s;
+    const long rows = (long)(s / (size_t)m), mL = m;
+    const long h = kappa / 2;
+    if (h > rows) return -1; /* "kernel reach exceeds one neighbor shard" */
+    double* mask = malloc(s * sizeof(double));
+    double* y = malloc(s * sizeof(double));
+    double* acc = malloc(s * sizeof(double));
+    for (int g = 0; g < c_out; g++)
+        for (size_t v = 0; v < pc; v++) {
+            int have = 0;
+            for (int f = 0; f < c; f++)
+                for (long kk = -h; kk <= h; kk++)
+                    for (long ll = -h; ll <= h; ll++) {
+                        const double w = filt_centered(filt, c_out, kappa, f, g, kk, ll) * 1.0;
+                        if (w == 0.0) continue;
+                        const long amount = kk * mL + ll;
+                        const long j_lo = ll < 0 ? -ll : 0, j_hi = ll > 0 ? mL - ll : mL;
+                        if (j_lo >= j_hi) continue;
+                        for (int spill = 0; spill < 2; spill++) {
+                            long src = (long)v;
+                            if (spill) {
+                                if (kk == 0) continue;
+                                src = (long)v + (kk > 0 ? 1 : -1);
+                                if (src < 0 || src >= (long)pc) continue;
+                            }
+                            int any = 0;
+                            for (size_t i = 0; i < s; i++) mask[i] = 0.0;
+                            for (long rr = 0; rr < rows; rr++) {
+                                const int inside = rr + kk >= 0 && rr + kk < rows;
+                                if (inside == spill) continue;
+                                any = 1;
+                                for (long j = j_lo; j < j_hi; j++) mask[(size_t)(rr * mL + j)] = w;
+                            }
+                            if (!any) continue;
+                            emu_rotate(img + ((size_t)f * pc + (size_t)src) * s, y, s, amount);
+                            if (!have) {
+                                for (size_t i = 0; i < s; i++) acc[i] = y[i] * mask[i];
+                                have = 1;
+                            } else {
+                                for (size_t i = 0; i < s; i++) acc[i] = acc[i] + y[i] * mask[i];
+                            }
+                        }
+                    }
+            if (!have) /* Acc::finish zero product against shard 0 */
+                for (size_t i = 0; i < s; i++) acc[i] = img[i] * 0.0;
+            memcpy(out + ((size_t)g * pc + v) * s, acc, s * sizeof(double));
+        }
+    free(mask);
+    free(y);
+    free(acc);
+    return (int)((size_t)c_out * pc);
+}
+
 void emu_oracle_conv(int c, int m, int kappa, int c_out, const double* img, const double* filt,
                      double* out) { /* oracle.cpp:7-31, stride 1 */
     const long h = kappa / 2;

@@ -51,6 +51,10 @@ int emu_fused_plain_ms(int c, int m, int kappa, int c_out, size_t s, const doubl
                        int r, long kk, long ll, double scale, double* plain);
 int emu_conv_shards_slots(int c, int m, int kappa, int c_out, size_t s, const double* img, const double* filt,
                           double* out);
+/* channel-shard mode (conv_channel_shards, conv.cpp:273-362), m^2 > s:
+ * out = [c_out][m^2 / s][s]; returns the output shard count */
+int emu_conv_channel_slots(int c, int m, int kappa, int c_out, size_t s, const double* img, const double* filt,
+                           double* out);
 
 /* Textbook same-padding cross-correlation, stride 1 (oracle.cpp:7-31). */
 void emu_oracle_conv(int c, int m, int kappa, int c_out, const double* img, const double* filt,

@@ -98,6 +98,7 @@ def lib():
         L.emu_fused_plain_ms.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, dp, C.c_int, C.c_int,
                                          C.c_int, C.c_long, C.c_long, C.c_double, dp]
         L.emu_conv_shards_slots.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, dp, dp, dp]
+        L.emu_conv_channel_slots.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, dp, dp, dp]
         L.emu_decompose.argtypes = [C.c_int, C.c_uint64, C.c_uint64, lp, C.c_int]
         L.emu_min_lengths.argtypes = [C.c_uint64, C.c_uint64, u64p]
         _lib = L
@@ -159,6 +160,29 @@ def emu_conv_shards_slots(c, m, kappa, c_out, s, img, filt):
                                      _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), _ptr(out, dp))
     assert rc == n_out, rc
     return out.reshape(n_out, s)
+
+
+def emu_conv_channel_slots(c, m, kappa, c_out, s, img, filt):
+    """conv_channel_shards slots ([c_out * m^2 / s][s]) of a channel-shard image (m^2 > s)."""
+    n = c_out * (m * m // s)
+    out = np.zeros(n * s)
+    rc = lib().emu_conv_channel_slots(c, m, kappa, c_out, s, _ptr(np.ascontiguousarray(img, dtype=np.float64), dp),
+                                      _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), _ptr(out, dp))
+    assert rc == n, rc
+    return out.reshape(n, s)
+
+
+def ref_conv_channel(c, m, kappa, c_out, img, filt, s):
+    """the reference's convolve() on a channel-shard image: conv_channel_shards slots."""
+    n = c_out * (m * m // s)
+    out_slots = np.zeros(n * s)
+    out_img = np.zeros(c_out * m * m)
+    ledger = np.zeros(9, dtype=np.uint64)
+    drop = C.c_int(0)
+    rc = ref().ref_conv(c, m, kappa, c_out, _ptr(np.ascontiguousarray(img), dp), _ptr(np.ascontiguousarray(filt), dp),
+                        0, s, _ptr(out_slots, dp), _ptr(out_img, dp), _ptr(ledger, u64p), C.byref(drop))
+    assert rc == 0
+    return out_slots.reshape(n, s), out_img, ledger, drop.value
 
 
 def emu_oracle_conv(c, m, kappa, c_out, img, filt):

@@ -38,6 +38,12 @@ MS_CASES = {
     "ms_cfg1_c4to8": (4, 32, 3, 8, 1012, 2012, 0, 4096),    # t = 1, n_out = 2
     "ms_cfg3_c32": (32, 32, 3, 32, 1013, 2013, 0, 16384),   # t = 2, n_out = 2
 }
+# channel-shard mode (conv_channel_shards conv.cpp:273-362): m^2 > s, pc = m^2 / s shards per channel
+CS_CASES = {
+    "cs_cfg1_c2m128": (2, 128, 3, 2, 1020, 2020, 0, 4096),     # pc = 4
+    "cs_cfg1_c2to4m128": (2, 128, 3, 4, 1021, 2021, 0, 4096),  # pc = 4, 16 output shards
+    "cs_cfg3_c1m256k5": (1, 256, 5, 2, 1022, 2022, 0, 16384),  # pc = 4, 5x5
+}
 
 
 def main():
@@ -69,6 +75,13 @@ def main():
     for name, (c, m, k, co, si, sf, wk, s) in MS_CASES.items():
         img, filt = po.make_inputs(c, m, k, co, si, sf, wk, use_ref=True)
         slots, image, ledger, drop = po.ref_conv_shards(c, m, k, co, img, filt, s)
+        out[f"{name}/params"] = np.array([c, m, k, co, si, sf, wk, s], dtype=np.int64)
+        out[f"{name}/img_sum"] = np.array([img.sum(), np.abs(img).sum()])
+        out[f"{name}/slots"] = slots
+        out[f"{name}/ledger"] = ledger
+    for name, (c, m, k, co, si, sf, wk, s) in CS_CASES.items():
+        img, filt = po.make_inputs(c, m, k, co, si, sf, wk, use_ref=True)
+        slots, image, ledger, drop = po.ref_conv_channel(c, m, k, co, img, filt, s)
         out[f"{name}/params"] = np.array([c, m, k, co, si, sf, wk, s], dtype=np.int64)
         out[f"{name}/img_sum"] = np.array([img.sum(), np.abs(img).sum()])
         out[f"{name}/slots"] = slots

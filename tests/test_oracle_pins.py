@@ -133,3 +133,16 @@ def test_multishard_restatement_bit_exact(oracle, golden, name):
     # and it is the textbook same-padding conv of the image
     want = oracle.emu_oracle_conv(c, m, k, co, img, filt)
     assert np.abs(got.ravel()[: co * m * m] - want).max() < 1e-12
+
+
+@pytest.mark.parametrize("name", ["cs_cfg1_c2m128", "cs_cfg1_c2to4m128", "cs_cfg3_c1m256k5"])
+def test_channel_shard_restatement_bit_exact(oracle, golden, name):
+    """emu_conv_channel_slots (channel-shard mode, m^2 > slots, in-shard + neighbour-spill masks)
+    == the reference's conv_channel_shards slots, bit for bit."""
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    assert np.isclose(img.sum(), golden[f"{name}/img_sum"][0])
+    got = oracle.emu_conv_channel_slots(c, m, k, co, s, img, filt)
+    assert np.array_equal(got, golden[f"{name}/slots"])
+    want = oracle.emu_oracle_conv(c, m, k, co, img, filt)
+    assert np.abs(got.ravel() - want).max() < 1e-12
