@@ -1173,6 +1173,145 @@ int ck_conv_shards(const ck_ctx* ck, const uint64_t* cts, int t, int level, int 
     return n_out;
 }
 
+/* Channel-shard mode conv (slots as conv_channel_shards,
+ * conv.cpp:273-362): m^2 > s, pc = m^2 / s shards per channel, rows = s / m.
+ * Fused BSGS per output shard (g, v): babies = column shifts ll of input
+ * shard (f, src), src in {v, v + sign(kk)}; giants = row shifts kk m:
+ *   Y_kk = sum_f sum_ll [ rot_{-kk m}(w mask_in(kk, ll)) * X~_{(f, v), ll}
+ *                       + rot_{-kk m}(w mask_spill(kk, ll)) * X~_{(f, v + sign kk), ll} ],
+ *   out  = Rescale(ModDown(Y_0 + sum_{kk != 0} KS_{kk m}(Y_kk))).
+ * cts = [c][pc][2][level+1][N], outs = [c_out][pc][2][level][N]. */
+static int cs_mask(int m, long rows, long kk, long ll, int spill, double w, size_t s, double* mask) {
+    const long j_lo = ll < 0 ? -ll : 0, j_hi = ll > 0 ? m - ll : m;
+    for (size_t i = 0; i < s; i++) mask[i] = 0.0;
+    if (j_lo >= j_hi) return 0;
+    int any = 0;
+    for (long rr = 0; rr < rows; rr++) {
+        const int inside = rr + kk >= 0 && rr + kk < rows;
+        if (inside == spill) continue;
+        any = 1;
+        for (long j = j_lo; j < j_hi; j++) mask[(size_t)(rr * m + j)] = w;
+    }
+    return any;
+}
+
+int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int m, int kappa, int c_out,
+                    const double* filt, uint64_t* outs, double* out_scale) {
+    const size_t N = ck->N, s = N / 2, block = (size_t)m * m;
+    if (block <= s || block % s || s % (size_t)m || level < 1) return -1;
+    const size_t pc = block / s;
+    const long rows = (long)(s / (size_t)m);
+    const long h = kappa / 2;
+    if (h > rows) return -1;
+    const int kap = (int)(2 * h + 1);
+    const int nr = level + 1, ne = nr + ck->K, dn = ck_dnum_at(ck, level);
+    const size_t extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, octw = (size_t)2 * level * N;
+    const uint64_t ql = ck->q[level];
+    const size_t nsh = (size_t)c * pc;
+    uint64_t Pmod[CK_MAXP];
+    for (int u = 0; u < ne; u++) {
+        const uint64_t q = ck->q[ext_prime(ck, level, u)];
+        uint64_t P = 1;
+        for (int k = 0; k < ck->K; k++) P = ck_mulmod(P, ck->q[ck->L + k] % q, q);
+        Pmod[u] = u < nr ? P : 0;
+    }
+    key_cache kc = {.n = 0};
+    uint64_t* dsrc = malloc(nsh * dn * extw * 8);
+    for (size_t sh = 0; sh < nsh; sh++) ck_modup(ck, cts + sh * ctw + (size_t)nr * N, level, dsrc + sh * dn * extw);
+    /* inner products of every (shard, ll != 0), computed once */
+    uint64_t* ips = malloc(nsh * kap * 2 * extw * 8);
+    for (size_t sh = 0; sh < nsh; sh++)
+        for (long ll = -h; ll <= h; ll++) {
+            if (ll == 0) continue;
+            const uint64_t g = ck_galois_elt(ck, ll);
+            uint64_t* ip = ips + (sh * kap + (size_t)(ll + h)) * 2 * extw;
+            ck_inner_product(ck, dsrc + sh * dn * extw, level, cache_get(ck, &kc, g), g, ip, ip + extw);
+        }
+    double* mask = malloc(s * sizeof(double));
+    double* rmask = malloc(s * sizeof(double));
+    uint64_t* pt = malloc(extw * 8);
+    uint64_t* Y = malloc((size_t)kap * 2 * extw * 8);
+    int* gne = malloc(kap * sizeof(int));
+    uint64_t* acc0 = malloc(extw * 8);
+    uint64_t* acc1 = malloc(extw * 8);
+    uint64_t* yq = malloc(ctw * 8);
+    uint64_t* perm = malloc(extw * 8);
+    uint64_t* dg = malloc((size_t)dn * extw * 8);
+    uint64_t* ip0 = malloc(extw * 8);
+    uint64_t* ip1 = malloc(extw * 8);
+    uint64_t* md = malloc(ctw * 8);
+    for (int g = 0; g < c_out; g++)
+        for (size_t v = 0; v < pc; v++) {
+            memset(Y, 0, (size_t)kap * 2 * extw * 8);
+            for (int i = 0; i < kap; i++) gne[i] = 0;
+            for (long kk = -h; kk <= h; kk++) {
+                uint64_t* y = Y + (size_t)(kk + h) * 2 * extw;
+                for (int f = 0; f < c; f++)
+                    for (long ll = -h; ll <= h; ll++) {
+                        const double w = emu_filt_centered(filt, c_out, kappa, f, g, kk, ll) * 1.0;
+                        if (w == 0.0) continue;
+                        for (int spill = 0; spill < 2; spill++) {
+                            long src = (long)v;
+                            if (spill) {
+                                if (kk == 0) continue;
+                                src = (long)v + (kk > 0 ? 1 : -1);
+                                if (src < 0 || src >= (long)pc) continue;
+                            }
+                            if (!cs_mask(m, rows, kk, ll, spill, w, s, mask)) continue;
+                            emu_rotate(mask, rmask, s, -kk * m);
+                            ck_encode_plain(ck, rmask, s, (double)ql, level, 1, pt);
+                            const size_t sh = (size_t)f * pc + (size_t)src;
+                            gne[kk + h] = 1;
+                            if (ll == 0) {
+                                conv_accumulate(ck, level, pt, cts + sh * ctw, 1, NULL, NULL, Pmod, y, y + extw);
+                            } else {
+                                const uint64_t* ip = ips + (sh * kap + (size_t)(ll + h)) * 2 * extw;
+                                conv_accumulate(ck, level, pt, cts + sh * ctw, ck_galois_elt(ck, ll), ip, ip + extw,
+                                                Pmod, y, y + extw);
+                            }
+                        }
+                    }
+            }
+            memset(acc0, 0, extw * 8);
+            memset(acc1, 0, extw * 8);
+            for (long kk = -h; kk <= h; kk++) {
+                if (!gne[kk + h]) continue;
+                const uint64_t* y = Y + (size_t)(kk + h) * 2 * extw;
+                const uint64_t ge = ck_galois_elt(ck, kk * m);
+                if (ge == 1) {
+                    for (int u = 0; u < ne; u++) {
+                        const uint64_t q = ck->q[ext_prime(ck, level, u)];
+                        for (size_t k = 0; k < N; k++) {
+                            acc0[(size_t)u * N + k] = addm(acc0[(size_t)u * N + k], y[(size_t)u * N + k], q);
+                            acc1[(size_t)u * N + k] = addm(acc1[(size_t)u * N + k], y[extw + (size_t)u * N + k], q);
+                        }
+                    }
+                    continue;
+                }
+                ck_moddown(ck, y + extw, level, yq + (size_t)nr * N);
+                ck_modup(ck, yq + (size_t)nr * N, level, dg);
+                ck_inner_product(ck, dg, level, cache_get(ck, &kc, ge), ge, ip0, ip1);
+                for (int u = 0; u < ne; u++) ck_automorph_ntt(ck, y + (size_t)u * N, perm + (size_t)u * N, ge);
+                for (int u = 0; u < ne; u++) {
+                    const uint64_t q = ck->q[ext_prime(ck, level, u)];
+                    for (size_t k = 0; k < N; k++) {
+                        const uint64_t t0 = addm(ip0[(size_t)u * N + k], perm[(size_t)u * N + k], q);
+                        acc0[(size_t)u * N + k] = addm(acc0[(size_t)u * N + k], t0, q);
+                        acc1[(size_t)u * N + k] = addm(acc1[(size_t)u * N + k], ip1[(size_t)u * N + k], q);
+                    }
+                }
+            }
+            ck_moddown(ck, acc0, level, md);
+            ck_moddown(ck, acc1, level, md + (size_t)nr * N);
+            ck_rescale(ck, md, level, outs + ((size_t)g * pc + v) * octw);
+        }
+    if (out_scale) *out_scale = (ck->scale * (double)ql) / (double)ql;
+    cache_free(&kc);
+    free(dsrc); free(ips); free(mask); free(rmask); free(pt); free(Y); free(gne);
+    free(acc0); free(acc1); free(yq); free(perm); free(dg); free(ip0); free(ip1); free(md);
+    return (int)((size_t)c_out * pc);
+}
+
 int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,
             const double* filt, int plan, uint64_t* out, double* out_scale) {
     const size_t N = ck->N, s = N / 2, block = (size_t)m * m;

@@ -105,6 +105,11 @@ int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int k
 int ck_conv_shards(const ck_ctx* ck, const uint64_t* cts, int t, int level, int c, int m, int kappa, int c_out,
                    const double* filt, uint64_t* outs, double* out_scale);
 
+/* Channel-shard mode conv (fused BSGS, see ckks_ref.c): cts [c][m^2/s][2][level+1][N]
+ * -> outs [c_out][m^2/s][2][level][N]; returns the output shard count. */
+int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int m, int kappa, int c_out,
+                    const double* filt, uint64_t* outs, double* out_scale);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,7 @@ void emu_rotate(const double* in, double* out, size_t s, long k) { /* emu.cpp:15
     for (size_t i = 0; i < s; i++) out[i] = in[(i + a) % s];
 }
 
-static double filt_centered(const double* filt, int c_out, int kappa, int f, int g, long k, long l) {
+double emu_filt_centered(const double* filt, int c_out, int kappa, int f, int g, long k, long l) {
     /* tensor.hpp:53-67 */
     const long h = kappa / 2;
     return filt[(((size_t)f * c_out + g) * kappa + (size_t)(k + h)) * kappa + (size_t)(l + h)];
@@ -40,7 +40,7 @@ int emu_fused_plain(int c, int m, int kappa, int c_out, size_t s, const double* 
     for (size_t b = 0; b < z; b++) {
         const int in_ch = (int)(((b + (size_t)r) % z) % (size_t)c);
         const int out_ch = (int)(b % (size_t)c_out);
-        const double w = filt_centered(filt, c_out, kappa, in_ch, out_ch, kk, ll) * scale;
+        const double w = emu_filt_centered(filt, c_out, kappa, in_ch, out_ch, kk, ll) * scale;
         if (w == 0.0) continue;
         any = 1;
         const long i_lo = kk < 0 ? -kk : 0, i_hi = kk > 0 ? m - kk : m;
@@ -129,7 +129,7 @@ int emu_fused_plain_ms(int c, int m, int kappa, int c_out, size_t s, const doubl
     for (size_t b = 0; b < z; b++) {
         const int in_ch = (int)((size_t)u * z + (b + (size_t)r) % z);
         const int out_ch = (int)(((size_t)v * z + b) % (size_t)c_out);
-        const double w = filt_centered(filt, c_out, kappa, in_ch, out_ch, kk, ll) * scale;
+        const double w = emu_filt_centered(filt, c_out, kappa, in_ch, out_ch, kk, ll) * scale;
         if (w == 0.0) continue;
         any = 1;
         const long i_lo = kk < 0 ? -kk : 0, i_hi = kk > 0 ? m - kk : m;
@@ -239,7 +239,7 @@ int emu_conv_channel_slots(int c, int m, int kappa, int c_out, size_t s, const d
             for (int f = 0; f < c; f++)
                 for (long kk = -h; kk <= h; kk++)
                     for (long ll = -h; ll <= h; ll++) {
-                        const double w = filt_centered(filt, c_out, kappa, f, g, kk, ll) * 1.0;
+                        const double w = emu_filt_centered(filt, c_out, kappa, f, g, kk, ll) * 1.0;
                         if (w == 0.0) continue;
                         const long amount = kk * mL + ll;
                         const long j_lo = ll < 0 ? -ll : 0, j_hi = ll > 0 ? mL - ll : mL;
@@ -293,7 +293,7 @@ void emu_oracle_conv(int c, int m, int kappa, int c_out, const double* img, cons
                             const double v = (ii < 0 || jj < 0 || ii >= m || jj >= m)
                                                  ? 0.0
                                                  : img[((size_t)f * m + (size_t)ii) * m + (size_t)jj];
-                            acc += filt_centered(filt, c_out, kappa, f, g, kr, kc) * v;
+                            acc += emu_filt_centered(filt, c_out, kappa, f, g, kr, kc) * v;
                         }
                 out[((size_t)g * m + (size_t)i) * m + (size_t)j] = acc;
             }

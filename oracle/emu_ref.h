@@ -36,6 +36,8 @@ void emu_rotate(const double* in, double* out, size_t s, long k);
 /* Fused plaintext of conv.cpp:69-85 for a single image shard of s slots
  * (t = 1, rep = 1, identity tau, n_out = 1): returns 0 when every entry is
  * zero (the reference then skips the term), else 1. */
+/* K.centered(f, g, k, l), tensor.hpp:53-67 */
+double emu_filt_centered(const double* filt, int c_out, int kappa, int f, int g, long k, long l);
 int emu_fused_plain(int c, int m, int kappa, int c_out, size_t s, const double* filt, int r,
                     long kk, long ll, double scale, double* plain);
 

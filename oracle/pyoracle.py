@@ -87,6 +87,7 @@ def lib():
                               C.c_int, u64p, dp]
         L.ck_conv_shards.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp,
                                      u64p, dp]
+        L.ck_conv_channel.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp, u64p, dp]
         L.emu_make_inputs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
                                       C.c_int, dp, dp]
         L.emu_rotate.argtypes = [dp, dp, C.c_size_t, C.c_long]
@@ -386,4 +387,16 @@ class CKKS:
                                   _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), _ptr(out, u64p),
                                   C.byref(sc))
         assert rc == n_out, rc
+        return out, sc.value
+
+    def conv_channel(self, cts, level, c, m, kappa, c_out, filt):
+        """channel-shard conv: cts [c * pc][2][level+1][N] -> [c_out * pc][2][level][N]."""
+        cts = np.ascontiguousarray(cts, dtype=np.uint64)
+        pc = m * m // (self.N // 2)
+        out = np.zeros((c_out * pc, 2, level, self.N), dtype=np.uint64)
+        sc = C.c_double(0)
+        rc = lib().ck_conv_channel(self.h, _ptr(cts, u64p), level, c, m, kappa, c_out,
+                                   _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), _ptr(out, u64p),
+                                   C.byref(sc))
+        assert rc == c_out * pc, rc
         return out, sc.value

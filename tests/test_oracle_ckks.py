@@ -171,3 +171,16 @@ def test_multishard_conv_decrypts_to_reference(cfg1, oracle, golden, name):
     out, sc = cfg1.conv_shards(cts, 4, c, m, k, co, filt)
     dec = np.stack([cfg1.decrypt(out[v], 3, sc) for v in range(out.shape[0])])
     assert np.abs(dec - golden[f"{name}/slots"]).max() < 1e-6
+
+
+@pytest.mark.parametrize("name", ["cs_cfg1_c2m128", "cs_cfg1_c2to4m128"])
+def test_channel_shard_conv_decrypts_to_reference(cfg1, oracle, golden, name):
+    """the golden model's channel-shard conv (in-shard + neighbour-spill plaintexts, fused BSGS)
+    decrypts to the reference's conv_channel_shards slots, <= 1e-6."""
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    nin = c * m * m // s
+    cts = np.stack([cfg1.encrypt(cfg1.encode(img[u * s:(u + 1) * s], cfg1.scale, 4), 4, 9000 + u) for u in range(nin)])
+    out, sc = cfg1.conv_channel(cts, 4, c, m, k, co, filt)
+    dec = np.stack([cfg1.decrypt(out[v], 3, sc) for v in range(out.shape[0])])
+    assert np.abs(dec - golden[f"{name}/slots"]).max() < 1e-6
