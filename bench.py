@@ -488,6 +488,38 @@ def other_configs(world, device):
                                   "decrypt_max_abs_err": err,
                                   "note": "32x32x32 image, 3x3 32->32, one rescale; fhe_conv2d_shards_into"}
     ctx.close()
+    # channel-shard mode at cfg3 parameters: a 256x256x2 image (each channel spans
+    # 4 ciphertexts of 64 rows) -> 2 channels, 3x3, batch of 4 images
+    ctx = Context.from_config("cfg3", device=device)
+    ctx.keygen(7)
+    rng = np.random.default_rng(99)
+    c, m, k, nimg = 2, 256, 3, 4
+    w = rng.uniform(-1, 1, c * c * k * k)
+    layer = ctx.conv_layer_shards(c, c, m, k, w)
+    ctx.gen_galois_keys(layer.steps())
+    s = ctx.slots
+    imgs = [rng.uniform(-1, 1, c * m * m) for _ in range(nimg)]
+    ins = [ctx.encrypt(ctx.encode(x[u * s:(u + 1) * s]), 800 + i * 16 + u) for i, x in enumerate(imgs)
+           for u in range(layer.t)]
+    outs = [ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1) for _ in range(nimg * layer.n_out)]
+    ctx.conv2d_shards_into(ins, layer, outs)
+    x = imgs[0].reshape(c, m, m)
+    wt = w.reshape(c, c, k, k)
+    xp = np.pad(x, ((0, 0), (1, 1), (1, 1)))
+    ref = sum(np.einsum("fg,fij->gij", wt[:, :, a, b], xp[:, a:a + m, b:b + m]) for a in range(k) for b in range(k))
+    got = np.concatenate([ctx.decrypt(outs[v]) for v in range(layer.n_out)])
+    err = float(np.abs(got - ref.ravel()).max())
+    ms = float("inf")
+    for _ in range(3):
+        ctx.synchronize()
+        ctx.timer_start()
+        ctx.conv2d_shards_into(ins, layer, outs)
+        ms = min(ms, ctx.timer_stop())
+    res["channelshard_cfg3_m256"] = {"images_per_s": round(world * nimg / (ms / 1e3), 1), "batch_images": nimg,
+                                     "input_shards": layer.t, "output_shards": layer.n_out,
+                                     "decrypt_max_abs_err": err,
+                                     "note": "256x256x2 image, 3x3 2->2, one rescale; fhe_conv2d_shards_into"}
+    ctx.close()
     # cfg5: 3 stacked 3x3 16->16 layers (weights U[-0.5,0.5]), one rescale each, batch 32
     ctx = Context.from_config("cfg5", device=device)
     ctx.keygen(7)

@@ -231,6 +231,8 @@ struct fhe_conv_layer {
     // channels, n_out output shards; fused-BSGS plaintexts
     // pt'[v][kk][b = (u, r, ll)] = rot_{-kk m}(fused_plain_ms(v, u, r, kk, ll))
     bool ms = false;
+    bool cs = false;  // channel-shard mode (m^2 > slots): pc = m^2 / slots shards per channel
+    int pc = 1;
     int t = 1, z = 0, n_out = 1, nb_ms = 0;
     std::vector<uint8_t> ms_nonempty;  // [n_out][kappa][nb_ms]
     uint64_t* d_pts_ms = nullptr;
@@ -566,6 +568,23 @@ bool fused_plain_ms(int c_out, int m, int kappa, size_t s, const double* w, int 
         const long j_lo = std::max(0L, -ll), j_hi = std::min<long>(m, m - ll);
         for (long i = i_lo; i < i_hi; ++i)
             for (long j = j_lo; j < j_hi; ++j) plain[b * block + (size_t)(i * m + j)] = wt;
+    }
+    return any;
+}
+
+// channel-shard masks (reference conv.cpp:305-344): rows rr of a shard whose
+// shifted source stays inside it (spill = 0) or comes from the neighbour shard
+// (spill = 1), columns j in [max(0, -ll), min(m, m - ll))
+bool cs_mask(int m, long rows, long kk, long ll, int spill, double w, size_t s, std::vector<double>& mask) {
+    mask.assign(s, 0.0);
+    const long j_lo = std::max(0L, -ll), j_hi = std::min<long>(m, m - ll);
+    if (j_lo >= j_hi) return false;
+    bool any = false;
+    for (long rr = 0; rr < rows; ++rr) {
+        const bool inside = rr + kk >= 0 && rr + kk < rows;
+        if (inside == (spill != 0)) continue;
+        any = true;
+        for (long j = j_lo; j < j_hi; ++j) mask[(size_t)(rr * m + j)] = w;
     }
     return any;
 }
@@ -1309,6 +1328,108 @@ void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
         c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[i]->depth);
     }
     c->ledger.hoist_groups += (uint64_t)B * T;
+    c->release(md);
+    c->release(Y);
+    c->release(buf);
+}
+
+// Channel-shard conv of B images (B x c x pc input shards -> B x c_out x pc
+// output shards), fused BSGS per output shard (g, v): babies = column shifts
+// ll of input shard (f, src), src in {v, v +- 1} (in-shard / spill masks),
+// giants = row shifts kk m; plaintexts pt'[g][f][kk][ll][spill].
+void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_layer* ly, fhe_ct* const* outs) {
+    const int level = ly->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
+    const int C_ = ly->c_in, CO = ly->c_out, PC = ly->pc, kap = ly->kappa, h = kap / 2;
+    const int NSH = C_ * PC, NOUT = CO * PC;
+    for (int i = 0; i < B * NSH; ++i)
+        if (in[i]->level != level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
+    for (int i = 0; i < B * NOUT; ++i)
+        if (outs[i]->level != level - 1) fail(FHE_E_INVALID, "output level must be input level - 1");
+    uint64_t* buf = c->alloc((size_t)B * NSH * ctw);
+    for (int i = 0; i < B * NSH; ++i)
+        ck(cudaMemcpyAsync(buf + (size_t)i * ctw, in[i]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    uint64_t* dig = c->alloc((size_t)B * NSH * dw);
+    modup_batch(c, buf + (size_t)nr * N, ctw, B * NSH, level, dig);
+    const size_t ys = (size_t)kap * 2 * extw;
+    uint64_t* Y = c->alloc((size_t)B * NOUT * ys);  // [B][c_out][pc][kappa][2][ne][N]
+    ck(cudaMemsetAsync(Y, 0, (size_t)B * NOUT * ys * 8, c->st), "memset");
+    auto pt_of = [&](int g, int f, int kk, int ll, int spill) {  // kk, ll offsets in [0, kappa)
+        return ((((size_t)g * C_ + f) * kap + kk) * kap + ll) * 2 + spill;
+    };
+    for (int g = 0; g < CO; ++g)
+        for (int v = 0; v < PC; ++v)
+            for (int g0 = 0; g0 < kap; g0 += 3) {
+                const int ng = std::min(3, kap - g0);
+                FusedBsgs f{};
+                f.nsrc = B;
+                f.ng = ng;
+                f.digits = dig;
+                f.digit_src_stride = (size_t)NSH * dw;
+                f.digit_slot_stride = dw;
+                f.ct = buf;
+                f.ct_src_stride = (size_t)NSH * ctw;
+                f.ct_slot_stride = ctw;
+                f.pt_g_stride = (size_t)kap * 2 * extw;  // next row shift kk
+                f.Y = Y + ((size_t)g * PC + v) * ys + (size_t)g0 * 2 * extw;
+                f.y_src_stride = (size_t)NOUT * ys;
+                f.y_g_stride = 2 * extw;
+                f.accumulate = 1;
+                double keyed = 0, pts = 0;
+                for (int fi = 0; fi < C_; ++fi)
+                    for (int dv = -1; dv <= 1; ++dv) {
+                        const int src = v + dv;
+                        if (src < 0 || src >= PC) continue;
+                        const int spill = dv != 0;
+                        for (int lo = 0; lo < kap; ++lo) {
+                            uint32_t mask = 0;
+                            for (int gg = 0; gg < ng; ++gg) {
+                                const int kk = g0 + gg - h;  // row shift of this giant
+                                if (spill && (kk == 0 || (kk > 0) != (dv > 0))) continue;
+                                if (ly->ms_nonempty[pt_of(g, fi, g0 + gg, lo, spill)]) mask |= 1u << gg;
+                            }
+                            if (!mask) continue;
+                            if (f.nb == kMaxFused) fail(FHE_E_INVALID, "too many baby steps for one output shard");
+                            const uint32_t gal = c->galois_of(c->reduce_amount(lo - h));
+                            f.galois[f.nb] = gal;
+                            f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+                            f.gmask[f.nb] = mask;
+                            f.pt[f.nb] = ly->d_pts_ms + pt_of(g, fi, g0, lo, spill) * extw;
+                            f.srcslot[f.nb] = (uint16_t)(fi * PC + src);
+                            f.nb++;
+                            pts += __builtin_popcount(mask);
+                            if (gal != 1) {
+                                keyed += 1;
+                                c->ledger.key_switches += B;
+                            }
+                        }
+                    }
+                if (!f.nb) continue;
+                c->timed("bsgs_fused",
+                         c->rows(keyed * 2.0 * dn * ne + pts * ne + B * (3.0 * C_ * dn * ne + 2.0 * nr + 4.0 * ng * ne)),
+                         [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+            }
+    c->release(dig);
+    std::vector<int> giants;
+    std::vector<int64_t> gamt;
+    int id = -1;
+    for (int kk = -h; kk <= h; ++kk) {
+        gamt.push_back((int64_t)kk * ly->m);
+        if (kk == 0)
+            id = kk + h;
+        else
+            giants.push_back(kk + h);
+    }
+    const size_t otw = (size_t)2 * level * N;
+    uint64_t* md = c->alloc((size_t)B * NOUT * otw);
+    giants_finish(c, Y, ys, B * NOUT, level, giants, gamt, id, md);
+    for (int i = 0; i < B * NOUT; ++i) {
+        ck(cudaMemcpyAsync(outs[i]->d, md + (size_t)i * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+        const fhe_ct* src = in[(i / NOUT) * NSH];
+        outs[i]->scale = (src->scale * (double)c->primes[level]) / (double)c->primes[level];
+        outs[i]->depth = src->depth + 1;
+        c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[i]->depth);
+    }
     c->release(md);
     c->release(Y);
     c->release(buf);
@@ -2270,7 +2391,52 @@ int fhe_conv_layer_create_shards(fhe_ctx* c, int c_in, int c_out, int m, int kap
         if (c_out <= 0 || (c_out & (c_out - 1))) fail(FHE_E_INVALID, "output channel count must be a power of two");
         if (c_in <= 0 || (c_in & (c_in - 1))) fail(FHE_E_INVALID, "channel count must be a power of two");
         const size_t s = c->slots(), block = (size_t)m * m;
-        if (m <= 0 || (m & (m - 1)) || block > s) fail(FHE_E_INVALID, "channel side must be a power of two");
+        const size_t s2 = s;
+        if (m <= 0 || (m & (m - 1))) fail(FHE_E_INVALID, "channel side must be a power of two");
+        if (block > s2) {  // channel-shard mode (reference conv_channel_shards, conv.cpp:273-362)
+            const long rows = (long)(s2 / (size_t)m), h = kappa / 2;
+            if (h > rows) fail(FHE_E_INVALID, "kernel reach exceeds one neighbor shard");
+            if (level < 1 || level >= c->L) fail(FHE_E_INVALID, "level out of range");
+            fhe_conv_layer* ly = new fhe_conv_layer();
+            ly->ctx = c;
+            ly->c_in = c_in;
+            ly->c_out = c_out;
+            ly->m = m;
+            ly->kappa = kappa;
+            ly->level = level;
+            ly->nk = kappa * kappa;
+            ly->d_pts = nullptr;
+            ly->weights.assign(weights, weights + (size_t)c_in * c_out * kappa * kappa);
+            ly->ms = true;
+            ly->cs = true;
+            ly->pc = (int)(block / s2);
+            ly->t = c_in * ly->pc;
+            ly->n_out = c_out * ly->pc;
+            const int ne = c->ne_at(level);
+            const size_t extw = (size_t)ne * c->N, npt = (size_t)c_out * c_in * kappa * kappa * 2;
+            ly->ms_nonempty.assign(npt, 0);
+            ck(cudaMalloc(&ly->d_pts_ms, npt * extw * 8), "cudaMalloc");
+            const double pscale = (double)c->primes[level];
+            std::vector<double> mask, rot(s2);
+            size_t idx = 0;
+            for (int g = 0; g < c_out; ++g)
+                for (int f = 0; f < c_in; ++f)
+                    for (long kk = -h; kk <= h; ++kk)
+                        for (long ll = -h; ll <= h; ++ll)
+                            for (int spill = 0; spill < 2; ++spill, ++idx) {
+                                const double w =
+                                    weights[(((size_t)f * c_out + g) * kappa + (size_t)(kk + h)) * kappa + (size_t)(ll + h)];
+                                if (w == 0.0 || (spill && kk == 0)) continue;
+                                if (!cs_mask(m, rows, kk, ll, spill, w, s2, mask)) continue;
+                                ly->ms_nonempty[idx] = 1;
+                                const uint64_t gsh = c->reduce_amount(kk * m);
+                                for (size_t j = 0; j < s2; ++j) rot[j] = mask[(j + s2 - gsh) % s2];  // rot_{-kk m}
+                                encode_rows(c, rot.data(), s2, level, pscale, ne, ly->d_pts_ms + idx * extw);
+                            }
+            ck(cudaStreamSynchronize(c->st), "sync");
+            *out = ly;
+            return;
+        }
         if ((size_t)c_in * block < s)
             fail(FHE_E_INVALID, "multi-shard convolution needs c_in m^2 >= slots (no duplication)");
         if (kappa / 2 >= m) fail(FHE_E_INVALID, "kernel reach exceeds channel size");
@@ -2330,7 +2496,10 @@ int fhe_conv2d_shards_into(fhe_ctx* c, const fhe_ct* const* in, size_t n_images,
         if (!ly || !ly->ms) fail(FHE_E_INVALID, "layer was not created by fhe_conv_layer_create_shards");
         for (size_t i0 = 0; i0 < n_images; i0 += 8) {
             const int B = (int)std::min<size_t>(8, n_images - i0);
-            conv_ms_batch(c, in + i0 * ly->t, B, ly, outs + i0 * ly->n_out);
+            if (ly->cs)
+                conv_cs_batch(c, in + i0 * ly->t, B, ly, outs + i0 * ly->n_out);
+            else
+                conv_ms_batch(c, in + i0 * ly->t, B, ly, outs + i0 * ly->n_out);
         }
     });
 }
@@ -2342,7 +2511,13 @@ int fhe_conv_layer_steps(const fhe_conv_layer* ly, int approach, int64_t* steps,
     std::set<int64_t> st;
     const long h = ly->kappa / 2;
     const int64_t block = (int64_t)ly->m * ly->m;
-    if (ly->ms) {  // multi-shard layers run the fused schedule: r m^2 + ll (r < z) and kk m
+    if (ly->cs) {  // channel-shard layers: column shifts ll and row shifts kk m
+        for (long ll = -h; ll <= h; ++ll)
+            if (ll) st.insert(ll);
+        for (long kk = -h; kk <= h; ++kk)
+            if (kk) st.insert(kk * ly->m);
+        approach = -1;
+    } else if (ly->ms) {  // multi-shard layers run the fused schedule: r m^2 + ll (r < z) and kk m
         for (int r = 0; r < ly->z; ++r)
             for (long ll = -h; ll <= h; ++ll)
                 if (r || ll) st.insert((int64_t)r * block + ll);

@@ -378,3 +378,36 @@ def test_multishard_conv_cfg3(oracle, golden):
     outs = p.ctx.conv2d_shards(cts, layer)
     for v, o in enumerate(outs):
         assert np.abs(p.ctx.decrypt(o) - golden["ms_cfg3_c32/slots"][v]).max() < TOL
+
+
+@pytest.mark.parametrize("name", ["cs_cfg1_c2m128", "cs_cfg1_c2to4m128"])
+def test_channel_shard_conv_bit_exact_and_within_tolerance(oracle, golden, p1, name):
+    """channel-shard mode (m^2 > slots): bit-exact vs the golden model's
+    ck_conv_channel, decrypted within 1e-6 of the reference's conv_channel_shards."""
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    layer = p1.ctx.conv_layer_shards(c, co, m, k, filt)
+    nin = c * m * m // s
+    assert layer.t == nin and layer.n_out == golden[f"{name}/slots"].shape[0]
+    p1.ctx.gen_galois_keys(layer.steps())
+    cts = [p1.ctx.encrypt(p1.ctx.encode(img[u * s:(u + 1) * s]), ENC_SEED + u) for u in range(nin)]
+    outs = p1.ctx.conv2d_shards(cts, layer)
+    ctr = np.stack([p1.ck.encrypt(p1.ck.encode(img[u * s:(u + 1) * s], p1.ck.scale, p1.top), p1.top, ENC_SEED + u)
+                    for u in range(nin)])
+    ref, _ = p1.ck.conv_channel(ctr, p1.top, c, m, k, co, filt)
+    for v, o in enumerate(outs):
+        assert np.array_equal(o.residues(), ref[v])
+        assert np.abs(p1.ctx.decrypt(o) - golden[f"{name}/slots"][v]).max() < TOL
+
+
+def test_channel_shard_conv_cfg3_5x5(oracle, golden):
+    """cfg3 parameters: one 256x256 channel (4 shards) -> 2 channels, 5x5 kernel (giants in two chunks)."""
+    p = pair(oracle, "cfg3")
+    c, m, k, co, si, sf, wk, s = (int(x) for x in golden["cs_cfg3_c1m256k5/params"])
+    img, filt = oracle.make_inputs(c, m, k, co, si, sf, wk)
+    layer = p.ctx.conv_layer_shards(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    cts = [p.ctx.encrypt(p.ctx.encode(img[u * s:(u + 1) * s]), ENC_SEED + u) for u in range(layer.t)]
+    outs = p.ctx.conv2d_shards(cts, layer)
+    for v, o in enumerate(outs):
+        assert np.abs(p.ctx.decrypt(o) - golden["cs_cfg3_c1m256k5/slots"][v]).max() < TOL
