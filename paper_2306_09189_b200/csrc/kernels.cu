@@ -245,48 +245,6 @@ namespace {
 
 // one thread per (digit j, coefficient k): computes the centered
 // [x_i (Q_J/q_i)^-1]_{q_i} once and extends it to every target row.
-__global__ void k_modup_bconv(DevCtx c, const uint64_t* coef_all, const uint64_t* c1_all, size_t src_stride,
-                              int nsrc, uint64_t* digits_all, const ModUpDigit* tables, int level, int dn) {
-    const int ne = level + 1 + c.K, nr = level + 1;
-    const size_t total = (size_t)nsrc * dn * c.N;
-    RowMap rm{ne, level, c.L, 0};
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int sj = (int)(i >> c.logN);
-        const int src = sj / dn, j = sj % dn;
-        const int k = (int)(i & (size_t)(c.N - 1));
-        const uint64_t* coef = coef_all + (size_t)src * nr * c.N;
-        const uint64_t* c1_ntt = c1_all + (size_t)src * src_stride;
-        uint64_t* digits = digits_all + (size_t)src * dn * ne * c.N;
-        const ModUpDigit& T = tables[j];
-        uint64_t v[kMaxAlpha];
-        int neg = 0;
-        const int na = T.hi - T.lo;
-#pragma unroll
-        for (int a = 0; a < kMaxAlpha; ++a) {
-            if (a < na) {
-                const int qi = T.lo + a;
-                const uint64_t q = c.primes[qi].q;
-                v[a] = mul_shoup(coef[(size_t)qi * c.N + k], T.inv[a], T.inv_sh[a], q);
-                neg += v[a] > (q >> 1);
-            }
-        }
-        uint64_t* dj = digits + (size_t)j * ne * c.N + k;
-        for (int u = 0; u < ne; ++u) {
-            if (u >= T.lo && u < T.hi) {
-                dj[(size_t)u * c.N] = c1_ntt[(size_t)u * c.N + k];
-                continue;
-            }
-            const uint64_t t = c.primes[row_prime(rm, u)].q;
-            uint64_t acc = 0;
-#pragma unroll
-            for (int a = 0; a < kMaxAlpha; ++a)
-                if (a < na) acc = add_mod(acc, mul_shoup(v[a], T.hat[u][a], T.hat_sh[u][a], t), t);
-            // centered lift: each v > q_i/2 stands for v - q_i, i.e. -Q_J
-            for (int n = 0; n < neg; ++n) acc = sub_mod(acc, T.qj[u], t);
-            dj[(size_t)u * c.N] = acc;
-        }
-    }
-}
 
 __global__ void k_ks_inner(DevCtx c, const uint64_t* D, const uint64_t* key, uint64_t* acc0, uint64_t* acc1,
                            uint32_t g, int level, int dn) {
@@ -324,52 +282,6 @@ __global__ void k_gather_special(DevCtx c, uint64_t* dst, const uint64_t* acc, s
         const int r = (int)(i >> c.logN);
         const int p = r / c.K, kk = r % c.K;
         dst[i] = acc[(size_t)p * acc_stride + ((size_t)level + 1 + kk) * c.N + (i & (size_t)(c.N - 1))];
-    }
-}
-
-__global__ void k_moddown_bconv(DevCtx c, const uint64_t* pcoef, uint64_t* conv, const ModDownTable* md, int level,
-                                int npoly) {
-    const int nr = level + 1;
-    const size_t total = (size_t)npoly * c.N;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int p = (int)(i >> c.logN);
-        const int k = (int)(i & (size_t)(c.N - 1));
-        uint64_t v[kMaxAlpha];
-        int neg = 0;
-#pragma unroll
-        for (int a = 0; a < kMaxAlpha; ++a) {
-            if (a < c.K) {
-                const uint64_t q = c.primes[c.L + a].q;
-                v[a] = mul_shoup(pcoef[((size_t)p * c.K + a) * c.N + k], md->pinv[a], md->pinv_sh[a], q);
-                neg += v[a] > (q >> 1);
-            }
-        }
-        for (int t = 0; t < nr; ++t) {
-            const uint64_t q = c.primes[t].q;
-            uint64_t acc = 0;
-#pragma unroll
-            for (int a = 0; a < kMaxAlpha; ++a)
-                if (a < c.K) acc = add_mod(acc, mul_shoup(v[a], md->hat[t][a], md->hat_sh[t][a], q), q);
-            for (int n = 0; n < neg; ++n) acc = sub_mod(acc, md->pmod[t], q);
-            conv[((size_t)p * nr + t) * c.N + k] = acc;
-        }
-    }
-}
-
-__global__ void k_moddown_finish(DevCtx c, uint64_t* out, const uint64_t* acc, const uint64_t* conv,
-                                 const ModDownTable* md, int level, int npoly, const uint64_t* add_src,
-                                 uint32_t g) {
-    const int nr = level + 1, ne = nr + c.K;
-    const size_t total = (size_t)npoly * nr * c.N;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i >> c.logN);
-        const int p = r / nr, t = r % nr;
-        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
-        const uint64_t q = c.primes[t].q;
-        const uint64_t x = acc[((size_t)p * ne + t) * c.N + k];
-        uint64_t o = mul_shoup(sub_mod(x, conv[i], q), md->pinvq[t], md->pinvq_sh[t], q);
-        if (add_src && p == 0) o = add_mod(o, add_src[(size_t)t * c.N + perm_index(k, g, c.logN)], q);
-        out[i] = o;
     }
 }
 
@@ -423,12 +335,6 @@ __global__ void __launch_bounds__(256) k_conv_mac(DevCtx c, uint64_t* acc, const
 
 }  // namespace
 
-void modup_bconv(const DevCtx& c, const uint64_t* coef, const uint64_t* c1_ntt, size_t src_stride, int nsrc,
-                 uint64_t* digits, const ModUpDigit* tables, int level, int dn, cudaStream_t st) {
-    ++g_launches;
-    k_modup_bconv<<<ew_blocks((size_t)nsrc * dn * c.N), kEwThreads, 0, st>>>(c, coef, c1_ntt, src_stride, nsrc,
-                                                                              digits, tables, level, dn);
-}
 void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* key, uint64_t* acc0,
                       uint64_t* acc1, uint32_t galois, int level, int dn, cudaStream_t st) {
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
@@ -445,18 +351,6 @@ void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, size_t 
     k_gather_special<<<ew_blocks((size_t)npoly * c.K * c.N), kEwThreads, 0, st>>>(c, dst, acc, acc_stride, level,
                                                                                    npoly);
 }
-void moddown_bconv(const DevCtx& c, const uint64_t* pcoef, uint64_t* conv, const ModDownTable* md, int level,
-                   int npoly, cudaStream_t st) {
-    ++g_launches;
-    k_moddown_bconv<<<ew_blocks((size_t)npoly * c.N), kEwThreads, 0, st>>>(c, pcoef, conv, md, level, npoly);
-}
-void moddown_finish(const DevCtx& c, uint64_t* out, const uint64_t* acc, const uint64_t* conv,
-                    const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
-                    cudaStream_t st) {
-    ++g_launches;
-    k_moddown_finish<<<ew_blocks((size_t)npoly * (level + 1) * c.N), kEwThreads, 0, st>>>(
-        c, out, acc, conv, md, level, npoly, add_src, galois);
-}
 void conv_mac(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* x, const MacTerms& t,
               const ModDownTable* md, int level, int dn, cudaStream_t st) {
     const size_t total = (size_t)(level + 1 + c.K) * c.N;
@@ -471,9 +365,6 @@ namespace {
 // digit pair is the aligned pair {2j, 2j+1} (possibly swapped): every access
 // below is a 16-byte vector load.
 __device__ __forceinline__ ulonglong2 ld2(const uint64_t* p) { return __ldg(reinterpret_cast<const ulonglong2*>(p)); }
-__device__ __forceinline__ ulonglong2 ld2cs(const uint64_t* p) {
-    return __ldcs(reinterpret_cast<const ulonglong2*>(p));
-}
 // volatile (non-reorderable) 16-byte loads: issued in program order so that a
 // whole batch of independent loads is in flight before the first use
 __device__ __forceinline__ ulonglong2 vld2_nc(const uint64_t* p) {
@@ -486,37 +377,8 @@ __device__ __forceinline__ ulonglong2 vld2_cs(const uint64_t* p) {
     asm volatile("ld.global.cs.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
     return r;
 }
-__device__ __forceinline__ uint64_t vld_cs(const uint64_t* p) {
-    uint64_t r;
-    asm volatile("ld.global.cs.u64 %0, [%1];" : "=l"(r) : "l"(p));
-    return r;
-}
 __device__ __forceinline__ void st2(uint64_t* p, uint64_t a, uint64_t b) {
     *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(a, b);
-}
-
-template <int DN>
-__device__ __forceinline__ void ip_pair(const uint64_t* __restrict__ D, const uint64_t* __restrict__ key, int ne,
-                                        int np, int u, int p, uint32_t k, uint32_t pk, int N, U128 (&s0)[2],
-                                        U128 (&s1)[2]) {
-    const uint32_t base = pk & ~1u;
-    const bool swp = pk & 1u;
-    ulonglong2 d[DN], k0[DN], k1[DN];
-#pragma unroll
-    for (int j = 0; j < DN; ++j) {
-        k0[j] = vld2_cs(key + (((size_t)j * 2 + 0) * np + p) * N + k);
-        k1[j] = vld2_cs(key + (((size_t)j * 2 + 1) * np + p) * N + k);
-    }
-#pragma unroll
-    for (int j = 0; j < DN; ++j) d[j] = vld2_nc(D + ((size_t)j * ne + u) * N + base);
-#pragma unroll
-    for (int j = 0; j < DN; ++j) {
-        const uint64_t da = swp ? d[j].y : d[j].x, db = swp ? d[j].x : d[j].y;
-        mac(s0[0], da, k0[j].x);
-        mac(s0[1], db, k0[j].y);
-        mac(s1[0], da, k1[j].x);
-        mac(s1[1], db, k1[j].y);
-    }
 }
 
 // ---- cp.async (LDGSTS) helpers: per-thread asynchronous 16-byte copies to smem
@@ -621,71 +483,6 @@ __global__ void __launch_bounds__(kStreamThreads) k_ks_stream(DevCtx c, KsStream
 // ---- batched key switching: work item = (coefficient pair, source), source
 // fastest, so the lanes of a warp that share a pair issue identical key
 // addresses (one transaction serves all sources of the batch).
-template <int DN, int MODE>
-__global__ void __launch_bounds__(256) k_ks_batch(DevCtx c, KsBatch a, const ModDownTable* md, int level) {
-    const int nr = level + 1, ne = nr + c.K;
-    const int np = c.L + c.K;
-    const size_t total = (size_t)ne * c.N;
-    const size_t items = (total / 2) * a.nsrc;
-    RowMap rm{ne, level, c.L, 0};
-    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < items; it += (size_t)gridDim.x * blockDim.x) {
-        const int s = (int)(it % a.nsrc);
-        const size_t i = (it / a.nsrc) * 2;
-        const int u = (int)(i >> c.logN);
-        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
-        const int p = row_prime(rm, u);
-        const Prime pr = c.primes[p];
-        const bool qrow = u < nr;
-        const uint64_t pm = qrow ? md->pmod[u] : 0, pms = qrow ? md->pmod_sh[u] : 0;
-        U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
-        for (int t = 0; t < a.n; ++t) {
-            const uint32_t pk = perm_index(k, a.galois[t], c.logN);
-            const bool swp = pk & 1u;
-            const uint64_t* key = a.key[t];
-            const uint64_t* D = a.digits + (size_t)s * a.digit_src_stride + (size_t)t * a.digit_term_stride;
-            const uint64_t* c0 = a.c0 + (size_t)s * a.c0_src_stride + a.c0_off[t];
-            ulonglong2 k0[DN], k1[DN], d[DN];
-#pragma unroll
-            for (int j = 0; j < DN; ++j) {
-                k0[j] = vld2_nc(key + (((size_t)j * 2 + 0) * np + p) * c.N + k);
-                k1[j] = vld2_nc(key + (((size_t)j * 2 + 1) * np + p) * c.N + k);
-                d[j] = vld2_nc(D + ((size_t)j * ne + u) * c.N + (pk & ~1u));
-            }
-            const ulonglong2 x = (a.c0_qp || qrow) ? vld2_nc(c0 + (size_t)u * c.N + (pk & ~1u)) : make_ulonglong2(0, 0);
-            if (MODE == 0) s0[0] = s0[1] = s1[0] = s1[1] = U128{0, 0};
-#pragma unroll
-            for (int j = 0; j < DN; ++j) {
-                const uint64_t da = swp ? d[j].y : d[j].x, db = swp ? d[j].x : d[j].y;
-                mac(s0[0], da, k0[j].x);
-                mac(s0[1], db, k0[j].y);
-                mac(s1[0], da, k1[j].x);
-                mac(s1[1], db, k1[j].y);
-            }
-            if (a.c0_qp) {
-                add128(s0[0], swp ? x.y : x.x);
-                add128(s0[1], swp ? x.x : x.y);
-            } else if (qrow) {
-                add128(s0[0], mul_shoup(swp ? x.y : x.x, pm, pms, pr.q));
-                add128(s0[1], mul_shoup(swp ? x.x : x.y, pm, pms, pr.q));
-            }
-            if (MODE == 0) {
-                uint64_t* xt = a.out + (size_t)s * a.out_src_stride + (size_t)a.slot[t] * 2 * total;
-                st2(xt + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
-                st2(xt + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
-            }
-        }
-        if (MODE == 1) {
-            uint64_t* acc = a.out + (size_t)s * a.out_src_stride;
-            const ulonglong2 a0 = ld2(acc + i), a1 = ld2(acc + total + i);
-            add128(s0[0], a0.x);
-            add128(s0[1], a0.y);
-            add128(s1[0], a1.x);
-            add128(s1[1], a1.y);
-            st2(acc + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
-            st2(acc + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
-        }
-    }
-}
 
 // batched plaintext mat-vec: Y[s][g] = sum_b pt[g][b] * XT[s][b] (item = (pair, source),
 // the sources of a pair share every plaintext load)
@@ -786,93 +583,8 @@ __global__ void k_identity_term(DevCtx c, uint64_t* xt, const uint64_t* X, const
 }
 
 // XT[b][c] = (IP_0(D, key_b) + [u<=l] P sigma_b(X.c0), IP_1(D, key_b)); identity b: P X
-template <int DN>
-__global__ void __launch_bounds__(256) k_ks_multi(DevCtx c, uint64_t* XT, const uint64_t* D, const uint64_t* X,
-                                                  BabyTerms t, const ModDownTable* md, int level) {
-    const int nr = level + 1, ne = nr + c.K;
-    const int np = c.L + c.K;
-    const size_t total = (size_t)ne * c.N;
-    const size_t pairs = total / 2;
-    RowMap rm{ne, level, c.L, 0};
-    for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < pairs; ip += (size_t)gridDim.x * blockDim.x) {
-        const size_t i = ip * 2;
-        const int u = (int)(i >> c.logN);
-        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
-        const int p = row_prime(rm, u);
-        const Prime pr = c.primes[p];
-        const bool qrow = u < nr;
-        const uint64_t pm = qrow ? md->pmod[u] : 0, pms = qrow ? md->pmod_sh[u] : 0;
-        for (int b = 0; b < t.nb; ++b) {
-            uint64_t* xt = XT + (size_t)b * 2 * total;
-            const uint32_t gal = t.galois[b];
-            if (t.gmask[b] == 0) continue;
-            if (gal == 1) {
-                if (qrow) {
-                    const ulonglong2 a = ld2(X + (size_t)u * c.N + k);
-                    const ulonglong2 bb = ld2(X + ((size_t)nr + u) * c.N + k);
-                    st2(xt + i, mul_shoup(a.x, pm, pms, pr.q), mul_shoup(a.y, pm, pms, pr.q));
-                    st2(xt + total + i, mul_shoup(bb.x, pm, pms, pr.q), mul_shoup(bb.y, pm, pms, pr.q));
-                } else {
-                    st2(xt + i, 0, 0);
-                    st2(xt + total + i, 0, 0);
-                }
-                continue;
-            }
-            const uint32_t pk = perm_index(k, gal, c.logN);
-            U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
-            ip_pair<DN>(D, t.key[b], ne, np, u, p, k, pk, c.N, s0, s1);
-            if (qrow) {
-                const ulonglong2 x = ld2(X + (size_t)u * c.N + (pk & ~1u));
-                const bool swp = pk & 1u;
-                add128(s0[0], mul_shoup(swp ? x.y : x.x, pm, pms, pr.q));
-                add128(s0[1], mul_shoup(swp ? x.x : x.y, pm, pms, pr.q));
-            }
-            st2(xt + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
-            st2(xt + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
-        }
-    }
-}
 
 // Y[g][c] = sum_b pt[g][b] * XT[b][c]  (the plaintext "matrix-vector" of the baby steps)
-template <int NG>
-__global__ void __launch_bounds__(256) k_pt_matvec(DevCtx c, uint64_t* Y, const uint64_t* XT, BabyTerms t,
-                                                   int level) {
-    const int ne = level + 1 + c.K;
-    const size_t total = (size_t)ne * c.N;
-    RowMap rm{ne, level, c.L, 0};
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int u = (int)(i >> c.logN);
-        const Prime pr = c.primes[row_prime(rm, u)];
-        U128 a0[NG], a1[NG];
-#pragma unroll
-        for (int g = 0; g < NG; ++g) a0[g] = a1[g] = U128{0, 0};
-        for (int b = 0; b < t.nb; ++b) {
-            const uint32_t mask = t.gmask[b];
-            if (mask == 0) continue;
-            uint64_t w[NG];
-#pragma unroll
-            for (int g = 0; g < NG; ++g)
-                w[g] = (g < t.ngi && ((mask >> g) & 1u))
-                           ? vld_cs(t.pts + (((size_t)(t.g0 + g) * t.nb_total + b) * ne) * c.N + i)
-                           : 0;
-            const uint64_t x0 = vld_cs(XT + (size_t)b * 2 * total + i);
-            const uint64_t x1 = vld_cs(XT + (size_t)b * 2 * total + total + i);
-#pragma unroll
-            for (int g = 0; g < NG; ++g) {
-                mac(a0[g], w[g], x0);
-                mac(a1[g], w[g], x1);
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-            if (g < t.ngi) {
-                uint64_t* y = Y + (size_t)g * 2 * total;
-                y[i] = reduce128(a0[g].hi, a0[g].lo, pr);
-                y[total + i] = reduce128(a1[g].hi, a1[g].lo, pr);
-            }
-        }
-    }
-}
 
 // Plaintext mat-vec on coefficient pairs: the baby-step terms X~_b of the
 // thread's pair are staged once in private shared-memory slots, then every
@@ -1299,75 +1011,6 @@ __global__ void __launch_bounds__(128, 3) k_ks_hoist(DevCtx c, KsBatch a, const 
     }
 }
 
-template <int DN>
-__global__ void __launch_bounds__(256) k_ks_accumulate_t(DevCtx c, uint64_t* acc, const uint64_t* D,
-                                                         const uint64_t* key, const uint64_t* c0, uint32_t g,
-                                                         const ModDownTable* md, int level) {
-    const int nr = level + 1, ne = nr + c.K;
-    const int np = c.L + c.K;
-    const size_t total = (size_t)ne * c.N;
-    RowMap rm{ne, level, c.L, 0};
-    for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < total / 2;
-         ip += (size_t)gridDim.x * blockDim.x) {
-        const size_t i = ip * 2;
-        const int u = (int)(i >> c.logN);
-        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
-        const int p = row_prime(rm, u);
-        const Prime pr = c.primes[p];
-        const uint32_t pk = perm_index(k, g, c.logN);
-        U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
-        ip_pair<DN>(D, key, ne, np, u, p, k, pk, c.N, s0, s1);
-        if (u < nr) {
-            const ulonglong2 x = ld2(c0 + (size_t)u * c.N + (pk & ~1u));
-            const bool swp = pk & 1u;
-            add128(s0[0], mul_shoup(swp ? x.y : x.x, md->pmod[u], md->pmod_sh[u], pr.q));
-            add128(s0[1], mul_shoup(swp ? x.x : x.y, md->pmod[u], md->pmod_sh[u], pr.q));
-        }
-        const ulonglong2 a0 = ld2(acc + i), a1 = ld2(acc + total + i);
-        add128(s0[0], a0.x);
-        add128(s0[1], a0.y);
-        add128(s1[0], a1.x);
-        add128(s1[1], a1.y);
-        st2(acc + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
-        st2(acc + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
-    }
-}
-
-template <int DN>
-__global__ void __launch_bounds__(256, 1) k_ks_accumulate_multi(DevCtx c, uint64_t* acc, GiantTerms t,
-                                                             const ModDownTable* md, int level) {
-    const int nr = level + 1, ne = nr + c.K;
-    const int np = c.L + c.K;
-    const size_t total = (size_t)ne * c.N;
-    RowMap rm{ne, level, c.L, 0};
-    for (size_t ip = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ip < total / 2;
-         ip += (size_t)gridDim.x * blockDim.x) {
-        const size_t i = ip * 2;
-        const int u = (int)(i >> c.logN);
-        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
-        const int p = row_prime(rm, u);
-        const Prime pr = c.primes[p];
-        U128 s0[2] = {{0, 0}, {0, 0}}, s1[2] = {{0, 0}, {0, 0}};
-        for (int g = 0; g < t.n; ++g) {
-            const uint32_t pk = perm_index(k, t.galois[g], c.logN);
-            ip_pair<DN>(t.digits + (size_t)g * DN * total, t.key[g], ne, np, u, p, k, pk, c.N, s0, s1);
-            if (u < nr) {
-                const ulonglong2 x = ld2(t.c0[g] + (size_t)u * c.N + (pk & ~1u));
-                const bool swp = pk & 1u;
-                add128(s0[0], mul_shoup(swp ? x.y : x.x, md->pmod[u], md->pmod_sh[u], pr.q));
-                add128(s0[1], mul_shoup(swp ? x.x : x.y, md->pmod[u], md->pmod_sh[u], pr.q));
-            }
-        }
-        const ulonglong2 a0 = ld2(acc + i), a1 = ld2(acc + total + i);
-        add128(s0[0], a0.x);
-        add128(s0[1], a0.y);
-        add128(s1[0], a1.x);
-        add128(s1[1], a1.y);
-        st2(acc + i, reduce128(s0[0].hi, s0[0].lo, pr), reduce128(s0[1].hi, s0[1].lo, pr));
-        st2(acc + total + i, reduce128(s1[0].hi, s1[0].lo, pr), reduce128(s1[1].hi, s1[1].lo, pr));
-    }
-}
-
 __global__ void k_qp_add(DevCtx c, uint64_t* acc, const uint64_t* y, int level) {
     const int ne = level + 1 + c.K;
     const size_t total = (size_t)2 * ne * c.N;
@@ -1392,16 +1035,6 @@ __global__ void k_qp_add(DevCtx c, uint64_t* acc, const uint64_t* y, int level) 
         case 8: CALL(8); break;    \
         default: break;            \
     }
-
-void ks_multi(const DevCtx& c, uint64_t* XT, const uint64_t* digits, const uint64_t* ct, const BabyTerms& t,
-              const ModDownTable* md, int level, int dn, cudaStream_t st) {
-    const size_t total = (size_t)(level + 1 + c.K) * c.N;
-    const int blocks = ew_blocks(total / 2);
-#define FHE_KS_MULTI(D) k_ks_multi<D><<<blocks, 256, 0, st>>>(c, XT, digits, ct, t, md, level)
-    ++g_launches;
-    FHE_DN_SWITCH(dn, FHE_KS_MULTI)
-#undef FHE_KS_MULTI
-}
 
 // CTA caps of the HBM-streaming kernels (per SM). Smaller grids leave SM room
 // for the integer-bound NTT CTAs of other lanes to co-reside.
@@ -1504,18 +1137,7 @@ void ks_batch(const DevCtx& c, const KsBatch& a, int mode, const ModDownTable* m
 #undef FHE_GIANT
         return;
     }
-    const size_t items = (size_t)(level + 1 + c.K) * c.N / 2 * a.nsrc;
-    const int blocks = (int)((items + 255) / 256 < 148 * 8 ? (items + 255) / 256 : 148 * 8);
-    ++g_launches;
-#define FHE_KSB(D)                                                                     \
-    do {                                                                               \
-        if (mode == 0)                                                                 \
-            k_ks_batch<D, 0><<<blocks, 256, 0, st>>>(c, a, md, level);                 \
-        else                                                                           \
-            k_ks_batch<D, 1><<<blocks, 256, 0, st>>>(c, a, md, level);                 \
-    } while (0)
-    FHE_DN_SWITCH(dn, FHE_KSB)
-#undef FHE_KSB
+    // the host only builds (mode 0, source c0) and (mode 1, P-scaled QP c0) batches
 }
 
 void pt_matvec_batch(const DevCtx& c, uint64_t* Y, size_t y_src_stride, const uint64_t* XT, size_t xt_src_stride,
@@ -1598,26 +1220,6 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
     } while (0)
     FHE_DN_SWITCH(dn, FHE_FUSED)
 #undef FHE_FUSED
-}
-
-void ks_accumulate(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* key, const uint64_t* c0,
-                   uint32_t galois, const ModDownTable* md, int level, int dn, cudaStream_t st) {
-    const size_t total = (size_t)(level + 1 + c.K) * c.N;
-    ++g_launches;
-    const int blocks = ew_blocks(total / 2);
-#define FHE_KS_ACC(D) k_ks_accumulate_t<D><<<blocks, 256, 0, st>>>(c, acc, digits, key, c0, galois, md, level)
-    FHE_DN_SWITCH(dn, FHE_KS_ACC)
-#undef FHE_KS_ACC
-}
-
-void ks_accumulate_multi(const DevCtx& c, uint64_t* acc, const GiantTerms& t, const ModDownTable* md, int level,
-                         int dn, cudaStream_t st) {
-    const size_t total = (size_t)(level + 1 + c.K) * c.N;
-    ++g_launches;
-    const int blocks = ew_blocks(total / 2);
-#define FHE_KS_ACCM(D) k_ks_accumulate_multi<D><<<blocks, 256, 0, st>>>(c, acc, t, md, level)
-    FHE_DN_SWITCH(dn, FHE_KS_ACCM)
-#undef FHE_KS_ACCM
 }
 
 void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st) {

@@ -170,24 +170,11 @@ void rescale_spread(const DevCtx& c, const uint64_t* tmp, uint64_t* spread, int 
 void rescale_finish(const DevCtx& c, uint64_t* out, const uint64_t* in, const uint64_t* spread, int level,
                     const uint64_t* qlinv, const uint64_t* qlinv_sh, cudaStream_t st);
 
-// ModUp FastBConv for nsrc sources: coef = INTT(c1) ([nsrc][level+1][N]);
-// digits [nsrc][dn][ne][N]; own rows copied from the NTT-domain c1 of each
-// source (c1_ntt + s * src_stride), the others in the coefficient domain.
-void modup_bconv(const DevCtx& c, const uint64_t* coef, const uint64_t* c1_ntt, size_t src_stride, int nsrc,
-                 uint64_t* digits, const ModUpDigit* tables, int level, int dn, cudaStream_t st);
 
 // acc_c[u][k] = sum_j D[j][u][perm_g(k)] key[j][c][prime(u)][k], ne = level+1+K rows
 void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* key, uint64_t* acc0,
                       uint64_t* acc1, uint32_t galois, int level, int dn, cudaStream_t st);
 
-// ModDown, batched over npoly polys of ne = level+1+K rows each:
-//  pcoef: [npoly][K][N] INTT'd special rows -> conv: [npoly][level+1][N]
-void moddown_bconv(const DevCtx& c, const uint64_t* pcoef, uint64_t* conv, const ModDownTable* md,
-                   int level, int npoly, cudaStream_t st);
-// out[p][i] = (acc[p][i] - conv[p][i]) P^-1 (+ sigma_g(add_src)[i] for p == 0 if add_src)
-void moddown_finish(const DevCtx& c, uint64_t* out, const uint64_t* acc, const uint64_t* conv,
-                    const ModDownTable* md, int level, int npoly, const uint64_t* add_src, uint32_t galois,
-                    cudaStream_t st);
 // copy the K special rows of each poly's accumulator into [npoly][K][N]
 // dst[p] = src[p * stride] row (N words) for p < npoly
 void gather_row(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t stride, int npoly, cudaStream_t st);
@@ -206,27 +193,8 @@ void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, size_t 
 void conv_mac(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* x, const MacTerms& t,
               const ModDownTable* md, int level, int dn, cudaStream_t st);
 
-// Baby steps of the BSGS conv, in two streaming passes:
-// XT[b] = (IP_0(D, key_b) + [u<=l] P sigma_b(ct.c0), IP_1(D, key_b)) (identity b: P ct) over the
-// QP basis, XT = [nb][2][ne][N], for babies with gmask[b] != 0;
-void ks_multi(const DevCtx& c, uint64_t* XT, const uint64_t* digits, const uint64_t* ct, const BabyTerms& t,
-              const ModDownTable* md, int level, int dn, cudaStream_t st);
 // Y[g][c] = sum_b pt[g0 + g][b] * XT[b][c] for g < t.ngi, Y = [ngi][2][ne][N] (overwritten)
 void pt_matvec(const DevCtx& c, uint64_t* Y, const uint64_t* XT, const BabyTerms& t, int level, cudaStream_t st);
-// acc_0 += IP_0(D, key, g) + [u <= l] P sigma_g(c0);  acc_1 += IP_1(D, key, g)   (acc = [2][ne][N])
-void ks_accumulate(const DevCtx& c, uint64_t* acc, const uint64_t* digits, const uint64_t* key, const uint64_t* c0,
-                   uint32_t galois, const ModDownTable* md, int level, int dn, cudaStream_t st);
-// Giant steps of the BSGS conv, one launch:
-// acc_0 += sum_g IP_0(D_g, key_g) + [u<=l] P sigma_g(c0_g);  acc_1 += sum_g IP_1(D_g, key_g)
-struct GiantTerms {
-    int n;
-    uint32_t galois[kMaxGiant];
-    const uint64_t* key[kMaxGiant];
-    const uint64_t* c0[kMaxGiant];  // [level+1][N] NTT
-    const uint64_t* digits;          // [n][dn][ne][N]
-};
-void ks_accumulate_multi(const DevCtx& c, uint64_t* acc, const GiantTerms& t, const ModDownTable* md, int level,
-                         int dn, cudaStream_t st);
 // Streaming key-switch term list (k_ks_stream): term t uses Galois element
 // galois[t], key[t], digits + t * digit_stride and the NTT-domain c0[t].
 struct KsStream {
