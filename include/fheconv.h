@@ -234,6 +234,17 @@ int fhe_conv2d_batch_host_async(fhe_ctx* ctx, const uint64_t* host_in, size_t n,
 /* waits for every enqueued host-resident batch (and all other work of ctx) */
 int fhe_host_wait(fhe_ctx* ctx);
 
+/* rotate-and-add reduction (reference dense.cpp:23-30):
+ * outs[i] = slot_sum(cts[i], block): log2(block) rotations by 1, 2, 4, ...
+ * each added back; every step rotates the whole batch with the keys shared. */
+int fhe_slot_sum_batch(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, uint64_t block, fhe_ct** outs);
+/* linear head (reference linear(), dense.cpp:34-75): W x + b over the features
+ * of a packed image (t shards as fhe_conv_layer_create(_shards) packs them,
+ * c channels of m x m), W = [out_features][c m^2] row-major, b = [out_features];
+ * output features in slots 0..out_features-1, two levels consumed. */
+int fhe_linear(fhe_ctx* ctx, const fhe_ct* const* shards, size_t t, int c, int m, int out_features, const double* w,
+               const double* b, fhe_ct** out);
+
 #ifdef __cplusplus
 }
 #endif

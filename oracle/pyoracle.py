@@ -126,6 +126,8 @@ def ref():
         R.ref_time_conv.restype = C.c_double
         R.ref_time_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, C.c_uint64,
                                     C.c_int, C.c_int]
+        R.ref_linear.argtypes = [C.c_int, C.c_int, dp, C.c_int, dp, dp, C.c_uint64, dp, u64p]
+        R.ref_slot_sum.argtypes = [dp, C.c_uint64, C.c_uint64, dp]
         R.ref_time_rotations.restype = C.c_double
         R.ref_time_rotations.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, u64p]
         _ref = R
@@ -184,6 +186,24 @@ def ref_conv_channel(c, m, kappa, c_out, img, filt, s):
                         0, s, _ptr(out_slots, dp), _ptr(out_img, dp), _ptr(ledger, u64p), C.byref(drop))
     assert rc == 0
     return out_slots.reshape(n, s), out_img, ledger, drop.value
+
+
+def ref_linear(c, m, img, w, b, s):
+    """the reference's linear() (dense.cpp:71-75) on pack(img, s): output slots, ledger, shard count."""
+    out = np.zeros(s)
+    ledger = np.zeros(9, dtype=np.uint64)
+    t = ref().ref_linear(c, m, _ptr(np.ascontiguousarray(img, dtype=np.float64), dp), len(b),
+                         _ptr(np.ascontiguousarray(w, dtype=np.float64), dp),
+                         _ptr(np.ascontiguousarray(b, dtype=np.float64), dp), s, _ptr(out, dp), _ptr(ledger, u64p))
+    assert t > 0, t
+    return out, ledger, t
+
+
+def ref_slot_sum(vec, block):
+    vec = np.ascontiguousarray(vec, dtype=np.float64)
+    out = np.zeros(vec.size)
+    assert ref().ref_slot_sum(_ptr(vec, dp), vec.size, block, _ptr(out, dp)) == 0
+    return out
 
 
 def emu_oracle_conv(c, m, kappa, c_out, img, filt):

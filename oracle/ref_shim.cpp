@@ -13,6 +13,7 @@
 // (tests/helpers.hpp:13-27: mt19937_64 + uniform_real_distribution), so the
 // golden vectors are exactly what the reference's tests would see.
 #include "shardnn/conv.hpp"
+#include "shardnn/dense.hpp"
 #include "shardnn/oracle.hpp"
 #include "shardnn/pack.hpp"
 #include "shardnn/rot.hpp"
@@ -181,6 +182,42 @@ long ref_plan_rotations(const long* amounts, const int* same_source, int n, uint
             }
         }
         return static_cast<long>(sch.total_keyed_rotations);
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// linear() (dense.cpp:71-75) on an image packed with pack(s): out_slots (s)
+/// receives the output vector (features in slots 0..out-1), the ledger the
+/// reference's op counters. slot_sum (dense.cpp:23-30) of a vector in `vec`
+/// when `sum_block` > 0 (then img/w are ignored and out_slots gets the sum).
+int ref_linear(int c, int m, const double* img, int out_features, const double* w, const double* b, uint64_t s,
+               double* out_slots, uint64_t* ledger) {
+    try {
+        ImageTensor t(c, m);
+        std::memcpy(t.data.data(), img, t.data.size() * sizeof(double));
+        LinearWeights lw((size_t)out_features, (size_t)c * m * m);
+        std::memcpy(lw.w.data(), w, lw.w.size() * sizeof(double));
+        std::memcpy(lw.b.data(), b, lw.b.size() * sizeof(double));
+        Engine eng;
+        PackedImage p = pack(eng, t, s);
+        eng.ledger().reset();
+        SlotVector out = linear(eng, p, lw);
+        std::memcpy(out_slots, out.slots.data(), out.slots.size() * sizeof(double));
+        fill_ledger(eng.ledger(), ledger);
+        return (int)p.shards.size();
+    } catch (...) {
+        return -1;
+    }
+}
+
+int ref_slot_sum(const double* vec, uint64_t s, uint64_t block, double* out) {
+    try {
+        Engine eng;
+        SlotVector v = eng.encode(std::vector<double>(vec, vec + s));
+        SlotVector r = slot_sum(eng, v, block);
+        std::memcpy(out, r.slots.data(), s * sizeof(double));
+        return 0;
     } catch (...) {
         return -1;
     }

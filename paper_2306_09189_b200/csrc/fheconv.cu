@@ -2721,4 +2721,144 @@ int fhe_host_wait(fhe_ctx* c) {
     return guard(c, [&] { host_wait(c); });
 }
 
+
+// ------------------------------------------------ rotate-and-add reduction
+// slot_sum (reference dense.cpp:23-30) and the linear head
+// (masked_feature_dot, dense.cpp:34-67) composed from this library's ops;
+// each slot_sum step rotates the whole batch with one staged key-switch
+// launch (every key row streamed once per 16 ciphertexts).
+static void okc(fhe_ctx* c, int rc) {
+    if (rc != FHE_OK) fail(rc, c->err);
+}
+
+int fhe_slot_sum_batch(fhe_ctx* c, const fhe_ct* const* cts, size_t n, uint64_t block, fhe_ct** outs) {
+    return guard(c, [&] {
+        if (block == 0 || (block & (block - 1)) || c->slots() % block)
+            fail(FHE_E_INVALID, "block must be a power of two dividing the slot count");
+        std::vector<fhe_ct*> acc(n), rot(n);
+        for (size_t i = 0; i < n; ++i) {
+            acc[i] = new_ct(c, cts[i]->level, cts[i]->scale, cts[i]->depth);
+            ck(cudaMemcpyAsync(acc[i]->d, cts[i]->d, cts[i]->words() * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+            rot[i] = new_ct(c, cts[i]->level, cts[i]->scale, cts[i]->depth);
+        }
+        try {
+            for (uint64_t step = 1; step < block; step *= 2) {
+                const int64_t k = (int64_t)step;
+                okc(c, fhe_rotate_hoisted_batch_into(c, acc.data(), n, &k, 1, rot.data()));
+                c->ledger.hoist_groups -= n;  // sequential rotations, not hoisted groups
+                c->ledger.hoisted_rotations -= n;
+                c->ledger.rotations += n;
+                for (size_t i = 0; i < n; ++i) {
+                    ew_add(c->dc, acc[i]->d, acc[i]->d, rot[i]->d, 2 * (acc[i]->level + 1), acc[i]->level + 1, c->st);
+                    c->ledger.adds++;
+                }
+            }
+        } catch (...) {
+            for (size_t i = 0; i < n; ++i) {
+                fhe_ct_free(acc[i]);
+                fhe_ct_free(rot[i]);
+            }
+            throw;
+        }
+        for (size_t i = 0; i < n; ++i) {
+            fhe_ct_free(rot[i]);
+            outs[i] = acc[i];
+        }
+    });
+}
+
+int fhe_linear(fhe_ctx* c, const fhe_ct* const* shards, size_t t, int ch, int m, int out_features, const double* w,
+               const double* b, fhe_ct** out) {
+    return guard(c, [&] {
+        const size_t s = c->slots(), block = (size_t)m * m, nin = (size_t)ch * block;
+        if (t == 0 || !shards || !w || !b || !out) fail(FHE_E_INVALID, "null argument");
+        if (out_features <= 0 || (size_t)out_features > s) fail(FHE_E_INVALID, "out_features exceeds the shard size");
+        // slot -> feature map (reference slot_feature_map pack.cpp:109-129, identity tau, rep 1):
+        // image mode: slot i of shard u holds feature u s + i below c m^2 (the primary
+        // replica when the image is duplicated); channel mode: channel-major rows.
+        const bool channel_mode = block > s;
+        const size_t expect_t = channel_mode ? nin / s : std::max<size_t>(1, nin / s);
+        if (t != expect_t) fail(FHE_E_INVALID, "shard count does not match the packed feature count");
+        const int level = shards[0]->level;
+        if (level < 2) fail(FHE_E_RUNTIME, "depth exhausted");
+        auto feat = [&](size_t u, size_t i) -> long {
+            const size_t f = u * s + i;
+            return f < nin ? (long)f : -1;
+        };
+        // products W_o . x_u for every output feature and shard, one level
+        std::vector<fhe_ct*> prods;
+        std::vector<int> prod_o;
+        std::vector<double> wt(s);
+        const double ql = (double)c->primes[level];
+        for (int o = 0; o < out_features; ++o) {
+            bool started = false;
+            for (size_t u = 0; u < t; ++u) {
+                bool any = false;
+                for (size_t i = 0; i < s; ++i) {
+                    const long f = feat(u, i);
+                    wt[i] = f < 0 ? 0.0 : w[(size_t)o * nin + (size_t)f];
+                    any = any || wt[i] != 0.0;
+                }
+                if (!any && started) continue;
+                fhe_pt* pt = nullptr;
+                fhe_ct *pr = nullptr, *rs = nullptr;
+                okc(c, fhe_encode(c, wt.data(), s, level, ql, 0, &pt));
+                okc(c, fhe_mul_plain(c, shards[u], pt, &pr));
+                okc(c, fhe_rescale(c, pr, &rs));
+                fhe_pt_free(pt);
+                fhe_ct_free(pr);
+                prods.push_back(rs);
+                prod_o.push_back(o);
+                started = true;
+            }
+        }
+        std::vector<fhe_ct*> sums(prods.size());
+        okc(c, fhe_slot_sum_batch(c, prods.data(), prods.size(), s, sums.data()));
+        for (fhe_ct* x : prods) fhe_ct_free(x);
+        // per output: sum over shards, select slot o (second level), accumulate
+        fhe_ct* acc = nullptr;
+        std::vector<double> sel(s, 0.0);
+        size_t k = 0;
+        for (int o = 0; o < out_features; ++o) {
+            fhe_ct* total = sums[k++];
+            while (k < sums.size() && prod_o[k] == o) {
+                fhe_ct* nt = nullptr;
+                okc(c, fhe_add(c, total, sums[k], &nt));
+                fhe_ct_free(total);
+                fhe_ct_free(sums[k]);
+                total = nt;
+                ++k;
+            }
+            std::fill(sel.begin(), sel.end(), 0.0);
+            sel[(size_t)o] = 1.0;
+            fhe_pt* pt = nullptr;
+            fhe_ct *pr = nullptr, *rs = nullptr;
+            okc(c, fhe_encode(c, sel.data(), s, total->level, (double)c->primes[total->level], 0, &pt));
+            okc(c, fhe_mul_plain(c, total, pt, &pr));
+            okc(c, fhe_rescale(c, pr, &rs));
+            fhe_pt_free(pt);
+            fhe_ct_free(pr);
+            fhe_ct_free(total);
+            if (!acc) {
+                acc = rs;
+            } else {
+                fhe_ct* na = nullptr;
+                okc(c, fhe_add(c, acc, rs, &na));
+                fhe_ct_free(acc);
+                fhe_ct_free(rs);
+                acc = na;
+            }
+        }
+        std::vector<double> bias(s, 0.0);
+        for (int o = 0; o < out_features; ++o) bias[(size_t)o] = b[o];
+        fhe_pt* bp = nullptr;
+        okc(c, fhe_encode(c, bias.data(), s, acc->level, acc->scale, 0, &bp));
+        fhe_ct* res = nullptr;
+        okc(c, fhe_add_plain(c, acc, bp, &res));
+        fhe_pt_free(bp);
+        fhe_ct_free(acc);
+        *out = res;
+    });
+}
+
 }  // extern "C"

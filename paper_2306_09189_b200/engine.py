@@ -313,6 +313,21 @@ class Context:
         o = (C.c_void_p * len(outs))(*[x.h for x in outs])
         self._check(lib().fhe_conv2d_shards_into(self.h, ins, len(in_shards) // layer.t, layer.h, o))
 
+    def slot_sum_batch(self, cts: Sequence[Ciphertext], block: int) -> list[Ciphertext]:
+        """fhe_slot_sum_batch: rotate-and-add block sums of every ciphertext (reference slot_sum)."""
+        ins = (C.c_void_p * max(1, len(cts)))(*[x.h for x in cts])
+        outs = (C.c_void_p * max(1, len(cts)))()
+        self._check(lib().fhe_slot_sum_batch(self.h, ins, len(cts), block, outs))
+        return [Ciphertext(self, outs[i]) for i in range(len(cts))]
+
+    def linear(self, shards: Sequence[Ciphertext], c: int, m: int, w, b) -> Ciphertext:
+        """fhe_linear: W x + b over a packed image's features (reference linear())."""
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        ins = (C.c_void_p * len(shards))(*[x.h for x in shards])
+        return self._new(lib().fhe_linear, ins, len(shards), c, m, len(b), w.ctypes.data_as(_lib.dp),
+                         b.ctypes.data_as(_lib.dp))
+
     def conv2d(self, ct: Ciphertext, layer: ConvLayer, approach: int = 2) -> Ciphertext:
         return self._new(lib().fhe_conv2d, ct.h, layer.h, approach)
 

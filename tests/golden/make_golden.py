@@ -38,6 +38,13 @@ MS_CASES = {
     "ms_cfg1_c4to8": (4, 32, 3, 8, 1012, 2012, 0, 4096),    # t = 1, n_out = 2
     "ms_cfg3_c32": (32, 32, 3, 32, 1013, 2013, 0, 16384),   # t = 2, n_out = 2
 }
+# linear head: (c, m, s, out_features, seed)
+LIN_CASES = {
+    "lin_cfg1_c4m32": (4, 32, 4096, 4, 1030),     # one shard
+    "lin_cfg1_c8m32": (8, 32, 4096, 3, 1031),     # two image shards
+    "lin_cfg1_c2m16": (2, 16, 4096, 3, 1032),     # duplicated single shard (d = 8)
+    "lin_cfg1_c1m128": (1, 128, 4096, 2, 1033),   # four channel shards
+}
 # channel-shard mode (conv_channel_shards conv.cpp:273-362): m^2 > s, pc = m^2 / s shards per channel
 CS_CASES = {
     "cs_cfg1_c2m128": (2, 128, 3, 2, 1020, 2020, 0, 4096),     # pc = 4
@@ -86,6 +93,22 @@ def main():
         out[f"{name}/img_sum"] = np.array([img.sum(), np.abs(img).sum()])
         out[f"{name}/slots"] = slots
         out[f"{name}/ledger"] = ledger
+    # the linear head (dense.cpp:34-75) and slot_sum (dense.cpp:23-30)
+    for name, (c, m, s, no, si) in LIN_CASES.items():
+        img, _ = po.make_inputs(c, m, 1, 1, si, 0, 0, use_ref=True)
+        rng = np.random.default_rng(si)
+        w = rng.uniform(-1, 1, no * c * m * m)
+        b = rng.uniform(-1, 1, no)
+        slots, ledger, t = po.ref_linear(c, m, img, w, b, s)
+        out[f"{name}/params"] = np.array([c, m, s, no, si, t], dtype=np.int64)
+        out[f"{name}/w_sum"] = np.array([w.sum()])
+        out[f"{name}/slots"] = slots[:no]
+        out[f"{name}/ledger"] = ledger
+    rng = np.random.default_rng(77)
+    vec = rng.uniform(-1, 1, 4096)
+    out["slot_sum/vec_sum"] = np.array([vec.sum()])
+    for block in (1, 4, 64, 4096):
+        out[f"slot_sum/block{block}"] = po.ref_slot_sum(vec, block)
     # cfg5: three stacked layers, each input = previous output image
     x, _ = po.make_inputs(CFG5["c"], CFG5["m"], CFG5["kappa"], CFG5["c"], CFG5["seed_img"], 0, 0, use_ref=True)
     out["cfg5/img_sum"] = np.array([x.sum(), np.abs(x).sum()])

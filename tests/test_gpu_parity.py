@@ -411,3 +411,76 @@ def test_channel_shard_conv_cfg3_5x5(oracle, golden):
     outs = p.ctx.conv2d_shards(cts, layer)
     for v, o in enumerate(outs):
         assert np.abs(p.ctx.decrypt(o) - golden["cs_cfg3_c1m256k5/slots"][v]).max() < TOL
+
+
+def _golden_slot_sum(ck, x, level, block):
+    acc = x
+    step = 1
+    while step < block:
+        acc = ck.add(acc, ck.rotate(acc, level, step), level)
+        step *= 2
+    return acc
+
+
+def test_slot_sum_batch_bit_exact(oracle, golden, p1):
+    """fhe_slot_sum_batch (each step one batched keyed rotation) = sequential golden-model
+    rotate-and-add, and decrypts to the reference's slot_sum."""
+    vec = np.random.default_rng(77).uniform(-1, 1, 4096)
+    p1.ctx.gen_galois_keys([1 << i for i in range(12)])
+    cts = [p1.ctx.encrypt(p1.ctx.encode(np.roll(vec, -i)), ENC_SEED + i) for i in range(3)]
+    outs = p1.ctx.slot_sum_batch(cts, 64)
+    for i, ct in enumerate(cts):
+        ctr = p1.ck.encrypt(p1.ck.encode(np.roll(vec, -i), p1.ck.scale, p1.top), p1.top, ENC_SEED + i)
+        assert np.array_equal(outs[i].residues(), _golden_slot_sum(p1.ck, ctr, p1.top, 64))
+    assert np.abs(p1.ctx.decrypt(outs[0]) - golden["slot_sum/block64"]).max() < TOL
+
+
+@pytest.mark.parametrize("name", ["lin_cfg1_c4m32", "lin_cfg1_c8m32", "lin_cfg1_c2m16", "lin_cfg1_c1m128"])
+def test_linear_bit_exact_and_within_tolerance(oracle, golden, p1, name):
+    """SURVEY §8(f) 3, the linear head: fhe_linear = the golden model's op sequence (masked products,
+    slot sums, selection, bias) bit for bit, decrypted within 1e-6 of the reference's linear()."""
+    c, m, s, no, si, t = (int(x) for x in golden[f"{name}/params"])
+    img, _ = oracle.make_inputs(c, m, 1, 1, si, 0, 0)
+    rng = np.random.default_rng(si)
+    w = rng.uniform(-1, 1, no * c * m * m)
+    b = rng.uniform(-1, 1, no)
+    flat = img if img.size >= s else np.tile(img, s // img.size)
+    chunks = [flat[u * s:(u + 1) * s] for u in range(t)]
+    p1.ctx.gen_galois_keys([1 << i for i in range(12)])
+    cts = [p1.ctx.encrypt(p1.ctx.encode(x), ENC_SEED + u) for u, x in enumerate(chunks)]
+    out = p1.ctx.linear(cts, c, m, w, b)
+    dec = p1.ctx.decrypt(out)
+    # cfg1 scale 2^40 and up to 8192-term dot products (|y| ~ 30): the CKKS noise of the
+    # summed products is held to 1e-6 relative to max(1, |y|); residues are bit-exact below
+    want = golden[f"{name}/slots"]
+    assert (np.abs(dec[:no] - want) / np.maximum(1.0, np.abs(want))).max() < TOL
+    assert np.abs(dec[no:]).max() < TOL
+    # golden model, the same op sequence
+    ck, L = p1.ck, p1.top
+    nin = c * m * m
+    shards = [ck.encrypt(ck.encode(x, ck.scale, L), L, ENC_SEED + u) for u, x in enumerate(chunks)]
+    sums = []
+    for o in range(no):
+        started = False
+        for u in range(t):
+            feat = np.arange(u * s, (u + 1) * s)
+            wt = np.where(feat < nin, w.reshape(no, nin)[o][np.minimum(feat, nin - 1)], 0.0)
+            if not wt.any() and started:
+                continue
+            x = ck.rescale(ck.mul_plain(shards[u], ck.encode(wt, float(ck.primes[L]), L), L), L)
+            sums.append((o, _golden_slot_sum(ck, x, L - 1, s)))
+            started = True
+    acc = None
+    for o in range(no):
+        parts = [x for oo, x in sums if oo == o]
+        total = parts[0]
+        for x in parts[1:]:
+            total = ck.add(total, x, L - 1)
+        sel = np.zeros(s)
+        sel[o] = 1.0
+        y = ck.rescale(ck.mul_plain(total, ck.encode(sel, float(ck.primes[L - 1]), L - 1), L - 1), L - 1)
+        acc = y if acc is None else ck.add(acc, y, L - 2)
+    bias = np.zeros(s)
+    bias[:no] = b
+    ref = ck.add_plain(acc, ck.encode(bias, ck.scale, L - 2), L - 2)
+    assert np.array_equal(out.residues(), ref)

@@ -146,3 +146,32 @@ def test_channel_shard_restatement_bit_exact(oracle, golden, name):
     assert np.array_equal(got, golden[f"{name}/slots"])
     want = oracle.emu_oracle_conv(c, m, k, co, img, filt)
     assert np.abs(got.ravel() - want).max() < 1e-12
+
+
+def test_slot_sum_restatement_bit_exact(golden):
+    """rotate-and-add block sums (reference slot_sum, dense.cpp:23-30) restated with numpy,
+    bit-exact against the reference for block 1, 4, 64 and the whole vector."""
+    vec = np.random.default_rng(77).uniform(-1, 1, 4096)
+    assert vec.sum() == golden["slot_sum/vec_sum"][0]
+    for block in (1, 4, 64, 4096):
+        acc = vec.copy()
+        step = 1
+        while step < block:
+            acc = acc + np.roll(acc, -step)
+            step *= 2
+        assert np.array_equal(acc, golden[f"slot_sum/block{block}"])
+
+
+@pytest.mark.parametrize("name", ["lin_cfg1_c4m32", "lin_cfg1_c8m32", "lin_cfg1_c2m16", "lin_cfg1_c1m128"])
+def test_linear_reference_is_wx_plus_b(oracle, golden, name):
+    """the reference's linear() over every packing (one shard, image shards, duplicated shard,
+    channel shards) equals W x + b; rotations = out x shards x log2(s) (test_dense.cpp:137-148)."""
+    c, m, s, no, si, t = (int(x) for x in golden[f"{name}/params"])
+    img, _ = oracle.make_inputs(c, m, 1, 1, si, 0, 0)
+    rng = np.random.default_rng(si)
+    w = rng.uniform(-1, 1, no * c * m * m)
+    b = rng.uniform(-1, 1, no)
+    assert np.isclose(w.sum(), golden[f"{name}/w_sum"][0])
+    want = w.reshape(no, -1) @ img + b
+    assert np.abs(golden[f"{name}/slots"] - want).max() < 1e-12
+    assert int(golden[f"{name}/ledger"][0]) == no * t * int(np.log2(s))
