@@ -245,6 +245,14 @@ int fhe_slot_sum_batch(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, uint64_
 int fhe_linear(fhe_ctx* ctx, const fhe_ct* const* shards, size_t t, int c, int m, int out_features, const double* w,
                const double* b, fhe_ct** out);
 
+/* 2x2 average pooling (reference pool(), pool.cpp:291-297) of an
+ * image-mode feature map without duplication (c m^2 = t * slots; t = 1, 2 or a
+ * multiple of 4): outs (n_out ciphertexts, at most t) hold the (m/2)^2 channels
+ * with the reference's packing metadata: tau_out[c] (physical channel position ->
+ * logical channel), rep_out, d_out (duplication). Three levels. */
+int fhe_pool(fhe_ctx* ctx, const fhe_ct* const* in, size_t t, int c, int m, fhe_ct** outs, size_t* n_out,
+             int64_t* tau_out, int* rep_out, int* d_out);
+
 #ifdef __cplusplus
 }
 #endif

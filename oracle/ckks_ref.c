@@ -1312,6 +1312,48 @@ int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int
     return (int)((size_t)c_out * pc);
 }
 
+/* Plaintext-weighted sum of hoisted rotations (the linear-transform primitive
+ * the pooling stages are built from): out = Rescale(ModDown(sum_b pt_b * X~_b))
+ * with X~_b the QP-basis rotation of ct by amounts[b] (P sigma(c0) folded in,
+ * identity: P ct) and pt_b encoded over Q_l u P at scale q_l (ck_encode_plain
+ * with_p = 1), pts = [n][level+1+K][N]. Equals sum_b pt_b * rot_b(ct) after
+ * one rescale. */
+void ck_lintrans(const ck_ctx* ck, const uint64_t* ct, int level, int n, const long* amounts, const uint64_t* pts,
+                 uint64_t* out) {
+    const size_t N = ck->N;
+    const int nr = level + 1, ne = nr + ck->K, dn = ck_dnum_at(ck, level);
+    const size_t extw = (size_t)ne * N, ctw = (size_t)2 * nr * N;
+    uint64_t Pmod[CK_MAXP];
+    for (int u = 0; u < ne; u++) {
+        const uint64_t q = ck->q[ext_prime(ck, level, u)];
+        uint64_t P = 1;
+        for (int k = 0; k < ck->K; k++) P = ck_mulmod(P, ck->q[ck->L + k] % q, q);
+        Pmod[u] = u < nr ? P : 0;
+    }
+    key_cache kc = {.n = 0};
+    uint64_t* dsrc = malloc((size_t)dn * extw * 8);
+    ck_modup(ck, ct + (size_t)nr * N, level, dsrc);
+    uint64_t* ip0 = malloc(extw * 8);
+    uint64_t* ip1 = malloc(extw * 8);
+    uint64_t* y = calloc(2 * extw, 8);
+    for (int b = 0; b < n; b++) {
+        const uint64_t g = ck_galois_elt(ck, amounts[b]);
+        const uint64_t* pt = pts + (size_t)b * extw;
+        if (g == 1) {
+            conv_accumulate(ck, level, pt, ct, 1, NULL, NULL, Pmod, y, y + extw);
+        } else {
+            ck_inner_product(ck, dsrc, level, cache_get(ck, &kc, g), g, ip0, ip1);
+            conv_accumulate(ck, level, pt, ct, g, ip0, ip1, Pmod, y, y + extw);
+        }
+    }
+    uint64_t* md = malloc(ctw * 8);
+    ck_moddown(ck, y, level, md);
+    ck_moddown(ck, y + extw, level, md + (size_t)nr * N);
+    ck_rescale(ck, md, level, out);
+    cache_free(&kc);
+    free(dsrc); free(ip0); free(ip1); free(y); free(md);
+}
+
 int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,
             const double* filt, int plan, uint64_t* out, double* out_scale) {
     const size_t N = ck->N, s = N / 2, block = (size_t)m * m;

@@ -110,6 +110,11 @@ int ck_conv_shards(const ck_ctx* ck, const uint64_t* cts, int t, int level, int 
 int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int m, int kappa, int c_out,
                     const double* filt, uint64_t* outs, double* out_scale);
 
+/* out = Rescale(ModDown(sum_b pt_b * rot_{amounts[b]}(ct))) with QP-basis rotations;
+ * pts [n][level+1+K][N] encoded over Q_l u P at scale q_l (see ckks_ref.c) */
+void ck_lintrans(const ck_ctx* ck, const uint64_t* ct, int level, int n, const long* amounts, const uint64_t* pts,
+                 uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

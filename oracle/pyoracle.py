@@ -88,6 +88,7 @@ def lib():
         L.ck_conv_shards.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp,
                                      u64p, dp]
         L.ck_conv_channel.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp, u64p, dp]
+        L.ck_lintrans.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, lp, u64p, u64p]
         L.emu_make_inputs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
                                       C.c_int, dp, dp]
         L.emu_rotate.argtypes = [dp, dp, C.c_size_t, C.c_long]
@@ -127,6 +128,7 @@ def ref():
         R.ref_time_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, C.c_uint64,
                                     C.c_int, C.c_int]
         R.ref_linear.argtypes = [C.c_int, C.c_int, dp, C.c_int, dp, dp, C.c_uint64, dp, u64p]
+        R.ref_pool.argtypes = [C.c_int, C.c_int, dp, C.c_uint64, dp, C.c_int, u64p, u64p, u64p]
         R.ref_slot_sum.argtypes = [dp, C.c_uint64, C.c_uint64, dp]
         R.ref_time_rotations.restype = C.c_double
         R.ref_time_rotations.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, u64p]
@@ -197,6 +199,18 @@ def ref_linear(c, m, img, w, b, s):
                          _ptr(np.ascontiguousarray(b, dtype=np.float64), dp), s, _ptr(out, dp), _ptr(ledger, u64p))
     assert t > 0, t
     return out, ledger, t
+
+
+def ref_pool(c, m, img, s):
+    """the reference's pool() of pack(img, s): (shard slots [n][s], meta [m, c, d, rep, mode, n], tau, ledger)."""
+    out = np.zeros(16 * s)
+    meta = np.zeros(6, dtype=np.uint64)
+    tau = np.zeros(c, dtype=np.uint64)
+    ledger = np.zeros(9, dtype=np.uint64)
+    n = ref().ref_pool(c, m, _ptr(np.ascontiguousarray(img, dtype=np.float64), dp), s, _ptr(out, dp), 16,
+                       _ptr(meta, u64p), _ptr(tau, u64p), _ptr(ledger, u64p))
+    assert n > 0, n
+    return out[: n * s].reshape(n, s), meta, tau, ledger
 
 
 def ref_slot_sum(vec, block):
@@ -408,6 +422,16 @@ class CKKS:
                                   C.byref(sc))
         assert rc == n_out, rc
         return out, sc.value
+
+    def lintrans(self, ct, level, amounts, slot_vectors):
+        """Rescale(ModDown(sum_b pt_b * rot_{amounts[b]}(ct))), pt_b = slot_vectors[b] encoded over
+        Q_level u P at scale q_level."""
+        pts = np.stack([self.encode(v, float(self.primes[level]), level, with_p=True) for v in slot_vectors])
+        a = (C.c_long * len(amounts))(*amounts)
+        out = np.zeros((2, level, self.N), dtype=np.uint64)
+        lib().ck_lintrans(self.h, _ptr(np.ascontiguousarray(ct), u64p), level, len(amounts), a,
+                          _ptr(np.ascontiguousarray(pts), u64p), _ptr(out, u64p))
+        return out
 
     def conv_channel(self, cts, level, c, m, kappa, c_out, filt):
         """channel-shard conv: cts [c * pc][2][level+1][N] -> [c_out * pc][2][level][N]."""

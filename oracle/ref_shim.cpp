@@ -14,6 +14,7 @@
 // golden vectors are exactly what the reference's tests would see.
 #include "shardnn/conv.hpp"
 #include "shardnn/dense.hpp"
+#include "shardnn/pool.hpp"
 #include "shardnn/oracle.hpp"
 #include "shardnn/pack.hpp"
 #include "shardnn/rot.hpp"
@@ -218,6 +219,35 @@ int ref_slot_sum(const double* vec, uint64_t s, uint64_t block, double* out) {
         SlotVector r = slot_sum(eng, v, block);
         std::memcpy(out, r.slots.data(), s * sizeof(double));
         return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// pool() (pool.cpp:291-297): 2x2 average pooling of pack(img, s). Writes the
+/// pooled shards' slots (out_slots, up to `cap` shards), meta = [m, c, d, rep,
+/// mode, n_shards] and tau (c entries). Returns the shard count.
+int ref_pool(int c, int m, const double* img, uint64_t s, double* out_slots, int cap, uint64_t* meta,
+             uint64_t* tau, uint64_t* ledger) {
+    try {
+        ImageTensor t(c, m);
+        std::memcpy(t.data.data(), img, t.data.size() * sizeof(double));
+        Engine eng;
+        PackedImage p = pack(eng, t, s);
+        eng.ledger().reset();
+        PackedImage out = pool(eng, p);
+        const int n = (int)out.shards.size();
+        for (int u = 0; u < n && u < cap; ++u)
+            std::memcpy(out_slots + (size_t)u * s, out.shards[(size_t)u].slots.data(), s * sizeof(double));
+        meta[0] = out.m;
+        meta[1] = out.c;
+        meta[2] = out.d;
+        meta[3] = out.rep;
+        meta[4] = out.mode == ShardMode::ImageShard ? 0 : 1;
+        meta[5] = (uint64_t)n;
+        for (size_t j = 0; j < out.tau.size(); ++j) tau[j] = out.tau[j];
+        fill_ledger(eng.ledger(), ledger);
+        return n;
     } catch (...) {
         return -1;
     }

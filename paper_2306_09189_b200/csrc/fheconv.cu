@@ -96,6 +96,8 @@ struct fhe_ctx {
         uint64_t last_use = 0;
     };
     std::vector<GraphEntry> graphs;
+    // device plaintexts of the pooling stages, keyed by (stage, m, level)
+    std::map<std::string, uint64_t*> lt_cache;
     bool use_graphs = true;
     uint64_t graph_clock = 0;
     struct ProfRec {
@@ -1435,6 +1437,83 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
     c->release(buf);
 }
 
+// out_s = Rescale(ModDown(sum_b pt_b * X~_{s,b})) for S ciphertexts sharing the
+// term list (rotation amount, plaintext slot vector): the fused baby-step
+// kernel with one accumulator; pt_b = rot-free slot vectors encoded over
+// Q_l u P at scale q_l and cached under `key`. One level.
+void lintrans_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const std::string& key,
+                    const std::vector<int64_t>& amounts, const std::vector<std::vector<double>>& vecs,
+                    fhe_ct* const* outs) {
+    const int level = cts[0]->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
+    const int nb = (int)amounts.size();
+    if (level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
+    const std::string ck_key = key + "/" + std::to_string(level);
+    auto it = c->lt_cache.find(ck_key);
+    uint64_t* pts = nullptr;
+    if (it == c->lt_cache.end()) {
+        ck(cudaMalloc(&pts, (size_t)nb * extw * 8), "cudaMalloc");
+        for (int b = 0; b < nb; ++b)
+            encode_rows(c, vecs[(size_t)b].data(), vecs[(size_t)b].size(), level, (double)c->primes[level], ne,
+                        pts + (size_t)b * extw);
+        ck(cudaStreamSynchronize(c->st), "sync");
+        c->lt_cache[ck_key] = pts;
+    } else {
+        pts = it->second;
+    }
+    uint64_t* buf = c->alloc((size_t)S * ctw);
+    for (int i = 0; i < S; ++i)
+        ck(cudaMemcpyAsync(buf + (size_t)i * ctw, cts[i]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    uint64_t* dig = c->alloc((size_t)S * dw);
+    modup_batch(c, buf + (size_t)nr * N, ctw, S, level, dig);
+    uint64_t* Y = c->alloc((size_t)S * 2 * extw);
+    ck(cudaMemsetAsync(Y, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
+    FusedBsgs f{};
+    f.nsrc = S;
+    f.ng = 1;
+    f.digits = dig;
+    f.digit_src_stride = dw;
+    f.ct = buf;
+    f.ct_src_stride = ctw;
+    f.Y = Y;
+    f.y_src_stride = 2 * extw;
+    f.y_g_stride = 2 * extw;
+    f.accumulate = 1;
+    for (int b0 = 0; b0 < nb; b0 += kMaxFused) {
+        f.nb = 0;
+        double keyed = 0;
+        for (int b = b0; b < nb && f.nb < kMaxFused; ++b) {
+            const uint32_t gal = c->galois_of(c->reduce_amount(amounts[(size_t)b]));
+            f.galois[f.nb] = gal;
+            f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+            f.gmask[f.nb] = 1;
+            f.pt[f.nb] = pts + (size_t)b * extw;
+            f.srcslot[f.nb] = 0;
+            f.nb++;
+            if (gal != 1) {
+                keyed += 1;
+                c->ledger.key_switches += S;
+            }
+        }
+        c->timed("bsgs_fused", c->rows(keyed * 2.0 * dn * ne + f.nb * ne + S * ((double)dn * ne + 2.0 * nr + 4.0 * ne)),
+                 [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+    }
+    c->ledger.ct_pt_mults += (uint64_t)S * nb;
+    c->release(dig);
+    const size_t otw = (size_t)2 * level * N;
+    uint64_t* md = c->alloc((size_t)S * otw);
+    giants_finish(c, Y, 2 * extw, S, level, {}, {0}, 0, md);
+    for (int i = 0; i < S; ++i) {
+        ck(cudaMemcpyAsync(outs[i]->d, md + (size_t)i * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+        outs[i]->scale = cts[i]->scale;
+        outs[i]->depth = cts[i]->depth + 1;
+        c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[i]->depth);
+    }
+    c->release(md);
+    c->release(Y);
+    c->release(buf);
+}
+
 int auto_orient(const fhe_conv_layer* ly) {
     // giant steps each cost a ModDown + ModUp (~120 NTT rows at cfg3) while a
     // fused baby step costs one key stream: the fused schedule (kappa giant
@@ -1762,6 +1841,7 @@ void fhe_ctx_destroy(fhe_ctx* c) {
             cudaStreamDestroy(x);
         }
     host_pipe_free(c);
+    for (auto& kv : c->lt_cache) cudaFree(kv.second);
     for (auto& g : c->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     for (int b = 0; b < 2; ++b)
@@ -2858,6 +2938,138 @@ int fhe_linear(fhe_ctx* c, const fhe_ct* const* shards, size_t t, int ch, int m,
         fhe_pt_free(bp);
         fhe_ct_free(acc);
         *out = res;
+    });
+}
+
+
+// ------------------------------------------------------------- pooling
+// 2x2 average pooling (reference pool(), pool.cpp:291-297) of
+// an image-mode feature map without duplication (c m^2 = t slots, t = 1, 2
+// or a multiple of 4). The reference's three masked stages are each one
+// plaintext-weighted sum of hoisted rotations (rot_k(x * mask) = rot_k(mask)
+// * rot_k(x)), run by the fused baby-step kernel for all shards at once:
+//   window     W = sum_{(kk,ll) in 2x2} wmask(kk, ll) * rot_{kk m + ll}(x)      (pool.cpp:22-30)
+//   horizontal H = sum_{i < m/2} rot_i(hmask_i) * rot_i(W)                      (pool.cpp:76-86)
+//   vertical   V = sum_{j < m/2} rot_{3jm/2}(vmask_j) * rot_{3jm/2}(H)           (pool.cpp:90-104)
+// then the reference's consolidation rotations (pool.cpp:167-226) and channel
+// duplication (pool.cpp:280-289). Three levels.
+int fhe_pool(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, fhe_ct** outs, size_t* n_out,
+             int64_t* tau_out, int* rep_out, int* d_out) {
+    return guard(c, [&] {
+        const size_t s = c->slots(), block = (size_t)m * m;
+        if (m < 2 || (m & (m - 1))) fail(FHE_E_INVALID, "cannot pool a 1x1 channel");
+        if (block > s || (size_t)ch * block != t * s)
+            fail(FHE_E_INVALID, "pooling expects an image-mode feature map without duplication (c m^2 = t slots)");
+        if (!(t == 1 || t == 2 || t % 4 == 0)) fail(FHE_E_INVALID, "shard count must be 1, 2 or a multiple of 4");
+        const int level = in[0]->level;
+        if (level < 3) fail(FHE_E_RUNTIME, "depth exhausted");
+        const long mL = m;
+        auto window_mask = [&](long kk, long ll) {
+            std::vector<double> v(s, 0.0);
+            for (size_t b = 0; b * block < s; ++b)
+                for (long i = 0; i + kk < mL; ++i)
+                    for (long j = 0; j + ll < mL; ++j) v[b * block + (size_t)(i * mL + j)] = 0.25;
+            return v;
+        };
+        auto rotl = [&](const std::vector<double>& v, int64_t k) {
+            std::vector<double> r(s);
+            const size_t a = (size_t)(((k % (int64_t)s) + (int64_t)s) % (int64_t)s);
+            for (size_t i = 0; i < s; ++i) r[i] = v[(i + a) % s];
+            return r;
+        };
+        std::vector<int64_t> aw, ah, av;
+        std::vector<std::vector<double>> pw, ph, pv;
+        for (auto kl : {std::pair<long, long>{0, 0}, {0, 1}, {1, 0}, {1, 1}}) {
+            aw.push_back(kl.first * mL + kl.second);
+            pw.push_back(window_mask(kl.first, kl.second));
+        }
+        for (long i2 = 0; i2 < mL / 2; ++i2) {
+            std::vector<double> mk(s, 0.0);
+            for (size_t row = 0; row < s; row += (size_t)m) mk[row + 2 * (size_t)i2] = 1.0;
+            ah.push_back(i2);
+            ph.push_back(rotl(mk, i2));
+            std::vector<double> mv(s, 0.0);
+            for (size_t b = 0; b * block < s; ++b)
+                for (long col = 0; col < mL / 2; ++col) mv[b * block + (size_t)(2 * i2 * mL + col)] = 1.0;
+            av.push_back(3 * i2 * mL / 2);
+            pv.push_back(rotl(mv, 3 * i2 * mL / 2));
+        }
+        auto stage = [&](const std::vector<const fhe_ct*>& src, const char* name, const std::vector<int64_t>& am,
+                         const std::vector<std::vector<double>>& pts) {
+            std::vector<fhe_ct*> o(src.size());
+            for (size_t u = 0; u < src.size(); ++u)
+                o[u] = new_ct(c, src[u]->level - 1, src[u]->scale, src[u]->depth + 1);
+            lintrans_batch(c, src.data(), (int)src.size(), std::string("pool-") + name + "/" + std::to_string(m), am,
+                           pts, o.data());
+            return o;
+        };
+        std::vector<const fhe_ct*> x(in, in + t);
+        std::vector<fhe_ct*> W = stage(x, "window", aw, pw);
+        std::vector<fhe_ct*> H = stage(std::vector<const fhe_ct*>(W.begin(), W.end()), "horizontal", ah, ph);
+        for (fhe_ct* p : W) fhe_ct_free(p);
+        std::vector<fhe_ct*> V = stage(std::vector<const fhe_ct*>(H.begin(), H.end()), "vertical", av, pv);
+        for (fhe_ct* p : H) fhe_ct_free(p);
+        c->ledger.rotations += (uint64_t)t * (aw.size() + ah.size() + av.size() - 3);  // amount 0 terms are free
+        const int64_t bn = (int64_t)(block / 4);
+        const size_t z = (size_t)ch / t;
+        std::vector<int64_t> tau((size_t)ch);
+        std::vector<fhe_ct*> res;
+        int rep = 1, dup = 1;
+        auto rot1 = [&](const fhe_ct* a, int64_t k) {
+            fhe_ct* o = new_ct(c, a->level, a->scale, a->depth);
+            okc(c, fhe_rotate_hoisted_batch_into(c, &a, 1, &k, 1, &o));
+            return o;
+        };
+        auto add_into = [&](fhe_ct* acc, const fhe_ct* b) {
+            ew_add(c->dc, acc->d, acc->d, b->d, 2 * (acc->level + 1), acc->level + 1, c->st);
+            c->ledger.adds++;
+        };
+        if (t == 1) {
+            res.push_back(V[0]);
+            for (size_t j = 0; j < (size_t)ch; ++j) tau[j] = (int64_t)j;
+            rep = 4;
+            dup = 4;
+        } else if (t == 2) {
+            fhe_ct* r = rot1(V[1], -2 * bn);
+            add_into(V[0], r);
+            fhe_ct_free(r);
+            fhe_ct_free(V[1]);
+            res.push_back(V[0]);
+            for (size_t j = 0; j < (size_t)ch; ++j) tau[j] = (int64_t)((j % 2) * z + j / 2);
+            rep = 2;
+            dup = 2;
+        } else {
+            const size_t blocks_out = 4 * z;
+            for (size_t w4 = 0; w4 < t / 4; ++w4) {
+                for (size_t q = 1; q < 4; ++q) {
+                    fhe_ct* r = rot1(V[4 * w4 + q], -(int64_t)q * bn);
+                    add_into(V[4 * w4], r);
+                    fhe_ct_free(r);
+                    fhe_ct_free(V[4 * w4 + q]);
+                }
+                res.push_back(V[4 * w4]);
+                for (size_t g = 0; g < blocks_out; ++g) tau[w4 * blocks_out + g] = (int64_t)((4 * w4 + g % 4) * z + g / 4);
+            }
+        }
+        if (dup > 1) {  // channel duplication: base + sum_e rot_{-e block_new}(base), hoisted
+            fhe_ct* base = res[0];
+            std::vector<int64_t> ks;
+            for (int e = 1; e < dup; ++e) ks.push_back(-(int64_t)e * bn);
+            std::vector<fhe_ct*> rs(ks.size());
+            for (size_t e = 0; e < ks.size(); ++e) rs[e] = new_ct(c, base->level, base->scale, base->depth);
+            const fhe_ct* bc = base;
+            okc(c, fhe_rotate_hoisted_batch_into(c, &bc, 1, ks.data(), ks.size(), rs.data()));
+            for (fhe_ct* r : rs) {
+                add_into(base, r);
+                fhe_ct_free(r);
+            }
+        }
+        for (size_t u = 0; u < res.size(); ++u) outs[u] = res[u];
+        if (n_out) *n_out = res.size();
+        if (tau_out)
+            for (size_t j = 0; j < (size_t)ch; ++j) tau_out[j] = tau[j];
+        if (rep_out) *rep_out = rep;
+        if (d_out) *d_out = dup;
     });
 }
 

@@ -320,6 +320,17 @@ class Context:
         self._check(lib().fhe_slot_sum_batch(self.h, ins, len(cts), block, outs))
         return [Ciphertext(self, outs[i]) for i in range(len(cts))]
 
+    def pool(self, shards: Sequence[Ciphertext], c: int, m: int):
+        """fhe_pool: 2x2 average pooling; returns (shards, tau, rep, d) like the reference's PackedImage."""
+        ins = (C.c_void_p * len(shards))(*[x.h for x in shards])
+        outs = (C.c_void_p * len(shards))()
+        n = C.c_size_t(0)
+        tau = np.zeros(c, dtype=np.int64)
+        rep, d = C.c_int(0), C.c_int(0)
+        self._check(lib().fhe_pool(self.h, ins, len(shards), c, m, outs, C.byref(n),
+                                   tau.ctypes.data_as(_lib.i64p), C.byref(rep), C.byref(d)))
+        return [Ciphertext(self, outs[i]) for i in range(n.value)], tau, rep.value, d.value
+
     def linear(self, shards: Sequence[Ciphertext], c: int, m: int, w, b) -> Ciphertext:
         """fhe_linear: W x + b over a packed image's features (reference linear())."""
         w = np.ascontiguousarray(w, dtype=np.float64)

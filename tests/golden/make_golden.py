@@ -38,6 +38,13 @@ MS_CASES = {
     "ms_cfg1_c4to8": (4, 32, 3, 8, 1012, 2012, 0, 4096),    # t = 1, n_out = 2
     "ms_cfg3_c32": (32, 32, 3, 32, 1013, 2013, 0, 16384),   # t = 2, n_out = 2
 }
+# 2x2 average pooling (pool.cpp:291-297): (c, m, s, seed), image mode without duplication
+POOL_CASES = {
+    "pool_cfg1_c4m32": (4, 32, 4096, 1040),    # t = 1: duplicated x4 after pooling
+    "pool_cfg1_c8m32": (8, 32, 4096, 1041),    # t = 2
+    "pool_cfg1_c16m32": (16, 32, 4096, 1042),  # t = 4
+    "pool_cfg3_c16m32": (16, 32, 16384, 1043), # cfg3 feature map, t = 1
+}
 # linear head: (c, m, s, out_features, seed)
 LIN_CASES = {
     "lin_cfg1_c4m32": (4, 32, 4096, 4, 1030),     # one shard
@@ -103,6 +110,14 @@ def main():
         out[f"{name}/params"] = np.array([c, m, s, no, si, t], dtype=np.int64)
         out[f"{name}/w_sum"] = np.array([w.sum()])
         out[f"{name}/slots"] = slots[:no]
+        out[f"{name}/ledger"] = ledger
+    for name, (c, m, s, si) in POOL_CASES.items():
+        img, _ = po.make_inputs(c, m, 1, 1, si, 0, 0, use_ref=True)
+        slots, meta, tau, ledger = po.ref_pool(c, m, img, s)
+        out[f"{name}/params"] = np.array([c, m, s, si], dtype=np.int64)
+        out[f"{name}/slots"] = slots
+        out[f"{name}/meta"] = meta
+        out[f"{name}/tau"] = tau
         out[f"{name}/ledger"] = ledger
     rng = np.random.default_rng(77)
     vec = rng.uniform(-1, 1, 4096)

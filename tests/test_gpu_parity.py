@@ -484,3 +484,78 @@ def test_linear_bit_exact_and_within_tolerance(oracle, golden, p1, name):
     bias[:no] = b
     ref = ck.add_plain(acc, ck.encode(bias, ck.scale, L - 2), L - 2)
     assert np.array_equal(out.residues(), ref)
+
+
+def _golden_pool(ck, cts, level, c, m, s):
+    """the golden model's pooling: three ck_lintrans stages (rotated masks), then the reference's
+    consolidation / duplication rotations and adds."""
+    block, bn = m * m, (m // 2) ** 2
+    t = len(cts)
+    rot = lambda v, k: np.roll(v, -k)
+
+    def wmask(kk, ll):
+        v = np.zeros(s)
+        for b in range(s // block):
+            for i in range(m - kk):
+                v[b * block + i * m: b * block + i * m + (m - ll)] = 0.25
+        return v
+    aw = [0, 1, m, m + 1]
+    pw = [wmask(0, 0), wmask(0, 1), wmask(1, 0), wmask(1, 1)]
+    ah, ph, av, pv = [], [], [], []
+    for i in range(m // 2):
+        mk = np.zeros(s)
+        mk[2 * i::m] = 1.0
+        ah.append(i)
+        ph.append(rot(mk, i))
+        mv = np.zeros(s)
+        for b in range(s // block):
+            mv[b * block + 2 * i * m: b * block + 2 * i * m + m // 2] = 1.0
+        av.append(3 * i * m // 2)
+        pv.append(rot(mv, 3 * i * m // 2))
+    V = []
+    for x in cts:
+        w_ = ck.lintrans(x, level, aw, pw)
+        h_ = ck.lintrans(w_, level - 1, ah, ph)
+        V.append(ck.lintrans(h_, level - 2, av, pv))
+    L = level - 3
+    if t == 1:
+        base = V[0]
+        out = base
+        for e in range(1, 4):
+            out = ck.add(out, ck.rotate(base, L, -e * bn), L)
+        return [out]
+    if t == 2:
+        sm = ck.add(V[0], ck.rotate(V[1], L, -2 * bn), L)
+        return [ck.add(sm, ck.rotate(sm, L, -bn), L)]
+    res = []
+    for w4 in range(t // 4):
+        acc = V[4 * w4]
+        for q in range(1, 4):
+            acc = ck.add(acc, ck.rotate(V[4 * w4 + q], L, -q * bn), L)
+        res.append(acc)
+    return res
+
+
+@pytest.mark.parametrize("name", ["pool_cfg1_c4m32", "pool_cfg1_c8m32", "pool_cfg1_c16m32"])
+def test_pool_bit_exact_and_within_tolerance(oracle, golden, p1, name):
+    """SURVEY §8(f) 2, 2x2 average pooling: bit-exact vs the golden model's staged pooling,
+    decrypted within 1e-6 of the reference's pool() shards, same packing metadata."""
+    c, m, s, si = (int(x) for x in golden[f"{name}/params"])
+    img, _ = oracle.make_inputs(c, m, 1, 1, si, 0, 0)
+    t = c * m * m // s
+    bn = (m // 2) ** 2
+    steps = [0, 1, m, m + 1] + list(range(m // 2)) + [3 * j * m // 2 for j in range(m // 2)] + \
+            [-e * bn for e in range(1, 4)]
+    p1.ctx.gen_galois_keys(sorted({k for k in steps if k}))
+    chunks = [img[u * s:(u + 1) * s] for u in range(t)]
+    cts = [p1.ctx.encrypt(p1.ctx.encode(x), ENC_SEED + u) for u, x in enumerate(chunks)]
+    outs, tau, rep, d = p1.ctx.pool(cts, c, m)
+    meta = golden[f"{name}/meta"]
+    assert len(outs) == int(meta[5]) and rep == int(meta[3]) and d == int(meta[2])
+    assert np.array_equal(tau, golden[f"{name}/tau"].astype(np.int64))
+    for u, o in enumerate(outs):
+        assert np.abs(p1.ctx.decrypt(o) - golden[f"{name}/slots"][u]).max() < TOL
+    ctr = [p1.ck.encrypt(p1.ck.encode(x, p1.ck.scale, p1.top), p1.top, ENC_SEED + u) for u, x in enumerate(chunks)]
+    ref = _golden_pool(p1.ck, ctr, p1.top, c, m, s)
+    for o, r in zip(outs, ref):
+        assert np.array_equal(o.residues(), r)

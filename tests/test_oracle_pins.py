@@ -175,3 +175,67 @@ def test_linear_reference_is_wx_plus_b(oracle, golden, name):
     want = w.reshape(no, -1) @ img + b
     assert np.abs(golden[f"{name}/slots"] - want).max() < 1e-12
     assert int(golden[f"{name}/ledger"][0]) == no * t * int(np.log2(s))
+
+
+def _pool_restatement(img, c, m, s):
+    """numpy restatement of the reference's pool() on an image-mode map (pool.cpp:10-104,
+    167-226, 280-289) through the rotation-of-mask form used by the GPU path."""
+    block, bn = m * m, (m // 2) ** 2
+    t = c * block // s
+    rot = lambda v, k: np.roll(v, -k)
+    shards = [img[u * s:(u + 1) * s] for u in range(t)]
+
+    def wmask(kk, ll):
+        v = np.zeros(s)
+        for b in range(s // block):
+            for i in range(m - kk):
+                v[b * block + i * m: b * block + i * m + (m - ll)] = 0.25
+        return v
+    W = [sum(wmask(kk, ll) * rot(x, kk * m + ll) for kk, ll in ((0, 0), (0, 1), (1, 0), (1, 1))) for x in shards]
+    H, V = [], []
+    for x in W:
+        acc = 0
+        for i in range(m // 2):
+            mk = np.zeros(s)
+            mk[2 * i::m] = 1.0
+            acc = acc + rot(mk, i) * rot(x, i)
+        H.append(acc)
+    for x in H:
+        acc = 0
+        for j in range(m // 2):
+            mv = np.zeros(s)
+            for b in range(s // block):
+                mv[b * block + 2 * j * m: b * block + 2 * j * m + m // 2] = 1.0
+            acc = acc + rot(mv, 3 * j * m // 2) * rot(x, 3 * j * m // 2)
+        V.append(acc)
+    if t == 1:
+        base = V[0]
+        return [base + sum(rot(base, -e * bn) for e in range(1, 4))]
+    if t == 2:
+        sm = V[0] + rot(V[1], -2 * bn)
+        return [sm + rot(sm, -bn)]
+    return [V[4 * w] + sum(rot(V[4 * w + q], -q * bn) for q in range(1, 4)) for w in range(t // 4)]
+
+
+@pytest.mark.parametrize("name", ["pool_cfg1_c4m32", "pool_cfg1_c8m32", "pool_cfg1_c16m32", "pool_cfg3_c16m32"])
+def test_pool_restatement_matches_reference(oracle, golden, name):
+    """the rotation-of-mask form of pooling (what the GPU runs) reproduces the reference's
+    pool() shards to 1e-12 (summation order differs), and the reference pools correctly."""
+    c, m, s, si = (int(x) for x in golden[f"{name}/params"])
+    img, _ = oracle.make_inputs(c, m, 1, 1, si, 0, 0)
+    got = _pool_restatement(img, c, m, s)
+    want = golden[f"{name}/slots"]
+    assert len(got) == want.shape[0]
+    for a, b in zip(got, want):
+        assert np.abs(a - b).max() < 1e-12
+    # logical check: pooled channel tau[g] at physical block g of the first shard
+    meta, tau = golden[f"{name}/meta"], golden[f"{name}/tau"]
+    mn = m // 2
+    x = img.reshape(c, m, m)
+    pooled = 0.25 * (x[:, 0::2, 0::2] + x[:, 1::2, 0::2] + x[:, 0::2, 1::2] + x[:, 1::2, 1::2])
+    rep = int(meta[3])
+    for g in range(min(c * rep, s // (mn * mn))):
+        if g % rep:
+            continue
+        ch = int(tau[(g // rep) % c])
+        assert np.abs(want[0][g * mn * mn:(g + 1) * mn * mn] - pooled[ch].ravel()).max() < 1e-12
