@@ -253,6 +253,18 @@ int fhe_linear(fhe_ctx* ctx, const fhe_ct* const* shards, size_t t, int c, int m
 int fhe_pool(fhe_ctx* ctx, const fhe_ct* const* in, size_t t, int c, int m, fhe_ct** outs, size_t* n_out,
              int64_t* tau_out, int* rep_out, int* d_out);
 
+/* ciphertext x ciphertext multiplication and the Chebyshev
+ * activation (reference Engine::mul_ct emu.cpp:69-80, eval_chebyshev act.cpp:151-162).
+ * The relinearisation key (s^2 -> s) must exist: fhe_gen_relin_key. fhe_mul
+ * drops the higher operand to the common level, relinearises and rescales
+ * (one level; scale = scale_a * scale_b / q_l). */
+int fhe_gen_relin_key(fhe_ctx* ctx);
+int fhe_mul(fhe_ctx* ctx, const fhe_ct* a, const fhe_ct* b, fhe_ct** out);
+/* sum_k coeffs[k] T_k(x / bound) (x / bound already in [-1, 1] when prescaled),
+ * the reference's power-of-two split; levels: bit length of n - 1 (+1 unless prescaled) */
+int fhe_eval_chebyshev(fhe_ctx* ctx, const fhe_ct* x, const double* coeffs, size_t n, double bound, int prescaled,
+                       fhe_ct** out);
+
 #ifdef __cplusplus
 }
 #endif

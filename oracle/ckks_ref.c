@@ -496,14 +496,21 @@ void ck_keygen(ck_ctx* ck, uint64_t seed) {
 
 void ck_secret_coef(const ck_ctx* ck, int64_t* s) { memcpy(s, ck->s_coef, ck->N * sizeof(int64_t)); }
 
-/* Hybrid key-switching key for s' = sigma_g(s):
+/* Hybrid key-switching key for s' = sigma_g(s), or s' = s^2 when g == 0:
  * key[j][0][t] = -a s + e + [t in digit j] * (P mod q_t) * s'
  * key[j][1][t] = a                                  (NTT domain)     */
 void ck_galois_key(const ck_ctx* ck, uint64_t g, uint64_t* key) {
     const size_t N = ck->N;
     const int np = ck->np, L = ck->L;
     uint64_t* sp = malloc((size_t)np * N * 8);
-    for (int t = 0; t < np; t++) ck_automorph_ntt(ck, ck->s_ntt + (size_t)t * N, sp + (size_t)t * N, g);
+    for (int t = 0; t < np; t++) {
+        const uint64_t* s = ck->s_ntt + (size_t)t * N;
+        uint64_t* d = sp + (size_t)t * N;
+        if (g == 0) /* relinearisation key: s' = s^2 */
+            for (size_t k = 0; k < N; k++) d[k] = ck_mulmod(s[k], s[k], ck->q[t]);
+        else
+            ck_automorph_ntt(ck, s, d, g);
+    }
     uint64_t Pmod[CK_MAXP];
     for (int t = 0; t < np; t++) {
         uint64_t P = 1;
@@ -847,6 +854,49 @@ void ck_rotate_hoisted(const ck_ctx* ck, const uint64_t* ct, int level, const lo
 
 void ck_rotate(const ck_ctx* ck, const uint64_t* ct, int level, long k, uint64_t* out) {
     ck_rotate_hoisted(ck, ct, level, &k, 1, out);
+}
+
+/* Relinearised product (reference Engine::mul_ct, emu.cpp:69-80): tensor
+ * (d0, d1, d2) = (a0 b0, a0 b1 + a1 b0, a1 b1), key-switch d2 with the s^2 key,
+ * add, rescale. a, b at `level`; out at level - 1. */
+void ck_mul_ct(const ck_ctx* ck, const uint64_t* a, const uint64_t* b, int level, uint64_t* out) {
+    const size_t N = ck->N;
+    const int nr = level + 1, ne = nr + ck->K;
+    const size_t pw = (size_t)nr * N;
+    uint64_t* d = malloc(3 * pw * 8);
+    for (int t = 0; t < nr; t++) {
+        const uint64_t q = ck->q[t];
+        for (size_t k = 0; k < N; k++) {
+            const size_t i = (size_t)t * N + k;
+            const uint64_t a0 = a[i], a1 = a[pw + i], b0 = b[i], b1 = b[pw + i];
+            d[i] = ck_mulmod(a0, b0, q);
+            d[pw + i] = addm(ck_mulmod(a0, b1, q), ck_mulmod(a1, b0, q), q);
+            d[2 * pw + i] = ck_mulmod(a1, b1, q);
+        }
+    }
+    uint64_t* digits = malloc((size_t)ck_dnum_at(ck, level) * ne * N * 8);
+    ck_modup(ck, d + 2 * pw, level, digits);
+    uint64_t* key = malloc(key_words(ck) * 8);
+    ck_galois_key(ck, 0, key);
+    uint64_t* a0 = malloc((size_t)ne * N * 8);
+    uint64_t* a1 = malloc((size_t)ne * N * 8);
+    ck_inner_product(ck, digits, level, key, 1, a0, a1);
+    uint64_t* sum = malloc(2 * pw * 8);
+    ck_moddown(ck, a0, level, sum);
+    ck_moddown(ck, a1, level, sum + pw);
+    for (int t = 0; t < nr; t++)
+        for (size_t k = 0; k < N; k++)
+            for (int p = 0; p < 2; p++) {
+                const size_t i = p * pw + (size_t)t * N + k;
+                sum[i] = addm(sum[i], d[i], ck->q[t]);
+            }
+    ck_rescale(ck, sum, level, out);
+    free(sum);
+    free(a1);
+    free(a0);
+    free(key);
+    free(digits);
+    free(d);
 }
 
 /* ------------------------------------------------------------------ */

@@ -86,6 +86,7 @@ void ck_moddown(const ck_ctx* ck, const uint64_t* acc, int level, uint64_t* out)
 
 /* rotations (keys regenerated from the key seed on demand) */
 void ck_rotate(const ck_ctx* ck, const uint64_t* ct, int level, long k, uint64_t* out);
+void ck_mul_ct(const ck_ctx* ck, const uint64_t* a, const uint64_t* b, int level, uint64_t* out);
 void ck_rotate_hoisted(const ck_ctx* ck, const uint64_t* ct, int level, const long* ks, int n,
                        uint64_t* outs);
 

@@ -13,6 +13,8 @@ import ctypes as C
 import os
 import subprocess
 
+import math
+
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -82,6 +84,7 @@ def lib():
         L.ck_inner_product.argtypes = [C.c_void_p, u64p, C.c_int, u64p, C.c_uint64, u64p, u64p]
         L.ck_moddown.argtypes = [C.c_void_p, u64p, C.c_int, u64p]
         L.ck_rotate.argtypes = [C.c_void_p, u64p, C.c_int, C.c_long, u64p]
+        L.ck_mul_ct.argtypes = [C.c_void_p, u64p, u64p, C.c_int, u64p]
         L.ck_rotate_hoisted.argtypes = [C.c_void_p, u64p, C.c_int, lp, C.c_int, u64p]
         L.ck_conv.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp,
                               C.c_int, u64p, dp]
@@ -107,6 +110,9 @@ def lib():
     return _lib
 
 
+_CHEB_FN = C.CFUNCTYPE(C.c_double, C.c_double)
+
+
 def ref_available():
     return os.path.exists(REF_SO)
 
@@ -130,6 +136,9 @@ def ref():
         R.ref_linear.argtypes = [C.c_int, C.c_int, dp, C.c_int, dp, dp, C.c_uint64, dp, u64p]
         R.ref_pool.argtypes = [C.c_int, C.c_int, dp, C.c_uint64, dp, C.c_int, u64p, u64p, u64p]
         R.ref_slot_sum.argtypes = [dp, C.c_uint64, C.c_uint64, dp]
+        R.ref_eval_chebyshev.argtypes = [dp, C.c_uint64, C.c_int, dp, C.c_uint64, C.c_double, C.c_int, dp,
+                                         C.POINTER(C.c_int64), u64p, C.c_char_p, C.c_uint64]
+        R.ref_cheb_interpolate.argtypes = [_CHEB_FN, C.c_uint64, C.c_double, dp]
         R.ref_time_rotations.restype = C.c_double
         R.ref_time_rotations.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, u64p]
         _ref = R
@@ -218,6 +227,57 @@ def ref_slot_sum(vec, block):
     out = np.zeros(vec.size)
     assert ref().ref_slot_sum(_ptr(vec, dp), vec.size, block, _ptr(out, dp)) == 0
     return out
+
+
+def ref_eval_chebyshev(x, level, coeffs, bound, prescaled):
+    """the reference's eval_chebyshev (act.cpp:151-162) on slots x at `level`:
+    (slots, output level, max depth, ledger) or raises RuntimeError with its text."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    co = np.ascontiguousarray(coeffs, dtype=np.float64)
+    out = np.zeros(x.size)
+    meta = (C.c_int64 * 2)()
+    ledger = np.zeros(9, dtype=np.uint64)
+    err = C.create_string_buffer(256)
+    rc = ref().ref_eval_chebyshev(_ptr(x, dp), x.size, level, _ptr(co, dp), co.size, bound, int(prescaled),
+                                  _ptr(out, dp), meta, _ptr(ledger, u64p), err, 256)
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    return out, meta[0], meta[1], ledger
+
+
+def ref_cheb_interpolate(f, n, bound):
+    """the reference's cheb_interpolate (act.cpp:90-113)."""
+    co = np.zeros(n + 1)
+    cb = _CHEB_FN(f)
+    assert ref().ref_cheb_interpolate(cb, n, bound, _ptr(co, dp)) == 0
+    return co
+
+
+def cheb_interpolate(f, n, bound):
+    """restatement of act.cpp:90-113: Chebyshev interpolant through the n+1
+    Chebyshev nodes (same loop order and rounding as the reference)."""
+    if bound <= 0.0:
+        raise ValueError("bound must be positive")
+    pts = n + 1
+    y = [f(bound * math.cos(math.pi * (2.0 * j + 1.0) / (2.0 * pts))) for j in range(pts)]
+    co = []
+    for k in range(pts):
+        acc = 0.0
+        for j in range(pts):
+            acc += y[j] * math.cos(math.pi * k * (2.0 * j + 1.0) / (2.0 * pts))
+        co.append(2.0 * acc / pts)
+    co[0] /= 2.0
+    return np.array(co)
+
+
+def cheb_eval(coeffs, bound, x):
+    """Clenshaw evaluation (act.cpp:115-125), vectorised over x."""
+    t = np.asarray(x, dtype=np.float64) / bound
+    b1 = np.zeros_like(t)
+    b2 = np.zeros_like(t)
+    for k in range(len(coeffs) - 1, 0, -1):
+        b1, b2 = 2.0 * t * b1 - b2 + coeffs[k], b1
+    return t * b1 - b2 + coeffs[0]
 
 
 def emu_oracle_conv(c, m, kappa, c_out, img, filt):
@@ -392,6 +452,99 @@ class CKKS:
         out = np.zeros((2, level + 1, self.N), dtype=np.uint64)
         lib().ck_rotate(self.h, _ptr(np.ascontiguousarray(ct), u64p), level, k, _ptr(out, u64p))
         return out
+
+    def mul_ct(self, a, b, level):
+        """relinearised, rescaled product (ck_mul_ct): [2][level+1][N] x2 -> [2][level][N]."""
+        out = np.zeros((2, level, self.N), dtype=np.uint64)
+        lib().ck_mul_ct(self.h, _ptr(np.ascontiguousarray(a[:, : level + 1]), u64p),
+                        _ptr(np.ascontiguousarray(b[:, : level + 1]), u64p), level, _ptr(out, u64p))
+        return out
+
+    def eval_chebyshev(self, ct, level, scale, coeffs, bound, prescaled):
+        """Chebyshev series on a ciphertext: the reference's split (act.cpp:49-82, 151-162)
+        with the scale targeting of fheconv.cu's ChebEval, op for op, so the residues
+        are comparable bit for bit. Returns (ct, level, scale)."""
+        primes = self.primes
+        S = self.N // 2
+
+        def const(k, lv, sc):
+            return self.encode(np.full(S, k), sc, lv)
+
+        def drop(v, lv):
+            c, l0, sc = v
+            if l0 < lv:
+                raise RuntimeError("insufficient level for activation: bootstrap required")
+            return (np.ascontiguousarray(c[:, : lv + 1]), lv, sc)
+
+        def add(a, b):
+            assert a[1] == b[1]
+            return (self.add(a[0], b[0], a[1]), a[1], a[2])
+
+        def add_scalar(v, k):
+            return (self.add_plain(v[0], const(k, v[1], v[2]), v[1]), v[1], v[2])
+
+        def mul_scalar(v, k, lv, sc):
+            c, _, vs = drop(v, lv + 1)
+            pr = self.mul_plain(c, const(k, lv + 1, sc * float(primes[lv + 1]) / vs), lv + 1)
+            return (self.rescale(pr, lv + 1), lv, sc)
+
+        def mul(a, b):
+            lv = a[1]
+            assert b[1] == lv
+            return (self.mul_ct(a[0], b[0], lv), lv - 1, a[2] * b[2] / float(primes[lv]))
+
+        def floor_pow2(d):
+            p = 1
+            while p * 2 <= d:
+                p *= 2
+            return p
+
+        basis = []
+
+        def of_degree(p2):
+            return basis[p2.bit_length() - 1]
+
+        def series(co, lv, sc):
+            d = len(co) - 1
+            if d <= 2:
+                acc = mul_scalar(of_degree(1), co[1], lv, sc)
+                if d == 2:
+                    acc = add(acc, mul_scalar(of_degree(2), co[2], lv, sc))
+                return add_scalar(acc, co[0])
+            p = floor_pow2(d)
+            if p == d:
+                top = mul_scalar(of_degree(p), co[d], lv, sc)
+                return add(top, series(co[:-1], lv, sc))
+            q = [0.0] * (d - p + 1)
+            r = list(co[: p + 1])
+            for a in range(1, d - p + 1):
+                q[a] = 2.0 * co[p + a]
+                r[p - a] -= co[p + a]
+            tp = drop(of_degree(p), lv + 1)
+            qv = series(q, lv + 1, sc * float(primes[lv + 1]) / tp[2])
+            prod = mul(qv, tp)
+            return add((prod[0], prod[1], sc), series(r, lv, sc))
+
+        co = [float(v) for v in coeffs]
+        d = len(co) - 1
+        needed = d.bit_length() + (0 if prescaled else 1)
+        if level < needed:
+            raise RuntimeError("insufficient level for activation: bootstrap required")
+        out_level = level - needed
+        if d == 0:  # the reference's fresh encode (act.cpp:158)
+            pt = const(co[0], level, scale)
+            return (np.stack([pt, np.zeros_like(pt)]), level, scale)
+        t = (np.ascontiguousarray(ct), level, scale)
+        if not prescaled:
+            t = mul_scalar(t, 1.0 / bound, level - 1, scale)
+        basis.append(t)
+        p = 2
+        while p <= floor_pow2(d):
+            half = basis[-1]
+            sq = mul(half, half)
+            basis.append(add_scalar(add(sq, sq), -1.0))
+            p *= 2
+        return series(co, out_level, scale)
 
     def rotate_hoisted(self, ct, level, ks):
         out = np.zeros((len(ks), 2, level + 1, self.N), dtype=np.uint64)

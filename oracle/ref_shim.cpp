@@ -12,6 +12,7 @@
 // Inputs are generated with the reference's own test helpers
 // (tests/helpers.hpp:13-27: mt19937_64 + uniform_real_distribution), so the
 // golden vectors are exactly what the reference's tests would see.
+#include "shardnn/act.hpp"
 #include "shardnn/conv.hpp"
 #include "shardnn/dense.hpp"
 #include "shardnn/pool.hpp"
@@ -23,6 +24,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -248,6 +250,40 @@ int ref_pool(int c, int m, const double* img, uint64_t s, double* out_slots, int
         for (size_t j = 0; j < out.tau.size(); ++j) tau[j] = out.tau[j];
         fill_ledger(eng.ledger(), ledger);
         return n;
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// eval_chebyshev (act.cpp:151-162) of the slot vector `x` (s slots) placed at
+/// `level`: out receives the slots, meta = [output level, max depth consumed],
+/// ledger the op counters. Returns 0, or -2 with the exception text in `err`.
+int ref_eval_chebyshev(const double* x, uint64_t s, int level, const double* coeffs, uint64_t n, double bound,
+                       int prescaled, double* out, int64_t* meta, uint64_t* ledger, char* err, uint64_t err_cap) {
+    try {
+        Engine eng(EngineConfig{.initial_level = level});
+        SlotVector v = eng.encode(std::vector<double>(x, x + s));
+        ChebPoly p;
+        p.bound = bound;
+        p.coeffs.assign(coeffs, coeffs + n);
+        SlotVector y = eval_chebyshev(eng, v, p, prescaled != 0);
+        std::memcpy(out, y.slots.data(), s * sizeof(double));
+        meta[0] = y.level;
+        meta[1] = (int64_t)eng.ledger().max_depth_consumed.load();
+        fill_ledger(eng.ledger(), ledger);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, err_cap, "%s", e.what());
+        return -2;
+    }
+}
+
+/// cheb_interpolate (act.cpp:90-113) of f on [-bound, bound] at degree n.
+int ref_cheb_interpolate(double (*f)(double), uint64_t n, double bound, double* coeffs) {
+    try {
+        ChebPoly p = cheb_interpolate([f](double x) { return f(x); }, n, bound);
+        std::memcpy(coeffs, p.coeffs.data(), p.coeffs.size() * sizeof(double));
+        return 0;
     } catch (...) {
         return -1;
     }

@@ -371,6 +371,8 @@ void rescale_into(fhe_ctx* c, const uint64_t* in, int level, uint64_t* out) {
     c->ledger.rescales++;
 }
 
+// Galois key for element g, or (g == 0) the relinearisation key s^2 -> s; the
+// PRNG streams are keyed by g, so the golden model derives the same keys.
 void gen_key(fhe_ctx* c, uint32_t g) {
     if (c->keys.count(g)) return;
     const size_t N = c->N;
@@ -379,6 +381,11 @@ void gen_key(fhe_ctx* c, uint32_t g) {
     int64_t* e = (int64_t*)c->alloc(N);
     uint64_t* erows = c->alloc((size_t)np * N);
     const RowMap all{np, c->L - 1, c->L, 0};
+    uint64_t* s2 = nullptr;
+    if (g == 0) {  // s^2 in the NTT domain, every prime
+        s2 = c->alloc((size_t)np * N);
+        ew_mul_bcast(c->dc, s2, c->d_s, c->d_s, np, np, c->st);
+    }
     for (int j = 0; j < c->dnum; ++j) {
         uint64_t* b = key + (size_t)(2 * j) * np * N;
         uint64_t* a = key + (size_t)(2 * j + 1) * np * N;
@@ -387,8 +394,9 @@ void gen_key(fhe_ctx* c, uint32_t g) {
         ntt_forward(c->dc, erows, np, all, c->st);
         sample_uniform_rows(c->dc, a, np, all, stream_key(c->key_seed, stream_id(DOM_KEY_A, g, j)), c->st);
         const int lo = j * c->alpha, hi = std::min(lo + c->alpha, c->L);
-        keygen_combine(c->dc, b, a, erows, c->d_s, g, lo, hi, c->d_md, np, c->st);
+        keygen_combine(c->dc, b, a, erows, c->d_s, g == 0 ? 1u : g, lo, hi, c->d_md, np, c->st, s2);
     }
+    c->release(s2);
     c->release(e);
     c->release(erows);
     c->keys[g] = key;
@@ -3070,6 +3078,205 @@ int fhe_pool(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, fhe_c
             for (size_t j = 0; j < (size_t)ch; ++j) tau_out[j] = tau[j];
         if (rep_out) *rep_out = rep;
         if (d_out) *d_out = dup;
+    });
+}
+
+
+// ------------------------------------------- ct x ct and Chebyshev series
+// mul_ct with relinearisation (hybrid key switching of d2 with
+// the s^2 key, the same ModUp / inner-product / ModDown kernels) and the
+// reference's power-of-two-split Chebyshev evaluation (act.cpp:30-82, 151-162).
+int fhe_gen_relin_key(fhe_ctx* c) {
+    return guard(c, [&] {
+        require_key(c);
+        gen_key(c, 0);
+        ck(cudaStreamSynchronize(c->st), "sync");
+    });
+}
+
+static fhe_ct* drop_to(fhe_ctx* c, const fhe_ct* a, int level) {
+    // modulus drop: keep rows 0..level of both polynomials (scale unchanged)
+    fhe_ct* o = new_ct(c, level, a->scale, a->depth);
+    const size_t N = c->N, w = (size_t)(level + 1) * N;
+    ck(cudaMemcpyAsync(o->c0(), a->c0(), w * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    ck(cudaMemcpyAsync(o->c1(), a->c1(), w * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    return o;
+}
+
+// relinearised product of two ciphertexts at the same level, then one rescale
+static fhe_ct* mul_relin_rescale(fhe_ctx* c, const fhe_ct* a, const fhe_ct* b) {
+    const int level = a->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    if (level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
+    if (!c->keys.count(0)) fail(FHE_E_NOKEY, "missing relinearisation key (fhe_gen_relin_key)");
+    const size_t N = c->N, pw = (size_t)nr * N, extw = (size_t)ne * N;
+    uint64_t* d = c->alloc(3 * pw);
+    tensor(c->dc, d, a->d, b->d, level, c->st);
+    uint64_t* dig = c->alloc((size_t)dn * extw);
+    modup(c, d + 2 * pw, level, dig);
+    uint64_t* acc = c->alloc(2 * extw);
+    c->timed("ks_inner", c->rows(3.0 * dn * ne + 2.0 * ne), [&] {
+        ks_inner_product(c->dc, dig, c->keys.at(0), acc, acc + extw, 1, level, dn, c->st);
+    });
+    c->ledger.key_switches++;
+    uint64_t* md = c->alloc(2 * pw);
+    moddown(c, acc, level, 2, md, nullptr, 1);
+    ew_add(c->dc, md, md, d, 2 * nr, nr, c->st);  // (d0, d1) + ModDown(IP(d2))
+    fhe_ct* o = new_ct(c, level - 1, a->scale * b->scale / (double)c->primes[level], std::max(a->depth, b->depth) + 1);
+    rescale_into(c, md, level, o->d);
+    c->ledger.ct_ct_mults++;
+    c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, o->depth);
+    c->release(md);
+    c->release(acc);
+    c->release(dig);
+    c->release(d);
+    return o;
+}
+
+int fhe_mul(fhe_ctx* c, const fhe_ct* a, const fhe_ct* b, fhe_ct** out) {
+    return guard(c, [&] {
+        const int level = std::min(a->level, b->level);
+        fhe_ct* ad = a->level == level ? nullptr : drop_to(c, a, level);
+        fhe_ct* bd = b->level == level ? nullptr : drop_to(c, b, level);
+        try {
+            *out = mul_relin_rescale(c, ad ? ad : a, bd ? bd : b);
+        } catch (...) {
+            fhe_ct_free(ad);
+            fhe_ct_free(bd);
+            throw;
+        }
+        fhe_ct_free(ad);
+        fhe_ct_free(bd);
+    });
+}
+
+namespace {
+// Chebyshev-series evaluation with exact scale management. The reference's
+// emulator (act.cpp:49-82) adds values freely; in CKKS an addition needs equal
+// levels and scales, and ct x ct products land at scale s_a s_b / q_l. So every
+// sub-series is evaluated towards a (level, scale) target: leaves T_j * c are
+// plaintext products whose constant is encoded at exactly the scale that
+// rescales onto the target, and a product q * T_p asks q for the scale that
+// makes q * T_p / q_{l+1} hit the target. Same split, same basis, same depth.
+struct ChebEval {
+    fhe_ctx* c;
+    std::vector<fhe_ct*> owned;
+    std::vector<fhe_ct*> basis;  // T_1, T_2, T_4, ...
+    ~ChebEval() {
+        for (fhe_ct* x : owned) fhe_ct_free(x);
+    }
+    fhe_ct* keep(fhe_ct* x) {
+        owned.push_back(x);
+        return x;
+    }
+    fhe_ct* at_level(fhe_ct* x, int level) {
+        if (x->level < level) fail(FHE_E_RUNTIME, "insufficient level for activation: bootstrap required");
+        return x->level == level ? x : keep(drop_to(c, x, level));
+    }
+    fhe_pt* constant(double k, int level, double scale) {
+        std::vector<double> v(c->slots(), k);
+        fhe_pt* pt = nullptr;
+        okc(c, fhe_encode(c, v.data(), v.size(), level, scale, 0, &pt));
+        return pt;
+    }
+    fhe_ct* add(fhe_ct* a, fhe_ct* b) {
+        fhe_ct* o = nullptr;
+        okc(c, fhe_add(c, a, b, &o));
+        return keep(o);
+    }
+    fhe_ct* add_scalar(fhe_ct* x, double k) {
+        fhe_pt* pt = constant(k, x->level, x->scale);
+        fhe_ct* o = nullptr;
+        const int rc = fhe_add_plain(c, x, pt, &o);
+        fhe_pt_free(pt);
+        okc(c, rc);
+        return keep(o);
+    }
+    // x * k landing on (level, scale): constant encoded at scale * q_{level+1} / x.scale
+    fhe_ct* mul_scalar(fhe_ct* x, double k, int level, double scale) {
+        fhe_ct* xs = at_level(x, level + 1);
+        fhe_pt* pt = constant(k, level + 1, scale * (double)c->primes[level + 1] / xs->scale);
+        fhe_ct* pr = nullptr;
+        const int rc = fhe_mul_plain(c, xs, pt, &pr);
+        fhe_pt_free(pt);
+        okc(c, rc);
+        keep(pr);
+        fhe_ct* rs = nullptr;
+        okc(c, fhe_rescale(c, pr, &rs));
+        rs->scale = scale;  // exact up to the double rounding of the encode scale
+        return keep(rs);
+    }
+    fhe_ct* of_degree(size_t p2) const {
+        size_t j = 0;
+        while ((size_t{1} << j) < p2) ++j;
+        return basis[j];
+    }
+    static size_t floor_pow2(size_t d) {
+        size_t p = 1;
+        while (p * 2 <= d) p *= 2;
+        return p;
+    }
+    // sum_k co[k] T_k at (level, scale); degree >= 1 (act.cpp:49-82)
+    fhe_ct* series(std::vector<double> co, int level, double scale) {
+        const size_t d = co.size() - 1;
+        if (d <= 2) {
+            fhe_ct* acc = mul_scalar(of_degree(1), co[1], level, scale);
+            if (d == 2) acc = add(acc, mul_scalar(of_degree(2), co[2], level, scale));
+            return add_scalar(acc, co[0]);
+        }
+        const size_t p = floor_pow2(d);
+        if (p == d) {
+            fhe_ct* top = mul_scalar(of_degree(p), co[d], level, scale);
+            co.pop_back();
+            return add(top, series(std::move(co), level, scale));
+        }
+        std::vector<double> q(d - p + 1, 0.0), r(co.begin(), co.begin() + (long)p + 1);
+        for (size_t a = 1; a <= d - p; ++a) {
+            q[a] = 2.0 * co[p + a];
+            r[p - a] -= co[p + a];
+        }
+        fhe_ct* tp = at_level(of_degree(p), level + 1);
+        fhe_ct* qv = series(std::move(q), level + 1, scale * (double)c->primes[level + 1] / tp->scale);
+        fhe_ct* prod = keep(mul_relin_rescale(c, qv, tp));
+        prod->scale = scale;
+        return add(prod, series(std::move(r), level, scale));
+    }
+};
+}  // namespace
+
+int fhe_eval_chebyshev(fhe_ctx* c, const fhe_ct* x, const double* coeffs, size_t n, double bound, int prescaled,
+                       fhe_ct** out) {
+    return guard(c, [&] {
+        if (n == 0) fail(FHE_E_INVALID, "empty coefficient list");
+        const size_t d = n - 1;
+        int bits = 0;
+        while ((size_t{1} << bits) <= d) ++bits;  // chebyshev_required_level (act.cpp:84-88)
+        const int needed = bits + (prescaled ? 0 : 1);
+        if (x->level < needed) fail(FHE_E_RUNTIME, "insufficient level for activation: bootstrap required");
+        const int out_level = x->level - needed;
+        ChebEval ev{c, {}, {}};
+        fhe_ct* t = const_cast<fhe_ct*>(x);
+        if (!prescaled) t = ev.mul_scalar(t, 1.0 / bound, x->level - 1, x->scale);  // act.cpp:156, also at d = 0
+        if (d == 0) {  // a constant (the reference's fresh encode, act.cpp:158): trivial c1 = 0 ciphertext
+            std::vector<double> v(c->slots(), coeffs[0]);
+            fhe_pt* pt = nullptr;
+            okc(c, fhe_encode(c, v.data(), v.size(), x->level, x->scale, 0, &pt));
+            fhe_ct* o = new_ct(c, x->level, x->scale, 0);
+            const size_t w = (size_t)(x->level + 1) * c->N;
+            ck(cudaMemcpyAsync(o->c0(), pt->d, w * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+            ck(cudaMemsetAsync(o->c1(), 0, w * 8, c->st), "memset");
+            fhe_pt_free(pt);
+            *out = o;
+            return;
+        }
+        ev.basis.push_back(t);  // PowerBasis (act.cpp:28-37): T_2n = 2 T_n^2 - 1
+        for (size_t p = 2; p <= ChebEval::floor_pow2(d); p *= 2) {
+            fhe_ct* half = ev.basis.back();
+            fhe_ct* sq = ev.keep(mul_relin_rescale(c, half, half));
+            ev.basis.push_back(ev.add_scalar(ev.add(sq, sq), -1.0));
+        }
+        fhe_ct* res = ev.series(std::vector<double>(coeffs, coeffs + n), out_level, x->scale);
+        ev.owned.erase(std::find(ev.owned.begin(), ev.owned.end(), res));  // hand the result out
+        *out = res;
     });
 }
 

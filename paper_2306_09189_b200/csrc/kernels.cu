@@ -78,7 +78,8 @@ __global__ void k_sample_ternary(DevCtx c, int64_t* out, uint64_t key) {
 }
 
 __global__ void k_keygen_combine(DevCtx c, uint64_t* b, const uint64_t* a, const uint64_t* e, const uint64_t* s,
-                                 uint32_t galois, int lo, int hi, const ModDownTable* md, int nrows) {
+                                 uint32_t galois, int lo, int hi, const ModDownTable* md, int nrows,
+                                 const uint64_t* target) {
     const size_t total = (size_t)nrows * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         const int t = (int)(i >> c.logN);
@@ -86,7 +87,8 @@ __global__ void k_keygen_combine(DevCtx c, uint64_t* b, const uint64_t* a, const
         const Prime pr = c.primes[t];
         uint64_t v = sub_mod(e[i], mul_mod(a[i], s[i], pr), pr.q);
         if (t >= lo && t < hi) {
-            const uint64_t sp = s[(size_t)t * c.N + perm_index(k, galois, c.logN)];
+            // switching target: sigma_g(s) for Galois keys, the given rows (s^2) for relinearisation
+            const uint64_t sp = target ? target[i] : s[(size_t)t * c.N + perm_index(k, galois, c.logN)];
             v = add_mod(v, mul_shoup(sp, md->pmod[t], md->pmod_sh[t], pr.q), pr.q);
         }
         b[i] = v;
@@ -134,10 +136,27 @@ void sample_ternary(const DevCtx& c, int64_t* out, uint64_t key, cudaStream_t st
 }
 void keygen_combine(const DevCtx& c, uint64_t* key_b, const uint64_t* key_a, const uint64_t* e,
                     const uint64_t* s, uint32_t galois, int lo, int hi, const ModDownTable* md, int nrows,
-                    cudaStream_t st) {
+                    cudaStream_t st, const uint64_t* target) {
     ++g_launches;
     k_keygen_combine<<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, key_b, key_a, e, s, galois, lo,
-                                                                              hi, md, nrows);
+                                                                              hi, md, nrows, target);
+}
+
+// ct x ct tensor product in the NTT domain: d0 = a0 b0, d1 = a0 b1 + a1 b0,
+// d2 = a1 b1 (rows 0..level of each polynomial; d = [3][level+1][N])
+__global__ void k_tensor(DevCtx c, uint64_t* d, const uint64_t* a, const uint64_t* b, int nr) {
+    const size_t pw = (size_t)nr * c.N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < pw; i += (size_t)gridDim.x * blockDim.x) {
+        const Prime pr = c.primes[i >> c.logN];
+        const uint64_t a0 = a[i], a1 = a[pw + i], b0 = b[i], b1 = b[pw + i];
+        d[i] = mul_mod(a0, b0, pr);
+        d[pw + i] = add_mod(mul_mod(a0, b1, pr), mul_mod(a1, b0, pr), pr.q);
+        d[2 * pw + i] = mul_mod(a1, b1, pr);
+    }
+}
+void tensor(const DevCtx& c, uint64_t* d, const uint64_t* a, const uint64_t* b, int level, cudaStream_t st) {
+    ++g_launches;
+    k_tensor<<<ew_blocks((size_t)(level + 1) * c.N), kEwThreads, 0, st>>>(c, d, a, b, level + 1);
 }
 void encrypt_combine(const DevCtx& c, uint64_t* c0, const uint64_t* c1, const uint64_t* e,
                      const uint64_t* s, const uint64_t* pt, int nrows, cudaStream_t st) {

@@ -144,7 +144,9 @@ void sample_ternary(const DevCtx& c, int64_t* out, uint64_t key, cudaStream_t st
 // key[j][0][t] = e[t] - a[t] s[t] + [t in digit j] pmod[t] sigma_g(s)[t]; a already in key[j][1]
 void keygen_combine(const DevCtx& c, uint64_t* key_b, const uint64_t* key_a, const uint64_t* e,
                     const uint64_t* s, uint32_t galois, int lo, int hi, const ModDownTable* md, int nrows,
-                    cudaStream_t st);
+                    cudaStream_t st, const uint64_t* target = nullptr);
+// ct x ct tensor product: d = [3][level+1][N] from a, b = [2][level+1][N] (NTT domain)
+void tensor(const DevCtx& c, uint64_t* d, const uint64_t* a, const uint64_t* b, int level, cudaStream_t st);
 // c0 = e - a s + pt (rows 0..level), a already in c1
 void encrypt_combine(const DevCtx& c, uint64_t* c0, const uint64_t* c1, const uint64_t* e,
                      const uint64_t* s, const uint64_t* pt, int nrows, cudaStream_t st);

@@ -331,6 +331,18 @@ class Context:
                                    tau.ctypes.data_as(_lib.i64p), C.byref(rep), C.byref(d)))
         return [Ciphertext(self, outs[i]) for i in range(n.value)], tau, rep.value, d.value
 
+    def gen_relin_key(self):
+        self._check(lib().fhe_gen_relin_key(self.h))
+
+    def mul(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+        """fhe_mul: relinearised, rescaled ciphertext product (reference Engine::mul_ct)."""
+        return self._new(lib().fhe_mul, a.h, b.h)
+
+    def eval_chebyshev(self, ct: Ciphertext, coeffs, bound: float, prescaled: bool = False) -> Ciphertext:
+        """fhe_eval_chebyshev: sum_k c_k T_k(x / bound) (reference eval_chebyshev)."""
+        co = np.ascontiguousarray(coeffs, dtype=np.float64)
+        return self._new(lib().fhe_eval_chebyshev, ct.h, co.ctypes.data_as(_lib.dp), co.size, bound, int(prescaled))
+
     def linear(self, shards: Sequence[Ciphertext], c: int, m: int, w, b) -> Ciphertext:
         """fhe_linear: W x + b over a packed image's features (reference linear())."""
         w = np.ascontiguousarray(w, dtype=np.float64)

@@ -9,6 +9,7 @@ adapts calling conventions): inputs from its test helpers
 (tests/helpers.hpp:13-27), conv outputs and ledgers from conv_plan /
 convolve (conv.cpp:254-371), decompositions from rot.cpp:21-129.
 """
+import math
 import os
 import sys
 
@@ -58,6 +59,42 @@ CS_CASES = {
     "cs_cfg1_c2to4m128": (2, 128, 3, 4, 1021, 2021, 0, 4096),  # pc = 4, 16 output shards
     "cs_cfg3_c1m256k5": (1, 256, 5, 2, 1022, 2022, 0, 16384),  # pc = 4, 5x5
 }
+
+
+# Chebyshev activation (act.cpp:151-162): (func, degree, bound, prescaled, level, slots, seed); the
+# input is uniform on [-bound, bound] (divided by bound when prescaled), slots = the config's slots
+CHEB_CASES = {
+    "cheb_cfg3_gelu27_pre": ("gelu", 27, 10.0, 1, 12, 16384, 1050),  # test_act.cpp:78-96
+    "cheb_cfg3_gelu59_raw": ("gelu", 59, 16.0, 0, 12, 16384, 1051),  # the degree-59 table entry
+    "cheb_cfg3_relu27_raw": ("relu", 27, 16.0, 0, 12, 16384, 1052),
+    "cheb_cfg3_relu16_raw": ("relu", 16, 4.0, 0, 7, 16384, 1053),    # exact power of two: the p == d peel
+    "cheb_cfg1_gelu7_raw": ("gelu", 7, 4.0, 0, 4, 4096, 1054),      # cfg1: ends at level 0
+    "cheb_cfg1_identity": ("ident", 1, 4.0, 0, 4, 4096, 1055),     # test_act.cpp:99-110
+    "cheb_cfg1_const": ("const", 0, 4.0, 0, 4, 4096, 1056),        # degree 0
+}
+CHEB_KEEP = 2048  # stored output slots per case
+
+
+def cheb_func(name):
+    if name == "gelu":
+        return lambda x: x * 0.5 * (1.0 + math.erf(x / math.sqrt(2.0)))  # oracle.cpp:78-81
+    if name == "relu":
+        return lambda x: x if x > 0.0 else 0.0
+    return lambda x: x
+
+
+def cheb_case(name):
+    func, deg, bound, pre, level, s, seed = CHEB_CASES[name]
+    x = np.random.default_rng(seed).uniform(-bound, bound, s)
+    if pre:
+        x = x / bound
+    if func == "ident":
+        co = np.array([0.0, bound])
+    elif func == "const":
+        co = np.array([0.7])
+    else:
+        co = po.ref_cheb_interpolate(cheb_func(func), deg, bound)
+    return x, co
 
 
 def main():
@@ -119,6 +156,20 @@ def main():
         out[f"{name}/meta"] = meta
         out[f"{name}/tau"] = tau
         out[f"{name}/ledger"] = ledger
+    for name, (func, deg, bound, pre, level, s, seed) in CHEB_CASES.items():
+        x, co = cheb_case(name)
+        y, lv, depth, ledger = po.ref_eval_chebyshev(x, level, co, bound, pre)
+        out[f"{name}/params"] = np.array([deg, bound, pre, level, s, seed], dtype=np.float64)
+        out[f"{name}/x_sum"] = np.array([x.sum(), np.abs(x).sum()])
+        out[f"{name}/coeffs"] = co
+        out[f"{name}/slots"] = y[:CHEB_KEEP]
+        out[f"{name}/meta"] = np.array([lv, depth], dtype=np.int64)
+        out[f"{name}/ledger"] = ledger
+    try:
+        po.ref_eval_chebyshev(np.full(16, 0.1), 3, po.ref_cheb_interpolate(cheb_func("gelu"), 27, 10.0), 10.0, 1)
+        raise AssertionError("expected the level check to throw")
+    except RuntimeError as e:
+        out["cheb_level_error"] = np.frombuffer(str(e).encode(), dtype=np.uint8)
     rng = np.random.default_rng(77)
     vec = rng.uniform(-1, 1, 4096)
     out["slot_sum/vec_sum"] = np.array([vec.sum()])

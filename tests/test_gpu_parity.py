@@ -559,3 +559,87 @@ def test_pool_bit_exact_and_within_tolerance(oracle, golden, p1, name):
     ref = _golden_pool(p1.ck, ctr, p1.top, c, m, s)
     for o, r in zip(outs, ref):
         assert np.array_equal(o.residues(), r)
+
+
+# ------------------------------------------------------------ ct x ct, Chebyshev
+
+CHEB = ["cheb_cfg3_gelu27_pre", "cheb_cfg3_gelu59_raw", "cheb_cfg3_relu27_raw", "cheb_cfg3_relu16_raw",
+        "cheb_cfg1_gelu7_raw", "cheb_cfg1_identity", "cheb_cfg1_const"]
+# golden-model composition is CPU-heavy at cfg3; these are also checked residue for residue
+CHEB_BIT_EXACT = {"cheb_cfg3_gelu27_pre", "cheb_cfg1_gelu7_raw", "cheb_cfg1_identity", "cheb_cfg1_const"}
+
+
+def cheb_input(golden, name):
+    deg, bound, pre, level, s, seed = golden[f"{name}/params"]
+    x = np.random.default_rng(int(seed)).uniform(-bound, bound, int(s))
+    if pre:
+        x = x / bound
+    assert np.array_equal(np.array([x.sum(), np.abs(x).sum()]), golden[f"{name}/x_sum"])
+    return x, int(deg), float(bound), bool(pre), int(level)
+
+
+def test_mul_relin_bit_exact(p1):
+    """fhe_mul (tensor, relinearisation with the s^2 key, rescale) = ck_mul_ct; operands at
+    different levels are first brought to the common level (Engine::mul_ct's min level)."""
+    ctx, ck, L = p1.ctx, p1.ck, p1.top
+    ctx.gen_relin_key()
+    a, b = rnd(ctx.slots, 31), rnd(ctx.slots, 32)
+    ca = ctx.encrypt(ctx.encode(a), ENC_SEED)
+    cb = ctx.encrypt(ctx.encode(b, level=L - 1), ENC_SEED + 1)
+    out = ctx.mul(ca, cb)
+    assert out.level == L - 2
+    want = ck.mul_ct(ca.residues()[:, :L], cb.residues(), L - 1)
+    assert np.array_equal(out.residues(), want)
+    assert np.abs(ctx.decrypt(out) - a * b).max() < TOL
+    sq = ctx.mul(out, out)  # a second level: keys and scales compose
+    assert np.array_equal(sq.residues(), ck.mul_ct(want, want, L - 2))
+    assert np.abs(ctx.decrypt(sq) - (a * b) ** 2).max() < 1e-5
+
+
+def test_mul_requires_relin_key():
+    from paper_2306_09189_b200 import Context, FheError
+    ctx = Context.from_config("cfg1")
+    ctx.keygen(KEY_SEED)
+    ct = ctx.encrypt(ctx.encode(rnd(ctx.slots, 1)), ENC_SEED)
+    with pytest.raises(FheError, match="relinearisation key"):
+        ctx.mul(ct, ct)
+
+
+@pytest.mark.parametrize("name", CHEB)
+def test_chebyshev_matches_reference(oracle, golden, name):
+    """fhe_eval_chebyshev decrypts within 1e-6 of the reference's eval_chebyshev slots
+    (act.cpp:151-162), lands on the reference's output level with the same op counts, and
+    (CHEB_BIT_EXACT) equals the golden model's composition residue for residue."""
+    p = pair(oracle, "cfg3" if "cfg3" in name else "cfg1")
+    x, deg, bound, pre, level = cheb_input(golden, name)
+    co = golden[f"{name}/coeffs"]
+    p.ctx.gen_relin_key()
+    ct = p.ctx.encrypt(p.ctx.encode(x, level=level), ENC_SEED)
+    p.ctx.ledger_reset()
+    y = p.ctx.eval_chebyshev(ct, co, bound, pre)
+    lg = p.ctx.ledger()
+    want_level, want_depth = golden[f"{name}/meta"]
+    assert y.level == want_level
+    assert abs(y.scale - p.ctx.scale) <= 1e-9 * p.ctx.scale
+    dec = p.ctx.decrypt(y)
+    want = golden[f"{name}/slots"]
+    assert np.abs(dec[: want.size] - want).max() < TOL
+    assert np.abs(dec - oracle.cheb_eval(co, bound, x * (bound if pre else 1.0))).max() < TOL
+    ref_ledger = golden[f"{name}/ledger"]
+    assert (lg["ct_pt_mults"], lg["ct_ct_mults"], lg["adds"], lg["max_depth_consumed"]) == \
+        (ref_ledger[3], ref_ledger[4], ref_ledger[5], ref_ledger[7])
+    if name in CHEB_BIT_EXACT:
+        ck = p.ck
+        ctr = ck.encrypt(ck.encode(x, ck.scale, level), level, ENC_SEED)
+        out, lv, _ = ck.eval_chebyshev(ctr, level, ck.scale, co, bound, pre)
+        assert lv == y.level
+        assert np.array_equal(y.residues(), out)
+
+
+def test_chebyshev_insufficient_level(oracle, golden):
+    from paper_2306_09189_b200 import FheError
+    p = pair(oracle, "cfg3")
+    p.ctx.gen_relin_key()
+    ct = p.ctx.encrypt(p.ctx.encode(np.full(p.ctx.slots, 0.1), level=3), ENC_SEED)
+    with pytest.raises(FheError, match=bytes(golden["cheb_level_error"]).decode()):
+        p.ctx.eval_chebyshev(ct, golden["cheb_cfg3_gelu27_pre/coeffs"], 10.0, True)

@@ -239,3 +239,60 @@ def test_pool_restatement_matches_reference(oracle, golden, name):
             continue
         ch = int(tau[(g // rep) % c])
         assert np.abs(want[0][g * mn * mn:(g + 1) * mn * mn] - pooled[ch].ravel()).max() < 1e-12
+
+
+CHEB = ["cheb_cfg3_gelu27_pre", "cheb_cfg3_gelu59_raw", "cheb_cfg3_relu27_raw", "cheb_cfg3_relu16_raw",
+        "cheb_cfg1_gelu7_raw", "cheb_cfg1_identity", "cheb_cfg1_const"]
+
+
+def cheb_input(golden, name):
+    """the case's input slots (seeded uniform on [-B, B], / B when prescaled), checked against the fixture"""
+    deg, bound, pre, level, s, seed = golden[f"{name}/params"]
+    x = np.random.default_rng(int(seed)).uniform(-bound, bound, int(s))
+    if pre:
+        x = x / bound
+    assert np.array_equal(np.array([x.sum(), np.abs(x).sum()]), golden[f"{name}/x_sum"])
+    return x, int(deg), float(bound), bool(pre), int(level)
+
+
+@pytest.mark.parametrize("name", [n for n in CHEB if "gelu" in n or "relu" in n])
+def test_cheb_interpolate_restatement_bit_exact(oracle, golden, name):
+    """pyoracle.cheb_interpolate (restating act.cpp:90-113) = the reference's coefficients bit for bit."""
+    import math
+    deg, bound = int(golden[f"{name}/params"][0]), float(golden[f"{name}/params"][1])
+    if "gelu" in name:
+        f = lambda x: x * 0.5 * (1.0 + math.erf(x / math.sqrt(2.0)))  # noqa: E731
+    else:
+        f = lambda x: x if x > 0.0 else 0.0  # noqa: E731
+    assert np.array_equal(oracle.cheb_interpolate(f, deg, bound), golden[f"{name}/coeffs"])
+
+
+@pytest.mark.parametrize("name", CHEB)
+def test_cheb_series_equals_clenshaw(oracle, golden, name):
+    """The reference's power-of-two split evaluation (act.cpp:49-82) equals the plain Clenshaw
+    evaluation slotwise (test_act.cpp:78-96), and its level bookkeeping is bits(d) (+1 raw)."""
+    x, deg, bound, pre, level = cheb_input(golden, name)
+    want = golden[f"{name}/slots"]
+    co = golden[f"{name}/coeffs"]
+    xr = x[: want.size] * (bound if pre else 1.0)
+    assert np.abs(oracle.cheb_eval(co, bound, xr) - want).max() < 1e-9
+    lv, depth = golden[f"{name}/meta"]
+    assert lv == (level - (int(deg).bit_length() + (0 if pre else 1)) if deg > 0 else level)
+
+
+def test_cheb_level_error_text(golden):
+    assert bytes(golden["cheb_level_error"]).decode() == "insufficient level for activation: bootstrap required"
+
+
+def test_cheb_ckks_composition_matches_reference(oracle, golden):
+    """The golden model's ciphertext composition (relinearised products, scale targeting)
+    decrypts to the reference's eval_chebyshev slots (cfg1: degree 7, unprescaled)."""
+    name = "cheb_cfg1_gelu7_raw"
+    x, deg, bound, pre, level = cheb_input(golden, name)
+    ck = oracle.CKKS(13, [60] + [40] * 4, [60], 40)
+    ck.keygen(7)
+    ct = ck.encrypt(ck.encode(x, ck.scale, level), level, 9000)
+    out, lv, sc = ck.eval_chebyshev(ct, level, ck.scale, golden[f"{name}/coeffs"], bound, pre)
+    assert lv == golden[f"{name}/meta"][0] and sc == ck.scale
+    want = golden[f"{name}/slots"]
+    assert np.abs(ck.decrypt(out, lv, sc)[: want.size] - want).max() < 1e-6
