@@ -259,6 +259,10 @@ int fhe_pool(fhe_ctx* ctx, const fhe_ct* const* in, size_t t, int c, int m, fhe_
  * drops the higher operand to the common level, relinearises and rescales
  * (one level; scale = scale_a * scale_b / q_l). */
 int fhe_gen_relin_key(fhe_ctx* ctx);
+/* Engine::add_scalar (emu.cpp:113-119): ct + k in every slot, no level consumed */
+int fhe_add_scalar(fhe_ctx* ctx, const fhe_ct* ct, double k, fhe_ct** out);
+/* mul_plain by a constant vector (emu.cpp:56-67): ct * k, one level, scale preserved exactly */
+int fhe_mul_scalar(fhe_ctx* ctx, const fhe_ct* ct, double k, fhe_ct** out);
 int fhe_mul(fhe_ctx* ctx, const fhe_ct* a, const fhe_ct* b, fhe_ct** out);
 /* sum_k coeffs[k] T_k(x / bound) (x / bound already in [-1, 1] when prescaled),
  * the reference's power-of-two split; levels: bit length of n - 1 (+1 unless prescaled) */

@@ -465,10 +465,13 @@ class CKKS:
         with the scale targeting of fheconv.cu's ChebEval, op for op, so the residues
         are comparable bit for bit. Returns (ct, level, scale)."""
         primes = self.primes
-        S = self.N // 2
 
         def const(k, lv, sc):
-            return self.encode(np.full(S, k), sc, lv)
+            # the constant polynomial round(k * sc): its NTT rows are the constant itself
+            v = float(np.rint(k * sc))
+            assert abs(v) < 9.2e18
+            iv = int(v)
+            return np.stack([np.full(self.N, iv % int(primes[i]), dtype=np.uint64) for i in range(lv + 1)])
 
         def drop(v, lv):
             c, l0, sc = v
@@ -531,12 +534,12 @@ class CKKS:
         if level < needed:
             raise RuntimeError("insufficient level for activation: bootstrap required")
         out_level = level - needed
-        if d == 0:  # the reference's fresh encode (act.cpp:158)
-            pt = const(co[0], level, scale)
-            return (np.stack([pt, np.zeros_like(pt)]), level, scale)
         t = (np.ascontiguousarray(ct), level, scale)
         if not prescaled:
             t = mul_scalar(t, 1.0 / bound, level - 1, scale)
+        if d == 0:  # the reference's fresh encode (act.cpp:158)
+            pt = const(co[0], level, scale)
+            return (np.stack([pt, np.zeros_like(pt)]), level, scale)
         basis.append(t)
         p = 2
         while p <= floor_pow2(d):

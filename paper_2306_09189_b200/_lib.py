@@ -92,6 +92,8 @@ SIGNATURES = [
     ("fhe_conv_layer_shards", C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("fhe_slot_sum_batch", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, C.c_uint64, vpp]),
     ("fhe_gen_relin_key", C.c_int, [vp]),
+    ("fhe_add_scalar", C.c_int, [vp, vp, C.c_double, vpp]),
+    ("fhe_mul_scalar", C.c_int, [vp, vp, C.c_double, vpp]),
     ("fhe_mul", C.c_int, [vp, vp, vp, vpp]),
     ("fhe_eval_chebyshev", C.c_int, [vp, vp, dp, C.c_size_t, C.c_double, C.c_int, vpp]),
     ("fhe_pool", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, C.c_int, C.c_int, vpp, C.POINTER(C.c_size_t),

@@ -3086,6 +3086,55 @@ int fhe_pool(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, fhe_c
 // mul_ct with relinearisation (hybrid key switching of d2 with
 // the s^2 key, the same ModUp / inner-product / ModDown kernels) and the
 // reference's power-of-two-split Chebyshev evaluation (act.cpp:30-82, 151-162).
+// round(k * scale) as residues of the level's primes (the exact encoding of a constant slot vector)
+static RowConsts const_residues(fhe_ctx* c, double k, double scale, int level) {
+    const double v = std::nearbyint(k * scale);
+    if (!(std::fabs(v) < 9.2e18)) fail(FHE_E_INVALID, "constant too large for its scale");
+    const int64_t iv = (int64_t)v;
+    const uint64_t mag = iv < 0 ? (uint64_t)0 - (uint64_t)iv : (uint64_t)iv;
+    RowConsts r{};
+    for (int i = 0; i <= level; ++i) {
+        const uint64_t q = c->primes[i], m = mag % q;
+        r.v[i] = iv < 0 && m ? q - m : m;
+    }
+    return r;
+}
+
+// ct + k (reference Engine::add_scalar, emu.cpp:113-119): no level consumed
+static fhe_ct* add_scalar_ct(fhe_ctx* c, const fhe_ct* x, double k) {
+    fhe_ct* o = new_ct(c, x->level, x->scale, x->depth);
+    ew_const(c->dc, o->d, x->d, const_residues(c, k, x->scale, x->level), x->level + 1, 0, c->st);
+    c->ledger.adds++;
+    return o;
+}
+
+// ct * k rescaled onto (level, scale): the constant is scaled by scale * q_{level+1} / x.scale
+// (reference mul_plain with a constant vector, emu.cpp:56-67); x at level + 1
+static fhe_ct* mul_scalar_ct(fhe_ctx* c, const fhe_ct* x, double k, int level, double scale) {
+    const int nr = level + 2;
+    if (x->level != level + 1) fail(FHE_E_INVALID, "level mismatch");
+    uint64_t* pr = c->alloc((size_t)2 * nr * c->N);
+    ew_const(c->dc, pr, x->d, const_residues(c, k, scale * (double)c->primes[level + 1] / x->scale, level + 1), nr,
+             1, c->st);
+    fhe_ct* o = new_ct(c, level, scale, x->depth + 1);
+    rescale_into(c, pr, level + 1, o->d);
+    c->release(pr);
+    c->ledger.ct_pt_mults++;
+    c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, o->depth);
+    return o;
+}
+
+int fhe_add_scalar(fhe_ctx* c, const fhe_ct* x, double k, fhe_ct** out) {
+    return guard(c, [&] { *out = add_scalar_ct(c, x, k); });
+}
+
+int fhe_mul_scalar(fhe_ctx* c, const fhe_ct* x, double k, fhe_ct** out) {
+    return guard(c, [&] {
+        if (x->level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
+        *out = mul_scalar_ct(c, x, k, x->level - 1, x->scale);
+    });
+}
+
 int fhe_gen_relin_key(fhe_ctx* c) {
     return guard(c, [&] {
         require_key(c);
@@ -3154,9 +3203,11 @@ namespace {
 // emulator (act.cpp:49-82) adds values freely; in CKKS an addition needs equal
 // levels and scales, and ct x ct products land at scale s_a s_b / q_l. So every
 // sub-series is evaluated towards a (level, scale) target: leaves T_j * c are
-// plaintext products whose constant is encoded at exactly the scale that
-// rescales onto the target, and a product q * T_p asks q for the scale that
-// makes q * T_p / q_{l+1} hit the target. Same split, same basis, same depth.
+// constant products whose integer constant round(c * s') is picked so the
+// rescale lands exactly on the target, and a product q * T_p asks q for the scale
+// that makes q * T_p / q_{l+1} hit the target. Same split, same basis, same depth.
+// Constants never go through the slot encoder: a constant slot vector is the
+// constant polynomial, whose NTT rows are the constant itself.
 struct ChebEval {
     fhe_ctx* c;
     std::vector<fhe_ct*> owned;
@@ -3172,38 +3223,14 @@ struct ChebEval {
         if (x->level < level) fail(FHE_E_RUNTIME, "insufficient level for activation: bootstrap required");
         return x->level == level ? x : keep(drop_to(c, x, level));
     }
-    fhe_pt* constant(double k, int level, double scale) {
-        std::vector<double> v(c->slots(), k);
-        fhe_pt* pt = nullptr;
-        okc(c, fhe_encode(c, v.data(), v.size(), level, scale, 0, &pt));
-        return pt;
-    }
     fhe_ct* add(fhe_ct* a, fhe_ct* b) {
         fhe_ct* o = nullptr;
         okc(c, fhe_add(c, a, b, &o));
         return keep(o);
     }
-    fhe_ct* add_scalar(fhe_ct* x, double k) {
-        fhe_pt* pt = constant(k, x->level, x->scale);
-        fhe_ct* o = nullptr;
-        const int rc = fhe_add_plain(c, x, pt, &o);
-        fhe_pt_free(pt);
-        okc(c, rc);
-        return keep(o);
-    }
-    // x * k landing on (level, scale): constant encoded at scale * q_{level+1} / x.scale
+    fhe_ct* add_scalar(fhe_ct* x, double k) { return keep(add_scalar_ct(c, x, k)); }
     fhe_ct* mul_scalar(fhe_ct* x, double k, int level, double scale) {
-        fhe_ct* xs = at_level(x, level + 1);
-        fhe_pt* pt = constant(k, level + 1, scale * (double)c->primes[level + 1] / xs->scale);
-        fhe_ct* pr = nullptr;
-        const int rc = fhe_mul_plain(c, xs, pt, &pr);
-        fhe_pt_free(pt);
-        okc(c, rc);
-        keep(pr);
-        fhe_ct* rs = nullptr;
-        okc(c, fhe_rescale(c, pr, &rs));
-        rs->scale = scale;  // exact up to the double rounding of the encode scale
-        return keep(rs);
+        return keep(mul_scalar_ct(c, at_level(x, level + 1), k, level, scale));
     }
     fhe_ct* of_degree(size_t p2) const {
         size_t j = 0;
@@ -3257,14 +3284,9 @@ int fhe_eval_chebyshev(fhe_ctx* c, const fhe_ct* x, const double* coeffs, size_t
         fhe_ct* t = const_cast<fhe_ct*>(x);
         if (!prescaled) t = ev.mul_scalar(t, 1.0 / bound, x->level - 1, x->scale);  // act.cpp:156, also at d = 0
         if (d == 0) {  // a constant (the reference's fresh encode, act.cpp:158): trivial c1 = 0 ciphertext
-            std::vector<double> v(c->slots(), coeffs[0]);
-            fhe_pt* pt = nullptr;
-            okc(c, fhe_encode(c, v.data(), v.size(), x->level, x->scale, 0, &pt));
             fhe_ct* o = new_ct(c, x->level, x->scale, 0);
-            const size_t w = (size_t)(x->level + 1) * c->N;
-            ck(cudaMemcpyAsync(o->c0(), pt->d, w * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
-            ck(cudaMemsetAsync(o->c1(), 0, w * 8, c->st), "memset");
-            fhe_pt_free(pt);
+            ck(cudaMemsetAsync(o->d, 0, (size_t)2 * (x->level + 1) * c->N * 8, c->st), "memset");
+            ew_const(c->dc, o->d, o->d, const_residues(c, coeffs[0], x->scale, x->level), x->level + 1, 0, c->st);
             *out = o;
             return;
         }

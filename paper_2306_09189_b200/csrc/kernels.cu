@@ -185,6 +185,20 @@ __global__ void k_ew(DevCtx c, uint64_t* out, const uint64_t* a, const uint64_t*
     }
 }
 
+// per-prime constant (the NTT of a constant polynomial is that constant everywhere):
+// MODE 0 adds k_u to poly 0 and copies poly 1; MODE 1 multiplies both polys by k_u
+template <int MODE>
+__global__ void k_ew_const(DevCtx c, uint64_t* out, const uint64_t* a, RowConsts k, int nr) {
+    const size_t total = (size_t)2 * nr * c.N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i >> c.logN);
+        const int u = r % nr;
+        const Prime pr = c.primes[u];
+        if (MODE == 0) out[i] = r < nr ? add_mod(a[i], k.v[u], pr.q) : a[i];
+        if (MODE == 1) out[i] = mul_mod(a[i], k.v[u], pr);
+    }
+}
+
 __global__ void k_automorph(DevCtx c, uint64_t* out, const uint64_t* in, int nrows, uint32_t g) {
     const size_t total = (size_t)nrows * c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -243,6 +257,14 @@ void ew_mul_bcast(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint6
                   cudaStream_t st) {
     ++g_launches;
     k_ew<2><<<ew_blocks((size_t)nrows * c.N), kEwThreads, 0, st>>>(c, out, a, b, nrows, rpp);
+}
+void ew_const(const DevCtx& c, uint64_t* out, const uint64_t* a, const RowConsts& k, int nr, int mul,
+              cudaStream_t st) {
+    ++g_launches;
+    if (mul)
+        k_ew_const<1><<<ew_blocks((size_t)2 * nr * c.N), kEwThreads, 0, st>>>(c, out, a, k, nr);
+    else
+        k_ew_const<0><<<ew_blocks((size_t)2 * nr * c.N), kEwThreads, 0, st>>>(c, out, a, k, nr);
 }
 void automorph(const DevCtx& c, uint64_t* out, const uint64_t* in, int nrows, uint32_t galois, cudaStream_t st) {
     ++g_launches;

@@ -160,6 +160,12 @@ void ew_add(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b
 void ew_sub(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b, int nrows, int rpp,
             cudaStream_t st);
 // out[p][u] = a[p][u] * b[u] (b is one poly broadcast over the polys of a)
+struct RowConsts {
+    uint64_t v[kMaxPrimes];
+};
+// ciphertext (2 polys of nr rows) + / x a per-prime constant (mul = 0: add to poly 0)
+void ew_const(const DevCtx& c, uint64_t* out, const uint64_t* a, const RowConsts& k, int nr, int mul,
+              cudaStream_t st);
 void ew_mul_bcast(const DevCtx& c, uint64_t* out, const uint64_t* a, const uint64_t* b, int nrows,
                   int rpp, cudaStream_t st);
 void automorph(const DevCtx& c, uint64_t* out, const uint64_t* in, int nrows, uint32_t galois,

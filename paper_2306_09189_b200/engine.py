@@ -334,6 +334,13 @@ class Context:
     def gen_relin_key(self):
         self._check(lib().fhe_gen_relin_key(self.h))
 
+    def add_scalar(self, ct: Ciphertext, k: float) -> Ciphertext:
+        return self._new(lib().fhe_add_scalar, ct.h, float(k))
+
+    def mul_scalar(self, ct: Ciphertext, k: float) -> Ciphertext:
+        """ct * k in every slot, rescaled (one level, scale kept exactly)."""
+        return self._new(lib().fhe_mul_scalar, ct.h, float(k))
+
     def mul(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
         """fhe_mul: relinearised, rescaled ciphertext product (reference Engine::mul_ct)."""
         return self._new(lib().fhe_mul, a.h, b.h)

@@ -596,6 +596,27 @@ def test_mul_relin_bit_exact(p1):
     assert np.abs(ctx.decrypt(sq) - (a * b) ** 2).max() < 1e-5
 
 
+def test_scalar_ops_bit_exact(p1):
+    """fhe_add_scalar / fhe_mul_scalar: the constant polynomial round(k * scale) (its NTT rows are
+    the constant), added to c0 / multiplied in and rescaled with the scale kept exactly."""
+    ctx, ck, L = p1.ctx, p1.ck, p1.top
+    a = rnd(ctx.slots, 41)
+    ca = ctx.encrypt(ctx.encode(a), ENC_SEED)
+
+    def rows(v, lv):
+        iv = int(np.rint(v))
+        return np.stack([np.full(ck.N, iv % int(ck.primes[i]), dtype=np.uint64) for i in range(lv + 1)])
+
+    s1 = ctx.add_scalar(ca, -0.375)
+    assert np.array_equal(s1.residues(), ck.add_plain(ca.residues(), rows(-0.375 * ctx.scale, L), L))
+    assert np.abs(ctx.decrypt(s1) - (a - 0.375)).max() < TOL
+    m1 = ctx.mul_scalar(ca, -2.5)
+    assert m1.level == L - 1 and m1.scale == ctx.scale
+    want = ck.rescale(ck.mul_plain(ca.residues(), rows(-2.5 * ctx.scale * float(ck.primes[L]) / ctx.scale, L), L), L)
+    assert np.array_equal(m1.residues(), want)
+    assert np.abs(ctx.decrypt(m1) - (-2.5 * a)).max() < TOL
+
+
 def test_mul_requires_relin_key():
     from paper_2306_09189_b200 import Context, FheError
     ctx = Context.from_config("cfg1")
