@@ -551,7 +551,60 @@ def other_configs(world, device):
     res["cfg5"] = {"three_layer_passes_per_s": round(world * B5 / (ms / 1e3), 2),
                    "conv_per_s": round(world * 3 * B5 / (ms / 1e3), 1), "batch": B5, "levels_consumed": 3}
     ctx.close()
+    res["activation_cfg3"] = activation_bench(world, device)
     return res
+
+
+def _cheb_coeffs(f, n, bound):
+    """Chebyshev interpolant through n+1 Chebyshev nodes (the reference's cheb_interpolate rule)."""
+    j = np.arange(n + 1)
+    y = f(bound * np.cos(np.pi * (2 * j + 1) / (2 * (n + 1))))
+    co = np.array([2.0 * np.sum(y * np.cos(np.pi * k * (2 * j + 1) / (2 * (n + 1)))) / (n + 1)
+                   for k in range(n + 1)])
+    co[0] /= 2.0
+    return co
+
+
+def _cheb_clenshaw(co, bound, x):
+    t = x / bound
+    b1 = np.zeros_like(t)
+    b2 = np.zeros_like(t)
+    for k in range(len(co) - 1, 0, -1):
+        b1, b2 = 2.0 * t * b1 - b2 + co[k], b1
+    return t * b1 - b2 + co[0]
+
+
+def activation_bench(world, device):
+    """Chebyshev GELU on one cfg3 ciphertext at the top level (fhe_eval_chebyshev:
+    relinearised products + exact-scale constant leaves), degrees 27 (prescaled) and 59 (raw)."""
+    from math import erf, sqrt
+    from paper_2306_09189_b200 import Context
+    ctx = Context.from_config("cfg3", device=device)
+    ctx.keygen(7)
+    ctx.gen_relin_key()
+    gelu = np.vectorize(lambda v: v * 0.5 * (1.0 + erf(v / sqrt(2.0))))
+    x = np.random.default_rng(66).uniform(-16, 16, ctx.slots)
+    out = {}
+    for deg, pre in ((27, True), (59, False)):
+        co = _cheb_coeffs(gelu, deg, 16.0)
+        ct = ctx.encrypt(ctx.encode(x / 16.0 if pre else x), 1234)
+        y = ctx.eval_chebyshev(ct, co, 16.0, pre)
+        err = float(np.abs(ctx.decrypt(y) - _cheb_clenshaw(co, 16.0, x)).max())
+        ctx.ledger_reset()
+        reps, ms = 5, float("inf")
+        for _ in range(3):
+            ctx.synchronize()
+            ctx.timer_start()
+            for _ in range(reps):
+                ctx.eval_chebyshev(ct, co, 16.0, pre)
+            ms = min(ms, ctx.timer_stop())
+        lg = ctx.ledger()
+        out[f"gelu{deg}_{'prescaled' if pre else 'raw'}"] = {
+            "ms_per_ciphertext": round(ms / reps, 3), "ciphertexts_per_s": round(world * reps / (ms / 1e3), 1),
+            "levels_consumed": ctx.max_level - y.level, "ct_ct_mults": lg["ct_ct_mults"] // (3 * reps),
+            "ct_pt_mults": lg["ct_pt_mults"] // (3 * reps), "decrypt_max_abs_err_vs_clenshaw": err}
+    ctx.close()
+    return out
 
 
 def cfg2_rotations(world, nct=256):
