@@ -245,13 +245,25 @@ int fhe_slot_sum_batch(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, uint64_
 int fhe_linear(fhe_ctx* ctx, const fhe_ct* const* shards, size_t t, int c, int m, int out_features, const double* w,
                const double* b, fhe_ct** out);
 
-/* 2x2 average pooling (reference pool(), pool.cpp:291-297) of an
- * image-mode feature map without duplication (c m^2 = t * slots; t = 1, 2 or a
- * multiple of 4): outs (n_out ciphertexts, at most t) hold the (m/2)^2 channels
- * with the reference's packing metadata: tau_out[c] (physical channel position ->
- * logical channel), rep_out, d_out (duplication). Three levels. */
+/* 2x2 average pooling (reference pool(), pool.cpp:291-297) of
+ * the t shards of pack(img, slots) (image mode, t = 1, 2 or a multiple of 4,
+ * a single shard possibly duplicated; or channel shards, m^2 > slots): outs
+ * (n_out ciphertexts, at most t) hold the (m/2)^2 channels with the reference's
+ * packing metadata: tau_out[c] (physical channel position -> logical channel),
+ * rep_out, d_out (duplication). Three levels. */
 int fhe_pool(fhe_ctx* ctx, const fhe_ct* const* in, size_t t, int c, int m, fhe_ct** outs, size_t* n_out,
              int64_t* tau_out, int* rep_out, int* d_out);
+/* subsample_stride2 (pool.cpp:299-306): the same without the 2x2 window sum
+ * (every other row and column kept). Two levels. */
+int fhe_subsample_stride2(fhe_ctx* ctx, const fhe_ct* const* in, size_t t, int c, int m, fhe_ct** outs,
+                          size_t* n_out, int64_t* tau_out, int* rep_out, int* d_out);
+/* the general form (downsample + consolidate + duplicate_channels, pool.cpp:238-297)
+ * for any PackedImage: input tau (NULL = identity), rep, d; window 1 = 2x2 average
+ * (pool), 0 = stride-2; output_scale multiplies the vertical masks
+ * (reduce_vertical_*'s `scale`); mode_out 0 = image shards, 1 = channel shards. */
+int fhe_downsample(fhe_ctx* ctx, const fhe_ct* const* in, size_t t, int c, int m, const int64_t* tau_in, int rep_in,
+                   int d_in, int window, double output_scale, fhe_ct** outs, size_t* n_out, int64_t* tau_out,
+                   int* rep_out, int* d_out, int* mode_out);
 
 /* ciphertext x ciphertext multiplication and the Chebyshev
  * activation (reference Engine::mul_ct emu.cpp:69-80, eval_chebyshev act.cpp:151-162).

@@ -1368,8 +1368,12 @@ int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int
  * identity: P ct) and pt_b encoded over Q_l u P at scale q_l (ck_encode_plain
  * with_p = 1), pts = [n][level+1+K][N]. Equals sum_b pt_b * rot_b(ct) after
  * one rescale. */
-void ck_lintrans(const ck_ctx* ck, const uint64_t* ct, int level, int n, const long* amounts, const uint64_t* pts,
-                 uint64_t* out) {
+/* out = Rescale(ModDown(sum_b pt_b * KS_{amount_b}(ct_{src_b}))): several source
+   ciphertexts ([nsrc][2][level+1][N]), each ModUp'd once; every term is
+   accumulated in the QP basis before the single ModDown + rescale (the GPU's
+   lintrans_batch / channel-shard pooling window with spill terms). */
+void ck_lintrans_src(const ck_ctx* ck, const uint64_t* cts, int nsrc, int level, int n, const int* src,
+                     const long* amounts, const uint64_t* pts, uint64_t* out) {
     const size_t N = ck->N;
     const int nr = level + 1, ne = nr + ck->K, dn = ck_dnum_at(ck, level);
     const size_t extw = (size_t)ne * N, ctw = (size_t)2 * nr * N;
@@ -1381,18 +1385,20 @@ void ck_lintrans(const ck_ctx* ck, const uint64_t* ct, int level, int n, const l
         Pmod[u] = u < nr ? P : 0;
     }
     key_cache kc = {.n = 0};
-    uint64_t* dsrc = malloc((size_t)dn * extw * 8);
-    ck_modup(ck, ct + (size_t)nr * N, level, dsrc);
+    uint64_t* dsrc = malloc((size_t)nsrc * dn * extw * 8);
+    for (int j = 0; j < nsrc; j++) ck_modup(ck, cts + (size_t)j * ctw + (size_t)nr * N, level, dsrc + (size_t)j * dn * extw);
     uint64_t* ip0 = malloc(extw * 8);
     uint64_t* ip1 = malloc(extw * 8);
     uint64_t* y = calloc(2 * extw, 8);
     for (int b = 0; b < n; b++) {
         const uint64_t g = ck_galois_elt(ck, amounts[b]);
         const uint64_t* pt = pts + (size_t)b * extw;
+        const int j = src ? src[b] : 0;
+        const uint64_t* ct = cts + (size_t)j * ctw;
         if (g == 1) {
             conv_accumulate(ck, level, pt, ct, 1, NULL, NULL, Pmod, y, y + extw);
         } else {
-            ck_inner_product(ck, dsrc, level, cache_get(ck, &kc, g), g, ip0, ip1);
+            ck_inner_product(ck, dsrc + (size_t)j * dn * extw, level, cache_get(ck, &kc, g), g, ip0, ip1);
             conv_accumulate(ck, level, pt, ct, g, ip0, ip1, Pmod, y, y + extw);
         }
     }
@@ -1402,6 +1408,11 @@ void ck_lintrans(const ck_ctx* ck, const uint64_t* ct, int level, int n, const l
     ck_rescale(ck, md, level, out);
     cache_free(&kc);
     free(dsrc); free(ip0); free(ip1); free(y); free(md);
+}
+
+void ck_lintrans(const ck_ctx* ck, const uint64_t* ct, int level, int n, const long* amounts, const uint64_t* pts,
+                 uint64_t* out) {
+    ck_lintrans_src(ck, ct, 1, level, n, NULL, amounts, pts, out);
 }
 
 int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int kappa, int c_out,

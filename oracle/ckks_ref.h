@@ -115,6 +115,9 @@ int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int
  * pts [n][level+1+K][N] encoded over Q_l u P at scale q_l (see ckks_ref.c) */
 void ck_lintrans(const ck_ctx* ck, const uint64_t* ct, int level, int n, const long* amounts, const uint64_t* pts,
                  uint64_t* out);
+/* the same over nsrc source ciphertexts cts [nsrc][2][level+1][N]; term b reads cts[src[b]] */
+void ck_lintrans_src(const ck_ctx* ck, const uint64_t* cts, int nsrc, int level, int n, const int* src,
+                     const long* amounts, const uint64_t* pts, uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -92,6 +92,8 @@ def lib():
                                      u64p, dp]
         L.ck_conv_channel.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp, u64p, dp]
         L.ck_lintrans.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, lp, u64p, u64p]
+        L.ck_lintrans_src.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), lp, u64p,
+                                      u64p]
         L.emu_make_inputs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
                                       C.c_int, dp, dp]
         L.emu_rotate.argtypes = [dp, dp, C.c_size_t, C.c_long]
@@ -135,6 +137,8 @@ def ref():
                                     C.c_int, C.c_int]
         R.ref_linear.argtypes = [C.c_int, C.c_int, dp, C.c_int, dp, dp, C.c_uint64, dp, u64p]
         R.ref_pool.argtypes = [C.c_int, C.c_int, dp, C.c_uint64, dp, C.c_int, u64p, u64p, u64p]
+        R.ref_downsample.argtypes = [C.c_int, C.c_int, dp, C.c_uint64, C.c_int, C.c_double, dp, C.c_int, u64p, u64p,
+                                     u64p]
         R.ref_slot_sum.argtypes = [dp, C.c_uint64, C.c_uint64, dp]
         R.ref_eval_chebyshev.argtypes = [dp, C.c_uint64, C.c_int, dp, C.c_uint64, C.c_double, C.c_int, dp,
                                          C.POINTER(C.c_int64), u64p, C.c_char_p, C.c_uint64]
@@ -218,6 +222,20 @@ def ref_pool(c, m, img, s):
     ledger = np.zeros(9, dtype=np.uint64)
     n = ref().ref_pool(c, m, _ptr(np.ascontiguousarray(img, dtype=np.float64), dp), s, _ptr(out, dp), 16,
                        _ptr(meta, u64p), _ptr(tau, u64p), _ptr(ledger, u64p))
+    assert n > 0, n
+    return out[: n * s].reshape(n, s), meta, tau, ledger
+
+
+def ref_downsample(c, m, img, s, window=True, output_scale=1.0, cap=64):
+    """the reference's pool() (window) / subsample_stride2() of pack(img, s):
+    (shard slots [n][s], meta [m, c, d, rep, mode, n, rows_per_shard], tau, ledger)."""
+    out = np.zeros(cap * s)
+    meta = np.zeros(7, dtype=np.uint64)
+    tau = np.zeros(c, dtype=np.uint64)
+    ledger = np.zeros(9, dtype=np.uint64)
+    n = ref().ref_downsample(c, m, _ptr(np.ascontiguousarray(img, dtype=np.float64), dp), s, int(window),
+                             float(output_scale), _ptr(out, dp), cap, _ptr(meta, u64p), _ptr(tau, u64p),
+                             _ptr(ledger, u64p))
     assert n > 0, n
     return out[: n * s].reshape(n, s), meta, tau, ledger
 
@@ -589,6 +607,18 @@ class CKKS:
                           _ptr(np.ascontiguousarray(pts), u64p), _ptr(out, u64p))
         return out
 
+    def lintrans_src(self, cts, level, terms):
+        """Rescale(ModDown(sum pt * rot_amount(cts[src]))) over terms (src, amount, slot vector), all
+        accumulated in the QP basis before one ModDown + rescale."""
+        cts = np.ascontiguousarray(np.stack(cts), dtype=np.uint64)
+        pts = np.stack([self.encode(v, float(self.primes[level]), level, with_p=True) for _, _, v in terms])
+        src = (C.c_int * len(terms))(*[t[0] for t in terms])
+        a = (C.c_long * len(terms))(*[t[1] for t in terms])
+        out = np.zeros((2, level, self.N), dtype=np.uint64)
+        lib().ck_lintrans_src(self.h, _ptr(cts, u64p), cts.shape[0], level, len(terms), src, a,
+                              _ptr(np.ascontiguousarray(pts), u64p), _ptr(out, u64p))
+        return out
+
     def conv_channel(self, cts, level, c, m, kappa, c_out, filt):
         """channel-shard conv: cts [c * pc][2][level+1][N] -> [c_out * pc][2][level][N]."""
         cts = np.ascontiguousarray(cts, dtype=np.uint64)
@@ -600,3 +630,161 @@ class CKKS:
                                    C.byref(sc))
         assert rc == c_out * pc, rc
         return out, sc.value
+
+
+# ------------------------------------------------------------------ pooling restatement
+class NumpyOps:
+    """slot-vector backend of downsample_restated (the reference's arithmetic, no cryptography)."""
+
+    @staticmethod
+    def lintrans(srcs, terms):
+        return sum(v * np.roll(srcs[j], -a) for j, a, v in terms)
+
+    @staticmethod
+    def rotate(x, k):
+        return np.roll(x, -k)
+
+    @staticmethod
+    def add(a, b):
+        return a + b
+
+
+class CkksOps:
+    """golden CKKS backend: items are (residues, level); lintrans = ck_lintrans_src (all terms in
+    the QP basis, one ModDown + rescale), rotate = ck_rotate, add = ck_add."""
+
+    def __init__(self, ck):
+        self.ck = ck
+
+    def lintrans(self, srcs, terms):
+        lv = srcs[0][1]
+        return self.ck.lintrans_src([x for x, _ in srcs], lv, terms), lv - 1
+
+    def rotate(self, x, k):
+        return self.ck.rotate(x[0], x[1], k), x[1]
+
+    def add(self, a, b):
+        return self.ck.add(a[0], b[0], a[1]), a[1]
+
+
+def downsample_restated(ops, xs, c, m, s, window=True, oscale=1.0, d_in=1, tau_in=None, rep_in=1):
+    """pool() / subsample_stride2() (pool.cpp:10-306) restated in the rotation-of-mask form the
+    GPU runs (rot_k(x * mask) = rot_k(mask) * rot_k(x)): window (image: pool.cpp:22-30; channel
+    shards with the next shard's spill masks: :34-72), horizontal (:76-86) and vertical (:90-129)
+    stages as plaintext-weighted sums of rotations, then consolidation (:167-273) and channel
+    duplication (:276-289). Returns (shards, tau, rep, d, mode)."""
+    block = m * m
+    image = block <= s
+    t = len(xs)
+    tau0 = list(range(c)) if tau_in is None else list(tau_in)
+    pc, rows = (1, 0) if image else (block // s, s // m)
+    rot = lambda v, k: np.roll(v, -k)
+    X = list(xs)
+    if window:
+        if image:
+            terms = []
+            for kk, ll in ((0, 0), (0, 1), (1, 0), (1, 1)):
+                v = np.zeros(s)
+                for b in range(s // block):
+                    for i in range(m - kk):
+                        v[b * block + i * m: b * block + i * m + (m - ll)] = 0.25
+                terms.append((0, kk * m + ll, v))
+            X = [ops.lintrans([x], terms) for x in X]
+        else:
+            full, last = [], []
+            for kk, ll in ((0, 0), (0, 1), (1, 0), (1, 1)):
+                inm, spm = np.zeros(s), np.zeros(s)
+                for rr in range(rows):
+                    (inm if rr + kk < rows else spm)[rr * m: rr * m + (m - ll)] = 0.25
+                if inm.any():
+                    full.append((0, kk * m + ll, inm))
+                    last.append((0, kk * m + ll, inm))
+                if spm.any():
+                    full.append((1, kk * m + ll, spm))
+            X = [ops.lintrans([X[u], X[u + 1]], full) if (u % pc) + 1 < pc else ops.lintrans([X[u]], last)
+                 for u in range(t)]
+    live = [u for u in range(t) if image or rows != 1 or ((u % pc) * rows) % 2 == 0]
+    hterms = []
+    for i in range(m // 2):
+        mk = np.zeros(s)
+        mk[2 * i::m] = 1.0
+        hterms.append((0, i, rot(mk, i)))
+    R, vblock = (m, block) if image else (rows, s)
+    vterms = []
+    if R == 1:
+        mv = np.zeros(s)
+        mv[: m // 2] = oscale
+        vterms.append((0, 0, mv))
+    for j in range(R // 2):
+        mv = np.zeros(s)
+        for b in range(s // vblock):
+            mv[b * vblock + 2 * j * m: b * vblock + 2 * j * m + m // 2] = oscale
+        vterms.append((0, 3 * j * m // 2, rot(mv, 3 * j * m // 2)))
+    V = [None] * t
+    for u in live:
+        V[u] = ops.lintrans([ops.lintrans([X[u]], hterms)], vterms)
+    mn = m // 2
+    bn = mn * mn
+    tau, rep, d, mode, dup, stride = [0] * c, 1, 1, 0, 1, 0
+    res = []
+    if image:
+        z = c * d_in // t
+        if t == 1:
+            res, tau, rep, d, dup, stride = [V[0]], tau0, 4 * rep_in, 4 * d_in, 4, bn
+        elif t == 2:
+            res = [ops.add(V[0], ops.rotate(V[1], -2 * bn))]
+            tau = [tau0[(j % 2) * z + j // 2] for j in range(c)]
+            rep, d, dup, stride = 2, 2, 2, bn
+        else:
+            for w in range(t // 4):
+                acc = V[4 * w]
+                for q in range(1, 4):
+                    acc = ops.add(acc, ops.rotate(V[4 * w + q], -q * bn))
+                res.append(acc)
+                for g in range(4 * z):
+                    tau[w * 4 * z + g] = tau0[(4 * w + g % 4) * z + g // 4]
+    else:
+        for w in range((t + 3) // 4):
+            acc = None
+            for q in range(4):
+                if 4 * w + q >= t or V[4 * w + q] is None:
+                    continue
+                term = V[4 * w + q] if q == 0 else ops.rotate(V[4 * w + q], -q * (s // 4))
+                acc = term if acc is None else ops.add(acc, term)
+            res.append(acc)
+        tau = list(range(c))
+        if bn > s:
+            mode = 1
+        else:
+            valid = c * bn
+            d = s // valid if valid < s else 1
+            if d > 1:
+                dup, stride = d, valid
+    if dup > 1:
+        base = res[0]
+        out = base
+        for e in range(1, dup):
+            out = ops.add(out, ops.rotate(base, -e * stride))
+        res = [out]
+    return res, np.array(tau), rep, d, mode
+
+
+def downsample_steps(c, m, s, window=True):
+    """the Galois steps downsample_restated / fhe_downsample rotate by (nonzero, reduced mod s)."""
+    block, mn = m * m, m // 2
+    image = block <= s
+    rows = 0 if image else s // m
+    st = set()
+    if window:
+        st |= {1, m, m + 1}
+    st |= set(range(1, m // 2))
+    R = m if image else rows
+    st |= {3 * j * m // 2 for j in range(R // 2)}
+    bn = mn * mn
+    if image:
+        st |= {-q * bn for q in range(1, 4)}
+    else:
+        st |= {-q * (s // 4) for q in range(1, 4)}
+        if bn <= s and c * bn < s:
+            st |= {-e * c * bn for e in range(1, s // (c * bn))}
+    return sorted({k % s for k in st if k % s})

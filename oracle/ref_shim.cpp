@@ -255,6 +255,36 @@ int ref_pool(int c, int m, const double* img, uint64_t s, double* out_slots, int
     }
 }
 
+/// pool() / subsample_stride2() (pool.cpp:291-306) of pack(img, s) with an
+/// output scale: window 1 = pool, 0 = stride-2. Same outputs as ref_pool, meta
+/// gains [6] = rows_per_shard. Returns the shard count.
+int ref_downsample(int c, int m, const double* img, uint64_t s, int window, double output_scale, double* out_slots,
+                   int cap, uint64_t* meta, uint64_t* tau, uint64_t* ledger) {
+    try {
+        ImageTensor t(c, m);
+        std::memcpy(t.data.data(), img, t.data.size() * sizeof(double));
+        Engine eng;
+        PackedImage p = pack(eng, t, s);
+        eng.ledger().reset();
+        PackedImage out = window ? pool(eng, p, output_scale) : subsample_stride2(eng, p, output_scale);
+        const int n = (int)out.shards.size();
+        for (int u = 0; u < n && u < cap; ++u)
+            std::memcpy(out_slots + (size_t)u * s, out.shards[(size_t)u].slots.data(), s * sizeof(double));
+        meta[0] = out.m;
+        meta[1] = out.c;
+        meta[2] = out.d;
+        meta[3] = out.rep;
+        meta[4] = out.mode == ShardMode::ImageShard ? 0 : 1;
+        meta[5] = (uint64_t)n;
+        meta[6] = out.rows_per_shard;
+        for (size_t j = 0; j < out.tau.size(); ++j) tau[j] = out.tau[j];
+        fill_ledger(eng.ledger(), ledger);
+        return n;
+    } catch (...) {
+        return -1;
+    }
+}
+
 /// eval_chebyshev (act.cpp:151-162) of the slot vector `x` (s slots) placed at
 /// `level`: out receives the slots, meta = [output level, max depth consumed],
 /// ledger the op counters. Returns 0, or -2 with the exception text in `err`.

@@ -46,8 +46,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     objs = []
+    hdr = [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(ROOT, "include", "fheconv.h")]
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        deps = [os.path.join(CSRC, src)] + hdr
+        if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps
+                                                     if os.path.exists(d)):
+            objs.append(obj)
+            continue
         cmd = [_nvcc(), *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

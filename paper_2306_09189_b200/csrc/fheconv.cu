@@ -1445,6 +1445,110 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
     c->release(buf);
 }
 
+// QP plaintexts (slot vectors encoded over Q_l u P at scale q_l) of a term
+// list, encoded once per (key, level) and cached on the context.
+uint64_t* lt_plaintexts(fhe_ctx* c, const std::string& key, int level, const std::vector<std::vector<double>>& vecs) {
+    const int ne = c->ne_at(level);
+    const size_t extw = (size_t)ne * c->N;
+    const std::string ck_key = key + "/" + std::to_string(level);
+    auto it = c->lt_cache.find(ck_key);
+    if (it != c->lt_cache.end()) return it->second;
+    uint64_t* pts = nullptr;
+    ck(cudaMalloc(&pts, std::max<size_t>(1, vecs.size()) * extw * 8), "cudaMalloc");
+    for (size_t b = 0; b < vecs.size(); ++b)
+        encode_rows(c, vecs[b].data(), vecs[b].size(), level, (double)c->primes[level], ne, pts + b * extw);
+    ck(cudaStreamSynchronize(c->st), "sync");
+    c->lt_cache[ck_key] = pts;
+    return pts;
+}
+
+// one term of a plaintext-weighted sum of rotations: pt_b * rot_amount(source
+// shard u + slot) for output u (slot 1 = the next shard: channel-shard spill)
+struct LtTerm {
+    int64_t amount;
+    int slot;
+    int pt;  // index into the cached plaintexts
+};
+
+// Y_u += sum_b pt_b * X~_{src(u) + slot_b, amount_b} for nout outputs, output u
+// reading shard src0 + u * src_stride (+ slot) of the ModUp'd copies (dig, buf,
+// [shard][dn][ne][N] / [shard][2][l+1][N]); Y_u = Y + u * y_stride, [2][ne][N]
+// in the fused kernel's accumulation domain. Fused baby-step launches of <=
+// kMaxFused terms.
+void lt_accumulate(fhe_ctx* c, int level, const uint64_t* dig, const uint64_t* buf, int nout, size_t src0,
+                   size_t src_stride, const std::vector<LtTerm>& terms, const uint64_t* pts, uint64_t* Y,
+                   size_t y_stride) {
+    const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
+    if (nout <= 0 || terms.empty()) return;
+    FusedBsgs f{};
+    f.nsrc = nout;
+    f.ng = 1;
+    f.digits = dig + src0 * dw;
+    f.digit_src_stride = src_stride * dw;
+    f.digit_slot_stride = dw;
+    f.ct = buf + src0 * ctw;
+    f.ct_src_stride = src_stride * ctw;
+    f.ct_slot_stride = ctw;
+    f.Y = Y;
+    f.y_src_stride = y_stride;
+    f.y_g_stride = 2 * extw;
+    f.accumulate = 1;
+    for (size_t b0 = 0; b0 < terms.size(); b0 += kMaxFused) {
+        f.nb = 0;
+        double keyed = 0;
+        int nslot = 0;
+        for (size_t b = b0; b < terms.size() && f.nb < kMaxFused; ++b) {
+            const LtTerm& t = terms[b];
+            const uint32_t gal = c->galois_of(c->reduce_amount(t.amount));
+            f.galois[f.nb] = gal;
+            f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+            f.gmask[f.nb] = 1;
+            f.pt[f.nb] = pts + (size_t)t.pt * extw;
+            f.srcslot[f.nb] = (uint16_t)t.slot;
+            nslot = std::max(nslot, t.slot + 1);
+            f.nb++;
+            if (gal != 1) {
+                keyed += 1;
+                c->ledger.key_switches += (uint64_t)nout;
+            }
+        }
+        c->timed("bsgs_fused",
+                 c->rows(keyed * 2.0 * dn * ne + f.nb * ne +
+                         nout * (nslot * ((double)dn * ne + 2.0 * nr) + 4.0 * ne)),
+                 [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+    }
+    c->ledger.ct_pt_mults += (uint64_t)nout * terms.size();
+}
+
+// device copies + ModUp of n shards at one level: buf [n][2][l+1][N], dig [n][dn][ne][N]
+void lt_modup(fhe_ctx* c, const fhe_ct* const* cts, int n, uint64_t** buf, uint64_t** dig) {
+    const int level = cts[0]->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
+    const size_t N = c->N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * ne * N;
+    for (int i = 0; i < n; ++i)
+        if (cts[i]->level != level) fail(FHE_E_INVALID, "shards are at different levels");
+    *buf = c->alloc((size_t)n * ctw);
+    for (int i = 0; i < n; ++i)
+        ck(cudaMemcpyAsync(*buf + (size_t)i * ctw, cts[i]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    *dig = c->alloc((size_t)n * dw);
+    modup_batch(c, *buf + (size_t)nr * N, ctw, n, level, *dig);
+}
+
+// outs[u] = Rescale(ModDown(Y_u)) for S accumulators (one level), metadata from src[u]
+void lt_finish(fhe_ctx* c, const uint64_t* Y, int S, int level, const fhe_ct* const* src, fhe_ct* const* outs) {
+    const int ne = c->ne_at(level);
+    const size_t N = c->N, extw = (size_t)ne * N, otw = (size_t)2 * level * N;
+    uint64_t* md = c->alloc((size_t)S * otw);
+    giants_finish(c, Y, 2 * extw, S, level, {}, {0}, 0, md);
+    for (int i = 0; i < S; ++i) {
+        ck(cudaMemcpyAsync(outs[i]->d, md + (size_t)i * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+        outs[i]->scale = src[i]->scale;
+        outs[i]->depth = src[i]->depth + 1;
+        c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[i]->depth);
+    }
+    c->release(md);
+}
+
 // out_s = Rescale(ModDown(sum_b pt_b * X~_{s,b})) for S ciphertexts sharing the
 // term list (rotation amount, plaintext slot vector): the fused baby-step
 // kernel with one accumulator; pt_b = rot-free slot vectors encoded over
@@ -1452,72 +1556,19 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
 void lintrans_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const std::string& key,
                     const std::vector<int64_t>& amounts, const std::vector<std::vector<double>>& vecs,
                     fhe_ct* const* outs) {
-    const int level = cts[0]->level, nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
-    const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
-    const int nb = (int)amounts.size();
+    const int level = cts[0]->level, ne = c->ne_at(level);
+    const size_t extw = (size_t)ne * c->N;
     if (level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
-    const std::string ck_key = key + "/" + std::to_string(level);
-    auto it = c->lt_cache.find(ck_key);
-    uint64_t* pts = nullptr;
-    if (it == c->lt_cache.end()) {
-        ck(cudaMalloc(&pts, (size_t)nb * extw * 8), "cudaMalloc");
-        for (int b = 0; b < nb; ++b)
-            encode_rows(c, vecs[(size_t)b].data(), vecs[(size_t)b].size(), level, (double)c->primes[level], ne,
-                        pts + (size_t)b * extw);
-        ck(cudaStreamSynchronize(c->st), "sync");
-        c->lt_cache[ck_key] = pts;
-    } else {
-        pts = it->second;
-    }
-    uint64_t* buf = c->alloc((size_t)S * ctw);
-    for (int i = 0; i < S; ++i)
-        ck(cudaMemcpyAsync(buf + (size_t)i * ctw, cts[i]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
-    uint64_t* dig = c->alloc((size_t)S * dw);
-    modup_batch(c, buf + (size_t)nr * N, ctw, S, level, dig);
+    const uint64_t* pts = lt_plaintexts(c, key, level, vecs);
+    uint64_t *buf, *dig;
+    lt_modup(c, cts, S, &buf, &dig);
     uint64_t* Y = c->alloc((size_t)S * 2 * extw);
     ck(cudaMemsetAsync(Y, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
-    FusedBsgs f{};
-    f.nsrc = S;
-    f.ng = 1;
-    f.digits = dig;
-    f.digit_src_stride = dw;
-    f.ct = buf;
-    f.ct_src_stride = ctw;
-    f.Y = Y;
-    f.y_src_stride = 2 * extw;
-    f.y_g_stride = 2 * extw;
-    f.accumulate = 1;
-    for (int b0 = 0; b0 < nb; b0 += kMaxFused) {
-        f.nb = 0;
-        double keyed = 0;
-        for (int b = b0; b < nb && f.nb < kMaxFused; ++b) {
-            const uint32_t gal = c->galois_of(c->reduce_amount(amounts[(size_t)b]));
-            f.galois[f.nb] = gal;
-            f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
-            f.gmask[f.nb] = 1;
-            f.pt[f.nb] = pts + (size_t)b * extw;
-            f.srcslot[f.nb] = 0;
-            f.nb++;
-            if (gal != 1) {
-                keyed += 1;
-                c->ledger.key_switches += S;
-            }
-        }
-        c->timed("bsgs_fused", c->rows(keyed * 2.0 * dn * ne + f.nb * ne + S * ((double)dn * ne + 2.0 * nr + 4.0 * ne)),
-                 [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
-    }
-    c->ledger.ct_pt_mults += (uint64_t)S * nb;
+    std::vector<LtTerm> terms;
+    for (size_t b = 0; b < amounts.size(); ++b) terms.push_back({amounts[b], 0, (int)b});
+    lt_accumulate(c, level, dig, buf, S, 0, 1, terms, pts, Y, 2 * extw);
     c->release(dig);
-    const size_t otw = (size_t)2 * level * N;
-    uint64_t* md = c->alloc((size_t)S * otw);
-    giants_finish(c, Y, 2 * extw, S, level, {}, {0}, 0, md);
-    for (int i = 0; i < S; ++i) {
-        ck(cudaMemcpyAsync(outs[i]->d, md + (size_t)i * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
-        outs[i]->scale = cts[i]->scale;
-        outs[i]->depth = cts[i]->depth + 1;
-        c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[i]->depth);
-    }
-    c->release(md);
+    lt_finish(c, Y, S, level, cts, outs);
     c->release(Y);
     c->release(buf);
 }
@@ -2951,136 +3002,310 @@ int fhe_linear(fhe_ctx* c, const fhe_ct* const* shards, size_t t, int ch, int m,
 
 
 // ------------------------------------------------------------- pooling
-// 2x2 average pooling (reference pool(), pool.cpp:291-297) of
-// an image-mode feature map without duplication (c m^2 = t slots, t = 1, 2
-// or a multiple of 4). The reference's three masked stages are each one
-// plaintext-weighted sum of hoisted rotations (rot_k(x * mask) = rot_k(mask)
-// * rot_k(x)), run by the fused baby-step kernel for all shards at once:
-//   window     W = sum_{(kk,ll) in 2x2} wmask(kk, ll) * rot_{kk m + ll}(x)      (pool.cpp:22-30)
-//   horizontal H = sum_{i < m/2} rot_i(hmask_i) * rot_i(W)                      (pool.cpp:76-86)
-//   vertical   V = sum_{j < m/2} rot_{3jm/2}(vmask_j) * rot_{3jm/2}(H)           (pool.cpp:90-104)
-// then the reference's consolidation rotations (pool.cpp:167-226) and channel
-// duplication (pool.cpp:280-289). Three levels.
-int fhe_pool(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, fhe_ct** outs, size_t* n_out,
-             int64_t* tau_out, int* rep_out, int* d_out) {
-    return guard(c, [&] {
-        const size_t s = c->slots(), block = (size_t)m * m;
-        if (m < 2 || (m & (m - 1))) fail(FHE_E_INVALID, "cannot pool a 1x1 channel");
-        if (block > s || (size_t)ch * block != t * s)
-            fail(FHE_E_INVALID, "pooling expects an image-mode feature map without duplication (c m^2 = t slots)");
-        if (!(t == 1 || t == 2 || t % 4 == 0)) fail(FHE_E_INVALID, "shard count must be 1, 2 or a multiple of 4");
-        const int level = in[0]->level;
-        if (level < 3) fail(FHE_E_RUNTIME, "depth exhausted");
-        const long mL = m;
-        auto window_mask = [&](long kk, long ll) {
+// 2x2 average pooling (reference pool(), pool.cpp:291-297)
+// and stride-2 subsampling (subsample_stride2, pool.cpp:299-306) of image-mode
+// and channel-shard feature maps. The reference's masked stages become
+// plaintext-weighted sums of hoisted rotations (rot_k(x * mask) = rot_k(mask) *
+// rot_k(x)), each one fused baby-step pass over all shards:
+//   window     W = sum_{(kk,ll) in 2x2} wmask(kk, ll) * rot_{kk m + ll}(x)       (pool.cpp:22-30)
+//              channel shards add the spill masks of the next shard (:34-72)
+//   horizontal H = sum_{i < m/2} rot_i(hmask_i) * rot_i(W)                       (pool.cpp:76-86)
+//   vertical   V = sum_{j < R/2} rot_{3jm/2}(vmask_j) * rot_{3jm/2}(H)            (pool.cpp:90-129)
+//              R = m (image) or rows per shard (channel; rows = 1: even shards
+//              masked, odd shards dropped)
+// then the reference's consolidation (pool.cpp:167-273) and duplication
+// (:276-289) rotations. Stride-2 skips the window stage. 3 (pool) / 2 levels.
+static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, const int64_t* tau_in,
+                            int rep_in, int d_in, int window, double oscale, fhe_ct** outs, size_t* n_out,
+                            int64_t* tau_out, int* rep_out, int* d_out, int* mode_out) {
+    const size_t s = c->slots();
+    if (t == 0 || !in) fail(FHE_E_INVALID, "packed image has no shards");
+    if (m < 2) fail(FHE_E_INVALID, window ? "cannot pool a 1x1 channel" : "cannot subsample a 1x1 channel");
+    if ((m & (m - 1)) || ch < 1 || (ch & (ch - 1))) fail(FHE_E_INVALID, "dimensions must be powers of two");
+    const size_t block = (size_t)m * m;
+    const bool image = block <= s;
+    if (rep_in < 1 || d_in < 1) fail(FHE_E_INVALID, "metadata mismatch");
+    if (image) {
+        if (t >= 2 && d_in != 1) fail(FHE_E_INVALID, "metadata mismatch: duplicated multi-shard image");
+        if ((size_t)ch * block * (size_t)d_in != t * s) fail(FHE_E_INVALID, "metadata mismatch: shard count");
+    } else if (d_in != 1 || t != (size_t)ch * (block / s)) {
+        fail(FHE_E_INVALID, "metadata mismatch: shard count");
+    }
+    std::vector<int64_t> tau0((size_t)ch);
+    for (int j = 0; j < ch; ++j) tau0[(size_t)j] = tau_in ? tau_in[j] : j;
+    const int level = in[0]->level;
+    for (size_t u = 0; u < t; ++u)
+        if (in[u]->level != level) fail(FHE_E_INVALID, "shards are at different levels");
+    if (level < (window ? 3 : 2)) fail(FHE_E_RUNTIME, "depth exhausted");
+    const long mL = m;
+    const size_t pc = image ? 1 : block / s, rows = image ? 0 : s / (size_t)m;
+    auto rotl = [&](const std::vector<double>& v, int64_t k) {
+        std::vector<double> r(s);
+        const size_t a = (size_t)(((k % (int64_t)s) + (int64_t)s) % (int64_t)s);
+        for (size_t i = 0; i < s; ++i) r[i] = v[(i + a) % s];
+        return r;
+    };
+    const std::string geo = std::to_string(m) + "/" + std::to_string(s);
+    auto fresh = [&](const std::vector<const fhe_ct*>& src) {
+        std::vector<fhe_ct*> o(src.size());
+        for (size_t u = 0; u < src.size(); ++u) o[u] = new_ct(c, src[u]->level - 1, src[u]->scale, src[u]->depth + 1);
+        return o;
+    };
+    auto count_rot = [&](const std::vector<int64_t>& am, size_t times) {
+        size_t k = 0;
+        for (int64_t x : am) k += c->reduce_amount(x) != 0;
+        c->ledger.rotations += (uint64_t)(k * times);
+    };
+    auto stage = [&](const std::vector<const fhe_ct*>& src, const std::string& name, const std::vector<int64_t>& am,
+                     const std::vector<std::vector<double>>& pts) {
+        std::vector<fhe_ct*> o = fresh(src);
+        if (!src.empty()) lintrans_batch(c, src.data(), (int)src.size(), name + "/" + geo, am, pts, o.data());
+        count_rot(am, src.size());
+        return o;
+    };
+    auto free_all = [&](std::vector<fhe_ct*>& v) {
+        for (fhe_ct* x : v)
+            if (x) fhe_ct_free(x);
+        v.clear();
+    };
+    // ---- window stage
+    std::vector<fhe_ct*> W;
+    if (window && image) {
+        std::vector<int64_t> aw;
+        std::vector<std::vector<double>> pw;
+        for (auto kl : {std::pair<long, long>{0, 0}, {0, 1}, {1, 0}, {1, 1}}) {
             std::vector<double> v(s, 0.0);
             for (size_t b = 0; b * block < s; ++b)
-                for (long i = 0; i + kk < mL; ++i)
-                    for (long j = 0; j + ll < mL; ++j) v[b * block + (size_t)(i * mL + j)] = 0.25;
-            return v;
-        };
-        auto rotl = [&](const std::vector<double>& v, int64_t k) {
-            std::vector<double> r(s);
-            const size_t a = (size_t)(((k % (int64_t)s) + (int64_t)s) % (int64_t)s);
-            for (size_t i = 0; i < s; ++i) r[i] = v[(i + a) % s];
-            return r;
-        };
-        std::vector<int64_t> aw, ah, av;
-        std::vector<std::vector<double>> pw, ph, pv;
-        for (auto kl : {std::pair<long, long>{0, 0}, {0, 1}, {1, 0}, {1, 1}}) {
+                for (long i = 0; i + kl.first < mL; ++i)
+                    for (long j = 0; j + kl.second < mL; ++j) v[b * block + (size_t)(i * mL + j)] = 0.25;
             aw.push_back(kl.first * mL + kl.second);
-            pw.push_back(window_mask(kl.first, kl.second));
+            pw.push_back(std::move(v));
         }
-        for (long i2 = 0; i2 < mL / 2; ++i2) {
-            std::vector<double> mk(s, 0.0);
-            for (size_t row = 0; row < s; row += (size_t)m) mk[row + 2 * (size_t)i2] = 1.0;
-            ah.push_back(i2);
-            ph.push_back(rotl(mk, i2));
-            std::vector<double> mv(s, 0.0);
-            for (size_t b = 0; b * block < s; ++b)
-                for (long col = 0; col < mL / 2; ++col) mv[b * block + (size_t)(2 * i2 * mL + col)] = 1.0;
-            av.push_back(3 * i2 * mL / 2);
-            pv.push_back(rotl(mv, 3 * i2 * mL / 2));
+        W = stage(std::vector<const fhe_ct*>(in, in + t), "pool-window", aw, pw);
+    } else if (window) {  // channel shards: in-shard masks of shard v + spill masks of shard v + 1
+        std::vector<std::vector<double>> pv;
+        std::vector<LtTerm> full, last;
+        for (auto kl : {std::pair<long, long>{0, 0}, {0, 1}, {1, 0}, {1, 1}}) {
+            const long kk = kl.first, ll = kl.second, amount = kk * mL + ll;
+            std::vector<double> inm(s, 0.0), spm(s, 0.0);
+            bool any_in = false, any_spill = false;
+            for (long rr = 0; rr < (long)rows; ++rr)
+                for (long j = 0; j + ll < mL; ++j) {
+                    if (rr + kk < (long)rows) {
+                        inm[(size_t)(rr * mL + j)] = 0.25;
+                        any_in = true;
+                    } else {
+                        spm[(size_t)(rr * mL + j)] = 0.25;
+                        any_spill = true;
+                    }
+                }
+            if (any_in) {
+                pv.push_back(std::move(inm));
+                full.push_back({amount, 0, (int)pv.size() - 1});
+                last.push_back({amount, 0, (int)pv.size() - 1});
+            }
+            if (any_spill) {
+                pv.push_back(std::move(spm));
+                full.push_back({amount, 1, (int)pv.size() - 1});
+            }
         }
-        auto stage = [&](const std::vector<const fhe_ct*>& src, const char* name, const std::vector<int64_t>& am,
-                         const std::vector<std::vector<double>>& pts) {
-            std::vector<fhe_ct*> o(src.size());
-            for (size_t u = 0; u < src.size(); ++u)
-                o[u] = new_ct(c, src[u]->level - 1, src[u]->scale, src[u]->depth + 1);
-            lintrans_batch(c, src.data(), (int)src.size(), std::string("pool-") + name + "/" + std::to_string(m), am,
-                           pts, o.data());
-            return o;
-        };
-        std::vector<const fhe_ct*> x(in, in + t);
-        std::vector<fhe_ct*> W = stage(x, "window", aw, pw);
-        std::vector<fhe_ct*> H = stage(std::vector<const fhe_ct*>(W.begin(), W.end()), "horizontal", ah, ph);
-        for (fhe_ct* p : W) fhe_ct_free(p);
-        std::vector<fhe_ct*> V = stage(std::vector<const fhe_ct*>(H.begin(), H.end()), "vertical", av, pv);
-        for (fhe_ct* p : H) fhe_ct_free(p);
-        c->ledger.rotations += (uint64_t)t * (aw.size() + ah.size() + av.size() - 3);  // amount 0 terms are free
-        const int64_t bn = (int64_t)(block / 4);
-        const size_t z = (size_t)ch / t;
-        std::vector<int64_t> tau((size_t)ch);
-        std::vector<fhe_ct*> res;
-        int rep = 1, dup = 1;
-        auto rot1 = [&](const fhe_ct* a, int64_t k) {
-            fhe_ct* o = new_ct(c, a->level, a->scale, a->depth);
-            okc(c, fhe_rotate_hoisted_batch_into(c, &a, 1, &k, 1, &o));
-            return o;
-        };
-        auto add_into = [&](fhe_ct* acc, const fhe_ct* b) {
-            ew_add(c->dc, acc->d, acc->d, b->d, 2 * (acc->level + 1), acc->level + 1, c->st);
-            c->ledger.adds++;
-        };
+        const uint64_t* pts = lt_plaintexts(c, "pool-window-ch/" + geo, level, pv);
+        const int ne = c->ne_at(level);
+        const size_t extw = (size_t)ne * c->N;
+        uint64_t *buf, *dig;
+        lt_modup(c, in, (int)t, &buf, &dig);
+        uint64_t* Y = c->alloc(t * 2 * extw);
+        ck(cudaMemsetAsync(Y, 0, t * 2 * extw * 8, c->st), "memset");
+        for (int f = 0; f < ch; ++f)
+            lt_accumulate(c, level, dig, buf, (int)pc - 1, (size_t)f * pc, 1, full, pts, Y + (size_t)f * pc * 2 * extw,
+                          2 * extw);
+        lt_accumulate(c, level, dig, buf, ch, pc - 1, pc, last, pts, Y + (pc - 1) * 2 * extw, pc * 2 * extw);
+        c->release(dig);
+        std::vector<const fhe_ct*> src(in, in + t);
+        W = fresh(src);
+        lt_finish(c, Y, (int)t, level, in, W.data());
+        c->release(Y);
+        c->release(buf);
+        size_t nrot = 0;
+        for (const LtTerm& x : full) nrot += (size_t)(c->reduce_amount(x.amount) != 0) * (pc - 1);
+        for (const LtTerm& x : last) nrot += (size_t)(c->reduce_amount(x.amount) != 0);
+        c->ledger.rotations += (uint64_t)(nrot * (size_t)ch);
+    }
+    // ---- compact: horizontal + vertical (pool.cpp:131-150); channel shards with one
+    // row drop odd shards (no output)
+    std::vector<const fhe_ct*> X(t);
+    for (size_t u = 0; u < t; ++u) X[u] = window ? W[u] : in[u];
+    std::vector<size_t> live;
+    for (size_t u = 0; u < t; ++u)
+        if (image || rows != 1 || ((u % pc) * rows) % 2 == 0) live.push_back(u);
+    std::vector<const fhe_ct*> xl;
+    for (size_t u : live) xl.push_back(X[u]);
+    std::vector<int64_t> ah, av;
+    std::vector<std::vector<double>> ph, pvv;
+    for (long i2 = 0; i2 < mL / 2; ++i2) {
+        std::vector<double> mk(s, 0.0);
+        for (size_t row = 0; row < s; row += (size_t)m) mk[row + 2 * (size_t)i2] = 1.0;
+        ah.push_back(i2);
+        ph.push_back(rotl(mk, i2));
+    }
+    std::vector<fhe_ct*> H = stage(xl, "pool-horizontal", ah, ph);
+    free_all(W);
+    const size_t R = image ? (size_t)m : rows;
+    const size_t vblock = image ? block : s;
+    if (R == 1) {
+        std::vector<double> mv(s, 0.0);
+        for (long col = 0; col < mL / 2; ++col) mv[(size_t)col] = oscale;
+        av.push_back(0);
+        pvv.push_back(std::move(mv));
+    }
+    for (size_t j = 0; j < R / 2; ++j) {
+        std::vector<double> mv(s, 0.0);
+        for (size_t b = 0; b * vblock < s; ++b)
+            for (long col = 0; col < mL / 2; ++col) mv[b * vblock + 2 * j * (size_t)m + (size_t)col] = oscale;
+        av.push_back((int64_t)(3 * j * (size_t)m / 2));
+        pvv.push_back(rotl(mv, av.back()));
+    }
+    char vkey[64];
+    snprintf(vkey, sizeof vkey, "pool-vertical-%d-%a", image ? 0 : 1, oscale);
+    std::vector<fhe_ct*> Vl = stage(std::vector<const fhe_ct*>(H.begin(), H.end()), vkey, av, pvv);
+    free_all(H);
+    std::vector<fhe_ct*> V(t, nullptr);
+    for (size_t k = 0; k < live.size(); ++k) V[live[k]] = Vl[k];
+    // ---- consolidation (pool.cpp:167-273)
+    auto rot1 = [&](const fhe_ct* a, int64_t k) {
+        fhe_ct* o = new_ct(c, a->level, a->scale, a->depth);
+        okc(c, fhe_rotate_hoisted_batch_into(c, &a, 1, &k, 1, &o));
+        return o;
+    };
+    auto add_into = [&](fhe_ct* acc, const fhe_ct* b) {
+        ew_add(c->dc, acc->d, acc->d, b->d, 2 * (acc->level + 1), acc->level + 1, c->st);
+        c->ledger.adds++;
+    };
+    const size_t mn = (size_t)m / 2, bn = mn * mn;
+    std::vector<int64_t> tau((size_t)ch);
+    std::vector<fhe_ct*> res;
+    int rep = 1, d = 1, mode = 0;
+    size_t dup = 1, dup_stride = 0;
+    if (image) {
+        const size_t z = (size_t)ch * (size_t)d_in / t;
         if (t == 1) {
             res.push_back(V[0]);
-            for (size_t j = 0; j < (size_t)ch; ++j) tau[j] = (int64_t)j;
-            rep = 4;
+            tau = tau0;
+            rep = 4 * rep_in;
+            d = 4 * d_in;
             dup = 4;
+            dup_stride = bn;
         } else if (t == 2) {
-            fhe_ct* r = rot1(V[1], -2 * bn);
+            fhe_ct* r = rot1(V[1], -2 * (int64_t)bn);
             add_into(V[0], r);
             fhe_ct_free(r);
             fhe_ct_free(V[1]);
             res.push_back(V[0]);
-            for (size_t j = 0; j < (size_t)ch; ++j) tau[j] = (int64_t)((j % 2) * z + j / 2);
+            for (size_t j = 0; j < (size_t)ch; ++j) tau[j] = tau0[(j % 2) * z + j / 2];
             rep = 2;
+            d = 2;
             dup = 2;
+            dup_stride = bn;
         } else {
+            if (t % 4) fail(FHE_E_INVALID, "shard count must be 1, 2 or a multiple of 4");
             const size_t blocks_out = 4 * z;
             for (size_t w4 = 0; w4 < t / 4; ++w4) {
                 for (size_t q = 1; q < 4; ++q) {
-                    fhe_ct* r = rot1(V[4 * w4 + q], -(int64_t)q * bn);
+                    fhe_ct* r = rot1(V[4 * w4 + q], -(int64_t)(q * bn));
                     add_into(V[4 * w4], r);
                     fhe_ct_free(r);
                     fhe_ct_free(V[4 * w4 + q]);
                 }
                 res.push_back(V[4 * w4]);
-                for (size_t g = 0; g < blocks_out; ++g) tau[w4 * blocks_out + g] = (int64_t)((4 * w4 + g % 4) * z + g / 4);
+                for (size_t g = 0; g < blocks_out; ++g) tau[w4 * blocks_out + g] = tau0[(4 * w4 + g % 4) * z + g / 4];
             }
         }
-        if (dup > 1) {  // channel duplication: base + sum_e rot_{-e block_new}(base), hoisted
-            fhe_ct* base = res[0];
-            std::vector<int64_t> ks;
-            for (int e = 1; e < dup; ++e) ks.push_back(-(int64_t)e * bn);
-            std::vector<fhe_ct*> rs(ks.size());
-            for (size_t e = 0; e < ks.size(); ++e) rs[e] = new_ct(c, base->level, base->scale, base->depth);
-            const fhe_ct* bc = base;
-            okc(c, fhe_rotate_hoisted_batch_into(c, &bc, 1, ks.data(), ks.size(), rs.data()));
-            for (fhe_ct* r : rs) {
-                add_into(base, r);
-                fhe_ct_free(r);
+    } else {  // channel shards consolidate in channel-major order, tau stays the identity
+        for (size_t w4 = 0; w4 < (t + 3) / 4; ++w4) {
+            fhe_ct* acc = nullptr;
+            for (size_t q = 0; q < 4 && 4 * w4 + q < t; ++q) {
+                fhe_ct* src = V[4 * w4 + q];
+                if (!src) continue;
+                if (q == 0) {
+                    acc = src;
+                    continue;
+                }
+                fhe_ct* r = rot1(src, -(int64_t)(q * (s / 4)));
+                fhe_ct_free(src);
+                if (acc) {
+                    add_into(acc, r);
+                    fhe_ct_free(r);
+                } else {
+                    acc = r;
+                }
+            }
+            res.push_back(acc);
+        }
+        for (size_t j = 0; j < (size_t)ch; ++j) tau[j] = (int64_t)j;
+        if (bn > s) {
+            mode = 1;
+        } else {
+            const size_t valid = (size_t)ch * bn;
+            d = valid < s ? (int)(s / valid) : 1;
+            if (d > 1) {
+                dup = (size_t)d;
+                dup_stride = valid;
             }
         }
-        for (size_t u = 0; u < res.size(); ++u) outs[u] = res[u];
-        if (n_out) *n_out = res.size();
-        if (tau_out)
-            for (size_t j = 0; j < (size_t)ch; ++j) tau_out[j] = tau[j];
-        if (rep_out) *rep_out = rep;
-        if (d_out) *d_out = dup;
+    }
+    if (dup > 1) {  // channel duplication: base + sum_e rot_{-e stride}(base), hoisted (pool.cpp:276-289)
+        if (res.size() != 1) fail(FHE_E_INVALID, "duplication applies to a single shard");
+        fhe_ct* base = res[0];
+        std::vector<int64_t> ks;
+        for (size_t e = 1; e < dup; ++e) ks.push_back(-(int64_t)(e * dup_stride));
+        std::vector<fhe_ct*> rs(ks.size());
+        for (size_t e = 0; e < ks.size(); ++e) rs[e] = new_ct(c, base->level, base->scale, base->depth);
+        const fhe_ct* bc = base;
+        okc(c, fhe_rotate_hoisted_batch_into(c, &bc, 1, ks.data(), ks.size(), rs.data()));
+        for (fhe_ct* r : rs) {
+            add_into(base, r);
+            fhe_ct_free(r);
+        }
+    }
+    for (size_t u = 0; u < res.size(); ++u) outs[u] = res[u];
+    if (n_out) *n_out = res.size();
+    if (tau_out)
+        for (size_t j = 0; j < (size_t)ch; ++j) tau_out[j] = tau[j];
+    if (rep_out) *rep_out = rep;
+    if (d_out) *d_out = d;
+    if (mode_out) *mode_out = mode;
+}
+
+// pack()'s duplication of a single image-mode shard (pack.cpp:19-21)
+static int natural_dup(const fhe_ctx* c, int ch, int m) {
+    const size_t s = c->slots(), block = (size_t)m * m;
+    return (block <= s && ch > 0 && (size_t)ch * block < s) ? (int)(s / ((size_t)ch * block)) : 1;
+}
+
+int fhe_downsample(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, const int64_t* tau_in, int rep_in,
+                   int d_in, int window, double output_scale, fhe_ct** outs, size_t* n_out, int64_t* tau_out,
+                   int* rep_out, int* d_out, int* mode_out) {
+    return guard(c, [&] {
+        downsample_impl(c, in, t, ch, m, tau_in, rep_in, d_in, window, output_scale, outs, n_out, tau_out, rep_out,
+                        d_out, mode_out);
     });
 }
 
+int fhe_pool(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, fhe_ct** outs, size_t* n_out,
+             int64_t* tau_out, int* rep_out, int* d_out) {
+    return guard(c, [&] {
+        downsample_impl(c, in, t, ch, m, nullptr, 1, natural_dup(c, ch, m), 1, 1.0, outs, n_out, tau_out, rep_out,
+                        d_out, nullptr);
+    });
+}
+
+int fhe_subsample_stride2(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, fhe_ct** outs,
+                          size_t* n_out, int64_t* tau_out, int* rep_out, int* d_out) {
+    return guard(c, [&] {
+        downsample_impl(c, in, t, ch, m, nullptr, 1, natural_dup(c, ch, m), 0, 1.0, outs, n_out, tau_out, rep_out,
+                        d_out, nullptr);
+    });
+}
 
 // ------------------------------------------- ct x ct and Chebyshev series
 // mul_ct with relinearisation (hybrid key switching of d2 with

@@ -322,14 +322,37 @@ class Context:
 
     def pool(self, shards: Sequence[Ciphertext], c: int, m: int):
         """fhe_pool: 2x2 average pooling; returns (shards, tau, rep, d) like the reference's PackedImage."""
+        return self._downsample(lib().fhe_pool, shards, c, m)
+
+    def subsample_stride2(self, shards: Sequence[Ciphertext], c: int, m: int):
+        """fhe_subsample_stride2 (reference subsample_stride2); returns (shards, tau, rep, d)."""
+        return self._downsample(lib().fhe_subsample_stride2, shards, c, m)
+
+    def _downsample(self, fn, shards, c, m):
         ins = (C.c_void_p * len(shards))(*[x.h for x in shards])
         outs = (C.c_void_p * len(shards))()
         n = C.c_size_t(0)
         tau = np.zeros(c, dtype=np.int64)
         rep, d = C.c_int(0), C.c_int(0)
-        self._check(lib().fhe_pool(self.h, ins, len(shards), c, m, outs, C.byref(n),
-                                   tau.ctypes.data_as(_lib.i64p), C.byref(rep), C.byref(d)))
+        self._check(fn(self.h, ins, len(shards), c, m, outs, C.byref(n), tau.ctypes.data_as(_lib.i64p),
+                       C.byref(rep), C.byref(d)))
         return [Ciphertext(self, outs[i]) for i in range(n.value)], tau, rep.value, d.value
+
+    def downsample(self, shards: Sequence[Ciphertext], c: int, m: int, tau=None, rep: int = 1, d: int = 1,
+                   window: bool = True, output_scale: float = 1.0):
+        """fhe_downsample: pool (window) / stride-2 of any PackedImage; returns (shards, tau, rep, d, mode)."""
+        ins = (C.c_void_p * len(shards))(*[x.h for x in shards])
+        outs = (C.c_void_p * len(shards))()
+        n = C.c_size_t(0)
+        tau_out = np.zeros(c, dtype=np.int64)
+        tin = None if tau is None else np.ascontiguousarray(tau, dtype=np.int64)
+        rep_o, d_o, mode = C.c_int(0), C.c_int(0), C.c_int(0)
+        self._check(lib().fhe_downsample(self.h, ins, len(shards), c, m,
+                                         None if tin is None else tin.ctypes.data_as(_lib.i64p), rep, d,
+                                         int(window), float(output_scale), outs, C.byref(n),
+                                         tau_out.ctypes.data_as(_lib.i64p), C.byref(rep_o), C.byref(d_o),
+                                         C.byref(mode)))
+        return [Ciphertext(self, outs[i]) for i in range(n.value)], tau_out, rep_o.value, d_o.value, mode.value
 
     def gen_relin_key(self):
         self._check(lib().fhe_gen_relin_key(self.h))

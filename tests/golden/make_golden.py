@@ -46,6 +46,19 @@ POOL_CASES = {
     "pool_cfg1_c16m32": (16, 32, 4096, 1042),  # t = 4
     "pool_cfg3_c16m32": (16, 32, 16384, 1043), # cfg3 feature map, t = 1
 }
+# pool / subsample_stride2 over every packing (pool.cpp:238-306): (c, m, s, window, output_scale, seed)
+DS_CASES = {
+    "ds_cfg1_c2m128_pool": (2, 128, 4096, 1, 1.0, 1050),   # channel shards (pc 4, 32 rows) -> 2 image shards
+    "ds_cfg1_c1m256_pool": (1, 256, 4096, 1, 1.0, 1051),   # channel shards (pc 16) -> channel shards (pc 4)
+    "ds_cfg1_c1m128_pool": (1, 128, 4096, 1, 1.0, 1052),   # channel shards -> one full image shard
+    "ds_cfg2_c1m128_pool": (1, 128, 8192, 1, 1.0, 1053),   # channel shards -> image shard duplicated x2
+    "ds_cfg1_c2m32_pool": (2, 32, 4096, 1, 1.0, 1054),     # duplicated input (d 2) -> rep 4, d 8
+    "ds_cfg1_c8m32_pool_sc": (8, 32, 4096, 1, 0.5, 1055),  # output_scale on the vertical masks
+    "ds_cfg1_c4m32_s2": (4, 32, 4096, 0, 1.0, 1056),       # stride-2, one shard
+    "ds_cfg1_c16m32_s2": (16, 32, 4096, 0, 1.0, 1057),     # stride-2, four shards
+    "ds_cfg1_c2m128_s2": (2, 128, 4096, 0, 1.0, 1058),     # stride-2, channel -> image shards
+    "ds_cfg1_c1m256_s2": (1, 256, 4096, 0, 1.0, 1059),     # stride-2, channel -> channel shards
+}
 # linear head: (c, m, s, out_features, seed)
 LIN_CASES = {
     "lin_cfg1_c4m32": (4, 32, 4096, 4, 1030),     # one shard
@@ -152,6 +165,14 @@ def main():
         img, _ = po.make_inputs(c, m, 1, 1, si, 0, 0, use_ref=True)
         slots, meta, tau, ledger = po.ref_pool(c, m, img, s)
         out[f"{name}/params"] = np.array([c, m, s, si], dtype=np.int64)
+        out[f"{name}/slots"] = slots
+        out[f"{name}/meta"] = meta
+        out[f"{name}/tau"] = tau
+        out[f"{name}/ledger"] = ledger
+    for name, (c, m, s, window, osc, si) in DS_CASES.items():
+        img, _ = po.make_inputs(c, m, 1, 1, si, 0, 0, use_ref=True)
+        slots, meta, tau, ledger = po.ref_downsample(c, m, img, s, window, osc)
+        out[f"{name}/params"] = np.array([c, m, s, window, osc, si], dtype=np.float64)
         out[f"{name}/slots"] = slots
         out[f"{name}/meta"] = meta
         out[f"{name}/tau"] = tau

@@ -561,6 +561,62 @@ def test_pool_bit_exact_and_within_tolerance(oracle, golden, p1, name):
         assert np.array_equal(o.residues(), r)
 
 
+DS = ["ds_cfg1_c2m128_pool", "ds_cfg1_c1m256_pool", "ds_cfg1_c1m128_pool", "ds_cfg2_c1m128_pool",
+      "ds_cfg1_c2m32_pool", "ds_cfg1_c8m32_pool_sc", "ds_cfg1_c4m32_s2", "ds_cfg1_c16m32_s2",
+      "ds_cfg1_c2m128_s2", "ds_cfg1_c1m256_s2"]
+
+
+@pytest.mark.parametrize("name", DS)
+def test_downsample_bit_exact_and_within_tolerance(oracle, golden, name):
+    """SURVEY §8(f) 2, pool() / subsample_stride2() over channel shards, duplicated inputs and
+    output scales: residues bit-exact vs the golden model running the same stages
+    (oracle.downsample_restated over ck_lintrans_src / ck_rotate / ck_add), decrypted shards
+    within 1e-6 of the reference's, same packing metadata (tau, rep, d, mode)."""
+    c, m, s, window, osc, si = golden[f"{name}/params"]
+    c, m, s, window, si, osc = int(c), int(m), int(s), int(window), int(si), float(osc)
+    p = pair(oracle, "cfg1" if s == 4096 else "cfg2")
+    assert p.ctx.slots == s
+    img, _ = oracle.make_inputs(c, m, 1, 1, si, 0, 0)
+    block = m * m
+    d_in = s // (block * c) if block <= s and block * c < s else 1
+    chunks = list(np.tile(img, d_in).reshape(-1, s))
+    p.ctx.gen_galois_keys(oracle.downsample_steps(c, m, s, bool(window)))
+    cts = [p.ctx.encrypt(p.ctx.encode(x), ENC_SEED + u) for u, x in enumerate(chunks)]
+    if osc == 1.0 and d_in == 1:
+        fn = p.ctx.pool if window else p.ctx.subsample_stride2
+        outs, tau, rep, d = fn(cts, c, m)
+        mode = int(m * m // 4 > s)
+    else:
+        outs, tau, rep, d, mode = p.ctx.downsample(cts, c, m, d=d_in, window=bool(window), output_scale=osc)
+    meta = golden[f"{name}/meta"]
+    assert (len(outs), rep, d, mode) == (int(meta[5]), int(meta[3]), int(meta[2]), int(meta[4]))
+    assert np.array_equal(tau, golden[f"{name}/tau"].astype(np.int64))
+    for u, o in enumerate(outs):
+        assert o.level == p.top - (3 if window else 2)
+        assert np.abs(p.ctx.decrypt(o) - golden[f"{name}/slots"][u]).max() < TOL
+    ctr = [(p.ck.encrypt(p.ck.encode(x, p.ck.scale, p.top), p.top, ENC_SEED + u), p.top)
+           for u, x in enumerate(chunks)]
+    ref, *_ = oracle.downsample_restated(oracle.CkksOps(p.ck), ctr, c, m, s, bool(window), osc, d_in=d_in)
+    for o, r in zip(outs, ref):
+        assert np.array_equal(o.residues(), r[0])
+
+
+def test_downsample_errors(p1):
+    """the reference's exception texts (pool.cpp:231-306, pack.cpp:54-70)."""
+    from paper_2306_09189_b200 import FheError
+    ct = p1.ctx.encrypt(p1.ctx.encode(rnd(p1.ctx.slots, 3)), ENC_SEED)
+    with pytest.raises(FheError, match="cannot pool a 1x1 channel"):
+        p1.ctx.pool([ct], 4, 1)
+    with pytest.raises(FheError, match="cannot subsample a 1x1 channel"):
+        p1.ctx.subsample_stride2([ct], 4, 1)
+    with pytest.raises(FheError, match="duplicated multi-shard image"):
+        p1.ctx.downsample([ct, ct], 8, 32, d=2)
+    with pytest.raises(FheError, match="metadata mismatch"):
+        p1.ctx.pool([ct], 8, 32)
+    with pytest.raises(FheError, match="dimensions must be powers of two"):
+        p1.ctx.pool([ct], 3, 32)
+
+
 # ------------------------------------------------------------ SURVEY §8(f) 4: ct x ct, Chebyshev
 
 CHEB = ["cheb_cfg3_gelu27_pre", "cheb_cfg3_gelu59_raw", "cheb_cfg3_relu27_raw", "cheb_cfg3_relu16_raw",

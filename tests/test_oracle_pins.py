@@ -241,6 +241,84 @@ def test_pool_restatement_matches_reference(oracle, golden, name):
         assert np.abs(want[0][g * mn * mn:(g + 1) * mn * mn] - pooled[ch].ravel()).max() < 1e-12
 
 
+DS = ["ds_cfg1_c2m128_pool", "ds_cfg1_c1m256_pool", "ds_cfg1_c1m128_pool", "ds_cfg2_c1m128_pool",
+      "ds_cfg1_c2m32_pool", "ds_cfg1_c8m32_pool_sc", "ds_cfg1_c4m32_s2", "ds_cfg1_c16m32_s2",
+      "ds_cfg1_c2m128_s2", "ds_cfg1_c1m256_s2"]
+
+
+def packed(img, c, m, s):
+    """pack(img, s) slot vectors (pack.cpp:7-49): image mode duplicates a small image d times."""
+    block = m * m
+    d = s // (block * c) if block <= s and block * c < s else 1
+    flat = np.tile(img, d)
+    return list(flat.reshape(-1, s)), d
+
+
+@pytest.mark.parametrize("name", DS)
+def test_downsample_restatement_matches_reference(oracle, golden, name):
+    """pool() / subsample_stride2() over channel shards, duplicated inputs and output scales:
+    the rotation-of-mask restatement (what the GPU runs) reproduces the reference's shards
+    (1e-12) and packing metadata, and the result is the average-pooled / subsampled image."""
+    c, m, s, window, osc, si = golden[f"{name}/params"]
+    c, m, s, window, si = int(c), int(m), int(s), int(window), int(si)
+    img, _ = oracle.make_inputs(c, m, 1, 1, si, 0, 0)
+    xs, d_in = packed(img, c, m, s)
+    got, tau, rep, d, mode = oracle.downsample_restated(oracle.NumpyOps, xs, c, m, s, bool(window), float(osc),
+                                                        d_in=d_in)
+    want, meta = golden[f"{name}/slots"], golden[f"{name}/meta"]
+    assert len(got) == want.shape[0] == int(meta[5])
+    assert (rep, d, mode) == (int(meta[3]), int(meta[2]), int(meta[4]))
+    assert np.array_equal(tau, golden[f"{name}/tau"].astype(np.int64))
+    for a, b in zip(got, want):
+        assert np.abs(a - b).max() < 1e-12
+    # logical check on the reference's output: unpack and compare with the numpy pooled image
+    x = img.reshape(c, m, m)
+    if window:
+        want_img = 0.25 * (x[:, 0::2, 0::2] + x[:, 1::2, 0::2] + x[:, 0::2, 1::2] + x[:, 1::2, 1::2])
+    else:
+        want_img = x[:, 0::2, 0::2].copy()
+    want_img *= float(osc)
+    mn = m // 2
+    if mode == 1:  # channel shards: channel-major, rows_per_shard rows each
+        flat = np.concatenate(list(want))
+        assert np.abs(flat[: c * mn * mn] - want_img.ravel()).max() < 1e-12
+    else:
+        bn = mn * mn
+        for ph in range(min(c * rep, s // bn) if len(want) == 1 else c):
+            if ph % rep:
+                continue
+            sh, pos = divmod(ph // rep, s // bn) if len(want) > 1 else (0, ph)
+            ch = int(tau[ph // rep])
+            assert np.abs(want[sh][pos * bn:(pos + 1) * bn] - want_img[ch].ravel()).max() < 1e-12
+
+
+def test_downsample_steps_cover_restatement():
+    """downsample_steps lists every rotation the restatement performs (the Galois key set)."""
+    for c, m, s, w in [(2, 128, 4096, 1), (1, 256, 4096, 0), (4, 32, 4096, 1), (1, 128, 8192, 1)]:
+        used = set()
+
+        class Rec(oracle_mod().NumpyOps):
+            @staticmethod
+            def lintrans(srcs, terms):
+                used.update(a % s for _, a, _ in terms if a % s)
+                return oracle_mod().NumpyOps.lintrans(srcs, terms)
+
+            @staticmethod
+            def rotate(x, k):
+                if k % s:
+                    used.add(k % s)
+                return np.roll(x, -k)
+        img = np.random.default_rng(0).uniform(-1, 1, c * m * m)
+        xs, d_in = packed(img, c, m, s)
+        oracle_mod().downsample_restated(Rec, xs, c, m, s, bool(w), d_in=d_in)
+        assert used <= set(oracle_mod().downsample_steps(c, m, s, bool(w)))
+
+
+def oracle_mod():
+    import pyoracle
+    return pyoracle
+
+
 CHEB = ["cheb_cfg3_gelu27_pre", "cheb_cfg3_gelu59_raw", "cheb_cfg3_relu27_raw", "cheb_cfg3_relu16_raw",
         "cheb_cfg1_gelu7_raw", "cheb_cfg1_identity", "cheb_cfg1_const"]
 
