@@ -184,6 +184,15 @@ void fhe_conv_layer_free(fhe_conv_layer* layer);
  * (v z + b) mod c_out). Runs the fused BSGS schedule. */
 int fhe_conv_layer_create_shards(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
                                  int level, fhe_conv_layer** out);
+/* image-mode layer over ANY PackedImage (conv_image_mode conv.cpp:40-211 as
+ * convolve() reaches it after pooling): t input shards, tau[c_in] (physical
+ * channel position -> logical channel; NULL = identity), rep, d (duplication,
+ * t = 1 only). Channel rotations r rep m^2 (r < c_in for t = 1, else < z), fused
+ * plaintexts from block_channel (pack.hpp:44). Run with fhe_conv2d_shards_into. */
+int fhe_conv_layer_create_packed(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
+                                 int level, size_t t, const int64_t* tau, int rep, int d, fhe_conv_layer** out);
+/* output duplication d of a layer (ImageConv::make_output: n_out z / c_out; rep 1, identity tau) */
+int fhe_conv_layer_output_packing(const fhe_conv_layer* layer, int* d_out);
 /* input / output shard counts of a layer (1 / 1 for single-shard layers) */
 int fhe_conv_layer_shards(const fhe_conv_layer* layer, int* t, int* n_out);
 /* n_images multi-shard convs: in = [n_images][t] ciphertexts at the layer level,
@@ -244,6 +253,13 @@ int fhe_slot_sum_batch(fhe_ctx* ctx, const fhe_ct* const* cts, size_t n, uint64_
  * output features in slots 0..out_features-1, two levels consumed. */
 int fhe_linear(fhe_ctx* ctx, const fhe_ct* const* shards, size_t t, int c, int m, int out_features, const double* w,
                const double* b, fhe_ct** out);
+
+/* linear() / pool_linear() over ANY PackedImage: features[u * slots + i] is the
+ * input feature held by slot i of shard u, -1 for none (the reference's
+ * slot_feature_map, pack.cpp:109-129: non-primary replicas and padding are -1);
+ * w is [out_features][in_features]. */
+int fhe_linear_features(fhe_ctx* ctx, const fhe_ct* const* shards, size_t t, const int64_t* features,
+                        size_t in_features, int out_features, const double* w, const double* b, fhe_ct** out);
 
 /* 2x2 average pooling (reference pool(), pool.cpp:291-297) of
  * the t shards of pack(img, slots) (image mode, t = 1, 2 or a multiple of 4,

@@ -137,6 +137,9 @@ def ref():
                                     C.c_int, C.c_int]
         R.ref_linear.argtypes = [C.c_int, C.c_int, dp, C.c_int, dp, dp, C.c_uint64, dp, u64p]
         R.ref_pool.argtypes = [C.c_int, C.c_int, dp, C.c_uint64, dp, C.c_int, u64p, u64p, u64p]
+        R.ref_write_network.argtypes = [C.c_int, C.c_char_p, C.c_uint64]
+        R.ref_run_network.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_int, C.c_int, dp, dp, C.c_int,
+                                      C.POINTER(C.c_int64), dp, C.POINTER(C.c_int64), u64p, C.c_char_p, C.c_uint64]
         R.ref_downsample.argtypes = [C.c_int, C.c_int, dp, C.c_uint64, C.c_int, C.c_double, dp, C.c_int, u64p, u64p,
                                      u64p]
         R.ref_slot_sum.argtypes = [dp, C.c_uint64, C.c_uint64, dp]
@@ -238,6 +241,34 @@ def ref_downsample(c, m, img, s, window=True, output_scale=1.0, cap=64):
                              _ptr(ledger, u64p))
     assert n > 0, n
     return out[: n * s].reshape(n, s), meta, tau, ledger
+
+
+def ref_write_network(which, directory, side=16):
+    """the reference's test networks (tests/test_net.cpp, tiny_net.hpp) written as JSON + fixtures
+    with the reference's own io.cpp savers."""
+    assert ref().ref_write_network(which, str(directory).encode(), side) == 0
+
+
+def ref_run_network(json_path, input_path, shard_size=0, initial_level=0, auto_boot=-1):
+    """the reference's run_network (net.cpp:112-257) on a JSON network: dict with logits,
+    oracle_logits, per-layer info [level_before, level_after, depth, bootstrapped], errors,
+    ledger totals; raises RuntimeError with the reference's message."""
+    cap = 64
+    lg, ol = np.zeros(cap), np.zeros(cap)
+    info = np.zeros(4 * 32, dtype=np.int64)
+    err = np.zeros(32)
+    meta = np.zeros(2, dtype=np.int64)
+    tot = np.zeros(8, dtype=np.uint64)
+    msg = C.create_string_buffer(512)
+    rc = ref().ref_run_network(str(json_path).encode(), str(input_path).encode(), shard_size, initial_level,
+                               auto_boot, _ptr(lg, dp), _ptr(ol, dp), cap,
+                               info.ctypes.data_as(C.POINTER(C.c_int64)), _ptr(err, dp),
+                               meta.ctypes.data_as(C.POINTER(C.c_int64)), _ptr(tot, u64p), msg, 512)
+    if rc != 0:
+        raise RuntimeError(msg.value.decode())
+    nl, no = int(meta[0]), int(meta[1])
+    return dict(logits=lg[:no].copy(), oracle_logits=ol[:no].copy(), info=info[:4 * nl].reshape(nl, 4).copy(),
+                errors=err[:nl].copy(), totals=tot.copy())
 
 
 def ref_slot_sum(vec, block):

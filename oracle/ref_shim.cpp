@@ -13,6 +13,8 @@
 // (tests/helpers.hpp:13-27: mt19937_64 + uniform_real_distribution), so the
 // golden vectors are exactly what the reference's tests would see.
 #include "shardnn/act.hpp"
+#include "shardnn/io.hpp"
+#include "shardnn/net.hpp"
 #include "shardnn/conv.hpp"
 #include "shardnn/dense.hpp"
 #include "shardnn/pool.hpp"
@@ -20,12 +22,16 @@
 #include "shardnn/pack.hpp"
 #include "shardnn/rot.hpp"
 #include "helpers.hpp"
+#include "tiny_net.hpp"
 
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <iomanip>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -367,6 +373,189 @@ double ref_time_rotations(uint64_t s, int strategy, int n_amounts, int vectors, 
     for (int i = 0; i < threads; ++i) pool.emplace_back(work, i);
     for (auto& th : pool) th.join();
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+
+
+// ------------------------------------------------------------ network runner (net.cpp)
+namespace {
+
+/// The networks of the reference's tests/test_net.cpp, built with its own
+/// helpers: 0 = tiny_network() (tiny_net.hpp), 1 = the stride-2 network
+/// (test_net.cpp:202-235), 2 = the activation-first network (:236-262),
+/// 3 = the channel-sharded network (:263-301; m = side of the input).
+NetworkSpec build_net(int which, ImageTensor& input, std::size_t side) {
+    if (which == 0) {
+        input = tiny_input();
+        return tiny_network();
+    }
+    NetworkSpec spec;
+    spec.shard_size = 256;
+    spec.initial_level = 16;
+    if (which == 1) {
+        std::mt19937_64 rng(2024);
+        LayerSpec conv;
+        conv.type = LayerType::Conv;
+        conv.name = "conv_s2";
+        conv.filter = random_filter(rng, 4, 4, 3);
+        for (double& w : conv.filter.weights) w *= 0.2;
+        conv.bias = random_values(rng, 4, -0.1, 0.1);
+        conv.stride = 2;
+        spec.layers.push_back(conv);
+        LayerSpec act;
+        act.type = LayerType::Gelu;
+        act.name = "gelu";
+        act.degree = 27;
+        act.bound = 10.0;
+        spec.layers.push_back(act);
+        LayerSpec head;
+        head.type = LayerType::PoolLinear;
+        head.name = "head";
+        head.weights = LinearWeights(3, 4);
+        head.weights.w = random_values(rng, 12);
+        head.weights.b = random_values(rng, 3);
+        spec.layers.push_back(head);
+        input = tiny_input();
+    } else if (which == 2) {
+        std::mt19937_64 rng(2025);
+        LayerSpec act;
+        act.type = LayerType::Gelu;
+        act.name = "gelu_first";
+        act.degree = 27;
+        act.bound = 4.0;
+        spec.layers.push_back(act);
+        LayerSpec head;
+        head.type = LayerType::Linear;
+        head.name = "fc";
+        head.weights = LinearWeights(5, 4 * 64);
+        head.weights.w = random_values(rng, head.weights.w.size());
+        head.weights.b = random_values(rng, 5);
+        spec.layers.push_back(head);
+        input = tiny_input();
+    } else {
+        std::mt19937_64 rng(2026);
+        spec.shard_size = 128;
+        LayerSpec conv;
+        conv.type = LayerType::Conv;
+        conv.name = "conv";
+        conv.filter = random_filter(rng, 2, 2, 3);
+        for (double& w : conv.filter.weights) w *= 0.3;
+        conv.bias = random_values(rng, 2, -0.1, 0.1);
+        spec.layers.push_back(conv);
+        LayerSpec pool_layer;
+        pool_layer.type = LayerType::Pool;
+        pool_layer.name = "pool";
+        spec.layers.push_back(pool_layer);
+        LayerSpec act;
+        act.type = LayerType::Gelu;
+        act.name = "gelu";
+        act.degree = 27;
+        act.bound = 10.0;
+        spec.layers.push_back(act);
+        LayerSpec head;
+        head.type = LayerType::PoolLinear;
+        head.name = "head";
+        head.weights = LinearWeights(4, 2);
+        head.weights.w = random_values(rng, 8);
+        head.weights.b = random_values(rng, 4);
+        spec.layers.push_back(head);
+        std::mt19937_64 irng(77);
+        input = random_tensor(irng, 2, side);
+    }
+    return spec;
+}
+
+void json_array(std::ofstream& f, const std::vector<double>& v) {
+    f << "[";
+    for (std::size_t i = 0; i < v.size(); ++i) f << v[i] << (i + 1 < v.size() ? ", " : "");
+    f << "]";
+}
+
+}  // namespace
+
+/// Writes network `which` as a JSON description + fixture files (the
+/// reference's own save_filter / save_linear / save_tensor formats, io.cpp)
+/// into `dir`: net.json, <layer>.filt, <layer>.lin, input.tensor.
+int ref_write_network(int which, const char* dir, uint64_t side) {
+    try {
+        ImageTensor input(1, 1);
+        NetworkSpec spec = build_net(which, input, side);
+        const std::string d(dir);
+        std::ofstream f(d + "/net.json");
+        f << std::setprecision(17);
+        f << "{\n  \"shard_size\": " << spec.shard_size << ",\n  \"initial_level\": " << spec.initial_level
+          << ",\n  \"seed\": " << spec.seed << ",\n  \"noise\": {\"enabled\": false},\n"
+          << "  \"bootstrap\": {\"auto\": true},\n  \"layers\": [\n";
+        for (std::size_t i = 0; i < spec.layers.size(); ++i) {
+            const LayerSpec& l = spec.layers[i];
+            f << "    {\"type\": \"" << layer_type_name(l.type) << "\", \"name\": \"" << l.name << "\"";
+            if (l.type == LayerType::Conv) {
+                save_filter(d + "/" + l.name + ".filt", l.filter, l.bias);
+                f << ", \"filter\": \"" << l.name << ".filt\"";
+                if (l.stride != 1) f << ", \"stride\": " << l.stride;
+                if (l.bn) {
+                    f << ", \"bn_scale\": ";
+                    json_array(f, l.bn->scale);
+                    f << ", \"bn_bias\": ";
+                    json_array(f, l.bn->bias);
+                }
+            } else if (l.type == LayerType::Gelu) {
+                f << ", \"degree\": " << l.degree << ", \"bound\": " << l.bound;
+            } else if (l.type == LayerType::Linear || l.type == LayerType::PoolLinear) {
+                save_linear(d + "/" + l.name + ".lin", l.weights);
+                f << ", \"weights\": \"" << l.name << ".lin\"";
+            }
+            f << "}" << (i + 1 < spec.layers.size() ? "," : "") << "\n";
+        }
+        f << "  ]\n}\n";
+        save_tensor(d + "/input.tensor", input);
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+/// run_network (net.cpp:112-257) of a JSON network on a tensor fixture, with
+/// the shard size / initial level overridden when > 0. info[i] = [level_before,
+/// level_after, depth_consumed, bootstrapped] per layer, err[i] = its max_abs_err;
+/// meta = [n_layers, n_logits]; logits / oracle_logits (cap entries). Returns 0,
+/// or -2 with the exception text in `msg`.
+int ref_run_network(const char* json, const char* input_path, uint64_t shard_size, int initial_level,
+                    int auto_boot, double* logits, double* oracle_logits, int cap, int64_t* info, double* err,
+                    int64_t* meta, uint64_t* totals, char* msg, uint64_t msg_cap) {
+    try {
+        NetworkSpec spec = load_network(json);
+        if (shard_size) spec.shard_size = shard_size;
+        if (initial_level > 0) spec.initial_level = initial_level;
+        if (auto_boot >= 0) spec.bootstrap.auto_insert = auto_boot != 0;
+        ImageTensor input = load_tensor(input_path);
+        RunReport r = run_network(spec, input);
+        meta[0] = (int64_t)r.layers.size();
+        meta[1] = (int64_t)r.logits.size();
+        for (std::size_t i = 0; i < r.layers.size(); ++i) {
+            info[4 * i + 0] = r.layers[i].level_before;
+            info[4 * i + 1] = r.layers[i].level_after;
+            info[4 * i + 2] = r.layers[i].depth_consumed;
+            info[4 * i + 3] = r.layers[i].bootstrapped;
+            err[i] = r.layers[i].max_abs_err;
+        }
+        for (std::size_t o = 0; o < r.logits.size() && (int)o < cap; ++o) {
+            logits[o] = r.logits[o];
+            oracle_logits[o] = r.oracle_logits[o];
+        }
+        totals[0] = r.totals.rotations;
+        totals[1] = r.totals.hoisted_rotations;
+        totals[2] = r.totals.hoist_groups;
+        totals[3] = r.totals.ct_pt_mults;
+        totals[4] = r.totals.ct_ct_mults;
+        totals[5] = r.totals.adds;
+        totals[6] = r.totals.bootstraps;
+        totals[7] = (uint64_t)r.totals.max_depth_consumed;
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(msg, msg_cap, "%s", e.what());
+        return -2;
+    }
 }
 
 }  // extern "C"

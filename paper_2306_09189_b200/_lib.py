@@ -103,6 +103,11 @@ SIGNATURES = [
     ("fhe_downsample", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, C.c_int, C.c_int, i64p, C.c_int, C.c_int,
                                  C.c_int, C.c_double, vpp, C.POINTER(C.c_size_t), i64p, C.POINTER(C.c_int),
                                  C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("fhe_linear_features", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, i64p, C.c_size_t, C.c_int, dp, dp,
+                                      vpp]),
+    ("fhe_conv_layer_create_packed", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_int, C.c_size_t,
+                                               i64p, C.c_int, C.c_int, vpp]),
+    ("fhe_conv_layer_output_packing", C.c_int, [vp, C.POINTER(C.c_int)]),
     ("fhe_linear", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, C.c_int, C.c_int, C.c_int, dp, dp, vpp]),
     ("fhe_conv2d_shards_into", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, vp, C.POINTER(C.c_void_p)]),
     ("fhe_conv2d_batch_host_async", C.c_int, [vp, u64p, C.c_size_t, C.c_double, vp, C.c_int, C.c_size_t, u64p]),

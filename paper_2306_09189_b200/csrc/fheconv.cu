@@ -236,6 +236,10 @@ struct fhe_conv_layer {
     bool cs = false;  // channel-shard mode (m^2 > slots): pc = m^2 / slots shards per channel
     int pc = 1;
     int t = 1, z = 0, n_out = 1, nb_ms = 0;
+    // input packing (PackedImage::tau / rep, pack.hpp:44): channel rotations r < rmax
+    // by r rep m^2; block g of the input holds channel tau[(g / rep) % c_in]
+    int rep = 1, rmax = 0;
+    std::vector<int64_t> tau;
     std::vector<uint8_t> ms_nonempty;  // [n_out][kappa][nb_ms]
     uint64_t* d_pts_ms = nullptr;
 };
@@ -562,13 +566,16 @@ bool fused_plain(int c_in, int c_out, int m, int kappa, size_t s, const double* 
 // multi-shard image mode (reference conv.cpp:37-85 with d = 1, rep = 1, tau = identity):
 //   in_channel(u, r, b) = u z + (b + r) % z,  out_channel(v, b) = (v z + b) % c_out
 bool fused_plain_ms(int c_out, int m, int kappa, size_t s, const double* w, int v, int u, int r, long kk, long ll,
-                    std::vector<double>& plain) {
+                    std::vector<double>& plain, const std::vector<int64_t>* tau = nullptr, int rep = 1) {
+    // ImageConv::fused_plain (conv.cpp:69-85): in_channel(u, r, b) =
+    // block_channel(u z + (b + r rep) mod z), out_channel(v, b) = (v z + b) mod c_out
     const size_t block = (size_t)m * m, z = s / block;
     const long h = kappa / 2;
     plain.assign(s, 0.0);
     bool any = false;
     for (size_t b = 0; b < z; ++b) {
-        const size_t in_ch = (size_t)u * z + (b + (size_t)r) % z;
+        const size_t g = (size_t)u * z + (b + (size_t)r * (size_t)rep) % z;
+        const size_t in_ch = tau ? (size_t)(*tau)[(g / (size_t)rep) % tau->size()] : g;
         const size_t out_ch = ((size_t)v * z + b) % (size_t)c_out;
         const double wt =
             w[((in_ch * c_out + out_ch) * kappa + (size_t)(kk + h)) * kappa + (size_t)(ll + h)] * 1.0;
@@ -1287,6 +1294,10 @@ void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
             double keyed = 0, pts = 0;
             auto flush = [&] {
                 if (!f.nb) return;
+                for (int q = 0; q < f.nb; ++q)
+                    if (f.key[q]) c->ledger.hoisted_rotations += (uint64_t)B;
+                c->ledger.ct_pt_mults += (uint64_t)B * (uint64_t)pts;
+                c->ledger.adds += (uint64_t)B * (uint64_t)pts;
                 c->timed("bsgs_fused",
                          c->rows(keyed * 2.0 * dn * ne + pts * ne + B * (T * (double)dn * ne + 2.0 * nr + 4.0 * ng * ne)),
                          [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
@@ -1299,9 +1310,9 @@ void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
                     if (ly->ms_nonempty[((size_t)v * kap + g0 + g) * nb + b]) mask |= 1u << g;
                 if (!mask) continue;
                 if (f.nb == kMaxFused) flush();
-                const int u = b / (ly->z * kap), r = (b / kap) % ly->z;
+                const int u = b / (ly->rmax * kap), r = (b / kap) % ly->rmax;
                 const long ll = b % kap - h;
-                const uint32_t gal = c->galois_of(c->reduce_amount((int64_t)r * block + ll));
+                const uint32_t gal = c->galois_of(c->reduce_amount((int64_t)r * ly->rep * block + ll));
                 f.galois[f.nb] = gal;
                 f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
                 f.gmask[f.nb] = mask;
@@ -1338,6 +1349,7 @@ void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
         c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, outs[i]->depth);
     }
     c->ledger.hoist_groups += (uint64_t)B * T;
+    c->ledger.rotations += (uint64_t)B * NO * giants.size();
     c->release(md);
     c->release(Y);
     c->release(buf);
@@ -1415,6 +1427,9 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
                         }
                     }
                 if (!f.nb) continue;
+                c->ledger.hoisted_rotations += (uint64_t)B * (uint64_t)keyed;
+                c->ledger.ct_pt_mults += (uint64_t)B * (uint64_t)pts;
+                c->ledger.adds += (uint64_t)B * (uint64_t)pts;
                 c->timed("bsgs_fused",
                          c->rows(keyed * 2.0 * dn * ne + pts * ne + B * (3.0 * C_ * dn * ne + 2.0 * nr + 4.0 * ng * ne)),
                          [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
@@ -1432,6 +1447,8 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
     }
     const size_t otw = (size_t)2 * level * N;
     uint64_t* md = c->alloc((size_t)B * NOUT * otw);
+    c->ledger.hoist_groups += (uint64_t)B * NSH;
+    c->ledger.rotations += (uint64_t)B * NOUT * giants.size();
     giants_finish(c, Y, ys, B * NOUT, level, giants, gamt, id, md);
     for (int i = 0; i < B * NOUT; ++i) {
         ck(cudaMemcpyAsync(outs[i]->d, md + (size_t)i * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
@@ -2523,6 +2540,9 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
     delete ly;
 }
 
+static fhe_conv_layer* create_packed_layer(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights,
+                                           int level, int T, const int64_t* tau, int rep, int d);
+
 int fhe_conv_layer_create_shards(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights, int level,
                                  fhe_conv_layer** out) {
     return guard(c, [&] {
@@ -2578,48 +2598,89 @@ int fhe_conv_layer_create_shards(fhe_ctx* c, int c_in, int c_out, int m, int kap
         }
         if ((size_t)c_in * block < s)
             fail(FHE_E_INVALID, "multi-shard convolution needs c_in m^2 >= slots (no duplication)");
-        if (kappa / 2 >= m) fail(FHE_E_INVALID, "kernel reach exceeds channel size");
-        if (level < 1 || level >= c->L) fail(FHE_E_INVALID, "level out of range");
-        const int z = (int)(s / block), T = (int)((size_t)c_in * block / s);
-        const int NO = c_out <= z ? 1 : c_out / z;
-        if (T > 64) fail(FHE_E_INVALID, "too many input shards");
-        fhe_conv_layer* ly = new fhe_conv_layer();
-        ly->ctx = c;
-        ly->c_in = c_in;
-        ly->c_out = c_out;
-        ly->m = m;
-        ly->kappa = kappa;
-        ly->level = level;
-        ly->nk = kappa * kappa;
-        ly->d_pts = nullptr;
-        ly->weights.assign(weights, weights + (size_t)c_in * c_out * kappa * kappa);
-        ly->ms = true;
-        ly->t = T;
-        ly->z = z;
-        ly->n_out = NO;
-        ly->nb_ms = T * z * kappa;
-        const int ne = c->ne_at(level), nb = ly->nb_ms;
-        const size_t extw = (size_t)ne * c->N;
-        const long h = kappa / 2;
-        ly->ms_nonempty.assign((size_t)NO * kappa * nb, 0);
-        ck(cudaMalloc(&ly->d_pts_ms, (size_t)NO * kappa * nb * extw * 8), "cudaMalloc");
-        const double pscale = (double)c->primes[level];
-        std::vector<double> plain, rot(s);
-        for (int v = 0; v < NO; ++v)
-            for (int gi = 0; gi < kappa; ++gi)
-                for (int b = 0; b < nb; ++b) {
-                    const int u = b / (z * kappa), r = (b / kappa) % z;
-                    const long ll = b % kappa - h, kk = gi - h;
-                    if (!fused_plain_ms(c_out, m, kappa, s, weights, v, u, r, kk, ll, plain)) continue;
-                    ly->ms_nonempty[((size_t)v * kappa + gi) * nb + b] = 1;
-                    const uint64_t g = c->reduce_amount(kk * m);
-                    for (size_t j = 0; j < s; ++j) rot[j] = plain[(j + s - g) % s];  // rot_{-kk m}
-                    encode_rows(c, rot.data(), s, level, pscale, ne,
-                                ly->d_pts_ms + (((size_t)v * kappa + gi) * nb + b) * extw);
-                }
-        ck(cudaStreamSynchronize(c->st), "sync");
-        *out = ly;
+        *out = create_packed_layer(c, c_in, c_out, m, kappa, weights, level, (int)((size_t)c_in * block / s), nullptr,
+                                   1, 1);
     });
+}
+
+// image-mode layer over an arbitrary PackedImage (conv_image_mode, conv.cpp:40-211):
+// t shards, tau, rep, d (d > 1 only for one shard)
+static fhe_conv_layer* create_packed_layer(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights,
+                                           int level, int T, const int64_t* tau, int rep, int d) {
+    const size_t s = c->slots(), block = (size_t)m * m;
+    if (kappa % 2 == 0) fail(FHE_E_INVALID, "kernel size must be odd");
+    if (c_out <= 0 || (c_out & (c_out - 1))) fail(FHE_E_INVALID, "output channel count must be a power of two");
+    if (c_in <= 0 || (c_in & (c_in - 1))) fail(FHE_E_INVALID, "channel count must be a power of two");
+    if (m <= 0 || (m & (m - 1)) || block > s) fail(FHE_E_INVALID, "image-mode convolution requires image shards");
+    if (T < 1 || rep < 1 || d < 1) fail(FHE_E_INVALID, "metadata mismatch");
+    if (T >= 2 && d != 1) fail(FHE_E_INVALID, "metadata mismatch: duplicated multi-shard image");
+    if ((size_t)c_in * block * (size_t)d != (size_t)T * s) fail(FHE_E_INVALID, "metadata mismatch: shard count");
+    if (kappa / 2 >= m) fail(FHE_E_INVALID, "kernel reach exceeds channel size");
+    if (level < 1 || level >= c->L) fail(FHE_E_INVALID, "level out of range");
+    const int z = (int)(s / block);
+    const int NO = c_out <= z ? 1 : c_out / z;
+    if (T > 64) fail(FHE_E_INVALID, "too many input shards");
+    std::vector<int64_t> tv((size_t)c_in);
+    for (int j = 0; j < c_in; ++j) tv[(size_t)j] = tau ? tau[j] : j;
+    {
+        std::vector<int> seen((size_t)c_in, 0);
+        for (int64_t x : tv)
+            if (x < 0 || x >= c_in || seen[(size_t)x]++) fail(FHE_E_INVALID, "tau is not a permutation");
+    }
+    fhe_conv_layer* ly = new fhe_conv_layer();
+    ly->ctx = c;
+    ly->c_in = c_in;
+    ly->c_out = c_out;
+    ly->m = m;
+    ly->kappa = kappa;
+    ly->level = level;
+    ly->nk = kappa * kappa;
+    ly->d_pts = nullptr;
+    ly->weights.assign(weights, weights + (size_t)c_in * c_out * kappa * kappa);
+    ly->ms = true;
+    ly->t = T;
+    ly->z = z;
+    ly->n_out = NO;
+    ly->rep = rep;
+    ly->tau = tv;
+    ly->rmax = T == 1 ? c_in : z;  // ImageConv::r_max (conv.cpp:57)
+    ly->nb_ms = T * ly->rmax * kappa;
+    const int ne = c->ne_at(level), nb = ly->nb_ms;
+    const size_t extw = (size_t)ne * c->N;
+    const long h = kappa / 2;
+    ly->ms_nonempty.assign((size_t)NO * kappa * nb, 0);
+    ck(cudaMalloc(&ly->d_pts_ms, (size_t)NO * kappa * nb * extw * 8), "cudaMalloc");
+    const double pscale = (double)c->primes[level];
+    std::vector<double> plain, rot(s);
+    for (int v = 0; v < NO; ++v)
+        for (int gi = 0; gi < kappa; ++gi)
+            for (int b = 0; b < nb; ++b) {
+                const int u = b / (ly->rmax * kappa), r = (b / kappa) % ly->rmax;
+                const long ll = b % kappa - h, kk = gi - h;
+                if (!fused_plain_ms(c_out, m, kappa, s, weights, v, u, r, kk, ll, plain, &ly->tau, rep)) continue;
+                ly->ms_nonempty[((size_t)v * kappa + gi) * nb + b] = 1;
+                const uint64_t g = c->reduce_amount(kk * m);
+                for (size_t j = 0; j < s; ++j) rot[j] = plain[(j + s - g) % s];  // rot_{-kk m}
+                encode_rows(c, rot.data(), s, level, pscale, ne,
+                            ly->d_pts_ms + (((size_t)v * kappa + gi) * nb + b) * extw);
+            }
+    ck(cudaStreamSynchronize(c->st), "sync");
+    return ly;
+}
+
+int fhe_conv_layer_create_packed(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights, int level,
+                                 size_t t, const int64_t* tau, int rep, int d, fhe_conv_layer** out) {
+    return guard(c, [&] {
+        if (!out) fail(FHE_E_INVALID, "null output");
+        *out = create_packed_layer(c, c_in, c_out, m, kappa, weights, level, (int)t, tau, rep, d);
+    });
+}
+
+int fhe_conv_layer_output_packing(const fhe_conv_layer* ly, int* d_out) {
+    // ImageConv::make_output (conv.cpp:97-106): d = n_out z / c_out, rep 1, identity tau
+    if (!ly) return FHE_E_INVALID;
+    if (d_out) *d_out = (ly->ms && !ly->cs) ? std::max(1, ly->n_out * ly->z / ly->c_out) : 1;
+    return FHE_OK;
 }
 
 int fhe_conv_layer_shards(const fhe_conv_layer* ly, int* t, int* n_out) {
@@ -2657,9 +2718,9 @@ int fhe_conv_layer_steps(const fhe_conv_layer* ly, int approach, int64_t* steps,
             if (kk) st.insert(kk * ly->m);
         approach = -1;
     } else if (ly->ms) {  // multi-shard layers run the fused schedule: r m^2 + ll (r < z) and kk m
-        for (int r = 0; r < ly->z; ++r)
+        for (int r = 0; r < ly->rmax; ++r)
             for (long ll = -h; ll <= h; ++ll)
-                if (r || ll) st.insert((int64_t)r * block + ll);
+                if (r || ll) st.insert((int64_t)r * ly->rep * block + ll);
         for (long kk = -h; kk <= h; ++kk)
             if (kk) st.insert(kk * ly->m);
         approach = -1;
@@ -2906,97 +2967,116 @@ int fhe_slot_sum_batch(fhe_ctx* c, const fhe_ct* const* cts, size_t n, uint64_t 
     });
 }
 
+// masked_feature_dot (dense.cpp:34-67) over a slot -> feature map
+// (feat[u * s + i] = feature held by slot i of shard u, -1 = none)
+static void linear_impl(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const int64_t* featmap, size_t nin,
+                        int out_features, const double* w, const double* b, fhe_ct** out) {
+    const size_t s = c->slots();
+    if (t == 0 || !shards || !w || !b || !out) fail(FHE_E_INVALID, "null argument");
+    if (out_features <= 0 || (size_t)out_features > s) fail(FHE_E_INVALID, "out_features exceeds the shard size");
+    const int level = shards[0]->level;
+    if (level < 2) fail(FHE_E_RUNTIME, "depth exhausted");
+    auto feat = [&](size_t u, size_t i) -> long { return (long)featmap[u * s + i]; };
+    // products W_o . x_u for every output feature and shard, one level
+    std::vector<fhe_ct*> prods;
+    std::vector<int> prod_o;
+    std::vector<double> wt(s);
+    const double ql = (double)c->primes[level];
+    for (int o = 0; o < out_features; ++o) {
+        bool started = false;
+        for (size_t u = 0; u < t; ++u) {
+            bool any = false;
+            for (size_t i = 0; i < s; ++i) {
+                const long f = feat(u, i);
+                wt[i] = f < 0 ? 0.0 : w[(size_t)o * nin + (size_t)f];
+                any = any || wt[i] != 0.0;
+            }
+            if (!any && started) continue;
+            fhe_pt* pt = nullptr;
+            fhe_ct *pr = nullptr, *rs = nullptr;
+            okc(c, fhe_encode(c, wt.data(), s, level, ql, 0, &pt));
+            okc(c, fhe_mul_plain(c, shards[u], pt, &pr));
+            okc(c, fhe_rescale(c, pr, &rs));
+            fhe_pt_free(pt);
+            fhe_ct_free(pr);
+            prods.push_back(rs);
+            prod_o.push_back(o);
+            started = true;
+        }
+    }
+    std::vector<fhe_ct*> sums(prods.size());
+    okc(c, fhe_slot_sum_batch(c, prods.data(), prods.size(), s, sums.data()));
+    for (fhe_ct* x : prods) fhe_ct_free(x);
+    // per output: sum over shards, select slot o (second level), accumulate
+    fhe_ct* acc = nullptr;
+    std::vector<double> sel(s, 0.0);
+    size_t k = 0;
+    for (int o = 0; o < out_features; ++o) {
+        fhe_ct* total = sums[k++];
+        while (k < sums.size() && prod_o[k] == o) {
+            fhe_ct* nt = nullptr;
+            okc(c, fhe_add(c, total, sums[k], &nt));
+            fhe_ct_free(total);
+            fhe_ct_free(sums[k]);
+            total = nt;
+            ++k;
+        }
+        std::fill(sel.begin(), sel.end(), 0.0);
+        sel[(size_t)o] = 1.0;
+        fhe_pt* pt = nullptr;
+        fhe_ct *pr = nullptr, *rs = nullptr;
+        okc(c, fhe_encode(c, sel.data(), s, total->level, (double)c->primes[total->level], 0, &pt));
+        okc(c, fhe_mul_plain(c, total, pt, &pr));
+        okc(c, fhe_rescale(c, pr, &rs));
+        fhe_pt_free(pt);
+        fhe_ct_free(pr);
+        fhe_ct_free(total);
+        if (!acc) {
+            acc = rs;
+        } else {
+            fhe_ct* na = nullptr;
+            okc(c, fhe_add(c, acc, rs, &na));
+            fhe_ct_free(acc);
+            fhe_ct_free(rs);
+            acc = na;
+        }
+    }
+    std::vector<double> bias(s, 0.0);
+    for (int o = 0; o < out_features; ++o) bias[(size_t)o] = b[o];
+    fhe_pt* bp = nullptr;
+    okc(c, fhe_encode(c, bias.data(), s, acc->level, acc->scale, 0, &bp));
+    fhe_ct* res = nullptr;
+    okc(c, fhe_add_plain(c, acc, bp, &res));
+    fhe_pt_free(bp);
+    fhe_ct_free(acc);
+    *out = res;
+}
+
 int fhe_linear(fhe_ctx* c, const fhe_ct* const* shards, size_t t, int ch, int m, int out_features, const double* w,
                const double* b, fhe_ct** out) {
     return guard(c, [&] {
         const size_t s = c->slots(), block = (size_t)m * m, nin = (size_t)ch * block;
-        if (t == 0 || !shards || !w || !b || !out) fail(FHE_E_INVALID, "null argument");
-        if (out_features <= 0 || (size_t)out_features > s) fail(FHE_E_INVALID, "out_features exceeds the shard size");
         // slot -> feature map (reference slot_feature_map pack.cpp:109-129, identity tau, rep 1):
         // image mode: slot i of shard u holds feature u s + i below c m^2 (the primary
         // replica when the image is duplicated); channel mode: channel-major rows.
         const bool channel_mode = block > s;
         const size_t expect_t = channel_mode ? nin / s : std::max<size_t>(1, nin / s);
         if (t != expect_t) fail(FHE_E_INVALID, "shard count does not match the packed feature count");
-        const int level = shards[0]->level;
-        if (level < 2) fail(FHE_E_RUNTIME, "depth exhausted");
-        auto feat = [&](size_t u, size_t i) -> long {
-            const size_t f = u * s + i;
-            return f < nin ? (long)f : -1;
-        };
-        // products W_o . x_u for every output feature and shard, one level
-        std::vector<fhe_ct*> prods;
-        std::vector<int> prod_o;
-        std::vector<double> wt(s);
-        const double ql = (double)c->primes[level];
-        for (int o = 0; o < out_features; ++o) {
-            bool started = false;
-            for (size_t u = 0; u < t; ++u) {
-                bool any = false;
-                for (size_t i = 0; i < s; ++i) {
-                    const long f = feat(u, i);
-                    wt[i] = f < 0 ? 0.0 : w[(size_t)o * nin + (size_t)f];
-                    any = any || wt[i] != 0.0;
-                }
-                if (!any && started) continue;
-                fhe_pt* pt = nullptr;
-                fhe_ct *pr = nullptr, *rs = nullptr;
-                okc(c, fhe_encode(c, wt.data(), s, level, ql, 0, &pt));
-                okc(c, fhe_mul_plain(c, shards[u], pt, &pr));
-                okc(c, fhe_rescale(c, pr, &rs));
-                fhe_pt_free(pt);
-                fhe_ct_free(pr);
-                prods.push_back(rs);
-                prod_o.push_back(o);
-                started = true;
-            }
-        }
-        std::vector<fhe_ct*> sums(prods.size());
-        okc(c, fhe_slot_sum_batch(c, prods.data(), prods.size(), s, sums.data()));
-        for (fhe_ct* x : prods) fhe_ct_free(x);
-        // per output: sum over shards, select slot o (second level), accumulate
-        fhe_ct* acc = nullptr;
-        std::vector<double> sel(s, 0.0);
-        size_t k = 0;
-        for (int o = 0; o < out_features; ++o) {
-            fhe_ct* total = sums[k++];
-            while (k < sums.size() && prod_o[k] == o) {
-                fhe_ct* nt = nullptr;
-                okc(c, fhe_add(c, total, sums[k], &nt));
-                fhe_ct_free(total);
-                fhe_ct_free(sums[k]);
-                total = nt;
-                ++k;
-            }
-            std::fill(sel.begin(), sel.end(), 0.0);
-            sel[(size_t)o] = 1.0;
-            fhe_pt* pt = nullptr;
-            fhe_ct *pr = nullptr, *rs = nullptr;
-            okc(c, fhe_encode(c, sel.data(), s, total->level, (double)c->primes[total->level], 0, &pt));
-            okc(c, fhe_mul_plain(c, total, pt, &pr));
-            okc(c, fhe_rescale(c, pr, &rs));
-            fhe_pt_free(pt);
-            fhe_ct_free(pr);
-            fhe_ct_free(total);
-            if (!acc) {
-                acc = rs;
-            } else {
-                fhe_ct* na = nullptr;
-                okc(c, fhe_add(c, acc, rs, &na));
-                fhe_ct_free(acc);
-                fhe_ct_free(rs);
-                acc = na;
-            }
-        }
-        std::vector<double> bias(s, 0.0);
-        for (int o = 0; o < out_features; ++o) bias[(size_t)o] = b[o];
-        fhe_pt* bp = nullptr;
-        okc(c, fhe_encode(c, bias.data(), s, acc->level, acc->scale, 0, &bp));
-        fhe_ct* res = nullptr;
-        okc(c, fhe_add_plain(c, acc, bp, &res));
-        fhe_pt_free(bp);
-        fhe_ct_free(acc);
-        *out = res;
+        std::vector<int64_t> fm(t * s);
+        for (size_t f = 0; f < t * s; ++f) fm[f] = f < nin ? (int64_t)f : -1;
+        linear_impl(c, shards, t, fm.data(), nin, out_features, w, b, out);
+    });
+}
+
+int fhe_linear_features(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const int64_t* features,
+                        size_t in_features, int out_features, const double* w, const double* b, fhe_ct** out) {
+    return guard(c, [&] {
+        if (!features) fail(FHE_E_INVALID, "null argument");
+        const size_t s = c->slots();
+        for (size_t f = 0; f < t * s; ++f)
+            if (features[f] >= (int64_t)in_features || features[f] < -1)
+                fail(FHE_E_INVALID, "in_features does not match the packed feature count");
+        linear_impl(c, shards, t, features, in_features, out_features, w, b, out);
     });
 }
 

@@ -381,6 +381,34 @@ class Context:
         return self._new(lib().fhe_linear, ins, len(shards), c, m, len(b), w.ctypes.data_as(_lib.dp),
                          b.ctypes.data_as(_lib.dp))
 
+    def linear_features(self, shards: Sequence[Ciphertext], features, w, b) -> Ciphertext:
+        """fhe_linear_features: W x + b with an explicit slot -> feature map ([t][slots], -1 = none)."""
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        fm = np.ascontiguousarray(features, dtype=np.int64)
+        assert fm.shape == (len(shards), self.slots)
+        ins = (C.c_void_p * len(shards))(*[x.h for x in shards])
+        return self._new(lib().fhe_linear_features, ins, len(shards), fm.ctypes.data_as(_lib.i64p),
+                         w.size // len(b), len(b), w.ctypes.data_as(_lib.dp), b.ctypes.data_as(_lib.dp))
+
+    def conv_layer_packed(self, c_in: int, c_out: int, m: int, kappa: int, weights, t: int = 1, tau=None,
+                          rep: int = 1, d: int = 1, level: int | None = None) -> ConvLayer:
+        """fhe_conv_layer_create_packed: image-mode layer over any PackedImage (tau, rep, d)."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        assert w.size == c_in * c_out * kappa * kappa
+        level = self.max_level if level is None else level
+        tv = None if tau is None else np.ascontiguousarray(tau, dtype=np.int64)
+        out = C.c_void_p()
+        self._check(lib().fhe_conv_layer_create_packed(self.h, c_in, c_out, m, kappa, w.ctypes.data_as(_lib.dp),
+                                                       level, t, None if tv is None else tv.ctypes.data_as(_lib.i64p),
+                                                       rep, d, C.byref(out)))
+        ly = ConvLayer(self, out.value, c_in, c_out, m, kappa, level)
+        tt, no, dd = C.c_int(0), C.c_int(0), C.c_int(0)
+        self._check(lib().fhe_conv_layer_shards(ly.h, C.byref(tt), C.byref(no)))
+        self._check(lib().fhe_conv_layer_output_packing(ly.h, C.byref(dd)))
+        ly.t, ly.n_out, ly.d_out = tt.value, no.value, dd.value
+        return ly
+
     def conv2d(self, ct: Ciphertext, layer: ConvLayer, approach: int = 2) -> Ciphertext:
         return self._new(lib().fhe_conv2d, ct.h, layer.h, approach)
 
