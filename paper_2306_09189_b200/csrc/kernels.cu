@@ -6,6 +6,10 @@
 // 2^b blocks to aligned 2^b blocks and the permuted gathers below stay
 // inside 256-byte segments.
 #include "kernels.cuh"
+
+#ifndef FHE_FUSED_SPLITLD  // fused kernel: digit / c0 pairs as two 8-byte loads in output order
+#define FHE_FUSED_SPLITLD 1
+#endif
 #include "cdt_table.h"
 
 namespace fhe {
@@ -798,19 +802,33 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
                 // load (thread-linear slot, conflict-free), then select the order
                 const int swp = (int)(pk & 1u);
                 Acc3 s0a{0, 0, 0, 0}, s0b{0, 0, 0, 0}, s1a{0, 0, 0, 0}, s1b{0, 0, 0, 0};
+#if FHE_FUSED_SPLITLD
+                // the pair in output order as two 8-byte loads (no per-word selects)
+                const uint64_t* dga = reinterpret_cast<const uint64_t*>(s_dig + so) + swp;
+                const uint64_t* dgb = reinterpret_cast<const uint64_t*>(s_dig + so) + (swp ^ 1);
+#endif
 #pragma unroll
                 for (int j = 0; j < DN; ++j) {
                     const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
+#if FHE_FUSED_SPLITLD
+                    const uint64_t da = dga[2 * j * P], db = dgb[2 * j * P];
+#else
                     const ulonglong2 dv = s_dig[so + j * P];  // one conflict-free 16-byte load
                     const uint64_t da = swp ? dv.y : dv.x, db = swp ? dv.x : dv.y;
+#endif
                     mac3(s0a, da, k0.x);
                     mac3(s0b, db, k0.y);
                     mac3(s1a, da, k1.x);
                     mac3(s1b, db, k1.y);
                 }
                 if (qrow) {
+#if FHE_FUSED_SPLITLD
+                    const uint64_t ca = reinterpret_cast<const uint64_t*>(s_c0 + so)[swp];
+                    const uint64_t cb = reinterpret_cast<const uint64_t*>(s_c0 + so)[swp ^ 1];
+#else
                     const ulonglong2 cv = s_c0[so];
                     const uint64_t ca = swp ? cv.y : cv.x, cb = swp ? cv.x : cv.y;
+#endif
                     if (DN < 8) {  // P c0 as one more product term (s1 holds 8 terms)
                         mac3(s0a, ca, pm);
                         mac3(s0b, cb, pm);

@@ -16,6 +16,10 @@
 #define FHE_HD inline
 #endif
 
+#ifndef FHE_MACSMALL_V2
+#define FHE_MACSMALL_V2 1
+#endif
+
 namespace fhe {
 
 struct Prime {
@@ -125,6 +129,29 @@ __device__ __forceinline__ void mac3(Acc3& A, uint64_t a, uint64_t b) {
 // four 32x32->64 products and two 128-bit additions
 __device__ __forceinline__ void mac_small(U128& acc, uint64_t a, uint64_t b) {
     const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+#if FHE_MACSMALL_V2
+    // product = p00 + (mid << 32) + (p11 << 64) with mid = a0 b1 + a1 b0 + hi32(p00) < 2^63:
+    // four wide multiply-adds (p11 straight into the high word) and one 4-word carry chain
+    asm("{\n\t.reg .u64 p00, mid, t;\n\t.reg .u32 p0, p1, m0, m1, l0, l1, h0, h1;\n\t"
+        "mul.wide.u32 p00, %2, %4;\n\t"
+        "mov.b64 {p0, p1}, p00;\n\t"
+        "cvt.u64.u32 t, p1;\n\t"
+        "mad.wide.u32 mid, %2, %5, t;\n\t"
+        "mad.wide.u32 mid, %3, %4, mid;\n\t"
+        "mad.wide.u32 %1, %3, %5, %1;\n\t"
+        "mov.b64 {m0, m1}, mid;\n\t"
+        "mov.b64 {l0, l1}, %0;\n\t"
+        "mov.b64 {h0, h1}, %1;\n\t"
+        "add.cc.u32 l0, l0, p0;\n\t"
+        "addc.cc.u32 l1, l1, m0;\n\t"
+        "addc.cc.u32 h0, h0, m1;\n\t"
+        "addc.u32 h1, h1, 0;\n\t"
+        "mov.b64 %0, {l0, l1};\n\t"
+        "mov.b64 %1, {h0, h1};\n\t}"
+        : "+l"(acc.lo), "+l"(acc.hi)
+        : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+    return;
+#endif
     asm("{\n\t.reg .u64 p00, p11, mid, ml, mh;\n\t"
         "mul.wide.u32 p00, %2, %4;\n\t"
         "mul.wide.u32 mid, %2, %5;\n\t"

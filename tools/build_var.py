@@ -1,0 +1,16 @@
+"""Build a variant libfheconv.so with extra -D flags into scratch/var/<name>/ (kernels.cu only differs)."""
+import os, subprocess, sys
+sys.path.insert(0, ".")
+from paper_2306_09189_b200 import build as B
+name, defs = sys.argv[1], sys.argv[2:]
+out = os.path.join("tools", "var", name); os.makedirs(out, exist_ok=True)
+objs = []
+for src in B.SOURCES:
+    obj = os.path.join(out, src.replace(".cu", ".o"))
+    if src == "kernels.cu":
+        subprocess.run([B._nvcc(), *B.NVCC_FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", obj], check=True)
+    else:
+        obj = os.path.join(B.CSRC, src.replace(".cu", ".o"))
+    objs.append(obj)
+subprocess.run([B._nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", os.path.join(out, "libfheconv.so"), *objs], check=True)
+print(out)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU verification pass: gpu tests, bench line, launch list of the same bench command.
+# One GPU verification pass: gpu tests, smoke, bench line (+ reference arm), launch list of the timed region.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
@@ -8,3 +8,5 @@ echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-cfg2 > gpurun_out/ncu_launch.log 2>&1
