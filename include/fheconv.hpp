@@ -86,6 +86,13 @@ private:
     std::unique_ptr<fhe_conv_layer, Del> h_;
 };
 
+// PackedImage (reference pack.hpp) whose shards are ciphertexts
+struct Packed {
+    std::vector<Ciphertext> shards;
+    int m = 0, c = 0, rep = 1, d = 1, mode = 0;  // mode 0 image shards, 1 channel shards
+    std::vector<int64_t> tau;                    // physical channel position -> logical channel
+};
+
 class Engine {
 public:
     explicit Engine(const Params& p) {
@@ -177,6 +184,72 @@ public:
         return Ciphertext(o);
     }
 
+    // Engine::mul_ct (emu.cpp:69-80): relinearised and rescaled (gen_relin_key() first)
+    void gen_relin_key() { check(fhe_gen_relin_key(raw())); }
+    Ciphertext mul_ct(const Ciphertext& a, const Ciphertext& b) { return binary(fhe_mul, a, b); }
+    // Engine::add_scalar (emu.cpp:113-119)
+    Ciphertext add_scalar(const Ciphertext& v, double k) { return unary(fhe_add_scalar, v, k); }
+    // eval_chebyshev (act.cpp:151-162): sum_k coeffs[k] T_k(x / bound)
+    Ciphertext eval_chebyshev(const Ciphertext& x, const std::vector<double>& coeffs, double bound,
+                              bool prescaled) {
+        return unary(fhe_eval_chebyshev, x, coeffs.data(), coeffs.size(), bound, (int)prescaled);
+    }
+    // slot_sum (dense.cpp:23-30)
+    Ciphertext slot_sum(const Ciphertext& v, size_t block) {
+        const fhe_ct* in = v.get();
+        fhe_ct* o = nullptr;
+        check(fhe_slot_sum_batch(raw(), &in, 1, block, &o));
+        return Ciphertext(o);
+    }
+    // pool / subsample_stride2 (pool.cpp:291-306) of any PackedImage
+    Packed pool(const Packed& p, double output_scale = 1.0) { return downsample(p, true, output_scale); }
+    Packed subsample_stride2(const Packed& p, double output_scale = 1.0) { return downsample(p, false, output_scale); }
+    // convolve (conv.cpp:364-371) of an image-mode PackedImage (any tau / rep / duplication)
+    Packed convolve(const Packed& p, int c_out, int kappa, const std::vector<double>& weights) {
+        if (p.shards.empty()) throw std::invalid_argument("packed image has no shards");
+        fhe_conv_layer* l = nullptr;
+        check(fhe_conv_layer_create_packed(raw(), p.c, c_out, p.m, kappa, weights.data(), p.shards[0].level(),
+                                           p.shards.size(), p.tau.empty() ? nullptr : p.tau.data(), p.rep, p.d, &l));
+        ConvLayer layer(l);
+        {  // Galois keys of the layer's rotations (existing keys are kept)
+            std::vector<int64_t> st(4096);
+            size_t ns = 0;
+            check(fhe_conv_layer_steps(l, 0, st.data(), st.size(), &ns));
+            check(fhe_gen_galois_keys(raw(), st.data(), ns));
+        }
+        int t = 0, n_out = 0, d_out = 1;
+        fhe_conv_layer_shards(l, &t, &n_out);
+        fhe_conv_layer_output_packing(l, &d_out);
+        std::vector<const fhe_ct*> in;
+        for (const auto& s : p.shards) in.push_back(s.get());
+        std::vector<fhe_ct*> outs((size_t)n_out);
+        for (auto& o : outs) {  // output handles at level - 1 (contents overwritten)
+            fhe_pt* z = nullptr;
+            const double zero = 0.0;
+            check(fhe_encode(raw(), &zero, 1, p.shards[0].level() - 1, scale_, 0, &z));
+            Plaintext zp(z);
+            check(fhe_encrypt(raw(), z, 1, &o));
+        }
+        check(fhe_conv2d_shards_into(raw(), in.data(), 1, l, outs.data()));
+        Packed r;
+        for (fhe_ct* o : outs) r.shards.emplace_back(o);
+        r.m = p.m;
+        r.c = c_out;
+        r.d = d_out;
+        for (int j = 0; j < c_out; ++j) r.tau.push_back(j);
+        return r;
+    }
+    // linear (dense.cpp:71-75) over a slot -> feature map (pack.cpp:109-129)
+    Ciphertext linear(const Packed& p, const std::vector<int64_t>& features, size_t in_features, int out_features,
+                      const std::vector<double>& w, const std::vector<double>& b) {
+        std::vector<const fhe_ct*> in;
+        for (const auto& s : p.shards) in.push_back(s.get());
+        fhe_ct* o = nullptr;
+        check(fhe_linear_features(raw(), in.data(), in.size(), features.data(), in_features, out_features, w.data(),
+                                  b.data(), &o));
+        return Ciphertext(o);
+    }
+
     fhe_ledger ledger() const {
         fhe_ledger l{};
         fhe_ledger_get(raw(), &l);
@@ -184,6 +257,20 @@ public:
     }
 
 private:
+    Packed downsample(const Packed& p, bool window, double output_scale) {
+        std::vector<const fhe_ct*> in;
+        for (const auto& s : p.shards) in.push_back(s.get());
+        std::vector<fhe_ct*> outs(in.size() ? in.size() : 1, nullptr);
+        Packed r;
+        r.tau.assign((size_t)p.c, 0);
+        size_t n = 0;
+        check(fhe_downsample(raw(), in.data(), in.size(), p.c, p.m, p.tau.empty() ? nullptr : p.tau.data(), p.rep, p.d,
+                             (int)window, output_scale, outs.data(), &n, r.tau.data(), &r.rep, &r.d, &r.mode));
+        for (size_t u = 0; u < n; ++u) r.shards.emplace_back(outs[u]);
+        r.m = p.m / 2;
+        r.c = p.c;
+        return r;
+    }
     struct Del {
         void operator()(fhe_ctx* p) const { fhe_ctx_destroy(p); }
     };

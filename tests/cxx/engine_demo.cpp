@@ -56,6 +56,49 @@ int main() {
         } catch (const std::invalid_argument& e) {
             threw = std::string(e.what()) == "empty rotation batch";
         }
+        // pool (pool.cpp:291-297) of the input, then a 1x1 conv on the pooled packing (rep 4,
+        // duplicated), then slot_sum (dense.cpp:23-30) — the reference's operator chain (cfg1: 4 levels)
+        {
+            std::vector<int64_t> st = {1, m, m + 1};
+            for (int i = 1; i < m / 2; ++i) st.push_back(i);
+            for (int j = 1; j < m / 2; ++j) st.push_back(3 * j * m / 2);
+            const int bn = (m / 2) * (m / 2);
+            for (int q = 1; q < 4; ++q) st.push_back(-q * bn);
+            for (int e = 1; e < 4096; e *= 2) st.push_back(e);
+            eng.gen_galois_keys(st);
+            fheconv::Packed p;
+            p.shards.push_back(eng.encode_encrypt(img, 9001));
+            p.m = m;
+            p.c = c;
+            p.tau = {0, 1, 2, 3};
+            fheconv::Packed pooled = eng.pool(p);
+            if (pooled.rep != 4 || pooled.d != 4 || pooled.shards.size() != 1) return 4;
+            auto y = eng.decrypt(pooled.shards[0]);
+            const int mn = m / 2;
+            for (int g = 0; g < c; ++g)  // block (g * rep) holds channel tau[g]
+                for (int i = 0; i < mn; ++i)
+                    for (int j = 0; j < mn; ++j) {
+                        const int ch = (int)pooled.tau[g];
+                        const double want = 0.25 * (img[(ch * m + 2 * i) * m + 2 * j] + img[(ch * m + 2 * i + 1) * m + 2 * j] +
+                                                    img[(ch * m + 2 * i) * m + 2 * j + 1] +
+                                                    img[(ch * m + 2 * i + 1) * m + 2 * j + 1]);
+                        worst = std::fmax(worst, std::fabs(y[(size_t)(g * pooled.rep) * mn * mn + i * mn + j] - want));
+                    }
+            std::vector<double> w1(c * c, 0.0);  // 1x1 conv: identity on the channels
+            for (int f = 0; f < c; ++f) w1[f * c + f] = 1.0;
+            fheconv::Packed conv2 = eng.convolve(pooled, c, 1, w1);
+            auto z = eng.decrypt(conv2.shards[0]);
+            for (int g = 0; g < c; ++g)
+                for (int i = 0; i < mn * mn; ++i) {
+                    const int ch = (int)pooled.tau[g];
+                    // output block b holds channel b % c: compare channel ch at block ch
+                    worst = std::fmax(worst, std::fabs(z[(size_t)ch * mn * mn + i] - y[(size_t)(g * pooled.rep) * mn * mn + i]));
+                }
+            auto ssum = eng.decrypt(eng.slot_sum(conv2.shards[0], 4096));
+            double tot = 0;
+            for (double v : z) tot += v;
+            worst = std::fmax(worst, std::fabs(ssum[0] - tot) / 4096.0);
+        }
         std::printf("engine_demo max|err| %.3g empty-batch-throws %d\n", worst, (int)threw);
         return (worst < 1e-6 && threw) ? 0 : 1;
     } catch (const std::exception& e) {
