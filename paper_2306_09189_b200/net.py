@@ -373,11 +373,13 @@ def mirror_network(spec: NetworkSpec, x: ImageTensor):
 
 
 def run_network(ctx: Context, spec: NetworkSpec, x: ImageTensor, enc_seed: int = 9000,
-                check_layers: bool = True) -> RunReport:
+                check_layers: bool = True, cache: Optional[dict] = None) -> RunReport:
     """run_network (net.cpp:112-257) on ciphertexts. The context must hold a
     secret key (ctx.keygen); Galois and relinearisation keys are generated on
     demand. check_layers decrypts every intermediate map to report its error
-    against the mirror (the reference always does; the timed path skips it)."""
+    against the mirror (the reference always does; the timed path skips it). `cache`
+    (a dict owned by the caller) keeps the encoded conv layers between runs of the
+    same network, the serving case: layer plaintexts are encoded once."""
     if not spec.layers:
         raise ValueError("network has no layers")
     s = ctx.slots
@@ -403,7 +405,7 @@ def run_network(ctx: Context, spec: NetworkSpec, x: ImageTensor, enc_seed: int =
             k, bias = ly.filter, ly.bias
             if ly.bn_scale is not None:
                 k, bias = fold_bn(k, bias, ly.bn_scale, ly.bn_bias)
-            p = _conv(ctx, keys, p, k, bias, fold[i])
+            p = _conv(ctx, keys, p, k, bias, fold[i], cache, i)
             if ly.stride == 2:
                 p = _downsample(ctx, keys, p, False, 1.0)
         elif ly.type == "pool":
@@ -455,7 +457,7 @@ def run_network(ctx: Context, spec: NetworkSpec, x: ImageTensor, enc_seed: int =
 
 
 def _conv(ctx: Context, keys: _Keys, p: PackedCiphertexts, k: FilterTensor, bias: np.ndarray,
-          scale: float) -> PackedCiphertexts:
+          scale: float, cache: Optional[dict] = None, idx: int = -1) -> PackedCiphertexts:
     """convolve (conv.cpp:364-371) with the folded output scale and the bias (conv.cpp:87-94, :344)"""
     s = ctx.slots
     if k.c_in != p.c:
@@ -464,16 +466,24 @@ def _conv(ctx: Context, keys: _Keys, p: PackedCiphertexts, k: FilterTensor, bias
         raise ValueError("bias size does not match output channels")
     w = k.weights * scale
     lv = p.min_level()
+    ck = (idx, p.mode, len(p.shards), tuple(int(v) for v in p.tau), p.rep, p.d, lv, scale)
+    layer = cache.get(ck) if cache is not None else None
     if p.mode == 1:
-        layer = ctx.conv_layer_shards(k.c_in, k.c_out, p.m, k.kappa, w, level=lv)
+        if layer is None:
+            layer = ctx.conv_layer_shards(k.c_in, k.c_out, p.m, k.kappa, w, level=lv)
+        if cache is not None:
+            cache[ck] = layer
         keys.need(layer.steps())
         outs = ctx.conv2d_shards(p.shards, layer)
         pc = p.m * p.m // s
         if bias.size:
             outs = [ctx.add_scalar(o, bias[u // pc] * scale) for u, o in enumerate(outs)]
         return PackedCiphertexts(outs, p.m, k.c_out, np.arange(k.c_out), 1, 1, 1)
-    layer = ctx.conv_layer_packed(k.c_in, k.c_out, p.m, k.kappa, w, t=len(p.shards), tau=p.tau, rep=p.rep, d=p.d,
-                                  level=lv)
+    if layer is None:
+        layer = ctx.conv_layer_packed(k.c_in, k.c_out, p.m, k.kappa, w, t=len(p.shards), tau=p.tau, rep=p.rep,
+                                      d=p.d, level=lv)
+    if cache is not None:
+        cache[ck] = layer
     keys.need(layer.steps())
     outs = ctx.conv2d_shards(p.shards, layer)
     if bias.size:
