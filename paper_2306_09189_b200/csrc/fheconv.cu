@@ -294,14 +294,14 @@ void modup(fhe_ctx* c, const uint64_t* c1, int level, uint64_t* digits) { modup_
 
 // out[p] = ModDown(acc[p]) (+ sigma_g(add_src) on poly 0)
 void moddown_strided(fhe_ctx* c, const uint64_t* acc, size_t acc_stride, int level, int npoly, uint64_t* out,
-                     const uint64_t* add_src, uint32_t g) {
+                     const uint64_t* add_src, uint32_t g, uint64_t* const* outp = nullptr) {
     const int nr = level + 1;
     uint64_t* pc = c->alloc((size_t)npoly * c->K * c->N);
     uint64_t* conv = c->alloc((size_t)npoly * nr * c->N);
     c->timed("moddown", c->rows(2.0 * npoly * c->K), [&] { gather_special(c->dc, pc, acc, acc_stride, level, npoly, c->st); });
     c->timed("ntt", c->rows(2.0 * npoly * c->K), [&] { ntt_inverse(c->dc, pc, npoly * c->K, RowMap{c->K, -1, c->L, 0}, c->st); });
     c->timed("ntt_moddown", c->rows((double)npoly * (c->K + 2 * nr) + (add_src ? nr : 0)),
-             [&] { ntt_moddown(c->dc, conv, pc, acc, acc_stride, out, c->d_md, level, npoly, add_src, g, c->st); });
+             [&] { ntt_moddown(c->dc, conv, pc, acc, acc_stride, out, c->d_md, level, npoly, add_src, g, c->st, outp); });
     c->release(pc);
     c->release(conv);
     c->ledger.moddowns += npoly;
@@ -2285,12 +2285,14 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
         const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
         const size_t KK = keyed.size();
         const size_t SC = std::max<size_t>(1, std::min<size_t>(n, 16));  // sources per chunk
-        uint64_t *buf = nullptr, *dig = nullptr, *XT = nullptr, *md = nullptr;
+        uint64_t *buf = nullptr, *dig = nullptr, *XT = nullptr;
+        uint64_t** outp = nullptr;  // device table of the keyed outputs' residue buffers (ModDown writes there)
+        std::vector<uint64_t*> hostp;
         if (KK) {
             buf = c->alloc(SC * ctw);
             dig = c->alloc(SC * dw);
             XT = c->alloc(SC * KK * 2 * extw);
-            md = c->alloc(SC * KK * ctw);
+            outp = (uint64_t**)c->alloc(SC * KK);
         }
         for (size_t s0 = 0; s0 < n; s0 += SC) {
             const size_t sn = std::min(SC, n - s0);
@@ -2320,8 +2322,9 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
                              [&] { ks_batch(c->dc, kb, 0, c->d_md, level, dn, c->st); });
                 }
                 c->ledger.key_switches += sn * KK;
-                moddown(c, XT, level, (int)(2 * sn * KK), md, nullptr, 1);
             }
+            // outputs first (the keyed ones receive the ModDown directly, no staging copy)
+            hostp.assign(sn * KK, nullptr);
             for (size_t s = 0; s < sn; ++s) {
                 size_t kt = 0;
                 for (size_t j = 0; j < k; ++j) {
@@ -2330,18 +2333,26 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
                     fhe_ct* o = into ? outs[(s0 + s) * k + j] : new_ct(c, level, cts[s0 + s]->scale, cts[s0 + s]->depth);
                     if (into) {
                         if (!o || o->level != level) fail(FHE_E_INVALID, "output ciphertext level mismatch");
+                        if (o == cts[s0 + s]) fail(FHE_E_INVALID, "output ciphertext aliases an input");
                         o->scale = cts[s0 + s]->scale;
                         o->depth = cts[s0 + s]->depth;
                     }
-                    const uint64_t* src = a == 0 ? cts[s0 + s]->d : md + (s * KK + kt++) * ctw;
-                    ck(cudaMemcpyAsync(o->d, src, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+                    if (a == 0)
+                        ck(cudaMemcpyAsync(o->d, cts[s0 + s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+                    else
+                        hostp[s * KK + kt++] = o->d;
                     outs[(s0 + s) * k + j] = o;
                 }
+            }
+            if (KK) {
+                ck(cudaMemcpyAsync(outp, hostp.data(), hostp.size() * sizeof(uint64_t*), cudaMemcpyHostToDevice, c->st),
+                   "memcpy");
+                moddown_strided(c, XT, (size_t)ne * N, level, (int)(2 * sn * KK), nullptr, nullptr, 1, outp);
             }
             c->ledger.hoist_groups += sn;
             c->ledger.hoisted_rotations += sn * k;
         }
-        c->release(md);
+        c->release(outp);
         c->release(XT);
         c->release(dig);
         c->release(buf);

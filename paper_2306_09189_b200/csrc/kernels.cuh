@@ -103,6 +103,7 @@ struct NttFuse {
     const uint64_t* acc;    // poly pp at acc + pp * acc_stride, [ne][N] each
     size_t acc_stride;
     uint64_t* out;          // [npoly][level+1][N]
+    uint64_t* const* outp;  // optional: poly pp written to outp[pp / 2] + (pp % 2) [level+1][N] (ciphertexts)
     const uint64_t* add_src;
     uint32_t galois;
     // fused ModDown+rescale: output multiplier (P q_l)^-1 per row instead of P^-1
@@ -132,7 +133,7 @@ void moddown_coef(const DevCtx& c, uint64_t* out, const uint64_t* y, const ModDo
 // out[p] = (acc[p] - NTT(FastBConv_P->Q(pcoef[p]))) P^-1 (+ sigma_g(add_src) on poly 0)
 void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, size_t acc_stride,
                  uint64_t* out, const ModDownTable* md, int level, int npoly, const uint64_t* add_src,
-                 uint32_t galois, cudaStream_t st);
+                 uint32_t galois, cudaStream_t st, uint64_t* const* outp = nullptr);
 
 void reduce_signed_rows(const DevCtx& c, const int64_t* coef, uint64_t* out, int nrows, const RowMap& rm,
                         cudaStream_t st);

@@ -305,7 +305,9 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
             const int nr = rm.level + 1, ne = nr + c.K;
             (void)ne;
             const uint64_t* acc = fz.acc + (size_t)pp * fz.acc_stride + (size_t)u * c.N + (size_t)blk0 * B;
-            uint64_t* out = fz.out + ((size_t)pp * nr + u) * c.N + (size_t)blk0 * B;
+            uint64_t* out = (fz.outp ? fz.outp[pp >> 1] + ((size_t)(pp & 1) * nr + u) * c.N
+                                     : fz.out + ((size_t)pp * nr + u) * c.N) +
+                            (size_t)blk0 * B;
             const uint64_t pi = fz.outmul ? fz.outmul[u] : fz.md->pinvq[u];
             const uint64_t pis = fz.outmul ? fz.outmul_sh[u] : fz.md->pinvq_sh[u];
             const bool add = fz.add_src && pp == 0;
@@ -681,9 +683,10 @@ void ntt_modup_coef(const DevCtx& c, uint64_t* digits, const uint64_t* coef, int
 
 void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, size_t acc_stride,
                  uint64_t* out, const ModDownTable* md, int level, int npoly, const uint64_t* add_src,
-                 uint32_t galois, cudaStream_t st) {
+                 uint32_t galois, cudaStream_t st, uint64_t* const* outp) {
     const int nr = level + 1;
     NttFuse fz{};
+    fz.outp = outp;
     fz.pc = pcoef;
     fz.md = md;
     fz.acc = acc;
