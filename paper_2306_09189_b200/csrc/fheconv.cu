@@ -3109,6 +3109,18 @@ int fhe_linear_features(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const
 static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int ch, int m, const int64_t* tau_in,
                             int rep_in, int d_in, int window, double oscale, fhe_ct** outs, size_t* n_out,
                             int64_t* tau_out, int* rep_out, int* d_out, int* mode_out) {
+    // every intermediate ciphertext is tracked so that an exception (e.g. a missing
+    // Galois key) frees them; outputs are released from the tracker at the end
+    struct Tracker {
+        std::set<fhe_ct*> s;
+        fhe_ct* add(fhe_ct* x) { return s.insert(x), x; }
+        void drop(fhe_ct* x) {
+            if (x && s.erase(x)) fhe_ct_free(x);
+        }
+        ~Tracker() {
+            for (fhe_ct* x : s) fhe_ct_free(x);
+        }
+    } tr;
     const size_t s = c->slots();
     if (t == 0 || !in) fail(FHE_E_INVALID, "packed image has no shards");
     if (m < 2) fail(FHE_E_INVALID, window ? "cannot pool a 1x1 channel" : "cannot subsample a 1x1 channel");
@@ -3139,7 +3151,7 @@ static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int c
     const std::string geo = std::to_string(m) + "/" + std::to_string(s);
     auto fresh = [&](const std::vector<const fhe_ct*>& src) {
         std::vector<fhe_ct*> o(src.size());
-        for (size_t u = 0; u < src.size(); ++u) o[u] = new_ct(c, src[u]->level - 1, src[u]->scale, src[u]->depth + 1);
+        for (size_t u = 0; u < src.size(); ++u) o[u] = tr.add(new_ct(c, src[u]->level - 1, src[u]->scale, src[u]->depth + 1));
         return o;
     };
     auto count_rot = [&](const std::vector<int64_t>& am, size_t times) {
@@ -3156,7 +3168,7 @@ static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int c
     };
     auto free_all = [&](std::vector<fhe_ct*>& v) {
         for (fhe_ct* x : v)
-            if (x) fhe_ct_free(x);
+            if (x) tr.drop(x);
         v.clear();
     };
     // ---- window stage
@@ -3264,7 +3276,7 @@ static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int c
     for (size_t k = 0; k < live.size(); ++k) V[live[k]] = Vl[k];
     // ---- consolidation (pool.cpp:167-273)
     auto rot1 = [&](const fhe_ct* a, int64_t k) {
-        fhe_ct* o = new_ct(c, a->level, a->scale, a->depth);
+        fhe_ct* o = tr.add(new_ct(c, a->level, a->scale, a->depth));
         okc(c, fhe_rotate_hoisted_batch_into(c, &a, 1, &k, 1, &o));
         return o;
     };
@@ -3289,8 +3301,8 @@ static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int c
         } else if (t == 2) {
             fhe_ct* r = rot1(V[1], -2 * (int64_t)bn);
             add_into(V[0], r);
-            fhe_ct_free(r);
-            fhe_ct_free(V[1]);
+            tr.drop(r);
+            tr.drop(V[1]);
             res.push_back(V[0]);
             for (size_t j = 0; j < (size_t)ch; ++j) tau[j] = tau0[(j % 2) * z + j / 2];
             rep = 2;
@@ -3304,8 +3316,8 @@ static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int c
                 for (size_t q = 1; q < 4; ++q) {
                     fhe_ct* r = rot1(V[4 * w4 + q], -(int64_t)(q * bn));
                     add_into(V[4 * w4], r);
-                    fhe_ct_free(r);
-                    fhe_ct_free(V[4 * w4 + q]);
+                    tr.drop(r);
+                    tr.drop(V[4 * w4 + q]);
                 }
                 res.push_back(V[4 * w4]);
                 for (size_t g = 0; g < blocks_out; ++g) tau[w4 * blocks_out + g] = tau0[(4 * w4 + g % 4) * z + g / 4];
@@ -3322,10 +3334,10 @@ static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int c
                     continue;
                 }
                 fhe_ct* r = rot1(src, -(int64_t)(q * (s / 4)));
-                fhe_ct_free(src);
+                tr.drop(src);
                 if (acc) {
                     add_into(acc, r);
-                    fhe_ct_free(r);
+                    tr.drop(r);
                 } else {
                     acc = r;
                 }
@@ -3350,15 +3362,18 @@ static void downsample_impl(fhe_ctx* c, const fhe_ct* const* in, size_t t, int c
         std::vector<int64_t> ks;
         for (size_t e = 1; e < dup; ++e) ks.push_back(-(int64_t)(e * dup_stride));
         std::vector<fhe_ct*> rs(ks.size());
-        for (size_t e = 0; e < ks.size(); ++e) rs[e] = new_ct(c, base->level, base->scale, base->depth);
+        for (size_t e = 0; e < ks.size(); ++e) rs[e] = tr.add(new_ct(c, base->level, base->scale, base->depth));
         const fhe_ct* bc = base;
         okc(c, fhe_rotate_hoisted_batch_into(c, &bc, 1, ks.data(), ks.size(), rs.data()));
         for (fhe_ct* r : rs) {
             add_into(base, r);
-            fhe_ct_free(r);
+            tr.drop(r);
         }
     }
-    for (size_t u = 0; u < res.size(); ++u) outs[u] = res[u];
+    for (size_t u = 0; u < res.size(); ++u) {
+        tr.s.erase(res[u]);
+        outs[u] = res[u];
+    }
     if (n_out) *n_out = res.size();
     if (tau_out)
         for (size_t j = 0; j < (size_t)ch; ++j) tau_out[j] = tau[j];

@@ -720,3 +720,16 @@ def test_chebyshev_insufficient_level(oracle, golden):
     ct = p.ctx.encrypt(p.ctx.encode(np.full(p.ctx.slots, 0.1), level=3), ENC_SEED)
     with pytest.raises(FheError, match=bytes(golden["cheb_level_error"]).decode()):
         p.ctx.eval_chebyshev(ct, golden["cheb_cfg3_gelu27_pre/coeffs"], 10.0, True)
+
+
+def test_downsample_missing_key_is_an_error_and_leaks_nothing():
+    """a pool without its Galois keys fails with FHE_E_NOKEY; the intermediate ciphertexts are
+    freed (the context's device pool returns to its level), and the context stays usable."""
+    from paper_2306_09189_b200 import CONFIGS, Context, FheError
+    ctx = Context(**CONFIGS["cfg1"])
+    ctx.keygen(7)
+    ct = ctx.encrypt(ctx.encode(rnd(ctx.slots, 4)), ENC_SEED)
+    with pytest.raises(FheError, match="key"):
+        ctx.pool([ct], 4, 32)
+    ctx.gen_galois_keys([1])
+    assert np.abs(ctx.decrypt(ctx.rotate(ct, 1)) - np.roll(ctx.decrypt(ct), -1)).max() < 1e-6
