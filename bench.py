@@ -233,6 +233,15 @@ def run_ours(args, rank, world, local_rank):
     ctx.prof_enable(False)
     prof = {cl: ctx.prof_get_bytes(cl) for cl in KERNEL_CLASSES}
 
+    # ---- the same classes in the step's regime: the batch of B, CUDA events per launch (graphs off)
+    ctx.prof_reset()
+    ctx.prof_enable(True)
+    kbp = 3
+    for _ in range(kbp):
+        ctx.conv2d_batch_into(cts, layer, approach, outs)
+    ctx.prof_enable(False)
+    prof_b = {cl: ctx.prof_get_bytes(cl) for cl in KERNEL_CLASSES}
+
     def timed_convs(ap, steps, warmup):
         for _ in range(warmup):
             ctx.conv2d_into(ct, layer, ap, out)
@@ -377,6 +386,7 @@ def run_ours(args, rank, world, local_rank):
                      "note": KERNEL_NOTES.get(dom, "") +
                      ("; NTT-class kernels are integer-pipe bound (see kernels[].frac_hbm and profiles/)"
                       if dom.startswith("ntt") else "")},
+        "roofline_batched": roofline_batched(prof_b, kbp * B, peak),
         "keyswitch_roofline": {"kernels": ks_cls,
                                "achieved_gbs": round(ks_bytes / (ks_ms / 1e3) / 1e9, 1) if ks_ms else None,
                                "frac": round(ks_bytes / (ks_ms / 1e3) / 1e9 / peak, 4) if ks_ms else None},
@@ -404,6 +414,26 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.destroy_process_group()
     return line
+
+
+def roofline_batched(prof_b, n_convs, peak):
+    """the dominant kernel in the step's own regime (batch of B ciphertexts per launch): algorithmic
+    bytes / launch time against the HBM peak, and the integer-issue view the ncu capture gives
+    (profiles/ncu_r01_bsgs_fused_b16_summary.txt): batched, the fused kernel shares every key and
+    plaintext byte across the batch and is bound by 64-bit integer multiplies, not by HBM."""
+    tot = sum(v[0] for v in prof_b.values())
+    if not tot:
+        return None
+    dom = max(prof_b, key=lambda c: prof_b[c][0])
+    ms, n, by = prof_b[dom]
+    gbs = by / (ms / 1e3) / 1e9
+    return {"bound": "int-issue", "kernel": dom, "avg_launch_ms": round(ms / n, 4),
+            "algorithmic_bytes_per_launch": round(by / n), "achieved_gbs": round(gbs, 1),
+            "frac_hbm": round(gbs / peak, 4), "share_of_step": round(ms / tot, 3),
+            "ms_per_conv": round(ms / n_convs, 4),
+            "ncu_issue_utilisation": 0.472, "ncu_fmaheavy_busy": 0.65,
+            "note": "batched launches (graphs off, CUDA events per launch) right after the timed region; "
+                    "the ncu figures are from profiles/ncu_r01_bsgs_fused_b16_summary.txt (same kernel, batch 16)"}
 
 
 def other_configs(world, device):
