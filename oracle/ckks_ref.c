@@ -1121,9 +1121,19 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
  * giant steps as in conv_bsgs. cts = [t][2][level+1][N], outs = [n_out][2][level][N]. */
 int ck_conv_shards(const ck_ctx* ck, const uint64_t* cts, int t, int level, int c, int m, int kappa, int c_out,
                    const double* filt, uint64_t* outs, double* out_scale) {
+    return ck_conv_packed(ck, cts, t, level, c, m, kappa, c_out, filt, NULL, 1, 1, outs, out_scale);
+}
+
+/* image-mode conv over a PackedImage (tau, rep, duplication d; conv_image_mode
+ * conv.cpp:40-211): babies r rep m^2 + ll of input shard u (r < c for one shard,
+ * < z otherwise), giants kk m, the fused BSGS of ck_conv_shards. */
+int ck_conv_packed(const ck_ctx* ck, const uint64_t* cts, int t, int level, int c, int m, int kappa, int c_out,
+                   const double* filt, const long* tau, int rep, int d, uint64_t* outs, double* out_scale) {
     const size_t N = ck->N, s = N / 2, block = (size_t)m * m;
-    if (s % block || (size_t)c * block != (size_t)t * s || level < 1) return -1;
+    if (s % block || (size_t)c * block * (size_t)d != (size_t)t * s || level < 1 || rep < 1 || d < 1) return -1;
+    if (t >= 2 && d != 1) return -1;
     const size_t z = s / block;
+    const size_t rmax = t == 1 ? (size_t)c : z;
     const int n_out = (size_t)c_out <= z ? 1 : (int)((size_t)c_out / z);
     const int nr = level + 1, ne = nr + ck->K, dn = ck_dnum_at(ck, level);
     const long h = kappa / 2;
@@ -1149,14 +1159,15 @@ int ck_conv_shards(const ck_ctx* ck, const uint64_t* cts, int t, int level, int 
     double* rplain = malloc(s * sizeof(double));
     uint64_t* pt = malloc(extw * 8);
     for (int u = 0; u < t; u++)
-        for (size_t r = 0; r < z; r++)
+        for (size_t r = 0; r < rmax; r++)
             for (long ll = -h; ll <= h; ll++) {
-                const long bamt = (long)(r * block) + ll;
+                const long bamt = (long)(r * (size_t)rep * block) + ll;
                 const uint64_t g = ck_galois_elt(ck, bamt);
                 int have_ip = 0;
                 for (int v = 0; v < n_out; v++)
                     for (long kk = -h; kk <= h; kk++) {
-                        if (!emu_fused_plain_ms(c, m, kappa, c_out, s, filt, v, u, (int)r, kk, ll, 1.0, plain))
+                        if (!emu_fused_plain_packed(c, m, kappa, c_out, s, filt, tau, rep, v, u, (int)r, kk, ll, 1.0,
+                                                    plain))
                             continue;
                         if (g != 1 && !have_ip) {
                             ck_inner_product(ck, dsrc + (size_t)u * dn * extw, level, cache_get(ck, &kc, g), g, ip0,

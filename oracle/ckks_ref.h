@@ -106,6 +106,11 @@ int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int k
 int ck_conv_shards(const ck_ctx* ck, const uint64_t* cts, int t, int level, int c, int m, int kappa, int c_out,
                    const double* filt, uint64_t* outs, double* out_scale);
 
+/* image-mode conv over a PackedImage with channel permutation tau (NULL = identity),
+ * replication rep and duplication d (t = 1 only); same fused BSGS as ck_conv_shards */
+int ck_conv_packed(const ck_ctx* ck, const uint64_t* cts, int t, int level, int c, int m, int kappa, int c_out,
+                   const double* filt, const long* tau, int rep, int d, uint64_t* outs, double* out_scale);
+
 /* Channel-shard mode conv (fused BSGS, see ckks_ref.c): cts [c][m^2/s][2][level+1][N]
  * -> outs [c_out][m^2/s][2][level][N]; returns the output shard count. */
 int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int m, int kappa, int c_out,

@@ -119,15 +119,19 @@ int emu_conv_slots(int c, int m, int kappa, int c_out, size_t s, const double* i
 /* Multi-shard image-mode geometry (conv.cpp:37-67 with t >= 2, d = 1,
  * rep = 1, tau = identity): shard u holds channels [u z, (u+1) z),
  *   in_channel(u, r, b) = u z + (b + r) % z,  out_channel(v, b) = (v z + b) % c_out. */
-int emu_fused_plain_ms(int c, int m, int kappa, int c_out, size_t s, const double* filt, int v, int u,
-                       int r, long kk, long ll, double scale, double* plain) {
+/* ImageConv::fused_plain (conv.cpp:69-85) over a PackedImage with channel
+ * permutation tau (c entries, NULL = identity) and replication rep:
+ * in_channel(u, r, b) = block_channel(u z + (b + r rep) mod z) with
+ * block_channel(g) = tau[(g / rep) mod c] (pack.hpp:44, conv.cpp:63-65). */
+int emu_fused_plain_packed(int c, int m, int kappa, int c_out, size_t s, const double* filt, const long* tau, int rep,
+                           int v, int u, int r, long kk, long ll, double scale, double* plain) {
     const size_t block = (size_t)m * m;
     const size_t z = s / block;
     int any = 0;
-    (void)c;
     for (size_t i = 0; i < s; i++) plain[i] = 0.0;
     for (size_t b = 0; b < z; b++) {
-        const int in_ch = (int)((size_t)u * z + (b + (size_t)r) % z);
+        const size_t g = (size_t)u * z + (b + (size_t)r * (size_t)rep) % z;
+        const int in_ch = tau ? (int)tau[(g / (size_t)rep) % (size_t)c] : (int)g;
         const int out_ch = (int)(((size_t)v * z + b) % (size_t)c_out);
         const double w = emu_filt_centered(filt, c_out, kappa, in_ch, out_ch, kk, ll) * scale;
         if (w == 0.0) continue;
@@ -138,6 +142,11 @@ int emu_fused_plain_ms(int c, int m, int kappa, int c_out, size_t s, const doubl
             for (long j = j_lo; j < j_hi; j++) plain[b * block + (size_t)(i * m + j)] = w;
     }
     return any;
+}
+
+int emu_fused_plain_ms(int c, int m, int kappa, int c_out, size_t s, const double* filt, int v, int u,
+                       int r, long kk, long ll, double scale, double* plain) {
+    return emu_fused_plain_packed(c, m, kappa, c_out, s, filt, NULL, 1, v, u, r, kk, ll, scale, plain);
 }
 
 /* conv_image_shards (conv.cpp:261-264 -> conv_image_mode, plan = nullopt,

@@ -49,6 +49,9 @@ int emu_conv_slots(int c, int m, int kappa, int c_out, size_t s, const double* i
 /* multi-shard image mode (conv.cpp:37-67, 146-199 with t >= 2): the fused
  * plaintext of output shard v vs rotation r of input shard u, and the full
  * conv_image_shards slots; returns the output shard count n_out */
+/* fused_plain over a PackedImage with permutation tau (NULL = identity) and replication rep */
+int emu_fused_plain_packed(int c, int m, int kappa, int c_out, size_t s, const double* filt, const long* tau, int rep,
+                           int v, int u, int r, long kk, long ll, double scale, double* plain);
 int emu_fused_plain_ms(int c, int m, int kappa, int c_out, size_t s, const double* filt, int v, int u,
                        int r, long kk, long ll, double scale, double* plain);
 int emu_conv_shards_slots(int c, int m, int kappa, int c_out, size_t s, const double* img, const double* filt,

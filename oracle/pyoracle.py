@@ -90,6 +90,8 @@ def lib():
                               C.c_int, u64p, dp]
         L.ck_conv_shards.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp,
                                      u64p, dp]
+        L.ck_conv_packed.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp,
+                                     lp, C.c_int, C.c_int, u64p, dp]
         L.ck_conv_channel.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp, u64p, dp]
         L.ck_lintrans.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, lp, u64p, u64p]
         L.ck_lintrans_src.argtypes = [C.c_void_p, u64p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), lp, u64p,
@@ -140,6 +142,7 @@ def ref():
         R.ref_write_network.argtypes = [C.c_int, C.c_char_p, C.c_uint64]
         R.ref_run_network.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_int, C.c_int, dp, dp, C.c_int,
                                       C.POINTER(C.c_int64), dp, C.POINTER(C.c_int64), u64p, C.c_char_p, C.c_uint64]
+        R.ref_pool_conv.argtypes = [C.c_int, C.c_int, dp, C.c_uint64, C.c_int, C.c_int, dp, dp, C.c_int, u64p]
         R.ref_downsample.argtypes = [C.c_int, C.c_int, dp, C.c_uint64, C.c_int, C.c_double, dp, C.c_int, u64p, u64p,
                                      u64p]
         R.ref_slot_sum.argtypes = [dp, C.c_uint64, C.c_uint64, dp]
@@ -269,6 +272,17 @@ def ref_run_network(json_path, input_path, shard_size=0, initial_level=0, auto_b
     nl, no = int(meta[0]), int(meta[1])
     return dict(logits=lg[:no].copy(), oracle_logits=ol[:no].copy(), info=info[:4 * nl].reshape(nl, 4).copy(),
                 errors=err[:nl].copy(), totals=tot.copy())
+
+
+def ref_pool_conv(c, m, img, s, kappa, c_out, filt, cap=16):
+    """the reference's convolve(pool(pack(img, s)), k): (conv shard slots [n][s], meta [m, c, d, rep, mode, n])."""
+    out = np.zeros(cap * s)
+    meta = np.zeros(6, dtype=np.uint64)
+    n = ref().ref_pool_conv(c, m, _ptr(np.ascontiguousarray(img, dtype=np.float64), dp), s, kappa, c_out,
+                            _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), _ptr(out, dp), cap,
+                            _ptr(meta, u64p))
+    assert n > 0, n
+    return out[: n * s].reshape(n, s), meta
 
 
 def ref_slot_sum(vec, block):
@@ -649,6 +663,21 @@ class CKKS:
         lib().ck_lintrans_src(self.h, _ptr(cts, u64p), cts.shape[0], level, len(terms), src, a,
                               _ptr(np.ascontiguousarray(pts), u64p), _ptr(out, u64p))
         return out
+
+    def conv_packed(self, cts, level, c, m, kappa, c_out, filt, tau, rep, d):
+        """image-mode conv over a PackedImage (tau, rep, d): cts [t][2][level+1][N] -> [n_out][2][level][N]."""
+        cts = np.ascontiguousarray(cts, dtype=np.uint64)
+        t = cts.shape[0]
+        z = (self.N // 2) // (m * m)
+        n_out = 1 if c_out <= z else c_out // z
+        out = np.zeros((n_out, 2, level, self.N), dtype=np.uint64)
+        sc = C.c_double(0)
+        tv = (C.c_long * c)(*[int(x) for x in tau])
+        rc = lib().ck_conv_packed(self.h, _ptr(cts, u64p), t, level, c, m, kappa, c_out,
+                                  _ptr(np.ascontiguousarray(filt, dtype=np.float64), dp), tv, rep, d, _ptr(out, u64p),
+                                  C.byref(sc))
+        assert rc == n_out, rc
+        return out, sc.value
 
     def conv_channel(self, cts, level, c, m, kappa, c_out, filt):
         """channel-shard conv: cts [c * pc][2][level+1][N] -> [c_out * pc][2][level][N]."""

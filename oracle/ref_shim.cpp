@@ -291,6 +291,33 @@ int ref_downsample(int c, int m, const double* img, uint64_t s, int window, doub
     }
 }
 
+/// convolve(pool(pack(img, s)), k) (conv.cpp:364-371 on a pooled PackedImage: tau,
+/// rep, duplication): out_slots = the conv's shards, meta = [m, c, d, rep, mode, n].
+int ref_pool_conv(int c, int m, const double* img, uint64_t s, int kappa, int c_out, const double* filt,
+                  double* out_slots, int cap, uint64_t* meta) {
+    try {
+        ImageTensor t(c, m);
+        std::memcpy(t.data.data(), img, t.data.size() * sizeof(double));
+        FilterTensor k(c, c_out, kappa);
+        std::memcpy(k.weights.data(), filt, k.weights.size() * sizeof(double));
+        Engine eng;
+        PackedImage p = pool(eng, pack(eng, t, s));
+        PackedImage out = convolve(eng, p, k);
+        const int n = (int)out.shards.size();
+        for (int u = 0; u < n && u < cap; ++u)
+            std::memcpy(out_slots + (size_t)u * s, out.shards[(size_t)u].slots.data(), s * sizeof(double));
+        meta[0] = out.m;
+        meta[1] = out.c;
+        meta[2] = out.d;
+        meta[3] = out.rep;
+        meta[4] = out.mode == ShardMode::ImageShard ? 0 : 1;
+        meta[5] = (uint64_t)n;
+        return n;
+    } catch (...) {
+        return -1;
+    }
+}
+
 /// eval_chebyshev (act.cpp:151-162) of the slot vector `x` (s slots) placed at
 /// `level`: out receives the slots, meta = [output level, max depth consumed],
 /// ledger the op counters. Returns 0, or -2 with the exception text in `err`.

@@ -733,3 +733,30 @@ def test_downsample_missing_key_is_an_error_and_leaks_nothing():
         ctx.pool([ct], 4, 32)
     ctx.gen_galois_keys([1])
     assert np.abs(ctx.decrypt(ctx.rotate(ct, 1)) - np.roll(ctx.decrypt(ct), -1)).max() < 1e-6
+
+
+@pytest.mark.parametrize("name", ["pc_cfg1_c4m32", "pc_cfg1_c8m32", "pc_cfg1_c16m32", "pc_cfg1_c2m32"])
+def test_packed_conv_after_pool_bit_exact(oracle, golden, p1, name):
+    """convolve() of a pooled map (fhe_conv_layer_create_packed: tau, rep, duplication):
+    residues bit-exact vs the golden model's ck_conv_packed on the same pooled ciphertexts,
+    decrypted within 1e-6 of the reference's convolve(pool(pack(img)))."""
+    c, m, s, kap, co, si, sf = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, kap, co, si, sf, 0)
+    block = m * m
+    d_in = s // (block * c) if block * c < s else 1
+    chunks = list(np.tile(img, d_in).reshape(-1, s))
+    p1.ctx.gen_galois_keys(oracle.downsample_steps(c, m, s, True))
+    cts = [p1.ctx.encrypt(p1.ctx.encode(x), ENC_SEED + u) for u, x in enumerate(chunks)]
+    pooled, tau, rep, d, mode = p1.ctx.downsample(cts, c, m, d=d_in)
+    layer = p1.ctx.conv_layer_packed(c, co, m // 2, kap, filt, t=len(pooled), tau=tau, rep=rep, d=d,
+                                     level=pooled[0].level)
+    p1.ctx.gen_galois_keys(layer.steps())
+    outs = p1.ctx.conv2d_shards(pooled, layer)
+    want = golden[f"{name}/slots"]
+    assert len(outs) == want.shape[0] and layer.d_out == int(golden[f"{name}/meta"][2])
+    for u, o in enumerate(outs):
+        assert np.abs(p1.ctx.decrypt(o) - want[u]).max() < TOL
+    ref, _ = p1.ck.conv_packed(np.stack([x.residues() for x in pooled]), pooled[0].level, c, m // 2, kap, co, filt,
+                               tau, rep, d)
+    for o, r in zip(outs, ref):
+        assert np.array_equal(o.residues(), r)

@@ -184,3 +184,27 @@ def test_channel_shard_conv_decrypts_to_reference(cfg1, oracle, golden, name):
     out, sc = cfg1.conv_channel(cts, 4, c, m, k, co, filt)
     dec = np.stack([cfg1.decrypt(out[v], 3, sc) for v in range(out.shape[0])])
     assert np.abs(dec - golden[f"{name}/slots"]).max() < 1e-6
+
+
+POOLCONV = ["pc_cfg1_c4m32", "pc_cfg1_c8m32", "pc_cfg1_c16m32", "pc_cfg1_c2m32"]
+
+
+@pytest.mark.parametrize("name", POOLCONV)
+def test_packed_conv_after_pool_decrypts_to_reference(cfg1, oracle, golden, name):
+    """the golden model's pooling (downsample_restated over ck_lintrans_src) followed by its
+    conv over the pooled packing (ck_conv_packed: tau, rep, duplication) decrypts to the
+    reference's convolve(pool(pack(img))) slots."""
+    c, m, s, kap, co, si, sf = (int(x) for x in golden[f"{name}/params"])
+    img, filt = oracle.make_inputs(c, m, kap, co, si, sf, 0)
+    block = m * m
+    d_in = s // (block * c) if block * c < s else 1
+    chunks = list(np.tile(img, d_in).reshape(-1, s))
+    top = 4
+    cts = [(cfg1.encrypt(cfg1.encode(x, cfg1.scale, top), top, 9000 + u), top) for u, x in enumerate(chunks)]
+    pooled, tau, rep, d, mode = oracle.downsample_restated(oracle.CkksOps(cfg1), cts, c, m, s, True, d_in=d_in)
+    lv = pooled[0][1]
+    out, sc = cfg1.conv_packed(np.stack([p[0] for p in pooled]), lv, c, m // 2, kap, co, filt, tau, rep, d)
+    want = golden[f"{name}/slots"]
+    assert out.shape[0] == want.shape[0]
+    for u in range(out.shape[0]):
+        assert np.abs(cfg1.decrypt(out[u], lv - 1, sc) - want[u]).max() < 1e-6
