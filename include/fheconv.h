@@ -164,6 +164,15 @@ int fhe_rescale(fhe_ctx* ctx, const fhe_ct* ct, fhe_ct** out);
  * rot.cpp:21-29), 1 signed (nearest power of two, rot.cpp:31-46). Requires
  * keys for the power-of-two steps used. */
 int fhe_rotate_decomposed(fhe_ctx* ctx, const fhe_ct* ct, int64_t k, int strategy, fhe_ct** out);
+/* plan_rotations + execute_schedule (rot.cpp:96-156) for one source: request i
+ * rotates by amounts[i]; same_source[i] != 0 joins the previous group and makes
+ * it hoisted (its members' first keyed steps share one ModUp, the remaining steps
+ * run sequentially). strategy 0 positive, 1 signed, 2 exact (one keyed step per
+ * request). outs[n] in request order; planned_keyed = the reference's
+ * total_keyed_rotations, groups / hoisted groups of the plan (all optional). */
+int fhe_execute_schedule(fhe_ctx* ctx, const fhe_ct* src, const int64_t* amounts, const int* same_source, size_t n,
+                         int strategy, fhe_ct** outs, uint64_t* planned_keyed, uint64_t* groups,
+                         uint64_t* hoisted_groups);
 /* keyed steps a decomposition uses (host-only planning) */
 int fhe_decompose(int strategy, uint64_t n, uint64_t s, int64_t* steps, int cap);
 

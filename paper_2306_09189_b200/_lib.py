@@ -108,6 +108,8 @@ SIGNATURES = [
     ("fhe_conv_layer_create_packed", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_int, C.c_size_t,
                                                i64p, C.c_int, C.c_int, vpp]),
     ("fhe_conv_layer_output_packing", C.c_int, [vp, C.POINTER(C.c_int)]),
+    ("fhe_execute_schedule", C.c_int, [vp, vp, i64p, C.POINTER(C.c_int), C.c_size_t, C.c_int, vpp,
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("fhe_linear", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, C.c_int, C.c_int, C.c_int, dp, dp, vpp]),
     ("fhe_conv2d_shards_into", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, vp, C.POINTER(C.c_void_p)]),
     ("fhe_conv2d_batch_host_async", C.c_int, [vp, u64p, C.c_size_t, C.c_double, vp, C.c_int, C.c_size_t, u64p]),

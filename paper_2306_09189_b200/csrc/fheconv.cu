@@ -2446,6 +2446,92 @@ int fhe_rotate_decomposed(fhe_ctx* c, const fhe_ct* ct, int64_t k, int strategy,
     });
 }
 
+static void okc(fhe_ctx* c, int rc);
+
+// plan_rotations + execute_schedule (reference rot.cpp:96-156): requests join
+// the previous group when flagged same_source (the group becomes hoisted); a
+// hoisted group rotates by its members' first keyed steps as one hoisted batch
+// (one ModUp of the source), then each member's remaining steps sequentially;
+// other groups rotate sequentially from the source. Steps equal to a full
+// cycle (the signed decomposition's +-s) are counted as the reference counts
+// them but executed as the identity.
+int fhe_execute_schedule(fhe_ctx* c, const fhe_ct* src, const int64_t* amounts, const int* same_source, size_t n,
+                         int strategy, fhe_ct** outs, uint64_t* planned_keyed, uint64_t* groups_out,
+                         uint64_t* hoisted_groups_out) {
+    return guard(c, [&] {
+        if (!src || !amounts || !outs) fail(FHE_E_INVALID, "null argument");
+        if (strategy < 0 || strategy > 2) fail(FHE_E_INVALID, "unknown decomposition strategy");
+        const uint64_t s = c->slots();
+        struct Group {
+            std::vector<std::vector<int64_t>> steps;
+            std::vector<size_t> req;
+            bool hoisted = false;
+        };
+        std::vector<Group> groups;
+        uint64_t total = 0;
+        for (size_t i = 0; i < n; ++i) {
+            const uint64_t a = c->reduce_amount(amounts[i]);
+            std::vector<int64_t> st;
+            if (a != 0) {
+                if (strategy == 2) {
+                    st.push_back((int64_t)a);
+                } else {
+                    int64_t buf[64];
+                    const int ns = fhe_decompose(strategy, a, s, buf, 64);
+                    if (ns < 0) fail(FHE_E_INVALID, "decomposition failed");
+                    st.assign(buf, buf + ns);
+                }
+            }
+            total += st.size();
+            if (same_source && same_source[i] && !groups.empty()) {
+                groups.back().steps.push_back(st);
+                groups.back().req.push_back(i);
+                groups.back().hoisted = true;
+            } else {
+                groups.push_back(Group{{st}, {i}, false});
+            }
+        }
+        auto rotate_chain = [&](fhe_ct* cur, const std::vector<int64_t>& st, size_t from) {
+            for (size_t k = from; k < st.size(); ++k) {
+                fhe_ct* nx = nullptr;
+                const int rc = fhe_rotate(c, cur, st[k], &nx);
+                fhe_ct_free(cur);
+                okc(c, rc);
+                cur = nx;
+            }
+            return cur;
+        };
+        std::vector<fhe_ct*> res(n, nullptr);
+        try {
+            for (const Group& g : groups) {
+                if (g.hoisted) {
+                    std::vector<int64_t> firsts;
+                    for (const auto& st : g.steps) firsts.push_back(st.empty() ? 0 : st[0]);
+                    std::vector<fhe_ct*> batch(firsts.size(), nullptr);
+                    okc(c, fhe_rotate_hoisted(c, src, firsts.data(), firsts.size(), batch.data()));
+                    for (size_t m2 = 0; m2 < g.steps.size(); ++m2) res[g.req[m2]] = rotate_chain(batch[m2], g.steps[m2], 1);
+                } else {
+                    fhe_ct* cur = nullptr;
+                    okc(c, fhe_rotate(c, src, 0, &cur));  // copy (recorded like the reference's v = source)
+                    res[g.req[0]] = rotate_chain(cur, g.steps[0], 0);
+                }
+            }
+        } catch (...) {
+            for (fhe_ct* x : res)
+                if (x) fhe_ct_free(x);
+            throw;
+        }
+        for (size_t i = 0; i < n; ++i) outs[i] = res[i];
+        if (planned_keyed) *planned_keyed = total;
+        if (groups_out) *groups_out = groups.size();
+        if (hoisted_groups_out) {
+            uint64_t h = 0;
+            for (const Group& g : groups) h += g.hoisted;
+            *hoisted_groups_out = h;
+        }
+    });
+}
+
 int fhe_mul_plain(fhe_ctx* c, const fhe_ct* ct, const fhe_pt* pt, fhe_ct** out) {
     return guard(c, [&] {
         if (pt->level < ct->level) fail(FHE_E_INVALID, "slot count mismatch");

@@ -260,6 +260,18 @@ class Context:
     def rotate_decomposed(self, ct: Ciphertext, k: int, strategy: int) -> Ciphertext:
         return self._new(lib().fhe_rotate_decomposed, ct.h, k, strategy)
 
+    def execute_schedule(self, ct: Ciphertext, amounts: Sequence[int], same_source: Sequence[int], strategy: int):
+        """fhe_execute_schedule (reference plan_rotations + execute_schedule): returns
+        (outputs, planned keyed rotations, groups, hoisted groups)."""
+        n = len(amounts)
+        a = np.ascontiguousarray(amounts, dtype=np.int64)
+        ss = (C.c_int * max(1, n))(*[int(x) for x in same_source])
+        outs = (C.c_void_p * max(1, n))()
+        tot, g, gh = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        self._check(lib().fhe_execute_schedule(self.h, ct.h, a.ctypes.data_as(_lib.i64p), ss, n, strategy, outs,
+                                               C.byref(tot), C.byref(g), C.byref(gh)))
+        return [Ciphertext(self, outs[i]) for i in range(n)], tot.value, g.value, gh.value
+
     def mul_plain(self, ct: Ciphertext, pt: Plaintext) -> Ciphertext:
         return self._new(lib().fhe_mul_plain, ct.h, pt.h)
 

@@ -760,3 +760,35 @@ def test_packed_conv_after_pool_bit_exact(oracle, golden, p1, name):
                                tau, rep, d)
     for o, r in zip(outs, ref):
         assert np.array_equal(o.residues(), r)
+
+
+@pytest.mark.parametrize("strat", [0, 1, 2])
+def test_execute_schedule_matches_reference_plan(oracle, golden, strat):
+    """plan_rotations + execute_schedule (rot.cpp:96-156) on the cfg2 stencil (m = 32, one
+    same-source group): the reference's keyed-step total and grouping, outputs equal the
+    slot rotations, residues equal the golden model's sequential rotations."""
+    p = pair(oracle, "cfg2")
+    s = p.ctx.slots
+    stencil = [kk * 32 + ll for kk in (-1, 0, 1) for ll in (-1, 0, 1)]
+    pow2 = [1 << i for i in range(14)]
+    p.ctx.gen_galois_keys(pow2 + [-x for x in pow2] + [a for a in stencil if a])
+    z = rnd(s, 31)
+    ct = p.ctx.encrypt(p.ctx.encode(z), ENC_SEED)
+    outs, tot, groups, hoisted = p.ctx.execute_schedule(ct, stencil, [0] + [1] * 8, strat)
+    assert tot == int(golden[f"plan_stencil/strat{strat}/total"][0])
+    assert (groups, hoisted) == (1, 1)
+    for a, o in zip(stencil, outs):
+        assert np.abs(p.ctx.decrypt(o) - np.roll(z, -a)).max() < TOL
+    from paper_2306_09189_b200 import decompose
+    ctr = p.ck.encrypt(p.ck.encode(z, p.ck.scale, p.top), p.top, ENC_SEED)
+    a = stencil[0]
+    steps = [a % s] if strat == 2 else decompose(strat, a % s, s)
+    cur = ctr
+    for st in steps:
+        if st % s:
+            cur = p.ck.rotate(cur, p.top, st)
+    assert np.array_equal(outs[0].residues(), cur)
+    # without same-source flags every request is its own sequential group
+    outs2, tot2, groups2, hoisted2 = p.ctx.execute_schedule(ct, stencil, [0] * 9, strat)
+    assert (tot2, groups2, hoisted2) == (tot, 9, 0)
+    assert np.array_equal(outs2[0].residues(), cur)
