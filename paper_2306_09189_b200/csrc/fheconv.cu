@@ -3074,79 +3074,92 @@ static void linear_impl(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const
     const int level = shards[0]->level;
     if (level < 2) fail(FHE_E_RUNTIME, "depth exhausted");
     auto feat = [&](size_t u, size_t i) -> long { return (long)featmap[u * s + i]; };
-    // products W_o . x_u for every output feature and shard, one level
-    std::vector<fhe_ct*> prods;
-    std::vector<int> prod_o;
-    std::vector<double> wt(s);
-    const double ql = (double)c->primes[level];
-    for (int o = 0; o < out_features; ++o) {
-        bool started = false;
-        for (size_t u = 0; u < t; ++u) {
-            bool any = false;
-            for (size_t i = 0; i < s; ++i) {
-                const long f = feat(u, i);
-                wt[i] = f < 0 ? 0.0 : w[(size_t)o * nin + (size_t)f];
-                any = any || wt[i] != 0.0;
+    std::vector<fhe_ct*> prods, sums;  // freed on any error (e.g. a missing slot-sum key)
+    try {
+        // products W_o . x_u for every output feature and shard, one level
+        std::vector<int> prod_o;
+        std::vector<double> wt(s);
+        const double ql = (double)c->primes[level];
+        for (int o = 0; o < out_features; ++o) {
+            bool started = false;
+            for (size_t u = 0; u < t; ++u) {
+                bool any = false;
+                for (size_t i = 0; i < s; ++i) {
+                    const long f = feat(u, i);
+                    wt[i] = f < 0 ? 0.0 : w[(size_t)o * nin + (size_t)f];
+                    any = any || wt[i] != 0.0;
+                }
+                if (!any && started) continue;
+                fhe_pt* pt = nullptr;
+                fhe_ct *pr = nullptr, *rs = nullptr;
+                okc(c, fhe_encode(c, wt.data(), s, level, ql, 0, &pt));
+                okc(c, fhe_mul_plain(c, shards[u], pt, &pr));
+                okc(c, fhe_rescale(c, pr, &rs));
+                fhe_pt_free(pt);
+                fhe_ct_free(pr);
+                prods.push_back(rs);
+                prod_o.push_back(o);
+                started = true;
             }
-            if (!any && started) continue;
+        }
+        sums.assign(prods.size(), nullptr);
+        okc(c, fhe_slot_sum_batch(c, prods.data(), prods.size(), s, sums.data()));
+        for (fhe_ct*& x : prods) {
+            fhe_ct_free(x);
+            x = nullptr;
+        }
+        // per output: sum over shards, select slot o (second level), accumulate
+        fhe_ct* acc = nullptr;
+        std::vector<double> sel(s, 0.0);
+        size_t k = 0;
+        for (int o = 0; o < out_features; ++o) {
+            fhe_ct* total = sums[k];
+            sums[k++] = nullptr;
+            while (k < sums.size() && prod_o[k] == o) {
+                fhe_ct* nt = nullptr;
+                okc(c, fhe_add(c, total, sums[k], &nt));
+                fhe_ct_free(total);
+                fhe_ct_free(sums[k]);
+                sums[k] = nullptr;
+                total = nt;
+                ++k;
+            }
+            std::fill(sel.begin(), sel.end(), 0.0);
+            sel[(size_t)o] = 1.0;
             fhe_pt* pt = nullptr;
             fhe_ct *pr = nullptr, *rs = nullptr;
-            okc(c, fhe_encode(c, wt.data(), s, level, ql, 0, &pt));
-            okc(c, fhe_mul_plain(c, shards[u], pt, &pr));
+            okc(c, fhe_encode(c, sel.data(), s, total->level, (double)c->primes[total->level], 0, &pt));
+            okc(c, fhe_mul_plain(c, total, pt, &pr));
             okc(c, fhe_rescale(c, pr, &rs));
             fhe_pt_free(pt);
             fhe_ct_free(pr);
-            prods.push_back(rs);
-            prod_o.push_back(o);
-            started = true;
-        }
-    }
-    std::vector<fhe_ct*> sums(prods.size());
-    okc(c, fhe_slot_sum_batch(c, prods.data(), prods.size(), s, sums.data()));
-    for (fhe_ct* x : prods) fhe_ct_free(x);
-    // per output: sum over shards, select slot o (second level), accumulate
-    fhe_ct* acc = nullptr;
-    std::vector<double> sel(s, 0.0);
-    size_t k = 0;
-    for (int o = 0; o < out_features; ++o) {
-        fhe_ct* total = sums[k++];
-        while (k < sums.size() && prod_o[k] == o) {
-            fhe_ct* nt = nullptr;
-            okc(c, fhe_add(c, total, sums[k], &nt));
             fhe_ct_free(total);
-            fhe_ct_free(sums[k]);
-            total = nt;
-            ++k;
+            if (!acc) {
+                acc = rs;
+            } else {
+                fhe_ct* na = nullptr;
+                okc(c, fhe_add(c, acc, rs, &na));
+                fhe_ct_free(acc);
+                fhe_ct_free(rs);
+                acc = na;
+            }
         }
-        std::fill(sel.begin(), sel.end(), 0.0);
-        sel[(size_t)o] = 1.0;
-        fhe_pt* pt = nullptr;
-        fhe_ct *pr = nullptr, *rs = nullptr;
-        okc(c, fhe_encode(c, sel.data(), s, total->level, (double)c->primes[total->level], 0, &pt));
-        okc(c, fhe_mul_plain(c, total, pt, &pr));
-        okc(c, fhe_rescale(c, pr, &rs));
-        fhe_pt_free(pt);
-        fhe_ct_free(pr);
-        fhe_ct_free(total);
-        if (!acc) {
-            acc = rs;
-        } else {
-            fhe_ct* na = nullptr;
-            okc(c, fhe_add(c, acc, rs, &na));
-            fhe_ct_free(acc);
-            fhe_ct_free(rs);
-            acc = na;
-        }
+        std::vector<double> bias(s, 0.0);
+        for (int o = 0; o < out_features; ++o) bias[(size_t)o] = b[o];
+        fhe_pt* bp = nullptr;
+        okc(c, fhe_encode(c, bias.data(), s, acc->level, acc->scale, 0, &bp));
+        fhe_ct* res = nullptr;
+        okc(c, fhe_add_plain(c, acc, bp, &res));
+        fhe_pt_free(bp);
+        fhe_ct_free(acc);
+        *out = res;
+    } catch (...) {
+        for (fhe_ct* x : prods)
+            if (x) fhe_ct_free(x);
+        for (fhe_ct* x : sums)
+            if (x) fhe_ct_free(x);
+        throw;
     }
-    std::vector<double> bias(s, 0.0);
-    for (int o = 0; o < out_features; ++o) bias[(size_t)o] = b[o];
-    fhe_pt* bp = nullptr;
-    okc(c, fhe_encode(c, bias.data(), s, acc->level, acc->scale, 0, &bp));
-    fhe_ct* res = nullptr;
-    okc(c, fhe_add_plain(c, acc, bp, &res));
-    fhe_pt_free(bp);
-    fhe_ct_free(acc);
-    *out = res;
 }
 
 int fhe_linear(fhe_ctx* c, const fhe_ct* const* shards, size_t t, int ch, int m, int out_features, const double* w,

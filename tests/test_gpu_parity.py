@@ -792,3 +792,13 @@ def test_execute_schedule_matches_reference_plan(oracle, golden, strat):
     outs2, tot2, groups2, hoisted2 = p.ctx.execute_schedule(ct, stencil, [0] * 9, strat)
     assert (tot2, groups2, hoisted2) == (tot, 9, 0)
     assert np.array_equal(outs2[0].residues(), cur)
+
+
+def test_linear_missing_key_is_an_error():
+    """linear() without its slot-sum keys fails with the missing-key error (products freed)."""
+    from paper_2306_09189_b200 import CONFIGS, Context, FheError
+    ctx = Context(**CONFIGS["cfg1"])
+    ctx.keygen(7)
+    ct = ctx.encrypt(ctx.encode(rnd(ctx.slots, 5)), ENC_SEED)
+    with pytest.raises(FheError, match="key"):
+        ctx.linear([ct], 4, 32, rnd(2 * 4096, 6), rnd(2, 7))
