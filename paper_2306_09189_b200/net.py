@@ -514,7 +514,9 @@ def bench_network(ctx: Context, spec: NetworkSpec, x: ImageTensor, repetitions: 
     for _ in range(repetitions):
         ctx.ledger_reset()
         r = run_network(ctx, spec, x, check_layers=False)
-        sig = [l.ops for l in r.layers]
+        # the reference's counters (CostLedger::Snapshot); GPU work counters such as kernel
+        # launches also count the keys generated on the first run
+        sig = [{k: l.ops.get(k, 0) for k in LEDGER_KEYS} for l in r.layers]
         if first is None:
             first = (r, sig)
         else:

@@ -84,3 +84,15 @@ def test_pooled_output_feeds_the_next_convolution(oracle, c, m):
     got = net.unpack_slots(out, [p.ctx.decrypt(o) for o in out.shards], s)
     want = net.oracle_conv(net.oracle_avgpool2x2(x), k).data
     assert np.abs(got - want).max() < TOL
+
+
+def test_cli_run_and_bench_demo(tmp_path, capsys):
+    """`run` / `bench` of the demo network on the GPU (tools/main.cpp:23-42 semantics)."""
+    from paper_2306_09189_b200.__main__ import main
+    d = str(tmp_path / "demo")
+    assert main(["demo", d]) == 0
+    assert main(["run", f"{d}/net.json", f"{d}/input.tensor", "--max-residual", "1e-6"]) == 0
+    out = capsys.readouterr().out
+    assert "residual mean" in out and "gelu" in out
+    assert main(["bench", f"{d}/net.json", f"{d}/input.tensor", "-n", "2"]) == 0
+    assert "deterministic across 2 runs: yes" in capsys.readouterr().out

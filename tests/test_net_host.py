@@ -111,3 +111,28 @@ def test_slot_feature_map_and_unpack():
     fm2 = net.slot_feature_map(p2, 32)
     assert np.array_equal(fm2[0, :4], 4 + np.arange(4)) and (fm2[0, 4:8] == -1).all()
     assert np.array_equal(fm2[0, 8:12], np.arange(4))
+
+
+def test_cli_decomp_matches_reference_tables(golden, capsys):
+    """`decomp` (tools/main.cpp:62-72): positive / signed lengths equal the reference's."""
+    from paper_2306_09189_b200.__main__ import main
+    assert main(["decomp", "0", "200", "--modulus", "4096"]) == 0
+    lines = capsys.readouterr().out.strip().splitlines()[1:]
+    lens = golden["decomp4096/lens"]
+    for ln in lines:
+        n, pos, sgn = (int(x) for x in ln.split()[:3])
+        assert (pos, sgn) == (int(lens[0][n]), int(lens[1][n])), n
+
+
+def test_cli_demo_and_poly_table(tmp_path, capsys):
+    from paper_2306_09189_b200.__main__ import main
+    d = str(tmp_path / "demo")
+    assert main(["demo", d]) == 0
+    spec = net.load_network(os.path.join(d, "net.json"))
+    assert [l.type for l in spec.layers] == ["conv", "conv", "pool", "gelu", "pool_linear"]
+    _, pre, _ = net._plan(spec)
+    assert sum(net.required_level(l, pre[i]) for i, l in enumerate(spec.layers)) <= 12  # fits cfg3
+    assert main(["poly-table", "--grid", "2000"]) == 0
+    out = capsys.readouterr().out
+    assert "Chebyshev nodes" in out
+    assert main(["run", os.path.join(d, "missing.json"), os.path.join(d, "input.tensor")]) == 1
