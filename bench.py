@@ -777,10 +777,15 @@ def golden_ckks_baseline():
     ck.keygen(7)
     ct = ck.encrypt(ck.encode(img, ck.scale, 12), 12, 9000)
     t = time.perf_counter()
+    ck.conv(ct, 12, C_IN, M, KAPPA, C_OUT, filt, 2)  # first call also generates the 23 Galois keys
+    dt_first = time.perf_counter() - t
+    t = time.perf_counter()
     ck.conv(ct, 12, C_IN, M, KAPPA, C_OUT, filt, 2)
     dt = time.perf_counter() - t
     return {"value": round(1.0 / dt, 4), "unit": "conv/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": "1 cfg3 Approach-2 conv incl. on-demand Galois keygen (23 keys), CPU RNS-CKKS golden model"}
+            "first_call_s_incl_keygen": round(dt_first, 3),
+            "sample": "1 cfg3 Approach-2 conv with the Galois keys already generated (a first call generated "
+                      "them), CPU RNS-CKKS golden model on all host cores"}
 
 
 def run_reference(args, rank):

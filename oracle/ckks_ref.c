@@ -28,6 +28,18 @@ typedef unsigned __int128 u128;
 /* pi as a double literal (same literal in the product encoder) */
 #define CK_PI 3.14159265358979323846
 
+typedef struct {
+    uint64_t g;
+    uint64_t* key;
+} key_slot;
+
+typedef struct key_cache_s {
+    key_slot* slots;
+    int n, cap;
+} key_cache;
+
+static void kc_reset(key_cache* kc);
+
 struct ck_ctx {
     int logN;
     size_t N;
@@ -45,6 +57,7 @@ struct ck_ctx {
     int64_t* s_coef;
     uint64_t* s_ntt; /* [np][N] */
     uint32_t* brv;
+    struct key_cache_s* kc; /* Galois / relinearisation keys generated on demand, kept until keygen / destroy */
 };
 
 /* ------------------------------------------------------------------ */
@@ -143,6 +156,7 @@ static uint64_t find_root(uint64_t q, uint64_t N) {
 ck_ctx* ck_create(int logN, int L, const int* qbits, int K, const int* pbits, int logscale) {
     if (L + K > CK_MAXP || L < 1 || K < 1) return NULL;
     ck_ctx* ck = calloc(1, sizeof(ck_ctx));
+    ck->kc = calloc(1, sizeof(key_cache));
     ck->logN = logN;
     ck->N = (size_t)1 << logN;
     ck->L = L;
@@ -192,6 +206,8 @@ ck_ctx* ck_create(int logN, int L, const int* qbits, int K, const int* pbits, in
 
 void ck_destroy(ck_ctx* ck) {
     if (!ck) return;
+    kc_reset(ck->kc);
+    free(ck->kc);
     for (int i = 0; i < ck->np; i++) {
         free(ck->tw[i]);
         free(ck->tw_sh[i]);
@@ -478,6 +494,7 @@ static void sample_error_ntt(const ck_ctx* ck, uint64_t key, const int* idx, int
 
 void ck_keygen(ck_ctx* ck, uint64_t seed) {
     const size_t N = ck->N;
+    kc_reset(ck->kc); /* keys of the previous secret are stale */
     ck->key_seed = seed;
     ck->have_key = 1;
     free(ck->s_coef);
@@ -903,28 +920,26 @@ void ck_mul_ct(const ck_ctx* ck, const uint64_t* a, const uint64_t* b, int level
 /* fused convolution                                     */
 /* ------------------------------------------------------------------ */
 
-typedef struct {
-    uint64_t g;
-    uint64_t* key;
-} key_slot;
-
-typedef struct {
-    key_slot slots[128];
-    int n;
-} key_cache;
 
 static const uint64_t* cache_get(const ck_ctx* ck, key_cache* kc, uint64_t g) {
     for (int i = 0; i < kc->n; i++)
         if (kc->slots[i].g == g) return kc->slots[i].key;
+    if (kc->n == kc->cap) {
+        kc->cap = kc->cap ? 2 * kc->cap : 64;
+        kc->slots = realloc(kc->slots, (size_t)kc->cap * sizeof(key_slot));
+    }
     key_slot* s = &kc->slots[kc->n++];
     s->g = g;
     s->key = malloc(key_words(ck) * 8);
     ck_galois_key(ck, g, s->key);
     return s->key;
 }
-static void cache_free(key_cache* kc) {
+static void kc_reset(key_cache* kc) {
+    if (!kc) return;
     for (int i = 0; i < kc->n; i++) free(kc->slots[i].key);
-    kc->n = 0;
+    free(kc->slots);
+    kc->slots = NULL;
+    kc->n = kc->cap = 0;
 }
 
 /* ACC_c[u] += pt[u] * term_c[u], where for a rotated term
@@ -1032,7 +1047,7 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
         }
     free(plain);
     free(rplain);
-    key_cache kc = {.n = 0};
+    key_cache* kcp = ck->kc;
     uint64_t* dsrc = malloc((size_t)dn * extw * 8);
     uint64_t* ip0 = malloc(extw * 8);
     uint64_t* ip1 = malloc(extw * 8);
@@ -1043,7 +1058,7 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
         for (int gi = 0; gi < ngi; gi++) any |= nonempty[gi * nb + bi];
         if (!any) continue;
         const uint64_t g = ck_galois_elt(ck, bamt[bi]);
-        if (g != 1) ck_inner_product(ck, dsrc, level, cache_get(ck, &kc, g), g, ip0, ip1);
+        if (g != 1) ck_inner_product(ck, dsrc, level, cache_get(ck, kcp, g), g, ip0, ip1);
         for (int gi = 0; gi < ngi; gi++) {
             if (!nonempty[gi * nb + bi]) continue;
             const uint64_t* pt = pts + ((size_t)gi * nb + bi) * extw;
@@ -1079,7 +1094,7 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
          * ModDown performs its rounding), saving a ModDown per giant step */
         ck_moddown(ck, y + extw, level, yq + (size_t)nr * N);
         ck_modup(ck, yq + (size_t)nr * N, level, dsrc);
-        ck_inner_product(ck, dsrc, level, cache_get(ck, &kc, g), g, ip0, ip1);
+        ck_inner_product(ck, dsrc, level, cache_get(ck, kcp, g), g, ip0, ip1);
         for (int t = 0; t < ne; t++) ck_automorph_ntt(ck, y + (size_t)t * N, perm + (size_t)t * N, g);
         for (int u = 0; u < ne; u++) {
             const uint64_t q = ck->q[ext_prime(ck, level, u)];
@@ -1090,7 +1105,6 @@ static int conv_bsgs(const ck_ctx* ck, const uint64_t* ct, int level, int c, int
             }
         }
     }
-    cache_free(&kc);
     uint64_t* md = malloc(ctw * 8);
     ck_moddown(ck, acc0, level, md);
     ck_moddown(ck, acc1, level, md + (size_t)nr * N);
@@ -1147,7 +1161,7 @@ int ck_conv_packed(const ck_ctx* ck, const uint64_t* cts, int t, int level, int 
         for (int k = 0; k < ck->K; k++) P = ck_mulmod(P, ck->q[ck->L + k] % q, q);
         Pmod[u] = u < nr ? P : 0;
     }
-    key_cache kc = {.n = 0};
+    key_cache* kcp = ck->kc;
     uint64_t* dsrc = malloc((size_t)t * dn * extw * 8);
     for (int u = 0; u < t; u++)
         ck_modup(ck, cts + (size_t)u * ctw + (size_t)nr * N, level, dsrc + (size_t)u * dn * extw);
@@ -1170,7 +1184,7 @@ int ck_conv_packed(const ck_ctx* ck, const uint64_t* cts, int t, int level, int 
                                                     plain))
                             continue;
                         if (g != 1 && !have_ip) {
-                            ck_inner_product(ck, dsrc + (size_t)u * dn * extw, level, cache_get(ck, &kc, g), g, ip0,
+                            ck_inner_product(ck, dsrc + (size_t)u * dn * extw, level, cache_get(ck, kcp, g), g, ip0,
                                              ip1);
                             have_ip = 1;
                         }
@@ -1212,7 +1226,7 @@ int ck_conv_packed(const ck_ctx* ck, const uint64_t* cts, int t, int level, int 
             }
             ck_moddown(ck, y + extw, level, yq + (size_t)nr * N);
             ck_modup(ck, yq + (size_t)nr * N, level, dg);
-            ck_inner_product(ck, dg, level, cache_get(ck, &kc, g), g, ip0, ip1);
+            ck_inner_product(ck, dg, level, cache_get(ck, kcp, g), g, ip0, ip1);
             for (int u = 0; u < ne; u++) ck_automorph_ntt(ck, y + (size_t)u * N, perm + (size_t)u * N, g);
             for (int u = 0; u < ne; u++) {
                 const uint64_t q = ck->q[ext_prime(ck, level, u)];
@@ -1228,7 +1242,6 @@ int ck_conv_packed(const ck_ctx* ck, const uint64_t* cts, int t, int level, int 
         ck_rescale(ck, md, level, outs + (size_t)v * octw);
     }
     if (out_scale) *out_scale = (ck->scale * (double)ql) / (double)ql;
-    cache_free(&kc);
     free(dsrc); free(ip0); free(ip1); free(Y); free(nonempty_g);
     free(acc0); free(acc1); free(yq); free(perm); free(dg); free(md);
     return n_out;
@@ -1276,7 +1289,7 @@ int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int
         for (int k = 0; k < ck->K; k++) P = ck_mulmod(P, ck->q[ck->L + k] % q, q);
         Pmod[u] = u < nr ? P : 0;
     }
-    key_cache kc = {.n = 0};
+    key_cache* kcp = ck->kc;
     uint64_t* dsrc = malloc(nsh * dn * extw * 8);
     for (size_t sh = 0; sh < nsh; sh++) ck_modup(ck, cts + sh * ctw + (size_t)nr * N, level, dsrc + sh * dn * extw);
     /* inner products of every (shard, ll != 0), computed once */
@@ -1286,7 +1299,7 @@ int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int
             if (ll == 0) continue;
             const uint64_t g = ck_galois_elt(ck, ll);
             uint64_t* ip = ips + (sh * kap + (size_t)(ll + h)) * 2 * extw;
-            ck_inner_product(ck, dsrc + sh * dn * extw, level, cache_get(ck, &kc, g), g, ip, ip + extw);
+            ck_inner_product(ck, dsrc + sh * dn * extw, level, cache_get(ck, kcp, g), g, ip, ip + extw);
         }
     double* mask = malloc(s * sizeof(double));
     double* rmask = malloc(s * sizeof(double));
@@ -1351,7 +1364,7 @@ int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int
                 }
                 ck_moddown(ck, y + extw, level, yq + (size_t)nr * N);
                 ck_modup(ck, yq + (size_t)nr * N, level, dg);
-                ck_inner_product(ck, dg, level, cache_get(ck, &kc, ge), ge, ip0, ip1);
+                ck_inner_product(ck, dg, level, cache_get(ck, kcp, ge), ge, ip0, ip1);
                 for (int u = 0; u < ne; u++) ck_automorph_ntt(ck, y + (size_t)u * N, perm + (size_t)u * N, ge);
                 for (int u = 0; u < ne; u++) {
                     const uint64_t q = ck->q[ext_prime(ck, level, u)];
@@ -1367,7 +1380,6 @@ int ck_conv_channel(const ck_ctx* ck, const uint64_t* cts, int level, int c, int
             ck_rescale(ck, md, level, outs + ((size_t)g * pc + v) * octw);
         }
     if (out_scale) *out_scale = (ck->scale * (double)ql) / (double)ql;
-    cache_free(&kc);
     free(dsrc); free(ips); free(mask); free(rmask); free(pt); free(Y); free(gne);
     free(acc0); free(acc1); free(yq); free(perm); free(dg); free(ip0); free(ip1); free(md);
     return (int)((size_t)c_out * pc);
@@ -1395,7 +1407,7 @@ void ck_lintrans_src(const ck_ctx* ck, const uint64_t* cts, int nsrc, int level,
         for (int k = 0; k < ck->K; k++) P = ck_mulmod(P, ck->q[ck->L + k] % q, q);
         Pmod[u] = u < nr ? P : 0;
     }
-    key_cache kc = {.n = 0};
+    key_cache* kcp = ck->kc;
     uint64_t* dsrc = malloc((size_t)nsrc * dn * extw * 8);
     for (int j = 0; j < nsrc; j++) ck_modup(ck, cts + (size_t)j * ctw + (size_t)nr * N, level, dsrc + (size_t)j * dn * extw);
     uint64_t* ip0 = malloc(extw * 8);
@@ -1409,7 +1421,7 @@ void ck_lintrans_src(const ck_ctx* ck, const uint64_t* cts, int nsrc, int level,
         if (g == 1) {
             conv_accumulate(ck, level, pt, ct, 1, NULL, NULL, Pmod, y, y + extw);
         } else {
-            ck_inner_product(ck, dsrc + (size_t)j * dn * extw, level, cache_get(ck, &kc, g), g, ip0, ip1);
+            ck_inner_product(ck, dsrc + (size_t)j * dn * extw, level, cache_get(ck, kcp, g), g, ip0, ip1);
             conv_accumulate(ck, level, pt, ct, g, ip0, ip1, Pmod, y, y + extw);
         }
     }
@@ -1417,7 +1429,6 @@ void ck_lintrans_src(const ck_ctx* ck, const uint64_t* cts, int nsrc, int level,
     ck_moddown(ck, y, level, md);
     ck_moddown(ck, y + extw, level, md + (size_t)nr * N);
     ck_rescale(ck, md, level, out);
-    cache_free(&kc);
     free(dsrc); free(ip0); free(ip1); free(y); free(md);
 }
 
@@ -1467,7 +1478,7 @@ int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int k
     uint64_t* X = malloc(ctw * 8);
     uint64_t* ip0 = malloc(extw * 8);
     uint64_t* ip1 = malloc(extw * 8);
-    key_cache kc = {.n = 0};
+    key_cache* kcp = ck->kc;
     ck_modup(ck, ct + (size_t)nr * N, level, dsrc);
 
     if (plan == 2) { /* Approach 2: channel rotations of src (hoisted), then shifts */
@@ -1479,7 +1490,7 @@ int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int k
             if (gr == 1)
                 memcpy(X, ct, ctw * 8);
             else
-                rotate_from_digits(ck, ct, dsrc, level, cache_get(ck, &kc, gr), gr, X);
+                rotate_from_digits(ck, ct, dsrc, level, cache_get(ck, kcp, gr), gr, X);
             ck_modup(ck, X + (size_t)nr * N, level, dtmp);
             int i = 0;
             for (long kk = -h; kk <= h; kk++)
@@ -1490,7 +1501,7 @@ int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int k
                     if (g == 1) {
                         conv_accumulate(ck, level, pt, X, 1, NULL, NULL, Pmod, acc0, acc1);
                     } else {
-                        ck_inner_product(ck, dtmp, level, cache_get(ck, &kc, g), g, ip0, ip1);
+                        ck_inner_product(ck, dtmp, level, cache_get(ck, kcp, g), g, ip0, ip1);
                         conv_accumulate(ck, level, pt, X, g, ip0, ip1, Pmod, acc0, acc1);
                     }
                 }
@@ -1506,7 +1517,7 @@ int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int k
                 if (gi == 1)
                     memcpy(X, ct, ctw * 8);
                 else
-                    rotate_from_digits(ck, ct, dsrc, level, cache_get(ck, &kc, gi), gi, X);
+                    rotate_from_digits(ck, ct, dsrc, level, cache_get(ck, kcp, gi), gi, X);
                 ck_modup(ck, X + (size_t)nr * N, level, dtmp);
                 for (int r = 0; r < c; r++) {
                     if (!nonempty[r * nk + i]) continue;
@@ -1515,13 +1526,12 @@ int ck_conv(const ck_ctx* ck, const uint64_t* ct, int level, int c, int m, int k
                     if (g == 1) {
                         conv_accumulate(ck, level, pt, X, 1, NULL, NULL, Pmod, acc0, acc1);
                     } else {
-                        ck_inner_product(ck, dtmp, level, cache_get(ck, &kc, g), g, ip0, ip1);
+                        ck_inner_product(ck, dtmp, level, cache_get(ck, kcp, g), g, ip0, ip1);
                         conv_accumulate(ck, level, pt, X, g, ip0, ip1, Pmod, acc0, acc1);
                     }
                 }
             }
     }
-    cache_free(&kc);
     /* one ModDown per component, then one rescale */
     uint64_t* md = malloc(ctw * 8);
     ck_moddown(ck, acc0, level, md);
