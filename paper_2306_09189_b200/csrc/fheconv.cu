@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -215,6 +216,13 @@ struct fhe_pt {
 
 struct fhe_conv_layer {
     fhe_ctx* ctx;
+    // unique per layer object (never reused, unlike the host address): keys the
+    // CUDA-graph cache so a freed layer's graphs can never be replayed for a new one
+    uint64_t uid = next_uid();
+    static uint64_t next_uid() {
+        static std::atomic<uint64_t> n{1};
+        return n++;
+    }
     int c_in, c_out, m, kappa, level, nk;
     std::vector<int> nonempty;  // [c_in][nk]
     uint64_t* d_pts;            // [c_in][nk][ne][N]
@@ -702,7 +710,7 @@ fhe_conv_layer::Bsgs& ensure_bsgs(fhe_ctx* c, const fhe_conv_layer* cly, int ori
     }
     B.nb = (int)B.bamt.size();
     B.ngi = (int)B.gamt.size();
-    if (B.nb > (orient == 5 ? kMaxFused : kMaxBaby)) fail(FHE_E_INVALID, "too many baby steps for the BSGS schedule");
+    if (orient != 5 && B.nb > kMaxBaby) fail(FHE_E_INVALID, "too many baby steps for the BSGS schedule");
     const int ne = c->ne_at(ly->level);
     const size_t extw = (size_t)ne * c->N, s = c->slots();
     ck(cudaMalloc(&B.d_pts, (size_t)B.ngi * B.nb * extw * 8), "cudaMalloc");
@@ -755,31 +763,50 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
         for (int g = 0; g < B.ngi; ++g) any |= B.nonempty[(size_t)g * B.nb + b] != 0;
         if (any && c->reduce_amount(B.bamt[b]) != 0) c->ledger.key_switches += nsrc;
     }
-    if (B.nb > kMaxFused) fail(FHE_E_INVALID, "too many baby steps for the fused BSGS schedule");
-    for (int g0 = 0; g0 < B.ngi; g0 += kFusedMaxG) {
-        const int ng = std::min(kFusedMaxG, B.ngi - g0);
+    // more than kMaxFused baby steps (large c kappa): several launches per giant chunk,
+    // the later ones continuing the accumulators (the accumulating variant holds <= 3 giants)
+    const bool chunked = B.nb > kMaxFused;
+    const int gstep = chunked ? 3 : kFusedMaxG;
+    for (int g0 = 0; g0 < B.ngi; g0 += gstep) {
+        const int ng = std::min(gstep, B.ngi - g0);
         f.ng = ng;
-        f.nb = 0;
-        double pt_words = 0, keyed = 0;
-        for (int b = 0; b < B.nb; ++b) {
-            uint32_t mask = 0;
-            for (int g = 0; g < ng; ++g)
-                if (B.nonempty[(size_t)(g0 + g) * B.nb + b]) mask |= 1u << g;
-            if (!mask) continue;
-            const uint32_t gal = c->galois_of(c->reduce_amount(B.bamt[b]));
-            f.galois[f.nb] = gal;
-            f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
-            f.gmask[f.nb] = mask;
-            f.pt[f.nb] = B.d_pts + ((size_t)g0 * B.nb + b) * extw;
-            pt_words += __builtin_popcount(mask);
-            if (gal != 1) keyed += 1;
-            f.nb++;
-        }
         f.Y = Y + (size_t)g0 * 2 * extw;
-        c->timed("bsgs_fused",
-                 c->rows(keyed * 2.0 * dn * ne + pt_words * ne +
-                         nsrc * ((double)dn * ne + 2.0 * nr + 2.0 * ng * ne)),
-                 [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+        std::vector<int> active;
+        for (int b = 0; b < B.nb; ++b)
+            for (int g = 0; g < ng; ++g)
+                if (B.nonempty[(size_t)(g0 + g) * B.nb + b]) {
+                    active.push_back(b);
+                    break;
+                }
+        if (active.empty()) {  // no term feeds these giants: their accumulators are zero
+            for (int s2 = 0; s2 < nsrc; ++s2)
+                ck(cudaMemsetAsync(f.Y + (size_t)s2 * ystride, 0, (size_t)ng * 2 * extw * 8, c->st), "memset");
+            continue;
+        }
+        for (size_t a0 = 0; a0 < active.size(); a0 += kMaxFused) {
+            f.nb = 0;
+            f.accumulate = a0 > 0;
+            double pt_words = 0, keyed = 0;
+            for (size_t ai = a0; ai < active.size() && f.nb < kMaxFused; ++ai) {
+                const int b = active[ai];
+                uint32_t mask = 0;
+                for (int g = 0; g < ng; ++g)
+                    if (B.nonempty[(size_t)(g0 + g) * B.nb + b]) mask |= 1u << g;
+                const uint32_t gal = c->galois_of(c->reduce_amount(B.bamt[b]));
+                f.galois[f.nb] = gal;
+                f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+                f.gmask[f.nb] = mask;
+                f.pt[f.nb] = B.d_pts + ((size_t)g0 * B.nb + b) * extw;
+                f.srcslot[f.nb] = 0;
+                pt_words += __builtin_popcount(mask);
+                if (gal != 1) keyed += 1;
+                f.nb++;
+            }
+            c->timed("bsgs_fused",
+                     c->rows(keyed * 2.0 * dn * ne + pt_words * ne +
+                             nsrc * ((double)dn * ne + 2.0 * nr + (f.accumulate ? 4.0 : 2.0) * ng * ne)),
+                     [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+        }
     }
 }
 
@@ -1592,11 +1619,10 @@ void lintrans_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const std::stri
 
 int auto_orient(const fhe_conv_layer* ly) {
     // giant steps each cost a ModDown + ModUp (~120 NTT rows at cfg3) while a
-    // fused baby step costs one key stream: the fused schedule (kappa giant
-    // steps) whenever its c kappa baby steps fit one launch, else the smaller
-    // of the two classic sets as giant steps
-    if (ly->c_in * ly->kappa <= kMaxFused) return 5;
-    return ly->kappa * ly->kappa <= ly->c_in ? 3 : 4;
+    // fused baby step costs one key stream: always the fused schedule (kappa
+    // giant steps); more than kMaxFused baby steps run in several launches
+    (void)ly;
+    return 5;
 }
 
 void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct* out) {
@@ -1726,7 +1752,8 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
             return;
         }
         if (approach >= 3) ensure_bsgs(c, ly, approach);  // host encoding + sync: never inside a capture
-        std::vector<const void*> key{ly, (const void*)(uintptr_t)approach, (const void*)(uintptr_t)n};
+        std::vector<const void*> key{(const void*)(uintptr_t)ly->uid, (const void*)(uintptr_t)approach,
+                                     (const void*)(uintptr_t)n};
         for (size_t s = 0; s < n; ++s) {
             key.push_back(cts[s]->d);
             key.push_back(outs[s]->d);
@@ -2630,6 +2657,15 @@ int fhe_conv_layer_create(fhe_ctx* c, int c_in, int c_out, int m, int kappa, con
 void fhe_conv_layer_free(fhe_conv_layer* ly) {
     if (!ly) return;
     cudaStreamSynchronize(ly->ctx->st);
+    auto& gs = ly->ctx->graphs;  // drop the layer's captured graphs (they reference its plaintexts)
+    for (size_t i = 0; i < gs.size();) {
+        if (!gs[i].key.empty() && gs[i].key[0] == (const void*)(uintptr_t)ly->uid) {
+            cudaGraphExecDestroy(gs[i].exec);
+            gs.erase(gs.begin() + (long)i);
+        } else {
+            ++i;
+        }
+    }
     cudaFree(ly->d_pts);
     if (ly->d_pts_ms) cudaFree(ly->d_pts_ms);
     for (auto& b : ly->bs)

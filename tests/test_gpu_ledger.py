@@ -126,3 +126,33 @@ def test_graph_replay_keeps_ledger_and_results(ctx, oracle):
     for r in results[1:]:
         for a, b in zip(results[0], r):
             assert np.array_equal(a, b)
+
+
+def test_graph_cache_never_replays_a_freed_layer(oracle):
+    """CUDA graphs are keyed by a per-layer id, not the host address: creating and freeing
+    layers of different geometry over the same ciphertext buffers always gives the new
+    layer's result (a stale graph would replay the freed layer's kernels)."""
+    import gc
+    import numpy as np
+    from paper_2306_09189_b200 import CONFIGS, Context
+    ctx = Context(**CONFIGS["cfg1"])
+    ctx.keygen(7)
+    rng = np.random.default_rng(3)
+    img = rng.uniform(-1, 1, 4096)
+    ct = ctx.encrypt(ctx.encode(img), 9000)
+    out = ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1)
+    for k in (3, 5, 3, 7):
+        filt = rng.uniform(-1, 1, 16 * k * k)
+        layer = ctx.conv_layer(4, 4, 32, k, filt)
+        ctx.gen_galois_keys(layer.steps(0))
+        for _ in range(2):
+            ctx.conv2d_into(ct, layer, 0, out)
+        x = img.reshape(4, 32, 32)
+        w = filt.reshape(4, 4, k, k)
+        h = k // 2
+        xp = np.pad(x, ((0, 0), (h, h), (h, h)))
+        ref = sum(np.einsum("fg,fij->gij", w[:, :, r, s], xp[:, r:r + 32, s:s + 32])
+                  for r in range(k) for s in range(k))
+        assert np.abs(ctx.decrypt(out) - ref.ravel()).max() < 1e-6
+        del layer
+        gc.collect()

@@ -802,3 +802,31 @@ def test_linear_missing_key_is_an_error():
     ct = ctx.encrypt(ctx.encode(rnd(ctx.slots, 5)), ENC_SEED)
     with pytest.raises(FheError, match="key"):
         ctx.linear([ct], 4, 32, rnd(2 * 4096, 6), rnd(2, 7))
+
+
+@pytest.mark.parametrize("c,m,k", [(16, 16, 7), (4, 32, 7), (1, 64, 9)])
+def test_conv_large_kernels_fused_schedule(oracle, c, m, k):
+    """kernels up to 9x9 and c kappa beyond one fused launch (16 x 7 = 112 baby steps run in
+    two launches per giant chunk): the default schedule is bit-exact with the golden model's
+    fused BSGS (plan 5), batched = single, decrypted within 1e-6 of a float64 conv."""
+    p = pair(oracle, "cfg1")
+    img, filt = oracle.make_inputs(c, m, k, c, 7000 + k, 8000 + k, 0)
+    layer = p.ctx.conv_layer(c, c, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps(0))
+    ct = p.ctx.encrypt(p.ctx.encode(img), ENC_SEED)
+    out = p.ctx.conv2d(ct, layer, 0)
+    outs = p.ctx.conv2d_batch([ct, ct, ct], layer, 0)
+    x = img.reshape(c, m, m)
+    w = filt.reshape(c, c, k, k)
+    h = k // 2
+    xp = np.pad(x, ((0, 0), (h, h), (h, h)))
+    ref = np.zeros((c, m, m))
+    for r in range(k):
+        for s in range(k):
+            ref += np.einsum("fg,fij->gij", w[:, :, r, s], xp[:, r:r + m, s:s + m])
+    assert np.abs(p.ctx.decrypt(out)[: c * m * m] - ref.ravel()).max() < TOL
+    ctr = p.ck.encrypt(p.ck.encode(img, p.ck.scale, p.top), p.top, ENC_SEED)
+    gold, _ = p.ck.conv(ctr, p.top, c, m, k, c, filt, 5)
+    assert np.array_equal(out.residues(), gold)
+    for o in outs:
+        assert np.array_equal(o.residues(), gold)
