@@ -1425,6 +1425,18 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
                 f.y_g_stride = 2 * extw;
                 f.accumulate = 1;
                 double keyed = 0, pts = 0;
+                auto flush = [&] {  // more babies than one launch holds: continue the accumulators
+                    if (!f.nb) return;
+                    c->ledger.hoisted_rotations += (uint64_t)B * (uint64_t)keyed;
+                    c->ledger.ct_pt_mults += (uint64_t)B * (uint64_t)pts;
+                    c->ledger.adds += (uint64_t)B * (uint64_t)pts;
+                    c->timed("bsgs_fused",
+                             c->rows(keyed * 2.0 * dn * ne + pts * ne +
+                                     B * (3.0 * C_ * dn * ne + 2.0 * nr + 4.0 * ng * ne)),
+                             [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+                    f.nb = 0;
+                    keyed = pts = 0;
+                };
                 for (int fi = 0; fi < C_; ++fi)
                     for (int dv = -1; dv <= 1; ++dv) {
                         const int src = v + dv;
@@ -1438,7 +1450,7 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
                                 if (ly->ms_nonempty[pt_of(g, fi, g0 + gg, lo, spill)]) mask |= 1u << gg;
                             }
                             if (!mask) continue;
-                            if (f.nb == kMaxFused) fail(FHE_E_INVALID, "too many baby steps for one output shard");
+                            if (f.nb == kMaxFused) flush();
                             const uint32_t gal = c->galois_of(c->reduce_amount(lo - h));
                             f.galois[f.nb] = gal;
                             f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
@@ -1453,13 +1465,7 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
                             }
                         }
                     }
-                if (!f.nb) continue;
-                c->ledger.hoisted_rotations += (uint64_t)B * (uint64_t)keyed;
-                c->ledger.ct_pt_mults += (uint64_t)B * (uint64_t)pts;
-                c->ledger.adds += (uint64_t)B * (uint64_t)pts;
-                c->timed("bsgs_fused",
-                         c->rows(keyed * 2.0 * dn * ne + pts * ne + B * (3.0 * C_ * dn * ne + 2.0 * nr + 4.0 * ng * ne)),
-                         [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+                flush();
             }
     c->release(dig);
     std::vector<int> giants;

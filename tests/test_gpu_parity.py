@@ -830,3 +830,29 @@ def test_conv_large_kernels_fused_schedule(oracle, c, m, k):
     assert np.array_equal(out.residues(), gold)
     for o in outs:
         assert np.array_equal(o.residues(), gold)
+
+
+def test_channel_shard_conv_many_input_channels(oracle):
+    """channel-shard conv whose baby steps per output shard exceed one fused launch
+    (16 input channels x 3 source shards x 3 column shifts = 144): chunked launches,
+    bit-exact vs the golden model, decrypted within 1e-6 of a float64 conv."""
+    p = pair(oracle, "cfg1")
+    c, co, m, k = 16, 1, 128, 3
+    img, filt = oracle.make_inputs(c, m, k, co, 7100, 8100, 0)
+    layer = p.ctx.conv_layer_shards(c, co, m, k, filt)
+    p.ctx.gen_galois_keys(layer.steps())
+    s = p.ctx.slots
+    chunks = list(img.reshape(-1, s))
+    cts = [p.ctx.encrypt(p.ctx.encode(x), ENC_SEED + u) for u, x in enumerate(chunks)]
+    outs = p.ctx.conv2d_shards(cts, layer)
+    x = img.reshape(c, m, m)
+    w = filt.reshape(c, co, k, k)
+    xp = np.pad(x, ((0, 0), (1, 1), (1, 1)))
+    ref = sum(np.einsum("fg,fij->gij", w[:, :, r, t], xp[:, r:r + m, t:t + m]) for r in range(k) for t in range(k))
+    got = np.concatenate([p.ctx.decrypt(o) for o in outs])
+    assert np.abs(got - ref.ravel()).max() < TOL
+    ctr = np.stack([p.ck.encrypt(p.ck.encode(x_, p.ck.scale, p.top), p.top, ENC_SEED + u)
+                    for u, x_ in enumerate(chunks)])
+    gold, _ = p.ck.conv_channel(ctr, p.top, c, m, k, co, filt)
+    for o, g in zip(outs, gold):
+        assert np.array_equal(o.residues(), g)
