@@ -856,3 +856,25 @@ def test_channel_shard_conv_many_input_channels(oracle):
     gold, _ = p.ck.conv_channel(ctr, p.top, c, m, k, co, filt)
     for o, g in zip(outs, gold):
         assert np.array_equal(o.residues(), g)
+
+
+def test_new_entry_points_reject_bad_arguments(p1):
+    """error texts of the packed conv, the feature-map linear and the schedule executor."""
+    from paper_2306_09189_b200 import FheError
+    s = p1.ctx.slots
+    w = rnd(4 * 4 * 9, 1)
+    with pytest.raises(FheError, match="tau is not a permutation"):
+        p1.ctx.conv_layer_packed(4, 4, 32, 3, w, t=1, tau=[0, 0, 1, 2])
+    with pytest.raises(FheError, match="metadata mismatch"):
+        p1.ctx.conv_layer_packed(4, 4, 32, 3, w, t=2)
+    with pytest.raises(FheError, match="duplicated multi-shard image"):
+        p1.ctx.conv_layer_packed(4, 4, 16, 3, w, t=2, d=2)
+    with pytest.raises(FheError, match="kernel size must be odd"):
+        p1.ctx.conv_layer_packed(4, 4, 32, 2, rnd(4 * 4 * 4, 1))
+    ct = p1.ctx.encrypt(p1.ctx.encode(rnd(s, 2)), ENC_SEED)
+    fm = np.full((1, s), -1, dtype=np.int64)
+    fm[0, :8] = np.arange(8) + 100
+    with pytest.raises(FheError, match="in_features does not match"):
+        p1.ctx.linear_features([ct], fm, rnd(2 * 8, 3), rnd(2, 4))
+    with pytest.raises(FheError, match="unknown decomposition strategy"):
+        p1.ctx.execute_schedule(ct, [1, 2], [0, 1], 7)
