@@ -7,6 +7,9 @@
 // inside 256-byte segments.
 #include "kernels.cuh"
 
+#ifndef FHE_FUSED_UNROLL2  // fused kernel: two baby steps per loop iteration (constant stage offsets)
+#define FHE_FUSED_UNROLL2 1
+#endif
 #ifndef FHE_FUSED_SPLITLD  // fused kernel: digit / c0 pairs as two 8-byte loads in output order
 #define FHE_FUSED_SPLITLD 1
 #endif
@@ -740,13 +743,12 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
         // bit-reversed exponent of this pair, reused for every baby's permutation
         const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
         auto pidx = [&](uint32_t g) { return brev_n((((e * g) & nmask) - 1) >> 1, c.logN); };
-        auto issue = [&](int b) {
+        auto issue_s = [&](int b, size_t so) {
             if (b >= a.nb) {
                 cp_async_commit();  // empty group keeps the wait count uniform
                 return;
             }
             const uint32_t pk = pidx(a.galois[b]);
-            const size_t so = (size_t)(b % NST) * LY::STAGE;
             const uint64_t* key = a.key[b];
             const uint32_t gm = a.gmask[b];
             const uint64_t* Du = SLOTS ? Du0 + (size_t)a.srcslot[b] * a.digit_slot_stride : Du0;
@@ -772,6 +774,7 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
             }
             cp_async_commit();
         };
+        auto issue = [&](int b) { issue_s(b, (size_t)(b % NST) * LY::STAGE); };
         U128 y[NG][2][2];
 #pragma unroll
         for (int g = 0; g < NG; ++g) y[g][0][0] = y[g][0][1] = y[g][1][0] = y[g][1][1] = U128{0, 0};
@@ -790,12 +793,12 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
         }
 #pragma unroll
         for (int b = 0; b < NST - 1; ++b) issue(b);
-        for (int b = 0; b < a.nb; ++b) {
+        // one baby step on pipeline stage `so` (the next stage `so_next` is refilled meanwhile)
+        auto baby = [&](int b, size_t so, size_t so_next) {
             cp_async_wait<NST - 2>();
             __syncthreads();  // stage b visible to all; everyone is past baby b-1
-            issue(b + NST - 1);
+            issue_s(b + NST - 1, so_next);
             const uint32_t pk = pidx(a.galois[b]);
-            const size_t so = (size_t)(b % NST) * LY::STAGE;
             uint64_t x0a = 0, x0b = 0, x1a = 0, x1b = 0;
             if (a.key[b]) {
                 // the gathered pair is (perm(k), perm(k)^1) in some order: one 16-byte
@@ -869,6 +872,17 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
                         for (int e2 = 0; e2 < 2; ++e2)
                             y[g][q2][e2] = U128{reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), 0};
             }
+        };
+        if constexpr (NST == 2 && FHE_FUSED_UNROLL2) {
+            // two babies per iteration: the stage offsets are compile-time constants
+            constexpr size_t S1 = LY::STAGE;
+            for (int b = 0; b < a.nb; b += 2) {
+                baby(b, 0, S1);
+                if (b + 1 < a.nb) baby(b + 1, S1, 0);
+            }
+        } else {
+            for (int b = 0; b < a.nb; ++b)
+                baby(b, (size_t)(b % NST) * LY::STAGE, (size_t)((b + NST - 1) % NST) * LY::STAGE);
         }
         cp_async_wait<0>();
         if (active) {
