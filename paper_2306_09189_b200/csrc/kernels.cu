@@ -700,7 +700,6 @@ __global__ void __launch_bounds__(kMatvecThreads) k_pt_matvec2(DevCtx c, uint64_
 template <int DN, int NG, int SG, int NST_>
 struct FusedLayout {
     static constexpr int P = 128 / SG;
-    static constexpr int NST = NST_;        // pipeline stages
     static constexpr int KW = 2 * DN * P;   // key words      [2*DN][P]
     static constexpr int PW = NG * P;       // plaintexts     [NG][P]
     static constexpr int DW = SG * DN * P;  // digits         [SG][DN][P]
