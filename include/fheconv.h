@@ -178,12 +178,17 @@ int fhe_decompose(int strategy, uint64_t n, uint64_t s, int64_t* steps, int cap)
 
 /* ----------------------------------------------------------------- conv */
 /* Host-side layer preparation (replaces ImageConv::fused_plain conv.cpp:69-85
- * + make_shift_plan :215-231): encodes the kappa^2 * c fused mask x weight
- * plaintexts at `level` over Q_level u P with scale q_level, uploads them
- * once. weights: (c_in, c_out, kappa, kappa) as FilterTensor::weights
- * (tensor.hpp:41-58). Single image shard, c_in * m^2 == s. */
+ * + make_shift_plan :215-231 + bias_plain :87-94): encodes the kappa^2 * c
+ * fused mask x weight plaintexts at `level` over Q_level u P with scale
+ * q_level, uploads them once. weights: (c_in, c_out, kappa, kappa) as
+ * FilterTensor::weights (tensor.hpp:41-58). Single image shard, c_in * m^2 <= s.
+ * bias: c_out values (or NULL) and output_scale (1.0 = none) as
+ * conv_plan(eng, p, k, plan, bias, output_scale) (conv.hpp:66-68): the fused
+ * plaintexts carry weight * output_scale, and bias[out_channel] * output_scale
+ * is added to every output block in the epilogue of the final fused ModDown +
+ * rescale (bit-identical to add_plain after the conv, conv.cpp:203-210). */
 int fhe_conv_layer_create(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
-                          int level, fhe_conv_layer** out);
+                          const double* bias, double output_scale, int level, fhe_conv_layer** out);
 void fhe_conv_layer_free(fhe_conv_layer* layer);
 /* multi-shard image mode (reference conv_image_shards, conv.cpp:261-264 via
  * conv_image_mode with t >= 2): an image of c_in channels
@@ -192,14 +197,15 @@ void fhe_conv_layer_free(fhe_conv_layer* layer);
  * land in n_out = max(1, c_out / z) ciphertexts (shard v block b = channel
  * (v z + b) mod c_out). Runs the fused BSGS schedule. */
 int fhe_conv_layer_create_shards(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
-                                 int level, fhe_conv_layer** out);
+                                 const double* bias, double output_scale, int level, fhe_conv_layer** out);
 /* image-mode layer over ANY PackedImage (conv_image_mode conv.cpp:40-211 as
  * convolve() reaches it after pooling): t input shards, tau[c_in] (physical
  * channel position -> logical channel; NULL = identity), rep, d (duplication,
  * t = 1 only). Channel rotations r rep m^2 (r < c_in for t = 1, else < z), fused
  * plaintexts from block_channel (pack.hpp:44). Run with fhe_conv2d_shards_into. */
 int fhe_conv_layer_create_packed(fhe_ctx* ctx, int c_in, int c_out, int m, int kappa, const double* weights,
-                                 int level, size_t t, const int64_t* tau, int rep, int d, fhe_conv_layer** out);
+                                 const double* bias, double output_scale, int level, size_t t, const int64_t* tau,
+                                 int rep, int d, fhe_conv_layer** out);
 /* output duplication d of a layer (ImageConv::make_output: n_out z / c_out; rep 1, identity tau) */
 int fhe_conv_layer_output_packing(const fhe_conv_layer* layer, int* d_out);
 /* input / output shard counts of a layer (1 / 1 for single-shard layers) */

@@ -9,15 +9,21 @@
 //
 //   fheconv::Engine eng(fheconv::Params::cfg3());
 //   eng.keygen(7);
-//   auto layer = eng.make_conv_layer(16, 16, 32, 3, weights, eng.max_level());
+//   auto layer = eng.make_conv_layer(16, 16, 32, 3, weights, eng.max_level(), bias, 0.5);
 //   eng.gen_galois_keys(layer.steps());
 //   auto ct  = eng.encode_encrypt(slots, 9000);
 //   auto out = eng.conv_plan(ct, layer, fheconv::ConvPlan::ShiftFirst);
 //   std::vector<double> y = eng.decrypt(out);
+//
+// or, with the reference's argument list (conv.hpp:66-68; the layer is built
+// once per (geometry, weights, bias, output_scale, level) and cached):
+//   auto out = eng.conv_plan(ct, 16, 16, 32, 3, weights, fheconv::ConvPlan::Fused, bias, 0.5);
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -27,16 +33,31 @@
 
 namespace fheconv {
 
-// reference conv.hpp:17 — ChannelFirst = paper Approach 1, ShiftFirst = Approach 2
-enum class ConvPlan { ChannelFirst = 1, ShiftFirst = 2 };
+// reference conv.hpp:17 — ChannelFirst = paper Approach 1, ShiftFirst = Approach 2;
+// the B200 schedules of fhe_conv2d (include/fheconv.h) follow: BabyGiant (channel
+// rotations hoisted, shifts as giant steps), BabyGiantShifts (roles swapped), Fused
+// (the c kappa rotations r m^2 + ll in one fused kernel, kappa row-shift giants) and
+// Auto (the fused schedule whenever it applies). All decrypt to the same slots.
+enum class ConvPlan { Auto = 0, ChannelFirst = 1, ShiftFirst = 2, BabyGiant = 3, BabyGiantShifts = 4, Fused = 5 };
 
+// BASELINE.json configs (N, Q and P prime bit sizes, log2 scale)
 struct Params {
     int log_n;
     std::vector<int> q_bits, p_bits;
     int log_scale;
     int device = 0;
     static Params cfg1() { return {13, {60, 40, 40, 40, 40}, {60}, 40}; }
-    static Params cfg3() { return {15, {60, 50, 50, 50, 50, 50, 50, 50, 50, 50, 50, 50, 50}, {60, 60}, 50}; }
+    static Params cfg2() { return {14, std::vector<int>(8, 50), {60}, 50}; }
+    static Params cfg3() { return {15, q_list(60, 50, 12), {60, 60}, 50}; }
+    static Params cfg4() { return {16, q_list(60, 50, 16), {60, 60, 60}, 50}; }
+    static Params cfg5() { return cfg3(); }  // three cfg3 layers, batch of 32
+
+private:
+    static std::vector<int> q_list(int first, int rest, int n) {
+        std::vector<int> v(1, first);
+        v.insert(v.end(), (size_t)n, rest);
+        return v;
+    }
 };
 
 class Ciphertext {
@@ -71,10 +92,11 @@ class ConvLayer {
 public:
     explicit ConvLayer(fhe_conv_layer* h) : h_(h) {}
     fhe_conv_layer* get() const { return h_.get(); }
-    std::vector<int64_t> steps() const {
-        std::vector<int64_t> s(1024);
+    // Galois steps of a plan's rotations; Auto (default) = the union, so every plan runs
+    std::vector<int64_t> steps(ConvPlan plan = ConvPlan::Auto) const {
+        std::vector<int64_t> s(8192);
         size_t n = 0;
-        fhe_conv_layer_steps(h_.get(), 2, s.data(), s.size(), &n);
+        fhe_conv_layer_steps(h_.get(), (int)plan, s.data(), s.size(), &n);
         s.resize(n);
         return s;
     }
@@ -109,6 +131,14 @@ public:
         max_level_ = nq - 1;
         scale_ = (double)(1ULL << p.log_scale);
     }
+
+    // cached layers release their device memory before the context goes away
+    ~Engine() {
+        layers_.clear();
+        packed_layers_.clear();
+    }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
 
     size_t slots() const { return slots_; }
     int max_level() const { return max_level_; }
@@ -172,16 +202,41 @@ public:
         return Ciphertext(o);
     }
 
-    // conv_plan (conv.cpp:266-271) on a pre-encoded layer
-    ConvLayer make_conv_layer(int c_in, int c_out, int m, int kappa, const std::vector<double>& weights, int level) {
+    // a pre-encoded conv layer: ImageConv's fused plaintexts (conv.cpp:69-85) with the
+    // output scale folded in, and the bias (bias_plain :87-94) added in the conv epilogue
+    ConvLayer make_conv_layer(int c_in, int c_out, int m, int kappa, const std::vector<double>& weights, int level,
+                              const std::vector<double>& bias = {}, double output_scale = 1.0) {
+        if (!bias.empty() && bias.size() != (size_t)c_out)
+            throw std::invalid_argument("bias size does not match output channels");
         fhe_conv_layer* l = nullptr;
-        check(fhe_conv_layer_create(raw(), c_in, c_out, m, kappa, weights.data(), level, &l));
+        check(fhe_conv_layer_create(raw(), c_in, c_out, m, kappa, weights.data(), bias.empty() ? nullptr : bias.data(),
+                                    output_scale, level, &l));
         return ConvLayer(l);
     }
+    // conv_plan (conv.cpp:266-271) on a pre-encoded layer
     Ciphertext conv_plan(const Ciphertext& ct, const ConvLayer& layer, ConvPlan plan) {
         fhe_ct* o = nullptr;
         check(fhe_conv2d(raw(), ct.get(), layer.get(), (int)plan, &o));
         return Ciphertext(o);
+    }
+    // conv_plan with the reference's argument list (conv.hpp:66-68): the layer for
+    // (geometry, weights, bias, output_scale, level) is encoded once and cached, its
+    // Galois keys generated on first use
+    Ciphertext conv_plan(const Ciphertext& ct, int c_in, int c_out, int m, int kappa, const std::vector<double>& weights,
+                         ConvPlan plan, const std::vector<double>& bias = {}, double output_scale = 1.0) {
+        return conv_plan(ct, cached_layer(c_in, c_out, m, kappa, weights, ct.level(), bias, output_scale), plan);
+    }
+    // a batch of independent ciphertexts through one layer (keys and plaintexts streamed
+    // once per batch; BASELINE cfg5)
+    std::vector<Ciphertext> conv_batch(const std::vector<const Ciphertext*>& cts, const ConvLayer& layer,
+                                       ConvPlan plan = ConvPlan::Auto) {
+        std::vector<const fhe_ct*> in;
+        for (const Ciphertext* c : cts) in.push_back(c->get());
+        std::vector<fhe_ct*> outs(in.size() ? in.size() : 1, nullptr);
+        check(fhe_conv2d_batch(raw(), in.data(), in.size(), layer.get(), (int)plan, outs.data()));
+        std::vector<Ciphertext> r;
+        for (size_t i = 0; i < in.size(); ++i) r.emplace_back(outs[i]);
+        return r;
     }
 
     // Engine::mul_ct (emu.cpp:69-80): relinearised and rescaled (gen_relin_key() first)
@@ -204,19 +259,31 @@ public:
     // pool / subsample_stride2 (pool.cpp:291-306) of any PackedImage
     Packed pool(const Packed& p, double output_scale = 1.0) { return downsample(p, true, output_scale); }
     Packed subsample_stride2(const Packed& p, double output_scale = 1.0) { return downsample(p, false, output_scale); }
-    // convolve (conv.cpp:364-371) of an image-mode PackedImage (any tau / rep / duplication)
-    Packed convolve(const Packed& p, int c_out, int kappa, const std::vector<double>& weights) {
+    // convolve (conv.cpp:364-371) of an image-mode PackedImage (any tau / rep /
+    // duplication), with bias and output_scale; the layer of a packing is encoded once
+    // and cached (repeated inference re-uses it and its keys)
+    Packed convolve(const Packed& p, int c_out, int kappa, const std::vector<double>& weights,
+                    const std::vector<double>& bias = {}, double output_scale = 1.0) {
         if (p.shards.empty()) throw std::invalid_argument("packed image has no shards");
-        fhe_conv_layer* l = nullptr;
-        check(fhe_conv_layer_create_packed(raw(), p.c, c_out, p.m, kappa, weights.data(), p.shards[0].level(),
-                                           p.shards.size(), p.tau.empty() ? nullptr : p.tau.data(), p.rep, p.d, &l));
-        ConvLayer layer(l);
-        {  // Galois keys of the layer's rotations (existing keys are kept)
-            std::vector<int64_t> st(4096);
+        if (!bias.empty() && bias.size() != (size_t)c_out)
+            throw std::invalid_argument("bias size does not match output channels");
+        const PackedKey key{p.c, c_out, p.m, kappa, p.shards[0].level(), (int)p.shards.size(), p.rep, p.d, p.tau,
+                            weights, bias, output_scale};
+        auto it = packed_layers_.find(key);
+        if (it == packed_layers_.end()) {
+            fhe_conv_layer* nl = nullptr;
+            check(fhe_conv_layer_create_packed(raw(), p.c, c_out, p.m, kappa, weights.data(),
+                                               bias.empty() ? nullptr : bias.data(), output_scale,
+                                               p.shards[0].level(), p.shards.size(),
+                                               p.tau.empty() ? nullptr : p.tau.data(), p.rep, p.d, &nl));
+            it = packed_layers_.emplace(key, std::make_shared<ConvLayer>(nl)).first;
+            // Galois keys of the layer's rotations (existing keys are kept)
+            std::vector<int64_t> st(8192);
             size_t ns = 0;
-            check(fhe_conv_layer_steps(l, 0, st.data(), st.size(), &ns));
+            check(fhe_conv_layer_steps(nl, 0, st.data(), st.size(), &ns));
             check(fhe_gen_galois_keys(raw(), st.data(), ns));
         }
+        fhe_conv_layer* l = it->second->get();
         int t = 0, n_out = 0, d_out = 1;
         fhe_conv_layer_shards(l, &t, &n_out);
         fhe_conv_layer_output_packing(l, &d_out);
@@ -257,6 +324,26 @@ public:
     }
 
 private:
+    // layer caches (conv_plan with weights, convolve): keyed by everything the encoding depends on
+    using LayerKey = std::tuple<int, int, int, int, int, std::vector<double>, std::vector<double>, double>;
+    using PackedKey = std::tuple<int, int, int, int, int, int, int, int, std::vector<int64_t>, std::vector<double>,
+                                 std::vector<double>, double>;
+    std::map<LayerKey, std::shared_ptr<ConvLayer>> layers_;
+    std::map<PackedKey, std::shared_ptr<ConvLayer>> packed_layers_;
+
+    const ConvLayer& cached_layer(int c_in, int c_out, int m, int kappa, const std::vector<double>& weights, int level,
+                                  const std::vector<double>& bias, double output_scale) {
+        const LayerKey key{c_in, c_out, m, kappa, level, weights, bias, output_scale};
+        auto it = layers_.find(key);
+        if (it == layers_.end()) {
+            auto ly = std::make_shared<ConvLayer>(make_conv_layer(c_in, c_out, m, kappa, weights, level, bias,
+                                                                  output_scale));
+            gen_galois_keys(ly->steps());
+            it = layers_.emplace(key, std::move(ly)).first;
+        }
+        return *it->second;
+    }
+
     Packed downsample(const Packed& p, bool window, double output_scale) {
         std::vector<const fhe_ct*> in;
         for (const auto& s : p.shards) in.push_back(s.get());

@@ -129,6 +129,8 @@ def ref():
                                       C.c_int, dp, dp]
         R.ref_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, C.c_uint64, dp,
                                dp, u64p, ip]
+        R.ref_conv_biased.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, C.c_uint64, dp,
+                                      C.c_double, dp, C.c_int, u64p]
         R.ref_oracle_conv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, dp]
         R.ref_decompose.argtypes = [C.c_int, C.c_uint64, C.c_uint64, lp, C.c_int]
         R.ref_min_lengths.argtypes = [C.c_uint64, C.c_uint64, u64p]
@@ -394,6 +396,18 @@ def ref_conv_shards(c, m, kappa, c_out, img, filt, s):
                         0, s, _ptr(out_slots, dp), _ptr(out_img, dp), _ptr(ledger, u64p), C.byref(drop))
     assert rc == 0
     return out_slots.reshape(n_out, s), out_img, ledger, drop.value
+
+
+def ref_conv_biased(c, m, kappa, c_out, img, filt, plan, s, bias, output_scale, cap=64):
+    """conv_plan / convolve with bias and output_scale (conv.hpp:46-68): output slots [n_out][s]."""
+    out = np.zeros(cap * s)
+    ledger = np.zeros(9, dtype=np.uint64)
+    n = ref().ref_conv_biased(c, m, kappa, c_out, _ptr(np.ascontiguousarray(img), dp),
+                              _ptr(np.ascontiguousarray(filt), dp), plan, s,
+                              _ptr(np.ascontiguousarray(bias, dtype=np.float64), dp), float(output_scale),
+                              _ptr(out, dp), cap, _ptr(ledger, u64p))
+    assert n > 0
+    return out[: n * s].reshape(n, s), ledger
 
 
 # ---------------------------------------------------------------- CKKS model

@@ -128,6 +128,38 @@ int ref_conv(int c, int m, int kappa, int c_out, const double* img, const double
     }
 }
 
+/// conv with bias and output_scale (conv.hpp:46-68): plan 1 / 2 = conv_plan
+/// (ChannelFirst / ShiftFirst), 0 = convolve (image shards or channel shards,
+/// chosen from the packing as the reference does). out_slots receives every
+/// output shard's slots in order ([n_out][s]); returns the shard count (or -1).
+int ref_conv_biased(int c, int m, int kappa, int c_out, const double* img, const double* filt, int plan,
+                    uint64_t shard_size, const double* bias, double output_scale, double* out_slots, int cap_shards,
+                    uint64_t* ledger) {
+    try {
+        ImageTensor t(c, m);
+        std::memcpy(t.data.data(), img, t.data.size() * sizeof(double));
+        FilterTensor k(c, c_out, kappa);
+        std::memcpy(k.weights.data(), filt, k.weights.size() * sizeof(double));
+        std::vector<double> b(bias, bias + c_out);
+        Engine eng;
+        PackedImage p = pack(eng, t, shard_size);
+        eng.ledger().reset();
+        PackedImage out = plan == 1   ? conv_plan(eng, p, k, ConvPlan::ChannelFirst, b, output_scale)
+                          : plan == 2 ? conv_plan(eng, p, k, ConvPlan::ShiftFirst, b, output_scale)
+                                      : convolve(eng, p, k, b, output_scale);
+        if (static_cast<int>(out.shards.size()) > cap_shards) return -1;
+        size_t off = 0;
+        for (const auto& sh : out.shards) {
+            std::memcpy(out_slots + off, sh.slots.data(), sh.slots.size() * sizeof(double));
+            off += sh.slots.size();
+        }
+        if (ledger) fill_ledger(eng.ledger(), ledger);
+        return static_cast<int>(out.shards.size());
+    } catch (...) {
+        return -1;
+    }
+}
+
 /// Textbook same-padding conv (reference oracle.cpp:7-31).
 int ref_oracle_conv(int c, int m, int kappa, int c_out, const double* img, const double* filt,
                     int stride, double* out) {

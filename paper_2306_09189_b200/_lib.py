@@ -80,7 +80,7 @@ SIGNATURES = [
     ("fhe_rescale", C.c_int, [vp, vp, vpp]),
     ("fhe_rotate_decomposed", C.c_int, [vp, vp, C.c_int64, C.c_int, vpp]),
     ("fhe_decompose", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, i64p, C.c_int]),
-    ("fhe_conv_layer_create", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_int, vpp]),
+    ("fhe_conv_layer_create", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_double, C.c_int, vpp]),
     ("fhe_conv_layer_free", None, [vp]),
     ("fhe_conv_layer_steps", C.c_int, [vp, C.c_int, i64p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("fhe_conv2d", C.c_int, [vp, vp, vp, C.c_int, vpp]),
@@ -88,7 +88,8 @@ SIGNATURES = [
     ("fhe_conv2d_batch", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, vp, C.c_int, vpp]),
     ("fhe_conv2d_batch_into", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, vp, C.c_int, C.POINTER(C.c_void_p)]),
     ("fhe_conv2d_batch_host", C.c_int, [vp, u64p, C.c_size_t, C.c_double, vp, C.c_int, C.c_size_t, u64p]),
-    ("fhe_conv_layer_create_shards", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_int, vpp]),
+    ("fhe_conv_layer_create_shards", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_double, C.c_int,
+                                               vpp]),
     ("fhe_conv_layer_shards", C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("fhe_slot_sum_batch", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, C.c_uint64, vpp]),
     ("fhe_gen_relin_key", C.c_int, [vp]),
@@ -105,8 +106,8 @@ SIGNATURES = [
                                  C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("fhe_linear_features", C.c_int, [vp, C.POINTER(C.c_void_p), C.c_size_t, i64p, C.c_size_t, C.c_int, dp, dp,
                                       vpp]),
-    ("fhe_conv_layer_create_packed", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_int, C.c_size_t,
-                                               i64p, C.c_int, C.c_int, vpp]),
+    ("fhe_conv_layer_create_packed", C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, C.c_double,
+                                               C.c_int, C.c_size_t, i64p, C.c_int, C.c_int, vpp]),
     ("fhe_conv_layer_output_packing", C.c_int, [vp, C.POINTER(C.c_int)]),
     ("fhe_execute_schedule", C.c_int, [vp, vp, i64p, C.POINTER(C.c_int), C.c_size_t, C.c_int, vpp,
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -93,6 +93,7 @@ struct fhe_ctx {
         std::vector<const void*> key;
         cudaGraphExec_t exec = nullptr;
         fhe_ledger delta{};
+        std::vector<uint64_t> amounts;  // rotation amounts the captured conv records
         uint64_t launches = 0;
         uint64_t last_use = 0;
     };
@@ -187,7 +188,11 @@ struct fhe_ctx {
         if (m < 0) m += s;
         return (uint64_t)m;
     }
-    void note_amount(uint64_t a) { amounts.insert(a); }
+    std::vector<uint64_t>* amount_rec = nullptr;  // amounts noted while a graph is captured
+    void note_amount(uint64_t a) {
+        amounts.insert(a);
+        if (amount_rec) amount_rec->push_back(a);
+    }
     const uint64_t* key_for(uint32_t g) const {
         auto it = keys.find(g);
         if (it == keys.end()) fail(FHE_E_NOKEY, "missing Galois key for rotation");
@@ -250,6 +255,13 @@ struct fhe_conv_layer {
     std::vector<int64_t> tau;
     std::vector<uint8_t> ms_nonempty;  // [n_out][kappa][nb_ms]
     uint64_t* d_pts_ms = nullptr;
+    // bias (ImageConv::bias_plain conv.cpp:87-94, conv_channel_shards :344): one
+    // slot vector per output shard (bias[out_channel] * output_scale per block),
+    // encoded lazily at level - 1 and the input scale, added in the epilogue of
+    // the final fused ModDown + rescale
+    std::vector<std::vector<double>> bias_vecs;
+    uint64_t* d_bias = nullptr;  // [n_out][level][N]
+    double d_bias_scale = 0;
 };
 
 namespace {
@@ -340,7 +352,8 @@ void rotate_from_digits(fhe_ctx* c, const fhe_ct* ct, const uint64_t* digits, ui
 // polynomial instead of 28: the rescale's INTT of row q_l is
 // taken from the coefficient-domain ModDown of that row, and
 //   out_i = (acc_i - NTT(conv_i + P spread_i(c_l))) (P q_l)^-1.
-void moddown_rescale(fhe_ctx* c, const uint64_t* acc, size_t acc_stride, int level, int npoly, uint64_t* out) {
+void moddown_rescale(fhe_ctx* c, const uint64_t* acc, size_t acc_stride, int level, int npoly, uint64_t* out,
+                     const uint64_t* bias = nullptr, int bias_mod = 1) {
     const size_t N = c->N;
     const int K = c->K;
     uint64_t* pc = c->alloc((size_t)npoly * (K + 1) * N);  // [npoly][K] special rows, then [npoly] q_l rows
@@ -356,8 +369,9 @@ void moddown_rescale(fhe_ctx* c, const uint64_t* acc, size_t acc_stride, int lev
     });
     c->timed("ntt_moddown", c->rows((double)npoly * (K + 1 + 3.0 * level)), [&] {
         ntt_moddown_rescale(c->dc, w, pc, qlc, acc, acc_stride, out, c->d_md, c->d_pqlinv + (size_t)level * c->L,
-                            c->d_pqlinv_sh + (size_t)level * c->L, level, npoly, c->st);
+                            c->d_pqlinv_sh + (size_t)level * c->L, level, npoly, c->st, bias, bias_mod);
     });
+    if (bias) c->ledger.adds += npoly / 2;  // the bias add_plain of every output (conv.cpp:207)
     c->release(pc);
     c->release(w);
     c->ledger.moddowns += npoly;
@@ -412,6 +426,14 @@ void gen_key(fhe_ctx* c, uint32_t g) {
     c->release(e);
     c->release(erows);
     c->keys[g] = key;
+}
+
+// destroy every captured conv graph (they embed key / plaintext device addresses)
+void drop_graphs(fhe_ctx* c) {
+    if (c->graphs.empty()) return;
+    ck(cudaStreamSynchronize(c->main_st), "sync");
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
 }
 
 void upload_tables(fhe_ctx* c) {
@@ -628,6 +650,53 @@ void encode_rows(fhe_ctx* c, const double* z, size_t n, int level, double scale,
 
 // Ledger replay of the reference schedule (conv.cpp:119-210) so the
 // operation-count laws (test_conv.cpp:244-276) hold for the CKKS path too.
+// Bias slot vectors of a layer, one per output shard: ImageConv::bias_plain
+// (conv.cpp:87-94: bias[out_channel(v, b)] * scale over block b) for image
+// mode, the constant bias[g] * scale of conv_channel_shards (conv.cpp:344) for
+// output shard (g, v) of a channel-shard layer.
+void set_bias(fhe_ctx* c, fhe_conv_layer* ly, const double* bias, double osc) {
+    ly->bias_vecs.clear();
+    if (!bias) return;
+    const size_t s = c->slots(), block = (size_t)ly->m * ly->m;
+    if (ly->cs) {
+        for (int o = 0; o < ly->n_out; ++o) ly->bias_vecs.emplace_back(s, bias[o / ly->pc] * osc);
+        return;
+    }
+    const size_t z = s / block;
+    const int nout = ly->ms ? ly->n_out : 1;
+    for (int v = 0; v < nout; ++v) {
+        std::vector<double> plain(s, 0.0);
+        for (size_t b = 0; b < z; ++b) {
+            const double val = bias[((size_t)v * z + b) % (size_t)ly->c_out] * osc;
+            std::fill_n(plain.begin() + (long)(b * block), block, val);
+        }
+        ly->bias_vecs.push_back(std::move(plain));
+    }
+}
+
+// device bias rows [n_out][level][N] at level - 1 and `scale` (the conv output's
+// scale); re-encoded in place when the scale changes, so captured graphs that
+// read them stay valid. Host encoding synchronises: never call inside a capture.
+void ensure_bias(fhe_ctx* c, const fhe_conv_layer* cly, double scale) {
+    fhe_conv_layer* ly = const_cast<fhe_conv_layer*>(cly);
+    if (ly->bias_vecs.empty() || (ly->d_bias && ly->d_bias_scale == scale)) return;
+    const int rows = ly->level;
+    const size_t rw = (size_t)rows * c->N;
+    if (!ly->d_bias) ck(cudaMalloc(&ly->d_bias, ly->bias_vecs.size() * rw * 8), "cudaMalloc");
+    for (size_t i = 0; i < ly->bias_vecs.size(); ++i)
+        encode_rows(c, ly->bias_vecs[i].data(), c->slots(), ly->level - 1, scale, rows, ly->d_bias + i * rw);
+    ck(cudaStreamSynchronize(c->st), "sync");
+    ly->d_bias_scale = scale;
+}
+
+// the scale every input of a biased conv call shares (the bias is encoded at it)
+void prepare_bias(fhe_ctx* c, const fhe_conv_layer* ly, const fhe_ct* const* cts, size_t n) {
+    if (ly->bias_vecs.empty() || n == 0) return;
+    for (size_t i = 1; i < n; ++i)
+        if (cts[i]->scale != cts[0]->scale) fail(FHE_E_INVALID, "biased conv: inputs at different scales");
+    ensure_bias(c, ly, cts[0]->scale);
+}
+
 void ledger_conv(fhe_ctx* c, const fhe_conv_layer* ly, int approach) {
     fhe_ledger& lg = c->ledger;
     const long m = ly->m, h = ly->kappa / 2;
@@ -936,7 +1005,7 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
     }
     if (id >= 0) qp_add(c->dc, acc, Y + (size_t)id * 2 * extw, level, c->st);
     uint64_t* md = nullptr;
-    moddown_rescale(c, acc, extw, level, 2, out->d);
+    moddown_rescale(c, acc, extw, level, 2, out->d, ly->d_bias, 1);
     out->scale = (ct->scale * (double)c->primes[level]) / (double)c->primes[level];
     out->depth = ct->depth + 1;
     c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, out->depth);
@@ -968,13 +1037,17 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
 // accumulator (ModDown(Y.c1) in the coefficient domain feeding a batched
 // ModUp), the identity giant `id` is added as is; md = [S][2][level][N].
 void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, const std::vector<int>& giants,
-                   const std::vector<int64_t>& gamt, int id, uint64_t* md) {
+                   const std::vector<int64_t>& gamt, int id, uint64_t* md, const uint64_t* bias = nullptr,
+                   int bias_mod = 1) {
     const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
     const size_t N = c->N, extw = (size_t)ne * N, dw = (size_t)dn * extw;
     uint64_t* acc = c->alloc((size_t)S * 2 * extw);
     ck(cudaMemsetAsync(acc, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
-    const int G = (int)giants.size();
-    if (G > 0) {
+    const int GT = (int)giants.size();
+    // giants in chunks of at most kMaxBaby (the KsBatch term capacity); every
+    // chunk accumulates into the same QP accumulators
+    for (int gb = 0; gb < GT; gb += kMaxBaby) {
+        const int G = std::min(kMaxBaby, GT - gb);
         const int SC = std::max(1, std::min(S, 8));
         uint64_t* yc = c->alloc((size_t)SC * G * extw);
         uint64_t* yq = c->alloc((size_t)SC * G * nr * N);
@@ -984,8 +1057,8 @@ void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, c
             for (int s = 0; s < sc; ++s)
                 for (int gi = 0; gi < G; ++gi)
                     ck(cudaMemcpyAsync(yc + ((size_t)s * G + gi) * extw,
-                                       Y + (size_t)(s0 + s) * ys + (size_t)giants[gi] * 2 * extw + extw, extw * 8,
-                                       cudaMemcpyDeviceToDevice, c->st),
+                                       Y + (size_t)(s0 + s) * ys + (size_t)giants[gb + gi] * 2 * extw + extw,
+                                       extw * 8, cudaMemcpyDeviceToDevice, c->st),
                        "memcpy");
             const int np_ = sc * G;
             c->timed("ntt", c->rows(2.0 * np_ * ne),
@@ -1009,10 +1082,10 @@ void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, c
             kg.out = acc + (size_t)s0 * 2 * extw;
             kg.out_src_stride = 2 * extw;
             for (int gi = 0; gi < G; ++gi) {
-                const uint32_t g = c->galois_of(c->reduce_amount(gamt[giants[gi]]));
+                const uint32_t g = c->galois_of(c->reduce_amount(gamt[giants[gb + gi]]));
                 kg.galois[gi] = g;
                 kg.key[gi] = c->key_for(g);
-                kg.c0_off[gi] = (size_t)giants[gi] * 2 * extw;
+                kg.c0_off[gi] = (size_t)giants[gb + gi] * 2 * extw;
             }
             c->ledger.key_switches += (uint64_t)G * sc;
             c->timed("ks_inner", c->rows((double)G * 2.0 * dn * ne + (double)sc * G * (dn * ne + ne) + 4.0 * ne * sc),
@@ -1025,7 +1098,7 @@ void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, c
     if (id >= 0)
         for (int s = 0; s < S; ++s)
             qp_add(c->dc, acc + (size_t)s * 2 * extw, Y + (size_t)s * ys + (size_t)id * 2 * extw, level, c->st);
-    moddown_rescale(c, acc, extw, level, 2 * S, md);
+    moddown_rescale(c, acc, extw, level, 2 * S, md, bias, bias_mod);
     c->release(acc);
 }
 
@@ -1118,7 +1191,7 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
     }
     const size_t otw = (size_t)2 * level * N;
     uint64_t* md = c->alloc((size_t)S * otw);
-    giants_finish(c, Y, ys, S, level, giants, B.gamt, id, md);
+    giants_finish(c, Y, ys, S, level, giants, B.gamt, id, md, ly->d_bias, 1);
     for (int s = 0; s < S; ++s) {
         ck(cudaMemcpyAsync(outs[s]->d, md + (size_t)s * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
         outs[s]->scale = (cts[s]->scale * (double)c->primes[level]) / (double)c->primes[level];
@@ -1266,7 +1339,7 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
     c->release(dig);
     const size_t otw = (size_t)2 * level * N;
     uint64_t* md = c->alloc((size_t)S * otw);
-    moddown_rescale(c, acc, extw, level, 2 * S, md);
+    moddown_rescale(c, acc, extw, level, 2 * S, md, ly->d_bias, 1);
     for (int s = 0; s < S; ++s) {
         ck(cudaMemcpyAsync(outs[s]->d, md + (size_t)s * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
         outs[s]->scale = (cts[s]->scale * (double)c->primes[level]) / (double)c->primes[level];
@@ -1367,7 +1440,7 @@ void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
     }
     const size_t otw = (size_t)2 * level * N;
     uint64_t* md = c->alloc((size_t)B * NO * otw);
-    giants_finish(c, Y, ys, B * NO, level, giants, gamt, id, md);
+    giants_finish(c, Y, ys, B * NO, level, giants, gamt, id, md, ly->d_bias, NO);
     for (int i = 0; i < B * NO; ++i) {
         ck(cudaMemcpyAsync(outs[i]->d, md + (size_t)i * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
         const fhe_ct* src = in[(i / NO) * T];
@@ -1482,7 +1555,7 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
     uint64_t* md = c->alloc((size_t)B * NOUT * otw);
     c->ledger.hoist_groups += (uint64_t)B * NSH;
     c->ledger.rotations += (uint64_t)B * NOUT * giants.size();
-    giants_finish(c, Y, ys, B * NOUT, level, giants, gamt, id, md);
+    giants_finish(c, Y, ys, B * NOUT, level, giants, gamt, id, md, ly->d_bias, NOUT);
     for (int i = 0; i < B * NOUT; ++i) {
         ck(cudaMemcpyAsync(outs[i]->d, md + (size_t)i * otw, otw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
         const fhe_ct* src = in[(i / NOUT) * NSH];
@@ -1719,7 +1792,7 @@ void conv_impl(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
             }
     }
     // one ModDown per component, then one rescale
-    moddown_rescale(c, acc, extw, level, 2, out->d);
+    moddown_rescale(c, acc, extw, level, 2, out->d, ly->d_bias, 1);
     out->scale = (ct->scale * (double)c->primes[level]) / (double)c->primes[level];
     out->depth = ct->depth + 1;
     c->ledger.max_depth_consumed = std::max<uint64_t>(c->ledger.max_depth_consumed, out->depth);
@@ -1739,9 +1812,11 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
     const bool paper_batch = (approach == 1 || approach == 2) && n > 1 && c->batch5;
     const bool bsgs_batch = approach >= 3 && n > 1 && (c->fused_batch || (approach == 5 && c->batch5));
     if (paper_batch || bsgs_batch || n == 1) {
-        if (cts[0]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
-        for (size_t s = 0; s < n; ++s)
+        for (size_t s = 0; s < n; ++s) {
+            if (cts[s]->level != ly->level) fail(FHE_E_INVALID, "conv layer was encoded for a different level");
             if (outs[s]->level != ly->level - 1) fail(FHE_E_INVALID, "output level must be input level - 1");
+        }
+        prepare_bias(c, ly, cts, n);
         auto body = [&] {
             if (n == 1) {
                 conv_impl(c, cts[0], ly, approach, outs[0]);
@@ -1770,6 +1845,7 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
             const uint64_t* del = reinterpret_cast<const uint64_t*>(&g.delta);
             for (size_t f = 0; f < sizeof(fhe_ledger) / sizeof(uint64_t); ++f) dst[f] += del[f];
             note_launch((int)g.launches);
+            for (uint64_t a : g.amounts) c->amounts.insert(a);
             for (size_t s = 0; s < n; ++s) {
                 outs[s]->scale = (cts[s]->scale * (double)c->primes[ly->level]) / (double)c->primes[ly->level];
                 outs[s]->depth = cts[s]->depth + 1;
@@ -1787,17 +1863,24 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
         const fhe_ledger before = c->ledger;
         const uint64_t l0 = launches_total();
         cudaGraph_t graph = nullptr;
+        std::vector<uint64_t> rec;
         ck(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        c->amount_rec = &rec;
         try {
             body();
         } catch (...) {
+            c->amount_rec = nullptr;
             cudaStreamEndCapture(c->st, &graph);
             if (graph) cudaGraphDestroy(graph);
             throw;
         }
+        c->amount_rec = nullptr;
         ck(cudaStreamEndCapture(c->st, &graph), "cudaStreamEndCapture");
         fhe_ctx::GraphEntry g;
         g.key = key;
+        std::sort(rec.begin(), rec.end());
+        rec.erase(std::unique(rec.begin(), rec.end()), rec.end());
+        g.amounts = std::move(rec);
         ck(cudaGraphInstantiate(&g.exec, graph, 0), "cudaGraphInstantiate");
         cudaGraphDestroy(graph);
         g.launches = launches_total() - l0;
@@ -1822,6 +1905,7 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
         return;
     }
     if (approach >= 3) ensure_bsgs(c, ly, approach);  // layer constants are built on the main stream
+    prepare_bias(c, ly, cts, n);
     if (n == 1 || c->lanes.size() <= 1) {
         for (size_t i = 0; i < n; ++i) conv_impl(c, cts[i], ly, approach, outs[i]);
         return;
@@ -1871,6 +1955,10 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
         if (p->log_n < 12 || p->log_n > 16) fail(FHE_E_INVALID, "log_n must be in [12, 16]");
         if (p->n_q < 1 || p->n_p < 1 || p->n_p > kMaxAlpha || p->n_q + p->n_p > kMaxPrimes)
             fail(FHE_E_INVALID, "unsupported prime counts");
+        // the keyed kernels are instantiated for 1..8 digits (and the carry-deferred
+        // inner product is exact for at most 8 terms)
+        if ((p->n_q + p->n_p - 1) / p->n_p > 8)
+            fail(FHE_E_INVALID, "unsupported prime counts: dnum = ceil(n_q / n_p) must be <= 8");
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
             fail(FHE_E_CUDA, "no CUDA device available (libfheconv has no CPU fallback)");
@@ -1908,7 +1996,7 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
         bits.insert(bits.end(), p->p_bits, p->p_bits + p->n_p);
         c->primes = host::generate_primes(bits, (uint64_t)c->N);
         c->scale = std::ldexp(1.0, p->log_scale);
-        if (const char* e = std::getenv("FHECONV_GIANT_CHUNK")) c->giant_chunk = std::max(1, std::atoi(e));
+        if (const char* e = std::getenv("FHECONV_GIANT_CHUNK")) c->giant_chunk = std::max(1, std::min(kMaxBaby, std::atoi(e)));
         upload_tables(c);
     });
     if (rc != FHE_OK) {
@@ -2080,6 +2168,8 @@ int fhe_keygen(fhe_ctx* c, uint64_t seed) {
     return guard(c, [&] {
         const size_t N = c->N;
         if (!c->d_s) ck(cudaMalloc(&c->d_s, (size_t)c->np * N * 8), "cudaMalloc");
+        // captured graphs hold the device addresses of the keys released below
+        drop_graphs(c);
         for (auto& kv : c->keys) c->release(kv.second);
         c->keys.clear();
         int64_t* s = (int64_t*)c->alloc(N);
@@ -2618,9 +2708,21 @@ int fhe_rescale(fhe_ctx* c, const fhe_ct* ct, fhe_ct** out) {
     });
 }
 
-int fhe_conv_layer_create(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights, int level,
-                          fhe_conv_layer** out) {
+// weights * output_scale, as ImageConv folds its scale into every fused plaintext
+// (conv.cpp:74: k.centered(...) * scale -- the same double product)
+static std::vector<double> scaled_weights(int c_in, int c_out, int kappa, const double* w, double osc) {
+    if (!w) fail(FHE_E_INVALID, "null weights");
+    std::vector<double> v(w, w + (size_t)c_in * c_out * kappa * kappa);
+    for (double& x : v) x = x * osc;
+    return v;
+}
+
+int fhe_conv_layer_create(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights_in,
+                          const double* bias, double output_scale, int level, fhe_conv_layer** out) {
     return guard(c, [&] {
+        if (!out) fail(FHE_E_INVALID, "null output");
+        const std::vector<double> wsc = scaled_weights(c_in, c_out, kappa, weights_in, output_scale);
+        const double* weights = wsc.data();
         if (kappa % 2 == 0) fail(FHE_E_INVALID, "kernel size must be odd");
         if (c_out <= 0 || (c_out & (c_out - 1))) fail(FHE_E_INVALID, "output channel count must be a power of two");
         const size_t s = c->slots(), block = (size_t)m * m;
@@ -2655,6 +2757,7 @@ int fhe_conv_layer_create(fhe_ctx* c, int c_in, int c_out, int m, int kappa, con
                                 ly->d_pts + ((size_t)r * ly->nk + i) * ne * c->N);
                 }
         }
+        set_bias(c, ly, bias, output_scale);
         ck(cudaStreamSynchronize(c->st), "sync");
         *out = ly;
     });
@@ -2674,6 +2777,7 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
     }
     cudaFree(ly->d_pts);
     if (ly->d_pts_ms) cudaFree(ly->d_pts_ms);
+    if (ly->d_bias) cudaFree(ly->d_bias);
     for (auto& b : ly->bs)
         if (b.d_pts) cudaFree(b.d_pts);
     delete ly;
@@ -2682,9 +2786,12 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
 static fhe_conv_layer* create_packed_layer(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights,
                                            int level, int T, const int64_t* tau, int rep, int d);
 
-int fhe_conv_layer_create_shards(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights, int level,
-                                 fhe_conv_layer** out) {
+int fhe_conv_layer_create_shards(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights_in,
+                                 const double* bias, double output_scale, int level, fhe_conv_layer** out) {
     return guard(c, [&] {
+        if (!out) fail(FHE_E_INVALID, "null output");
+        const std::vector<double> wsc = scaled_weights(c_in, c_out, kappa, weights_in, output_scale);
+        const double* weights = wsc.data();
         if (kappa % 2 == 0) fail(FHE_E_INVALID, "kernel size must be odd");
         if (c_out <= 0 || (c_out & (c_out - 1))) fail(FHE_E_INVALID, "output channel count must be a power of two");
         if (c_in <= 0 || (c_in & (c_in - 1))) fail(FHE_E_INVALID, "channel count must be a power of two");
@@ -2731,6 +2838,7 @@ int fhe_conv_layer_create_shards(fhe_ctx* c, int c_in, int c_out, int m, int kap
                                 for (size_t j = 0; j < s2; ++j) rot[j] = mask[(j + s2 - gsh) % s2];  // rot_{-kk m}
                                 encode_rows(c, rot.data(), s2, level, pscale, ne, ly->d_pts_ms + idx * extw);
                             }
+            set_bias(c, ly, bias, output_scale);
             ck(cudaStreamSynchronize(c->st), "sync");
             *out = ly;
             return;
@@ -2739,6 +2847,7 @@ int fhe_conv_layer_create_shards(fhe_ctx* c, int c_in, int c_out, int m, int kap
             fail(FHE_E_INVALID, "multi-shard convolution needs c_in m^2 >= slots (no duplication)");
         *out = create_packed_layer(c, c_in, c_out, m, kappa, weights, level, (int)((size_t)c_in * block / s), nullptr,
                                    1, 1);
+        set_bias(c, *out, bias, output_scale);
     });
 }
 
@@ -2807,11 +2916,14 @@ static fhe_conv_layer* create_packed_layer(fhe_ctx* c, int c_in, int c_out, int 
     return ly;
 }
 
-int fhe_conv_layer_create_packed(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights, int level,
-                                 size_t t, const int64_t* tau, int rep, int d, fhe_conv_layer** out) {
+int fhe_conv_layer_create_packed(fhe_ctx* c, int c_in, int c_out, int m, int kappa, const double* weights,
+                                 const double* bias, double output_scale, int level, size_t t, const int64_t* tau,
+                                 int rep, int d, fhe_conv_layer** out) {
     return guard(c, [&] {
         if (!out) fail(FHE_E_INVALID, "null output");
-        *out = create_packed_layer(c, c_in, c_out, m, kappa, weights, level, (int)t, tau, rep, d);
+        const std::vector<double> wsc = scaled_weights(c_in, c_out, kappa, weights, output_scale);
+        *out = create_packed_layer(c, c_in, c_out, m, kappa, wsc.data(), level, (int)t, tau, rep, d);
+        set_bias(c, *out, bias, output_scale);
     });
 }
 
@@ -2833,6 +2945,7 @@ int fhe_conv2d_shards_into(fhe_ctx* c, const fhe_ct* const* in, size_t n_images,
                            fhe_ct* const* outs) {
     return guard(c, [&] {
         if (!ly || !ly->ms) fail(FHE_E_INVALID, "layer was not created by fhe_conv_layer_create_shards");
+        prepare_bias(c, ly, in, n_images * (size_t)ly->t);
         for (size_t i0 = 0; i0 < n_images; i0 += 8) {
             const int B = (int)std::min<size_t>(8, n_images - i0);
             if (ly->cs)

@@ -5,6 +5,8 @@
 // bit-reversed evaluation order, so every Galois automorphism maps aligned
 // 2^b blocks to aligned 2^b blocks and the permuted gathers below stay
 // inside 256-byte segments.
+#include <stdexcept>
+
 #include "kernels.cuh"
 
 #ifndef FHE_FUSED_UNROLL2  // fused kernel: two baby steps per loop iteration (constant stage offsets)
@@ -1105,7 +1107,7 @@ __global__ void k_qp_add(DevCtx c, uint64_t* acc, const uint64_t* y, int level) 
         case 6: CALL(6); break;    \
         case 7: CALL(7); break;    \
         case 8: CALL(8); break;    \
-        default: break;            \
+        default: throw std::invalid_argument("unsupported digit count (dnum must be <= 8)"); \
     }
 
 // CTA caps of the HBM-streaming kernels (per SM). Smaller grids leave SM room

@@ -106,6 +106,11 @@ struct NttFuse {
     uint64_t* const* outp;  // optional: poly pp written to outp[pp / 2] + (pp % 2) [level+1][N] (ciphertexts)
     const uint64_t* add_src;
     uint32_t galois;
+    // add_mod > 0: add_src is added (unpermuted) to EVERY even poly pp (the c0 of
+    // output ciphertext pp / 2), from add_src + ((pp / 2) % add_mod) * add_stride
+    // (the conv bias plaintexts of the output shards)
+    int add_mod;
+    size_t add_stride;
     // fused ModDown+rescale: output multiplier (P q_l)^-1 per row instead of P^-1
     const uint64_t* outmul;
     const uint64_t* outmul_sh;
@@ -189,9 +194,12 @@ void ks_inner_product(const DevCtx& c, const uint64_t* digits, const uint64_t* k
 void gather_row(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t stride, int npoly, cudaStream_t st);
 // fused ModDown + rescale (fheconv.cu moddown_rescale): pcoef = INTT'd special rows
 // [npoly][K][N], qlc = INTT'd q_l rows [npoly][N], w scratch [npoly][level][N]
+// bias (optional): [bias_mod][level][N] plaintext rows added to the c0 of output i from
+// bias + (i % bias_mod) * level * N
 void ntt_moddown_rescale(const DevCtx& c, uint64_t* w, const uint64_t* pcoef, const uint64_t* qlc, const uint64_t* acc,
                          size_t acc_stride, uint64_t* out, const ModDownTable* md, const uint64_t* pqlinv,
-                         const uint64_t* pqlinv_sh, int level, int npoly, cudaStream_t st);
+                         const uint64_t* pqlinv_sh, int level, int npoly, cudaStream_t st,
+                         const uint64_t* bias = nullptr, int bias_mod = 1);
 void gather_special(const DevCtx& c, uint64_t* dst, const uint64_t* acc, size_t acc_stride, int level, int npoly,
                     cudaStream_t st);
 

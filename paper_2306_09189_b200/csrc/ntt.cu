@@ -310,15 +310,26 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
                             (size_t)blk0 * B;
             const uint64_t pi = fz.outmul ? fz.outmul[u] : fz.md->pinvq[u];
             const uint64_t pis = fz.outmul ? fz.outmul_sh[u] : fz.md->pinvq_sh[u];
-            const bool add = fz.add_src && pp == 0;
+            const bool add = fz.add_src && (fz.add_mod > 0 ? (pp & 1) == 0 : pp == 0);
             uint64_t av[EPT], sv[EPT];
+            if (fz.add_mod > 0) {  // conv bias of output pp / 2 (unpermuted rows)
+                const uint64_t* bsrc =
+                    fz.add_src + (size_t)((pp >> 1) % fz.add_mod) * fz.add_stride + (size_t)u * c.N + (size_t)blk0 * B;
 #pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-                const int i = threadIdx.x + e * NTT_THREADS;
-                av[e] = __ldcs(acc + i);
-                sv[e] = add ? __ldg(fz.add_src + (size_t)u * c.N +
-                                    perm_index_n((uint32_t)(blk0 * B + i), fz.galois, c.logN))
-                            : 0;
+                for (int e = 0; e < EPT; ++e) {
+                    const int i = threadIdx.x + e * NTT_THREADS;
+                    av[e] = __ldcs(acc + i);
+                    sv[e] = add ? __ldg(bsrc + i) : 0;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < EPT; ++e) {
+                    const int i = threadIdx.x + e * NTT_THREADS;
+                    av[e] = __ldcs(acc + i);
+                    sv[e] = add ? __ldg(fz.add_src + (size_t)u * c.N +
+                                        perm_index_n((uint32_t)(blk0 * B + i), fz.galois, c.logN))
+                                : 0;
+                }
             }
 #pragma unroll
             for (int e = 0; e < EPT; ++e) {
@@ -710,8 +721,12 @@ void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const u
 
 void ntt_moddown_rescale(const DevCtx& c, uint64_t* w, const uint64_t* pcoef, const uint64_t* qlc, const uint64_t* acc,
                          size_t acc_stride, uint64_t* out, const ModDownTable* md, const uint64_t* pqlinv,
-                         const uint64_t* pqlinv_sh, int level, int npoly, cudaStream_t st) {
+                         const uint64_t* pqlinv_sh, int level, int npoly, cudaStream_t st, const uint64_t* bias,
+                         int bias_mod) {
     NttFuse fz{};
+    fz.add_src = bias;
+    fz.add_mod = bias ? bias_mod : 0;
+    fz.add_stride = (size_t)level * c.N;
     fz.md = md;
     fz.acc = acc;
     fz.acc_stride = acc_stride;

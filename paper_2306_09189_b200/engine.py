@@ -288,24 +288,38 @@ class Context:
         return self._new(lib().fhe_rescale, ct.h)
 
     # ---------------------------------------------------------------- conv
-    def conv_layer(self, c_in: int, c_out: int, m: int, kappa: int, weights, level: int | None = None) -> ConvLayer:
+    @staticmethod
+    def _bias(bias, c_out: int):
+        """bias array (or None) for the C ABI; the reference's size check (conv.cpp:113-114)."""
+        if bias is None or len(bias) == 0:
+            return None, None
+        b = np.ascontiguousarray(bias, dtype=np.float64)
+        if b.size != c_out:
+            raise ValueError("bias size does not match output channels")
+        return b, b.ctypes.data_as(_lib.dp)
+
+    def conv_layer(self, c_in: int, c_out: int, m: int, kappa: int, weights, level: int | None = None,
+                   bias=None, output_scale: float = 1.0) -> ConvLayer:
+        """fhe_conv_layer_create: conv_plan's layer (conv.hpp:66-68) with optional bias and output_scale."""
         w = np.ascontiguousarray(weights, dtype=np.float64)
         assert w.size == c_in * c_out * kappa * kappa
         level = self.max_level if level is None else level
+        b, bp = self._bias(bias, c_out)
         out = C.c_void_p()
-        self._check(lib().fhe_conv_layer_create(self.h, c_in, c_out, m, kappa, w.ctypes.data_as(_lib.dp), level,
-                                                C.byref(out)))
+        self._check(lib().fhe_conv_layer_create(self.h, c_in, c_out, m, kappa, w.ctypes.data_as(_lib.dp), bp,
+                                                float(output_scale), level, C.byref(out)))
         return ConvLayer(self, out.value, c_in, c_out, m, kappa, level)
 
     def conv_layer_shards(self, c_in: int, c_out: int, m: int, kappa: int, weights,
-                          level: int | None = None) -> ConvLayer:
+                          level: int | None = None, bias=None, output_scale: float = 1.0) -> ConvLayer:
         """fhe_conv_layer_create_shards: multi-shard image-mode layer (c_in m^2 = t * slots)."""
         w = np.ascontiguousarray(weights, dtype=np.float64)
         assert w.size == c_in * c_out * kappa * kappa
         level = self.max_level if level is None else level
+        b, bp = self._bias(bias, c_out)
         out = C.c_void_p()
         self._check(lib().fhe_conv_layer_create_shards(self.h, c_in, c_out, m, kappa, w.ctypes.data_as(_lib.dp),
-                                                       level, C.byref(out)))
+                                                       bp, float(output_scale), level, C.byref(out)))
         ly = ConvLayer(self, out.value, c_in, c_out, m, kappa, level)
         t, no = C.c_int(0), C.c_int(0)
         self._check(lib().fhe_conv_layer_shards(ly.h, C.byref(t), C.byref(no)))
@@ -404,15 +418,18 @@ class Context:
                          w.size // len(b), len(b), w.ctypes.data_as(_lib.dp), b.ctypes.data_as(_lib.dp))
 
     def conv_layer_packed(self, c_in: int, c_out: int, m: int, kappa: int, weights, t: int = 1, tau=None,
-                          rep: int = 1, d: int = 1, level: int | None = None) -> ConvLayer:
+                          rep: int = 1, d: int = 1, level: int | None = None, bias=None,
+                          output_scale: float = 1.0) -> ConvLayer:
         """fhe_conv_layer_create_packed: image-mode layer over any PackedImage (tau, rep, d)."""
         w = np.ascontiguousarray(weights, dtype=np.float64)
         assert w.size == c_in * c_out * kappa * kappa
         level = self.max_level if level is None else level
+        b, bp = self._bias(bias, c_out)
         tv = None if tau is None else np.ascontiguousarray(tau, dtype=np.int64)
         out = C.c_void_p()
         self._check(lib().fhe_conv_layer_create_packed(self.h, c_in, c_out, m, kappa, w.ctypes.data_as(_lib.dp),
-                                                       level, t, None if tv is None else tv.ctypes.data_as(_lib.i64p),
+                                                       bp, float(output_scale), level, t,
+                                                       None if tv is None else tv.ctypes.data_as(_lib.i64p),
                                                        rep, d, C.byref(out)))
         ly = ConvLayer(self, out.value, c_in, c_out, m, kappa, level)
         tt, no, dd = C.c_int(0), C.c_int(0), C.c_int(0)

@@ -458,42 +458,33 @@ def run_network(ctx: Context, spec: NetworkSpec, x: ImageTensor, enc_seed: int =
 
 def _conv(ctx: Context, keys: _Keys, p: PackedCiphertexts, k: FilterTensor, bias: np.ndarray,
           scale: float, cache: Optional[dict] = None, idx: int = -1) -> PackedCiphertexts:
-    """convolve (conv.cpp:364-371) with the folded output scale and the bias (conv.cpp:87-94, :344)"""
-    s = ctx.slots
+    """convolve (conv.cpp:364-371) with the folded output scale and the bias (conv.cpp:87-94, :344):
+    both are properties of the libfheconv layer (fhe_conv_layer_create_*: the scale folded into the
+    fused plaintexts, the bias added in the conv epilogue)"""
     if k.c_in != p.c:
         raise ValueError("filter input channels do not match image")
     if bias.size and bias.size != k.c_out:
         raise ValueError("bias size does not match output channels")
-    w = k.weights * scale
+    b = bias if bias.size else None
     lv = p.min_level()
     ck = (idx, p.mode, len(p.shards), tuple(int(v) for v in p.tau), p.rep, p.d, lv, scale)
     layer = cache.get(ck) if cache is not None else None
     if p.mode == 1:
         if layer is None:
-            layer = ctx.conv_layer_shards(k.c_in, k.c_out, p.m, k.kappa, w, level=lv)
+            layer = ctx.conv_layer_shards(k.c_in, k.c_out, p.m, k.kappa, k.weights, level=lv, bias=b,
+                                          output_scale=scale)
         if cache is not None:
             cache[ck] = layer
         keys.need(layer.steps())
         outs = ctx.conv2d_shards(p.shards, layer)
-        pc = p.m * p.m // s
-        if bias.size:
-            outs = [ctx.add_scalar(o, bias[u // pc] * scale) for u, o in enumerate(outs)]
         return PackedCiphertexts(outs, p.m, k.c_out, np.arange(k.c_out), 1, 1, 1)
     if layer is None:
-        layer = ctx.conv_layer_packed(k.c_in, k.c_out, p.m, k.kappa, w, t=len(p.shards), tau=p.tau, rep=p.rep,
-                                      d=p.d, level=lv)
+        layer = ctx.conv_layer_packed(k.c_in, k.c_out, p.m, k.kappa, k.weights, t=len(p.shards), tau=p.tau,
+                                      rep=p.rep, d=p.d, level=lv, bias=b, output_scale=scale)
     if cache is not None:
         cache[ck] = layer
     keys.need(layer.steps())
     outs = ctx.conv2d_shards(p.shards, layer)
-    if bias.size:
-        block = p.m * p.m
-        z = s // block
-        res = []
-        for v, o in enumerate(outs):
-            vec = np.repeat(np.array([bias[(v * z + b) % k.c_out] * scale for b in range(z)]), block)
-            res.append(ctx.add_plain(o, ctx.encode(vec, level=o.level, scale=o.scale)))
-        outs = res
     return PackedCiphertexts(outs, p.m, k.c_out, np.arange(k.c_out), 1, layer.d_out, 0)
 
 

@@ -43,6 +43,30 @@ int main() {
             auto y = eng.decrypt(out);
             for (size_t i = 0; i < ref.size(); ++i) worst = std::fmax(worst, std::fabs(y[i] - ref[i]));
         }
+        // conv_plan with the reference's argument list (conv.hpp:66-68): bias and output_scale,
+        // every B200 schedule; the layer is cached across calls
+        {
+            const std::vector<double> bias = {0.25, -0.5, 0.125, 0.0};
+            const double osc = 0.5;
+            for (auto plan : {fheconv::ConvPlan::ShiftFirst, fheconv::ConvPlan::Fused, fheconv::ConvPlan::Auto,
+                              fheconv::ConvPlan::BabyGiant}) {
+                auto out = eng.conv_plan(ct, c, c, m, k, w, plan, bias, osc);
+                auto y = eng.decrypt(out);
+                for (size_t i = 0; i < ref.size(); ++i)
+                    worst = std::fmax(worst, std::fabs(y[i] - (ref[i] + bias[i / (m * m)]) * osc));
+            }
+            std::vector<const fheconv::Ciphertext*> batch = {&ct, &ct};
+            auto outs = eng.conv_batch(batch, layer, fheconv::ConvPlan::Fused);
+            auto y = eng.decrypt(outs[1]);
+            for (size_t i = 0; i < ref.size(); ++i) worst = std::fmax(worst, std::fabs(y[i] - ref[i]));
+            bool bad_bias = false;
+            try {
+                eng.make_conv_layer(c, c, m, k, w, eng.max_level(), {1.0, 2.0});
+            } catch (const std::invalid_argument& e) {
+                bad_bias = std::string(e.what()) == "bias size does not match output channels";
+            }
+            if (!bad_bias) return 5;
+        }
         // Engine::rotate_many / rotate / mul_plain semantics
         auto rots = eng.rotate_many(ct, {1, -1});
         auto r1 = eng.decrypt(rots[0]);

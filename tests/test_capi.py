@@ -73,3 +73,12 @@ def test_cxx_wrapper_compiles():
                     "-L", os.path.join(ROOT, "paper_2306_09189_b200"), "-lfheconv",
                     f"-Wl,-rpath,{os.path.join(ROOT, 'paper_2306_09189_b200')}"], check=True)
     assert os.path.exists(out)
+
+
+def test_context_rejects_more_than_eight_digits(product_lib):
+    """dnum = ceil(n_q / n_p) > 8 has no keyed-kernel instantiation: rejected up front
+    (before any device work), never silently skipped."""
+    from paper_2306_09189_b200 import Context, FheError
+    with pytest.raises(FheError) as e:
+        Context(log_n=13, q_bits=[50] * 9, p_bits=[60], log_scale=40)
+    assert e.value.code == -1 and "dnum" in str(e.value)

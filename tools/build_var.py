@@ -1,4 +1,4 @@
-"""Build a variant libfheconv.so with extra -D flags into scratch/var/<name>/ (kernels.cu only differs)."""
+"""Build a variant libfheconv.so with extra -D flags into tools/var/<name>/ (kernels.cu only differs)."""
 import os, subprocess, sys
 sys.path.insert(0, ".")
 from paper_2306_09189_b200 import build as B
