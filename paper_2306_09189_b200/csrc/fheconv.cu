@@ -3006,6 +3006,8 @@ int fhe_conv2d_into(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int 
 int fhe_conv2d(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int approach, fhe_ct** out) {
     return guard(c, [&] {
         if (ct->level < 1) fail(FHE_E_RUNTIME, "depth exhausted");
+        if (!ly) fail(FHE_E_INVALID, "null layer");
+        prepare_bias(c, ly, &ct, 1);
         fhe_ct* o = new_ct(c, ct->level - 1, ct->scale, ct->depth + 1);
         try {
             conv_impl(c, ct, ly, approach, o);

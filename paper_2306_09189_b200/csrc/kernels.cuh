@@ -25,6 +25,7 @@ struct RowMap {
     int L;
     int skip_alpha;
     int skip_dn;  // digits per source when several ModUps are batched (0: one source)
+    int limb;     // forward NTT: store the output rows in limb form (modarith.cuh)
 };
 
 FHE_HD int row_prime(const RowMap& m, int u) { return u <= m.level ? u : m.L + (u - m.level - 1); }
@@ -106,6 +107,7 @@ struct NttFuse {
     uint64_t* const* outp;  // optional: poly pp written to outp[pp / 2] + (pp % 2) [level+1][N] (ciphertexts)
     const uint64_t* add_src;
     uint32_t galois;
+    int limb;  // ModUp: digit rows in limb form (own rows copied from c1 converted here)
     // add_mod > 0: add_src is added (unpermuted) to EVERY even poly pp (the c0 of
     // output ciphertext pp / 2), from add_src + ((pp / 2) % add_mod) * add_stride
     // (the conv bias plaintexts of the output shards)
@@ -124,9 +126,9 @@ void note_launch(int n);
 // All launchers enqueue on `st` and never synchronise.
 void ntt_forward(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);
 void ntt_inverse(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, cudaStream_t st);
-// ModUp FastBConv fused into the forward NTT: digits = [nsrc][dn][ne][N]
+// ModUp FastBConv fused into the forward NTT: digits = [nsrc][dn][ne][N] (limb != 0: limb form)
 void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const uint64_t* c1, size_t c1_stride,
-               int nsrc, const ModUpDigit* tables, int level, int dn, cudaStream_t st);
+               int nsrc, const ModUpDigit* tables, int level, int dn, cudaStream_t st, int limb = 0);
 // ModUp of nsrc coefficient-domain sources coef = [nsrc][level+1][N]: every
 // digit row (own rows included) = conversion of coef, then the forward NTT
 void ntt_modup_coef(const DevCtx& c, uint64_t* digits, const uint64_t* coef, int nsrc, const ModUpDigit* tables,
@@ -281,6 +283,18 @@ struct FusedBsgs {
     int accumulate;                  // Y_g += (instead of =)
 };
 void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, int dn, cudaStream_t st);
+// The same baby steps on limb-form operands (k_bsgs_limb): a.key[b] and
+// a.pt[b] in limb form, a.digits the limb-form ModUp digits, a.ct the limb-form P-scaled
+// ciphertexts [P c]_q ([2][level+1][N] per source, ct_prescale). Same Y (normal form,
+// bit-identical). No source slots / accumulation, ng <= kFusedMaxG.
+void bsgs_limb(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st);
+// dst[i] = to_limb(src[i]) for nrows rows of N words; row r uses prime
+// row_prime(rm, r % rm.rows_per_poly) (rm.level < 0: prime index r % rows_per_poly)
+void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,
+                  cudaStream_t st);
+// dst[s][p][u] = to_limb([P ct_s[p][u]]_{q_u}) for nsrc ciphertexts at ct + s * stride ([2][level+1][N])
+void ct_prescale(const DevCtx& c, uint64_t* dst, const uint64_t* ct, size_t stride, int nsrc, const ModDownTable* md,
+                 int level, cudaStream_t st);
 // acc += y over [2][ne][N] (QP basis)
 void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st);
 

@@ -177,6 +177,21 @@ FHE_HD U128 fold3(const Acc3& A) {
     return U128{lo, hi};
 }
 
+// ------------------------------------------------------------------ limb form
+// A residue v < q < 2^60 in limb form is the word (v >> W) << 32 | (v mod 2^W) with
+// W = 25 when q < 2^50 and W = 30 otherwise: its two 32-bit halves
+// feed mad.wide.u32 directly, so sums of limb products need no carry handling
+// (k_bsgs_limb). Used only for operands of the fused baby-step kernel.
+FHE_HD int limb_w(uint64_t q) { return q < (1ULL << 50) ? 25 : 30; }
+FHE_HD uint64_t to_limb(uint64_t v, int w) { return ((v >> w) << 32) | (v & ((1ULL << w) - 1)); }
+FHE_HD uint64_t from_limb(uint64_t l, int w) { return ((l >> 32) << w) | (l & 0xffffffffULL); }
+#ifdef __CUDACC__
+// acc += a b (one IMAD.WIDE.U32 with a 64-bit addend)
+__device__ __forceinline__ void madw(uint64_t& acc, uint32_t a, uint32_t b) {
+    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+}
+#endif
+
 // ------------------------------------------------------------------ PRNG
 // Counter-based SplitMix64 hash. Deterministic on host and
 // device; benchmark-grade, NOT a cryptographic PRNG.

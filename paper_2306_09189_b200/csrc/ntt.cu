@@ -347,7 +347,8 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
                 const int i = threadIdx.x + e * NTT_THREADS;
                 uint64_t x = sm[(i / B) * PB + pad(i % B)];
                 x = x >= q2 ? x - q2 : x;
-                a[i] = x >= q ? x - q : x;
+                x = x >= q ? x - q : x;
+                a[i] = rm.limb ? to_limb(x, limb_w(q)) : x;
             }
         }
     } else {
@@ -420,8 +421,12 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
                 n1 += v1[a] > (q >> 1);
                 // own row of the digit: NTT-domain copy of c1, or (coefficient-domain
                 // sources, c1 == nullptr) the coefficients themselves, transformed later
-                *reinterpret_cast<ulonglong2*>(out + (size_t)qi * c.N) =
-                    c1 ? __ldcs(reinterpret_cast<const ulonglong2*>(c1 + (size_t)qi * c.N + k)) : x;
+                ulonglong2 own = c1 ? __ldcs(reinterpret_cast<const ulonglong2*>(c1 + (size_t)qi * c.N + k)) : x;
+                if (fz.limb && c1) {
+                    const int w = limb_w(q);
+                    own = make_ulonglong2(to_limb(own.x, w), to_limb(own.y, w));
+                }
+                *reinterpret_cast<ulonglong2*>(out + (size_t)qi * c.N) = own;
             }
         }
         const uint64_t* tj = tab + (size_t)j * ne * W;
@@ -602,9 +607,10 @@ void ntt_inverse(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, c
 }
 
 void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const uint64_t* c1, size_t c1_stride,
-               int nsrc, const ModUpDigit* tables, int level, int dn, cudaStream_t st) {
+               int nsrc, const ModUpDigit* tables, int level, int dn, cudaStream_t st, int limb) {
     const int ne = level + 1 + c.K;
     NttFuse fz{};
+    fz.limb = limb;
     fz.coef = coef;
     fz.c1 = c1;
     fz.c1_stride = c1_stride;
@@ -621,7 +627,7 @@ void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const ui
         }
         note_launch(1);
     }
-    ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, c.K, dn}, false, FUSE_NONE, fz, st);
+    ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, c.K, dn, limb}, false, FUSE_NONE, fz, st);
 }
 
 // coefficient-domain ModDown (one thread per coefficient pair and q row)
