@@ -60,6 +60,8 @@ struct fhe_ctx {
     } hp;
     bool fused_batch = false;        // FHECONV_BATCH_FUSED=1: batched kernels instead of lanes
     bool batch5 = true;              // approach 5: sources batched through one fused launch (FHECONV_BATCH5=0: lanes)
+    bool limb = true;                // approach 5 baby steps on limb-form operands (k_bsgs_limb; FHECONV_LIMB=0: k_bsgs_fused)
+    bool tma = false;                // limb baby steps TMA-staged (k_bsgs_tma; FHECONV_TMA=1)
     int logN = 0, N = 0, L = 0, K = 0, alpha = 0, dnum = 0, np = 0;
     std::vector<uint64_t> primes;
     double scale = 0;
@@ -75,6 +77,7 @@ struct fhe_ctx {
     bool have_key = false;
     uint64_t key_seed = 0;
     std::map<uint32_t, uint64_t*> keys;
+    std::map<uint32_t, uint64_t*> limb_keys;  // limb-form copies of the fused baby-step keys (cudaMalloc)
     fhe_ledger ledger{};
     uint64_t launch_base = 0;
     int giant_chunk = 8;  // giant steps per ModUp batch (FHECONV_GIANT_CHUNK)
@@ -241,6 +244,7 @@ struct fhe_conv_layer {
         std::vector<int64_t> bamt, gamt;
         std::vector<int> nonempty;  // [ngi][nb]
         uint64_t* d_pts = nullptr;  // [ngi][nb][ne][N], pt'[g][b] = rot_{-g}(pt)
+        uint64_t* d_pts_limb = nullptr;  // the same in limb form (approach 5, k_bsgs_limb)
     } bs[3];
     // multi-shard image mode (fhe_conv_layer_create_shards): t input shards of z
     // channels, n_out output shards; fused-BSGS plaintexts
@@ -294,7 +298,8 @@ fhe_ct* new_ct(fhe_ctx* c, int level, double scale, int depth) {
 // ------------------------------------------------------------ primitives
 
 // digits [nsrc][dn][ne][N] of nsrc polynomials c1 + s * stride (level+1 rows each, NTT)
-void modup_batch(fhe_ctx* c, const uint64_t* c1, size_t stride, int nsrc, int level, uint64_t* digits) {
+// (limb != 0: digit rows in limb form, modarith.cuh, for k_bsgs_limb)
+void modup_batch(fhe_ctx* c, const uint64_t* c1, size_t stride, int nsrc, int level, uint64_t* digits, int limb = 0) {
     const int nr = level + 1, dn = c->dn_at(level), ne = c->ne_at(level);
     const size_t rowsw = (size_t)nr * c->N;
     uint64_t* coef = c->alloc((size_t)nsrc * rowsw);
@@ -303,7 +308,7 @@ void modup_batch(fhe_ctx* c, const uint64_t* c1, size_t stride, int nsrc, int le
     c->timed("ntt", c->rows(2.0 * nsrc * nr), [&] { ntt_inverse(c->dc, coef, nsrc * nr, qmap(c, level), c->st); });
     (void)ne;
     c->timed("ntt_modup", c->rows(2.0 * nsrc * nr + (double)nsrc * dn * ne), [&] {
-        ntt_modup(c->dc, digits, coef, c1, stride, nsrc, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+        ntt_modup(c->dc, digits, coef, c1, stride, nsrc, c->d_modup + (size_t)level * c->dnum, level, dn, c->st, limb);
     });
     c->release(coef);
     c->ledger.modups += nsrc;
@@ -812,12 +817,54 @@ fhe_conv_layer::Bsgs& ensure_bsgs(fhe_ctx* c, const fhe_conv_layer* cly, int ori
     return B;
 }
 
+// Limb-form operands of the fused baby steps (k_bsgs_limb): a copy of
+// the layer's rotated plaintexts and of every baby-step key in limb form. Built once
+// (host-synchronising, so batch_impl calls it before a graph capture); keygen drops
+// the key copies with the keys.
+bool limb_ok(const fhe_ctx* c, const fhe_conv_layer::Bsgs& B) { return c->limb && B.nb <= kMaxFused; }
+
+void prepare_limb(fhe_ctx* c, const fhe_conv_layer* ly, int orient) {
+    if (orient != 5) return;
+    fhe_conv_layer::Bsgs& B = ensure_bsgs(c, ly, orient);
+    if (!limb_ok(c, B)) return;
+    bool dirty = false;
+    const int ne = c->ne_at(ly->level);
+    if (!B.d_pts_limb) {
+        const size_t rows = (size_t)B.ngi * B.nb * ne;
+        ck(cudaMalloc(&B.d_pts_limb, rows * c->N * 8), "cudaMalloc");
+        rows_to_limb(c->dc, B.d_pts_limb, B.d_pts, rows, RowMap{ne, ly->level, c->L, 0}, c->st);
+        dirty = true;
+    }
+    for (int64_t amt : B.bamt) {
+        const uint32_t g = c->galois_of(c->reduce_amount(amt));
+        if (g == 1 || c->limb_keys.count(g)) continue;
+        const uint64_t* key = c->key_for(g);
+        const size_t rows = (size_t)c->dnum * 2 * c->np;
+        uint64_t* d = nullptr;
+        ck(cudaMalloc(&d, rows * c->N * 8), "cudaMalloc");
+        rows_to_limb(c->dc, d, key, rows, RowMap{c->np, -1, c->L, 0}, c->st);
+        c->limb_keys[g] = d;
+        dirty = true;
+    }
+    if (dirty) ck(cudaStreamSynchronize(c->st), "limb operands");
+}
+
+void free_limb_keys(fhe_ctx* c) {
+    if (c->limb_keys.empty()) return;
+    ck(cudaStreamSynchronize(c->main_st), "sync");
+    for (auto& kv : c->limb_keys) cudaFree(kv.second);
+    c->limb_keys.clear();
+}
+
 // Baby steps of the fused BSGS schedule for nsrc sources: Y_g(s) for every
 // giant g (chunks of kFusedMaxG giants per launch), X~_b never materialised.
+// limb: digits are limb-form ModUp digits and cts the limb-form P-scaled
+// ciphertexts (ct_prescale); keys and plaintexts come from prepare_limb.
 void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const uint64_t* digits, size_t dstride,
-                  const uint64_t* cts, size_t ctstride, int nsrc, uint64_t* Y, size_t ystride) {
+                  const uint64_t* cts, size_t ctstride, int nsrc, uint64_t* Y, size_t ystride, bool limb = false) {
     const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
     const size_t extw = (size_t)ne * c->N;
+    if (limb && !(limb_ok(c, B) && B.d_pts_limb)) fail(FHE_E_RUNTIME, "limb operands not prepared");
     FusedBsgs f{};
     f.nsrc = nsrc;
     f.digits = digits;
@@ -863,9 +910,9 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
                     if (B.nonempty[(size_t)(g0 + g) * B.nb + b]) mask |= 1u << g;
                 const uint32_t gal = c->galois_of(c->reduce_amount(B.bamt[b]));
                 f.galois[f.nb] = gal;
-                f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+                f.key[f.nb] = gal == 1 ? nullptr : limb ? c->limb_keys.at(gal) : c->key_for(gal);
                 f.gmask[f.nb] = mask;
-                f.pt[f.nb] = B.d_pts + ((size_t)g0 * B.nb + b) * extw;
+                f.pt[f.nb] = (limb ? B.d_pts_limb : B.d_pts) + ((size_t)g0 * B.nb + b) * extw;
                 f.srcslot[f.nb] = 0;
                 pt_words += __builtin_popcount(mask);
                 if (gal != 1) keyed += 1;
@@ -874,7 +921,14 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
             c->timed("bsgs_fused",
                      c->rows(keyed * 2.0 * dn * ne + pt_words * ne +
                              nsrc * ((double)dn * ne + 2.0 * nr + (f.accumulate ? 4.0 : 2.0) * ng * ne)),
-                     [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+                     [&] {
+                         if (limb && c->tma)
+                             bsgs_tma(c->dc, f, level, dn, c->st);
+                         else if (limb)
+                             bsgs_limb(c->dc, f, level, dn, c->st);
+                         else
+                             bsgs_fused(c->dc, f, c->d_md, level, dn, c->st);
+                     });
         }
     }
 }
@@ -887,8 +941,17 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
     uint64_t* Y = c->alloc((size_t)B.ngi * 2 * extw);
     const bool fused = orient == 5;
     uint64_t* XT = fused ? nullptr : c->alloc((size_t)B.nb * 2 * extw);
-    modup(c, ct->c1(), level, dsrc);
-    if (fused) fused_babies(c, B, level, dsrc, 0, ct->d, 0, 1, Y, 0);
+    prepare_limb(c, ly, orient);
+    const bool limb = fused && limb_ok(c, B);
+    modup_batch(c, ct->c1(), 0, 1, level, dsrc, limb);
+    if (limb) {
+        uint64_t* pc = c->alloc((size_t)2 * nr * N);
+        ct_prescale(c->dc, pc, ct->d, 0, 1, c->d_md, level, c->st);
+        fused_babies(c, B, level, dsrc, 0, pc, 0, 1, Y, 0, true);
+        c->release(pc);
+    } else if (fused) {
+        fused_babies(c, B, level, dsrc, 0, ct->d, 0, 1, Y, 0);
+    }
     // baby steps: the hoisted key switches of the source, then the plaintext mat-vec
     BabyTerms t{};
     t.nb = B.nb;
@@ -1118,13 +1181,20 @@ void conv_bsgs_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_conv
     for (int s = 0; s < S; ++s)
         ck(cudaMemcpyAsync(buf + (size_t)s * ctw, cts[s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
     uint64_t* dsrc = c->alloc((size_t)S * dw);
-    modup_batch(c, buf + (size_t)nr * N, ctw, S, level, dsrc);
+    const bool fused = orient == 5;
+    prepare_limb(c, ly, orient);
+    const bool limb = fused && limb_ok(c, B);
+    modup_batch(c, buf + (size_t)nr * N, ctw, S, level, dsrc, limb);
     // baby steps
     const size_t xts = (size_t)B.nb * 2 * extw, ys = (size_t)B.ngi * 2 * extw;
-    const bool fused = orient == 5;
     uint64_t* Y = c->alloc((size_t)S * ys);
     uint64_t* XT = fused ? nullptr : c->alloc((size_t)S * xts);
-    if (fused) fused_babies(c, B, level, dsrc, dw, buf, ctw, S, Y, ys);
+    if (limb) {  // the P-scaled ciphertexts in limb form replace buf for the baby steps
+        ct_prescale(c->dc, buf, buf, ctw, S, c->d_md, level, c->st);
+        fused_babies(c, B, level, dsrc, dw, buf, ctw, S, Y, ys, true);
+    } else if (fused) {
+        fused_babies(c, B, level, dsrc, dw, buf, ctw, S, Y, ys);
+    }
     BabyTerms t{};
     t.nb = B.nb;
     t.nb_total = B.nb;
@@ -1833,6 +1903,7 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
             return;
         }
         if (approach >= 3) ensure_bsgs(c, ly, approach);  // host encoding + sync: never inside a capture
+        prepare_limb(c, ly, approach);
         std::vector<const void*> key{(const void*)(uintptr_t)ly->uid, (const void*)(uintptr_t)approach,
                                      (const void*)(uintptr_t)n};
         for (size_t s = 0; s < n; ++s) {
@@ -1905,6 +1976,7 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
         return;
     }
     if (approach >= 3) ensure_bsgs(c, ly, approach);  // layer constants are built on the main stream
+    prepare_limb(c, ly, approach);
     prepare_bias(c, ly, cts, n);
     if (n == 1 || c->lanes.size() <= 1) {
         for (size_t i = 0; i < n; ++i) conv_impl(c, cts[i], ly, approach, outs[i]);
@@ -1980,6 +2052,8 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
         }
         if (const char* e = std::getenv("FHECONV_BATCH_FUSED")) c->fused_batch = std::atoi(e) != 0;
         if (const char* e = std::getenv("FHECONV_BATCH5")) c->batch5 = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FHECONV_LIMB")) c->limb = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FHECONV_TMA")) c->tma = std::atoi(e) != 0;
         if (const char* e = std::getenv("FHECONV_GRAPHS")) c->use_graphs = std::atoi(e) != 0;
         cudaMemPool_t pool;
         ck(cudaDeviceGetDefaultMemPool(&pool, c->device), "mempool");
@@ -2015,6 +2089,7 @@ void fhe_ctx_destroy(fhe_ctx* c) {
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto& kv : c->keys) cudaFreeAsync(kv.second, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
+    for (auto& kv : c->limb_keys) cudaFree(kv.second);
     void* bufs[] = {c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv, c->d_ninv_sh,
                     c->d_modup, c->d_md, c->d_qlinv, c->d_qlinv_sh, c->d_pqlinv, c->d_pqlinv_sh, c->d_s};
     for (void* b : bufs)
@@ -2170,6 +2245,7 @@ int fhe_keygen(fhe_ctx* c, uint64_t seed) {
         if (!c->d_s) ck(cudaMalloc(&c->d_s, (size_t)c->np * N * 8), "cudaMalloc");
         // captured graphs hold the device addresses of the keys released below
         drop_graphs(c);
+        free_limb_keys(c);
         for (auto& kv : c->keys) c->release(kv.second);
         c->keys.clear();
         int64_t* s = (int64_t*)c->alloc(N);
@@ -2778,8 +2854,10 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
     cudaFree(ly->d_pts);
     if (ly->d_pts_ms) cudaFree(ly->d_pts_ms);
     if (ly->d_bias) cudaFree(ly->d_bias);
-    for (auto& b : ly->bs)
+    for (auto& b : ly->bs) {
         if (b.d_pts) cudaFree(b.d_pts);
+        if (b.d_pts_limb) cudaFree(b.d_pts_limb);
+    }
     delete ly;
 }
 

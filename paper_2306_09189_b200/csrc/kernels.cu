@@ -1218,6 +1218,290 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_limb(DevCtx c, FusedBsgs a, 
     }
 }
 
+// ------------------------------------------------------------ TMA-staged limb baby steps
+// k_bsgs_tma: the limb-form baby steps of k_bsgs_limb with the staging moved off the
+// compute threads. A CTA owns one aligned block of 32 coefficients of one extended
+// row and SG sources (thread = (coefficient, source): warp w = source w, lane =
+// coefficient; ONE coefficient per thread, so the accumulators take half the
+// registers and more warps are resident). Per baby step every operand row segment
+// is one 256-byte bulk copy (cp.async.bulk, completing on the stage's mbarrier)
+// issued by a few lanes: 2 DN key rows + the fed plaintext rows (shared by the SG
+// sources) and per source DN digit blocks + its c0 block. The Galois automorphism
+// maps an aligned 32-block of the bit-reversed NTT order onto an aligned 32-block,
+// so a source block is copied whole and the permutation is applied on the shared
+// read (lane -> pidx & 31, a bijection: conflict-free). NST stages in flight.
+constexpr int kTmaBlk = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int DN, int NG, int SG>
+struct TmaLayout {
+    static constexpr int B = kTmaBlk;
+    static constexpr int KW = 2 * DN * B;    // keys      [2 DN][B]
+    static constexpr int PW = NG * B;        // plaintexts [NG][B]
+    static constexpr int DW = SG * DN * B;   // digits    [SG][DN][B]
+    static constexpr int CW = SG * B;        // c0        [SG][B]
+    static constexpr int STAGE = KW + PW + DW + CW;  // words
+};
+
+template <int DN, int NG, int SG, int NST, int MINB>
+__global__ void __launch_bounds__(32 * SG, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, int level) {
+    using LY = TmaLayout<DN, NG, SG>;
+    constexpr int B = kTmaBlk;
+    extern __shared__ __align__(128) uint64_t tsm[];  // [NST][STAGE] words, then NST mbarriers
+    uint64_t* const bars = tsm + (size_t)NST * LY::STAGE;
+    const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
+    const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const size_t total = (size_t)ne * c.N;
+    const size_t chunks = total / B;
+    const int ngroups = (a.nsrc + SG - 1) / SG;
+    const size_t items = chunks * (size_t)ngroups;
+    const size_t keyrow = (size_t)np * c.N;
+    const uint32_t nmask = (2u << c.logN) - 1;
+    RowMap rm{ne, level, c.L, 0};
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < NST; ++st) mbar_init(bars + st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;  // bit st: parity of the next completion of stage st
+    for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const size_t chunk = it / (size_t)ngroups;
+        const int g0src = (int)(it % (size_t)ngroups) * SG;
+        const int s = g0src + sl;
+        const bool active = s < a.nsrc;
+        const int nact = min(SG, a.nsrc - g0src);
+        const size_t i0 = chunk * B;
+        const int u = (int)(i0 >> c.logN);
+        const uint32_t k0 = (uint32_t)(i0 & (size_t)(c.N - 1)), k = k0 + lane;
+        const int pi = row_prime(rm, u);
+        const Prime pr = c.primes[pi];
+        const bool qrow = u < nr;
+        const uint32_t e = 2 * brev_n(k, c.logN) + 1, e0 = 2 * brev_n(k0, c.logN) + 1;
+        auto pidx = [&](uint32_t ee, uint32_t g) { return brev_n((((ee * g) & nmask) - 1) >> 1, c.logN); };
+        // stage fill of baby b (warp-cooperative: lanes issue the copies of their warp's
+        // share; thread 0 arms the barrier with the stage's total bytes)
+        auto issue = [&](int b, int st) {
+            if (b >= a.nb) return;
+            uint64_t* sb = tsm + (size_t)st * LY::STAGE;
+            uint64_t* bar = bars + st;
+            const uint64_t* key = a.key[b];
+            const uint32_t gm = a.gmask[b];
+            const uint32_t blk = pidx(e0, a.galois[b]) & ~(uint32_t)(B - 1);
+            if (threadIdx.x == 0) {
+                uint32_t bytes = (uint32_t)__popc(gm & ((1u << NG) - 1)) * B * 8;
+                if (key) bytes += (2 * DN + nact * DN + (qrow ? nact : 0)) * B * 8;
+                else if (qrow) bytes += 2 * nact * B * 8;
+                mbar_expect_tx(bar, bytes);
+            }
+            if (sl == 0) {  // shared rows: keys, plaintexts
+                if (key && lane < 2 * DN)
+                    bulk_g2s(sb + lane * B, key + (size_t)lane * keyrow + (size_t)pi * c.N + k0, B * 8, bar);
+                if (lane >= 16 && lane < 16 + NG && ((gm >> (lane - 16)) & 1u))
+                    bulk_g2s(sb + LY::KW + (lane - 16) * B,
+                             a.pt[b] + (size_t)(lane - 16) * a.pt_g_stride + (size_t)u * c.N + k0, B * 8, bar);
+            }
+            if (active) {
+                const uint64_t* C0 = a.ct + (size_t)s * a.ct_src_stride + (size_t)u * c.N;
+                uint64_t* sd = sb + LY::KW + LY::PW + sl * DN * B;
+                uint64_t* sc = sb + LY::KW + LY::PW + LY::DW + sl * B;
+                if (key) {
+                    if (lane < DN)
+                        bulk_g2s(sd + lane * B,
+                                 a.digits + (size_t)s * a.digit_src_stride + (size_t)lane * total + (size_t)u * c.N + blk,
+                                 B * 8, bar);
+                    else if (lane == DN && qrow)
+                        bulk_g2s(sc, C0 + blk, B * 8, bar);
+                } else if (qrow) {  // identity baby: [P c1], [P c0] unpermuted
+                    if (lane == 0) bulk_g2s(sd, C0 + (size_t)nr * c.N + k0, B * 8, bar);
+                    if (lane == 1) bulk_g2s(sc, C0 + k0, B * 8, bar);
+                }
+            }
+        };
+        auto run = [&](auto wtag) {
+            constexpr int W = decltype(wtag)::value;
+            constexpr uint32_t MW = LimbConst<W>::M;
+            const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> W);
+            const uint32_t qinv = (uint32_t)pr.qinv & MW;
+            uint64_t b0[W == 25 ? NG : 1][2], b1[W == 25 ? NG : 1][2], b2[W == 25 ? NG : 1][2];
+            U128 y[W == 30 ? NG : 1][2];
+#pragma unroll
+            for (int g = 0; g < (W == 25 ? NG : 1); ++g)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) b0[g][q2] = b1[g][q2] = b2[g][q2] = 0;
+#pragma unroll
+            for (int g = 0; g < (W == 30 ? NG : 1); ++g)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) y[g][q2] = U128{0, 0};
+#pragma unroll
+            for (int b = 0; b < NST - 1; ++b) issue(b, b);
+            int st = 0;
+            for (int b = 0; b < a.nb; ++b) {
+                mbar_wait(bars + st, (phase >> st) & 1u);
+                phase ^= 1u << st;
+                const uint64_t* sb = tsm + (size_t)st * LY::STAGE;
+                const uint32_t pk = pidx(e, a.galois[b]) & (B - 1);
+                uint64_t x[2];
+                if (a.key[b]) {
+                    const uint64_t* sd = sb + LY::KW + LY::PW + sl * DN * B + pk;
+                    uint64_t z0[2] = {0, 0}, z1[2] = {0, 0}, z2[2] = {0, 0};
+#pragma unroll
+                    for (int j = 0; j < DN; ++j) {
+                        const uint64_t dw = sd[j * B];
+                        const uint64_t kw[2] = {sb[(2 * j) * B + lane], sb[(2 * j + 1) * B + lane]};
+                        const uint32_t d0 = lo32(dw), d1 = hi32(dw);
+                        if constexpr (W == 25) {
+                            const uint32_t ds = d0 + d1;
+#pragma unroll
+                            for (int q2 = 0; q2 < 2; ++q2) {
+                                const uint32_t kk0 = lo32(kw[q2]), kk1 = hi32(kw[q2]);
+                                madw(z0[q2], d0, kk0);
+                                madw(z2[q2], d1, kk1);
+                                madw(z1[q2], ds, kk0 + kk1);
+                            }
+                        } else {
+#pragma unroll
+                            for (int q2 = 0; q2 < 2; ++q2) {
+                                const uint32_t kk0 = lo32(kw[q2]), kk1 = hi32(kw[q2]);
+                                madw(z0[q2], d0, kk0);
+                                madw(z1[q2], d0, kk1);
+                                madw(z1[q2], d1, kk0);
+                                madw(z2[q2], d1, kk1);
+                            }
+                        }
+                    }
+                    if constexpr (W == 25) {
+#pragma unroll
+                        for (int q2 = 0; q2 < 2; ++q2) z1[q2] -= z0[q2] + z2[q2];
+                    } else if constexpr (DN >= 8) {
+#pragma unroll
+                        for (int q2 = 0; q2 < 2; ++q2) {
+                            z2[q2] += z1[q2] >> W;
+                            z1[q2] &= MW;
+                        }
+                    }
+                    if (qrow) {  // + [P sigma(c0)]_q in limb form
+                        const uint64_t cw = sb[LY::KW + LY::PW + LY::DW + sl * B + pk];
+                        z0[0] += lo32(cw);
+                        z1[0] += hi32(cw);
+                    }
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2)
+                        x[q2] = W == 25 ? mont_l25(z0[q2], z1[q2], z2[q2], q0, q1, qinv)
+                                        : mont_l30(z0[q2], z1[q2], z2[q2], q0, q1, qinv);
+                } else if (qrow) {  // identity: X = [P c]_q
+                    const uint64_t cw[2] = {sb[LY::KW + LY::PW + LY::DW + sl * B + lane],
+                                            sb[LY::KW + LY::PW + sl * DN * B + lane]};
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2)
+                        x[q2] = W == 25 ? mont_l25(lo32(cw[q2]), hi32(cw[q2]), 0, q0, q1, qinv)
+                                        : mont_l30(lo32(cw[q2]), hi32(cw[q2]), 0, q0, q1, qinv);
+                } else {
+                    x[0] = x[1] = 0;
+                }
+                const uint32_t gm = a.gmask[b];
+                if constexpr (W == 25) {
+                    uint32_t xl[2], xh[2], xs[2];
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2) {
+                        xl[q2] = (uint32_t)x[q2] & MW;
+                        xh[q2] = (uint32_t)(x[q2] >> 25);
+                        xs[q2] = xl[q2] + xh[q2];
+                    }
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        if (!((gm >> g) & 1u)) continue;
+                        const uint64_t ww = sb[LY::KW + g * B + lane];
+                        const uint32_t w0 = lo32(ww), w1 = hi32(ww), ws = w0 + w1;
+#pragma unroll
+                        for (int q2 = 0; q2 < 2; ++q2) {
+                            madw(b0[g][q2], w0, xl[q2]);
+                            madw(b2[g][q2], w1, xh[q2]);
+                            madw(b1[g][q2], ws, xs[q2]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        if (!((gm >> g) & 1u)) continue;
+                        const uint64_t wa = from_limb(sb[LY::KW + g * B + lane], 30);
+                        mac_small(y[g][0], wa, x[0]);
+                        mac_small(y[g][1], wa, x[1]);
+                    }
+                    if ((b & 31) == 31) {
+#pragma unroll
+                        for (int g = 0; g < NG; ++g)
+#pragma unroll
+                            for (int q2 = 0; q2 < 2; ++q2) y[g][q2] = U128{reduce128(y[g][q2].hi, y[g][q2].lo, pr), 0};
+                    }
+                }
+                __syncthreads();  // every thread is done with stage st: refill it
+                const int nst = st == 0 ? NST - 1 : st - 1;  // (b + NST - 1) % NST
+                issue(b + NST - 1, nst);
+                st = st == NST - 1 ? 0 : st + 1;
+            }
+            if (active) {
+                uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
+                uint64_t r = reduce64(W == 25 ? (1ULL << 50) : (1ULL << 45), pr);
+                if (W == 30) r = mul_mod(r, r, pr);
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    if (g >= a.ng) break;
+                    uint64_t o[2];
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2) {
+                        uint64_t lo, hi;
+                        if constexpr (W == 25) {
+                            const uint64_t B0 = b0[g][q2], B2 = b2[g][q2];
+                            const uint64_t mid = b1[g][q2] - B0 - B2;
+                            const uint64_t t1 = mid << 25, t2 = B2 << 50;
+                            lo = B0 + t1;
+                            hi = (mid >> 39) + (B2 >> 14) + (lo < t1);
+                            lo += t2;
+                            hi += (lo < t2);
+                        } else {
+                            lo = y[g][q2].lo;
+                            hi = y[g][q2].hi;
+                        }
+                        o[q2] = mul_mod(reduce128(hi, lo, pr), r, pr);
+                    }
+                    uint64_t* yg = Ys + (size_t)g * a.y_g_stride;
+                    yg[i0 + lane] = o[0];
+                    yg[total + i0 + lane] = o[1];
+                }
+            }
+        };
+        if (pr.q < (1ULL << 50))
+            run(std::integral_constant<int, 25>{});
+        else
+            run(std::integral_constant<int, 30>{});
+    }
+}
+
 __global__ void k_rows_to_limb(DevCtx c, uint64_t* dst, const uint64_t* src, size_t nrows, RowMap rm) {
     const size_t total = nrows * (size_t)c.N;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -1671,6 +1955,49 @@ void bsgs_limb(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStrea
     } while (0)
     FHE_DN_SWITCH(dn, FHE_LIMB)
 #undef FHE_LIMB
+}
+
+#ifndef FHE_TMA_NST
+#define FHE_TMA_NST 3
+#endif
+#ifndef FHE_TMA_MINB
+#define FHE_TMA_MINB 5
+#endif
+template <int DN, int NG, int SG, int NST, int MINB>
+static void launch_tma(const DevCtx& c, const FusedBsgs& a, int level, cudaStream_t st) {
+    using LY = TmaLayout<DN, NG, SG>;
+    const int ne = level + 1 + c.K;
+    const size_t smem = (size_t)NST * LY::STAGE * 8 + NST * 8;
+    const size_t items = (size_t)ne * c.N / kTmaBlk * (size_t)((a.nsrc + SG - 1) / SG);
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_bsgs_tma<DN, NG, SG, NST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_tma<DN, NG, SG, NST, MINB>, 32 * SG, smem);
+    if (per_sm < 1) per_sm = 1;
+    const size_t cap = (size_t)sm_count() * per_sm;
+    const int blocks = (int)(items < cap ? items : cap);
+    k_bsgs_tma<DN, NG, SG, NST, MINB><<<blocks, 32 * SG, smem, st>>>(c, a, level);
+}
+
+void bsgs_tma(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st) {
+    if (a.nb <= 0 || a.nsrc <= 0 || a.ng <= 0) return;
+    if (a.accumulate || a.digit_slot_stride || a.ct_slot_stride || a.ng > kFusedMaxG)
+        throw std::invalid_argument("bsgs_tma: source slots / accumulation are not supported");
+    ++g_launches;
+    const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
+#define FHE_TMA(D)                                                                          \
+    do {                                                                                    \
+        if (a.ng <= 3) {                                                                    \
+            if (sg == 4) launch_tma<D, 3, 4, FHE_TMA_NST, FHE_TMA_MINB>(c, a, level, st);   \
+            else if (sg == 2) launch_tma<D, 3, 2, FHE_TMA_NST, 8>(c, a, level, st);         \
+            else launch_tma<D, 3, 1, FHE_TMA_NST, 8>(c, a, level, st);                      \
+        } else {                                                                            \
+            if (sg == 4) launch_tma<D, kFusedMaxG, 4, FHE_TMA_NST, 4>(c, a, level, st);     \
+            else if (sg == 2) launch_tma<D, kFusedMaxG, 2, FHE_TMA_NST, 6>(c, a, level, st); \
+            else launch_tma<D, kFusedMaxG, 1, FHE_TMA_NST, 8>(c, a, level, st);             \
+        }                                                                                   \
+    } while (0)
+    FHE_DN_SWITCH(dn, FHE_TMA)
+#undef FHE_TMA
 }
 
 void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,

@@ -288,6 +288,8 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
 // ciphertexts [P c]_q ([2][level+1][N] per source, ct_prescale). Same Y (normal form,
 // bit-identical). No source slots / accumulation, ng <= kFusedMaxG.
 void bsgs_limb(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st);
+// The same on TMA-staged blocks of 32 coefficients, one coefficient per thread (k_bsgs_tma).
+void bsgs_tma(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st);
 // dst[i] = to_limb(src[i]) for nrows rows of N words; row r uses prime
 // row_prime(rm, r % rm.rows_per_poly) (rm.level < 0: prime index r % rows_per_poly)
 void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,
