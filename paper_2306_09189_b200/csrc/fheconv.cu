@@ -61,7 +61,7 @@ struct fhe_ctx {
     bool fused_batch = false;        // FHECONV_BATCH_FUSED=1: batched kernels instead of lanes
     bool batch5 = true;              // approach 5: sources batched through one fused launch (FHECONV_BATCH5=0: lanes)
     bool limb = true;                // approach 5 baby steps on limb-form operands (k_bsgs_limb; FHECONV_LIMB=0: k_bsgs_fused)
-    bool tma = false;                // limb baby steps TMA-staged (k_bsgs_tma; FHECONV_TMA=1)
+    bool tma = true;                 // limb baby steps TMA-staged (k_bsgs_tma; FHECONV_TMA=0: k_bsgs_limb)
     int logN = 0, N = 0, L = 0, K = 0, alpha = 0, dnum = 0, np = 0;
     std::vector<uint64_t> primes;
     double scale = 0;
@@ -77,7 +77,7 @@ struct fhe_ctx {
     bool have_key = false;
     uint64_t key_seed = 0;
     std::map<uint32_t, uint64_t*> keys;
-    std::map<uint32_t, uint64_t*> limb_keys;  // limb-form copies of the fused baby-step keys (cudaMalloc)
+    uint64_t key_gen = 0;  // bumped by fhe_keygen: per-layer limb key copies are rebuilt
     fhe_ledger ledger{};
     uint64_t launch_base = 0;
     int giant_chunk = 8;  // giant steps per ModUp batch (FHECONV_GIANT_CHUNK)
@@ -244,7 +244,10 @@ struct fhe_conv_layer {
         std::vector<int64_t> bamt, gamt;
         std::vector<int> nonempty;  // [ngi][nb]
         uint64_t* d_pts = nullptr;  // [ngi][nb][ne][N], pt'[g][b] = rot_{-g}(pt)
-        uint64_t* d_pts_limb = nullptr;  // the same in limb form (approach 5, k_bsgs_limb)
+        uint64_t* d_pts_limb = nullptr;   // the same in limb form (approach 5, k_bsgs_limb / k_bsgs_tma)
+        uint64_t* d_keys_limb = nullptr;  // limb-form keys of the keyed baby steps [nkeys][2 dnum][L+K][N]
+        std::vector<int> kidx;            // baby b -> its key in d_keys_limb (-1: identity)
+        uint64_t limb_gen = 0;            // key generation d_keys_limb was built from
     } bs[3];
     // multi-shard image mode (fhe_conv_layer_create_shards): t input shards of z
     // channels, n_out output shards; fused-BSGS plaintexts
@@ -822,6 +825,9 @@ fhe_conv_layer::Bsgs& ensure_bsgs(fhe_ctx* c, const fhe_conv_layer* cly, int ori
 // (host-synchronising, so batch_impl calls it before a graph capture); keygen drops
 // the key copies with the keys.
 bool limb_ok(const fhe_ctx* c, const fhe_conv_layer::Bsgs& B) { return c->limb && B.nb <= kMaxFused; }
+// giants of the limb plaintext set, rounded up so that every launch's plaintext box
+// (3 giants when a launch has <= 3, else kFusedMaxG) stays inside the tensor
+int limb_giants(int ngi) { return ngi <= 3 ? 3 : (ngi + kFusedMaxG - 1) / kFusedMaxG * kFusedMaxG; }
 
 void prepare_limb(fhe_ctx* c, const fhe_conv_layer* ly, int orient) {
     if (orient != 5) return;
@@ -830,30 +836,36 @@ void prepare_limb(fhe_ctx* c, const fhe_conv_layer* ly, int orient) {
     bool dirty = false;
     const int ne = c->ne_at(ly->level);
     if (!B.d_pts_limb) {
-        const size_t rows = (size_t)B.ngi * B.nb * ne;
-        ck(cudaMalloc(&B.d_pts_limb, rows * c->N * 8), "cudaMalloc");
+        // padded (zero rows) to the giant count the TMA plaintext boxes of the launches span
+        const size_t rows = (size_t)B.ngi * B.nb * ne, prow = (size_t)limb_giants(B.ngi) * B.nb * ne;
+        ck(cudaMalloc(&B.d_pts_limb, prow * c->N * 8), "cudaMalloc");
+        ck(cudaMemsetAsync(B.d_pts_limb + rows * c->N, 0, (prow - rows) * c->N * 8, c->st), "memset");
         rows_to_limb(c->dc, B.d_pts_limb, B.d_pts, rows, RowMap{ne, ly->level, c->L, 0}, c->st);
         dirty = true;
     }
-    for (int64_t amt : B.bamt) {
-        const uint32_t g = c->galois_of(c->reduce_amount(amt));
-        if (g == 1 || c->limb_keys.count(g)) continue;
-        const uint64_t* key = c->key_for(g);
+    if (!B.d_keys_limb || B.limb_gen != c->key_gen) {
+        std::vector<const uint64_t*> src;
+        std::vector<int> kidx(B.nb, -1);
+        for (int b = 0; b < B.nb; ++b) {
+            const uint32_t g = c->galois_of(c->reduce_amount(B.bamt[b]));
+            if (g == 1) continue;
+            kidx[b] = (int)src.size();
+            src.push_back(c->key_for(g));
+        }
         const size_t rows = (size_t)c->dnum * 2 * c->np;
-        uint64_t* d = nullptr;
-        ck(cudaMalloc(&d, rows * c->N * 8), "cudaMalloc");
-        rows_to_limb(c->dc, d, key, rows, RowMap{c->np, -1, c->L, 0}, c->st);
-        c->limb_keys[g] = d;
+        if (B.d_keys_limb) {
+            ck(cudaStreamSynchronize(c->main_st), "sync");
+            cudaFree(B.d_keys_limb);
+            B.d_keys_limb = nullptr;
+        }
+        ck(cudaMalloc(&B.d_keys_limb, std::max<size_t>(1, src.size()) * rows * c->N * 8), "cudaMalloc");
+        for (size_t t = 0; t < src.size(); ++t)
+            rows_to_limb(c->dc, B.d_keys_limb + t * rows * c->N, src[t], rows, RowMap{c->np, -1, c->L, 0}, c->st);
+        B.kidx = kidx;
+        B.limb_gen = c->key_gen;
         dirty = true;
     }
     if (dirty) ck(cudaStreamSynchronize(c->st), "limb operands");
-}
-
-void free_limb_keys(fhe_ctx* c) {
-    if (c->limb_keys.empty()) return;
-    ck(cudaStreamSynchronize(c->main_st), "sync");
-    for (auto& kv : c->limb_keys) cudaFree(kv.second);
-    c->limb_keys.clear();
 }
 
 // Baby steps of the fused BSGS schedule for nsrc sources: Y_g(s) for every
@@ -864,7 +876,28 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
                   const uint64_t* cts, size_t ctstride, int nsrc, uint64_t* Y, size_t ystride, bool limb = false) {
     const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
     const size_t extw = (size_t)ne * c->N;
-    if (limb && !(limb_ok(c, B) && B.d_pts_limb)) fail(FHE_E_RUNTIME, "limb operands not prepared");
+    if (limb && !(limb_ok(c, B) && B.d_pts_limb && B.d_keys_limb && B.limb_gen == c->key_gen))
+        fail(FHE_E_RUNTIME, "limb operands not prepared");
+    const size_t keyw = (size_t)c->dnum * 2 * c->np * c->N;
+    TmaMaps tm{};
+    const bool tma = limb && c->tma;
+    if (tma) {  // tensor maps of this launch's operands (kernels.cuh TmaMaps)
+        if (nsrc > 1 && (dstride != (size_t)dn * extw || ctstride != (size_t)2 * nr * c->N))
+            fail(FHE_E_RUNTIME, "tma staging needs dense digit / ciphertext batches");
+        const uint32_t sg = (uint32_t)tma_sources(nsrc), P2 = 256u / sg;
+        const uint64_t N = c->N;
+        uint64_t nkeys = 0;
+        for (int v : B.kidx) nkeys += v >= 0;
+        const uint64_t dk[4] = {N, (uint64_t)c->np, 2ull * c->dnum, std::max<uint64_t>(1, nkeys)};
+        const uint32_t bk[4] = {P2, 1, 2u * dn, 1};
+        tma_map4(&tm.key, B.d_keys_limb, dk, bk);
+        const uint64_t dd[4] = {N, (uint64_t)ne, (uint64_t)dn, (uint64_t)nsrc};
+        const uint32_t bd[4] = {P2, 1, (uint32_t)dn, sg};
+        tma_map4(&tm.dig, digits, dd, bd);
+        const uint64_t dc4[4] = {N, (uint64_t)nr, 2, (uint64_t)nsrc};
+        const uint32_t bc[4] = {P2, 1, 2, sg};
+        tma_map4(&tm.ct, cts, dc4, bc);
+    }
     FusedBsgs f{};
     f.nsrc = nsrc;
     f.digits = digits;
@@ -886,6 +919,12 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
     for (int g0 = 0; g0 < B.ngi; g0 += gstep) {
         const int ng = std::min(gstep, B.ngi - g0);
         f.ng = ng;
+        tm.g0 = g0;
+        if (tma) {  // the plaintext box spans the kernel's NG giants (3 when ng <= 3, else kFusedMaxG)
+            const uint64_t dp[4] = {(uint64_t)c->N, (uint64_t)ne, (uint64_t)B.nb, (uint64_t)limb_giants(B.ngi)};
+            const uint32_t bp[4] = {256u / (uint32_t)tma_sources(nsrc), 1, 1, ng <= 3 ? 3u : (uint32_t)kFusedMaxG};
+            tma_map4(&tm.pt, B.d_pts_limb, dp, bp);
+        }
         f.Y = Y + (size_t)g0 * 2 * extw;
         std::vector<int> active;
         for (int b = 0; b < B.nb; ++b)
@@ -910,7 +949,9 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
                     if (B.nonempty[(size_t)(g0 + g) * B.nb + b]) mask |= 1u << g;
                 const uint32_t gal = c->galois_of(c->reduce_amount(B.bamt[b]));
                 f.galois[f.nb] = gal;
-                f.key[f.nb] = gal == 1 ? nullptr : limb ? c->limb_keys.at(gal) : c->key_for(gal);
+                f.key[f.nb] = gal == 1 ? nullptr : limb ? B.d_keys_limb + (size_t)B.kidx[b] * keyw : c->key_for(gal);
+                tm.kidx[f.nb] = (int16_t)(gal == 1 || !limb ? -1 : B.kidx[b]);
+                tm.bidx[f.nb] = (int16_t)b;
                 f.gmask[f.nb] = mask;
                 f.pt[f.nb] = (limb ? B.d_pts_limb : B.d_pts) + ((size_t)g0 * B.nb + b) * extw;
                 f.srcslot[f.nb] = 0;
@@ -922,8 +963,8 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
                      c->rows(keyed * 2.0 * dn * ne + pt_words * ne +
                              nsrc * ((double)dn * ne + 2.0 * nr + (f.accumulate ? 4.0 : 2.0) * ng * ne)),
                      [&] {
-                         if (limb && c->tma)
-                             bsgs_tma(c->dc, f, level, dn, c->st);
+                         if (tma)
+                             bsgs_tma(c->dc, f, tm, level, dn, c->st);
                          else if (limb)
                              bsgs_limb(c->dc, f, level, dn, c->st);
                          else
@@ -2089,7 +2130,6 @@ void fhe_ctx_destroy(fhe_ctx* c) {
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto& kv : c->keys) cudaFreeAsync(kv.second, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
-    for (auto& kv : c->limb_keys) cudaFree(kv.second);
     void* bufs[] = {c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv, c->d_ninv_sh,
                     c->d_modup, c->d_md, c->d_qlinv, c->d_qlinv_sh, c->d_pqlinv, c->d_pqlinv_sh, c->d_s};
     for (void* b : bufs)
@@ -2245,7 +2285,7 @@ int fhe_keygen(fhe_ctx* c, uint64_t seed) {
         if (!c->d_s) ck(cudaMalloc(&c->d_s, (size_t)c->np * N * 8), "cudaMalloc");
         // captured graphs hold the device addresses of the keys released below
         drop_graphs(c);
-        free_limb_keys(c);
+        c->key_gen++;  // layers rebuild their limb key copies on next use
         for (auto& kv : c->keys) c->release(kv.second);
         c->keys.clear();
         int64_t* s = (int64_t*)c->alloc(N);
@@ -2857,6 +2897,7 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
     for (auto& b : ly->bs) {
         if (b.d_pts) cudaFree(b.d_pts);
         if (b.d_pts_limb) cudaFree(b.d_pts_limb);
+        if (b.d_keys_limb) cudaFree(b.d_keys_limb);
     }
     delete ly;
 }

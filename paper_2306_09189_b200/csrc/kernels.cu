@@ -1219,19 +1219,17 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_limb(DevCtx c, FusedBsgs a, 
 }
 
 // ------------------------------------------------------------ TMA-staged limb baby steps
-// k_bsgs_tma: the limb-form baby steps of k_bsgs_limb with the staging moved off the
-// compute threads. A CTA owns one aligned block of 32 coefficients of one extended
-// row and SG sources (thread = (coefficient, source): warp w = source w, lane =
-// coefficient; ONE coefficient per thread, so the accumulators take half the
-// registers and more warps are resident). Per baby step every operand row segment
-// is one 256-byte bulk copy (cp.async.bulk, completing on the stage's mbarrier)
-// issued by a few lanes: 2 DN key rows + the fed plaintext rows (shared by the SG
-// sources) and per source DN digit blocks + its c0 block. The Galois automorphism
-// maps an aligned 32-block of the bit-reversed NTT order onto an aligned 32-block,
-// so a source block is copied whole and the permutation is applied on the shared
-// read (lane -> pidx & 31, a bijection: conflict-free). NST stages in flight.
-constexpr int kTmaBlk = 32;
-
+// k_bsgs_tma: the limb-form baby steps of k_bsgs_limb (same thread mapping: thread =
+// (coefficient pair, source), P = 128 / SG pairs per CTA) with the operand staging
+// taken off the compute threads: per baby step ONE thread issues at most four
+// tensor copies (cp.async.bulk.tensor.4d, TMA) that complete on the stage's
+// mbarrier -- the 2 DN key rows of the CTA's block (shared by its SG sources), the
+// NG plaintext rows, the SG x DN digit blocks and the SG x 2 ciphertext blocks.
+// The Galois automorphism maps an aligned block of the bit-reversed NTT order onto
+// an aligned block, so the digits and c0 of every source are copied as one whole
+// block and the permutation is applied on the shared-memory read (pair slot
+// (pidx & (2P - 1)) / 2: a bijection over the warp, conflict-free). Two stages:
+// baby b + 2 is fetched while b + 1 is computed.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -1251,95 +1249,75 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
+__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
 }
 
 template <int DN, int NG, int SG>
-struct TmaLayout {
-    static constexpr int B = kTmaBlk;
-    static constexpr int KW = 2 * DN * B;    // keys      [2 DN][B]
-    static constexpr int PW = NG * B;        // plaintexts [NG][B]
-    static constexpr int DW = SG * DN * B;   // digits    [SG][DN][B]
-    static constexpr int CW = SG * B;        // c0        [SG][B]
-    static constexpr int STAGE = KW + PW + DW + CW;  // words
+struct TmaLayout {  // one stage, in 16-byte pair slots
+    static constexpr int P = 128 / SG;
+    static constexpr int KW = 2 * DN * P;  // keys       [2 DN][P]
+    static constexpr int PW = NG * P;      // plaintexts [NG][P]
+    static constexpr int DW = SG * DN * P; // digits     [SG][DN][P]
+    static constexpr int CW = SG * 2 * P;  // c0, c1     [SG][2][P]
+    static constexpr int STAGE = KW + PW + DW + CW;
 };
 
-template <int DN, int NG, int SG, int NST, int MINB>
-__global__ void __launch_bounds__(32 * SG, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, int level) {
+template <int DN, int NG, int SG, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, const __grid_constant__ TmaMaps m,
+                                                        int level) {
     using LY = TmaLayout<DN, NG, SG>;
-    constexpr int B = kTmaBlk;
-    extern __shared__ __align__(128) uint64_t tsm[];  // [NST][STAGE] words, then NST mbarriers
-    uint64_t* const bars = tsm + (size_t)NST * LY::STAGE;
-    const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
-    const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    constexpr int P = LY::P, BW = 2 * P;
+    extern __shared__ __align__(1024) ulonglong2 tsb[];  // [2][STAGE], then 2 mbarriers
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(tsb + 2 * LY::STAGE);
+    const int nr = level + 1, ne = nr + c.K;
+    const int tid = threadIdx.x, p = tid % P, sl = tid / P;
     const size_t total = (size_t)ne * c.N;
-    const size_t chunks = total / B;
+    const size_t chunks = total / BW;
     const int ngroups = (a.nsrc + SG - 1) / SG;
     const size_t items = chunks * (size_t)ngroups;
-    const size_t keyrow = (size_t)np * c.N;
     const uint32_t nmask = (2u << c.logN) - 1;
     RowMap rm{ne, level, c.L, 0};
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < NST; ++st) mbar_init(bars + st, 1);
+    if (tid == 0) {
+        mbar_init(bars, 1);
+        mbar_init(bars + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t phase = 0;  // bit st: parity of the next completion of stage st
+    uint32_t phase = 0;
     for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
         const size_t chunk = it / (size_t)ngroups;
-        const int g0src = (int)(it % (size_t)ngroups) * SG;
-        const int s = g0src + sl;
+        const int s0 = (int)(it % (size_t)ngroups) * SG;
+        const int s = s0 + sl;
         const bool active = s < a.nsrc;
-        const int nact = min(SG, a.nsrc - g0src);
-        const size_t i0 = chunk * B;
+        // boxes never leave the tensors: the source box of a partial last group is
+        // shifted back (nsrc >= SG), and special rows (no ciphertext row) read row 0
+        const int s0c = min(s0, a.nsrc - SG), slot = active ? s - s0c : 0;
+        const size_t i0 = chunk * BW, i = i0 + 2 * p;
         const int u = (int)(i0 >> c.logN);
-        const uint32_t k0 = (uint32_t)(i0 & (size_t)(c.N - 1)), k = k0 + lane;
+        const uint32_t k0 = (uint32_t)(i0 & (size_t)(c.N - 1)), k = k0 + 2 * p;
         const int pi = row_prime(rm, u);
         const Prime pr = c.primes[pi];
         const bool qrow = u < nr;
         const uint32_t e = 2 * brev_n(k, c.logN) + 1, e0 = 2 * brev_n(k0, c.logN) + 1;
         auto pidx = [&](uint32_t ee, uint32_t g) { return brev_n((((ee * g) & nmask) - 1) >> 1, c.logN); };
-        // stage fill of baby b (warp-cooperative: lanes issue the copies of their warp's
-        // share; thread 0 arms the barrier with the stage's total bytes)
         auto issue = [&](int b, int st) {
-            if (b >= a.nb) return;
-            uint64_t* sb = tsm + (size_t)st * LY::STAGE;
+            if (tid != 0 || b >= a.nb) return;
+            ulonglong2* sb = tsb + st * LY::STAGE;
             uint64_t* bar = bars + st;
-            const uint64_t* key = a.key[b];
-            const uint32_t gm = a.gmask[b];
-            const uint32_t blk = pidx(e0, a.galois[b]) & ~(uint32_t)(B - 1);
-            if (threadIdx.x == 0) {
-                uint32_t bytes = (uint32_t)__popc(gm & ((1u << NG) - 1)) * B * 8;
-                if (key) bytes += (2 * DN + nact * DN + (qrow ? nact : 0)) * B * 8;
-                else if (qrow) bytes += 2 * nact * B * 8;
-                mbar_expect_tx(bar, bytes);
-            }
-            if (sl == 0) {  // shared rows: keys, plaintexts
-                if (key && lane < 2 * DN)
-                    bulk_g2s(sb + lane * B, key + (size_t)lane * keyrow + (size_t)pi * c.N + k0, B * 8, bar);
-                if (lane >= 16 && lane < 16 + NG && ((gm >> (lane - 16)) & 1u))
-                    bulk_g2s(sb + LY::KW + (lane - 16) * B,
-                             a.pt[b] + (size_t)(lane - 16) * a.pt_g_stride + (size_t)u * c.N + k0, B * 8, bar);
-            }
-            if (active) {
-                const uint64_t* C0 = a.ct + (size_t)s * a.ct_src_stride + (size_t)u * c.N;
-                uint64_t* sd = sb + LY::KW + LY::PW + sl * DN * B;
-                uint64_t* sc = sb + LY::KW + LY::PW + LY::DW + sl * B;
-                if (key) {
-                    if (lane < DN)
-                        bulk_g2s(sd + lane * B,
-                                 a.digits + (size_t)s * a.digit_src_stride + (size_t)lane * total + (size_t)u * c.N + blk,
-                                 B * 8, bar);
-                    else if (lane == DN && qrow)
-                        bulk_g2s(sc, C0 + blk, B * 8, bar);
-                } else if (qrow) {  // identity baby: [P c1], [P c0] unpermuted
-                    if (lane == 0) bulk_g2s(sd, C0 + (size_t)nr * c.N + k0, B * 8, bar);
-                    if (lane == 1) bulk_g2s(sc, C0 + k0, B * 8, bar);
-                }
+            const bool keyed = m.kidx[b] >= 0;
+            const int blk = (int)(pidx(e0, a.galois[b]) & ~(uint32_t)(BW - 1));
+            mbar_expect_tx(bar, (uint32_t)(LY::PW + LY::CW + (keyed ? LY::KW + LY::DW : 0)) * 16u);
+            tma_load4(sb + LY::KW, &m.pt, (int)k0, u, m.bidx[b], m.g0, bar);
+            tma_load4(sb + LY::KW + LY::PW + LY::DW, &m.ct, blk, qrow ? u : 0, 0, s0c, bar);
+            if (keyed) {
+                tma_load4(sb, &m.key, (int)k0, pi, 0, m.kidx[b], bar);
+                tma_load4(sb + LY::KW + LY::PW, &m.dig, blk, u, 0, s0c, bar);
             }
         };
         auto run = [&](auto wtag) {
@@ -1347,122 +1325,155 @@ __global__ void __launch_bounds__(32 * SG, MINB) k_bsgs_tma(DevCtx c, FusedBsgs 
             constexpr uint32_t MW = LimbConst<W>::M;
             const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> W);
             const uint32_t qinv = (uint32_t)pr.qinv & MW;
-            uint64_t b0[W == 25 ? NG : 1][2], b1[W == 25 ? NG : 1][2], b2[W == 25 ? NG : 1][2];
-            U128 y[W == 30 ? NG : 1][2];
+            uint64_t b0[W == 25 ? NG : 1][2][2], b1[W == 25 ? NG : 1][2][2], b2[W == 25 ? NG : 1][2][2];
+            U128 y[W == 30 ? NG : 1][2][2];
 #pragma unroll
             for (int g = 0; g < (W == 25 ? NG : 1); ++g)
 #pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2) b0[g][q2] = b1[g][q2] = b2[g][q2] = 0;
+                for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) b0[g][q2][e2] = b1[g][q2][e2] = b2[g][q2][e2] = 0;
 #pragma unroll
             for (int g = 0; g < (W == 30 ? NG : 1); ++g)
 #pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2) y[g][q2] = U128{0, 0};
+                for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
-            for (int b = 0; b < NST - 1; ++b) issue(b, b);
-            int st = 0;
-            for (int b = 0; b < a.nb; ++b) {
+                    for (int e2 = 0; e2 < 2; ++e2) y[g][q2][e2] = U128{0, 0};
+            issue(0, 0);
+            issue(1, 1);
+            auto baby = [&](int b, int st) {
                 mbar_wait(bars + st, (phase >> st) & 1u);
                 phase ^= 1u << st;
-                const uint64_t* sb = tsm + (size_t)st * LY::STAGE;
-                const uint32_t pk = pidx(e, a.galois[b]) & (B - 1);
-                uint64_t x[2];
-                if (a.key[b]) {
-                    const uint64_t* sd = sb + LY::KW + LY::PW + sl * DN * B + pk;
-                    uint64_t z0[2] = {0, 0}, z1[2] = {0, 0}, z2[2] = {0, 0};
+                const ulonglong2* sb = tsb + st * LY::STAGE;
+                const uint32_t pk = pidx(e, a.galois[b]);
+                const int wo = (int)(pk & (uint32_t)(BW - 1));  // permuted word in the block
+                uint64_t x[2][2];
+                const uint64_t* sc = reinterpret_cast<const uint64_t*>(sb + LY::KW + LY::PW + LY::DW + slot * 2 * P);
+                if (m.kidx[b] >= 0) {
+                    const uint64_t* sd = reinterpret_cast<const uint64_t*>(sb + LY::KW + LY::PW + slot * DN * P);
+                    uint64_t z0[2][2] = {{0, 0}, {0, 0}}, z1[2][2] = {{0, 0}, {0, 0}}, z2[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
                     for (int j = 0; j < DN; ++j) {
-                        const uint64_t dw = sd[j * B];
-                        const uint64_t kw[2] = {sb[(2 * j) * B + lane], sb[(2 * j + 1) * B + lane]};
-                        const uint32_t d0 = lo32(dw), d1 = hi32(dw);
-                        if constexpr (W == 25) {
-                            const uint32_t ds = d0 + d1;
+                        const ulonglong2 kv0 = sb[(2 * j) * P + p], kv1 = sb[(2 * j + 1) * P + p];
+                        const uint64_t dw[2] = {sd[j * BW + wo], sd[j * BW + (wo ^ 1)]};
+                        const uint64_t kw[2][2] = {{kv0.x, kv0.y}, {kv1.x, kv1.y}};
 #pragma unroll
-                            for (int q2 = 0; q2 < 2; ++q2) {
-                                const uint32_t kk0 = lo32(kw[q2]), kk1 = hi32(kw[q2]);
-                                madw(z0[q2], d0, kk0);
-                                madw(z2[q2], d1, kk1);
-                                madw(z1[q2], ds, kk0 + kk1);
-                            }
-                        } else {
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            const uint32_t d0 = lo32(dw[e2]), d1 = hi32(dw[e2]);
+                            if constexpr (W == 25) {
+                                const uint32_t ds = d0 + d1;
 #pragma unroll
-                            for (int q2 = 0; q2 < 2; ++q2) {
-                                const uint32_t kk0 = lo32(kw[q2]), kk1 = hi32(kw[q2]);
-                                madw(z0[q2], d0, kk0);
-                                madw(z1[q2], d0, kk1);
-                                madw(z1[q2], d1, kk0);
-                                madw(z2[q2], d1, kk1);
+                                for (int q2 = 0; q2 < 2; ++q2) {
+                                    const uint32_t kk0 = lo32(kw[q2][e2]), kk1 = hi32(kw[q2][e2]);
+                                    madw(z0[q2][e2], d0, kk0);
+                                    madw(z2[q2][e2], d1, kk1);
+                                    madw(z1[q2][e2], ds, kk0 + kk1);
+                                }
+                            } else {
+#pragma unroll
+                                for (int q2 = 0; q2 < 2; ++q2) {
+                                    const uint32_t kk0 = lo32(kw[q2][e2]), kk1 = hi32(kw[q2][e2]);
+                                    madw(z0[q2][e2], d0, kk0);
+                                    madw(z1[q2][e2], d0, kk1);
+                                    madw(z1[q2][e2], d1, kk0);
+                                    madw(z2[q2][e2], d1, kk1);
+                                }
                             }
                         }
                     }
                     if constexpr (W == 25) {
 #pragma unroll
-                        for (int q2 = 0; q2 < 2; ++q2) z1[q2] -= z0[q2] + z2[q2];
+                        for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                            for (int e2 = 0; e2 < 2; ++e2) z1[q2][e2] -= z0[q2][e2] + z2[q2][e2];
                     } else if constexpr (DN >= 8) {
 #pragma unroll
-                        for (int q2 = 0; q2 < 2; ++q2) {
-                            z2[q2] += z1[q2] >> W;
-                            z1[q2] &= MW;
-                        }
+                        for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                            for (int e2 = 0; e2 < 2; ++e2) {
+                                z2[q2][e2] += z1[q2][e2] >> W;
+                                z1[q2][e2] &= MW;
+                            }
                     }
                     if (qrow) {  // + [P sigma(c0)]_q in limb form
-                        const uint64_t cw = sb[LY::KW + LY::PW + LY::DW + sl * B + pk];
-                        z0[0] += lo32(cw);
-                        z1[0] += hi32(cw);
+                        const uint64_t cw[2] = {sc[wo], sc[wo ^ 1]};
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            z0[0][e2] += lo32(cw[e2]);
+                            z1[0][e2] += hi32(cw[e2]);
+                        }
                     }
 #pragma unroll
                     for (int q2 = 0; q2 < 2; ++q2)
-                        x[q2] = W == 25 ? mont_l25(z0[q2], z1[q2], z2[q2], q0, q1, qinv)
-                                        : mont_l30(z0[q2], z1[q2], z2[q2], q0, q1, qinv);
-                } else if (qrow) {  // identity: X = [P c]_q
-                    const uint64_t cw[2] = {sb[LY::KW + LY::PW + LY::DW + sl * B + lane],
-                                            sb[LY::KW + LY::PW + sl * DN * B + lane]};
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2)
+                            x[q2][e2] = W == 25 ? mont_l25(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv)
+                                                : mont_l30(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv);
+                } else if (qrow) {  // identity: X = [P c]_q, unpermuted
+                    const uint64_t cw[2][2] = {{sc[2 * p], sc[2 * p + 1]}, {sc[BW + 2 * p], sc[BW + 2 * p + 1]}};
 #pragma unroll
                     for (int q2 = 0; q2 < 2; ++q2)
-                        x[q2] = W == 25 ? mont_l25(lo32(cw[q2]), hi32(cw[q2]), 0, q0, q1, qinv)
-                                        : mont_l30(lo32(cw[q2]), hi32(cw[q2]), 0, q0, q1, qinv);
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2)
+                            x[q2][e2] = W == 25 ? mont_l25(lo32(cw[q2][e2]), hi32(cw[q2][e2]), 0, q0, q1, qinv)
+                                                : mont_l30(lo32(cw[q2][e2]), hi32(cw[q2][e2]), 0, q0, q1, qinv);
                 } else {
-                    x[0] = x[1] = 0;
+                    x[0][0] = x[0][1] = x[1][0] = x[1][1] = 0;
                 }
                 const uint32_t gm = a.gmask[b];
                 if constexpr (W == 25) {
-                    uint32_t xl[2], xh[2], xs[2];
+                    uint32_t xl[2][2], xh[2][2], xs[2][2];
 #pragma unroll
-                    for (int q2 = 0; q2 < 2; ++q2) {
-                        xl[q2] = (uint32_t)x[q2] & MW;
-                        xh[q2] = (uint32_t)(x[q2] >> 25);
-                        xs[q2] = xl[q2] + xh[q2];
-                    }
+                    for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            xl[q2][e2] = (uint32_t)x[q2][e2] & MW;
+                            xh[q2][e2] = (uint32_t)(x[q2][e2] >> 25);
+                            xs[q2][e2] = xl[q2][e2] + xh[q2][e2];
+                        }
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
                         if (!((gm >> g) & 1u)) continue;
-                        const uint64_t ww = sb[LY::KW + g * B + lane];
-                        const uint32_t w0 = lo32(ww), w1 = hi32(ww), ws = w0 + w1;
+                        const ulonglong2 wv = sb[LY::KW + g * P + p];
+                        const uint64_t ww[2] = {wv.x, wv.y};
 #pragma unroll
-                        for (int q2 = 0; q2 < 2; ++q2) {
-                            madw(b0[g][q2], w0, xl[q2]);
-                            madw(b2[g][q2], w1, xh[q2]);
-                            madw(b1[g][q2], ws, xs[q2]);
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            const uint32_t w0 = lo32(ww[e2]), w1 = hi32(ww[e2]), ws = w0 + w1;
+#pragma unroll
+                            for (int q2 = 0; q2 < 2; ++q2) {
+                                madw(b0[g][q2][e2], w0, xl[q2][e2]);
+                                madw(b2[g][q2][e2], w1, xh[q2][e2]);
+                                madw(b1[g][q2][e2], ws, xs[q2][e2]);
+                            }
                         }
                     }
                 } else {
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
                         if (!((gm >> g) & 1u)) continue;
-                        const uint64_t wa = from_limb(sb[LY::KW + g * B + lane], 30);
-                        mac_small(y[g][0], wa, x[0]);
-                        mac_small(y[g][1], wa, x[1]);
+                        const ulonglong2 wv = sb[LY::KW + g * P + p];
+                        const uint64_t wa = from_limb(wv.x, 30), wb = from_limb(wv.y, 30);
+                        mac_small(y[g][0][0], wa, x[0][0]);
+                        mac_small(y[g][0][1], wb, x[0][1]);
+                        mac_small(y[g][1][0], wa, x[1][0]);
+                        mac_small(y[g][1][1], wb, x[1][1]);
                     }
                     if ((b & 31) == 31) {
 #pragma unroll
                         for (int g = 0; g < NG; ++g)
 #pragma unroll
-                            for (int q2 = 0; q2 < 2; ++q2) y[g][q2] = U128{reduce128(y[g][q2].hi, y[g][q2].lo, pr), 0};
+                            for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                                for (int e2 = 0; e2 < 2; ++e2)
+                                    y[g][q2][e2] = U128{reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), 0};
                     }
                 }
-                __syncthreads();  // every thread is done with stage st: refill it
-                const int nst = st == 0 ? NST - 1 : st - 1;  // (b + NST - 1) % NST
-                issue(b + NST - 1, nst);
-                st = st == NST - 1 ? 0 : st + 1;
+                __syncthreads();  // stage st is free: fetch baby b + 2 into it
+                issue(b + 2, st);
+            };
+            for (int b = 0; b < a.nb; b += 2) {
+                baby(b, 0);
+                if (b + 1 < a.nb) baby(b + 1, 1);
             }
             if (active) {
                 uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
@@ -1471,27 +1482,29 @@ __global__ void __launch_bounds__(32 * SG, MINB) k_bsgs_tma(DevCtx c, FusedBsgs 
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
                     if (g >= a.ng) break;
-                    uint64_t o[2];
+                    uint64_t o[2][2];
 #pragma unroll
-                    for (int q2 = 0; q2 < 2; ++q2) {
-                        uint64_t lo, hi;
-                        if constexpr (W == 25) {
-                            const uint64_t B0 = b0[g][q2], B2 = b2[g][q2];
-                            const uint64_t mid = b1[g][q2] - B0 - B2;
-                            const uint64_t t1 = mid << 25, t2 = B2 << 50;
-                            lo = B0 + t1;
-                            hi = (mid >> 39) + (B2 >> 14) + (lo < t1);
-                            lo += t2;
-                            hi += (lo < t2);
-                        } else {
-                            lo = y[g][q2].lo;
-                            hi = y[g][q2].hi;
+                    for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            uint64_t lo, hi;
+                            if constexpr (W == 25) {
+                                const uint64_t B0 = b0[g][q2][e2], B2 = b2[g][q2][e2];
+                                const uint64_t mid = b1[g][q2][e2] - B0 - B2;
+                                const uint64_t t1 = mid << 25, t2 = B2 << 50;
+                                lo = B0 + t1;
+                                hi = (mid >> 39) + (B2 >> 14) + (lo < t1);
+                                lo += t2;
+                                hi += (lo < t2);
+                            } else {
+                                lo = y[g][q2][e2].lo;
+                                hi = y[g][q2][e2].hi;
+                            }
+                            o[q2][e2] = mul_mod(reduce128(hi, lo, pr), r, pr);
                         }
-                        o[q2] = mul_mod(reduce128(hi, lo, pr), r, pr);
-                    }
                     uint64_t* yg = Ys + (size_t)g * a.y_g_stride;
-                    yg[i0 + lane] = o[0];
-                    yg[total + i0 + lane] = o[1];
+                    st2(yg + i, o[0][0], o[0][1]);
+                    st2(yg + total + i, o[1][0], o[1][1]);
                 }
             }
         };
@@ -1957,47 +1970,73 @@ void bsgs_limb(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStrea
 #undef FHE_LIMB
 }
 
-#ifndef FHE_TMA_NST
-#define FHE_TMA_NST 3
-#endif
 #ifndef FHE_TMA_MINB
-#define FHE_TMA_MINB 5
+#define FHE_TMA_MINB 3
 #endif
-template <int DN, int NG, int SG, int NST, int MINB>
-static void launch_tma(const DevCtx& c, const FusedBsgs& a, int level, cudaStream_t st) {
+template <int DN, int NG, int SG, int MINB>
+static void launch_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, cudaStream_t st) {
     using LY = TmaLayout<DN, NG, SG>;
     const int ne = level + 1 + c.K;
-    const size_t smem = (size_t)NST * LY::STAGE * 8 + NST * 8;
-    const size_t items = (size_t)ne * c.N / kTmaBlk * (size_t)((a.nsrc + SG - 1) / SG);
+    const size_t smem = (size_t)2 * LY::STAGE * 16 + 16;
+    const size_t items = (size_t)ne * c.N / (2 * LY::P) * (size_t)((a.nsrc + SG - 1) / SG);
     int per_sm = 0;
-    cudaFuncSetAttribute(k_bsgs_tma<DN, NG, SG, NST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_tma<DN, NG, SG, NST, MINB>, 32 * SG, smem);
+    cudaFuncSetAttribute(k_bsgs_tma<DN, NG, SG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_tma<DN, NG, SG, MINB>, 128, smem);
     if (per_sm < 1) per_sm = 1;
     const size_t cap = (size_t)sm_count() * per_sm;
     const int blocks = (int)(items < cap ? items : cap);
-    k_bsgs_tma<DN, NG, SG, NST, MINB><<<blocks, 32 * SG, smem, st>>>(c, a, level);
+    k_bsgs_tma<DN, NG, SG, MINB><<<blocks, 128, smem, st>>>(c, a, m, level);
 }
 
-void bsgs_tma(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st) {
+void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st) {
     if (a.nb <= 0 || a.nsrc <= 0 || a.ng <= 0) return;
     if (a.accumulate || a.digit_slot_stride || a.ct_slot_stride || a.ng > kFusedMaxG)
         throw std::invalid_argument("bsgs_tma: source slots / accumulation are not supported");
     ++g_launches;
-    const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
-#define FHE_TMA(D)                                                                          \
-    do {                                                                                    \
-        if (a.ng <= 3) {                                                                    \
-            if (sg == 4) launch_tma<D, 3, 4, FHE_TMA_NST, FHE_TMA_MINB>(c, a, level, st);   \
-            else if (sg == 2) launch_tma<D, 3, 2, FHE_TMA_NST, 8>(c, a, level, st);         \
-            else launch_tma<D, 3, 1, FHE_TMA_NST, 8>(c, a, level, st);                      \
-        } else {                                                                            \
-            if (sg == 4) launch_tma<D, kFusedMaxG, 4, FHE_TMA_NST, 4>(c, a, level, st);     \
-            else if (sg == 2) launch_tma<D, kFusedMaxG, 2, FHE_TMA_NST, 6>(c, a, level, st); \
-            else launch_tma<D, kFusedMaxG, 1, FHE_TMA_NST, 8>(c, a, level, st);             \
-        }                                                                                   \
+    const int sg = tma_sources(a.nsrc);
+#define FHE_TMA(D)                                                               \
+    do {                                                                         \
+        if (a.ng <= 3) {                                                         \
+            if (sg == 4) launch_tma<D, 3, 4, FHE_TMA_MINB>(c, a, m, level, st);  \
+            else if (sg == 2) launch_tma<D, 3, 2, 3>(c, a, m, level, st);        \
+            else launch_tma<D, 3, 1, 2>(c, a, m, level, st);                     \
+        } else {                                                                 \
+            if (sg == 4) launch_tma<D, kFusedMaxG, 4, 2>(c, a, m, level, st);    \
+            else if (sg == 2) launch_tma<D, kFusedMaxG, 2, 2>(c, a, m, level, st); \
+            else launch_tma<D, kFusedMaxG, 1, 2>(c, a, m, level, st);            \
+        }                                                                        \
     } while (0)
     FHE_DN_SWITCH(dn, FHE_TMA)
 #undef FHE_TMA
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q{};
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            throw std::runtime_error("cuTensorMapEncodeTiled is unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+void tma_map4(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint32_t box[4]) {
+    cuuint64_t gd[4], gs[3];
+    cuuint32_t bx[4], es[4] = {1, 1, 1, 1};
+    uint64_t stride = 8;
+    for (int d = 0; d < 4; ++d) {
+        gd[d] = dims[d];
+        bx[d] = box[d];
+        if (d > 0) gs[d - 1] = stride;
+        stride *= dims[d];
+    }
+    const CUresult r = tma_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(base), gd, gs, bx, es,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
 }
 
 void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,

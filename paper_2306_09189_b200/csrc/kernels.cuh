@@ -1,6 +1,9 @@
 // Device data structures and kernel launchers of the encrypted-conv hot path.
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -288,8 +291,26 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
 // ciphertexts [P c]_q ([2][level+1][N] per source, ct_prescale). Same Y (normal form,
 // bit-identical). No source slots / accumulation, ng <= kFusedMaxG.
 void bsgs_limb(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st);
-// The same on TMA-staged blocks of 32 coefficients, one coefficient per thread (k_bsgs_tma).
-void bsgs_tma(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st);
+// The same with TMA tensor-copy staging (k_bsgs_tma). The four 4-D maps
+// (innermost dimension first, 8-byte elements) and their boxes, P2 = 2 * 128 / SG
+// coefficients per CTA block (tma_sources(nsrc) = SG):
+//   key: limb keys [nkeys][2 dnum][L+K][N],  box {P2, 1, 2 dn, 1}, coords (k0, prime, 0, kidx[b])
+//   pt : limb plaintexts [ngi][nb][ne][N],   box {P2, 1, 1, NG},  coords (k0, u, bidx[b], g0)
+//   dig: limb digits [nsrc][dn][ne][N],      box {P2, 1, dn, SG}, coords (blk, u, 0, s0c)
+//   ct : limb [P c] [nsrc][2][level+1][N],   box {P2, 1, 2, SG},  coords (blk, u or 0, 0, s0c)
+// (s0c = min(s0, nsrc - SG): no box leaves its tensor -- a partially out-of-bounds box hangs the
+// mbarrier -- and the plaintext set is padded to the giants the boxes span, limb_giants)
+// with NG = 3 when ng <= 3, else kFusedMaxG.
+struct TmaMaps {
+    CUtensorMap key, pt, dig, ct;
+    int16_t kidx[kMaxFused];  // baby b's key in the key map, -1: identity
+    int16_t bidx[kMaxFused];  // baby b's index in the plaintext map
+    int g0;                   // first giant of the launch
+};
+inline int tma_sources(int nsrc) { return nsrc >= 4 ? 4 : nsrc >= 2 ? 2 : 1; }
+void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st);
+// encode a 4-D uint64 tensor map (dims innermost first, dense)
+void tma_map4(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint32_t box[4]);
 // dst[i] = to_limb(src[i]) for nrows rows of N words; row r uses prime
 // row_prime(rm, r % rm.rows_per_poly) (rm.level < 0: prime index r % rows_per_poly)
 void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,
