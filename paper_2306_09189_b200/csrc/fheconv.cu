@@ -60,8 +60,9 @@ struct fhe_ctx {
     } hp;
     bool fused_batch = false;        // FHECONV_BATCH_FUSED=1: batched kernels instead of lanes
     bool batch5 = true;              // approach 5: sources batched through one fused launch (FHECONV_BATCH5=0: lanes)
-    bool limb = true;                // approach 5 baby steps on limb-form operands (k_bsgs_limb; FHECONV_LIMB=0: k_bsgs_fused)
-    bool tma = true;                 // limb baby steps TMA-staged (k_bsgs_tma; FHECONV_TMA=0: k_bsgs_limb)
+    bool limb = true;                // approach 5 baby steps on operand-form rows, TMA-staged (k_bsgs_tma);
+                                     // FHECONV_LIMB=0 or FHECONV_TMA=0: k_bsgs_fused on plain rows
+    bool tma = true;
     int logN = 0, N = 0, L = 0, K = 0, alpha = 0, dnum = 0, np = 0;
     std::vector<uint64_t> primes;
     double scale = 0;
@@ -69,6 +70,7 @@ struct fhe_ctx {
     Prime* d_primes = nullptr;
     uint64_t *d_tw = nullptr, *d_tw_sh = nullptr, *d_itw = nullptr, *d_itw_sh = nullptr;
     uint64_t *d_ninv = nullptr, *d_ninv_sh = nullptr;
+    double2 *d_twd = nullptr, *d_itwd = nullptr, *d_ninvd = nullptr;
     ModUpDigit* d_modup = nullptr;  // [L][dnum]
     ModDownTable* d_md = nullptr;
     uint64_t *d_qlinv = nullptr, *d_qlinv_sh = nullptr;  // [L][L]
@@ -244,7 +246,7 @@ struct fhe_conv_layer {
         std::vector<int64_t> bamt, gamt;
         std::vector<int> nonempty;  // [ngi][nb]
         uint64_t* d_pts = nullptr;  // [ngi][nb][ne][N], pt'[g][b] = rot_{-g}(pt)
-        uint64_t* d_pts_limb = nullptr;   // the same in limb form (approach 5, k_bsgs_limb / k_bsgs_tma)
+        uint64_t* d_pts_limb = nullptr;   // the same in operand form (approach 5, k_bsgs_tma)
         uint64_t* d_keys_limb = nullptr;  // limb-form keys of the keyed baby steps [nkeys][2 dnum][L+K][N]
         std::vector<int> kidx;            // baby b -> its key in d_keys_limb (-1: identity)
         uint64_t limb_gen = 0;            // key generation d_keys_limb was built from
@@ -301,7 +303,7 @@ fhe_ct* new_ct(fhe_ctx* c, int level, double scale, int depth) {
 // ------------------------------------------------------------ primitives
 
 // digits [nsrc][dn][ne][N] of nsrc polynomials c1 + s * stride (level+1 rows each, NTT)
-// (limb != 0: digit rows in limb form, modarith.cuh, for k_bsgs_limb)
+// (limb != 0: digit rows in operand form, modarith.cuh, for k_bsgs_tma)
 void modup_batch(fhe_ctx* c, const uint64_t* c1, size_t stride, int nsrc, int level, uint64_t* digits, int limb = 0) {
     const int nr = level + 1, dn = c->dn_at(level), ne = c->ne_at(level);
     const size_t rowsw = (size_t)nr * c->N;
@@ -458,6 +460,12 @@ void upload_tables(fhe_ctx* c) {
     }
     std::vector<uint64_t> tw((size_t)np * N), tws((size_t)np * N), itw((size_t)np * N), itws((size_t)np * N);
     std::vector<uint64_t> ninv(np), ninvs(np);
+    // FP64 companions (centred value, value / q), used by the NTT for primes < 2^50
+    std::vector<double2> twd((size_t)np * N), itwd((size_t)np * N), ninvd(np);
+    auto cdbl = [](uint64_t w, uint64_t q) {
+        const double wc = w > q / 2 ? -(double)(q - w) : (double)w;
+        return make_double2(wc, wc / (double)q);
+    };
     std::vector<uint32_t> brv(N);
     for (size_t k = 0; k < N; ++k) brv[k] = bitrev((uint32_t)k, c->logN);
     std::vector<uint64_t> pw(N), ipw(N);
@@ -477,9 +485,12 @@ void upload_tables(fhe_ctx* c) {
             itw[o] = ipw[brv[k]];
             tws[o] = shoup(tw[o], q);
             itws[o] = shoup(itw[o], q);
+            twd[o] = cdbl(tw[o], q);
+            itwd[o] = cdbl(itw[o], q);
         }
         ninv[i] = invmod(N % q, q);
         ninvs[i] = shoup(ninv[i], q);
+        ninvd[i] = cdbl(ninv[i], q);
     }
     // ModUp digit tables [L][dnum]
     std::vector<ModUpDigit> mu((size_t)L * c->dnum);
@@ -562,14 +573,17 @@ void upload_tables(fhe_ctx* c) {
     up((void**)&c->d_itw_sh, itws.data(), itws.size() * 8);
     up((void**)&c->d_ninv, ninv.data(), ninv.size() * 8);
     up((void**)&c->d_ninv_sh, ninvs.data(), ninvs.size() * 8);
+    up((void**)&c->d_twd, twd.data(), twd.size() * sizeof(double2));
+    up((void**)&c->d_itwd, itwd.data(), itwd.size() * sizeof(double2));
+    up((void**)&c->d_ninvd, ninvd.data(), ninvd.size() * sizeof(double2));
     up((void**)&c->d_modup, mu.data(), mu.size() * sizeof(ModUpDigit));
     up((void**)&c->d_md, &md, sizeof(md));
     up((void**)&c->d_qlinv, ql.data(), ql.size() * 8);
     up((void**)&c->d_qlinv_sh, qls.data(), qls.size() * 8);
     up((void**)&c->d_pqlinv, pql.data(), pql.size() * 8);
     up((void**)&c->d_pqlinv_sh, pqls.data(), pqls.size() * 8);
-    c->dc = DevCtx{c->logN, c->N, L, K, c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv,
-                   c->d_ninv_sh};
+    c->dc = DevCtx{c->logN,    c->N,        L,        K,          c->d_primes, c->d_tw,   c->d_tw_sh,
+                   c->d_itw,   c->d_itw_sh, c->d_ninv, c->d_ninv_sh, c->d_twd,   c->d_itwd, c->d_ninvd};
 }
 
 void require_key(const fhe_ctx* c) {
@@ -820,7 +834,7 @@ fhe_conv_layer::Bsgs& ensure_bsgs(fhe_ctx* c, const fhe_conv_layer* cly, int ori
     return B;
 }
 
-// Limb-form operands of the fused baby steps (k_bsgs_limb): a copy of
+// Operand-form copies for the fused baby steps (k_bsgs_tma): a copy of
 // the layer's rotated plaintexts and of every baby-step key in limb form. Built once
 // (host-synchronising, so batch_impl calls it before a graph capture); keygen drops
 // the key copies with the keys.
@@ -965,8 +979,6 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
                      [&] {
                          if (tma)
                              bsgs_tma(c->dc, f, tm, level, dn, c->st);
-                         else if (limb)
-                             bsgs_limb(c->dc, f, level, dn, c->st);
                          else
                              bsgs_fused(c->dc, f, c->d_md, level, dn, c->st);
                      });
@@ -2095,6 +2107,7 @@ int fhe_ctx_create(const fhe_params* p, fhe_ctx** out) {
         if (const char* e = std::getenv("FHECONV_BATCH5")) c->batch5 = std::atoi(e) != 0;
         if (const char* e = std::getenv("FHECONV_LIMB")) c->limb = std::atoi(e) != 0;
         if (const char* e = std::getenv("FHECONV_TMA")) c->tma = std::atoi(e) != 0;
+        c->limb = c->limb && c->tma;
         if (const char* e = std::getenv("FHECONV_GRAPHS")) c->use_graphs = std::atoi(e) != 0;
         cudaMemPool_t pool;
         ck(cudaDeviceGetDefaultMemPool(&pool, c->device), "mempool");
@@ -2131,6 +2144,7 @@ void fhe_ctx_destroy(fhe_ctx* c) {
     for (auto& kv : c->keys) cudaFreeAsync(kv.second, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
     void* bufs[] = {c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv, c->d_ninv_sh,
+                    c->d_twd,    c->d_itwd, c->d_ninvd,
                     c->d_modup, c->d_md, c->d_qlinv, c->d_qlinv_sh, c->d_pqlinv, c->d_pqlinv_sh, c->d_s};
     for (void* b : bufs)
         if (b) cudaFree(b);

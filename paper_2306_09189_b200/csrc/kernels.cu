@@ -903,37 +903,21 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_fused(DevCtx c, FusedBsgs a,
     }
 }
 
-// ------------------------------------------------------------ limb-form fused baby steps
-// k_bsgs_limb: the baby steps of k_bsgs_fused (same staging: thread = (coefficient
-// pair, source), key and plaintext rows staged once per CTA for its SG sources) on
-// limb-form operands (modarith.cuh). Per extended row the limb width W is fixed:
-//  W = 25 (q < 2^50, 12 of the 15 rows at cfg3): Karatsuba products
-//      d k = d0 k0 + ((d0 + d1)(k0 + k1) - d0 k0 - d1 k1) 2^25 + d1 k1 2^50,
-//      three mad.wide.u32 per product into three 64-bit sums that cannot overflow;
-//      X~ = Montgomery reduction by 2^50 in two 25-bit digit steps (X~ < 2^54), split
-//      at 25 bits and multiplied into the giant accumulators the same way;
-//  W = 30 (60-bit primes): four mad.wide.u32 per product, Montgomery by 2^90 in three
-//      30-bit steps (X~ < 2q), 128-bit plaintext sums (mac_small) as k_bsgs_fused.
-// P sigma(c0) enters as a pre-scaled operand ([P c0]_q, ct_prescale) added to the sums,
-// not as a product. Outputs Y are fully reduced: bit-identical to k_bsgs_fused.
+// ------------------------------------------------------------ operand-form baby steps
+// k_bsgs_tma computes the baby steps of k_bsgs_fused on operands stored in the
+// operand form of modarith.cuh (keys, plaintexts, ModUp digits, P-scaled
+// ciphertexts; converted once per layer / per ModUp), per extended row:
+//  q < 2^50 (12 of the 15 rows at cfg3): centred doubles; every product is one
+//      fmac_d (7 FP64 operations, exact) into integer-valued double sums: the key
+//      inner product X~ = sum_j d_j k_j + [P sigma(c0)]_q, reduced once (red_d), then
+//      Y_g += X~ pt'_g, reduced every 8 baby steps;
+//  60-bit primes: 30-bit limb form, four mad.wide.u32 per product, Montgomery by
+//      2^90 in three 30-bit steps (X~ < 2q), 128-bit plaintext sums (mac_small).
+// Outputs Y are fully reduced: bit-identical to k_bsgs_fused.
 template <int W>
 struct LimbConst {
     static constexpr uint32_t M = (1u << W) - 1;
 };
-
-// X 2^-50 mod q (< 2^54) for X = z0 + m 2^25 + z2 2^50 (W = 25)
-__device__ __forceinline__ uint64_t mont_l25(uint64_t z0, uint64_t m, uint64_t z2, uint32_t q0, uint32_t q1,
-                                             uint32_t qinv) {
-    constexpr uint32_t M = LimbConst<25>::M;
-    const uint32_t t0 = ((uint32_t)z0 * qinv) & M;
-    madw(z0, t0, q0);
-    madw(m, t0, q1);
-    m += z0 >> 25;
-    const uint32_t t1 = ((uint32_t)m * qinv) & M;
-    madw(m, t1, q0);
-    madw(z2, t1, q1);
-    return z2 + (m >> 25);
-}
 
 // X 2^-90 mod q (< 2q) for X = z0 + z1 2^30 + z2 2^60 (W = 30)
 __device__ __forceinline__ uint64_t mont_l30(uint64_t z0, uint64_t z1, uint64_t z2, uint32_t q0, uint32_t q1,
@@ -957,270 +941,9 @@ __device__ __forceinline__ uint64_t mont_l30(uint64_t z0, uint64_t z1, uint64_t 
 __device__ __forceinline__ uint32_t lo32(uint64_t x) { return (uint32_t)x; }
 __device__ __forceinline__ uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
 
-template <int DN, int NG, int SG, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_bsgs_limb(DevCtx c, FusedBsgs a, int level) {
-    using LY = FusedLayout<DN, NG, SG, 2>;
-    constexpr int P = LY::P;
-    extern __shared__ ulonglong2 sb[];  // [2 stages][STAGE]
-    const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
-    const int tid = threadIdx.x, p = tid % P, sl = tid / P;
-    const size_t total = (size_t)ne * c.N;
-    const size_t chunks = total / 2 / P;
-    const int ngroups = (a.nsrc + SG - 1) / SG;
-    const size_t items = chunks * (size_t)ngroups;
-    const size_t keyrow = (size_t)np * c.N;
-    RowMap rm{ne, level, c.L, 0};
-    ulonglong2* const s_key = sb + p;
-    ulonglong2* const s_pt = sb + LY::KW + p;
-    ulonglong2* const s_dig = sb + LY::KW + LY::PW + sl * DN * P + p;
-    ulonglong2* const s_c0 = sb + LY::KW + LY::PW + LY::DW + sl * P + p;
-    constexpr size_t S1 = LY::STAGE;
-    for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const size_t chunk = it / (size_t)ngroups;
-        const int s = (int)(it % (size_t)ngroups) * SG + sl;
-        const bool active = s < a.nsrc;
-        const size_t i = (chunk * P + p) * 2;
-        const int u = (int)(i >> c.logN);
-        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
-        const int pi = row_prime(rm, u);
-        const Prime pr = c.primes[pi];
-        const bool qrow = u < nr;
-        const uint64_t* Du = a.digits + (size_t)(active ? s : 0) * a.digit_src_stride + (size_t)u * c.N;
-        const uint64_t* C0u = a.ct + (size_t)(active ? s : 0) * a.ct_src_stride + (size_t)u * c.N;
-        const uint64_t* C1u = C0u + (size_t)nr * c.N;
-        const size_t kofs = (size_t)pi * c.N + k, pofs = (size_t)u * c.N + k;
-        const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
-        auto pidx = [&](uint32_t g) { return brev_n((((e * g) & nmask) - 1) >> 1, c.logN); };
-        auto issue_s = [&](int b, size_t so) {
-            if (b >= a.nb) {
-                cp_async_commit();
-                return;
-            }
-            const uint32_t pk = pidx(a.galois[b]);
-            const uint64_t* key = a.key[b];
-            const uint32_t gm = a.gmask[b];
-#pragma unroll
-            for (int g = sl; g < NG; g += SG)
-                if ((gm >> g) & 1u) cp_async16(s_pt + so + g * P, a.pt[b] + (size_t)g * a.pt_g_stride + pofs);
-            if (key) {
-                const uint64_t* kp = key + kofs;
-#pragma unroll
-                for (int j = sl; j < 2 * DN; j += SG) cp_async16(s_key + so + j * P, kp + (size_t)j * keyrow);
-                if (active) {
-                    const uint64_t* dp = Du + (pk & ~1u);
-#pragma unroll
-                    for (int j = 0; j < DN; ++j) cp_async16(s_dig + so + j * P, dp + (size_t)j * total);
-                    if (qrow) cp_async16(s_c0 + so, C0u + (pk & ~1u));
-                }
-            } else if (active && qrow) {  // identity baby: P c0, P c1 unpermuted
-                cp_async16(s_dig + so, C1u + k);
-                cp_async16(s_c0 + so, C0u + k);
-            }
-            cp_async_commit();
-        };
-        // one item: the baby loop for limb width W (row-uniform)
-        auto run = [&](auto wtag) {
-            constexpr int W = decltype(wtag)::value;
-            constexpr uint32_t MW = LimbConst<W>::M;
-            const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> W);
-            const uint32_t qinv = (uint32_t)pr.qinv & MW;
-            // W = 25: Karatsuba sums [g][poly][coef]; W = 30: 128-bit sums
-            uint64_t b0[W == 25 ? NG : 1][2][2], b1[W == 25 ? NG : 1][2][2], b2[W == 25 ? NG : 1][2][2];
-            U128 y[W == 30 ? NG : 1][2][2];
-#pragma unroll
-            for (int g = 0; g < (W == 25 ? NG : 1); ++g)
-#pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) b0[g][q2][e2] = b1[g][q2][e2] = b2[g][q2][e2] = 0;
-#pragma unroll
-            for (int g = 0; g < (W == 30 ? NG : 1); ++g)
-#pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) y[g][q2][e2] = U128{0, 0};
-            issue_s(0, 0);
-            auto baby = [&](int b, size_t so, size_t so_next) {
-                cp_async_wait<0>();
-                __syncthreads();
-                issue_s(b + 1, so_next);
-                const uint32_t pk = pidx(a.galois[b]);
-                const int swp = (int)(pk & 1u);
-                uint64_t x[2][2];  // X~ [poly][coef]
-                if (a.key[b]) {
-                    const uint64_t* dga = reinterpret_cast<const uint64_t*>(s_dig + so) + swp;
-                    const uint64_t* dgb = reinterpret_cast<const uint64_t*>(s_dig + so) + (swp ^ 1);
-                    uint64_t z0[2][2] = {{0, 0}, {0, 0}}, z1[2][2] = {{0, 0}, {0, 0}}, z2[2][2] = {{0, 0}, {0, 0}};
-#pragma unroll
-                    for (int j = 0; j < DN; ++j) {
-                        const ulonglong2 kv0 = s_key[so + (2 * j) * P], kv1 = s_key[so + (2 * j + 1) * P];
-                        const uint64_t dw[2] = {dga[2 * j * P], dgb[2 * j * P]};
-                        const uint64_t kw[2][2] = {{kv0.x, kv0.y}, {kv1.x, kv1.y}};
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            const uint32_t d0 = lo32(dw[e2]), d1 = hi32(dw[e2]);
-                            if constexpr (W == 25) {
-                                const uint32_t ds = d0 + d1;
-#pragma unroll
-                                for (int q2 = 0; q2 < 2; ++q2) {
-                                    const uint32_t k0 = lo32(kw[q2][e2]), k1 = hi32(kw[q2][e2]);
-                                    madw(z0[q2][e2], d0, k0);
-                                    madw(z2[q2][e2], d1, k1);
-                                    madw(z1[q2][e2], ds, k0 + k1);
-                                }
-                            } else {
-#pragma unroll
-                                for (int q2 = 0; q2 < 2; ++q2) {
-                                    const uint32_t k0 = lo32(kw[q2][e2]), k1 = hi32(kw[q2][e2]);
-                                    madw(z0[q2][e2], d0, k0);
-                                    madw(z1[q2][e2], d0, k1);
-                                    madw(z1[q2][e2], d1, k0);
-                                    madw(z2[q2][e2], d1, k1);
-                                }
-                            }
-                        }
-                    }
-                    if constexpr (W == 25) {
-#pragma unroll
-                        for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                            for (int e2 = 0; e2 < 2; ++e2) z1[q2][e2] -= z0[q2][e2] + z2[q2][e2];
-                    } else if constexpr (DN >= 8) {  // keep z1 + the c0 and Montgomery terms below 2^64
-#pragma unroll
-                        for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                            for (int e2 = 0; e2 < 2; ++e2) {
-                                z2[q2][e2] += z1[q2][e2] >> W;
-                                z1[q2][e2] &= MW;
-                            }
-                    }
-                    if (qrow) {  // + [P sigma(c0)]_q in limb form
-                        const uint64_t* cg = reinterpret_cast<const uint64_t*>(s_c0 + so);
-                        const uint64_t cw[2] = {cg[swp], cg[swp ^ 1]};
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            z0[0][e2] += lo32(cw[e2]);
-                            z1[0][e2] += hi32(cw[e2]);
-                        }
-                    }
-#pragma unroll
-                    for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2)
-                            x[q2][e2] = W == 25 ? mont_l25(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv)
-                                                : mont_l30(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv);
-                } else if (qrow) {  // identity: X = [P c]_q
-                    const ulonglong2 c1 = s_dig[so], c0 = s_c0[so];
-                    const uint64_t cw[2][2] = {{c0.x, c0.y}, {c1.x, c1.y}};
-#pragma unroll
-                    for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2)
-                            x[q2][e2] = W == 25 ? mont_l25(lo32(cw[q2][e2]), hi32(cw[q2][e2]), 0, q0, q1, qinv)
-                                                : mont_l30(lo32(cw[q2][e2]), hi32(cw[q2][e2]), 0, q0, q1, qinv);
-                } else {
-                    x[0][0] = x[0][1] = x[1][0] = x[1][1] = 0;
-                }
-                const uint32_t gm = a.gmask[b];
-                if constexpr (W == 25) {
-                    uint32_t xl[2][2], xh[2][2], xs[2][2];
-#pragma unroll
-                    for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            xl[q2][e2] = (uint32_t)x[q2][e2] & MW;
-                            xh[q2][e2] = (uint32_t)(x[q2][e2] >> 25);
-                            xs[q2][e2] = xl[q2][e2] + xh[q2][e2];
-                        }
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        if (!((gm >> g) & 1u)) continue;
-                        const ulonglong2 wv = s_pt[so + g * P];
-                        const uint64_t ww[2] = {wv.x, wv.y};
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            const uint32_t w0 = lo32(ww[e2]), w1 = hi32(ww[e2]), ws = w0 + w1;
-#pragma unroll
-                            for (int q2 = 0; q2 < 2; ++q2) {
-                                madw(b0[g][q2][e2], w0, xl[q2][e2]);
-                                madw(b2[g][q2][e2], w1, xh[q2][e2]);
-                                madw(b1[g][q2][e2], ws, xs[q2][e2]);
-                            }
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        if (!((gm >> g) & 1u)) continue;
-                        const ulonglong2 wv = s_pt[so + g * P];
-                        const uint64_t wa = from_limb(wv.x, 30), wb = from_limb(wv.y, 30);
-                        mac_small(y[g][0][0], wa, x[0][0]);
-                        mac_small(y[g][0][1], wb, x[0][1]);
-                        mac_small(y[g][1][0], wa, x[1][0]);
-                        mac_small(y[g][1][1], wb, x[1][1]);
-                    }
-                    if ((b & 31) == 31) {  // 32 terms < 2^61 * 2^60 each stay below 2^128
-#pragma unroll
-                        for (int g = 0; g < NG; ++g)
-#pragma unroll
-                            for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                                for (int e2 = 0; e2 < 2; ++e2)
-                                    y[g][q2][e2] = U128{reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), 0};
-                    }
-                }
-            };
-            for (int b = 0; b < a.nb; b += 2) {
-                baby(b, 0, S1);
-                if (b + 1 < a.nb) baby(b + 1, S1, 0);
-            }
-            cp_async_wait<0>();
-            if (active) {
-                uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
-                // the Montgomery factor 2^-50 (W = 25) / 2^-90 (W = 30) of every X~ is restored once
-                uint64_t r = reduce64(W == 25 ? (1ULL << 50) : (1ULL << 45), pr);
-                if (W == 30) r = mul_mod(r, r, pr);
-#pragma unroll
-                for (int g = 0; g < NG; ++g) {
-                    if (g >= a.ng) break;
-                    uint64_t o[2][2];
-#pragma unroll
-                    for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            uint64_t lo, hi;
-                            if constexpr (W == 25) {
-                                const uint64_t B0 = b0[g][q2][e2], B2 = b2[g][q2][e2];
-                                const uint64_t mid = b1[g][q2][e2] - B0 - B2;
-                                // Y = B0 + mid 2^25 + B2 2^50 (< 2^112)
-                                const uint64_t t1 = mid << 25, t2 = B2 << 50;
-                                lo = B0 + t1;
-                                hi = (mid >> 39) + (B2 >> 14) + (lo < t1);
-                                lo += t2;
-                                hi += (lo < t2);
-                            } else {
-                                lo = y[g][q2][e2].lo;
-                                hi = y[g][q2][e2].hi;
-                            }
-                            o[q2][e2] = mul_mod(reduce128(hi, lo, pr), r, pr);
-                        }
-                    uint64_t* yg = Ys + (size_t)g * a.y_g_stride;
-                    st2(yg + i, o[0][0], o[0][1]);
-                    st2(yg + total + i, o[1][0], o[1][1]);
-                }
-            }
-        };
-        if (pr.q < (1ULL << 50))
-            run(std::integral_constant<int, 25>{});
-        else
-            run(std::integral_constant<int, 30>{});
-        __syncthreads();  // the next item's first stage reuses stage 0
-    }
-}
-
-// ------------------------------------------------------------ TMA-staged limb baby steps
-// k_bsgs_tma: the limb-form baby steps of k_bsgs_limb (same thread mapping: thread =
-// (coefficient pair, source), P = 128 / SG pairs per CTA) with the operand staging
+// ------------------------------------------------------------ TMA-staged baby steps
+// k_bsgs_tma: the baby steps of k_bsgs_fused on operand-form rows (same thread
+// mapping: thread = (coefficient pair, source), P = 128 / SG pairs per CTA) with the operand staging
 // taken off the compute threads: per baby step ONE thread issues at most four
 // tensor copies (cp.async.bulk.tensor.4d, TMA) that complete on the stage's
 // mbarrier -- the 2 DN key rows of the CTA's block (shared by its SG sources), the
@@ -1320,21 +1043,103 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                 tma_load4(sb + LY::KW + LY::PW, &m.dig, blk, u, 0, s0c, bar);
             }
         };
-        auto run = [&](auto wtag) {
-            constexpr int W = decltype(wtag)::value;
-            constexpr uint32_t MW = LimbConst<W>::M;
-            const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> W);
-            const uint32_t qinv = (uint32_t)pr.qinv & MW;
-            uint64_t b0[W == 25 ? NG : 1][2][2], b1[W == 25 ? NG : 1][2][2], b2[W == 25 ? NG : 1][2][2];
-            U128 y[W == 30 ? NG : 1][2][2];
+        // q < 2^50: FP64 operand form (modarith.cuh): every product is one fmac_d on the
+        // FP64 pipe, the sums stay exact integers below 2^53
+        auto run_fp = [&]() {
+            const ArD ad = make_ard(pr.q);
+            double y[NG][2][2];
 #pragma unroll
-            for (int g = 0; g < (W == 25 ? NG : 1); ++g)
+            for (int g = 0; g < NG; ++g)
 #pragma unroll
                 for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) b0[g][q2][e2] = b1[g][q2][e2] = b2[g][q2][e2] = 0;
+                    for (int e2 = 0; e2 < 2; ++e2) y[g][q2][e2] = 0.0;
+            issue(0, 0);
+            issue(1, 1);
+            auto baby = [&](int b, int st) {
+                mbar_wait(bars + st, (phase >> st) & 1u);
+                phase ^= 1u << st;
+                const ulonglong2* sb = tsb + st * LY::STAGE;
+                const uint32_t pk = pidx(e, a.galois[b]);
+                const int wo = (int)(pk & (uint32_t)(BW - 1));
+                const double* sc = reinterpret_cast<const double*>(sb + LY::KW + LY::PW + LY::DW + slot * 2 * P);
+                double x[2][2];
+                if (m.kidx[b] >= 0) {
+                    const double* sd = reinterpret_cast<const double*>(sb + LY::KW + LY::PW + slot * DN * P);
+                    const double2* sk = reinterpret_cast<const double2*>(sb);
+                    double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                    if (qrow) {  // + [P sigma(c0)]_q
+                        z[0][0] = sc[wo];
+                        z[0][1] = sc[wo ^ 1];
+                    }
 #pragma unroll
-            for (int g = 0; g < (W == 30 ? NG : 1); ++g)
+                    for (int j = 0; j < DN; ++j) {
+                        const double2 k0 = sk[(2 * j) * P + p], k1 = sk[(2 * j + 1) * P + p];
+                        const double d0 = sd[j * BW + wo], d1 = sd[j * BW + (wo ^ 1)];
+                        fmac_d(z[0][0], d0, k0.x, ad);
+                        fmac_d(z[0][1], d1, k0.y, ad);
+                        fmac_d(z[1][0], d0, k1.x, ad);
+                        fmac_d(z[1][1], d1, k1.y, ad);
+                    }
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) x[q2][e2] = red_d(z[q2][e2], ad);
+                } else if (qrow) {  // identity: X = [P c]_q, unpermuted
+                    x[0][0] = sc[2 * p];
+                    x[0][1] = sc[2 * p + 1];
+                    x[1][0] = sc[BW + 2 * p];
+                    x[1][1] = sc[BW + 2 * p + 1];
+                } else {
+                    x[0][0] = x[0][1] = x[1][0] = x[1][1] = 0.0;
+                }
+                const uint32_t gm = a.gmask[b];
+                const double2* sp = reinterpret_cast<const double2*>(sb + LY::KW);
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    if (!((gm >> g) & 1u)) continue;
+                    const double2 w = sp[g * P + p];
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2) {
+                        fmac_d(y[g][q2][0], x[q2][0], w.x, ad);
+                        fmac_d(y[g][q2][1], x[q2][1], w.y, ad);
+                    }
+                }
+                if ((b & 7) == 7) {  // 8 terms of <= 0.5 q + 2^44 each: far below 2^53
+#pragma unroll
+                    for (int g = 0; g < NG; ++g)
+#pragma unroll
+                        for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                            for (int e2 = 0; e2 < 2; ++e2) y[g][q2][e2] = red_d(y[g][q2][e2], ad);
+                }
+                __syncthreads();  // stage st is free: fetch baby b + 2 into it
+                issue(b + 2, st);
+            };
+            for (int b = 0; b < a.nb; b += 2) {
+                baby(b, 0);
+                if (b + 1 < a.nb) baby(b + 1, 1);
+            }
+            if (active) {
+                uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    if (g >= a.ng) break;
+                    uint64_t* yg = Ys + (size_t)g * a.y_g_stride;
+                    st2(yg + i, canon_d(red_d(y[g][0][0], ad), ad), canon_d(red_d(y[g][0][1], ad), ad));
+                    st2(yg + total + i, canon_d(red_d(y[g][1][0], ad), ad), canon_d(red_d(y[g][1][1], ad), ad));
+                }
+            }
+        };
+        // 60-bit primes: 30-bit limb form (four mad.wide.u32 per product, Montgomery by 2^90)
+        auto run_l30 = [&]() {
+            constexpr int W = 30;
+            constexpr uint32_t MW = LimbConst<W>::M;
+            const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> W);
+            const uint32_t qinv = (uint32_t)pr.qinv & MW;
+            U128 y[NG][2][2];
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
 #pragma unroll
                 for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
@@ -1360,33 +1165,17 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
 #pragma unroll
                         for (int e2 = 0; e2 < 2; ++e2) {
                             const uint32_t d0 = lo32(dw[e2]), d1 = hi32(dw[e2]);
-                            if constexpr (W == 25) {
-                                const uint32_t ds = d0 + d1;
 #pragma unroll
-                                for (int q2 = 0; q2 < 2; ++q2) {
-                                    const uint32_t kk0 = lo32(kw[q2][e2]), kk1 = hi32(kw[q2][e2]);
-                                    madw(z0[q2][e2], d0, kk0);
-                                    madw(z2[q2][e2], d1, kk1);
-                                    madw(z1[q2][e2], ds, kk0 + kk1);
-                                }
-                            } else {
-#pragma unroll
-                                for (int q2 = 0; q2 < 2; ++q2) {
-                                    const uint32_t kk0 = lo32(kw[q2][e2]), kk1 = hi32(kw[q2][e2]);
-                                    madw(z0[q2][e2], d0, kk0);
-                                    madw(z1[q2][e2], d0, kk1);
-                                    madw(z1[q2][e2], d1, kk0);
-                                    madw(z2[q2][e2], d1, kk1);
-                                }
+                            for (int q2 = 0; q2 < 2; ++q2) {
+                                const uint32_t kk0 = lo32(kw[q2][e2]), kk1 = hi32(kw[q2][e2]);
+                                madw(z0[q2][e2], d0, kk0);
+                                madw(z1[q2][e2], d0, kk1);
+                                madw(z1[q2][e2], d1, kk0);
+                                madw(z2[q2][e2], d1, kk1);
                             }
                         }
                     }
-                    if constexpr (W == 25) {
-#pragma unroll
-                        for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                            for (int e2 = 0; e2 < 2; ++e2) z1[q2][e2] -= z0[q2][e2] + z2[q2][e2];
-                    } else if constexpr (DN >= 8) {
+                    if constexpr (DN >= 8) {  // keep z1 + the c0 and Montgomery terms below 2^64
 #pragma unroll
                         for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
@@ -1407,66 +1196,36 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                     for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
                         for (int e2 = 0; e2 < 2; ++e2)
-                            x[q2][e2] = W == 25 ? mont_l25(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv)
-                                                : mont_l30(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv);
+                            x[q2][e2] = mont_l30(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv);
                 } else if (qrow) {  // identity: X = [P c]_q, unpermuted
                     const uint64_t cw[2][2] = {{sc[2 * p], sc[2 * p + 1]}, {sc[BW + 2 * p], sc[BW + 2 * p + 1]}};
 #pragma unroll
                     for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
                         for (int e2 = 0; e2 < 2; ++e2)
-                            x[q2][e2] = W == 25 ? mont_l25(lo32(cw[q2][e2]), hi32(cw[q2][e2]), 0, q0, q1, qinv)
-                                                : mont_l30(lo32(cw[q2][e2]), hi32(cw[q2][e2]), 0, q0, q1, qinv);
+                            x[q2][e2] = mont_l30(lo32(cw[q2][e2]), hi32(cw[q2][e2]), 0, q0, q1, qinv);
                 } else {
                     x[0][0] = x[0][1] = x[1][0] = x[1][1] = 0;
                 }
                 const uint32_t gm = a.gmask[b];
-                if constexpr (W == 25) {
-                    uint32_t xl[2][2], xh[2][2], xs[2][2];
 #pragma unroll
-                    for (int q2 = 0; q2 < 2; ++q2)
+                for (int g = 0; g < NG; ++g) {
+                    if (!((gm >> g) & 1u)) continue;
+                    const ulonglong2 wv = sb[LY::KW + g * P + p];
+                    const uint64_t wa = from_limb(wv.x, 30), wb = from_limb(wv.y, 30);
+                    mac_small(y[g][0][0], wa, x[0][0]);
+                    mac_small(y[g][0][1], wb, x[0][1]);
+                    mac_small(y[g][1][0], wa, x[1][0]);
+                    mac_small(y[g][1][1], wb, x[1][1]);
+                }
+                if ((b & 31) == 31) {  // 32 terms < 2^61 * 2^60 each stay below 2^128
 #pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            xl[q2][e2] = (uint32_t)x[q2][e2] & MW;
-                            xh[q2][e2] = (uint32_t)(x[q2][e2] >> 25);
-                            xs[q2][e2] = xl[q2][e2] + xh[q2][e2];
-                        }
+                    for (int g = 0; g < NG; ++g)
 #pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        if (!((gm >> g) & 1u)) continue;
-                        const ulonglong2 wv = sb[LY::KW + g * P + p];
-                        const uint64_t ww[2] = {wv.x, wv.y};
+                        for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            const uint32_t w0 = lo32(ww[e2]), w1 = hi32(ww[e2]), ws = w0 + w1;
-#pragma unroll
-                            for (int q2 = 0; q2 < 2; ++q2) {
-                                madw(b0[g][q2][e2], w0, xl[q2][e2]);
-                                madw(b2[g][q2][e2], w1, xh[q2][e2]);
-                                madw(b1[g][q2][e2], ws, xs[q2][e2]);
-                            }
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        if (!((gm >> g) & 1u)) continue;
-                        const ulonglong2 wv = sb[LY::KW + g * P + p];
-                        const uint64_t wa = from_limb(wv.x, 30), wb = from_limb(wv.y, 30);
-                        mac_small(y[g][0][0], wa, x[0][0]);
-                        mac_small(y[g][0][1], wb, x[0][1]);
-                        mac_small(y[g][1][0], wa, x[1][0]);
-                        mac_small(y[g][1][1], wb, x[1][1]);
-                    }
-                    if ((b & 31) == 31) {
-#pragma unroll
-                        for (int g = 0; g < NG; ++g)
-#pragma unroll
-                            for (int q2 = 0; q2 < 2; ++q2)
-#pragma unroll
-                                for (int e2 = 0; e2 < 2; ++e2)
-                                    y[g][q2][e2] = U128{reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), 0};
-                    }
+                            for (int e2 = 0; e2 < 2; ++e2)
+                                y[g][q2][e2] = U128{reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), 0};
                 }
                 __syncthreads();  // stage st is free: fetch baby b + 2 into it
                 issue(b + 2, st);
@@ -1477,8 +1236,9 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
             }
             if (active) {
                 uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
-                uint64_t r = reduce64(W == 25 ? (1ULL << 50) : (1ULL << 45), pr);
-                if (W == 30) r = mul_mod(r, r, pr);
+                // the Montgomery factor 2^-90 of every X~ is restored once
+                uint64_t r = reduce64(1ULL << 45, pr);
+                r = mul_mod(r, r, pr);
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
                     if (g >= a.ng) break;
@@ -1486,32 +1246,18 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
 #pragma unroll
                     for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            uint64_t lo, hi;
-                            if constexpr (W == 25) {
-                                const uint64_t B0 = b0[g][q2][e2], B2 = b2[g][q2][e2];
-                                const uint64_t mid = b1[g][q2][e2] - B0 - B2;
-                                const uint64_t t1 = mid << 25, t2 = B2 << 50;
-                                lo = B0 + t1;
-                                hi = (mid >> 39) + (B2 >> 14) + (lo < t1);
-                                lo += t2;
-                                hi += (lo < t2);
-                            } else {
-                                lo = y[g][q2][e2].lo;
-                                hi = y[g][q2][e2].hi;
-                            }
-                            o[q2][e2] = mul_mod(reduce128(hi, lo, pr), r, pr);
-                        }
+                        for (int e2 = 0; e2 < 2; ++e2)
+                            o[q2][e2] = mul_mod(reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), r, pr);
                     uint64_t* yg = Ys + (size_t)g * a.y_g_stride;
                     st2(yg + i, o[0][0], o[0][1]);
                     st2(yg + total + i, o[1][0], o[1][1]);
                 }
             }
         };
-        if (pr.q < (1ULL << 50))
-            run(std::integral_constant<int, 25>{});
+        if (opf_fp(pr.q))
+            run_fp();
         else
-            run(std::integral_constant<int, 30>{});
+            run_l30();
     }
 }
 
@@ -1520,7 +1266,7 @@ __global__ void k_rows_to_limb(DevCtx c, uint64_t* dst, const uint64_t* src, siz
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         const int r = (int)((i >> c.logN) % (size_t)rm.rows_per_poly);
         const int pi = rm.level < 0 ? r : row_prime(rm, r);
-        dst[i] = to_limb(src[i], limb_w(c.primes[pi].q));
+        dst[i] = to_opf(src[i], c.primes[pi].q);
     }
 }
 
@@ -1532,7 +1278,7 @@ __global__ void k_ct_prescale(DevCtx c, uint64_t* dst, const uint64_t* ct, size_
         const size_t sidx = i / per, w = i - sidx * per;
         const int u = (int)((w >> c.logN) % (size_t)nr);
         const uint64_t q = c.primes[u].q;
-        dst[i] = to_limb(mul_shoup(ct[sidx * stride + w], md->pmod[u], md->pmod_sh[u], q), limb_w(q));
+        dst[i] = to_opf(mul_shoup(ct[sidx * stride + w], md->pmod[u], md->pmod_sh[u], q), q);
     }
 }
 
@@ -1928,46 +1674,6 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
     } while (0)
     FHE_DN_SWITCH(dn, FHE_FUSED)
 #undef FHE_FUSED
-}
-
-template <int DN, int NG, int SG, int MINB>
-static void launch_limb(const DevCtx& c, const FusedBsgs& a, int level, cudaStream_t st) {
-    using LY = FusedLayout<DN, NG, SG, 2>;
-    const int ne = level + 1 + c.K;
-    const size_t smem = (size_t)2 * LY::STAGE * sizeof(ulonglong2);
-    const size_t items = (size_t)ne * c.N / 2 / LY::P * (size_t)((a.nsrc + SG - 1) / SG);
-    int per_sm = 0;
-    cudaFuncSetAttribute(k_bsgs_limb<DN, NG, SG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_limb<DN, NG, SG, MINB>, 128, smem);
-    if (per_sm < 1) per_sm = 1;
-    const size_t cap = (size_t)sm_count() * per_sm;
-    const int blocks = (int)(items < cap ? items : cap);
-    k_bsgs_limb<DN, NG, SG, MINB><<<blocks, 128, smem, st>>>(c, a, level);
-}
-
-#ifndef FHE_LIMB_MINB
-#define FHE_LIMB_MINB 3
-#endif
-void bsgs_limb(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st) {
-    if (a.nb <= 0 || a.nsrc <= 0 || a.ng <= 0) return;
-    if (a.accumulate || a.digit_slot_stride || a.ct_slot_stride || a.ng > kFusedMaxG)
-        throw std::invalid_argument("bsgs_limb: source slots / accumulation are not supported");
-    ++g_launches;
-    const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
-#define FHE_LIMB(D)                                                                   \
-    do {                                                                              \
-        if (a.ng <= 3) {                                                              \
-            if (sg == 4) launch_limb<D, 3, 4, FHE_LIMB_MINB>(c, a, level, st);        \
-            else if (sg == 2) launch_limb<D, 3, 2, 3>(c, a, level, st);               \
-            else launch_limb<D, 3, 1, 2>(c, a, level, st);                            \
-        } else {                                                                      \
-            if (sg == 4) launch_limb<D, kFusedMaxG, 4, 2>(c, a, level, st);           \
-            else if (sg == 2) launch_limb<D, kFusedMaxG, 2, 2>(c, a, level, st);      \
-            else launch_limb<D, kFusedMaxG, 1, 2>(c, a, level, st);                   \
-        }                                                                             \
-    } while (0)
-    FHE_DN_SWITCH(dn, FHE_LIMB)
-#undef FHE_LIMB
 }
 
 #ifndef FHE_TMA_MINB

@@ -46,6 +46,10 @@ struct DevCtx {
     const uint64_t* itw_sh;
     const uint64_t* ninv;  // [L+K] N^-1 and Shoup
     const uint64_t* ninv_sh;
+    // FP64 NTT companions (primes q < 2^50, ntt.cu): centred twiddle w_c and w_c / q
+    const double2* twd;    // [L+K][N] of psi^brv(k)
+    const double2* itwd;   // [L+K][N] of psi^-brv(k)
+    const double2* ninvd;  // [L+K] of N^-1
 };
 
 // FastBConv constants of ModUp digit j at level l.
@@ -286,12 +290,11 @@ struct FusedBsgs {
     int accumulate;                  // Y_g += (instead of =)
 };
 void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int level, int dn, cudaStream_t st);
-// The same baby steps on limb-form operands (k_bsgs_limb): a.key[b] and
-// a.pt[b] in limb form, a.digits the limb-form ModUp digits, a.ct the limb-form P-scaled
-// ciphertexts [P c]_q ([2][level+1][N] per source, ct_prescale). Same Y (normal form,
-// bit-identical). No source slots / accumulation, ng <= kFusedMaxG.
-void bsgs_limb(const DevCtx& c, const FusedBsgs& a, int level, int dn, cudaStream_t st);
-// The same with TMA tensor-copy staging (k_bsgs_tma). The four 4-D maps
+// The same baby steps on operand-form rows (modarith.cuh to_opf) with
+// TMA tensor-copy staging (k_bsgs_tma): a.key[b] and a.pt[b] in operand form, a.digits
+// the operand-form ModUp digits, a.ct the operand-form P-scaled ciphertexts [P c]_q
+// ([2][level+1][N] per source, ct_prescale). Same Y (normal form, bit-identical).
+// No source slots / accumulation, ng <= kFusedMaxG. The four 4-D maps
 // (innermost dimension first, 8-byte elements) and their boxes, P2 = 2 * 128 / SG
 // coefficients per CTA block (tma_sources(nsrc) = SG):
 //   key: limb keys [nkeys][2 dnum][L+K][N],  box {P2, 1, 2 dn, 1}, coords (k0, prime, 0, kidx[b])
@@ -311,11 +314,11 @@ inline int tma_sources(int nsrc) { return nsrc >= 4 ? 4 : nsrc >= 2 ? 2 : 1; }
 void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st);
 // encode a 4-D uint64 tensor map (dims innermost first, dense)
 void tma_map4(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint32_t box[4]);
-// dst[i] = to_limb(src[i]) for nrows rows of N words; row r uses prime
+// dst[i] = to_opf(src[i]) for nrows rows of N words; row r uses prime
 // row_prime(rm, r % rm.rows_per_poly) (rm.level < 0: prime index r % rows_per_poly)
 void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,
                   cudaStream_t st);
-// dst[s][p][u] = to_limb([P ct_s[p][u]]_{q_u}) for nsrc ciphertexts at ct + s * stride ([2][level+1][N])
+// dst[s][p][u] = to_opf([P ct_s[p][u]]_{q_u}) for nsrc ciphertexts at ct + s * stride ([2][level+1][N])
 void ct_prescale(const DevCtx& c, uint64_t* dst, const uint64_t* ct, size_t stride, int nsrc, const ModDownTable* md,
                  int level, cudaStream_t st);
 // acc += y over [2][ne][N] (QP basis)

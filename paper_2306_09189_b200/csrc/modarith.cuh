@@ -177,14 +177,81 @@ FHE_HD U128 fold3(const Acc3& A) {
     return U128{lo, hi};
 }
 
-// ------------------------------------------------------------------ limb form
-// A residue v < q < 2^60 in limb form is the word (v >> W) << 32 | (v mod 2^W) with
-// W = 25 when q < 2^50 and W = 30 otherwise: its two 32-bit halves
-// feed mad.wide.u32 directly, so sums of limb products need no carry handling
-// (k_bsgs_limb). Used only for operands of the fused baby-step kernel.
-FHE_HD int limb_w(uint64_t q) { return q < (1ULL << 50) ? 25 : 30; }
+// ------------------------------------------------------------------ operand form
+// Operands of the fused baby-step kernel (k_bsgs_tma) are stored in
+// an "operand form" chosen per prime:
+//  q < 2^50: the centred residue (-q/2, q/2] as an IEEE double (exact): the
+//            products run on the FP64 pipe (kernels.cu fmac_d);
+//  else:     30-bit limb form, the word (v >> 30) << 32 | (v mod 2^30), whose two
+//            32-bit halves feed mad.wide.u32 directly.
 FHE_HD uint64_t to_limb(uint64_t v, int w) { return ((v >> w) << 32) | (v & ((1ULL << w) - 1)); }
 FHE_HD uint64_t from_limb(uint64_t l, int w) { return ((l >> 32) << w) | (l & 0xffffffffULL); }
+FHE_HD bool opf_fp(uint64_t q) { return q < (1ULL << 50); }
+FHE_HD uint64_t dbl_bits(double d) {
+#ifdef __CUDA_ARCH__
+    return (uint64_t)__double_as_longlong(d);
+#else
+    uint64_t b;
+    __builtin_memcpy(&b, &d, 8);
+    return b;
+#endif
+}
+FHE_HD uint64_t to_opf(uint64_t v, uint64_t q) {
+    if (opf_fp(q)) return dbl_bits(v > q / 2 ? -(double)(q - v) : (double)v);
+    return to_limb(v, 30);
+}
+#ifdef __CUDACC__
+// ------------------------------------------------------------------ FP64 residues
+// Exact modular arithmetic on the FP64 pipe for primes q < 2^50:
+// residues are integer-valued doubles, and every step below is exact because
+// its true result is an integer below 2^53 in magnitude.
+//  mulmod_d(x, w_c, w_c/q): t = rint(x w_c / q) by magic-constant rounding
+//    (|x w_c / q| < 2^51), (ph, pl) the exact product split in two doubles,
+//    r = (ph - t q) + pl; |r| <= 0.625 q for |x| < 2^52 and |w_c| <= q/2.
+//  fmac_d(acc, x, y): acc += x y mod q without a per-operand quotient
+//    (t = rint(ph / q)); |x y| <= q^2 / 4 adds <= 0.5 q + 2^44 to acc.
+//  red_d(x) = x - q rint(x / q): |result| <= 0.5 q + 1 for |x| < 2^53.
+struct ArD {
+    double q, qinv, qm;  // q, 1/q, 2^52 + q
+    uint64_t qi;
+};
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;  // 2^52
+
+__device__ __forceinline__ ArD make_ard(uint64_t q) {
+    const double qd = (double)q;
+    return ArD{qd, __drcp_rn(qd), __dadd_rn(qd, kTwo52), q};
+}
+__device__ __forceinline__ double red_d(double x, const ArD& a) {
+    const double t = __dadd_rn(__fma_rn(x, a.qinv, kMagic), -kMagic);
+    return __fma_rn(-t, a.q, x);
+}
+__device__ __forceinline__ double mulmod_d(double x, double w, double wq, const ArD& a) {
+    const double t = __dadd_rn(__fma_rn(x, wq, kMagic), -kMagic);
+    const double ph = __dmul_rn(x, w);
+    const double pl = __fma_rn(x, w, -ph);
+    return __dadd_rn(__fma_rn(-t, a.q, ph), pl);
+}
+__device__ __forceinline__ void fmac_d(double& acc, double x, double y, const ArD& a) {
+    const double ph = __dmul_rn(x, y);
+    const double pl = __fma_rn(x, y, -ph);
+    const double t = __dadd_rn(__fma_rn(ph, a.qinv, kMagic), -kMagic);
+    acc = __dadd_rn(acc, __dadd_rn(__fma_rn(-t, a.q, ph), pl));
+}
+// canonical word in [0, q) -> bits of the same value as a double (exact)
+__device__ __forceinline__ uint64_t u2d_bits(uint64_t x) {
+    return (uint64_t)__double_as_longlong(
+        __dadd_rn(__longlong_as_double((long long)(x | 0x4330000000000000ULL)), -kTwo52));
+}
+// |x| <= 0.625 q -> canonical word in [0, q)
+__device__ __forceinline__ uint64_t canon_d(double x, const ArD& a) {
+    const uint64_t u = (uint64_t)__double_as_longlong(__dadd_rn(x, a.qm)) - 0x4330000000000000ULL;  // x + q
+    return u >= a.qi ? u - a.qi : u;
+}
+__device__ __forceinline__ double asd(uint64_t b) { return __longlong_as_double((long long)b); }
+__device__ __forceinline__ uint64_t asu(double d) { return (uint64_t)__double_as_longlong(d); }
+#endif
+
 #ifdef __CUDACC__
 // acc += a b (one IMAD.WIDE.U32 with a 64-bit addend)
 __device__ __forceinline__ void madw(uint64_t& acc, uint32_t a, uint32_t b) {

@@ -181,6 +181,144 @@ __device__ __forceinline__ void inv_local(uint64_t* vec, int lt, int log_ntot, i
     }
 }
 
+// ------------------------------------------------------------ FP64 butterflies
+// For primes q < 2^50 the butterflies run on the FP64 pipe (the integer
+// multiply pipe is the NTT's bound, and the FP64 pipe is otherwise idle).
+// Residues are exact integer-valued doubles, signed, |x| < 2^52 = 4q at the
+// least; magnitudes are tracked in units of q/8 at compile time (the
+// unrolled loops constant-fold them), and every operation is exact:
+//  mulmod_d(x, w_c, w_c/q): t = rint(x w_c/q) (magic-constant rounding,
+//    |x w_c/q| < 2^51), (ph, pl) = exact product x w_c split in two doubles,
+//    r = (ph - t q) + pl: both steps are exact because the true values are
+//    integers below 2^53. |r| <= 0.625 q for |x| < 2^52 and centred w_c.
+//  red_d(x) = x - q rint(x / q): |result| <= 0.5 q + 1 (5 units).
+// Sums U +- r are exact while they stay below 2^53. Values enter from
+// canonical [0, q) words (8 units) and leave through canon_d (exact [0, q)).
+// The FP64 helpers (ArD, mulmod_d, red_d, canon_d) are in modarith.cuh.
+constexpr int kUnitQ = 8, kUnitMul = 5, kUnitRed = 5, kUnitMax = 32;  // in q / 8
+
+
+// Forward CT pass of R <= 4 stages on doubles (inputs <= 8 units: <= 28 after).
+template <int R>
+__device__ __forceinline__ void fwd_pass_d(double (&v)[EPT], int G0, int logn, int sigma0, int s0, int blk,
+                                           const double2* __restrict__ tw, const ArD& a) {
+    constexpr int GS = 1 << R;
+    const int logt = logn - sigma0 - 1;
+    const int logd = logt - (R - 1);
+#pragma unroll
+    for (int g = 0; g < EPT / GS; ++g) {
+        const int G = G0 + g;
+        const int j0 = ((G >> logd) << (logd + R)) | (G & ((1 << logd) - 1));
+#pragma unroll
+        for (int rho = 0; rho < R; ++rho) {
+            const int half = 1 << (R - 1 - rho);
+            const int sig = sigma0 + rho;
+            const double2* twb = tw + (1 << (s0 + sig)) + (blk << sig) + (j0 >> (logt + 1 - rho));
+#pragma unroll
+            for (int k = 0; k < GS; ++k) {
+                if (k & half) continue;
+                const double2 w = __ldg(twb + (k >> (R - rho)));
+                const double r = mulmod_d(v[g * GS + k + half], w.x, w.y, a);
+                const double U = v[g * GS + k];
+                v[g * GS + k] = __dadd_rn(U, r);
+                v[g * GS + k + half] = __dadd_rn(U, -r);
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) v[e] = red_d(v[e], a);  // <= 5 units for the next pass
+}
+
+// Inverse GS pass of R stages on doubles; sums are reduced only when the
+// tracked bound of a butterfly's inputs would pass 4q. Leaves <= 8 units.
+template <int R>
+__device__ __forceinline__ void inv_pass_d(double (&v)[EPT], int G0, int logt, int log_ntot, int log_nloc, int blk,
+                                           const double2* __restrict__ tw, const ArD& a) {
+    constexpr int GS = 1 << R;
+#pragma unroll
+    for (int g = 0; g < EPT / GS; ++g) {
+        const int G = G0 + g;
+        const int j0 = ((G >> logt) << (logt + R)) | (G & ((1 << logt) - 1));
+        int bd[GS];
+#pragma unroll
+        for (int k = 0; k < GS; ++k) bd[k] = kUnitQ;
+#pragma unroll
+        for (int rho = 0; rho < R; ++rho) {
+            const int half = 1 << rho;
+            const int lt = logt + rho;
+            const double2* twb = tw + (1 << (log_ntot - lt - 1)) + (blk << (log_nloc - lt - 1)) + (j0 >> (lt + 1));
+#pragma unroll
+            for (int k = 0; k < GS; ++k) {
+                if (k & half) continue;
+                const double2 w = __ldg(twb + (k >> (rho + 1)));
+                double U = v[g * GS + k], V = v[g * GS + k + half];
+                if (bd[k] + bd[k + half] > kUnitMax) {
+                    U = red_d(U, a);
+                    V = red_d(V, a);
+                    bd[k] = bd[k + half] = kUnitRed;
+                }
+                v[g * GS + k] = __dadd_rn(U, V);
+                bd[k] += bd[k + half];
+                v[g * GS + k + half] = mulmod_d(__dadd_rn(U, -V), w.x, w.y, a);
+                bd[k + half] = kUnitMul;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < GS; ++k)
+            if (bd[k] > kUnitQ) v[g * GS + k] = red_d(v[g * GS + k], a);
+    }
+}
+
+template <int R, int LOGN, int SIGMA0, bool WARP_SYNC>
+__device__ __forceinline__ void fwd_step_d(uint64_t* vec, int lt, int s0, int blk, const double2* tw, const ArD& a) {
+    double v[EPT];
+    const int G0 = lt * (EPT >> R);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) v[e] = asd(vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))]);
+    fwd_pass_d<R>(v, G0, LOGN, SIGMA0, s0, blk, tw, a);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))] = asu(v[e]);
+    if (WARP_SYNC)
+        __syncwarp();
+    else
+        __syncthreads();
+}
+
+template <int LOGN, int SIGMA0, bool WARP_SYNC>
+__device__ __forceinline__ void fwd_local_d(uint64_t* vec, int lt, int s0, int blk, const double2* tw, const ArD& a) {
+    if constexpr (SIGMA0 < LOGN) {
+        constexpr int R = (LOGN - SIGMA0) >= LOG_EPT ? LOG_EPT : (LOGN - SIGMA0);
+        fwd_step_d<R, LOGN, SIGMA0, WARP_SYNC>(vec, lt, s0, blk, tw, a);
+        fwd_local_d<LOGN, SIGMA0 + R, WARP_SYNC>(vec, lt, s0, blk, tw, a);
+    }
+}
+
+template <int R, int LOGN, int LOGT, bool WARP_SYNC>
+__device__ __forceinline__ void inv_step_d(uint64_t* vec, int lt, int log_ntot, int blk, const double2* tw,
+                                           const ArD& a) {
+    double v[EPT];
+    const int G0 = lt * (EPT >> R);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) v[e] = asd(vec[pad(inv_pos<R>(G0, e, LOGT))]);
+    inv_pass_d<R>(v, G0, LOGT, log_ntot, LOGN, blk, tw, a);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) vec[pad(inv_pos<R>(G0, e, LOGT))] = asu(v[e]);
+    if (WARP_SYNC)
+        __syncwarp();
+    else
+        __syncthreads();
+}
+
+template <int LOGN, int LOGT, bool WARP_SYNC>
+__device__ __forceinline__ void inv_local_d(uint64_t* vec, int lt, int log_ntot, int blk, const double2* tw,
+                                            const ArD& a) {
+    if constexpr (LOGT < LOGN) {
+        constexpr int R = (LOGT == 0 && LOGN % LOG_EPT != 0) ? LOGN % LOG_EPT : LOG_EPT;
+        inv_step_d<R, LOGN, LOGT, WARP_SYNC>(vec, lt, log_ntot, blk, tw, a);
+        inv_local_d<LOGN, LOGT + R, WARP_SYNC>(vec, lt, log_ntot, blk, tw, a);
+    }
+}
+
 __device__ __forceinline__ bool skip_row(const RowMap& rm, int row, int u) {
     if (!rm.skip_alpha) return false;
     int j = row / rm.rows_per_poly;
@@ -190,15 +328,13 @@ __device__ __forceinline__ bool skip_row(const RowMap& rm, int row, int u) {
     return u >= lo && u < hi;
 }
 
-// Fused-operand modes of the two NTT passes:
+// Fused-operand modes of the row pass:
 //  FUSE_NONE    : transform `data` in place;
-//  FUSE_MODUP   : forward; the column pass computes ModUp's FastBConv of the
-//                 digit on the fly from the INTT'd source rows and writes the
-//                 digit rows (own-prime rows are copied from the NTT input);
-//  FUSE_MODDOWN : forward; the column pass computes ModDown's FastBConv of the
-//                 special-prime rows, the row pass writes
-//                 out = (acc - NTT(conv)) P^-1 (+ sigma_g(add_src) on poly 0).
-enum { FUSE_NONE = 0, FUSE_MODUP = 1, FUSE_MODDOWN = 2 };
+//  FUSE_MODDOWN : forward; the row pass writes out = (acc - NTT(conv)) P^-1
+//                 (+ sigma_g(add_src) on poly 0, or the conv bias).
+// ModUp's FastBConv is a separate kernel (k_bconv_modup) ahead of the forward
+// transform of the extended rows.
+enum { FUSE_NONE = 0, FUSE_MODDOWN = 2 };
 
 // Phase A (columns). CTA = C columns x N1 rows; N1/8 threads per column.
 template <int LOG_N1, int C, bool INVERSE, int FUSE>
@@ -212,10 +348,14 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_cols(DevCtx c, uint64_t* da
     const int B = c.N >> LOG_N1;
     const int col0 = blockIdx.x * C;
     uint64_t* a = data + (size_t)row * c.N;
-    int p;
+    if (skip_row(rm, row, u)) return;
+    const int p = row_prime(rm, u);
+    const uint64_t q = c.primes[p].q;
+    // FP64 butterflies for q < 2^50. Forward: canonical words in, reduced doubles
+    // out (read by the row pass); inverse: doubles from the row pass in,
+    // canonical words out.
+    const bool fp = q < (1ULL << 50);
     {
-        if (skip_row(rm, row, u)) return;
-        p = row_prime(rm, u);
         // coalesced load: consecutive threads take consecutive columns of a row;
         // all EPT loads are issued before the shared-memory stores
         uint64_t tmp[EPT];
@@ -227,12 +367,32 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_cols(DevCtx c, uint64_t* da
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
             const int i = threadIdx.x + e * NTT_THREADS;
-            sm[(i % C) * PN + pad(i / C)] = tmp[e];
+            sm[(i % C) * PN + pad(i / C)] = (fp && !INVERSE) ? u2d_bits(tmp[e]) : tmp[e];
         }
     }
-    const uint64_t q = c.primes[p].q;
     __syncthreads();
     const int cc = threadIdx.x / TPC, lt = threadIdx.x % TPC;
+    if (fp) {
+        const ArD ad = make_ard(q);
+        if (!INVERSE) {
+            fwd_local_d<LOG_N1, 0, false>(sm + cc * PN, lt, 0, 0, c.twd + (size_t)p * c.N, ad);
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) {
+                const int i = threadIdx.x + e * NTT_THREADS;
+                a[(size_t)(i / C) * B + col0 + i % C] = sm[(i % C) * PN + pad(i / C)];
+            }
+        } else {
+            inv_local_d<LOG_N1, 0, false>(sm + cc * PN, lt, LOG_N1, 0, c.itwd + (size_t)p * c.N, ad);
+            const double2 ni = c.ninvd[p];
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) {
+                const int i = threadIdx.x + e * NTT_THREADS;
+                a[(size_t)(i / C) * B + col0 + i % C] =
+                    canon_d(mulmod_d(asd(sm[(i % C) * PN + pad(i / C)]), ni.x, ni.y, ad), ad);
+            }
+        }
+        return;
+    }
     if (!INVERSE) {
         fwd_local<LOG_N1, 0, false>(sm + cc * PN, lt, 0, 0, c.tw + (size_t)p * c.N, c.tw_sh + (size_t)p * c.N, q);
     } else {
@@ -276,6 +436,11 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
     const uint64_t q = c.primes[p].q;
     const int blk0 = blockIdx.x * BPC;
     uint64_t* a = data + (size_t)row * c.N + (size_t)blk0 * B;
+    // FP64 butterflies for q < 2^50 (see k_ntt_cols): forward reads the column
+    // pass's doubles and normalises them here; inverse reads canonical words and
+    // leaves doubles for the column pass
+    const bool fp = q < (1ULL << 50);
+    const ArD ad = make_ard(q);
     {
         uint64_t tmp[EPT];
 #pragma unroll
@@ -283,13 +448,18 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
             const int i = threadIdx.x + e * NTT_THREADS;
-            sm[(i / B) * PB + pad(i % B)] = tmp[e];
+            sm[(i / B) * PB + pad(i % B)] = (fp && INVERSE) ? u2d_bits(tmp[e]) : tmp[e];
         }
     }
     __syncthreads();
     const int bi = threadIdx.x / TPB, lt = threadIdx.x % TPB;
     constexpr bool WS = TPB <= 32;
-    if (!INVERSE) {
+    if (fp) {
+        if (!INVERSE)
+            fwd_local_d<LOG_B, 0, WS>(sm + bi * PB, lt, LOG_N1, blk0 + bi, c.twd + (size_t)p * c.N, ad);
+        else
+            inv_local_d<LOG_B, 0, WS>(sm + bi * PB, lt, LOG_N1 + LOG_B, blk0 + bi, c.itwd + (size_t)p * c.N, ad);
+    } else if (!INVERSE) {
         fwd_local<LOG_B, 0, WS>(sm + bi * PB, lt, LOG_N1, blk0 + bi, c.tw + (size_t)p * c.N,
                                 c.tw_sh + (size_t)p * c.N, q);
     } else {
@@ -297,9 +467,15 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
                                 c.itw_sh + (size_t)p * c.N, q);
     }
     __syncthreads();
-    if (!INVERSE) {
-        // forward transform ends here: normalise [0, 4q) -> [0, q)
+    // forward output word of smem slot i: [0, 4q) lazy integer or reduced double -> [0, q)
+    auto fwd_out = [&](int i) -> uint64_t {
+        const uint64_t w = sm[(i / B) * PB + pad(i % B)];
+        if (fp) return canon_d(asd(w), ad);
         const uint64_t q2 = 2 * q;
+        const uint64_t x = w >= q2 ? w - q2 : w;
+        return x >= q ? x - q : x;
+    };
+    if (!INVERSE) {
         if (FUSE == FUSE_MODDOWN) {
             const int pp = row / rm.rows_per_poly;
             const int nr = rm.level + 1, ne = nr + c.K;
@@ -334,9 +510,7 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
 #pragma unroll
             for (int e = 0; e < EPT; ++e) {
                 const int i = threadIdx.x + e * NTT_THREADS;
-                uint64_t x = sm[(i / B) * PB + pad(i % B)];
-                x = x >= q2 ? x - q2 : x;
-                x = x >= q ? x - q : x;
+                const uint64_t x = fwd_out(i);
                 uint64_t o = mul_shoup(sub_mod(av[e], x, q), pi, pis, q);
                 if (add) o = add_mod(o, sv[e], q);
                 out[i] = o;
@@ -345,10 +519,8 @@ __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* da
 #pragma unroll
             for (int e = 0; e < EPT; ++e) {
                 const int i = threadIdx.x + e * NTT_THREADS;
-                uint64_t x = sm[(i / B) * PB + pad(i % B)];
-                x = x >= q2 ? x - q2 : x;
-                x = x >= q ? x - q : x;
-                a[i] = rm.limb ? to_limb(x, limb_w(q)) : x;
+                const uint64_t x = fwd_out(i);
+                a[i] = rm.limb ? to_opf(x, q) : x;
             }
         }
     } else {
@@ -423,8 +595,7 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
                 // sources, c1 == nullptr) the coefficients themselves, transformed later
                 ulonglong2 own = c1 ? __ldcs(reinterpret_cast<const ulonglong2*>(c1 + (size_t)qi * c.N + k)) : x;
                 if (fz.limb && c1) {
-                    const int w = limb_w(q);
-                    own = make_ulonglong2(to_limb(own.x, w), to_limb(own.y, w));
+                    own = make_ulonglong2(to_opf(own.x, q), to_opf(own.y, q));
                 }
                 *reinterpret_cast<ulonglong2*>(out + (size_t)qi * c.N) = own;
             }

@@ -1,12 +1,14 @@
-"""GPU parity of the TMA-staged limb baby-step kernel (k_bsgs_tma, the default for
-approach 5) on the shapes its staging has to get right:
+"""GPU parity of the TMA-staged operand-form baby-step kernel (k_bsgs_tma, the default
+for approach 5: FP64 products on rows q < 2^50, 30-bit limbs on the 60-bit rows) on the
+shapes its staging has to get right:
 
 * plaintext boxes across giant chunks (7x7 kernel: 7 giants = a 5-giant and a
   2-giant launch) and 5-giant launches (5x5);
 * partial source groups (batches of 3, 5 and 6: the last group's box is shifted
   back inside the tensor) and single ciphertexts;
-* the three fused kernels (k_bsgs_fused, k_bsgs_limb, k_bsgs_tma) give identical
-  residues at cfg3 (FHECONV_LIMB / FHECONV_TMA select them per context).
+* the two fused kernels (k_bsgs_fused on plain rows, k_bsgs_tma on operand-form
+  rows) give identical residues at cfg3, cfg1 (40-bit rows) and cfg4 (FHECONV_TMA=0
+  selects k_bsgs_fused per context).
 
 Residues are compared bit-exact with the golden model's approach-5 conv (reference
 schedule: conv_plan conv.cpp:266-271 over the fused plaintexts conv.cpp:69-85).
@@ -43,20 +45,21 @@ def test_tma_giant_chunks_and_partial_groups_bit_exact(oracle, k):
                 assert np.array_equal(outs[i].residues(), refs[i]), f"k={k} batch {B} member {i}"
 
 
-def test_fused_limb_tma_kernels_identical_cfg3(oracle):
+@pytest.mark.parametrize("cfg,geo,B", [("cfg3", (16, 32, 3), 5), ("cfg1", (4, 32, 3), 6), ("cfg4", (8, 64, 5), 2)])
+def test_fused_and_tma_kernels_identical(oracle, cfg, geo, B):
     from paper_2306_09189_b200 import Context
     rng = np.random.default_rng(5)
-    c, m, k = 16, 32, 3
+    c, m, k = geo
     filt = rng.uniform(-1, 1, c * c * k * k)
-    imgs = [rng.uniform(-1, 1, c * m * m) for _ in range(5)]
+    imgs = [rng.uniform(-1, 1, c * m * m) for _ in range(B)]
     res = {}
-    for name, env in (("fused", {"FHECONV_LIMB": "0"}), ("limb", {"FHECONV_TMA": "0"}), ("tma", {})):
+    for name, env in (("fused", {"FHECONV_TMA": "0"}), ("tma", {})):
         old = {v: os.environ.get(v) for v in ("FHECONV_LIMB", "FHECONV_TMA")}
         for v in old:
             os.environ.pop(v, None)
         os.environ.update(env)
         try:
-            ctx = Context.from_config("cfg3")
+            ctx = Context.from_config(cfg)
         finally:
             for v, x in old.items():
                 if x is None:
@@ -72,6 +75,5 @@ def test_fused_limb_tma_kernels_identical_cfg3(oracle):
         single = ctx.conv2d(cts[0], layer, 5)
         res[name] = [o.residues() for o in outs] + [single.residues()]
         del ctx
-    for name in ("limb", "tma"):
-        for a, b in zip(res["fused"], res[name]):
-            assert np.array_equal(a, b), name
+    for a, b in zip(res["fused"], res["tma"]):
+        assert np.array_equal(a, b)
