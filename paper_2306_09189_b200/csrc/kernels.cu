@@ -1677,7 +1677,7 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
 }
 
 #ifndef FHE_TMA_MINB
-#define FHE_TMA_MINB 3
+#define FHE_TMA_MINB 4
 #endif
 template <int DN, int NG, int SG, int MINB>
 static void launch_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, cudaStream_t st) {

@@ -126,61 +126,6 @@ __device__ __forceinline__ int inv_pos(int G0, int e, int logt) {
     return j0 + (k << logt);
 }
 
-// Run all forward stages of a local vector of 2^LOGN elements held in smem
-// (element x at vec[pad(x)]); 2^LOGN / EPT cooperating threads, lt = lane.
-template <int R, int LOGN, int SIGMA0, bool WARP_SYNC>
-__device__ __forceinline__ void fwd_step(uint64_t* vec, int lt, int s0, int blk, const uint64_t* tw,
-                                         const uint64_t* tws, uint64_t q) {
-    uint64_t v[EPT];
-    const int G0 = lt * (EPT >> R);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) v[e] = vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))];
-    fwd_pass<R>(v, G0, LOGN, SIGMA0, s0, blk, tw, tws, q);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))] = v[e];
-    if (WARP_SYNC)
-        __syncwarp();
-    else
-        __syncthreads();
-}
-
-template <int LOGN, int SIGMA0, bool WARP_SYNC>
-__device__ __forceinline__ void fwd_local(uint64_t* vec, int lt, int s0, int blk, const uint64_t* tw,
-                                          const uint64_t* tws, uint64_t q) {
-    if constexpr (SIGMA0 < LOGN) {
-        constexpr int R = (LOGN - SIGMA0) >= LOG_EPT ? LOG_EPT : (LOGN - SIGMA0);
-        fwd_step<R, LOGN, SIGMA0, WARP_SYNC>(vec, lt, s0, blk, tw, tws, q);
-        fwd_local<LOGN, SIGMA0 + R, WARP_SYNC>(vec, lt, s0, blk, tw, tws, q);
-    }
-}
-
-template <int R, int LOGN, int LOGT, bool WARP_SYNC>
-__device__ __forceinline__ void inv_step(uint64_t* vec, int lt, int log_ntot, int blk, const uint64_t* tw,
-                                         const uint64_t* tws, uint64_t q) {
-    uint64_t v[EPT];
-    const int G0 = lt * (EPT >> R);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) v[e] = vec[pad(inv_pos<R>(G0, e, LOGT))];
-    inv_pass<R>(v, G0, LOGT, log_ntot, LOGN, blk, tw, tws, q);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) vec[pad(inv_pos<R>(G0, e, LOGT))] = v[e];
-    if (WARP_SYNC)
-        __syncwarp();
-    else
-        __syncthreads();
-}
-
-// inverse passes in growing distance; the first pass takes LOGN mod LOG_EPT stages
-template <int LOGN, int LOGT, bool WARP_SYNC>
-__device__ __forceinline__ void inv_local(uint64_t* vec, int lt, int log_ntot, int blk, const uint64_t* tw,
-                                          const uint64_t* tws, uint64_t q) {
-    if constexpr (LOGT < LOGN) {
-        constexpr int R = (LOGT == 0 && LOGN % LOG_EPT != 0) ? LOGN % LOG_EPT : LOG_EPT;
-        inv_step<R, LOGN, LOGT, WARP_SYNC>(vec, lt, log_ntot, blk, tw, tws, q);
-        inv_local<LOGN, LOGT + R, WARP_SYNC>(vec, lt, log_ntot, blk, tw, tws, q);
-    }
-}
-
 // ------------------------------------------------------------ FP64 butterflies
 // For primes q < 2^50 the butterflies run on the FP64 pipe (the integer
 // multiply pipe is the NTT's bound, and the FP64 pipe is otherwise idle).
@@ -269,56 +214,6 @@ __device__ __forceinline__ void inv_pass_d(double (&v)[EPT], int G0, int logt, i
     }
 }
 
-template <int R, int LOGN, int SIGMA0, bool WARP_SYNC>
-__device__ __forceinline__ void fwd_step_d(uint64_t* vec, int lt, int s0, int blk, const double2* tw, const ArD& a) {
-    double v[EPT];
-    const int G0 = lt * (EPT >> R);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) v[e] = asd(vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))]);
-    fwd_pass_d<R>(v, G0, LOGN, SIGMA0, s0, blk, tw, a);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) vec[pad(fwd_pos<R>(G0, e, LOGN, SIGMA0))] = asu(v[e]);
-    if (WARP_SYNC)
-        __syncwarp();
-    else
-        __syncthreads();
-}
-
-template <int LOGN, int SIGMA0, bool WARP_SYNC>
-__device__ __forceinline__ void fwd_local_d(uint64_t* vec, int lt, int s0, int blk, const double2* tw, const ArD& a) {
-    if constexpr (SIGMA0 < LOGN) {
-        constexpr int R = (LOGN - SIGMA0) >= LOG_EPT ? LOG_EPT : (LOGN - SIGMA0);
-        fwd_step_d<R, LOGN, SIGMA0, WARP_SYNC>(vec, lt, s0, blk, tw, a);
-        fwd_local_d<LOGN, SIGMA0 + R, WARP_SYNC>(vec, lt, s0, blk, tw, a);
-    }
-}
-
-template <int R, int LOGN, int LOGT, bool WARP_SYNC>
-__device__ __forceinline__ void inv_step_d(uint64_t* vec, int lt, int log_ntot, int blk, const double2* tw,
-                                           const ArD& a) {
-    double v[EPT];
-    const int G0 = lt * (EPT >> R);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) v[e] = asd(vec[pad(inv_pos<R>(G0, e, LOGT))]);
-    inv_pass_d<R>(v, G0, LOGT, log_ntot, LOGN, blk, tw, a);
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) vec[pad(inv_pos<R>(G0, e, LOGT))] = asu(v[e]);
-    if (WARP_SYNC)
-        __syncwarp();
-    else
-        __syncthreads();
-}
-
-template <int LOGN, int LOGT, bool WARP_SYNC>
-__device__ __forceinline__ void inv_local_d(uint64_t* vec, int lt, int log_ntot, int blk, const double2* tw,
-                                            const ArD& a) {
-    if constexpr (LOGT < LOGN) {
-        constexpr int R = (LOGT == 0 && LOGN % LOG_EPT != 0) ? LOGN % LOG_EPT : LOG_EPT;
-        inv_step_d<R, LOGN, LOGT, WARP_SYNC>(vec, lt, log_ntot, blk, tw, a);
-        inv_local_d<LOGN, LOGT + R, WARP_SYNC>(vec, lt, log_ntot, blk, tw, a);
-    }
-}
-
 __device__ __forceinline__ bool skip_row(const RowMap& rm, int row, int u) {
     if (!rm.skip_alpha) return false;
     int j = row / rm.rows_per_poly;
@@ -336,82 +231,110 @@ __device__ __forceinline__ bool skip_row(const RowMap& rm, int row, int u) {
 // transform of the extended rows.
 enum { FUSE_NONE = 0, FUSE_MODDOWN = 2 };
 
-// Phase A (columns). CTA = C columns x N1 rows; N1/8 threads per column.
-template <int LOG_N1, int C, bool INVERSE, int FUSE>
-__global__ void __launch_bounds__(NTT_THREADS) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
+// ------------------------------------------------------------ the two NTT kernels
+// Both phases run two register passes per thread (EPT = 16 residues, radix-16 /
+// radix-2^R2), with exactly one shared-memory exchange between them; residues
+// are read from and written to global memory straight from the registers of
+// the pass that owns them (coalesced: consecutive threads own consecutive
+// columns, or the pass's stride-TPB residues of a block; a thread's 16
+// contiguous residues of the row pass move with 256-bit accesses).
+template <int LOGN, bool INVERSE>
+struct PassPlan {  // stages of the two passes of a phase of 2^LOGN elements
+    static constexpr int R1 = INVERSE ? (LOGN % LOG_EPT ? LOGN % LOG_EPT : LOG_EPT) : LOG_EPT;
+    static constexpr int R2 = LOGN - R1;
+    static_assert(R2 >= 1 && R2 <= LOG_EPT, "two passes per phase");
+    __device__ static int pos1(int lt, int e) {
+        return INVERSE ? inv_pos<R1>(lt * (EPT >> R1), e, 0) : fwd_pos<R1>(lt * (EPT >> R1), e, LOGN, 0);
+    }
+    __device__ static int pos2(int lt, int e) {
+        return INVERSE ? inv_pos<R2>(lt * (EPT >> R2), e, R1) : fwd_pos<R2>(lt * (EPT >> R2), e, LOGN, R1);
+    }
+};
+
+__device__ __forceinline__ void ld256(const uint64_t* p, uint64_t* v) {
+    asm volatile("ld.global.cs.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld256_nc(const uint64_t* p, uint64_t* v) {
+    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st256(uint64_t* p, const uint64_t* v) {
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
+                 : "memory");
+}
+
+// Phase A (columns): CTA = C columns x N1 rows, thread (cc = tid % C, lt = tid / C).
+// Forward: canonical words in, lazy [0, 4q) words / reduced doubles out (read by the
+// row pass); inverse: the row pass's words in, canonical words out (times N^-1).
+template <int LOG_N1, int C, bool INVERSE>
+__global__ void __launch_bounds__(NTT_THREADS) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm) {
     constexpr int N1 = 1 << LOG_N1;
-    constexpr int TPC = N1 / EPT;             // threads per column
-    constexpr int PN = N1 + (N1 >> 4) + 1;    // padded column length (odd in words)
-    __shared__ uint64_t sm[C * PN];            // column-major: column cc at sm + cc * PN
+    constexpr int PN = N1 + (N1 >> 4) + 1;  // padded column length (odd in words)
+    using PP = PassPlan<LOG_N1, INVERSE>;
+    __shared__ uint64_t sm[C * PN];
     const int row = blockIdx.y;
     const int u = row % rm.rows_per_poly;
-    const int B = c.N >> LOG_N1;
-    const int col0 = blockIdx.x * C;
-    uint64_t* a = data + (size_t)row * c.N;
     if (skip_row(rm, row, u)) return;
     const int p = row_prime(rm, u);
     const uint64_t q = c.primes[p].q;
-    // FP64 butterflies for q < 2^50. Forward: canonical words in, reduced doubles
-    // out (read by the row pass); inverse: doubles from the row pass in,
-    // canonical words out.
-    const bool fp = q < (1ULL << 50);
-    {
-        // coalesced load: consecutive threads take consecutive columns of a row;
-        // all EPT loads are issued before the shared-memory stores
-        uint64_t tmp[EPT];
+    const int B = c.N >> LOG_N1;
+    const int cc = threadIdx.x % C, lt = threadIdx.x / C;
+    uint64_t* a = data + (size_t)row * c.N + blockIdx.x * C + cc;
+    uint64_t* col = sm + cc * PN;
+    uint64_t w[EPT];
 #pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int i = threadIdx.x + e * NTT_THREADS;
-            tmp[e] = __ldcs(a + (size_t)(i / C) * B + col0 + i % C);
-        }
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int i = threadIdx.x + e * NTT_THREADS;
-            sm[(i % C) * PN + pad(i / C)] = (fp && !INVERSE) ? u2d_bits(tmp[e]) : tmp[e];
-        }
-    }
-    __syncthreads();
-    const int cc = threadIdx.x / TPC, lt = threadIdx.x % TPC;
-    if (fp) {
+    for (int e = 0; e < EPT; ++e) w[e] = __ldcs(a + (size_t)PP::pos1(lt, e) * B);
+    // FP64 butterflies for q < 2^50
+    if (q < (1ULL << 50)) {
         const ArD ad = make_ard(q);
-        if (!INVERSE) {
-            fwd_local_d<LOG_N1, 0, false>(sm + cc * PN, lt, 0, 0, c.twd + (size_t)p * c.N, ad);
+        const double2* tw = (INVERSE ? c.itwd : c.twd) + (size_t)p * c.N;
+        double v[EPT];
 #pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-                const int i = threadIdx.x + e * NTT_THREADS;
-                a[(size_t)(i / C) * B + col0 + i % C] = sm[(i % C) * PN + pad(i / C)];
-            }
+        for (int e = 0; e < EPT; ++e) v[e] = INVERSE ? asd(w[e]) : asd(u2d_bits(w[e]));
+        if (!INVERSE)
+            fwd_pass_d<PP::R1>(v, lt * (EPT >> PP::R1), LOG_N1, 0, 0, 0, tw, ad);
+        else
+            inv_pass_d<PP::R1>(v, lt * (EPT >> PP::R1), 0, LOG_N1, LOG_N1, 0, tw, ad);
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) col[pad(PP::pos1(lt, e))] = asu(v[e]);
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) v[e] = asd(col[pad(PP::pos2(lt, e))]);
+        if (!INVERSE) {
+            fwd_pass_d<PP::R2>(v, lt * (EPT >> PP::R2), LOG_N1, PP::R1, 0, 0, tw, ad);
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = asu(v[e]);
         } else {
-            inv_local_d<LOG_N1, 0, false>(sm + cc * PN, lt, LOG_N1, 0, c.itwd + (size_t)p * c.N, ad);
+            inv_pass_d<PP::R2>(v, lt * (EPT >> PP::R2), PP::R1, LOG_N1, LOG_N1, 0, tw, ad);
             const double2 ni = c.ninvd[p];
 #pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-                const int i = threadIdx.x + e * NTT_THREADS;
-                a[(size_t)(i / C) * B + col0 + i % C] =
-                    canon_d(mulmod_d(asd(sm[(i % C) * PN + pad(i / C)]), ni.x, ni.y, ad), ad);
-            }
+            for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = canon_d(mulmod_d(v[e], ni.x, ni.y, ad), ad);
         }
         return;
     }
+    const uint64_t* tw = (INVERSE ? c.itw : c.tw) + (size_t)p * c.N;
+    const uint64_t* tws = (INVERSE ? c.itw_sh : c.tw_sh) + (size_t)p * c.N;
+    if (!INVERSE)
+        fwd_pass<PP::R1>(w, lt * (EPT >> PP::R1), LOG_N1, 0, 0, 0, tw, tws, q);
+    else
+        inv_pass<PP::R1>(w, lt * (EPT >> PP::R1), 0, LOG_N1, LOG_N1, 0, tw, tws, q);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) col[pad(PP::pos1(lt, e))] = w[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) w[e] = col[pad(PP::pos2(lt, e))];
     if (!INVERSE) {
-        fwd_local<LOG_N1, 0, false>(sm + cc * PN, lt, 0, 0, c.tw + (size_t)p * c.N, c.tw_sh + (size_t)p * c.N, q);
+        fwd_pass<PP::R2>(w, lt * (EPT >> PP::R2), LOG_N1, PP::R1, 0, 0, tw, tws, q);
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = w[e];
     } else {
-        inv_local<LOG_N1, 0, false>(sm + cc * PN, lt, LOG_N1, 0, c.itw + (size_t)p * c.N,
-                                    c.itw_sh + (size_t)p * c.N, q);
-    }
-    if (INVERSE) {
+        inv_pass<PP::R2>(w, lt * (EPT >> PP::R2), PP::R1, LOG_N1, LOG_N1, 0, tw, tws, q);
         const uint64_t ni = c.ninv[p], nis = c.ninv_sh[p];
 #pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int i = threadIdx.x + e * NTT_THREADS;
-            a[(size_t)(i / C) * B + col0 + i % C] = mul_shoup(sm[(i % C) * PN + pad(i / C)], ni, nis, q);
-        }
-    } else {
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int i = threadIdx.x + e * NTT_THREADS;
-            a[(size_t)(i / C) * B + col0 + i % C] = sm[(i % C) * PN + pad(i / C)];
-        }
+        for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = mul_shoup(w[e], ni, nis, q);
     }
 }
 
@@ -421,114 +344,133 @@ __device__ __forceinline__ uint32_t perm_index_n(uint32_t k, uint32_t g, int log
     return __brev((e2 - 1) >> 1) >> (32 - logN);
 }
 
-// Phase B (contiguous blocks of B). CTA = BPC blocks; B/8 threads per block.
+// Phase B (contiguous blocks of B): CTA = BPC blocks, TPB = B / 16 threads per block
+// (one or a fraction of a warp: the exchange needs only __syncwarp). The forward
+// transform ends here (canonical words; FUSE_MODDOWN: the ModDown epilogue), the
+// inverse starts here (canonical words in, words for the column pass out).
 template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE>
 __global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
     constexpr int B = 1 << LOG_B;
     constexpr int TPB = B / EPT;
     constexpr int BPC = NTT_THREADS / TPB;
     constexpr int PB = B + (B >> 4);
+    static_assert(TPB <= 32, "a block is at most one warp");
+    using PP = PassPlan<LOG_B, INVERSE>;
     __shared__ uint64_t sm[BPC * PB];
     const int row = blockIdx.y;
     const int u = row % rm.rows_per_poly;
     if (skip_row(rm, row, u)) return;
     const int p = row_prime(rm, u);
     const uint64_t q = c.primes[p].q;
-    const int blk0 = blockIdx.x * BPC;
-    uint64_t* a = data + (size_t)row * c.N + (size_t)blk0 * B;
-    // FP64 butterflies for q < 2^50 (see k_ntt_cols): forward reads the column
-    // pass's doubles and normalises them here; inverse reads canonical words and
-    // leaves doubles for the column pass
+    const int bi = threadIdx.x / TPB, lt = threadIdx.x % TPB;
+    const int blk = blockIdx.x * BPC + bi;
+    const size_t base = (size_t)blk * B;  // block offset in the row
+    uint64_t* a = data + (size_t)row * c.N + base;
+    uint64_t* vec = sm + bi * PB;
     const bool fp = q < (1ULL << 50);
     const ArD ad = make_ard(q);
-    {
-        uint64_t tmp[EPT];
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) tmp[e] = __ldcs(a + threadIdx.x + e * NTT_THREADS);
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-            const int i = threadIdx.x + e * NTT_THREADS;
-            sm[(i / B) * PB + pad(i % B)] = (fp && INVERSE) ? u2d_bits(tmp[e]) : tmp[e];
-        }
-    }
-    __syncthreads();
-    const int bi = threadIdx.x / TPB, lt = threadIdx.x % TPB;
-    constexpr bool WS = TPB <= 32;
-    if (fp) {
-        if (!INVERSE)
-            fwd_local_d<LOG_B, 0, WS>(sm + bi * PB, lt, LOG_N1, blk0 + bi, c.twd + (size_t)p * c.N, ad);
-        else
-            inv_local_d<LOG_B, 0, WS>(sm + bi * PB, lt, LOG_N1 + LOG_B, blk0 + bi, c.itwd + (size_t)p * c.N, ad);
-    } else if (!INVERSE) {
-        fwd_local<LOG_B, 0, WS>(sm + bi * PB, lt, LOG_N1, blk0 + bi, c.tw + (size_t)p * c.N,
-                                c.tw_sh + (size_t)p * c.N, q);
-    } else {
-        inv_local<LOG_B, 0, WS>(sm + bi * PB, lt, LOG_N1 + LOG_B, blk0 + bi, c.itw + (size_t)p * c.N,
-                                c.itw_sh + (size_t)p * c.N, q);
-    }
-    __syncthreads();
-    // forward output word of smem slot i: [0, 4q) lazy integer or reduced double -> [0, q)
-    auto fwd_out = [&](int i) -> uint64_t {
-        const uint64_t w = sm[(i / B) * PB + pad(i % B)];
-        if (fp) return canon_d(asd(w), ad);
-        const uint64_t q2 = 2 * q;
-        const uint64_t x = w >= q2 ? w - q2 : w;
-        return x >= q ? x - q : x;
-    };
+    uint64_t w[EPT];
+    // input: forward stride-TPB residues (pass 1 positions lt + k TPB), inverse 16
+    // contiguous residues lt 16 + e
     if (!INVERSE) {
-        if (FUSE == FUSE_MODDOWN) {
-            const int pp = row / rm.rows_per_poly;
-            const int nr = rm.level + 1, ne = nr + c.K;
-            (void)ne;
-            const uint64_t* acc = fz.acc + (size_t)pp * fz.acc_stride + (size_t)u * c.N + (size_t)blk0 * B;
-            uint64_t* out = (fz.outp ? fz.outp[pp >> 1] + ((size_t)(pp & 1) * nr + u) * c.N
-                                     : fz.out + ((size_t)pp * nr + u) * c.N) +
-                            (size_t)blk0 * B;
-            const uint64_t pi = fz.outmul ? fz.outmul[u] : fz.md->pinvq[u];
-            const uint64_t pis = fz.outmul ? fz.outmul_sh[u] : fz.md->pinvq_sh[u];
-            const bool add = fz.add_src && (fz.add_mod > 0 ? (pp & 1) == 0 : pp == 0);
-            uint64_t av[EPT], sv[EPT];
-            if (fz.add_mod > 0) {  // conv bias of output pp / 2 (unpermuted rows)
-                const uint64_t* bsrc =
-                    fz.add_src + (size_t)((pp >> 1) % fz.add_mod) * fz.add_stride + (size_t)u * c.N + (size_t)blk0 * B;
 #pragma unroll
-                for (int e = 0; e < EPT; ++e) {
-                    const int i = threadIdx.x + e * NTT_THREADS;
-                    av[e] = __ldcs(acc + i);
-                    sv[e] = add ? __ldg(bsrc + i) : 0;
-                }
-            } else {
+        for (int e = 0; e < EPT; ++e) w[e] = __ldcs(a + PP::pos1(lt, e));
+    } else {
 #pragma unroll
-                for (int e = 0; e < EPT; ++e) {
-                    const int i = threadIdx.x + e * NTT_THREADS;
-                    av[e] = __ldcs(acc + i);
-                    sv[e] = add ? __ldg(fz.add_src + (size_t)u * c.N +
-                                        perm_index_n((uint32_t)(blk0 * B + i), fz.galois, c.logN))
-                                : 0;
-                }
-            }
+        for (int e = 0; e < EPT; e += 4) ld256(a + lt * EPT + e, w + e);
+    }
+    if (fp) {
+        const double2* tw = (INVERSE ? c.itwd : c.twd) + (size_t)p * c.N;
+        double v[EPT];
 #pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-                const int i = threadIdx.x + e * NTT_THREADS;
-                const uint64_t x = fwd_out(i);
-                uint64_t o = mul_shoup(sub_mod(av[e], x, q), pi, pis, q);
-                if (add) o = add_mod(o, sv[e], q);
-                out[i] = o;
+        for (int e = 0; e < EPT; ++e) v[e] = INVERSE ? asd(u2d_bits(w[e])) : asd(w[e]);
+        if (!INVERSE)
+            fwd_pass_d<PP::R1>(v, lt * (EPT >> PP::R1), LOG_B, 0, LOG_N1, blk, tw, ad);
+        else
+            inv_pass_d<PP::R1>(v, lt * (EPT >> PP::R1), 0, LOG_N1 + LOG_B, LOG_B, blk, tw, ad);
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) vec[pad(PP::pos1(lt, e))] = asu(v[e]);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) v[e] = asd(vec[pad(PP::pos2(lt, e))]);
+        if (!INVERSE) {
+            fwd_pass_d<PP::R2>(v, lt * (EPT >> PP::R2), LOG_B, PP::R1, LOG_N1, blk, tw, ad);
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) w[e] = canon_d(v[e], ad);
+        } else {
+            inv_pass_d<PP::R2>(v, lt * (EPT >> PP::R2), PP::R1, LOG_N1 + LOG_B, LOG_B, blk, tw, ad);
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) w[e] = asu(v[e]);
+        }
+    } else {
+        const uint64_t* tw = (INVERSE ? c.itw : c.tw) + (size_t)p * c.N;
+        const uint64_t* tws = (INVERSE ? c.itw_sh : c.tw_sh) + (size_t)p * c.N;
+        if (!INVERSE)
+            fwd_pass<PP::R1>(w, lt * (EPT >> PP::R1), LOG_B, 0, LOG_N1, blk, tw, tws, q);
+        else
+            inv_pass<PP::R1>(w, lt * (EPT >> PP::R1), 0, LOG_N1 + LOG_B, LOG_B, blk, tw, tws, q);
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) vec[pad(PP::pos1(lt, e))] = w[e];
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) w[e] = vec[pad(PP::pos2(lt, e))];
+        if (!INVERSE) {
+            fwd_pass<PP::R2>(w, lt * (EPT >> PP::R2), LOG_B, PP::R1, LOG_N1, blk, tw, tws, q);
+            const uint64_t q2 = 2 * q;
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) {  // [0, 4q) -> [0, q)
+                const uint64_t x = w[e] >= q2 ? w[e] - q2 : w[e];
+                w[e] = x >= q ? x - q : x;
             }
         } else {
-#pragma unroll
-            for (int e = 0; e < EPT; ++e) {
-                const int i = threadIdx.x + e * NTT_THREADS;
-                const uint64_t x = fwd_out(i);
-                a[i] = rm.limb ? to_opf(x, q) : x;
-            }
+            inv_pass<PP::R2>(w, lt * (EPT >> PP::R2), PP::R1, LOG_N1 + LOG_B, LOG_B, blk, tw, tws, q);
         }
-    } else {
+    }
+    if (INVERSE) {  // pass-2 positions lt + k TPB: coalesced
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) a[PP::pos2(lt, e)] = w[e];
+        return;
+    }
+    // forward output: residue e of this thread sits at block position lt 16 + e
+    if (FUSE == FUSE_MODDOWN) {
+        const int pp = row / rm.rows_per_poly;
+        const int nr = rm.level + 1;
+        const uint64_t* acc = fz.acc + (size_t)pp * fz.acc_stride + (size_t)u * c.N + base + lt * EPT;
+        uint64_t* out = (fz.outp ? fz.outp[pp >> 1] + ((size_t)(pp & 1) * nr + u) * c.N
+                                 : fz.out + ((size_t)pp * nr + u) * c.N) +
+                        base + lt * EPT;
+        const uint64_t pi = fz.outmul ? fz.outmul[u] : fz.md->pinvq[u];
+        const uint64_t pis = fz.outmul ? fz.outmul_sh[u] : fz.md->pinvq_sh[u];
+        const bool add = fz.add_src && (fz.add_mod > 0 ? (pp & 1) == 0 : pp == 0);
+        uint64_t av[EPT], sv[EPT];
+#pragma unroll
+        for (int e = 0; e < EPT; e += 4) ld256(acc + e, av + e);
+        if (add && fz.add_mod > 0) {  // conv bias of output pp / 2 (unpermuted rows)
+            const uint64_t* bsrc =
+                fz.add_src + (size_t)((pp >> 1) % fz.add_mod) * fz.add_stride + (size_t)u * c.N + base + lt * EPT;
+#pragma unroll
+            for (int e = 0; e < EPT; e += 4) ld256_nc(bsrc + e, sv + e);
+        } else if (add) {  // sigma_g(add_src)
+#pragma unroll
+            for (int e = 0; e < EPT; ++e)
+                sv[e] = __ldg(fz.add_src + (size_t)u * c.N +
+                              perm_index_n((uint32_t)(base + lt * EPT + e), fz.galois, c.logN));
+        }
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
-            const int i = threadIdx.x + e * NTT_THREADS;
-            a[i] = sm[(i / B) * PB + pad(i % B)];
+            uint64_t o = mul_shoup(sub_mod(av[e], w[e], q), pi, pis, q);
+            if (add) o = add_mod(o, sv[e], q);
+            w[e] = o;
         }
+#pragma unroll
+        for (int e = 0; e < EPT; e += 4) st256(out + e, w + e);
+    } else {
+        if (rm.limb) {
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) w[e] = to_opf(w[e], q);
+        }
+#pragma unroll
+        for (int e = 0; e < EPT; e += 4) st256(a + lt * EPT + e, w + e);
     }
 }
 
@@ -742,14 +684,14 @@ void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, 
     constexpr int BPC = NTT_THREADS / (B / EPT);
     const dim3 ga(B / C, nrows), gb((N1 + BPC - 1) / BPC, nrows);
     if (!inverse) {
-        k_ntt_cols<LOG_N1, C, false, FUSE_NONE><<<ga, NTT_THREADS, 0, st>>>(c, data, rm, fz);
+        k_ntt_cols<LOG_N1, C, false><<<ga, NTT_THREADS, 0, st>>>(c, data, rm);
         if (fuse == FUSE_MODDOWN)
             k_ntt_rows<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
         else
             k_ntt_rows<LOG_N1, LOG_B, false, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
     } else {
         k_ntt_rows<LOG_N1, LOG_B, true, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
-        k_ntt_cols<LOG_N1, C, true, FUSE_NONE><<<ga, NTT_THREADS, 0, st>>>(c, data, rm, fz);
+        k_ntt_cols<LOG_N1, C, true><<<ga, NTT_THREADS, 0, st>>>(c, data, rm);
     }
     note_launch(2);
 }
