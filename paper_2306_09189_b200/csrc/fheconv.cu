@@ -79,6 +79,7 @@ struct fhe_ctx {
     bool have_key = false;
     uint64_t key_seed = 0;
     std::map<uint32_t, uint64_t*> keys;
+    std::map<uint32_t, uint64_t*> keys_opf;  // operand-form copies (modarith.cuh to_opf) of the Galois keys
     uint64_t key_gen = 0;  // bumped by fhe_keygen: per-layer limb key copies are rebuilt
     fhe_ledger ledger{};
     uint64_t launch_base = 0;
@@ -201,6 +202,11 @@ struct fhe_ctx {
     const uint64_t* key_for(uint32_t g) const {
         auto it = keys.find(g);
         if (it == keys.end()) fail(FHE_E_NOKEY, "missing Galois key for rotation");
+        return it->second;
+    }
+    const uint64_t* key_opf_for(uint32_t g) const {
+        auto it = keys_opf.find(g);
+        if (it == keys_opf.end()) fail(FHE_E_NOKEY, "missing Galois key for rotation");
         return it->second;
     }
 };
@@ -436,6 +442,11 @@ void gen_key(fhe_ctx* c, uint32_t g) {
     c->release(e);
     c->release(erows);
     c->keys[g] = key;
+    if (g != 0) {  // operand-form copy for the FP64 / limb key-switch kernels (k_ks_hoist_opf)
+        uint64_t* ko = c->alloc((size_t)c->dnum * 2 * np * N);
+        rows_to_limb(c->dc, ko, key, (size_t)c->dnum * 2 * np, RowMap{np, -1, c->L, 0}, c->st);
+        c->keys_opf[g] = ko;
+    }
 }
 
 // destroy every captured conv graph (they embed key / plaintext device addresses)
@@ -2142,6 +2153,7 @@ void fhe_ctx_destroy(fhe_ctx* c) {
     if (!c) return;
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto& kv : c->keys) cudaFreeAsync(kv.second, c->st);
+    for (auto& kv : c->keys_opf) cudaFreeAsync(kv.second, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
     void* bufs[] = {c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv, c->d_ninv_sh,
                     c->d_twd,    c->d_itwd, c->d_ninvd,
@@ -2302,6 +2314,8 @@ int fhe_keygen(fhe_ctx* c, uint64_t seed) {
         c->key_gen++;  // layers rebuild their limb key copies on next use
         for (auto& kv : c->keys) c->release(kv.second);
         c->keys.clear();
+        for (auto& kv : c->keys_opf) c->release(kv.second);
+        c->keys_opf.clear();
         int64_t* s = (int64_t*)c->alloc(N);
         sample_ternary(c->dc, s, stream_key(seed, stream_id(DOM_SECRET, 0, 0)), c->st);
         const RowMap all{c->np, c->L - 1, c->L, 0};
@@ -2553,7 +2567,10 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
                 for (size_t s = 0; s < sn; ++s)
                     ck(cudaMemcpyAsync(buf + s * ctw, cts[s0 + s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st),
                        "memcpy");
-                modup_batch(c, buf + (size_t)nr * N, ctw, (int)sn, level, dig);
+                // operand-form digits and P-scaled ciphertexts (k_ks_hoist_opf: FP64 products on
+                // the rows q < 2^50); buf then holds [P c]_q in operand form
+                modup_batch(c, buf + (size_t)nr * N, ctw, (int)sn, level, dig, 1);
+                ct_prescale(c->dc, buf, buf, ctw, (int)sn, c->d_md, level, c->st);
                 for (size_t t0 = 0; t0 < KK; t0 += kMaxBaby) {
                     KsBatch kb{};
                     kb.nsrc = (int)sn;
@@ -2561,12 +2578,13 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
                     kb.digit_src_stride = dw;
                     kb.c0 = buf;
                     kb.c0_src_stride = ctw;
+                    kb.opf = 1;
                     kb.out = XT;
                     kb.out_src_stride = KK * 2 * extw;
                     for (size_t t = t0; t < KK && kb.n < kMaxBaby; ++t) {
                         const uint32_t g = c->galois_of(c->reduce_amount(ks[keyed[t]]));
                         kb.galois[kb.n] = g;
-                        kb.key[kb.n] = c->key_for(g);
+                        kb.key[kb.n] = c->key_opf_for(g);
                         kb.slot[kb.n] = (int)t;
                         kb.n++;
                     }

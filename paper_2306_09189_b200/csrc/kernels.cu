@@ -1465,6 +1465,147 @@ __global__ void __launch_bounds__(128, 3) k_ks_hoist(DevCtx c, KsBatch a, const 
     }
 }
 
+// k_ks_hoist on operand-form rows (KsBatch.opf): the same outputs, the products of
+// rows q < 2^50 on the FP64 pipe (fmac_d into exact double sums, one red_d), the
+// 60-bit rows on 30-bit limbs (four mad.wide.u32 per product, Montgomery by 2^90,
+// the factor restored per output). P sigma(c0) enters pre-scaled ([P c0]_q).
+template <int DN, int SG>
+__global__ void __launch_bounds__(128, 4) k_ks_hoist_opf(DevCtx c, KsBatch a, int level) {
+    constexpr int P = 128 / SG;
+    constexpr int KW = 2 * DN * P, DW = SG * DN * P, CW = SG * P, STAGE = KW + DW + CW;
+    extern __shared__ ulonglong2 sb[];  // [2][STAGE]
+    const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
+    const int tid = threadIdx.x, p = tid % P, sl = tid / P;
+    const size_t total = (size_t)ne * c.N;
+    const size_t chunks = total / 2 / P;
+    const int ngroups = (a.nsrc + SG - 1) / SG;
+    const size_t items = chunks * (size_t)ngroups;
+    const size_t keyrow = (size_t)np * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    ulonglong2* const s_key = sb + p;
+    ulonglong2* const s_dig = sb + KW + sl * DN * P + p;
+    ulonglong2* const s_c0 = sb + KW + DW + sl * P + p;
+    for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const size_t chunk = it / (size_t)ngroups;
+        const int s = (int)(it % (size_t)ngroups) * SG + sl;
+        const bool active = s < a.nsrc;
+        const size_t i = (chunk * P + p) * 2;
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
+        const int pi = row_prime(rm, u);
+        const bool qrow = u < nr;
+        const size_t kofs = (size_t)pi * c.N + k;
+        const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
+        auto pidx = [&](uint32_t g) { return brev_n((((e * g) & nmask) - 1) >> 1, c.logN); };
+        const uint64_t* Ds = a.digits + (size_t)(active ? s : 0) * a.digit_src_stride + (size_t)u * c.N;
+        const uint64_t* C0 = a.c0 + (size_t)(active ? s : 0) * a.c0_src_stride + (size_t)u * c.N;
+        auto issue = [&](int t) {
+            const size_t so = (size_t)(t & 1) * STAGE;
+            const uint64_t* kp = a.key[t] + kofs;
+#pragma unroll
+            for (int j = sl; j < 2 * DN; j += SG) cp_async16(s_key + so + j * P, kp + (size_t)j * keyrow);
+            if (active) {
+                const uint32_t pk = pidx(a.galois[t]) & ~1u;
+#pragma unroll
+                for (int j = 0; j < DN; ++j) cp_async16(s_dig + so + j * P, Ds + (size_t)j * total + pk);
+                if (qrow) cp_async16(s_c0 + so, C0 + pk);
+            }
+            cp_async_commit();
+        };
+        const Prime pr = c.primes[pi];
+        const bool fp = opf_fp(pr.q);
+        const ArD ad = make_ard(pr.q);
+        constexpr uint32_t MW = (1u << 30) - 1;
+        const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> 30), qinv = (uint32_t)pr.qinv & MW;
+        uint64_t r90 = 0;
+        if (!fp) {
+            r90 = reduce64(1ULL << 45, pr);
+            r90 = mul_mod(r90, r90, pr);
+        }
+        issue(0);
+        for (int t = 0; t < a.n; ++t) {
+            cp_async_wait<0>();
+            __syncthreads();
+            if (t + 1 < a.n) issue(t + 1);
+            const size_t so = (size_t)(t & 1) * STAGE;
+            const int swp = (int)(pidx(a.galois[t]) & 1u);
+            uint64_t o[2][2];
+            if (fp) {
+                double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                if (qrow) {
+                    const ulonglong2 cv = s_c0[so];
+                    z[0][0] = asd(swp ? cv.y : cv.x);
+                    z[0][1] = asd(swp ? cv.x : cv.y);
+                }
+#pragma unroll
+                for (int j = 0; j < DN; ++j) {
+                    const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
+                    const ulonglong2 dv = s_dig[so + j * P];
+                    const double da = asd(swp ? dv.y : dv.x), db = asd(swp ? dv.x : dv.y);
+                    fmac_d(z[0][0], da, asd(k0.x), ad);
+                    fmac_d(z[0][1], db, asd(k0.y), ad);
+                    fmac_d(z[1][0], da, asd(k1.x), ad);
+                    fmac_d(z[1][1], db, asd(k1.y), ad);
+                }
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) o[q2][e2] = canon_d(red_d(z[q2][e2], ad), ad);
+            } else {
+                uint64_t z0[2][2] = {{0, 0}, {0, 0}}, z1[2][2] = {{0, 0}, {0, 0}}, z2[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
+                for (int j = 0; j < DN; ++j) {
+                    const ulonglong2 kv0 = s_key[so + (2 * j) * P], kv1 = s_key[so + (2 * j + 1) * P];
+                    const ulonglong2 dv = s_dig[so + j * P];
+                    const uint64_t dw[2] = {swp ? dv.y : dv.x, swp ? dv.x : dv.y};
+                    const uint64_t kw[2][2] = {{kv0.x, kv0.y}, {kv1.x, kv1.y}};
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        const uint32_t d0 = lo32(dw[e2]), d1 = hi32(dw[e2]);
+#pragma unroll
+                        for (int q2 = 0; q2 < 2; ++q2) {
+                            const uint32_t kk0 = lo32(kw[q2][e2]), kk1 = hi32(kw[q2][e2]);
+                            madw(z0[q2][e2], d0, kk0);
+                            madw(z1[q2][e2], d0, kk1);
+                            madw(z1[q2][e2], d1, kk0);
+                            madw(z2[q2][e2], d1, kk1);
+                        }
+                    }
+                }
+                if constexpr (DN >= 8) {
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            z2[q2][e2] += z1[q2][e2] >> 30;
+                            z1[q2][e2] &= MW;
+                        }
+                }
+                if (qrow) {
+                    const ulonglong2 cv = s_c0[so];
+                    const uint64_t cw[2] = {swp ? cv.y : cv.x, swp ? cv.x : cv.y};
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        z0[0][e2] += lo32(cw[e2]);
+                        z1[0][e2] += hi32(cw[e2]);
+                    }
+                }
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2)
+                        o[q2][e2] = mul_mod(mont_l30(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv), r90, pr);
+            }
+            if (active) {
+                uint64_t* xt = a.out + (size_t)s * a.out_src_stride + (size_t)a.slot[t] * 2 * total;
+                st2(xt + i, o[0][0], o[0][1]);
+                st2(xt + total + i, o[1][0], o[1][1]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_qp_add(DevCtx c, uint64_t* acc, const uint64_t* y, int level) {
     const int ne = level + 1 + c.K;
     const size_t total = (size_t)2 * ne * c.N;
@@ -1551,6 +1692,18 @@ static void launch_giant(const DevCtx& c, const KsBatch& a, int level, cudaStrea
 }
 
 template <int DN, int SG>
+static void launch_hoist_opf(const DevCtx& c, const KsBatch& a, int level, cudaStream_t st) {
+    constexpr int P = 128 / SG;
+    const size_t smem = (size_t)2 * (2 * DN * P + SG * DN * P + SG * P) * sizeof(ulonglong2);
+    const size_t items = (size_t)(level + 1 + c.K) * c.N / 2 / P * (size_t)((a.nsrc + SG - 1) / SG);
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_ks_hoist_opf<DN, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ks_hoist_opf<DN, SG>, 128, smem);
+    const size_t cap = (size_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+    k_ks_hoist_opf<DN, SG><<<(int)(items < cap ? items : cap), 128, smem, st>>>(c, a, level);
+}
+
+template <int DN, int SG>
 static void launch_hoist(const DevCtx& c, const KsBatch& a, const ModDownTable* md, int level, cudaStream_t st) {
     constexpr int P = 128 / SG;
     const size_t smem = (size_t)2 * (2 * DN * P + SG * DN * P + SG * P) * sizeof(ulonglong2);
@@ -1568,11 +1721,17 @@ void ks_batch(const DevCtx& c, const KsBatch& a, int mode, const ModDownTable* m
     if (mode == 0 && !a.c0_qp) {  // hoisted rotations of a batch: one output per (source, term)
         ++g_launches;
         const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
-#define FHE_HOIST(D)                                                  \
-    do {                                                              \
-        if (sg == 4) launch_hoist<D, 4>(c, a, md, level, st);         \
-        else if (sg == 2) launch_hoist<D, 2>(c, a, md, level, st);    \
-        else launch_hoist<D, 1>(c, a, md, level, st);                 \
+#define FHE_HOIST(D)                                                      \
+    do {                                                                  \
+        if (a.opf) {                                                      \
+            if (sg == 4) launch_hoist_opf<D, 4>(c, a, level, st);         \
+            else if (sg == 2) launch_hoist_opf<D, 2>(c, a, level, st);    \
+            else launch_hoist_opf<D, 1>(c, a, level, st);                 \
+        } else {                                                          \
+            if (sg == 4) launch_hoist<D, 4>(c, a, md, level, st);         \
+            else if (sg == 2) launch_hoist<D, 2>(c, a, md, level, st);    \
+            else launch_hoist<D, 1>(c, a, md, level, st);                 \
+        }                                                                 \
     } while (0)
         FHE_DN_SWITCH(dn, FHE_HOIST)
 #undef FHE_HOIST

@@ -253,6 +253,9 @@ struct KsBatch {
     const uint64_t* c0;
     size_t c0_src_stride;
     int c0_qp;
+    // mode 0 only: digits, keys and c0 in operand form (modarith.cuh to_opf; c0 = the
+    // P-scaled [P c]_q of ct_prescale, same [2][level+1][N] layout): k_ks_hoist_opf
+    int opf;
     uint64_t* out;  // mode 0: XT of source s at out + s * out_src_stride; mode 1: acc of source s
     size_t out_src_stride;
 };

@@ -24,6 +24,53 @@ namespace {
 // padded shared-memory index (2-way bank conflicts at worst for 8-byte words)
 __device__ __forceinline__ int pad(int x) { return x + (x >> 4); }
 
+__device__ __forceinline__ void ld256(const uint64_t* p, uint64_t* v) {
+    asm volatile("ld.global.cs.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld256_nc(const uint64_t* p, uint64_t* v) {
+    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st256(uint64_t* p, const uint64_t* v) {
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
+                 : "memory");
+}
+
+
+// Twiddles of one sub-stage of a group are consecutive and aligned to their count
+// (a power of two): load them with 128-bit (integer: w, Shoup) or 256-bit (FP64:
+// (w_c, w_c / q) pairs) accesses, so a warp's requests use whole sectors.
+__device__ __forceinline__ void tw_ld(const uint64_t* p, uint64_t* o, int cnt) {
+    if (cnt == 1) {
+        o[0] = __ldg(p);
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2)
+        if (i < cnt) {
+            const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(p + i));
+            o[i] = t.x;
+            o[i + 1] = t.y;
+        }
+}
+__device__ __forceinline__ void tw_ld(const double2* p, double2* o, int cnt) {
+    if (cnt == 1) {
+        o[0] = __ldg(p);
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2)
+        if (i < cnt) {
+            uint64_t t[4];
+            ld256_nc(reinterpret_cast<const uint64_t*>(p + i), t);
+            o[i] = make_double2(asd(t[0]), asd(t[1]));
+            o[i + 1] = make_double2(asd(t[2]), asd(t[3]));
+        }
+}
+
 #ifndef FHE_NTT_EPT
 #define FHE_NTT_EPT 16
 #endif
@@ -55,13 +102,14 @@ __device__ __forceinline__ void fwd_pass(uint64_t (&v)[EPT], int G0, int logn, i
             const int half = 1 << (R - 1 - rho);
             const int sig = sigma0 + rho;
             const int base = (1 << (s0 + sig)) + (blk << sig) + (j0 >> (logt + 1 - rho));
-            const uint64_t* twb = tw + base;
-            const uint64_t* twsb = tws + base;
+            uint64_t wt[GS / 2], wst[GS / 2];
+            tw_ld(tw + base, wt, 1 << rho);
+            tw_ld(tws + base, wst, 1 << rho);
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
                 const int off = k >> (R - rho);
-                const uint64_t w = __ldg(twb + off), ws = __ldg(twsb + off);
+                const uint64_t w = wt[off], ws = wst[off];
                 // Harvey's lazy CT butterfly: values live in [0, 4q) between stages
                 uint64_t U = v[g * GS + k];
                 U = U >= q2 ? U - q2 : U;
@@ -101,13 +149,14 @@ __device__ __forceinline__ void inv_pass(uint64_t (&v)[EPT], int G0, int logt, i
             const int half = 1 << rho;
             const int lt = logt + rho;  // current distance 2^lt
             const int base = (1 << (log_ntot - lt - 1)) + (blk << (log_nloc - lt - 1)) + (j0 >> (lt + 1));
-            const uint64_t* twb = tw + base;
-            const uint64_t* twsb = tws + base;
+            uint64_t wt[GS / 2], wst[GS / 2];
+            tw_ld(tw + base, wt, GS >> (rho + 1));
+            tw_ld(tws + base, wst, GS >> (rho + 1));
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
                 const int off = k >> (rho + 1);
-                const uint64_t w = __ldg(twb + off), ws = __ldg(twsb + off);
+                const uint64_t w = wt[off], ws = wst[off];
                 // Harvey's lazy GS butterfly: values live in [0, 2q) between stages
                 const uint64_t U = v[g * GS + k], V = v[g * GS + k + half];
                 const uint64_t T = U + V;
@@ -158,11 +207,12 @@ __device__ __forceinline__ void fwd_pass_d(double (&v)[EPT], int G0, int logn, i
         for (int rho = 0; rho < R; ++rho) {
             const int half = 1 << (R - 1 - rho);
             const int sig = sigma0 + rho;
-            const double2* twb = tw + (1 << (s0 + sig)) + (blk << sig) + (j0 >> (logt + 1 - rho));
+            double2 wt[GS / 2];
+            tw_ld(tw + (1 << (s0 + sig)) + (blk << sig) + (j0 >> (logt + 1 - rho)), wt, 1 << rho);
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
-                const double2 w = __ldg(twb + (k >> (R - rho)));
+                const double2 w = wt[k >> (R - rho)];
                 const double r = mulmod_d(v[g * GS + k + half], w.x, w.y, a);
                 const double U = v[g * GS + k];
                 v[g * GS + k] = __dadd_rn(U, r);
@@ -191,11 +241,13 @@ __device__ __forceinline__ void inv_pass_d(double (&v)[EPT], int G0, int logt, i
         for (int rho = 0; rho < R; ++rho) {
             const int half = 1 << rho;
             const int lt = logt + rho;
-            const double2* twb = tw + (1 << (log_ntot - lt - 1)) + (blk << (log_nloc - lt - 1)) + (j0 >> (lt + 1));
+            double2 wt[GS / 2];
+            tw_ld(tw + (1 << (log_ntot - lt - 1)) + (blk << (log_nloc - lt - 1)) + (j0 >> (lt + 1)), wt,
+                  GS >> (rho + 1));
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
-                const double2 w = __ldg(twb + (k >> (rho + 1)));
+                const double2 w = wt[k >> (rho + 1)];
                 double U = v[g * GS + k], V = v[g * GS + k + half];
                 if (bd[k] + bd[k + half] > kUnitMax) {
                     U = red_d(U, a);
@@ -250,21 +302,6 @@ struct PassPlan {  // stages of the two passes of a phase of 2^LOGN elements
         return INVERSE ? inv_pos<R2>(lt * (EPT >> R2), e, R1) : fwd_pos<R2>(lt * (EPT >> R2), e, LOGN, R1);
     }
 };
-
-__device__ __forceinline__ void ld256(const uint64_t* p, uint64_t* v) {
-    asm volatile("ld.global.cs.v4.u64 {%0, %1, %2, %3}, [%4];"
-                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
-                 : "l"(p));
-}
-__device__ __forceinline__ void ld256_nc(const uint64_t* p, uint64_t* v) {
-    asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
-                 : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
-                 : "l"(p));
-}
-__device__ __forceinline__ void st256(uint64_t* p, const uint64_t* v) {
-    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
-                 : "memory");
-}
 
 // Phase A (columns): CTA = C columns x N1 rows, thread (cc = tid % C, lt = tid / C).
 // Forward: canonical words in, lazy [0, 4q) words / reduced doubles out (read by the
@@ -572,35 +609,51 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
     }
 }
 
-// FastBConv of ModDown: conv[pp][t] = conv_P->q_t(pc[pp]) (coefficient domain)
+// FastBConv of ModDown: conv[pp][t] = conv_P->q_t(pc[pp]) (coefficient domain).
+// One thread per (poly, coefficient pair): the centred v_a = [x_a (P/p_a)^-1]_{p_a}
+// are computed once and extended to every target row t.
 template <int KA>
 __global__ void __launch_bounds__(256) k_bconv_moddown(DevCtx c, uint64_t* conv, NttFuse fz, int level, int npoly) {
     const int nr = level + 1;
     const size_t halfN = c.N / 2;
-    const size_t total = (size_t)npoly * nr * halfN;
+    const size_t total = (size_t)npoly * halfN;
     const ModDownTable* md = fz.md;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-        const int row = (int)(idx >> (c.logN - 1));
+        const int pp = (int)(idx >> (c.logN - 1));
         const size_t k = (idx & (halfN - 1)) * 2;
-        const int t = (int)(row % nr), pp = (int)(row / nr);
-        const uint64_t qt = c.primes[t].q;
         const uint64_t* pc = fz.pc + (size_t)pp * c.K * c.N;
-        uint64_t y0 = 0, y1 = 0;
+        uint64_t v0[KA], v1[KA];
         int n0 = 0, n1 = 0;
 #pragma unroll
         for (int a = 0; a < KA; ++a) {
             const uint64_t q = c.primes[c.L + a].q;
-            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(pc + (size_t)a * c.N + k);
-            const uint64_t v0 = mul_shoup(x.x, md->pinv[a], md->pinv_sh[a], q);
-            const uint64_t v1 = mul_shoup(x.y, md->pinv[a], md->pinv_sh[a], q);
-            n0 += v0 > (q >> 1);
-            n1 += v1 > (q >> 1);
-            y0 = add_mod(y0, mul_shoup(v0, md->hat[t][a], md->hat_sh[t][a], qt), qt);
-            y1 = add_mod(y1, mul_shoup(v1, md->hat[t][a], md->hat_sh[t][a], qt), qt);
+            const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(pc + (size_t)a * c.N + k));
+            v0[a] = mul_shoup(x.x, md->pinv[a], md->pinv_sh[a], q);
+            v1[a] = mul_shoup(x.y, md->pinv[a], md->pinv_sh[a], q);
+            n0 += v0[a] > (q >> 1);
+            n1 += v1[a] > (q >> 1);
         }
-        for (int n = 0; n < n0; ++n) y0 = sub_mod(y0, md->pmod[t], qt);
-        for (int n = 0; n < n1; ++n) y1 = sub_mod(y1, md->pmod[t], qt);
-        *reinterpret_cast<ulonglong2*>(conv + (size_t)row * c.N + k) = make_ulonglong2(y0, y1);
+        uint64_t* out = conv + (size_t)pp * nr * c.N + k;
+#pragma unroll 4
+        for (int t = 0; t < nr; ++t) {
+            const uint64_t qt = c.primes[t].q;
+            // lazy sum of KA products in [0, 2 qt), then the centred correction
+            uint64_t y0 = 0, y1 = 0;
+#pragma unroll
+            for (int a = 0; a < KA; ++a) {
+                y0 += mul_shoup_lazy(v0[a], md->hat[t][a], md->hat_sh[t][a], qt);
+                y1 += mul_shoup_lazy(v1[a], md->hat[t][a], md->hat_sh[t][a], qt);
+            }
+#pragma unroll
+            for (int r = (KA >= 3 ? 4 : (KA >= 2 ? 2 : 1)); r >= 1; r >>= 1) {
+                y0 = y0 >= r * qt ? y0 - r * qt : y0;
+                y1 = y1 >= r * qt ? y1 - r * qt : y1;
+            }
+            const uint64_t pm = md->pmod[t];
+            const uint64_t c0 = n0 ? mul_shoup((uint64_t)n0, pm, md->pmod_sh[t], qt) : 0;
+            const uint64_t c1 = n1 ? mul_shoup((uint64_t)n1, pm, md->pmod_sh[t], qt) : 0;
+            *reinterpret_cast<ulonglong2*>(out + (size_t)t * c.N) = make_ulonglong2(sub_mod(y0, c0, qt), sub_mod(y1, c1, qt));
+        }
     }
 }
 
@@ -825,7 +878,7 @@ void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const u
     fz.add_src = add_src;
     fz.galois = galois;
     {
-        const size_t total = (size_t)npoly * nr * (c.N / 2);
+        const size_t total = (size_t)npoly * (c.N / 2);
         const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
         switch (c.K) {
             case 1: k_bconv_moddown<1><<<blocks, 256, 0, st>>>(c, conv, fz, level, npoly); break;
