@@ -257,6 +257,15 @@ struct fhe_conv_layer {
         std::vector<int> kidx;            // baby b -> its key in d_keys_limb (-1: identity)
         uint64_t limb_gen = 0;            // key generation d_keys_limb was built from
     } bs[3];
+    // operand-form copies for the paper schedules on the TMA baby-step kernel
+    // (conv_paper_batch): the fused plaintexts [c_in][nk][ne][N], and per approach
+    // (1, 2) the keys of the second-level rotations [nkeys][2 dnum][L+K][N]
+    uint64_t* d_pts_opf = nullptr;
+    struct PaperKeys {
+        uint64_t* d_keys = nullptr;
+        std::vector<int> kidx;  // second-level member x -> its key (-1: identity)
+        uint64_t gen = 0;
+    } pk[2];
     // multi-shard image mode (fhe_conv_layer_create_shards): t input shards of z
     // channels, n_out output shards; fused-BSGS plaintexts
     // pt'[v][kk][b = (u, r, ll)] = rot_{-kk m}(fused_plain_ms(v, u, r, kk, ll))
@@ -893,6 +902,57 @@ void prepare_limb(fhe_ctx* c, const fhe_conv_layer* ly, int orient) {
     if (dirty) ck(cudaStreamSynchronize(c->st), "limb operands");
 }
 
+// Operand-form plaintexts and second-level keys of the paper schedules (approach 1:
+// channel rotations r m^2, approach 2: shifts) for conv_paper_batch on k_bsgs_tma.
+// Built once per layer (keys again after a keygen), host-synchronising: batch_impl
+// calls it before a graph capture.
+bool paper_opf_ok(const fhe_ctx* c, const fhe_conv_layer* ly) { return c->limb && !ly->ms && !ly->cs; }
+void prepare_paper(fhe_ctx* c, const fhe_conv_layer* ly, int approach) {
+    if ((approach != 1 && approach != 2) || !paper_opf_ok(c, ly)) return;
+    fhe_conv_layer* L = const_cast<fhe_conv_layer*>(ly);
+    const int ne = c->ne_at(ly->level);
+    bool dirty = false;
+    if (!L->d_pts_opf) {
+        const size_t rows = (size_t)ly->c_in * ly->nk * ne;
+        ck(cudaMalloc(&L->d_pts_opf, rows * c->N * 8), "cudaMalloc");
+        rows_to_limb(c->dc, L->d_pts_opf, ly->d_pts, rows, RowMap{ne, ly->level, c->L, 0}, c->st);
+        dirty = true;
+    }
+    fhe_conv_layer::PaperKeys& P = L->pk[approach - 1];
+    const long m = ly->m, h = ly->kappa / 2;
+    const int nsecond = approach == 2 ? ly->nk : ly->c_in;
+    auto amt_of = [&](int x) {
+        return approach == 2 ? (int64_t)(x / (2 * h + 1) - h) * m + (x % (2 * h + 1) - h) : (int64_t)x * m * m;
+    };
+    bool stale = !P.d_keys || P.gen != c->key_gen || (int)P.kidx.size() != nsecond;
+    for (int x = 0; !stale && x < nsecond; ++x) {  // a key generated since the copies were built
+        const uint32_t g = c->galois_of(c->reduce_amount(amt_of(x)));
+        stale = g != 1 && P.kidx[x] < 0 && c->keys.count(g);
+    }
+    if (stale) {
+        std::vector<const uint64_t*> src;
+        P.kidx.assign(nsecond, -1);
+        for (int x = 0; x < nsecond; ++x) {
+            const uint32_t g = c->galois_of(c->reduce_amount(amt_of(x)));
+            if (g == 1 || !c->keys.count(g)) continue;  // a missing key fails later, in key_for
+            P.kidx[x] = (int)src.size();
+            src.push_back(c->key_for(g));
+        }
+        const size_t rows = (size_t)c->dnum * 2 * c->np;
+        if (P.d_keys) {
+            ck(cudaStreamSynchronize(c->main_st), "sync");
+            cudaFree(P.d_keys);
+            P.d_keys = nullptr;
+        }
+        ck(cudaMalloc(&P.d_keys, std::max<size_t>(1, src.size()) * rows * c->N * 8), "cudaMalloc");
+        for (size_t t = 0; t < src.size(); ++t)
+            rows_to_limb(c->dc, P.d_keys + t * rows * c->N, src[t], rows, RowMap{c->np, -1, c->L, 0}, c->st);
+        P.gen = c->key_gen;
+        dirty = true;
+    }
+    if (dirty) ck(cudaStreamSynchronize(c->st), "paper operands");
+}
+
 // Baby steps of the fused BSGS schedule for nsrc sources: Y_g(s) for every
 // giant g (chunks of kFusedMaxG giants per launch), X~_b never materialised.
 // limb: digits are limb-form ModUp digits and cts the limb-form P-scaled
@@ -916,12 +976,12 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
         const uint64_t dk[4] = {N, (uint64_t)c->np, 2ull * c->dnum, std::max<uint64_t>(1, nkeys)};
         const uint32_t bk[4] = {P2, 1, 2u * dn, 1};
         tma_map4(&tm.key, B.d_keys_limb, dk, bk);
-        const uint64_t dd[4] = {N, (uint64_t)ne, (uint64_t)dn, (uint64_t)nsrc};
-        const uint32_t bd[4] = {P2, 1, (uint32_t)dn, sg};
-        tma_map4(&tm.dig, digits, dd, bd);
-        const uint64_t dc4[4] = {N, (uint64_t)nr, 2, (uint64_t)nsrc};
-        const uint32_t bc[4] = {P2, 1, 2, sg};
-        tma_map4(&tm.ct, cts, dc4, bc);
+        const uint64_t dd[5] = {N, (uint64_t)ne, (uint64_t)dn, 1, (uint64_t)nsrc};
+        const uint32_t bd[5] = {P2, 1, (uint32_t)dn, 1, sg};
+        tma_map5(&tm.dig, digits, dd, bd);
+        const uint64_t dc5[5] = {N, (uint64_t)nr, 2, 1, (uint64_t)nsrc};
+        const uint32_t bc[5] = {P2, 1, 2, 1, sg};
+        tma_map5(&tm.ct, cts, dc5, bc);
     }
     FusedBsgs f{};
     f.nsrc = nsrc;
@@ -1388,6 +1448,9 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
         else fl.push_back(f);
     }
     const int NF = (int)fl.size() + 1;  // slot 0: the input itself
+    // operand-form rows + TMA baby steps (k_bsgs_tma with source slots), when prepared
+    const fhe_conv_layer::PaperKeys& PK = ly->pk[approach - 1];
+    const bool opf = paper_opf_ok(c, ly) && c->tma && ly->d_pts_opf && PK.d_keys && PK.gen == c->key_gen;
     uint64_t* X = c->alloc((size_t)S * NF * ctw);
     for (int s = 0; s < S; ++s)
         ck(cudaMemcpyAsync(X + (size_t)s * NF * ctw, cts[s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
@@ -1395,7 +1458,12 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
     ck(cudaMemsetAsync(acc, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
     if (!fl.empty()) {  // first-level rotations of every input, hoisted, keys shared by the batch
         uint64_t* dig0 = c->alloc((size_t)S * dw);
-        modup_batch(c, X + (size_t)nr * N, (size_t)NF * ctw, S, level, dig0);
+        modup_batch(c, X + (size_t)nr * N, (size_t)NF * ctw, S, level, dig0, opf ? 1 : 0);
+        uint64_t* xp = nullptr;  // opf: the P-scaled inputs in operand form
+        if (opf) {
+            xp = c->alloc((size_t)S * ctw);
+            ct_prescale(c->dc, xp, X, (size_t)NF * ctw, S, c->d_md, level, c->st);
+        }
         const size_t F = fl.size();
         uint64_t* XT = c->alloc((size_t)S * F * 2 * extw);
         for (size_t t0 = 0; t0 < F; t0 += kMaxBaby) {
@@ -1403,14 +1471,15 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
             kb.nsrc = S;
             kb.digits = dig0;
             kb.digit_src_stride = dw;
-            kb.c0 = X;
-            kb.c0_src_stride = (size_t)NF * ctw;
+            kb.c0 = opf ? xp : X;
+            kb.c0_src_stride = opf ? ctw : (size_t)NF * ctw;
+            kb.opf = opf ? 1 : 0;
             kb.out = XT;
             kb.out_src_stride = F * 2 * extw;
             for (size_t t = t0; t < F && kb.n < kMaxBaby; ++t) {
                 const uint32_t g = c->galois_of(c->reduce_amount(first_amt(fl[t])));
                 kb.galois[kb.n] = g;
-                kb.key[kb.n] = c->key_for(g);
+                kb.key[kb.n] = opf ? c->key_opf_for(g) : c->key_for(g);
                 kb.slot[kb.n] = (int)t;
                 kb.n++;
             }
@@ -1421,11 +1490,81 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
         for (int s = 0; s < S; ++s)
             moddown(c, XT + (size_t)s * F * 2 * extw, level, (int)(2 * F), X + ((size_t)s * NF + 1) * ctw, nullptr, 1);
         c->release(XT);
+        c->release(xp);
         c->release(dig0);
     }
     // every copy's ModUp, then the fused second-level key switches + MAC
     uint64_t* dig = c->alloc((size_t)S * NF * dw);
-    modup_batch(c, X + (size_t)nr * N, ctw, S * NF, level, dig);
+    modup_batch(c, X + (size_t)nr * N, ctw, S * NF, level, dig, opf ? 1 : 0);
+    if (opf) {
+        // every copy P-scaled in operand form (in place: X is not read again), then the
+        // second-level key switches + MAC on k_bsgs_tma: babies (slot, x) read their
+        // copy's digits / c0 through the 5-D maps' slot coordinate, one giant
+        ct_prescale(c->dc, X, X, ctw, S * NF, c->d_md, level, c->st);
+        TmaMaps tm{};
+        const uint32_t sg = (uint32_t)tma_sources(S), P2 = 256u / sg;
+        const size_t keyw = (size_t)c->dnum * 2 * c->np * N;
+        uint64_t nkeys = 0;
+        for (int v : PK.kidx) nkeys += v >= 0;
+        const uint64_t dk[4] = {N, (uint64_t)c->np, 2ull * c->dnum, std::max<uint64_t>(1, nkeys)};
+        const uint32_t bk[4] = {P2, 1, 2u * dn, 1};
+        tma_map4(&tm.key, PK.d_keys, dk, bk);
+        const uint64_t dp[4] = {N, (uint64_t)ne, (uint64_t)cin * nk, 1};
+        const uint32_t bp[4] = {P2, 1, 1, 1};
+        tma_map4(&tm.pt, ly->d_pts_opf, dp, bp);
+        const uint64_t dd[5] = {N, (uint64_t)ne, (uint64_t)dn, (uint64_t)NF, (uint64_t)S};
+        const uint32_t bd[5] = {P2, 1, (uint32_t)dn, 1, sg};
+        tma_map5(&tm.dig, dig, dd, bd);
+        const uint64_t dc5[5] = {N, (uint64_t)nr, 2, (uint64_t)NF, (uint64_t)S};
+        const uint32_t bc[5] = {P2, 1, 2, 1, sg};
+        tma_map5(&tm.ct, X, dc5, bc);
+        tm.g0 = 0;
+        tm.ng1 = 1;
+        FusedBsgs f{};
+        f.nsrc = S;
+        f.ng = 1;
+        f.digits = dig;
+        f.ct = X;
+        f.Y = acc;
+        f.y_src_stride = 2 * extw;
+        f.y_g_stride = 2 * extw;
+        int launches = 0;
+        double keyed = 0;
+        auto flush_t = [&] {
+            if (!f.nb) return;
+            f.accumulate = launches > 0;
+            c->timed("bsgs_fused", c->rows(keyed * 2.0 * dn * ne + f.nb * (double)ne +
+                                            S * ((double)f.nb * (dn * ne + 2.0 * nr) / NF + 4.0 * ne)),
+                     [&] { bsgs_tma(c->dc, f, tm, level, dn, c->st); });
+            launches++;
+            f.nb = 0;
+            keyed = 0;
+        };
+        for (int slot = 0; slot < NF; ++slot) {
+            const int fi = slot == 0 ? fid : fl[slot - 1];
+            if (fi < 0) continue;
+            for (int x = 0; x < nsecond; ++x) {
+                const auto rp = rpos(fi, x);
+                if (!nonempty(rp.first, rp.second)) continue;
+                if (f.nb == kMaxFused) flush_t();
+                const uint32_t g = c->galois_of(c->reduce_amount(second_amt(x)));
+                if (g != 1) c->key_for(g);  // a missing key fails here
+                f.galois[f.nb] = g;
+                f.key[f.nb] = nullptr;
+                tm.kidx[f.nb] = (int16_t)(g == 1 ? -1 : PK.kidx[x]);
+                tm.bidx[f.nb] = (int16_t)(rp.first * nk + rp.second);
+                f.gmask[f.nb] = 1;
+                f.srcslot[f.nb] = (uint16_t)slot;
+                f.nb++;
+                if (g != 1) {
+                    keyed += 1;
+                    c->ledger.key_switches += S;
+                }
+            }
+        }
+        flush_t();
+        if (!launches) ck(cudaMemsetAsync(acc, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
+    }
     FusedBsgs fb{};
     fb.nsrc = S;
     fb.ng = 1;
@@ -1448,7 +1587,7 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
         fb.nb = 0;
         keyed = pts = 0;
     };
-    for (int slot = 0; slot < NF; ++slot) {
+    for (int slot = 0; slot < NF && !opf; ++slot) {
         const int f = slot == 0 ? fid : fl[slot - 1];
         if (f < 0) continue;
         for (int x = 0; x < nsecond; ++x) {
@@ -1943,7 +2082,9 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
     if (ly->ms) fail(FHE_E_INVALID, "multi-shard layer: use fhe_conv2d_shards_into");
     if (approach < 0 || approach > 5) fail(FHE_E_INVALID, "approach must be 0 (auto), 1, 2, 3, 4 or 5");
     if (approach == 0) approach = auto_orient(ly);
-    const bool paper_batch = (approach == 1 || approach == 2) && n > 1 && c->batch5;
+    // approaches 1 / 2 (also one ciphertext) through the batched paper schedule: the
+    // same residues as conv_impl, first-level rotations hoisted, second level fused
+    const bool paper_batch = (approach == 1 || approach == 2) && c->batch5 && !ly->ms && !ly->cs;
     const bool bsgs_batch = approach >= 3 && n > 1 && (c->fused_batch || (approach == 5 && c->batch5));
     if (paper_batch || bsgs_batch || n == 1) {
         for (size_t s = 0; s < n; ++s) {
@@ -1952,11 +2093,11 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
         }
         prepare_bias(c, ly, cts, n);
         auto body = [&] {
-            if (n == 1) {
-                conv_impl(c, cts[0], ly, approach, outs[0]);
-            } else if (paper_batch) {
+            if (paper_batch) {
                 for (size_t s0 = 0; s0 < n; s0 += 8)
                     conv_paper_batch(c, cts + s0, (int)std::min<size_t>(8, n - s0), ly, approach, outs + s0);
+            } else if (n == 1) {
+                conv_impl(c, cts[0], ly, approach, outs[0]);
             } else {
                 for (size_t s0 = 0; s0 < n; s0 += 32)
                     conv_bsgs_batch(c, cts + s0, (int)std::min<size_t>(32, n - s0), ly, approach, outs + s0);
@@ -1968,6 +2109,7 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
         }
         if (approach >= 3) ensure_bsgs(c, ly, approach);  // host encoding + sync: never inside a capture
         prepare_limb(c, ly, approach);
+        if (paper_batch) prepare_paper(c, ly, approach);
         std::vector<const void*> key{(const void*)(uintptr_t)ly->uid, (const void*)(uintptr_t)approach,
                                      (const void*)(uintptr_t)n};
         for (size_t s = 0; s < n; ++s) {
@@ -2041,6 +2183,7 @@ void batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size_t n, const fhe_conv_l
     }
     if (approach >= 3) ensure_bsgs(c, ly, approach);  // layer constants are built on the main stream
     prepare_limb(c, ly, approach);
+    if (paper_batch) prepare_paper(c, ly, approach);
     prepare_bias(c, ly, cts, n);
     if (n == 1 || c->lanes.size() <= 1) {
         for (size_t i = 0; i < n; ++i) conv_impl(c, cts[i], ly, approach, outs[i]);
@@ -2931,6 +3074,9 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
         if (b.d_pts_limb) cudaFree(b.d_pts_limb);
         if (b.d_keys_limb) cudaFree(b.d_keys_limb);
     }
+    if (ly->d_pts_opf) cudaFree(ly->d_pts_opf);
+    for (auto& k : ly->pk)
+        if (k.d_keys) cudaFree(k.d_keys);
     delete ly;
 }
 
@@ -3161,7 +3307,7 @@ int fhe_conv2d(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int appro
         prepare_bias(c, ly, &ct, 1);
         fhe_ct* o = new_ct(c, ct->level - 1, ct->scale, ct->depth + 1);
         try {
-            conv_impl(c, ct, ly, approach, o);
+            batch_impl(c, &ct, 1, ly, approach, &o);
         } catch (...) {
             fhe_ct_free(o);
             throw;

@@ -981,6 +981,15 @@ __device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, int
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int DN, int NG, int SG>
 struct TmaLayout {  // one stage, in 16-byte pair slots
     static constexpr int P = 128 / SG;
@@ -1036,11 +1045,12 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
             const bool keyed = m.kidx[b] >= 0;
             const int blk = (int)(pidx(e0, a.galois[b]) & ~(uint32_t)(BW - 1));
             mbar_expect_tx(bar, (uint32_t)(LY::PW + LY::CW + (keyed ? LY::KW + LY::DW : 0)) * 16u);
+            const int sl5 = a.srcslot[b];  // source slot (paper schedules: the rotated copy)
             tma_load4(sb + LY::KW, &m.pt, (int)k0, u, m.bidx[b], m.g0, bar);
-            tma_load4(sb + LY::KW + LY::PW + LY::DW, &m.ct, blk, qrow ? u : 0, 0, s0c, bar);
+            tma_load5(sb + LY::KW + LY::PW + LY::DW, &m.ct, blk, qrow ? u : 0, 0, sl5, s0c, bar);
             if (keyed) {
                 tma_load4(sb, &m.key, (int)k0, pi, 0, m.kidx[b], bar);
-                tma_load4(sb + LY::KW + LY::PW, &m.dig, blk, u, 0, s0c, bar);
+                tma_load5(sb + LY::KW + LY::PW, &m.dig, blk, u, 0, sl5, s0c, bar);
             }
         };
         // q < 2^50: FP64 operand form (modarith.cuh): every product is one fmac_d on the
@@ -1126,8 +1136,20 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                 for (int g = 0; g < NG; ++g) {
                     if (g >= a.ng) break;
                     uint64_t* yg = Ys + (size_t)g * a.y_g_stride;
-                    st2(yg + i, canon_d(red_d(y[g][0][0], ad), ad), canon_d(red_d(y[g][0][1], ad), ad));
-                    st2(yg + total + i, canon_d(red_d(y[g][1][0], ad), ad), canon_d(red_d(y[g][1][1], ad), ad));
+                    uint64_t o[2][2];
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) o[q2][e2] = canon_d(red_d(y[g][q2][e2], ad), ad);
+                    if (a.accumulate) {  // Y_g += (later launches of a long baby list)
+                        const ulonglong2 y0 = ld2(yg + i), y1 = ld2(yg + total + i);
+                        o[0][0] = add_mod(o[0][0], y0.x, pr.q);
+                        o[0][1] = add_mod(o[0][1], y0.y, pr.q);
+                        o[1][0] = add_mod(o[1][0], y1.x, pr.q);
+                        o[1][1] = add_mod(o[1][1], y1.y, pr.q);
+                    }
+                    st2(yg + i, o[0][0], o[0][1]);
+                    st2(yg + total + i, o[1][0], o[1][1]);
                 }
             }
         };
@@ -1249,6 +1271,13 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                         for (int e2 = 0; e2 < 2; ++e2)
                             o[q2][e2] = mul_mod(reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), r, pr);
                     uint64_t* yg = Ys + (size_t)g * a.y_g_stride;
+                    if (a.accumulate) {
+                        const ulonglong2 y0 = ld2(yg + i), y1 = ld2(yg + total + i);
+                        o[0][0] = add_mod(o[0][0], y0.x, pr.q);
+                        o[0][1] = add_mod(o[0][1], y0.y, pr.q);
+                        o[1][0] = add_mod(o[1][0], y1.x, pr.q);
+                        o[1][1] = add_mod(o[1][1], y1.y, pr.q);
+                    }
                     st2(yg + i, o[0][0], o[0][1]);
                     st2(yg + total + i, o[1][0], o[1][1]);
                 }
@@ -1855,13 +1884,16 @@ static void launch_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, in
 
 void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st) {
     if (a.nb <= 0 || a.nsrc <= 0 || a.ng <= 0) return;
-    if (a.accumulate || a.digit_slot_stride || a.ct_slot_stride || a.ng > kFusedMaxG)
-        throw std::invalid_argument("bsgs_tma: source slots / accumulation are not supported");
+    if (a.ng > kFusedMaxG) throw std::invalid_argument("bsgs_tma: too many giants per launch");
     ++g_launches;
     const int sg = tma_sources(a.nsrc);
 #define FHE_TMA(D)                                                               \
     do {                                                                         \
-        if (a.ng <= 3) {                                                         \
+        if (a.ng == 1 && m.ng1) {                                                \
+            if (sg == 4) launch_tma<D, 1, 4, FHE_TMA_MINB>(c, a, m, level, st);  \
+            else if (sg == 2) launch_tma<D, 1, 2, 3>(c, a, m, level, st);        \
+            else launch_tma<D, 1, 1, 2>(c, a, m, level, st);                     \
+        } else if (a.ng <= 3) {                                                  \
             if (sg == 4) launch_tma<D, 3, 4, FHE_TMA_MINB>(c, a, m, level, st);  \
             else if (sg == 2) launch_tma<D, 3, 2, 3>(c, a, m, level, st);        \
             else launch_tma<D, 3, 1, 2>(c, a, m, level, st);                     \
@@ -1888,20 +1920,28 @@ static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
     return fn;
 }
 
-void tma_map4(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint32_t box[4]) {
-    cuuint64_t gd[4], gs[3];
-    cuuint32_t bx[4], es[4] = {1, 1, 1, 1};
+template <int R>
+static void tma_map_r(CUtensorMap* map, const void* base, const uint64_t* dims, const uint32_t* box) {
+    cuuint64_t gd[R], gs[R - 1];
+    cuuint32_t bx[R], es[R];
     uint64_t stride = 8;
-    for (int d = 0; d < 4; ++d) {
+    for (int d = 0; d < R; ++d) {
+        es[d] = 1;
         gd[d] = dims[d];
         bx[d] = box[d];
         if (d > 0) gs[d - 1] = stride;
         stride *= dims[d];
     }
-    const CUresult r = tma_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(base), gd, gs, bx, es,
+    const CUresult r = tma_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, R, const_cast<void*>(base), gd, gs, bx, es,
                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
+}
+void tma_map4(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint32_t box[4]) {
+    tma_map_r<4>(map, base, dims, box);
+}
+void tma_map5(CUtensorMap* map, const void* base, const uint64_t dims[5], const uint32_t box[5]) {
+    tma_map_r<5>(map, base, dims, box);
 }
 
 void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,

@@ -308,11 +308,14 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
 // mbarrier -- and the plaintext set is padded to the giants the boxes span, limb_giants)
 // with NG = 3 when ng <= 3, else kFusedMaxG.
 struct TmaMaps {
-    CUtensorMap key, pt, dig, ct;
+    CUtensorMap key, pt, dig, ct;  // dig / ct: 5-D, dimension 3 = source slot (FusedBsgs.srcslot)
     int16_t kidx[kMaxFused];  // baby b's key in the key map, -1: identity
     int16_t bidx[kMaxFused];  // baby b's index in the plaintext map
     int g0;                   // first giant of the launch
+    int ng1;                  // the plaintext box spans one giant (paper schedules: ng == 1)
 };
+// encode a 5-D uint64 tensor map (dims innermost first, dense)
+void tma_map5(CUtensorMap* map, const void* base, const uint64_t dims[5], const uint32_t box[5]);
 inline int tma_sources(int nsrc) { return nsrc >= 4 ? 4 : nsrc >= 2 ? 2 : 1; }
 void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st);
 // encode a 4-D uint64 tensor map (dims innermost first, dense)
