@@ -80,6 +80,7 @@ struct fhe_ctx {
     uint64_t key_seed = 0;
     std::map<uint32_t, uint64_t*> keys;
     std::map<uint32_t, uint64_t*> keys_opf;  // operand-form copies (modarith.cuh to_opf) of the Galois keys
+    unsigned* d_sched = nullptr;             // k_bsgs_tma work queues (kTmaSchedWords)
     uint64_t key_gen = 0;  // bumped by fhe_keygen: per-layer limb key copies are rebuilt
     fhe_ledger ledger{};
     uint64_t launch_base = 0;
@@ -597,6 +598,7 @@ void upload_tables(fhe_ctx* c) {
     up((void**)&c->d_itwd, itwd.data(), itwd.size() * sizeof(double2));
     up((void**)&c->d_ninvd, ninvd.data(), ninvd.size() * sizeof(double2));
     up((void**)&c->d_modup, mu.data(), mu.size() * sizeof(ModUpDigit));
+    ck(cudaMalloc(&c->d_sched, kTmaSchedWords * sizeof(unsigned)), "cudaMalloc");
     up((void**)&c->d_md, &md, sizeof(md));
     up((void**)&c->d_qlinv, ql.data(), ql.size() * 8);
     up((void**)&c->d_qlinv_sh, qls.data(), qls.size() * 8);
@@ -953,6 +955,20 @@ void prepare_paper(fhe_ctx* c, const fhe_conv_layer* ly, int approach) {
     if (dirty) ck(cudaStreamSynchronize(c->st), "paper operands");
 }
 
+// Work-queue rows of k_bsgs_tma at a level: the integer-path (q >= 2^50) extended rows
+// first, then the FP64 rows (kernels.cuh TmaMaps)
+void tma_rows(fhe_ctx* c, int level, TmaMaps& tm) {
+    const int nr = level + 1, ne = nr + c->K;
+    int n = 0;
+    for (int pass = 0; pass < 2; ++pass)
+        for (int u = 0; u < ne; ++u) {
+            const uint64_t q = c->primes[u < nr ? u : c->L + (u - nr)];
+            if ((q >= (1ULL << 50)) == (pass == 0)) tm.rowlist[n++] = (uint8_t)u;
+            if (pass == 0 && u == ne - 1) tm.nint = n;
+        }
+    tm.sched = c->d_sched;  // allocated with the context tables (never inside a graph capture)
+}
+
 // Baby steps of the fused BSGS schedule for nsrc sources: Y_g(s) for every
 // giant g (chunks of kFusedMaxG giants per launch), X~_b never materialised.
 // limb: digits are limb-form ModUp digits and cts the limb-form P-scaled
@@ -967,6 +983,7 @@ void fused_babies(fhe_ctx* c, const fhe_conv_layer::Bsgs& B, int level, const ui
     TmaMaps tm{};
     const bool tma = limb && c->tma;
     if (tma) {  // tensor maps of this launch's operands (kernels.cuh TmaMaps)
+        tma_rows(c, level, tm);
         if (nsrc > 1 && (dstride != (size_t)dn * extw || ctstride != (size_t)2 * nr * c->N))
             fail(FHE_E_RUNTIME, "tma staging needs dense digit / ciphertext batches");
         const uint32_t sg = (uint32_t)tma_sources(nsrc), P2 = 256u / sg;
@@ -1502,6 +1519,7 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
         // copy's digits / c0 through the 5-D maps' slot coordinate, one giant
         ct_prescale(c->dc, X, X, ctw, S * NF, c->d_md, level, c->st);
         TmaMaps tm{};
+        tma_rows(c, level, tm);
         const uint32_t sg = (uint32_t)tma_sources(S), P2 = 256u / sg;
         const size_t keyw = (size_t)c->dnum * 2 * c->np * N;
         uint64_t nkeys = 0;
@@ -2297,6 +2315,7 @@ void fhe_ctx_destroy(fhe_ctx* c) {
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto& kv : c->keys) cudaFreeAsync(kv.second, c->st);
     for (auto& kv : c->keys_opf) cudaFreeAsync(kv.second, c->st);
+    if (c->d_sched) cudaFreeAsync(c->d_sched, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
     void* bufs[] = {c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv, c->d_ninv_sh,
                     c->d_twd,    c->d_itwd, c->d_ninvd,

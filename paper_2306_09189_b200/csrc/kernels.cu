@@ -1015,16 +1015,47 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
     const size_t items = chunks * (size_t)ngroups;
     const uint32_t nmask = (2u << c.logN) - 1;
     RowMap rm{ne, level, c.L, 0};
+    // Work queues (m.sched, zeroed per launch): queue 0 = the items of the integer
+    // (60-bit) rows, queue 1 = the FP64 rows (m.rowlist: integer rows first). The
+    // first CTA resident on each SM drains queue 0, the others queue 1, so every SM
+    // runs integer-multiply and FP64 work side by side; a CTA whose queue is empty
+    // helps with the other one. Items: group fastest, then chunk, then row.
+    __shared__ int s_item[2];
+    const size_t cpr = (size_t)c.N / BW;  // chunks per row
+    const size_t nq[2] = {(size_t)m.nint * cpr * ngroups, (size_t)(ne - m.nint) * cpr * ngroups};
     if (tid == 0) {
         mbar_init(bars, 1);
         mbar_init(bars + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        s_item[1] = (m.nint > 0 && m.nint < ne && atomicAdd(m.sched + 2 + (smid & 255), 1u) == 0) ? 0 : 1;
     }
     __syncthreads();
+    const int role = s_item[1];
     uint32_t phase = 0;
-    for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const size_t chunk = it / (size_t)ngroups;
-        const int s0 = (int)(it % (size_t)ngroups) * SG;
+    (void)items;
+    for (;;) {
+        if (tid == 0) {
+            long long v = -1;
+            for (int r2 = 0; r2 < 2 && v < 0; ++r2) {
+                const int q = role ^ r2;
+                if (!nq[q]) continue;
+                const unsigned x = atomicAdd(m.sched + q, 1u);
+                if (x < nq[q]) v = (long long)q << 40 | x;
+            }
+            s_item[0] = (int)(v < 0 ? -1 : ((v >> 40) << 30 | (v & ((1ll << 30) - 1))));
+        }
+        __syncthreads();
+        const int sv = s_item[0];
+        __syncthreads();
+        if (sv < 0) break;
+        const int qsel = sv >> 30;
+        const size_t xi = (size_t)(sv & ((1 << 30) - 1));
+        const size_t per_row = cpr * ngroups;
+        const int urow = m.rowlist[(qsel ? m.nint : 0) + (int)(xi / per_row)];
+        const size_t chunk = (size_t)urow * cpr + (xi % per_row) / ngroups;
+        const int s0 = (int)(xi % (size_t)ngroups) * SG;
         const int s = s0 + sl;
         const bool active = s < a.nsrc;
         // boxes never leave the tensors: the source box of a partial last group is
@@ -1885,6 +1916,8 @@ static void launch_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, in
 void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st) {
     if (a.nb <= 0 || a.nsrc <= 0 || a.ng <= 0) return;
     if (a.ng > kFusedMaxG) throw std::invalid_argument("bsgs_tma: too many giants per launch");
+    if (!m.sched) throw std::invalid_argument("bsgs_tma: no work-queue buffer");
+    cudaMemsetAsync(m.sched, 0, kTmaSchedWords * sizeof(unsigned), st);
     ++g_launches;
     const int sg = tma_sources(a.nsrc);
 #define FHE_TMA(D)                                                               \

@@ -313,7 +313,14 @@ struct TmaMaps {
     int16_t bidx[kMaxFused];  // baby b's index in the plaintext map
     int g0;                   // first giant of the launch
     int ng1;                  // the plaintext box spans one giant (paper schedules: ng == 1)
+    // work queues (k_bsgs_tma): extended rows in queue order, the nint integer-path
+    // (q >= 2^50) rows first; sched = [2 queue heads][256 per-SM arrival counters],
+    // zeroed before every launch (bsgs_tma does it on the launch stream)
+    uint8_t rowlist[kMaxPrimes];
+    int nint;
+    unsigned* sched;
 };
+constexpr int kTmaSchedWords = 2 + 256;
 // encode a 5-D uint64 tensor map (dims innermost first, dense)
 void tma_map5(CUtensorMap* map, const void* base, const uint64_t dims[5], const uint32_t box[5]);
 inline int tma_sources(int nsrc) { return nsrc >= 4 ? 4 : nsrc >= 2 ? 2 : 1; }
