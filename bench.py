@@ -130,14 +130,15 @@ def measured_peak():
 
 # committed ncu --set full capture of the dominant kernel at the step's batch (same build);
 # written by tools/ncu_fused.sh + tools/ncu_summary.py and copied under profiles/
-NCU_DOMINANT = os.path.join("profiles", "ncu_r02_bsgs_tma_b16_summary.txt")
+NCU_DOMINANT = os.path.join("profiles", "ncu_r02_bsgs_fp64_b16_summary.txt")
 
 
 def ncu_capture(path=NCU_DOMINANT):
-    """duration, DRAM bytes and integer-pipe utilisation of the committed ncu capture"""
+    """duration, DRAM bytes and issue / integer / FP64 pipe utilisation of the committed ncu capture"""
     keys = {"gpu__time_duration.sum": "duration_ms", "dram__bytes_read.sum": "dram_read",
             "dram__bytes_write.sum": "dram_write", "sm__inst_issued.avg.pct_of_peak_sustained_active": "issue_pct",
             "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed": "fmaheavy_pct",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pct",
             "smsp__inst_executed.sum": "warp_instructions"}
     scale = {"ms": 1.0, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3,
              "byte": 1.0, "%": 1.0, "inst": 1.0}
@@ -451,8 +452,9 @@ def roofline_timed(prof_b, kbp, B, peak, peak_kind, step_s, level):
     launch read once, every ciphertext read once; ModUp digits and QP accumulators are
     intermediates): the fused baby-step launch touches the 47 keyed baby-step keys of the schedule
     (r m^2 + ll), its 144 rotated plaintexts and the B input ciphertexts. `traffic` and the
-    integer-pipe figures come from the committed ncu capture of the same kernel at the same batch
-    (profiles/, NCU_DOMINANT); the batched kernel is integer-issue bound, not HBM-bound."""
+    pipe figures come from the committed ncu capture of the same kernel at the same batch
+    (profiles/, NCU_DOMINANT); the batched kernel is bound by its FP64 (rows q < 2^50) and integer
+    (60-bit rows) multiply pipes, not by HBM."""
     tot = sum(v[0] for v in prof_b.values())
     if not tot:
         return None
@@ -473,14 +475,16 @@ def roofline_timed(prof_b, kbp, B, peak, peak_kind, step_s, level):
                                  "(c-1 + k^2-1) and 144 plaintexts once per batch, B ciphertexts in and out",
                          "achieved_gbs": round(step_bytes / step_s / 1e9, 1),
                          "frac": round(step_bytes / step_s / 1e9 / peak, 4)},
-            "int_pipe": {"issue_frac": round(ncu["issue_pct"] / 100, 3) if "issue_pct" in ncu else None,
+            "pipes": {"issue_frac": round(ncu["issue_pct"] / 100, 3) if "issue_pct" in ncu else None,
+                      "fp64_frac": round(ncu["fp64_pct"] / 100, 3) if "fp64_pct" in ncu else None,
                          "fmaheavy_frac": round(ncu["fmaheavy_pct"] / 100, 3) if "fmaheavy_pct" in ncu else None,
                          "ncu_duration_ms": ncu.get("duration_ms"), "ncu_kernel": ncu.get("kernel"),
                          "source": ncu.get("source")},
             "measured_on": f"{kbp} batched steps of {B} ciphertexts (graphs off, CUDA events per launch) right "
                            "after the timed region",
             "note": "batched, every key and plaintext byte is shared by the B ciphertexts: the kernel is bound "
-                    "by 64-bit integer multiply issue (int_pipe), so the HBM fraction is low by construction; "
+                    "by its multiply pipes (FP64 for the rows q < 2^50, IMAD for the 60-bit rows; `pipes`), so the "
+                    "HBM fraction is low by construction; "
                     "roofline_single_ct is the HBM-bound latency regime"}
 
 

@@ -1240,11 +1240,16 @@ void conv_bsgs(fhe_ctx* c, const fhe_ct* ct, const fhe_conv_layer* ly, int orien
 // gamt[gi]) is key-switched as KS(Y.c1) + sigma(Y.c0) into the source's QP
 // accumulator (ModDown(Y.c1) in the coefficient domain feeding a batched
 // ModUp), the identity giant `id` is added as is; md = [S][2][level][N].
-void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, const std::vector<int>& giants,
+void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, const std::vector<int>& giants_in,
                    const std::vector<int64_t>& gamt, int id, uint64_t* md, const uint64_t* bias = nullptr,
                    int bias_mod = 1) {
     const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
     const size_t N = c->N, extw = (size_t)ne * N, dw = (size_t)dn * extw;
+    // a giant whose amount is a multiple of the slot count (single-row channel shards:
+    // kk m = kk slots) is the identity: its accumulator is added, not key-switched
+    std::vector<int> giants, idg;
+    if (id >= 0) idg.push_back(id);
+    for (int g : giants_in) (c->reduce_amount(gamt[g]) == 0 ? idg : giants).push_back(g);
     uint64_t* acc = c->alloc((size_t)S * 2 * extw);
     ck(cudaMemsetAsync(acc, 0, (size_t)S * 2 * extw * 8, c->st), "memset");
     const int GT = (int)giants.size();
@@ -1299,9 +1304,9 @@ void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, c
         c->release(yq);
         c->release(yc);
     }
-    if (id >= 0)
+    for (int g : idg)
         for (int s = 0; s < S; ++s)
-            qp_add(c->dc, acc + (size_t)s * 2 * extw, Y + (size_t)s * ys + (size_t)id * 2 * extw, level, c->st);
+            qp_add(c->dc, acc + (size_t)s * 2 * extw, Y + (size_t)s * ys + (size_t)g * 2 * extw, level, c->st);
     moddown_rescale(c, acc, extw, level, 2 * S, md, bias, bias_mod);
     c->release(acc);
 }

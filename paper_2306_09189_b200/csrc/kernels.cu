@@ -10,6 +10,12 @@
 
 #include "kernels.cuh"
 
+// k_bsgs_tma FP64 rows: read a digit pair with one 16-byte shared load and swap in
+// registers (1), or as two 8-byte loads in output order (0)
+#ifndef FHE_DIG128
+#define FHE_DIG128 0
+#endif
+
 #ifndef FHE_FUSED_UNROLL2  // fused kernel: two baby steps per loop iteration (constant stage offsets)
 #define FHE_FUSED_UNROLL2 1
 #endif
@@ -1116,7 +1122,13 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
 #pragma unroll
                     for (int j = 0; j < DN; ++j) {
                         const double2 k0 = sk[(2 * j) * P + p], k1 = sk[(2 * j + 1) * P + p];
+#if FHE_DIG128
+                        // one conflict-free 16-byte load of the permuted pair, swapped in registers
+                        const double2 dp = reinterpret_cast<const double2*>(sd)[j * P + (wo >> 1)];
+                        const double d0 = (wo & 1) ? dp.y : dp.x, d1 = (wo & 1) ? dp.x : dp.y;
+#else
                         const double d0 = sd[j * BW + wo], d1 = sd[j * BW + (wo ^ 1)];
+#endif
                         fmac_d(z[0][0], d0, k0.x, ad);
                         fmac_d(z[0][1], d1, k0.y, ad);
                         fmac_d(z[1][0], d0, k1.x, ad);
