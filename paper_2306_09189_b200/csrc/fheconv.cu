@@ -1261,21 +1261,24 @@ void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, c
         uint64_t* yc = c->alloc((size_t)SC * G * extw);
         uint64_t* yq = c->alloc((size_t)SC * G * nr * N);
         uint64_t* dg = c->alloc((size_t)SC * G * dw);
+        // operand-form key switches (k_ks_giant_opf): digits, keys and the giants' QP c0
+        // rows in operand form
+        const bool opf = c->limb;
+        uint64_t* yc0 = opf ? c->alloc((size_t)SC * G * extw) : nullptr;
         for (int s0 = 0; s0 < S; s0 += SC) {
             const int sc = std::min(SC, S - s0);
-            for (int s = 0; s < sc; ++s)
-                for (int gi = 0; gi < G; ++gi)
-                    ck(cudaMemcpyAsync(yc + ((size_t)s * G + gi) * extw,
-                                       Y + (size_t)(s0 + s) * ys + (size_t)giants[gb + gi] * 2 * extw + extw,
-                                       extw * 8, cudaMemcpyDeviceToDevice, c->st),
-                       "memcpy");
+            GiantSel gsel{};
+            gsel.n = G;
+            for (int gi = 0; gi < G; ++gi) gsel.idx[gi] = giants[gb + gi];
+            giant_gather(c->dc, yc, yc0, Y + (size_t)s0 * ys, ys, sc, gsel, level, c->st);
             const int np_ = sc * G;
             c->timed("ntt", c->rows(2.0 * np_ * ne),
                      [&] { ntt_inverse(c->dc, yc, np_ * ne, RowMap{ne, level, c->L, 0}, c->st); });
             c->timed("moddown", c->rows((double)np_ * (ne + nr)),
                      [&] { moddown_coef(c->dc, yq, yc, c->d_md, level, np_, c->st); });
             c->timed("ntt_modup", c->rows((double)np_ * nr + (double)np_ * dn * ne), [&] {
-                ntt_modup_coef(c->dc, dg, yq, np_, c->d_modup + (size_t)level * c->dnum, level, dn, c->st);
+                ntt_modup_coef(c->dc, dg, yq, np_, c->d_modup + (size_t)level * c->dnum, level, dn, c->st,
+                               opf ? 1 : 0);
             });
             c->ledger.moddowns += np_;
             c->ledger.modups += np_;
@@ -1285,21 +1288,23 @@ void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, c
             kg.digits = dg;
             kg.digit_src_stride = (size_t)G * dw;
             kg.digit_term_stride = dw;
-            kg.c0 = Y + (size_t)s0 * ys;
-            kg.c0_src_stride = ys;
+            kg.c0 = opf ? yc0 : Y + (size_t)s0 * ys;
+            kg.c0_src_stride = opf ? (size_t)G * extw : ys;
             kg.c0_qp = 1;
+            kg.opf = opf ? 1 : 0;
             kg.out = acc + (size_t)s0 * 2 * extw;
             kg.out_src_stride = 2 * extw;
             for (int gi = 0; gi < G; ++gi) {
                 const uint32_t g = c->galois_of(c->reduce_amount(gamt[giants[gb + gi]]));
                 kg.galois[gi] = g;
-                kg.key[gi] = c->key_for(g);
-                kg.c0_off[gi] = (size_t)giants[gb + gi] * 2 * extw;
+                kg.key[gi] = opf ? c->key_opf_for(g) : c->key_for(g);
+                kg.c0_off[gi] = opf ? (size_t)gi * extw : (size_t)giants[gb + gi] * 2 * extw;
             }
             c->ledger.key_switches += (uint64_t)G * sc;
             c->timed("ks_inner", c->rows((double)G * 2.0 * dn * ne + (double)sc * G * (dn * ne + ne) + 4.0 * ne * sc),
                      [&] { ks_batch(c->dc, kg, 1, c->d_md, level, dn, c->st); });
         }
+        c->release(yc0);
         c->release(dg);
         c->release(yq);
         c->release(yc);
@@ -2718,7 +2723,10 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
         const int nr = level + 1, ne = c->ne_at(level), dn = c->dn_at(level);
         const size_t N = c->N, extw = (size_t)ne * N, ctw = (size_t)2 * nr * N, dw = (size_t)dn * extw;
         const size_t KK = keyed.size();
-        const size_t SC = std::max<size_t>(1, std::min<size_t>(n, 16));  // sources per chunk
+        // sources per chunk: as many as ~4 GB of temporaries hold (input copies, digits,
+        // QP key-switch outputs), at most 256; large chunks keep small rings (cfg2) busy
+        const size_t per_src = 8 * (ctw + dw + KK * 2 * extw);
+        const size_t SC = std::max<size_t>(1, std::min<size_t>({n, (size_t)256, ((size_t)4 << 30) / per_src}));
         uint64_t *buf = nullptr, *dig = nullptr, *XT = nullptr;
         uint64_t** outp = nullptr;  // device table of the keyed outputs' residue buffers (ModDown writes there)
         std::vector<uint64_t*> hostp;

@@ -1342,6 +1342,23 @@ __global__ void k_rows_to_limb(DevCtx c, uint64_t* dst, const uint64_t* src, siz
     }
 }
 
+// Giant-step inputs of sc sources x G giants in one pass: the c1 rows of Y(s, giant[g])
+// copied to yc ([sc][G][ne][N], for the coefficient-domain ModDown) and the c0 rows
+// converted to operand form into yc0 (same layout, for k_ks_giant_opf).
+__global__ void k_giant_gather(DevCtx c, uint64_t* yc, uint64_t* yc0, const uint64_t* Y, size_t ys, int sc,
+                               GiantSel gs, int level) {
+    const int ne = level + 1 + c.K;
+    const size_t extw = (size_t)ne * c.N, total = (size_t)sc * gs.n * extw;
+    RowMap rm{ne, level, c.L, 0};
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t pg = i / extw, w = i - pg * extw;
+        const int s = (int)(pg / gs.n), g = (int)(pg % gs.n);
+        const uint64_t* y = Y + (size_t)s * ys + (size_t)gs.idx[g] * 2 * extw;
+        yc[i] = y[extw + w];
+        if (yc0) yc0[i] = to_opf(y[w], c.primes[row_prime(rm, (int)(w >> c.logN))].q);
+    }
+}
+
 __global__ void k_ct_prescale(DevCtx c, uint64_t* dst, const uint64_t* ct, size_t stride, int nsrc,
                               const ModDownTable* md, int level) {
     const int nr = level + 1;
@@ -1443,6 +1460,153 @@ __global__ void __launch_bounds__(128, 3) k_ks_giant(DevCtx c, KsBatch a, int le
             add128(r1b, a1.y);
             st2(out + i, reduce128(r0a.hi, r0a.lo, pr), reduce128(r0b.hi, r0b.lo, pr));
             st2(out + total + i, reduce128(r1a.hi, r1a.lo, pr), reduce128(r1b.hi, r1b.lo, pr));
+        }
+        __syncthreads();
+    }
+}
+
+// k_ks_giant on operand-form rows (KsBatch.opf, mode 1): acc(s) += sum_t (IP(D(s,t),
+// key_t) + sigma_t(Y(s,t).c0)), the products of rows q < 2^50 on the FP64 pipe (one
+// red_d per term keeps the double sums exact), the 60-bit rows on 30-bit limbs.
+template <int DN, int SG>
+__global__ void __launch_bounds__(128, 4) k_ks_giant_opf(DevCtx c, KsBatch a, int level) {
+    constexpr int P = 128 / SG;
+    constexpr int KW = 2 * DN * P, DW = SG * DN * P, CW = SG * P, STAGE = KW + DW + CW;
+    extern __shared__ ulonglong2 sb[];  // [2][STAGE]
+    const int nr = level + 1, ne = nr + c.K, np = c.L + c.K;
+    const int tid = threadIdx.x, p = tid % P, sl = tid / P;
+    const size_t total = (size_t)ne * c.N;
+    const size_t chunks = total / 2 / P;
+    const int ngroups = (a.nsrc + SG - 1) / SG;
+    const size_t items = chunks * (size_t)ngroups;
+    const size_t keyrow = (size_t)np * c.N;
+    RowMap rm{ne, level, c.L, 0};
+    ulonglong2* const s_key = sb + p;
+    ulonglong2* const s_dig = sb + KW + sl * DN * P + p;
+    ulonglong2* const s_c0 = sb + KW + DW + sl * P + p;
+    constexpr uint32_t MW = (1u << 30) - 1;
+    for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const size_t chunk = it / (size_t)ngroups;
+        const int s = (int)(it % (size_t)ngroups) * SG + sl;
+        const bool active = s < a.nsrc;
+        const size_t i = (chunk * P + p) * 2;
+        const int u = (int)(i >> c.logN);
+        const uint32_t k = (uint32_t)(i & (size_t)(c.N - 1));
+        const int pi = row_prime(rm, u);
+        const size_t kofs = (size_t)pi * c.N + k;
+        const uint32_t e = 2 * brev_n(k, c.logN) + 1, nmask = (2u << c.logN) - 1;
+        auto pidx = [&](uint32_t g) { return brev_n((((e * g) & nmask) - 1) >> 1, c.logN); };
+        auto issue = [&](int t) {
+            const size_t so = (size_t)(t & 1) * STAGE;
+            const uint64_t* kp = a.key[t] + kofs;
+#pragma unroll
+            for (int j = sl; j < 2 * DN; j += SG) cp_async16(s_key + so + j * P, kp + (size_t)j * keyrow);
+            if (active) {
+                const uint32_t pk = pidx(a.galois[t]) & ~1u;
+                const uint64_t* D = a.digits + (size_t)s * a.digit_src_stride + (size_t)t * a.digit_term_stride +
+                                    (size_t)u * c.N + pk;
+#pragma unroll
+                for (int j = 0; j < DN; ++j) cp_async16(s_dig + so + j * P, D + (size_t)j * total);
+                cp_async16(s_c0 + so, a.c0 + (size_t)s * a.c0_src_stride + a.c0_off[t] + (size_t)u * c.N + pk);
+            }
+            cp_async_commit();
+        };
+        const Prime pr = c.primes[pi];
+        const bool fp = opf_fp(pr.q);
+        const ArD ad = make_ard(pr.q);
+        const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> 30), qinv = (uint32_t)pr.qinv & MW;
+        double zf[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        uint64_t zi[2][2] = {{0, 0}, {0, 0}};  // 60-bit rows: sum of the terms' X 2^-90, reduced
+        issue(0);
+        for (int t = 0; t < a.n; ++t) {
+            cp_async_wait<0>();
+            __syncthreads();
+            if (t + 1 < a.n) issue(t + 1);
+            const size_t so = (size_t)(t & 1) * STAGE;
+            const int swp = (int)(pidx(a.galois[t]) & 1u);
+            const ulonglong2 cv = s_c0[so];
+            const uint64_t ca = swp ? cv.y : cv.x, cb = swp ? cv.x : cv.y;
+            if (fp) {
+                double z[2][2] = {{zf[0][0] + asd(ca), zf[0][1] + asd(cb)}, {zf[1][0], zf[1][1]}};
+#pragma unroll
+                for (int j = 0; j < DN; ++j) {
+                    const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
+                    const ulonglong2 dv = s_dig[so + j * P];
+                    const double da = asd(swp ? dv.y : dv.x), db = asd(swp ? dv.x : dv.y);
+                    fmac_d(z[0][0], da, asd(k0.x), ad);
+                    fmac_d(z[0][1], db, asd(k0.y), ad);
+                    fmac_d(z[1][0], da, asd(k1.x), ad);
+                    fmac_d(z[1][1], db, asd(k1.y), ad);
+                }
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) zf[q2][e2] = red_d(z[q2][e2], ad);
+            } else {
+                uint64_t z0[2][2] = {{0, 0}, {0, 0}}, z1[2][2] = {{0, 0}, {0, 0}}, z2[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
+                for (int j = 0; j < DN; ++j) {
+                    const ulonglong2 kv0 = s_key[so + (2 * j) * P], kv1 = s_key[so + (2 * j + 1) * P];
+                    const ulonglong2 dv = s_dig[so + j * P];
+                    const uint64_t dw[2] = {swp ? dv.y : dv.x, swp ? dv.x : dv.y};
+                    const uint64_t kw[2][2] = {{kv0.x, kv0.y}, {kv1.x, kv1.y}};
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        const uint32_t d0 = lo32(dw[e2]), d1 = hi32(dw[e2]);
+#pragma unroll
+                        for (int q2 = 0; q2 < 2; ++q2) {
+                            const uint32_t kk0 = lo32(kw[q2][e2]), kk1 = hi32(kw[q2][e2]);
+                            madw(z0[q2][e2], d0, kk0);
+                            madw(z1[q2][e2], d0, kk1);
+                            madw(z1[q2][e2], d1, kk0);
+                            madw(z2[q2][e2], d1, kk1);
+                        }
+                    }
+                }
+                if constexpr (DN >= 8) {
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            z2[q2][e2] += z1[q2][e2] >> 30;
+                            z1[q2][e2] &= MW;
+                        }
+                }
+                const uint64_t cw[2] = {ca, cb};
+#pragma unroll
+                for (int e2 = 0; e2 < 2; ++e2) {  // + sigma(Y.c0), every row
+                    z0[0][e2] += lo32(cw[e2]);
+                    z1[0][e2] += hi32(cw[e2]);
+                }
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        uint64_t x = mont_l30(z0[q2][e2], z1[q2][e2], z2[q2][e2], q0, q1, qinv);  // < 2q
+                        x = x >= pr.q ? x - pr.q : x;
+                        zi[q2][e2] = add_mod(zi[q2][e2], x, pr.q);
+                    }
+            }
+        }
+        if (active) {
+            uint64_t o[2][2];
+            if (fp) {
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) o[q2][e2] = canon_d(zf[q2][e2], ad);
+            } else {
+                uint64_t r90 = reduce64(1ULL << 45, pr);
+                r90 = mul_mod(r90, r90, pr);
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) o[q2][e2] = mul_mod(zi[q2][e2], r90, pr);
+            }
+            uint64_t* out = a.out + (size_t)s * a.out_src_stride;
+            const ulonglong2 a0 = ld2(out + i), a1 = ld2(out + total + i);
+            st2(out + i, add_mod(o[0][0], a0.x, pr.q), add_mod(o[0][1], a0.y, pr.q));
+            st2(out + total + i, add_mod(o[1][0], a1.x, pr.q), add_mod(o[1][1], a1.y, pr.q));
         }
         __syncthreads();
     }
@@ -1764,6 +1928,18 @@ static void launch_giant(const DevCtx& c, const KsBatch& a, int level, cudaStrea
 }
 
 template <int DN, int SG>
+static void launch_giant_opf(const DevCtx& c, const KsBatch& a, int level, cudaStream_t st) {
+    constexpr int P = 128 / SG;
+    const size_t smem = (size_t)2 * (2 * DN * P + SG * DN * P + SG * P) * sizeof(ulonglong2);
+    const size_t items = (size_t)(level + 1 + c.K) * c.N / 2 / P * (size_t)((a.nsrc + SG - 1) / SG);
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_ks_giant_opf<DN, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ks_giant_opf<DN, SG>, 128, smem);
+    const size_t cap = (size_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+    k_ks_giant_opf<DN, SG><<<(int)(items < cap ? items : cap), 128, smem, st>>>(c, a, level);
+}
+
+template <int DN, int SG>
 static void launch_hoist_opf(const DevCtx& c, const KsBatch& a, int level, cudaStream_t st) {
     constexpr int P = 128 / SG;
     const size_t smem = (size_t)2 * (2 * DN * P + SG * DN * P + SG * P) * sizeof(ulonglong2);
@@ -1812,11 +1988,17 @@ void ks_batch(const DevCtx& c, const KsBatch& a, int mode, const ModDownTable* m
     if (mode == 1 && a.c0_qp) {  // giant steps: staged, key rows shared by the sources of a CTA
         ++g_launches;
         const int sg = a.nsrc >= 4 ? 4 : a.nsrc >= 2 ? 2 : 1;
-#define FHE_GIANT(D)                                                 \
-    do {                                                             \
-        if (sg == 4) launch_giant<D, 4>(c, a, level, st);            \
-        else if (sg == 2) launch_giant<D, 2>(c, a, level, st);       \
-        else launch_giant<D, 1>(c, a, level, st);                    \
+#define FHE_GIANT(D)                                                     \
+    do {                                                                 \
+        if (a.opf) {                                                     \
+            if (sg == 4) launch_giant_opf<D, 4>(c, a, level, st);        \
+            else if (sg == 2) launch_giant_opf<D, 2>(c, a, level, st);   \
+            else launch_giant_opf<D, 1>(c, a, level, st);                \
+        } else {                                                         \
+            if (sg == 4) launch_giant<D, 4>(c, a, level, st);            \
+            else if (sg == 2) launch_giant<D, 2>(c, a, level, st);       \
+            else launch_giant<D, 1>(c, a, level, st);                    \
+        }                                                                \
     } while (0)
         FHE_DN_SWITCH(dn, FHE_GIANT)
 #undef FHE_GIANT
@@ -1993,6 +2175,13 @@ void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nr
                   cudaStream_t st) {
     ++g_launches;
     k_rows_to_limb<<<ew_blocks(nrows * c.N), kEwThreads, 0, st>>>(c, dst, src, nrows, rm);
+}
+
+void giant_gather(const DevCtx& c, uint64_t* yc, uint64_t* yc0, const uint64_t* Y, size_t ys, int sc, const GiantSel& gs,
+                  int level, cudaStream_t st) {
+    ++g_launches;
+    k_giant_gather<<<ew_blocks((size_t)sc * gs.n * (level + 1 + c.K) * c.N), kEwThreads, 0, st>>>(c, yc, yc0, Y, ys, sc,
+                                                                                                gs, level);
 }
 
 void ct_prescale(const DevCtx& c, uint64_t* dst, const uint64_t* ct, size_t stride, int nsrc, const ModDownTable* md,

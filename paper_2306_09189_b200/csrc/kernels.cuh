@@ -139,7 +139,7 @@ void ntt_modup(const DevCtx& c, uint64_t* digits, const uint64_t* coef, const ui
 // ModUp of nsrc coefficient-domain sources coef = [nsrc][level+1][N]: every
 // digit row (own rows included) = conversion of coef, then the forward NTT
 void ntt_modup_coef(const DevCtx& c, uint64_t* digits, const uint64_t* coef, int nsrc, const ModUpDigit* tables,
-                    int level, int dn, cudaStream_t st);
+                    int level, int dn, cudaStream_t st, int limb = 0);
 // coefficient-domain ModDown: out[p][t] = (y[p][t] - conv_P->q_t(y[p][P rows])) P^-1, y = [npoly][ne][N]
 void moddown_coef(const DevCtx& c, uint64_t* out, const uint64_t* y, const ModDownTable* md, int level, int npoly,
                   cudaStream_t st);
@@ -253,8 +253,9 @@ struct KsBatch {
     const uint64_t* c0;
     size_t c0_src_stride;
     int c0_qp;
-    // mode 0 only: digits, keys and c0 in operand form (modarith.cuh to_opf; c0 = the
-    // P-scaled [P c]_q of ct_prescale, same [2][level+1][N] layout): k_ks_hoist_opf
+    // digits, keys and c0 in operand form (modarith.cuh to_opf): mode 0 (k_ks_hoist_opf)
+    // c0 = the P-scaled [P c]_q of ct_prescale, same [2][level+1][N] layout; mode 1
+    // (k_ks_giant_opf) c0 = operand-form copies of the QP c0 rows at c0 + c0_off[t]
     int opf;
     uint64_t* out;  // mode 0: XT of source s at out + s * out_src_stride; mode 1: acc of source s
     size_t out_src_stride;
@@ -329,6 +330,14 @@ void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, 
 void tma_map4(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint32_t box[4]);
 // dst[i] = to_opf(src[i]) for nrows rows of N words; row r uses prime
 // row_prime(rm, r % rm.rows_per_poly) (rm.level < 0: prime index r % rows_per_poly)
+struct GiantSel {
+    int n;
+    int idx[kMaxBaby];  // giant index of entry g
+};
+// yc[s][g] = Y(s, idx[g]).c1 rows and (yc0 != null) yc0[s][g] = to_opf(Y(s, idx[g]).c0 rows),
+// Y(s, j) = Y + s * ys + j * 2 ne N ([2][ne][N] QP accumulators), one launch
+void giant_gather(const DevCtx& c, uint64_t* yc, uint64_t* yc0, const uint64_t* Y, size_t ys, int sc, const GiantSel& gs,
+                  int level, cudaStream_t st);
 void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,
                   cudaStream_t st);
 // dst[s][p][u] = to_opf([P ct_s[p][u]]_{q_u}) for nsrc ciphertexts at ct + s * stride ([2][level+1][N])

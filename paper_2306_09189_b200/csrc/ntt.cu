@@ -845,7 +845,7 @@ void moddown_coef(const DevCtx& c, uint64_t* out, const uint64_t* y, const ModDo
 }
 
 void ntt_modup_coef(const DevCtx& c, uint64_t* digits, const uint64_t* coef, int nsrc, const ModUpDigit* tables,
-                    int level, int dn, cudaStream_t st) {
+                    int level, int dn, cudaStream_t st, int limb) {
     const int ne = level + 1 + c.K;
     NttFuse fz{};
     fz.coef = coef;
@@ -861,7 +861,7 @@ void ntt_modup_coef(const DevCtx& c, uint64_t* digits, const uint64_t* coef, int
         default: k_bconv_modup<4><<<blocks, 256, 0, st>>>(c, digits, fz, level, nsrc); break;
     }
     note_launch(1);
-    ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, 0, dn}, false, FUSE_NONE, fz, st);
+    ntt_run(c, digits, nsrc * dn * ne, RowMap{ne, level, c.L, 0, dn, limb}, false, FUSE_NONE, fz, st);
 }
 
 void ntt_moddown(const DevCtx& c, uint64_t* conv, const uint64_t* pcoef, const uint64_t* acc, size_t acc_stride,
