@@ -77,6 +77,9 @@ __device__ __forceinline__ void tw_ld(const double2* p, double2* o, int cnt) {
 #ifndef FHE_NTT_THREADS
 #define FHE_NTT_THREADS 128
 #endif
+#ifndef FHE_NTT_MINB
+#define FHE_NTT_MINB 1
+#endif
 constexpr int EPT = FHE_NTT_EPT;         // residues per thread in a pass
 constexpr int NTT_THREADS = FHE_NTT_THREADS;
 constexpr int LOG_EPT = EPT == 16 ? 4 : 3;
@@ -307,7 +310,7 @@ struct PassPlan {  // stages of the two passes of a phase of 2^LOGN elements
 // Forward: canonical words in, lazy [0, 4q) words / reduced doubles out (read by the
 // row pass); inverse: the row pass's words in, canonical words out (times N^-1).
 template <int LOG_N1, int C, bool INVERSE>
-__global__ void __launch_bounds__(NTT_THREADS) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm) {
+__global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm) {
     constexpr int N1 = 1 << LOG_N1;
     constexpr int PN = N1 + (N1 >> 4) + 1;  // padded column length (odd in words)
     using PP = PassPlan<LOG_N1, INVERSE>;
@@ -386,7 +389,7 @@ __device__ __forceinline__ uint32_t perm_index_n(uint32_t k, uint32_t g, int log
 // transform ends here (canonical words; FUSE_MODDOWN: the ModDown epilogue), the
 // inverse starts here (canonical words in, words for the column pass out).
 template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE>
-__global__ void __launch_bounds__(NTT_THREADS) k_ntt_rows(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
+__global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_rows(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
     constexpr int B = 1 << LOG_B;
     constexpr int TPB = B / EPT;
     constexpr int BPC = NTT_THREADS / TPB;

@@ -1,4 +1,5 @@
-"""Build a variant libfheconv.so with extra -D flags into tools/var/<name>/ (kernels.cu only differs)."""
+"""Build a variant libfheconv.so with extra -D flags into tools/var/<name>/ (the sources in $VAR_SOURCES,
+default kernels.cu, are recompiled with the flags)."""
 import os, subprocess, sys
 sys.path.insert(0, ".")
 from paper_2306_09189_b200 import build as B
@@ -7,7 +8,7 @@ out = os.path.join("tools", "var", name); os.makedirs(out, exist_ok=True)
 objs = []
 for src in B.SOURCES:
     obj = os.path.join(out, src.replace(".cu", ".o"))
-    if src == "kernels.cu":
+    if src in os.environ.get("VAR_SOURCES", "kernels.cu").split(","):
         subprocess.run([B._nvcc(), *B.NVCC_FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", obj], check=True)
     else:
         obj = os.path.join(B.CSRC, src.replace(".cu", ".o"))

@@ -8,4 +8,4 @@ ncu -f --profile-from-start off --set full --clock-control none --import-source 
 ncu -i gpurun_out/$NAME.ncu-rep --page raw --csv > gpurun_out/${NAME}_raw.csv 2>&1
 ncu -i gpurun_out/$NAME.ncu-rep --page source --csv --print-source sass > gpurun_out/${NAME}_sass.csv 2>&1
 python tools/ncu_summary.py $NAME > gpurun_out/${NAME}_summary.txt 2>&1
-rm -f gpurun_out/${NAME}_sass.csv gpurun_out/${NAME}_raw.csv
+rm -f gpurun_out/${NAME}_sass.csv gpurun_out/${NAME}_raw.csv; [ -n "$KEEP_REP" ] || rm -f gpurun_out/$NAME.ncu-rep
