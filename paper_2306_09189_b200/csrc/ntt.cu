@@ -524,8 +524,10 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
     const int nr = level + 1, ne = nr + c.K;
     const int halfN = c.N / 2;
     const int total = nsrc * fz.dn * halfN;
-    // smem: per digit j, per target u: t, hat[KA], hat_sh[KA], n * Q_J mod t for n = 0..KA
-    constexpr int W = 1 + 2 * KA + (KA + 1);
+    // smem: per digit j, per target u: t, hat[KA], hat_sh[KA], n * Q_J mod t for n = 0..KA,
+    // then (FP64 path) the centred hat[KA] as doubles, t, 1 / t and 2^52 + t as doubles
+    constexpr int WD = 1 + 2 * KA + (KA + 1);
+    constexpr int W = WD + KA + 3;
     __shared__ uint64_t tab[8 * 24 * W];
     __shared__ int lohi[8][2];
     for (int x = threadIdx.x; x < fz.dn * ne; x += blockDim.x) {
@@ -544,6 +546,15 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
             e[1 + 2 * KA + n] = m;
             m = add_mod(m, T.qj[u], t);
         }
+        const ArD ad = make_ard(t);
+#pragma unroll
+        for (int a = 0; a < KA; ++a) {
+            const uint64_t h = T.hat[u][a];
+            e[WD + a] = asu(h > t / 2 ? -(double)(t - h) : (double)h);
+        }
+        e[WD + KA] = asu(ad.q);
+        e[WD + KA + 1] = asu(ad.qinv);
+        e[WD + KA + 2] = asu(ad.qm);
         if (u == 0) {
             lohi[j][0] = T.lo;
             lohi[j][1] = T.hi;
@@ -583,6 +594,18 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
             }
         }
         const uint64_t* tj = tab + (size_t)j * ne * W;
+        // digits whose own primes are all < 2^50: v_a < 2^50 are exact doubles, and the
+        // targets t < 2^50 take the FP64 pipe (fmac_d), the others the integer path
+        bool vfp = true;
+#pragma unroll
+        for (int a = 0; a < KA; ++a)
+            if (a < na) vfp = vfp && tab[((size_t)j * ne + lo + a) * W] < (1ULL << 50);
+        double vd0[KA], vd1[KA];
+#pragma unroll
+        for (int a = 0; a < KA; ++a) {
+            vd0[a] = asd(u2d_bits(v0[a]));
+            vd1[a] = asd(u2d_bits(v1[a]));
+        }
         // targets outside [lo, hi): two branch-free runs
 #pragma unroll 1
         for (int run = 0; run < 2; ++run) {
@@ -591,6 +614,20 @@ __global__ void __launch_bounds__(256) k_bconv_modup(DevCtx c, uint64_t* digits,
             for (int u = ub; u < ue; ++u) {
                 const uint64_t* e = tj + (size_t)u * W;
                 const uint64_t t = e[0];
+                if (vfp && t < (1ULL << 50)) {
+                    const ArD ad{asd(e[WD + KA]), asd(e[WD + KA + 1]), asd(e[WD + KA + 2]), t};
+                    double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+                    for (int a = 0; a < KA; ++a) {
+                        const double h = asd(e[WD + a]);
+                        fmac_d(z0, vd0[a], h, ad);
+                        fmac_d(z1, vd1[a], h, ad);
+                    }
+                    const uint64_t y0 = sub_mod(canon_d(red_d(z0, ad), ad), e[1 + 2 * KA + n0], t);
+                    const uint64_t y1 = sub_mod(canon_d(red_d(z1, ad), ad), e[1 + 2 * KA + n1], t);
+                    *reinterpret_cast<ulonglong2*>(out + (size_t)u * c.N) = make_ulonglong2(y0, y1);
+                    continue;
+                }
                 // lazy sum of na < KA + 1 products, each in [0, 2t)
                 uint64_t y0 = 0, y1 = 0;
 #pragma unroll
