@@ -80,6 +80,11 @@ struct fhe_ctx {
     uint64_t key_seed = 0;
     std::map<uint32_t, uint64_t*> keys;
     std::map<uint32_t, uint64_t*> keys_opf;  // operand-form copies (modarith.cuh to_opf) of the Galois keys
+    // the operand-form keys live in one arena [cap][2 dnum][L+K][N] (slot per key), so a
+    // single TMA tensor map covers all of them (k_bsgs_tma key map, hoisted batches)
+    uint64_t* d_key_arena = nullptr;
+    int arena_cap = 0, arena_n = 0;
+    std::map<uint32_t, int> key_slot;
     unsigned* d_sched = nullptr;             // k_bsgs_tma work queues (kTmaSchedWords)
     uint64_t key_gen = 0;  // bumped by fhe_keygen: per-layer limb key copies are rebuilt
     fhe_ledger ledger{};
@@ -425,6 +430,7 @@ void rescale_into(fhe_ctx* c, const uint64_t* in, int level, uint64_t* out) {
 
 // Galois key for element g, or (g == 0) the relinearisation key s^2 -> s; the
 // PRNG streams are keyed by g, so the golden model derives the same keys.
+void drop_graphs(fhe_ctx* c);
 void gen_key(fhe_ctx* c, uint32_t g) {
     if (c->keys.count(g)) return;
     const size_t N = c->N;
@@ -452,10 +458,27 @@ void gen_key(fhe_ctx* c, uint32_t g) {
     c->release(e);
     c->release(erows);
     c->keys[g] = key;
-    if (g != 0) {  // operand-form copy for the FP64 / limb key-switch kernels (k_ks_hoist_opf)
-        uint64_t* ko = c->alloc((size_t)c->dnum * 2 * np * N);
+    if (g != 0) {  // operand-form copy for the FP64 / limb key-switch kernels, in the key arena
+        const size_t kw = (size_t)c->dnum * 2 * np * N;
+        if (c->arena_n == c->arena_cap) {  // grow: captured graphs hold the old addresses
+            drop_graphs(c);
+            const int cap = std::max(16, 2 * c->arena_cap);
+            uint64_t* na = nullptr;
+            ck(cudaMalloc(&na, (size_t)cap * kw * 8), "cudaMalloc");
+            if (c->arena_n)
+                ck(cudaMemcpyAsync(na, c->d_key_arena, (size_t)c->arena_n * kw * 8, cudaMemcpyDeviceToDevice, c->st),
+                   "memcpy");
+            ck(cudaStreamSynchronize(c->st), "sync");
+            if (c->d_key_arena) cudaFree(c->d_key_arena);
+            c->d_key_arena = na;
+            c->arena_cap = cap;
+            for (auto& kv : c->key_slot) c->keys_opf[kv.first] = na + (size_t)kv.second * kw;
+        }
+        const int slot = c->arena_n++;
+        uint64_t* ko = c->d_key_arena + (size_t)slot * kw;
         rows_to_limb(c->dc, ko, key, (size_t)c->dnum * 2 * np, RowMap{np, -1, c->L, 0}, c->st);
         c->keys_opf[g] = ko;
+        c->key_slot[g] = slot;
     }
 }
 
@@ -2324,7 +2347,7 @@ void fhe_ctx_destroy(fhe_ctx* c) {
     if (!c) return;
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto& kv : c->keys) cudaFreeAsync(kv.second, c->st);
-    for (auto& kv : c->keys_opf) cudaFreeAsync(kv.second, c->st);
+    if (c->d_key_arena) cudaFreeAsync(c->d_key_arena, c->st);
     if (c->d_sched) cudaFreeAsync(c->d_sched, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
     void* bufs[] = {c->d_primes, c->d_tw, c->d_tw_sh, c->d_itw, c->d_itw_sh, c->d_ninv, c->d_ninv_sh,
@@ -2486,8 +2509,9 @@ int fhe_keygen(fhe_ctx* c, uint64_t seed) {
         c->key_gen++;  // layers rebuild their limb key copies on next use
         for (auto& kv : c->keys) c->release(kv.second);
         c->keys.clear();
-        for (auto& kv : c->keys_opf) c->release(kv.second);
-        c->keys_opf.clear();
+        c->keys_opf.clear();  // the arena is reused from slot 0
+        c->key_slot.clear();
+        c->arena_n = 0;
         int64_t* s = (int64_t*)c->alloc(N);
         sample_ternary(c->dc, s, stream_key(seed, stream_id(DOM_SECRET, 0, 0)), c->st);
         const RowMap all{c->np, c->L - 1, c->L, 0};
@@ -2746,7 +2770,40 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
                 // the rows q < 2^50); buf then holds [P c]_q in operand form
                 modup_batch(c, buf + (size_t)nr * N, ctw, (int)sn, level, dig, 1);
                 ct_prescale(c->dc, buf, buf, ctw, (int)sn, c->d_md, level, c->st);
-                for (size_t t0 = 0; t0 < KK; t0 += kMaxBaby) {
+                if (c->tma) {  // k_bsgs_tma MODE 1: TMA staging, keys from the arena, work queues
+                    TmaMaps tm{};
+                    tma_rows(c, level, tm);
+                    const uint32_t sg = (uint32_t)tma_sources((int)sn), P2 = 256u / sg;
+                    const uint64_t dk[4] = {N, (uint64_t)c->np, 2ull * c->dnum, (uint64_t)c->arena_n};
+                    const uint32_t bk[4] = {P2, 1, 2u * dn, 1};
+                    tma_map4(&tm.key, c->d_key_arena, dk, bk);
+                    const uint64_t dd[5] = {N, (uint64_t)ne, (uint64_t)dn, 1, (uint64_t)sn};
+                    const uint32_t bd[5] = {P2, 1, (uint32_t)dn, 1, sg};
+                    tma_map5(&tm.dig, dig, dd, bd);
+                    const uint64_t dc5[5] = {N, (uint64_t)nr, 2, 1, (uint64_t)sn};
+                    const uint32_t bc[5] = {P2, 1, 2, 1, sg};
+                    tma_map5(&tm.ct, buf, dc5, bc);
+                    for (size_t t0 = 0; t0 < KK; t0 += kMaxFused) {
+                        FusedBsgs f{};
+                        f.nsrc = (int)sn;
+                        f.ng = 1;
+                        f.digits = dig;
+                        f.ct = buf;
+                        f.Y = XT + t0 * 2 * extw;
+                        f.y_src_stride = KK * 2 * extw;
+                        f.y_g_stride = 2 * extw;
+                        for (size_t t = t0; t < KK && f.nb < kMaxFused; ++t) {
+                            const uint32_t g = c->galois_of(c->reduce_amount(ks[keyed[t]]));
+                            f.galois[f.nb] = g;
+                            tm.kidx[f.nb] = (int16_t)c->key_slot.at(g);
+                            f.nb++;
+                        }
+                        c->timed("ks_multi",
+                                 c->rows((double)f.nb * 2.0 * dn * ne + sn * ((double)dn * ne + nr + 2.0 * f.nb * ne)),
+                                 [&] { bsgs_tma_hoist(c->dc, f, tm, level, dn, c->st); });
+                    }
+                }
+                for (size_t t0 = 0; t0 < KK && !c->tma; t0 += kMaxBaby) {
                     KsBatch kb{};
                     kb.nsrc = (int)sn;
                     kb.digits = dig;

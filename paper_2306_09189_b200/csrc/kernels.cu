@@ -1006,7 +1006,10 @@ struct TmaLayout {  // one stage, in 16-byte pair slots
     static constexpr int STAGE = KW + PW + DW + CW;
 };
 
-template <int DN, int NG, int SG, int MINB>
+// MODE 1 (hoisted key switches, no plaintexts): every baby's X~_b is written to
+// Y + s * y_src_stride + b * y_g_stride ([2][ne][N], QP, canonical) instead of being
+// multiplied into giant accumulators.
+template <int DN, int NG, int SG, int MINB, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, const __grid_constant__ TmaMaps m,
                                                         int level) {
     using LY = TmaLayout<DN, NG, SG>;
@@ -1081,9 +1084,9 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
             uint64_t* bar = bars + st;
             const bool keyed = m.kidx[b] >= 0;
             const int blk = (int)(pidx(e0, a.galois[b]) & ~(uint32_t)(BW - 1));
-            mbar_expect_tx(bar, (uint32_t)(LY::PW + LY::CW + (keyed ? LY::KW + LY::DW : 0)) * 16u);
+            mbar_expect_tx(bar, (uint32_t)((MODE == 0 ? LY::PW : 0) + LY::CW + (keyed ? LY::KW + LY::DW : 0)) * 16u);
             const int sl5 = a.srcslot[b];  // source slot (paper schedules: the rotated copy)
-            tma_load4(sb + LY::KW, &m.pt, (int)k0, u, m.bidx[b], m.g0, bar);
+            if (MODE == 0) tma_load4(sb + LY::KW, &m.pt, (int)k0, u, m.bidx[b], m.g0, bar);
             tma_load5(sb + LY::KW + LY::PW + LY::DW, &m.ct, blk, qrow ? u : 0, 0, sl5, s0c, bar);
             if (keyed) {
                 tma_load4(sb, &m.key, (int)k0, pi, 0, m.kidx[b], bar);
@@ -1146,6 +1149,16 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                 } else {
                     x[0][0] = x[0][1] = x[1][0] = x[1][1] = 0.0;
                 }
+                if constexpr (MODE == 1) {
+                    if (active) {
+                        uint64_t* yb = a.Y + (size_t)s * a.y_src_stride + (size_t)b * a.y_g_stride;
+                        st2(yb + i, canon_d(x[0][0], ad), canon_d(x[0][1], ad));
+                        st2(yb + total + i, canon_d(x[1][0], ad), canon_d(x[1][1], ad));
+                    }
+                    __syncthreads();  // stage st is free: fetch baby b + 2 into it
+                    issue(b + 2, st);
+                    return;
+                }
                 const uint32_t gm = a.gmask[b];
                 const double2* sp = reinterpret_cast<const double2*>(sb + LY::KW);
 #pragma unroll
@@ -1173,7 +1186,7 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                 baby(b, 0);
                 if (b + 1 < a.nb) baby(b + 1, 1);
             }
-            if (active) {
+            if (MODE == 0 && active) {
                 uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
@@ -1272,6 +1285,18 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                 } else {
                     x[0][0] = x[0][1] = x[1][0] = x[1][1] = 0;
                 }
+                if constexpr (MODE == 1) {
+                    if (active) {
+                        uint64_t r90 = reduce64(1ULL << 45, pr);
+                        r90 = mul_mod(r90, r90, pr);
+                        uint64_t* yb = a.Y + (size_t)s * a.y_src_stride + (size_t)b * a.y_g_stride;
+                        st2(yb + i, mul_mod(x[0][0], r90, pr), mul_mod(x[0][1], r90, pr));
+                        st2(yb + total + i, mul_mod(x[1][0], r90, pr), mul_mod(x[1][1], r90, pr));
+                    }
+                    __syncthreads();
+                    issue(b + 2, st);
+                    return;
+                }
                 const uint32_t gm = a.gmask[b];
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
@@ -1299,7 +1324,7 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                 baby(b, 0);
                 if (b + 1 < a.nb) baby(b + 1, 1);
             }
-            if (active) {
+            if (MODE == 0 && active) {
                 uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
                 // the Montgomery factor 2^-90 of every X~ is restored once
                 uint64_t r = reduce64(1ULL << 45, pr);
@@ -2092,19 +2117,35 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
 #ifndef FHE_TMA_MINB
 #define FHE_TMA_MINB 4
 #endif
-template <int DN, int NG, int SG, int MINB>
+template <int DN, int NG, int SG, int MINB, int MODE = 0>
 static void launch_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, cudaStream_t st) {
     using LY = TmaLayout<DN, NG, SG>;
     const int ne = level + 1 + c.K;
     const size_t smem = (size_t)2 * LY::STAGE * 16 + 16;
     const size_t items = (size_t)ne * c.N / (2 * LY::P) * (size_t)((a.nsrc + SG - 1) / SG);
     int per_sm = 0;
-    cudaFuncSetAttribute(k_bsgs_tma<DN, NG, SG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_tma<DN, NG, SG, MINB>, 128, smem);
+    cudaFuncSetAttribute(k_bsgs_tma<DN, NG, SG, MINB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_tma<DN, NG, SG, MINB, MODE>, 128, smem);
     if (per_sm < 1) per_sm = 1;
     const size_t cap = (size_t)sm_count() * per_sm;
     const int blocks = (int)(items < cap ? items : cap);
-    k_bsgs_tma<DN, NG, SG, MINB><<<blocks, 128, smem, st>>>(c, a, m, level);
+    k_bsgs_tma<DN, NG, SG, MINB, MODE><<<blocks, 128, smem, st>>>(c, a, m, level);
+}
+
+void bsgs_tma_hoist(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st) {
+    if (a.nb <= 0 || a.nsrc <= 0) return;
+    if (!m.sched) throw std::invalid_argument("bsgs_tma: no work-queue buffer");
+    cudaMemsetAsync(m.sched, 0, kTmaSchedWords * sizeof(unsigned), st);
+    ++g_launches;
+    const int sg = tma_sources(a.nsrc);
+#define FHE_TMAH(D)                                                                \
+    do {                                                                           \
+        if (sg == 4) launch_tma<D, 1, 4, FHE_TMA_MINB, 1>(c, a, m, level, st);     \
+        else if (sg == 2) launch_tma<D, 1, 2, 3, 1>(c, a, m, level, st);           \
+        else launch_tma<D, 1, 1, 2, 1>(c, a, m, level, st);                        \
+    } while (0)
+    FHE_DN_SWITCH(dn, FHE_TMAH)
+#undef FHE_TMAH
 }
 
 void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st) {

@@ -322,6 +322,10 @@ struct TmaMaps {
     unsigned* sched;
 };
 constexpr int kTmaSchedWords = 2 + 256;
+// Hoisted key switches on the same kernel (k_bsgs_tma MODE 1, no plaintexts): every
+// baby's X~_b (keyed, [P sigma(c0)] folded into poly 0) is written in the QP basis to
+// a.Y + s * a.y_src_stride + b * a.y_g_stride; the pt map is unused.
+void bsgs_tma_hoist(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st);
 // encode a 5-D uint64 tensor map (dims innermost first, dense)
 void tma_map5(CUtensorMap* map, const void* base, const uint64_t dims[5], const uint32_t box[5]);
 inline int tma_sources(int nsrc) { return nsrc >= 4 ? 4 : nsrc >= 2 ? 2 : 1; }
