@@ -29,6 +29,7 @@ struct RowMap {
     int skip_alpha;
     int skip_dn;  // digits per source when several ModUps are batched (0: one source)
     int limb;     // forward NTT: store the output rows in limb form (modarith.cuh)
+    int row0;     // NTT launches: first row of this launch (row-chunked transforms)
 };
 
 FHE_HD int row_prime(const RowMap& m, int u) { return u <= m.level ? u : m.L + (u - m.level - 1); }

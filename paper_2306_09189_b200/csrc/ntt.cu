@@ -13,6 +13,8 @@
 // registers and runs radix-8 (3-stage) passes; passes exchange data through
 // padded shared memory. Phase B gives each block of B = 2^7..2^8 words to one
 // or half a warp, so its passes only need __syncwarp.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace fhe {
@@ -79,6 +81,9 @@ __device__ __forceinline__ void tw_ld(const double2* p, double2* o, int cnt) {
 #endif
 #ifndef FHE_NTT_MINB
 #define FHE_NTT_MINB 1
+#endif
+#ifndef FHE_NTT_CHUNK
+#define FHE_NTT_CHUNK 0  // MB of rows per NTT launch pair (0: all rows in one pair)
 #endif
 constexpr int EPT = FHE_NTT_EPT;         // residues per thread in a pass
 constexpr int NTT_THREADS = FHE_NTT_THREADS;
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_cols(DevCtx c
     constexpr int PN = N1 + (N1 >> 4) + 1;  // padded column length (odd in words)
     using PP = PassPlan<LOG_N1, INVERSE>;
     __shared__ uint64_t sm[C * PN];
-    const int row = blockIdx.y;
+    const int row = blockIdx.y + rm.row0;
     const int u = row % rm.rows_per_poly;
     if (skip_row(rm, row, u)) return;
     const int p = row_prime(rm, u);
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_rows(DevCtx c
     static_assert(TPB <= 32, "a block is at most one warp");
     using PP = PassPlan<LOG_B, INVERSE>;
     __shared__ uint64_t sm[BPC * PB];
-    const int row = blockIdx.y;
+    const int row = blockIdx.y + rm.row0;
     const int u = row % rm.rows_per_poly;
     if (skip_row(rm, row, u)) return;
     const int p = row_prime(rm, u);
@@ -775,18 +780,25 @@ void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, 
     constexpr int N1 = 1 << LOG_N1, B = 1 << LOG_B;
     constexpr int C = NTT_THREADS / (N1 / EPT);
     constexpr int BPC = NTT_THREADS / (B / EPT);
-    const dim3 ga(B / C, nrows), gb((N1 + BPC - 1) / BPC, nrows);
-    if (!inverse) {
-        k_ntt_cols<LOG_N1, C, false><<<ga, NTT_THREADS, 0, st>>>(c, data, rm);
-        if (fuse == FUSE_MODDOWN)
-            k_ntt_rows<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
-        else
-            k_ntt_rows<LOG_N1, LOG_B, false, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
-    } else {
-        k_ntt_rows<LOG_N1, LOG_B, true, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rm, fz);
-        k_ntt_cols<LOG_N1, C, true><<<ga, NTT_THREADS, 0, st>>>(c, data, rm);
+    // rows in chunks whose intermediate (column pass -> row pass) stays in L2
+    const int chunk = FHE_NTT_CHUNK > 0 ? std::max(1, (int)(((size_t)FHE_NTT_CHUNK << 20) / ((size_t)c.N * 8))) : nrows;
+    for (int r0 = 0; r0 < nrows; r0 += chunk) {
+        const int nr_ = std::min(chunk, nrows - r0);
+        RowMap rc = rm;
+        rc.row0 = rm.row0 + r0;
+        const dim3 ga(B / C, nr_), gb((N1 + BPC - 1) / BPC, nr_);
+        if (!inverse) {
+            k_ntt_cols<LOG_N1, C, false><<<ga, NTT_THREADS, 0, st>>>(c, data, rc);
+            if (fuse == FUSE_MODDOWN)
+                k_ntt_rows<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gb, NTT_THREADS, 0, st>>>(c, data, rc, fz);
+            else
+                k_ntt_rows<LOG_N1, LOG_B, false, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rc, fz);
+        } else {
+            k_ntt_rows<LOG_N1, LOG_B, true, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rc, fz);
+            k_ntt_cols<LOG_N1, C, true><<<ga, NTT_THREADS, 0, st>>>(c, data, rc);
+        }
+        note_launch(2);
     }
-    note_launch(2);
 }
 
 }  // namespace
