@@ -621,7 +621,7 @@ void upload_tables(fhe_ctx* c) {
     up((void**)&c->d_itwd, itwd.data(), itwd.size() * sizeof(double2));
     up((void**)&c->d_ninvd, ninvd.data(), ninvd.size() * sizeof(double2));
     up((void**)&c->d_modup, mu.data(), mu.size() * sizeof(ModUpDigit));
-    ck(cudaMalloc(&c->d_sched, kTmaSchedWords * sizeof(unsigned)), "cudaMalloc");
+    ck(cudaMalloc(&c->d_sched, kTmaSchedSlots * kTmaSchedWords * sizeof(unsigned)), "cudaMalloc");
     up((void**)&c->d_md, &md, sizeof(md));
     up((void**)&c->d_qlinv, ql.data(), ql.size() * 8);
     up((void**)&c->d_qlinv_sh, qls.data(), qls.size() * 8);
@@ -989,7 +989,12 @@ void tma_rows(fhe_ctx* c, int level, TmaMaps& tm) {
             if ((q >= (1ULL << 50)) == (pass == 0)) tm.rowlist[n++] = (uint8_t)u;
             if (pass == 0 && u == ne - 1) tm.nint = n;
         }
-    tm.sched = c->d_sched;  // allocated with the context tables (never inside a graph capture)
+    // one work-queue slot per compute stream (main, lanes): launches on different streams
+    // may overlap; allocated with the context tables (never inside a graph capture)
+    int slot = 0;
+    for (size_t i = 0; i < c->lanes.size(); ++i)
+        if (c->st == c->lanes[i]) slot = 1 + (int)(i % (kTmaSchedSlots - 1));
+    tm.sched = c->d_sched + (size_t)slot * kTmaSchedWords;
 }
 
 // Baby steps of the fused BSGS schedule for nsrc sources: Y_g(s) for every

@@ -323,6 +323,7 @@ struct TmaMaps {
     unsigned* sched;
 };
 constexpr int kTmaSchedWords = 2 + 256;
+constexpr int kTmaSchedSlots = 16;  // per compute stream (fheconv.cu tma_rows)
 // Hoisted key switches on the same kernel (k_bsgs_tma MODE 1, no plaintexts): every
 // baby's X~_b (keyed, [P sigma(c0)] folded into poly 0) is written in the QP basis to
 // a.Y + s * a.y_src_stride + b * a.y_g_stride; the pt map is unused.

@@ -77,3 +77,37 @@ def test_fused_and_tma_kernels_identical(oracle, cfg, geo, B):
         del ctx
     for a, b in zip(res["fused"], res["tma"]):
         assert np.array_equal(a, b)
+
+
+def test_tma_on_concurrent_lanes_identical(oracle):
+    """FHECONV_BATCH5=0 runs approach 5 one ciphertext per CUDA-stream lane: several
+    k_bsgs_tma launches overlap, each with its own work-queue slot (fheconv.cu tma_rows);
+    the residues equal the batched path's."""
+    from paper_2306_09189_b200 import Context
+    rng = np.random.default_rng(9)
+    c, m, k = 16, 32, 3
+    filt = rng.uniform(-1, 1, c * c * k * k)
+    imgs = [rng.uniform(-1, 1, c * m * m) for _ in range(6)]
+    res = {}
+    for name, env in (("batched", {}), ("lanes", {"FHECONV_BATCH5": "0"})):
+        old = os.environ.get("FHECONV_BATCH5")
+        os.environ.pop("FHECONV_BATCH5", None)
+        os.environ.update(env)
+        try:
+            ctx = Context.from_config("cfg3")
+        finally:
+            if old is None:
+                os.environ.pop("FHECONV_BATCH5", None)
+            else:
+                os.environ["FHECONV_BATCH5"] = old
+        ctx.keygen(7)
+        layer = ctx.conv_layer(c, c, m, k, filt)
+        ctx.gen_galois_keys(layer.steps(5))
+        cts = [ctx.encrypt(ctx.encode(x), ENC_SEED + i) for i, x in enumerate(imgs)]
+        outs = [ctx.encrypt(ctx.encode(np.zeros(8), level=ctx.max_level - 1), 1) for _ in imgs]
+        for _ in range(2):
+            ctx.conv2d_batch_into(cts, layer, 5, outs)
+        res[name] = [o.residues() for o in outs]
+        del ctx
+    for a, b in zip(res["batched"], res["lanes"]):
+        assert np.array_equal(a, b)
