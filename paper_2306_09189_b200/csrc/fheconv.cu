@@ -285,6 +285,7 @@ struct fhe_conv_layer {
     std::vector<int64_t> tau;
     std::vector<uint8_t> ms_nonempty;  // [n_out][kappa][nb_ms]
     uint64_t* d_pts_ms = nullptr;
+    uint64_t* d_pts_ms_opf = nullptr;  // operand form, padded by two giants (k_bsgs_tma boxes)
     // bias (ImageConv::bias_plain conv.cpp:87-94, conv_channel_shards :344): one
     // slot vector per output shard (bias[out_channel] * output_scale per block),
     // encoded lazily at level - 1 and the input scale, added in the epilogue of
@@ -1698,8 +1699,36 @@ void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
     uint64_t* buf = c->alloc((size_t)B * T * ctw);
     for (int i = 0; i < B * T; ++i)
         ck(cudaMemcpyAsync(buf + (size_t)i * ctw, in[i]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    // operand-form rows on k_bsgs_tma (keys from the arena, plaintexts from the layer's
+    // operand-form copy, digits / [P c] of input shard u through the slot coordinate)
+    const bool opf = c->limb && c->tma;
+    TmaMaps tm{};
+    if (opf && !ly->d_pts_ms_opf) {
+        fhe_conv_layer* L = const_cast<fhe_conv_layer*>(ly);
+        const size_t rows = (size_t)NO * kap * nb * ne, prow = (size_t)(NO * kap + 2) * nb * ne;
+        ck(cudaMalloc(&L->d_pts_ms_opf, prow * N * 8), "cudaMalloc");
+        ck(cudaMemsetAsync(L->d_pts_ms_opf + rows * N, 0, (prow - rows) * N * 8, c->st), "memset");
+        rows_to_limb(c->dc, L->d_pts_ms_opf, ly->d_pts_ms, rows, RowMap{ne, level, c->L, 0}, c->st);
+    }
     uint64_t* dig = c->alloc((size_t)B * T * dw);
-    modup_batch(c, buf + (size_t)nr * N, ctw, B * T, level, dig);
+    modup_batch(c, buf + (size_t)nr * N, ctw, B * T, level, dig, opf ? 1 : 0);
+    if (opf) {
+        ct_prescale(c->dc, buf, buf, ctw, B * T, c->d_md, level, c->st);
+        tma_rows(c, level, tm);
+        const uint32_t sg = (uint32_t)tma_sources(B), P2 = 256u / sg;
+        const uint64_t dk[4] = {N, (uint64_t)c->np, 2ull * c->dnum, (uint64_t)std::max(1, c->arena_n)};
+        const uint32_t bk[4] = {P2, 1, 2u * dn, 1};
+        tma_map4(&tm.key, c->d_key_arena, dk, bk);
+        const uint64_t dp[4] = {N, (uint64_t)ne, (uint64_t)nb, (uint64_t)(NO * kap + 2)};
+        const uint32_t bp[4] = {P2, 1, 1, 3};
+        tma_map4(&tm.pt, ly->d_pts_ms_opf, dp, bp);
+        const uint64_t dd[5] = {N, (uint64_t)ne, (uint64_t)dn, (uint64_t)T, (uint64_t)B};
+        const uint32_t bd[5] = {P2, 1, (uint32_t)dn, 1, sg};
+        tma_map5(&tm.dig, dig, dd, bd);
+        const uint64_t dc5[5] = {N, (uint64_t)nr, 2, (uint64_t)T, (uint64_t)B};
+        const uint32_t bc[5] = {P2, 1, 2, 1, sg};
+        tma_map5(&tm.ct, buf, dc5, bc);
+    }
     const size_t ys = (size_t)kap * 2 * extw;
     uint64_t* Y = c->alloc((size_t)B * NO * ys);  // [B][n_out][kappa][2][ne][N]
     ck(cudaMemsetAsync(Y, 0, (size_t)B * NO * ys * 8, c->st), "memset");
@@ -1720,16 +1749,25 @@ void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
             f.y_src_stride = (size_t)NO * ys;
             f.y_g_stride = 2 * extw;
             f.accumulate = 1;
+            int launches = 0;
+            tm.g0 = v * kap + g0;
             double keyed = 0, pts = 0;
             auto flush = [&] {
                 if (!f.nb) return;
                 for (int q = 0; q < f.nb; ++q)
-                    if (f.key[q]) c->ledger.hoisted_rotations += (uint64_t)B;
+                    if (f.galois[q] != 1) c->ledger.hoisted_rotations += (uint64_t)B;
                 c->ledger.ct_pt_mults += (uint64_t)B * (uint64_t)pts;
                 c->ledger.adds += (uint64_t)B * (uint64_t)pts;
+                if (opf) f.accumulate = launches > 0;
                 c->timed("bsgs_fused",
                          c->rows(keyed * 2.0 * dn * ne + pts * ne + B * (T * (double)dn * ne + 2.0 * nr + 4.0 * ng * ne)),
-                         [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+                         [&] {
+                             if (opf)
+                                 bsgs_tma(c->dc, f, tm, level, dn, c->st);
+                             else
+                                 bsgs_fused(c->dc, f, c->d_md, level, dn, c->st);
+                         });
+                launches++;
                 f.nb = 0;
                 keyed = pts = 0;
             };
@@ -1744,6 +1782,8 @@ void conv_ms_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
                 const uint32_t gal = c->galois_of(c->reduce_amount((int64_t)r * ly->rep * block + ll));
                 f.galois[f.nb] = gal;
                 f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+                tm.kidx[f.nb] = (int16_t)(gal == 1 ? -1 : c->key_slot.at(gal));
+                tm.bidx[f.nb] = (int16_t)b;
                 f.gmask[f.nb] = mask;
                 f.pt[f.nb] = ly->d_pts_ms + (((size_t)v * kap + g0) * nb + b) * extw;
                 f.srcslot[f.nb] = (uint16_t)u;
@@ -3162,6 +3202,7 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
     }
     cudaFree(ly->d_pts);
     if (ly->d_pts_ms) cudaFree(ly->d_pts_ms);
+    if (ly->d_pts_ms_opf) cudaFree(ly->d_pts_ms_opf);
     if (ly->d_bias) cudaFree(ly->d_bias);
     for (auto& b : ly->bs) {
         if (b.d_pts) cudaFree(b.d_pts);
