@@ -1338,9 +1338,8 @@ void giants_finish(fhe_ctx* c, const uint64_t* Y, size_t ys, int S, int level, c
         c->release(yq);
         c->release(yc);
     }
-    for (int g : idg)
-        for (int s = 0; s < S; ++s)
-            qp_add(c->dc, acc + (size_t)s * 2 * extw, Y + (size_t)s * ys + (size_t)g * 2 * extw, level, c->st);
+    for (int g : idg)  // one launch per identity giant for all S accumulators
+        qp_add(c->dc, acc, Y + (size_t)g * 2 * extw, level, c->st, S, 2 * extw, ys);
     moddown_rescale(c, acc, extw, level, 2 * S, md, bias, bias_mod);
     c->release(acc);
 }

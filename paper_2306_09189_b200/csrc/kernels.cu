@@ -1867,13 +1867,16 @@ __global__ void __launch_bounds__(128, 4) k_ks_hoist_opf(DevCtx c, KsBatch a, in
     }
 }
 
-__global__ void k_qp_add(DevCtx c, uint64_t* acc, const uint64_t* y, int level) {
+// acc(s) += y(s) for S QP ciphertexts [2][ne][N] at acc + s * as, y + s * ys
+__global__ void k_qp_add(DevCtx c, uint64_t* acc, size_t as, const uint64_t* y, size_t ys, int S, int level) {
     const int ne = level + 1 + c.K;
-    const size_t total = (size_t)2 * ne * c.N;
+    const size_t per = (size_t)2 * ne * c.N, total = per * S;
     RowMap rm{ne, level, c.L, 0};
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        const int u = (int)((i >> c.logN) % ne);
-        acc[i] = add_mod(acc[i], y[i], c.primes[row_prime(rm, u)].q);
+        const size_t s = i / per, w = i - s * per;
+        const int u = (int)((w >> c.logN) % ne);
+        uint64_t* a = acc + s * as + w;
+        *a = add_mod(*a, y[s * ys + w], c.primes[row_prime(rm, u)].q);
     }
 }
 
@@ -2232,10 +2235,11 @@ void ct_prescale(const DevCtx& c, uint64_t* dst, const uint64_t* ct, size_t stri
                                                                                         md, level);
 }
 
-void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st) {
-    const size_t total = (size_t)2 * (level + 1 + c.K) * c.N;
+void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st, int S, size_t as,
+            size_t ys) {
+    const size_t total = (size_t)2 * (level + 1 + c.K) * c.N * S;
     ++g_launches;
-    k_qp_add<<<ew_blocks(total), kEwThreads, 0, st>>>(c, acc, y, level);
+    k_qp_add<<<ew_blocks(total), kEwThreads, 0, st>>>(c, acc, as, y, ys, S, level);
 }
 
 uint64_t launches_total() { return g_launches; }

@@ -350,6 +350,7 @@ void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nr
 void ct_prescale(const DevCtx& c, uint64_t* dst, const uint64_t* ct, size_t stride, int nsrc, const ModDownTable* md,
                  int level, cudaStream_t st);
 // acc += y over [2][ne][N] (QP basis)
-void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st);
+void qp_add(const DevCtx& c, uint64_t* acc, const uint64_t* y, int level, cudaStream_t st, int S = 1, size_t as = 0,
+            size_t ys = 0);
 
 }  // namespace fhe
