@@ -286,6 +286,7 @@ struct fhe_conv_layer {
     std::vector<uint8_t> ms_nonempty;  // [n_out][kappa][nb_ms]
     uint64_t* d_pts_ms = nullptr;
     uint64_t* d_pts_ms_opf = nullptr;  // operand form, padded by two giants (k_bsgs_tma boxes)
+    uint64_t* d_pts_cs_opf = nullptr;  // channel-shard plaintexts in operand form, padded likewise
     // bias (ImageConv::bias_plain conv.cpp:87-94, conv_channel_shards :344): one
     // slot vector per output shard (bias[out_channel] * output_scale per block),
     // encoded lazily at level - 1 and the input scale, added in the epilogue of
@@ -1839,8 +1840,37 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
     uint64_t* buf = c->alloc((size_t)B * NSH * ctw);
     for (int i = 0; i < B * NSH; ++i)
         ck(cudaMemcpyAsync(buf + (size_t)i * ctw, in[i]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st), "memcpy");
+    // operand-form rows on k_bsgs_tma: plaintext map (N, ne, 2 kappa [ll, spill], CO C kappa
+    // [(g, f), kk]), the giant base (g, f) per baby (TmaMaps.gidx), input shards by slot
+    const bool opf = c->limb && c->tma;
+    TmaMaps tm{};
+    const int GD = CO * C_ * kap;  // giant coordinate extent
+    if (opf && !ly->d_pts_cs_opf) {
+        fhe_conv_layer* Lm = const_cast<fhe_conv_layer*>(ly);
+        const size_t rows = (size_t)GD * 2 * kap * ne, prow = (size_t)(GD + 2) * 2 * kap * ne;
+        ck(cudaMalloc(&Lm->d_pts_cs_opf, prow * N * 8), "cudaMalloc");
+        ck(cudaMemsetAsync(Lm->d_pts_cs_opf + rows * N, 0, (prow - rows) * N * 8, c->st), "memset");
+        rows_to_limb(c->dc, Lm->d_pts_cs_opf, ly->d_pts_ms, rows, RowMap{ne, level, c->L, 0}, c->st);
+    }
     uint64_t* dig = c->alloc((size_t)B * NSH * dw);
-    modup_batch(c, buf + (size_t)nr * N, ctw, B * NSH, level, dig);
+    modup_batch(c, buf + (size_t)nr * N, ctw, B * NSH, level, dig, opf ? 1 : 0);
+    if (opf) {
+        ct_prescale(c->dc, buf, buf, ctw, B * NSH, c->d_md, level, c->st);
+        tma_rows(c, level, tm);
+        const uint32_t sg = (uint32_t)tma_sources(B), P2 = 256u / sg;
+        const uint64_t dk[4] = {N, (uint64_t)c->np, 2ull * c->dnum, (uint64_t)std::max(1, c->arena_n)};
+        const uint32_t bk[4] = {P2, 1, 2u * dn, 1};
+        tma_map4(&tm.key, c->d_key_arena, dk, bk);
+        const uint64_t dp[4] = {N, (uint64_t)ne, (uint64_t)(2 * kap), (uint64_t)(GD + 2)};
+        const uint32_t bp[4] = {P2, 1, 1, 3};
+        tma_map4(&tm.pt, ly->d_pts_cs_opf, dp, bp);
+        const uint64_t dd[5] = {N, (uint64_t)ne, (uint64_t)dn, (uint64_t)NSH, (uint64_t)B};
+        const uint32_t bd[5] = {P2, 1, (uint32_t)dn, 1, sg};
+        tma_map5(&tm.dig, dig, dd, bd);
+        const uint64_t dc5[5] = {N, (uint64_t)nr, 2, (uint64_t)NSH, (uint64_t)B};
+        const uint32_t bc[5] = {P2, 1, 2, 1, sg};
+        tma_map5(&tm.ct, buf, dc5, bc);
+    }
     const size_t ys = (size_t)kap * 2 * extw;
     uint64_t* Y = c->alloc((size_t)B * NOUT * ys);  // [B][c_out][pc][kappa][2][ne][N]
     ck(cudaMemsetAsync(Y, 0, (size_t)B * NOUT * ys * 8, c->st), "memset");
@@ -1865,16 +1895,25 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
                 f.y_src_stride = (size_t)NOUT * ys;
                 f.y_g_stride = 2 * extw;
                 f.accumulate = 1;
+                int launches = 0;
+                tm.g0 = g0;
                 double keyed = 0, pts = 0;
                 auto flush = [&] {  // more babies than one launch holds: continue the accumulators
                     if (!f.nb) return;
                     c->ledger.hoisted_rotations += (uint64_t)B * (uint64_t)keyed;
                     c->ledger.ct_pt_mults += (uint64_t)B * (uint64_t)pts;
                     c->ledger.adds += (uint64_t)B * (uint64_t)pts;
+                    if (opf) f.accumulate = launches > 0;
                     c->timed("bsgs_fused",
                              c->rows(keyed * 2.0 * dn * ne + pts * ne +
                                      B * (3.0 * C_ * dn * ne + 2.0 * nr + 4.0 * ng * ne)),
-                             [&] { bsgs_fused(c->dc, f, c->d_md, level, dn, c->st); });
+                             [&] {
+                                 if (opf)
+                                     bsgs_tma(c->dc, f, tm, level, dn, c->st);
+                                 else
+                                     bsgs_fused(c->dc, f, c->d_md, level, dn, c->st);
+                             });
+                    launches++;
                     f.nb = 0;
                     keyed = pts = 0;
                 };
@@ -1895,6 +1934,9 @@ void conv_cs_batch(fhe_ctx* c, const fhe_ct* const* in, int B, const fhe_conv_la
                             const uint32_t gal = c->galois_of(c->reduce_amount(lo - h));
                             f.galois[f.nb] = gal;
                             f.key[f.nb] = gal == 1 ? nullptr : c->key_for(gal);
+                            tm.kidx[f.nb] = (int16_t)(gal == 1 ? -1 : c->key_slot.at(gal));
+                            tm.bidx[f.nb] = (int16_t)(2 * lo + spill);
+                            tm.gidx[f.nb] = (int16_t)((g * C_ + fi) * kap);
                             f.gmask[f.nb] = mask;
                             f.pt[f.nb] = ly->d_pts_ms + pt_of(g, fi, g0, lo, spill) * extw;
                             f.srcslot[f.nb] = (uint16_t)(fi * PC + src);
@@ -3202,6 +3244,7 @@ void fhe_conv_layer_free(fhe_conv_layer* ly) {
     cudaFree(ly->d_pts);
     if (ly->d_pts_ms) cudaFree(ly->d_pts_ms);
     if (ly->d_pts_ms_opf) cudaFree(ly->d_pts_ms_opf);
+    if (ly->d_pts_cs_opf) cudaFree(ly->d_pts_cs_opf);
     if (ly->d_bias) cudaFree(ly->d_bias);
     for (auto& b : ly->bs) {
         if (b.d_pts) cudaFree(b.d_pts);

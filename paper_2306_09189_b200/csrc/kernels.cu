@@ -1086,7 +1086,7 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
             const int blk = (int)(pidx(e0, a.galois[b]) & ~(uint32_t)(BW - 1));
             mbar_expect_tx(bar, (uint32_t)((MODE == 0 ? LY::PW : 0) + LY::CW + (keyed ? LY::KW + LY::DW : 0)) * 16u);
             const int sl5 = a.srcslot[b];  // source slot (paper schedules: the rotated copy)
-            if (MODE == 0) tma_load4(sb + LY::KW, &m.pt, (int)k0, u, m.bidx[b], m.g0, bar);
+            if (MODE == 0) tma_load4(sb + LY::KW, &m.pt, (int)k0, u, m.bidx[b], m.g0 + m.gidx[b], bar);
             tma_load5(sb + LY::KW + LY::PW + LY::DW, &m.ct, blk, qrow ? u : 0, 0, sl5, s0c, bar);
             if (keyed) {
                 tma_load4(sb, &m.key, (int)k0, pi, 0, m.kidx[b], bar);

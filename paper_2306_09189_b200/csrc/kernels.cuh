@@ -313,6 +313,7 @@ struct TmaMaps {
     CUtensorMap key, pt, dig, ct;  // dig / ct: 5-D, dimension 3 = source slot (FusedBsgs.srcslot)
     int16_t kidx[kMaxFused];  // baby b's key in the key map, -1: identity
     int16_t bidx[kMaxFused];  // baby b's index in the plaintext map
+    int16_t gidx[kMaxFused];  // baby b's giant-coordinate offset (added to g0; 0 unless set)
     int g0;                   // first giant of the launch
     int ng1;                  // the plaintext box spans one giant (paper schedules: ng == 1)
     // work queues (k_bsgs_tma): extended rows in queue order, the nint integer-path
