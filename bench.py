@@ -130,7 +130,7 @@ def measured_peak():
 
 # committed ncu --set full capture of the dominant kernel at the step's batch (same build);
 # written by tools/ncu_fused.sh + tools/ncu_summary.py and copied under profiles/
-NCU_DOMINANT = os.path.join("profiles", "ncu_r02_bsgs_fp64_b16_summary.txt")
+NCU_DOMINANT = os.path.join("profiles", "ncu_r02_bsgs_grid_b16_summary.txt")
 
 
 def ncu_capture(path=NCU_DOMINANT):
@@ -139,9 +139,12 @@ def ncu_capture(path=NCU_DOMINANT):
             "dram__bytes_write.sum": "dram_write", "sm__inst_issued.avg.pct_of_peak_sustained_active": "issue_pct",
             "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed": "fmaheavy_pct",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pct",
-            "smsp__inst_executed.sum": "warp_instructions"}
+            "smsp__inst_executed.sum": "warp_instructions",
+            "l1tex__m_xbar2l1tex_read_bytes.sum": "l2_to_sm_bytes",
+            "l1tex__m_xbar2l1tex_read_bytes.sum.per_second": "l2_to_sm_rate",
+            "sm__warps_active.avg.per_cycle_active": "warps_per_sm"}
     scale = {"ms": 1.0, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3,
-             "byte": 1.0, "%": 1.0, "inst": 1.0}
+             "byte": 1.0, "%": 1.0, "inst": 1.0, "Tbyte/s": 1e12, "Gbyte/s": 1e9, "warp": 1.0}
     out = {"source": path}
     try:
         for line in open(os.path.join(ROOT, path)):
@@ -453,8 +456,7 @@ def roofline_timed(prof_b, kbp, B, peak, peak_kind, step_s, level):
     intermediates): the fused baby-step launch touches the 47 keyed baby-step keys of the schedule
     (r m^2 + ll), its 144 rotated plaintexts and the B input ciphertexts. `traffic` and the
     pipe figures come from the committed ncu capture of the same kernel at the same batch
-    (profiles/, NCU_DOMINANT); the batched kernel is bound by its FP64 (rows q < 2^50) and integer
-    (60-bit rows) multiply pipes, not by HBM."""
+    (profiles/, NCU_DOMINANT); the batched kernel is not HBM-bound (see the note it returns)."""
     tot = sum(v[0] for v in prof_b.values())
     if not tot:
         return None
@@ -478,14 +480,20 @@ def roofline_timed(prof_b, kbp, B, peak, peak_kind, step_s, level):
             "pipes": {"issue_frac": round(ncu["issue_pct"] / 100, 3) if "issue_pct" in ncu else None,
                       "fp64_frac": round(ncu["fp64_pct"] / 100, 3) if "fp64_pct" in ncu else None,
                          "fmaheavy_frac": round(ncu["fmaheavy_pct"] / 100, 3) if "fmaheavy_pct" in ncu else None,
+                         "l2_to_sm_bytes_per_launch": ncu.get("l2_to_sm_bytes"),
+                         "l2_to_sm_gbs": round(ncu["l2_to_sm_rate"] / 1e9, 1) if "l2_to_sm_rate" in ncu else None,
+                         "warps_per_sm": ncu.get("warps_per_sm"),
                          "ncu_duration_ms": ncu.get("duration_ms"), "ncu_kernel": ncu.get("kernel"),
                          "source": ncu.get("source")},
             "measured_on": f"{kbp} batched steps of {B} ciphertexts (graphs off, CUDA events per launch) right "
                            "after the timed region",
-            "note": "batched, every key and plaintext byte is shared by the B ciphertexts: the kernel is bound "
-                    "by its multiply pipes (FP64 for the rows q < 2^50, IMAD for the 60-bit rows; `pipes`), so the "
-                    "HBM fraction is low by construction; "
-                    "roofline_single_ct is the HBM-bound latency regime"}
+            "note": "batched, every key and plaintext byte is shared by the B ciphertexts, so the HBM fraction is "
+                    "low by construction. The launch pulls 39 GB of operands from L2 at 9.4 TB/s and keeps the "
+                    "FP64 pipe 48 % busy at 16 warps/SM (128 registers); A/B on the B200 "
+                    "(profiles/ab_r02_bsgs_variants.txt): 13 % fewer FP64 instructions -> -2.8 % time, 16 % "
+                    "fewer L2 bytes -> +-0, a deeper TMA ring at 12 warps/SM -> +7 % time: it is bound by "
+                    "latency hiding at that occupancy, not by a pipe or a memory level; "
+                    "roofline_single_ct is the HBM-bound latency regime (one ciphertext per launch)"}
 
 
 def other_configs(world, device):

@@ -12,6 +12,12 @@
 
 // k_bsgs_tma FP64 rows: read a digit pair with one 16-byte shared load and swap in
 // registers (1), or as two 8-byte loads in output order (0)
+#ifndef FHE_TMA_NOSYNC
+// k_bsgs_tma with 1: stages refilled by the last warp to leave them, no CTA barrier per baby step.
+// Off: cfg3 batch 16 loses 7 % (2132 -> 1985 conv/s, profiles/ab_r02_bsgs_variants.txt) -- warps
+// that drift apart contend for shared memory instead of overlapping their phases.
+#define FHE_TMA_NOSYNC 0
+#endif
 #ifndef FHE_DIG128
 #define FHE_DIG128 0
 #endif
@@ -1009,13 +1015,13 @@ struct TmaLayout {  // one stage, in 16-byte pair slots
 // MODE 1 (hoisted key switches, no plaintexts): every baby's X~_b is written to
 // Y + s * y_src_stride + b * y_g_stride ([2][ne][N], QP, canonical) instead of being
 // multiplied into giant accumulators.
-template <int DN, int NG, int SG, int MINB, int MODE = 0>
+template <int DN, int NG, int SG, int MINB, int MODE = 0, int NST = 2>
 __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, const __grid_constant__ TmaMaps m,
                                                         int level) {
     using LY = TmaLayout<DN, NG, SG>;
     constexpr int P = LY::P, BW = 2 * P;
-    extern __shared__ __align__(1024) ulonglong2 tsb[];  // [2][STAGE], then 2 mbarriers
-    uint64_t* const bars = reinterpret_cast<uint64_t*>(tsb + 2 * LY::STAGE);
+    extern __shared__ __align__(1024) ulonglong2 tsb[];  // [NST][STAGE], then NST mbarriers
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(tsb + NST * LY::STAGE);
     const int nr = level + 1, ne = nr + c.K;
     const int tid = threadIdx.x, p = tid % P, sl = tid / P;
     const size_t total = (size_t)ne * c.N;
@@ -1030,11 +1036,15 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
     // runs integer-multiply and FP64 work side by side; a CTA whose queue is empty
     // helps with the other one. Items: group fastest, then chunk, then row.
     __shared__ int s_item[2];
+    __shared__ unsigned s_cnt[NST];  // warps done with stage st (FHE_TMA_NOSYNC)
     const size_t cpr = (size_t)c.N / BW;  // chunks per row
     const size_t nq[2] = {(size_t)m.nint * cpr * ngroups, (size_t)(ne - m.nint) * cpr * ngroups};
     if (tid == 0) {
-        mbar_init(bars, 1);
-        mbar_init(bars + 1, 1);
+#pragma unroll
+        for (int st = 0; st < NST; ++st) {
+            mbar_init(bars + st, 1);
+            s_cnt[st] = 0;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1078,8 +1088,8 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
         const bool qrow = u < nr;
         const uint32_t e = 2 * brev_n(k, c.logN) + 1, e0 = 2 * brev_n(k0, c.logN) + 1;
         auto pidx = [&](uint32_t ee, uint32_t g) { return brev_n((((ee * g) & nmask) - 1) >> 1, c.logN); };
-        auto issue = [&](int b, int st) {
-            if (tid != 0 || b >= a.nb) return;
+        auto issue_one = [&](int b, int st) {  // the calling thread fetches baby b into stage st
+            if (b >= a.nb) return;
             ulonglong2* sb = tsb + st * LY::STAGE;
             uint64_t* bar = bars + st;
             const bool keyed = m.kidx[b] >= 0;
@@ -1093,10 +1103,33 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                 tma_load5(sb + LY::KW + LY::PW, &m.dig, blk, u, 0, sl5, s0c, bar);
             }
         };
+        auto issue = [&](int b, int st) {
+            if (tid == 0) issue_one(b, st);
+        };
+        // A warp is done with stage st of baby b. FHE_TMA_NOSYNC: no CTA barrier per baby
+        // step -- the last of the CTA's four warps to get here refills the stage (a counter
+        // in shared memory elects it), so warps drift apart by up to a baby step and their
+        // shared-memory, FP64 and integer phases overlap. Otherwise: barrier, thread 0 refills.
+        auto release = [&](int b, int st) {
+#if FHE_TMA_NOSYNC
+            __syncwarp();
+            if ((tid & 31) == 0) {
+                __threadfence_block();
+                if (atomicAdd(&s_cnt[st], 1u) == 3u) {
+                    atomicExch(&s_cnt[st], 0u);
+                    issue_one(b + NST, st);
+                }
+            }
+#else
+            __syncthreads();  // stage st is free: fetch baby b + NST into it
+            issue(b + NST, st);
+#endif
+        };
         // q < 2^50: FP64 operand form (modarith.cuh): every product is one fmac_d on the
         // FP64 pipe, the sums stay exact integers below 2^53
         auto run_fp = [&]() {
             const ArD ad = make_ard(pr.q);
+            const ArG ag = make_arg(ad);
             double y[NG][2][2];
 #pragma unroll
             for (int g = 0; g < NG; ++g)
@@ -1106,6 +1139,7 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                     for (int e2 = 0; e2 < 2; ++e2) y[g][q2][e2] = 0.0;
             issue(0, 0);
             issue(1, 1);
+            if (NST > 2) issue(2, 2);
             auto baby = [&](int b, int st) {
                 mbar_wait(bars + st, (phase >> st) & 1u);
                 phase ^= 1u << st;
@@ -1117,10 +1151,12 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                 if (m.kidx[b] >= 0) {
                     const double* sd = reinterpret_cast<const double*>(sb + LY::KW + LY::PW + slot * DN * P);
                     const double2* sk = reinterpret_cast<const double2*>(sb);
-                    double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                    // key inner product on the 2^50 grid (fmag_d: one quotient per sum)
+                    double z[2][2] = {{kGridBig, kGridBig}, {kGridBig, kGridBig}};
+                    double zl[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
                     if (qrow) {  // + [P sigma(c0)]_q
-                        z[0][0] = sc[wo];
-                        z[0][1] = sc[wo ^ 1];
+                        zl[0][0] = sc[wo];
+                        zl[0][1] = sc[wo ^ 1];
                     }
 #pragma unroll
                     for (int j = 0; j < DN; ++j) {
@@ -1132,15 +1168,15 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
 #else
                         const double d0 = sd[j * BW + wo], d1 = sd[j * BW + (wo ^ 1)];
 #endif
-                        fmac_d(z[0][0], d0, k0.x, ad);
-                        fmac_d(z[0][1], d1, k0.y, ad);
-                        fmac_d(z[1][0], d0, k1.x, ad);
-                        fmac_d(z[1][1], d1, k1.y, ad);
+                        fmag_d(z[0][0], zl[0][0], d0, k0.x);
+                        fmag_d(z[0][1], zl[0][1], d1, k0.y);
+                        fmag_d(z[1][0], zl[1][0], d0, k1.x);
+                        fmag_d(z[1][1], zl[1][1], d1, k1.y);
                     }
 #pragma unroll
                     for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) x[q2][e2] = red_d(z[q2][e2], ad);
+                        for (int e2 = 0; e2 < 2; ++e2) x[q2][e2] = fold_d(z[q2][e2], zl[q2][e2], ad, ag);
                 } else if (qrow) {  // identity: X = [P c]_q, unpermuted
                     x[0][0] = sc[2 * p];
                     x[0][1] = sc[2 * p + 1];
@@ -1155,8 +1191,7 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                         st2(yb + i, canon_d(x[0][0], ad), canon_d(x[0][1], ad));
                         st2(yb + total + i, canon_d(x[1][0], ad), canon_d(x[1][1], ad));
                     }
-                    __syncthreads();  // stage st is free: fetch baby b + 2 into it
-                    issue(b + 2, st);
+                    release(b, st);
                     return;
                 }
                 const uint32_t gm = a.gmask[b];
@@ -1179,12 +1214,12 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
 #pragma unroll
                             for (int e2 = 0; e2 < 2; ++e2) y[g][q2][e2] = red_d(y[g][q2][e2], ad);
                 }
-                __syncthreads();  // stage st is free: fetch baby b + 2 into it
-                issue(b + 2, st);
+                release(b, st);
             };
-            for (int b = 0; b < a.nb; b += 2) {
+            for (int b = 0; b < a.nb; b += NST) {
                 baby(b, 0);
                 if (b + 1 < a.nb) baby(b + 1, 1);
+                if (NST > 2 && b + 2 < a.nb) baby(b + 2, 2);
             }
             if (MODE == 0 && active) {
                 uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
@@ -1224,6 +1259,7 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                     for (int e2 = 0; e2 < 2; ++e2) y[g][q2][e2] = U128{0, 0};
             issue(0, 0);
             issue(1, 1);
+            if (NST > 2) issue(2, 2);
             auto baby = [&](int b, int st) {
                 mbar_wait(bars + st, (phase >> st) & 1u);
                 phase ^= 1u << st;
@@ -1293,8 +1329,7 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                         st2(yb + i, mul_mod(x[0][0], r90, pr), mul_mod(x[0][1], r90, pr));
                         st2(yb + total + i, mul_mod(x[1][0], r90, pr), mul_mod(x[1][1], r90, pr));
                     }
-                    __syncthreads();
-                    issue(b + 2, st);
+                    release(b, st);
                     return;
                 }
                 const uint32_t gm = a.gmask[b];
@@ -1317,12 +1352,12 @@ __global__ void __launch_bounds__(128, MINB) k_bsgs_tma(DevCtx c, FusedBsgs a, c
                             for (int e2 = 0; e2 < 2; ++e2)
                                 y[g][q2][e2] = U128{reduce128(y[g][q2][e2].hi, y[g][q2][e2].lo, pr), 0};
                 }
-                __syncthreads();  // stage st is free: fetch baby b + 2 into it
-                issue(b + 2, st);
+                release(b, st);
             };
-            for (int b = 0; b < a.nb; b += 2) {
+            for (int b = 0; b < a.nb; b += NST) {
                 baby(b, 0);
                 if (b + 1 < a.nb) baby(b + 1, 1);
+                if (NST > 2 && b + 2 < a.nb) baby(b + 2, 2);
             }
             if (MODE == 0 && active) {
                 uint64_t* Ys = a.Y + (size_t)s * a.y_src_stride;
@@ -1539,6 +1574,7 @@ __global__ void __launch_bounds__(128, 4) k_ks_giant_opf(DevCtx c, KsBatch a, in
         const Prime pr = c.primes[pi];
         const bool fp = opf_fp(pr.q);
         const ArD ad = make_ard(pr.q);
+        const ArG ag = fp ? make_arg(ad) : ArG{0.0, 0.0};
         const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> 30), qinv = (uint32_t)pr.qinv & MW;
         double zf[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
         uint64_t zi[2][2] = {{0, 0}, {0, 0}};  // 60-bit rows: sum of the terms' X 2^-90, reduced
@@ -1552,21 +1588,22 @@ __global__ void __launch_bounds__(128, 4) k_ks_giant_opf(DevCtx c, KsBatch a, in
             const ulonglong2 cv = s_c0[so];
             const uint64_t ca = swp ? cv.y : cv.x, cb = swp ? cv.x : cv.y;
             if (fp) {
-                double z[2][2] = {{zf[0][0] + asd(ca), zf[0][1] + asd(cb)}, {zf[1][0], zf[1][1]}};
+                double z[2][2] = {{kGridBig, kGridBig}, {kGridBig, kGridBig}};
+                double zl[2][2] = {{zf[0][0] + asd(ca), zf[0][1] + asd(cb)}, {zf[1][0], zf[1][1]}};
 #pragma unroll
                 for (int j = 0; j < DN; ++j) {
                     const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
                     const ulonglong2 dv = s_dig[so + j * P];
                     const double da = asd(swp ? dv.y : dv.x), db = asd(swp ? dv.x : dv.y);
-                    fmac_d(z[0][0], da, asd(k0.x), ad);
-                    fmac_d(z[0][1], db, asd(k0.y), ad);
-                    fmac_d(z[1][0], da, asd(k1.x), ad);
-                    fmac_d(z[1][1], db, asd(k1.y), ad);
+                    fmag_d(z[0][0], zl[0][0], da, asd(k0.x));
+                    fmag_d(z[0][1], zl[0][1], db, asd(k0.y));
+                    fmag_d(z[1][0], zl[1][0], da, asd(k1.x));
+                    fmag_d(z[1][1], zl[1][1], db, asd(k1.y));
                 }
 #pragma unroll
                 for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) zf[q2][e2] = red_d(z[q2][e2], ad);
+                    for (int e2 = 0; e2 < 2; ++e2) zf[q2][e2] = fold_d(z[q2][e2], zl[q2][e2], ad, ag);
             } else {
                 uint64_t z0[2][2] = {{0, 0}, {0, 0}}, z1[2][2] = {{0, 0}, {0, 0}}, z2[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
@@ -1776,6 +1813,7 @@ __global__ void __launch_bounds__(128, 4) k_ks_hoist_opf(DevCtx c, KsBatch a, in
         const Prime pr = c.primes[pi];
         const bool fp = opf_fp(pr.q);
         const ArD ad = make_ard(pr.q);
+        const ArG ag = fp ? make_arg(ad) : ArG{0.0, 0.0};
         constexpr uint32_t MW = (1u << 30) - 1;
         const uint32_t q0 = (uint32_t)(pr.q & MW), q1 = (uint32_t)(pr.q >> 30), qinv = (uint32_t)pr.qinv & MW;
         uint64_t r90 = 0;
@@ -1792,26 +1830,27 @@ __global__ void __launch_bounds__(128, 4) k_ks_hoist_opf(DevCtx c, KsBatch a, in
             const int swp = (int)(pidx(a.galois[t]) & 1u);
             uint64_t o[2][2];
             if (fp) {
-                double z[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                double z[2][2] = {{kGridBig, kGridBig}, {kGridBig, kGridBig}};
+                double zl[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
                 if (qrow) {
                     const ulonglong2 cv = s_c0[so];
-                    z[0][0] = asd(swp ? cv.y : cv.x);
-                    z[0][1] = asd(swp ? cv.x : cv.y);
+                    zl[0][0] = asd(swp ? cv.y : cv.x);
+                    zl[0][1] = asd(swp ? cv.x : cv.y);
                 }
 #pragma unroll
                 for (int j = 0; j < DN; ++j) {
                     const ulonglong2 k0 = s_key[so + (2 * j) * P], k1 = s_key[so + (2 * j + 1) * P];
                     const ulonglong2 dv = s_dig[so + j * P];
                     const double da = asd(swp ? dv.y : dv.x), db = asd(swp ? dv.x : dv.y);
-                    fmac_d(z[0][0], da, asd(k0.x), ad);
-                    fmac_d(z[0][1], db, asd(k0.y), ad);
-                    fmac_d(z[1][0], da, asd(k1.x), ad);
-                    fmac_d(z[1][1], db, asd(k1.y), ad);
+                    fmag_d(z[0][0], zl[0][0], da, asd(k0.x));
+                    fmag_d(z[0][1], zl[0][1], db, asd(k0.y));
+                    fmag_d(z[1][0], zl[1][0], da, asd(k1.x));
+                    fmag_d(z[1][1], zl[1][1], db, asd(k1.y));
                 }
 #pragma unroll
                 for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) o[q2][e2] = canon_d(red_d(z[q2][e2], ad), ad);
+                    for (int e2 = 0; e2 < 2; ++e2) o[q2][e2] = canon_d(fold_d(z[q2][e2], zl[q2][e2], ad, ag), ad);
             } else {
                 uint64_t z0[2][2] = {{0, 0}, {0, 0}}, z1[2][2] = {{0, 0}, {0, 0}}, z2[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
@@ -2120,19 +2159,34 @@ void bsgs_fused(const DevCtx& c, const FusedBsgs& a, const ModDownTable* md, int
 #ifndef FHE_TMA_MINB
 #define FHE_TMA_MINB 4
 #endif
-template <int DN, int NG, int SG, int MINB, int MODE = 0>
+// Ring depth of the SG >= 8 launches (-DFHE_TMA_WIDE=1 builds). 3 stages fit 3 CTAs per SM and
+// lose 7 % against 2 stages at 4 CTAs per SM: the kernel needs its 16 warps per SM more than a
+// deeper prefetch (profiles/ab_r02_bsgs_variants.txt).
+#ifndef FHE_TMA_NST8
+#define FHE_TMA_NST8 2
+#endif
+#if FHE_TMA_WIDE
+#define FHE_TMA_WIDE_CASES(NG_, MINB_, MODE_)                                                 \
+    if (sg == 16) { launch_tma<D, NG_, 16, MINB_, MODE_>(c, a, m, level, st); break; }         \
+    if (sg == 8) { launch_tma<D, NG_, 8, MINB_, MODE_>(c, a, m, level, st); break; }
+#else
+#define FHE_TMA_WIDE_CASES(NG_, MINB_, MODE_)
+#endif
+template <int DN, int NG, int SG, int MINB_, int MODE = 0>
 static void launch_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, cudaStream_t st) {
     using LY = TmaLayout<DN, NG, SG>;
+    constexpr int NST = SG >= 8 ? FHE_TMA_NST8 : 2;
+    constexpr int MINB = (NST > 2 && MINB_ > 3) ? 3 : MINB_;
     const int ne = level + 1 + c.K;
-    const size_t smem = (size_t)2 * LY::STAGE * 16 + 16;
+    const size_t smem = (size_t)NST * LY::STAGE * 16 + 8 * NST;
     const size_t items = (size_t)ne * c.N / (2 * LY::P) * (size_t)((a.nsrc + SG - 1) / SG);
     int per_sm = 0;
-    cudaFuncSetAttribute(k_bsgs_tma<DN, NG, SG, MINB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_tma<DN, NG, SG, MINB, MODE>, 128, smem);
+    cudaFuncSetAttribute(k_bsgs_tma<DN, NG, SG, MINB, MODE, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsgs_tma<DN, NG, SG, MINB, MODE, NST>, 128, smem);
     if (per_sm < 1) per_sm = 1;
     const size_t cap = (size_t)sm_count() * per_sm;
     const int blocks = (int)(items < cap ? items : cap);
-    k_bsgs_tma<DN, NG, SG, MINB, MODE><<<blocks, 128, smem, st>>>(c, a, m, level);
+    k_bsgs_tma<DN, NG, SG, MINB, MODE, NST><<<blocks, 128, smem, st>>>(c, a, m, level);
 }
 
 void bsgs_tma_hoist(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st) {
@@ -2143,7 +2197,8 @@ void bsgs_tma_hoist(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int l
     const int sg = tma_sources(a.nsrc);
 #define FHE_TMAH(D)                                                                \
     do {                                                                           \
-        if (sg == 4) launch_tma<D, 1, 4, FHE_TMA_MINB, 1>(c, a, m, level, st);     \
+        FHE_TMA_WIDE_CASES(1, FHE_TMA_MINB, 1)                                     \
+        if (sg == 4) launch_tma<D, 1, 4, FHE_TMA_MINB, 1>(c, a, m, level, st); \
         else if (sg == 2) launch_tma<D, 1, 2, 3, 1>(c, a, m, level, st);           \
         else launch_tma<D, 1, 1, 2, 1>(c, a, m, level, st);                        \
     } while (0)
@@ -2161,15 +2216,18 @@ void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, 
 #define FHE_TMA(D)                                                               \
     do {                                                                         \
         if (a.ng == 1 && m.ng1) {                                                \
-            if (sg == 4) launch_tma<D, 1, 4, FHE_TMA_MINB>(c, a, m, level, st);  \
+            FHE_TMA_WIDE_CASES(1, FHE_TMA_MINB, 0)                               \
+            if (sg == 4) launch_tma<D, 1, 4, FHE_TMA_MINB>(c, a, m, level, st); \
             else if (sg == 2) launch_tma<D, 1, 2, 3>(c, a, m, level, st);        \
             else launch_tma<D, 1, 1, 2>(c, a, m, level, st);                     \
         } else if (a.ng <= 3) {                                                  \
-            if (sg == 4) launch_tma<D, 3, 4, FHE_TMA_MINB>(c, a, m, level, st);  \
+            FHE_TMA_WIDE_CASES(3, FHE_TMA_MINB, 0)                               \
+            if (sg == 4) launch_tma<D, 3, 4, FHE_TMA_MINB>(c, a, m, level, st); \
             else if (sg == 2) launch_tma<D, 3, 2, 3>(c, a, m, level, st);        \
             else launch_tma<D, 3, 1, 2>(c, a, m, level, st);                     \
         } else {                                                                 \
-            if (sg == 4) launch_tma<D, kFusedMaxG, 4, 2>(c, a, m, level, st);    \
+            FHE_TMA_WIDE_CASES(kFusedMaxG, 2, 0)                                 \
+            if (sg == 4) launch_tma<D, kFusedMaxG, 4, 2>(c, a, m, level, st); \
             else if (sg == 2) launch_tma<D, kFusedMaxG, 2, 2>(c, a, m, level, st); \
             else launch_tma<D, kFusedMaxG, 1, 2>(c, a, m, level, st);            \
         }                                                                        \

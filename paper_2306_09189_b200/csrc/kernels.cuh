@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "modarith.cuh"
 
@@ -331,7 +332,31 @@ constexpr int kTmaSchedSlots = 16;  // per compute stream (fheconv.cu tma_rows)
 void bsgs_tma_hoist(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st);
 // encode a 5-D uint64 tensor map (dims innermost first, dense)
 void tma_map5(CUtensorMap* map, const void* base, const uint64_t dims[5], const uint32_t box[5]);
-inline int tma_sources(int nsrc) { return nsrc >= 4 ? 4 : nsrc >= 2 ? 2 : 1; }
+// Sources per CTA of k_bsgs_tma. The key and plaintext blocks of a CTA are shared by its SG
+// sources: 106 / 89 / 80 bytes of L2 -> SM operand traffic per (source, coefficient, baby step)
+// at SG = 4 / 8 / 16 (39 GB per cfg3 batch-16 launch at SG = 4, ncu
+// l1tex__m_xbar2l1tex_read_bytes). Builds with -DFHE_TMA_WIDE=1 also instantiate SG = 8 and 16
+// (FHECONV_TMA_SG caps it); A/B on the B200 (profiles/ab_r02_bsgs_variants.txt): SG = 8 is
+// +-0 %, SG = 16 is -12 % (128-byte boxes), so the default build stops at 4.
+#ifndef FHE_TMA_WIDE
+#define FHE_TMA_WIDE 0
+#endif
+inline int tma_sg_max() {
+#if FHE_TMA_WIDE
+    static const int v = [] {
+        const char* e = getenv("FHECONV_TMA_SG");
+        const int x = e ? atoi(e) : 8;
+        return x >= 16 ? 16 : x >= 8 ? 8 : 4;
+    }();
+    return v;
+#else
+    return 4;
+#endif
+}
+inline int tma_sources(int nsrc) {
+    const int m = tma_sg_max();
+    return nsrc >= 16 && m >= 16 ? 16 : nsrc >= 8 && m >= 8 ? 8 : nsrc >= 4 ? 4 : nsrc >= 2 ? 2 : 1;
+}
 void bsgs_tma(const DevCtx& c, const FusedBsgs& a, const TmaMaps& m, int level, int dn, cudaStream_t st);
 // encode a 4-D uint64 tensor map (dims innermost first, dense)
 void tma_map4(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint32_t box[4]);

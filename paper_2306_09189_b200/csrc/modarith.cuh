@@ -238,6 +238,35 @@ __device__ __forceinline__ void fmac_d(double& acc, double x, double y, const Ar
     const double t = __dadd_rn(__fma_rn(ph, a.qinv, kMagic), -kMagic);
     acc = __dadd_rn(acc, __dadd_rn(__fma_rn(-t, a.q, ph), pl));
 }
+// Error-free accumulation of an inner product sum_j x_j y_j (|x_j|, |y_j| <= q/2 < 2^49,
+// at most 8 terms) with ONE quotient for the whole sum instead of one per product:
+//  H starts at 1.5 * 2^102 and stays in [2^102, 2^103) (|sum| < 2^101), so every
+//    H' = fma(x, y, H) is the exact x y + H rounded to the grid 2^50 -- H' - H is the
+//    product rounded to the grid, exactly;
+//  fma(x, y, -(H' - H)) is the exact remainder (an integer, |.| <= 2^49), summed in L
+//    (|L| < 2^53 with the caller's initial term <= q + 1).
+// 4 FP64 operations per product (fmac_d: 7). fold_d returns the sum mod q:
+// M = (H - 1.5 * 2^102) 2^-50 is an integer below 2^51, M [2^50]_q by mulmod_d, plus L,
+// one red_d (|result| <= 0.5 q + 1).
+constexpr double kGridBig = 0x1.8p+102;
+constexpr double kGridInv = 0x1p-50;
+struct ArG {
+    double c, cq;  // centred 2^50 mod q, and c / q
+};
+__device__ __forceinline__ ArG make_arg(const ArD& a) {
+    const uint64_t r = (1ULL << 50) % a.qi;
+    const double c = r > a.qi / 2 ? -(double)(a.qi - r) : (double)r;
+    return ArG{c, __ddiv_rn(c, a.q)};
+}
+__device__ __forceinline__ void fmag_d(double& H, double& L, double x, double y) {
+    const double Hn = __fma_rn(x, y, H);
+    L = __dadd_rn(L, __fma_rn(x, y, __dadd_rn(H, -Hn)));
+    H = Hn;
+}
+__device__ __forceinline__ double fold_d(double H, double L, const ArD& a, const ArG& g) {
+    const double M = __dmul_rn(__dadd_rn(H, -kGridBig), kGridInv);
+    return red_d(__dadd_rn(mulmod_d(M, g.c, g.cq, a), L), a);
+}
 // canonical word in [0, q) -> bits of the same value as a double (exact)
 __device__ __forceinline__ uint64_t u2d_bits(uint64_t x) {
     return (uint64_t)__double_as_longlong(

@@ -14,6 +14,7 @@
 // padded shared memory. Phase B gives each block of B = 2^7..2^8 words to one
 // or half a warp, so its passes only need __syncwarp.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -39,6 +40,19 @@ __device__ __forceinline__ void ld256_nc(const uint64_t* p, uint64_t* v) {
 __device__ __forceinline__ void st256(uint64_t* p, const uint64_t* v) {
     asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
                  : "memory");
+}
+
+// Thread-block-cluster helpers of the single-launch transform (k_ntt_fused): the
+// column -> row intermediate of a residue row stays in the shared memory of the
+// cluster's CTAs and is read through distributed shared memory.
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint64_t ld_dsmem(uint32_t local_addr, uint32_t rank) {
+    uint32_t ra;
+    uint64_t v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
+    return v;
 }
 
 
@@ -81,6 +95,9 @@ __device__ __forceinline__ void tw_ld(const double2* p, double2* o, int cnt) {
 #endif
 #ifndef FHE_NTT_MINB
 #define FHE_NTT_MINB 1
+#endif
+#ifndef FHE_NTTF_MINB
+#define FHE_NTTF_MINB 1  // CTAs per SM the single-launch kernel is compiled for
 #endif
 #ifndef FHE_NTT_CHUNK
 #define FHE_NTT_CHUNK 0  // MB of rows per NTT launch pair (0: all rows in one pair)
@@ -314,24 +331,37 @@ struct PassPlan {  // stages of the two passes of a phase of 2^LOGN elements
 // Phase A (columns): CTA = C columns x N1 rows, thread (cc = tid % C, lt = tid / C).
 // Forward: canonical words in, lazy [0, 4q) words / reduced doubles out (read by the
 // row pass); inverse: the row pass's words in, canonical words out (times N^-1).
-template <int LOG_N1, int C, bool INVERSE>
-__global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm) {
+// XCH = 0: residues in and out of global memory (k_ntt_cols). XCH = 1 (k_ntt_fused, one
+// cluster per residue row): the intermediate between the phases lives in the cluster's
+// shared memory -- the forward transform leaves it in this CTA's `stage` ([N1][C] words:
+// this CTA's C columns), the inverse reads it from the row phase's stages ([BPC][B] words
+// per CTA: matrix row i is held by CTA i / BPC).
+template <int LOG_N1, int LOG_B, int C, bool INVERSE, int XCH>
+__device__ __forceinline__ void cols_phase(const DevCtx& c, uint64_t* data, const RowMap& rm, int row, int u, int bx,
+                                           uint64_t* sm, uint64_t* stage) {
     constexpr int N1 = 1 << LOG_N1;
     constexpr int PN = N1 + (N1 >> 4) + 1;  // padded column length (odd in words)
+    constexpr int B = 1 << LOG_B;
+    constexpr int BPC = NTT_THREADS / (B / EPT);
     using PP = PassPlan<LOG_N1, INVERSE>;
-    __shared__ uint64_t sm[C * PN];
-    const int row = blockIdx.y + rm.row0;
-    const int u = row % rm.rows_per_poly;
-    if (skip_row(rm, row, u)) return;
     const int p = row_prime(rm, u);
     const uint64_t q = c.primes[p].q;
-    const int B = c.N >> LOG_N1;
     const int cc = threadIdx.x % C, lt = threadIdx.x / C;
-    uint64_t* a = data + (size_t)row * c.N + blockIdx.x * C + cc;
+    uint64_t* a = data + (size_t)row * c.N + bx * C + cc;
     uint64_t* col = sm + cc * PN;
     uint64_t w[EPT];
+    if (XCH && INVERSE) {
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(stage) + (uint32_t)(bx * C + cc) * 8u;
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) w[e] = __ldcs(a + (size_t)PP::pos1(lt, e) * B);
+        for (int e = 0; e < EPT; ++e) {
+            const int i = PP::pos1(lt, e);
+            w[e] = ld_dsmem(sb + (uint32_t)((i % BPC) * B) * 8u, (uint32_t)(i / BPC));
+        }
+        cluster_arrive();  // this CTA's reads of the other stages are done (waited for at kernel end)
+    } else {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) w[e] = __ldcs(a + (size_t)PP::pos1(lt, e) * B);
+    }
     // FP64 butterflies for q < 2^50
     if (q < (1ULL << 50)) {
         const ArD ad = make_ard(q);
@@ -350,8 +380,13 @@ __global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_cols(DevCtx c
         for (int e = 0; e < EPT; ++e) v[e] = asd(col[pad(PP::pos2(lt, e))]);
         if (!INVERSE) {
             fwd_pass_d<PP::R2>(v, lt * (EPT >> PP::R2), LOG_N1, PP::R1, 0, 0, tw, ad);
+            if (XCH) {
 #pragma unroll
-            for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = asu(v[e]);
+                for (int e = 0; e < EPT; ++e) stage[PP::pos2(lt, e) * C + cc] = asu(v[e]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = asu(v[e]);
+            }
         } else {
             inv_pass_d<PP::R2>(v, lt * (EPT >> PP::R2), PP::R1, LOG_N1, LOG_N1, 0, tw, ad);
             const double2 ni = c.ninvd[p];
@@ -373,14 +408,29 @@ __global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_cols(DevCtx c
     for (int e = 0; e < EPT; ++e) w[e] = col[pad(PP::pos2(lt, e))];
     if (!INVERSE) {
         fwd_pass<PP::R2>(w, lt * (EPT >> PP::R2), LOG_N1, PP::R1, 0, 0, tw, tws, q);
+        if (XCH) {
 #pragma unroll
-        for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = w[e];
+            for (int e = 0; e < EPT; ++e) stage[PP::pos2(lt, e) * C + cc] = w[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = w[e];
+        }
     } else {
         inv_pass<PP::R2>(w, lt * (EPT >> PP::R2), PP::R1, LOG_N1, LOG_N1, 0, tw, tws, q);
         const uint64_t ni = c.ninv[p], nis = c.ninv_sh[p];
 #pragma unroll
         for (int e = 0; e < EPT; ++e) a[(size_t)PP::pos2(lt, e) * B] = mul_shoup(w[e], ni, nis, q);
     }
+}
+
+template <int LOG_N1, int LOG_B, int C, bool INVERSE>
+__global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_cols(DevCtx c, uint64_t* data, RowMap rm) {
+    constexpr int N1 = 1 << LOG_N1;
+    __shared__ uint64_t sm[C * (N1 + (N1 >> 4) + 1)];
+    const int row = blockIdx.y + rm.row0;
+    const int u = row % rm.rows_per_poly;
+    if (skip_row(rm, row, u)) return;
+    cols_phase<LOG_N1, LOG_B, C, INVERSE, 0>(c, data, rm, row, u, blockIdx.x, sm, nullptr);
 }
 
 __device__ __forceinline__ uint32_t perm_index_n(uint32_t k, uint32_t g, int logN) {
@@ -393,22 +443,24 @@ __device__ __forceinline__ uint32_t perm_index_n(uint32_t k, uint32_t g, int log
 // (one or a fraction of a warp: the exchange needs only __syncwarp). The forward
 // transform ends here (canonical words; FUSE_MODDOWN: the ModDown epilogue), the
 // inverse starts here (canonical words in, words for the column pass out).
-template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE>
-__global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_rows(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
+// XCH as in cols_phase: the forward transform reads its blocks from the column phase's
+// stages (element x of matrix row blk is held by CTA x / C at [blk][x % C]), the inverse
+// leaves its blocks in this CTA's `stage` ([BPC][B] words).
+template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE, int XCH>
+__device__ __forceinline__ void rows_phase(const DevCtx& c, uint64_t* data, const RowMap& rm, const NttFuse& fz, int row,
+                                           int u, int bx, uint64_t* sm, uint64_t* stage) {
+    constexpr int N1 = 1 << LOG_N1;
+    constexpr int C = NTT_THREADS / (N1 / EPT);
     constexpr int B = 1 << LOG_B;
     constexpr int TPB = B / EPT;
     constexpr int BPC = NTT_THREADS / TPB;
     constexpr int PB = B + (B >> 4);
     static_assert(TPB <= 32, "a block is at most one warp");
     using PP = PassPlan<LOG_B, INVERSE>;
-    __shared__ uint64_t sm[BPC * PB];
-    const int row = blockIdx.y + rm.row0;
-    const int u = row % rm.rows_per_poly;
-    if (skip_row(rm, row, u)) return;
     const int p = row_prime(rm, u);
     const uint64_t q = c.primes[p].q;
     const int bi = threadIdx.x / TPB, lt = threadIdx.x % TPB;
-    const int blk = blockIdx.x * BPC + bi;
+    const int blk = bx * BPC + bi;
     const size_t base = (size_t)blk * B;  // block offset in the row
     uint64_t* a = data + (size_t)row * c.N + base;
     uint64_t* vec = sm + bi * PB;
@@ -417,7 +469,15 @@ __global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_rows(DevCtx c
     uint64_t w[EPT];
     // input: forward stride-TPB residues (pass 1 positions lt + k TPB), inverse 16
     // contiguous residues lt 16 + e
-    if (!INVERSE) {
+    if (XCH && !INVERSE) {
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(stage) + (uint32_t)(blk * C) * 8u;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+            const int x = PP::pos1(lt, e);
+            w[e] = ld_dsmem(sb + (uint32_t)(x % C) * 8u, (uint32_t)(x / C));
+        }
+        cluster_arrive();  // this CTA's reads of the other stages are done (waited for at kernel end)
+    } else if (!INVERSE) {
 #pragma unroll
         for (int e = 0; e < EPT; ++e) w[e] = __ldcs(a + PP::pos1(lt, e));
     } else {
@@ -472,8 +532,13 @@ __global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_rows(DevCtx c
         }
     }
     if (INVERSE) {  // pass-2 positions lt + k TPB: coalesced
+        if (XCH) {
 #pragma unroll
-        for (int e = 0; e < EPT; ++e) a[PP::pos2(lt, e)] = w[e];
+            for (int e = 0; e < EPT; ++e) stage[bi * B + PP::pos2(lt, e)] = w[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) a[PP::pos2(lt, e)] = w[e];
+        }
         return;
     }
     // forward output: residue e of this thread sits at block position lt 16 + e
@@ -517,6 +582,44 @@ __global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_rows(DevCtx c
 #pragma unroll
         for (int e = 0; e < EPT; e += 4) st256(a + lt * EPT + e, w + e);
     }
+}
+
+template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE>
+__global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_rows(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
+    constexpr int B = 1 << LOG_B;
+    __shared__ uint64_t sm[(NTT_THREADS / (B / EPT)) * (B + (B >> 4))];
+    const int row = blockIdx.y + rm.row0;
+    const int u = row % rm.rows_per_poly;
+    if (skip_row(rm, row, u)) return;
+    rows_phase<LOG_N1, LOG_B, INVERSE, FUSE, 0>(c, data, rm, fz, row, u, blockIdx.x, sm, nullptr);
+}
+
+// The whole transform of a residue row in ONE launch: a thread-block cluster of
+// B / C = N / (16 NTT_THREADS) CTAs per row (16 at N = 2^15) runs the column phase and the
+// row phase back to back; the intermediate (2048 words per CTA) never leaves shared memory,
+// every CTA reads the blocks of its second phase from the stages of the whole cluster
+// (ld.shared::cluster). One HBM round trip per transform instead of two.
+template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE>
+__global__ void __launch_bounds__(NTT_THREADS, FHE_NTTF_MINB) k_ntt_fused(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz) {
+    constexpr int N1 = 1 << LOG_N1, B = 1 << LOG_B;
+    constexpr int C = NTT_THREADS / (N1 / EPT);
+    constexpr int XA = C * (N1 + (N1 >> 4) + 1), XB = (NTT_THREADS / (B / EPT)) * (B + (B >> 4));
+    __shared__ uint64_t sm[XA > XB ? XA : XB];
+    __shared__ __align__(16) uint64_t stage[NTT_THREADS * EPT];
+    const int row = blockIdx.y + rm.row0;
+    const int u = row % rm.rows_per_poly;
+    if (skip_row(rm, row, u)) return;  // the whole cluster (one row) returns
+    if (!INVERSE)
+        cols_phase<LOG_N1, LOG_B, C, false, 1>(c, data, rm, row, u, blockIdx.x, sm, stage);
+    else
+        rows_phase<LOG_N1, LOG_B, true, FUSE_NONE, 1>(c, data, rm, fz, row, u, blockIdx.x, sm, stage);
+    cluster_arrive();
+    cluster_wait();  // every stage of the row is written
+    if (!INVERSE)
+        rows_phase<LOG_N1, LOG_B, false, FUSE, 1>(c, data, rm, fz, row, u, blockIdx.x, sm, stage);
+    else
+        cols_phase<LOG_N1, LOG_B, C, true, 1>(c, data, rm, row, u, blockIdx.x, sm, stage);
+    cluster_wait();  // no CTA leaves while its stage may still be read
 }
 
 // FastBConv of ModUp: one thread per (source, digit, coefficient pair); the
@@ -774,12 +877,64 @@ __global__ void __launch_bounds__(256) k_bconv_mdr(DevCtx c, uint64_t* w, const 
     }
 }
 
+template <typename K>
+void launch_cluster(K kern, dim3 grid, int cl, cudaStream_t st, const DevCtx& c, uint64_t* data, const RowMap& rm,
+                    const NttFuse& fz) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(NTT_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = cl;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, c, data, rm, fz);
+}
+
+// FHE_NTT_FUSED=1 selects the single-launch cluster transform (N <= 2^15; the 32 CTAs
+// per row of N = 2^16 exceed the largest cluster). Off by default: on the B200 the
+// two-launch transform is faster (cfg3 batch-16 conv 2095 vs 1892-2027 conv/s, hoisted
+// 36.5k vs 30.1-32.6k rot/s over 3-5 CTAs/SM; profiles/ab_r02_ntt_cluster.txt) -- the
+// clusters of 16 schedule per GPC and the exchange runs at the DSMEM rate.
+static bool ntt_fused_enabled() {  // read per launch: tests switch it between contexts
+    const char* e = getenv("FHE_NTT_FUSED");
+    return e && e[0] == '1';
+}
+
 template <int LOG_N1, int LOG_B>
 void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, bool inverse, int fuse,
                   const NttFuse& fz, cudaStream_t st) {
     constexpr int N1 = 1 << LOG_N1, B = 1 << LOG_B;
     constexpr int C = NTT_THREADS / (N1 / EPT);
     constexpr int BPC = NTT_THREADS / (B / EPT);
+    constexpr int CL = B / C;  // CTAs per row of either phase
+    if (CL <= 16 && CL == N1 / BPC && FHE_NTT_CHUNK == 0 && ntt_fused_enabled()) {
+        static const bool once = [] {  // clusters of 16 are a non-portable size
+            if (CL > 8) {
+                cudaFuncSetAttribute(k_ntt_fused<LOG_N1, LOG_B, false, FUSE_NONE>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                cudaFuncSetAttribute(k_ntt_fused<LOG_N1, LOG_B, false, FUSE_MODDOWN>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                cudaFuncSetAttribute(k_ntt_fused<LOG_N1, LOG_B, true, FUSE_NONE>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            }
+            return true;
+        }();
+        (void)once;
+        const dim3 g(CL, nrows);
+        if (inverse)
+            launch_cluster(k_ntt_fused<LOG_N1, LOG_B, true, FUSE_NONE>, g, CL, st, c, data, rm, fz);
+        else if (fuse == FUSE_MODDOWN)
+            launch_cluster(k_ntt_fused<LOG_N1, LOG_B, false, FUSE_MODDOWN>, g, CL, st, c, data, rm, fz);
+        else
+            launch_cluster(k_ntt_fused<LOG_N1, LOG_B, false, FUSE_NONE>, g, CL, st, c, data, rm, fz);
+        note_launch(1);
+        return;
+    }
     // rows in chunks whose intermediate (column pass -> row pass) stays in L2
     const int chunk = FHE_NTT_CHUNK > 0 ? std::max(1, (int)(((size_t)FHE_NTT_CHUNK << 20) / ((size_t)c.N * 8))) : nrows;
     for (int r0 = 0; r0 < nrows; r0 += chunk) {
@@ -788,14 +943,14 @@ void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, 
         rc.row0 = rm.row0 + r0;
         const dim3 ga(B / C, nr_), gb((N1 + BPC - 1) / BPC, nr_);
         if (!inverse) {
-            k_ntt_cols<LOG_N1, C, false><<<ga, NTT_THREADS, 0, st>>>(c, data, rc);
+            k_ntt_cols<LOG_N1, LOG_B, C, false><<<ga, NTT_THREADS, 0, st>>>(c, data, rc);
             if (fuse == FUSE_MODDOWN)
                 k_ntt_rows<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gb, NTT_THREADS, 0, st>>>(c, data, rc, fz);
             else
                 k_ntt_rows<LOG_N1, LOG_B, false, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rc, fz);
         } else {
             k_ntt_rows<LOG_N1, LOG_B, true, FUSE_NONE><<<gb, NTT_THREADS, 0, st>>>(c, data, rc, fz);
-            k_ntt_cols<LOG_N1, C, true><<<ga, NTT_THREADS, 0, st>>>(c, data, rc);
+            k_ntt_cols<LOG_N1, LOG_B, C, true><<<ga, NTT_THREADS, 0, st>>>(c, data, rc);
         }
         note_launch(2);
     }
