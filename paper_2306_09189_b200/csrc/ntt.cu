@@ -59,7 +59,14 @@ __device__ __forceinline__ uint64_t ld_dsmem(uint32_t local_addr, uint32_t rank)
 // Twiddles of one sub-stage of a group are consecutive and aligned to their count
 // (a power of two): load them with 128-bit (integer: w, Shoup) or 256-bit (FP64:
 // (w_c, w_c / q) pairs) accesses, so a warp's requests use whole sectors.
+template <bool SM = false>
 __device__ __forceinline__ void tw_ld(const uint64_t* p, uint64_t* o, int cnt) {
+    if (SM) {  // the CTA's twiddle table in shared memory (k_ntt_rows_tw)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (i < cnt) o[i] = p[i];
+        return;
+    }
     if (cnt == 1) {
         o[0] = __ldg(p);
         return;
@@ -72,7 +79,14 @@ __device__ __forceinline__ void tw_ld(const uint64_t* p, uint64_t* o, int cnt) {
             o[i + 1] = t.y;
         }
 }
+template <bool SM = false>
 __device__ __forceinline__ void tw_ld(const double2* p, double2* o, int cnt) {
+    if (SM) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (i < cnt) o[i] = p[i];
+        return;
+    }
     if (cnt == 1) {
         o[0] = __ldg(p);
         return;
@@ -110,7 +124,7 @@ constexpr int LOG_EPT = EPT == 16 ? 4 : 3;
 // form EPT / 2^R groups. Local vector of n = 2^logn elements, local stage of
 // the pass sigma0, global stage offset s0, block index blk:
 //   twiddle(stage sigma, x) = 2^(s0+sigma) + blk 2^sigma + x / (2 t_sigma)
-template <int R>
+template <int R, bool SM = false>
 __device__ __forceinline__ void fwd_pass(uint64_t (&v)[EPT], int G0, int logn, int sigma0, int s0, int blk,
                                          const uint64_t* __restrict__ tw, const uint64_t* __restrict__ tws,
                                          uint64_t q) {
@@ -128,8 +142,8 @@ __device__ __forceinline__ void fwd_pass(uint64_t (&v)[EPT], int G0, int logn, i
             const int sig = sigma0 + rho;
             const int base = (1 << (s0 + sig)) + (blk << sig) + (j0 >> (logt + 1 - rho));
             uint64_t wt[GS / 2], wst[GS / 2];
-            tw_ld(tw + base, wt, 1 << rho);
-            tw_ld(tws + base, wst, 1 << rho);
+            tw_ld<SM>(tw + base, wt, 1 << rho);
+            tw_ld<SM>(tws + base, wst, 1 << rho);
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
@@ -159,7 +173,7 @@ __device__ __forceinline__ int fwd_pos(int G0, int e, int logn, int sigma0) {
 
 // Inverse GS pass of R stages starting at distance 2^logt (t grows):
 //   twiddle(t', x) = n_tot / (2 t') + blk n_loc / (2 t') + x / (2 t')
-template <int R>
+template <int R, bool SM = false>
 __device__ __forceinline__ void inv_pass(uint64_t (&v)[EPT], int G0, int logt, int log_ntot, int log_nloc, int blk,
                                          const uint64_t* __restrict__ tw, const uint64_t* __restrict__ tws,
                                          uint64_t q) {
@@ -175,8 +189,8 @@ __device__ __forceinline__ void inv_pass(uint64_t (&v)[EPT], int G0, int logt, i
             const int lt = logt + rho;  // current distance 2^lt
             const int base = (1 << (log_ntot - lt - 1)) + (blk << (log_nloc - lt - 1)) + (j0 >> (lt + 1));
             uint64_t wt[GS / 2], wst[GS / 2];
-            tw_ld(tw + base, wt, GS >> (rho + 1));
-            tw_ld(tws + base, wst, GS >> (rho + 1));
+            tw_ld<SM>(tw + base, wt, GS >> (rho + 1));
+            tw_ld<SM>(tws + base, wst, GS >> (rho + 1));
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
@@ -218,7 +232,7 @@ constexpr int kUnitQ = 8, kUnitMul = 5, kUnitRed = 5, kUnitMax = 32;  // in q / 
 
 
 // Forward CT pass of R <= 4 stages on doubles (inputs <= 8 units: <= 28 after).
-template <int R>
+template <int R, bool SM = false>
 __device__ __forceinline__ void fwd_pass_d(double (&v)[EPT], int G0, int logn, int sigma0, int s0, int blk,
                                            const double2* __restrict__ tw, const ArD& a) {
     constexpr int GS = 1 << R;
@@ -233,7 +247,7 @@ __device__ __forceinline__ void fwd_pass_d(double (&v)[EPT], int G0, int logn, i
             const int half = 1 << (R - 1 - rho);
             const int sig = sigma0 + rho;
             double2 wt[GS / 2];
-            tw_ld(tw + (1 << (s0 + sig)) + (blk << sig) + (j0 >> (logt + 1 - rho)), wt, 1 << rho);
+            tw_ld<SM>(tw + (1 << (s0 + sig)) + (blk << sig) + (j0 >> (logt + 1 - rho)), wt, 1 << rho);
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
@@ -251,7 +265,7 @@ __device__ __forceinline__ void fwd_pass_d(double (&v)[EPT], int G0, int logn, i
 
 // Inverse GS pass of R stages on doubles; sums are reduced only when the
 // tracked bound of a butterfly's inputs would pass 4q. Leaves <= 8 units.
-template <int R>
+template <int R, bool SM = false>
 __device__ __forceinline__ void inv_pass_d(double (&v)[EPT], int G0, int logt, int log_ntot, int log_nloc, int blk,
                                            const double2* __restrict__ tw, const ArD& a) {
     constexpr int GS = 1 << R;
@@ -267,8 +281,8 @@ __device__ __forceinline__ void inv_pass_d(double (&v)[EPT], int G0, int logt, i
             const int half = 1 << rho;
             const int lt = logt + rho;
             double2 wt[GS / 2];
-            tw_ld(tw + (1 << (log_ntot - lt - 1)) + (blk << (log_nloc - lt - 1)) + (j0 >> (lt + 1)), wt,
-                  GS >> (rho + 1));
+            tw_ld<SM>(tw + (1 << (log_ntot - lt - 1)) + (blk << (log_nloc - lt - 1)) + (j0 >> (lt + 1)), wt,
+                      GS >> (rho + 1));
 #pragma unroll
             for (int k = 0; k < GS; ++k) {
                 if (k & half) continue;
@@ -446,21 +460,29 @@ __device__ __forceinline__ uint32_t perm_index_n(uint32_t k, uint32_t g, int log
 // XCH as in cols_phase: the forward transform reads its blocks from the column phase's
 // stages (element x of matrix row blk is held by CTA x / C at [blk][x % C]), the inverse
 // leaves its blocks in this CTA's `stage` ([BPC][B] words).
-template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE, int XCH>
+// TWS (k_ntt_rows_tw): the twiddles of the CTA's BPC blocks are read from the shared-memory
+// table `twsm` (entry ((BPC + bi) << sigma) + x of stage sigma: the global table's index
+// with N1 + blk replaced by BPC + bi), filled once per CTA and reused for several rows.
+template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE, int XCH, bool TWS = false>
 __device__ __forceinline__ void rows_phase(const DevCtx& c, uint64_t* data, const RowMap& rm, const NttFuse& fz, int row,
-                                           int u, int bx, uint64_t* sm, uint64_t* stage) {
+                                           int u, int bx, uint64_t* sm, uint64_t* stage,
+                                           const uint64_t* twsm = nullptr) {
     constexpr int N1 = 1 << LOG_N1;
     constexpr int C = NTT_THREADS / (N1 / EPT);
     constexpr int B = 1 << LOG_B;
     constexpr int TPB = B / EPT;
     constexpr int BPC = NTT_THREADS / TPB;
     constexpr int PB = B + (B >> 4);
+    constexpr int LOG_BPC = LOG_EPT + (NTT_THREADS == 128 ? 7 : 8) - LOG_B;  // BPC = NTT_THREADS EPT / B
+    static_assert((1 << LOG_BPC) == BPC, "blocks per CTA");
     static_assert(TPB <= 32, "a block is at most one warp");
+    const int tS0 = TWS ? LOG_BPC : LOG_N1;  // twiddle index base: 2^(tS0 + sigma) + (tBlk << sigma)
     using PP = PassPlan<LOG_B, INVERSE>;
     const int p = row_prime(rm, u);
     const uint64_t q = c.primes[p].q;
     const int bi = threadIdx.x / TPB, lt = threadIdx.x % TPB;
     const int blk = bx * BPC + bi;
+    const int tBlk = TWS ? bi : blk;
     const size_t base = (size_t)blk * B;  // block offset in the row
     uint64_t* a = data + (size_t)row * c.N + base;
     uint64_t* vec = sm + bi * PB;
@@ -485,42 +507,44 @@ __device__ __forceinline__ void rows_phase(const DevCtx& c, uint64_t* data, cons
         for (int e = 0; e < EPT; e += 4) ld256(a + lt * EPT + e, w + e);
     }
     if (fp) {
-        const double2* tw = (INVERSE ? c.itwd : c.twd) + (size_t)p * c.N;
+        const double2* tw = TWS ? reinterpret_cast<const double2*>(twsm) - BPC
+                                : (INVERSE ? c.itwd : c.twd) + (size_t)p * c.N;
         double v[EPT];
 #pragma unroll
         for (int e = 0; e < EPT; ++e) v[e] = INVERSE ? asd(u2d_bits(w[e])) : asd(w[e]);
         if (!INVERSE)
-            fwd_pass_d<PP::R1>(v, lt * (EPT >> PP::R1), LOG_B, 0, LOG_N1, blk, tw, ad);
+            fwd_pass_d<PP::R1, TWS>(v, lt * (EPT >> PP::R1), LOG_B, 0, tS0, tBlk, tw, ad);
         else
-            inv_pass_d<PP::R1>(v, lt * (EPT >> PP::R1), 0, LOG_N1 + LOG_B, LOG_B, blk, tw, ad);
+            inv_pass_d<PP::R1, TWS>(v, lt * (EPT >> PP::R1), 0, tS0 + LOG_B, LOG_B, tBlk, tw, ad);
 #pragma unroll
         for (int e = 0; e < EPT; ++e) vec[pad(PP::pos1(lt, e))] = asu(v[e]);
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < EPT; ++e) v[e] = asd(vec[pad(PP::pos2(lt, e))]);
         if (!INVERSE) {
-            fwd_pass_d<PP::R2>(v, lt * (EPT >> PP::R2), LOG_B, PP::R1, LOG_N1, blk, tw, ad);
+            fwd_pass_d<PP::R2, TWS>(v, lt * (EPT >> PP::R2), LOG_B, PP::R1, tS0, tBlk, tw, ad);
 #pragma unroll
             for (int e = 0; e < EPT; ++e) w[e] = canon_d(v[e], ad);
         } else {
-            inv_pass_d<PP::R2>(v, lt * (EPT >> PP::R2), PP::R1, LOG_N1 + LOG_B, LOG_B, blk, tw, ad);
+            inv_pass_d<PP::R2, TWS>(v, lt * (EPT >> PP::R2), PP::R1, tS0 + LOG_B, LOG_B, tBlk, tw, ad);
 #pragma unroll
             for (int e = 0; e < EPT; ++e) w[e] = asu(v[e]);
         }
     } else {
-        const uint64_t* tw = (INVERSE ? c.itw : c.tw) + (size_t)p * c.N;
-        const uint64_t* tws = (INVERSE ? c.itw_sh : c.tw_sh) + (size_t)p * c.N;
+        // shared-memory table of an integer row: [BPC (B - 1)] twiddles, then their Shoup companions
+        const uint64_t* tw = TWS ? twsm - BPC : (INVERSE ? c.itw : c.tw) + (size_t)p * c.N;
+        const uint64_t* tws = TWS ? twsm + BPC * (B - 1) - BPC : (INVERSE ? c.itw_sh : c.tw_sh) + (size_t)p * c.N;
         if (!INVERSE)
-            fwd_pass<PP::R1>(w, lt * (EPT >> PP::R1), LOG_B, 0, LOG_N1, blk, tw, tws, q);
+            fwd_pass<PP::R1, TWS>(w, lt * (EPT >> PP::R1), LOG_B, 0, tS0, tBlk, tw, tws, q);
         else
-            inv_pass<PP::R1>(w, lt * (EPT >> PP::R1), 0, LOG_N1 + LOG_B, LOG_B, blk, tw, tws, q);
+            inv_pass<PP::R1, TWS>(w, lt * (EPT >> PP::R1), 0, tS0 + LOG_B, LOG_B, tBlk, tw, tws, q);
 #pragma unroll
         for (int e = 0; e < EPT; ++e) vec[pad(PP::pos1(lt, e))] = w[e];
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < EPT; ++e) w[e] = vec[pad(PP::pos2(lt, e))];
         if (!INVERSE) {
-            fwd_pass<PP::R2>(w, lt * (EPT >> PP::R2), LOG_B, PP::R1, LOG_N1, blk, tw, tws, q);
+            fwd_pass<PP::R2, TWS>(w, lt * (EPT >> PP::R2), LOG_B, PP::R1, tS0, tBlk, tw, tws, q);
             const uint64_t q2 = 2 * q;
 #pragma unroll
             for (int e = 0; e < EPT; ++e) {  // [0, 4q) -> [0, q)
@@ -528,7 +552,7 @@ __device__ __forceinline__ void rows_phase(const DevCtx& c, uint64_t* data, cons
                 w[e] = x >= q ? x - q : x;
             }
         } else {
-            inv_pass<PP::R2>(w, lt * (EPT >> PP::R2), PP::R1, LOG_N1 + LOG_B, LOG_B, blk, tw, tws, q);
+            inv_pass<PP::R2, TWS>(w, lt * (EPT >> PP::R2), PP::R1, tS0 + LOG_B, LOG_B, tBlk, tw, tws, q);
         }
     }
     if (INVERSE) {  // pass-2 positions lt + k TPB: coalesced
@@ -592,6 +616,48 @@ __global__ void __launch_bounds__(NTT_THREADS, FHE_NTT_MINB) k_ntt_rows(DevCtx c
     const int u = row % rm.rows_per_poly;
     if (skip_row(rm, row, u)) return;
     rows_phase<LOG_N1, LOG_B, INVERSE, FUSE, 0>(c, data, rm, fz, row, u, blockIdx.x, sm, nullptr);
+}
+
+// Row phase with the twiddles in shared memory: a CTA's BPC blocks use BPC (B - 1) twiddles
+// (16 bytes each: (w_c, w_c / q) or (w, Shoup w)), twice the bytes of the residues they
+// transform -- read per row from L2, they are most of the row phase's traffic and of its
+// long-scoreboard stalls. Here a CTA fills the table once and transforms the same blocks of
+// R rows of the same prime (row = pp rows_per_poly + u, pp = g R .. g R + R - 1).
+template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE>
+__global__ void __launch_bounds__(NTT_THREADS, 4) k_ntt_rows_tw(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz,
+                                                                         int npoly, int R) {
+    constexpr int N1 = 1 << LOG_N1, B = 1 << LOG_B;
+    constexpr int BPC = NTT_THREADS / (B / EPT);
+    constexpr int LOG_BPC = LOG_EPT + (NTT_THREADS == 128 ? 7 : 8) - LOG_B;
+    constexpr int XB = BPC * (B + (B >> 4));
+    constexpr int NTW = BPC * (B - 1);
+    extern __shared__ __align__(16) uint64_t dsm[];
+    uint64_t* sm = dsm;                       // pass exchange
+    uint64_t* twsm = dsm + ((XB + 1) & ~1);   // table: NTW double2, or NTW words + NTW Shoup words
+    const int u = blockIdx.y % rm.rows_per_poly, g = blockIdx.y / rm.rows_per_poly;
+    const int p = row_prime(rm, u);
+    const bool fp = c.primes[p].q < (1ULL << 50);
+    const int x0 = N1 + blockIdx.x * BPC;
+    for (int idx = threadIdx.x; idx < NTW; idx += NTT_THREADS) {
+        const int j = idx + BPC;  // table index ((BPC + bi) << sigma) + x
+        const int sig = 31 - __clz(j) - LOG_BPC;
+        const size_t src = (size_t)p * c.N + (size_t)(x0 << sig) + (size_t)(j - (BPC << sig));
+        if (fp) {
+            reinterpret_cast<double2*>(twsm)[idx] = __ldg((INVERSE ? c.itwd : c.twd) + src);
+        } else {
+            twsm[idx] = __ldg((INVERSE ? c.itw : c.tw) + src);
+            twsm[NTW + idx] = __ldg((INVERSE ? c.itw_sh : c.tw_sh) + src);
+        }
+    }
+    __syncthreads();
+    for (int rr = 0; rr < R; ++rr) {
+        const int pp = g * R + rr;
+        if (pp >= npoly) break;
+        const int row = pp * rm.rows_per_poly + u;
+        if (!skip_row(rm, row, u))
+            rows_phase<LOG_N1, LOG_B, INVERSE, FUSE, 0, true>(c, data, rm, fz, row, u, blockIdx.x, sm, nullptr, twsm);
+        __syncwarp();  // the next row reuses the exchange buffer
+    }
 }
 
 // The whole transform of a residue row in ONE launch: a thread-block cluster of
@@ -905,6 +971,12 @@ static bool ntt_fused_enabled() {  // read per launch: tests switch it between c
     return e && e[0] == '1';
 }
 
+static int ntt_tw_rows() {  // read per launch: tests switch it between contexts
+    const char* e = getenv("FHE_NTT_TWR");
+    const int v = e ? atoi(e) : 0;
+    return v < 0 ? 0 : v > 64 ? 64 : v;
+}
+
 template <int LOG_N1, int LOG_B>
 void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, bool inverse, int fuse,
                   const NttFuse& fz, cudaStream_t st) {
@@ -934,6 +1006,43 @@ void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, 
             launch_cluster(k_ntt_fused<LOG_N1, LOG_B, false, FUSE_NONE>, g, CL, st, c, data, rm, fz);
         note_launch(1);
         return;
+    }
+    // Opt-in (FHE_NTT_TWR=R > 1): the row phase keeps its twiddles in shared memory for R rows
+    // of the same prime (k_ntt_rows_tw), R small enough to leave two waves of CTAs. Off by
+    // default: on the B200 it loses 2-5 % (cfg3 batch-16 conv 2133 -> 2046-2083 conv/s, ModUp
+    // 0.626 -> 0.65-0.70 ms; profiles/ab_r02_ntt_twiddles.txt) -- 114-128 registers and the
+    // 50 KB table leave 4 CTAs per SM instead of 5, which costs more than the L2 twiddle
+    // reads it removes.
+    if (rm.row0 == 0 && FHE_NTT_CHUNK == 0 && nrows % rm.rows_per_poly == 0) {
+        const int npoly = nrows / rm.rows_per_poly;
+        int R = std::min(ntt_tw_rows(), npoly);
+        while (R > 1 && (size_t)(N1 / BPC) * rm.rows_per_poly * ((npoly + R - 1) / R) < (size_t)148 * 5 * 2) R /= 2;
+        if (R >= 2) {
+            constexpr size_t smem = (size_t)(((BPC * (B + (B >> 4)) + 1) & ~1) + 2 * BPC * (B - 1)) * 8;
+            static const bool once = [] {
+                cudaFuncSetAttribute(k_ntt_rows_tw<LOG_N1, LOG_B, false, FUSE_NONE>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(k_ntt_rows_tw<LOG_N1, LOG_B, false, FUSE_MODDOWN>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(k_ntt_rows_tw<LOG_N1, LOG_B, true, FUSE_NONE>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                return true;
+            }();
+            (void)once;
+            const dim3 ga(B / C, nrows), gt(N1 / BPC, rm.rows_per_poly * ((npoly + R - 1) / R));
+            if (!inverse) {
+                k_ntt_cols<LOG_N1, LOG_B, C, false><<<ga, NTT_THREADS, 0, st>>>(c, data, rm);
+                if (fuse == FUSE_MODDOWN)
+                    k_ntt_rows_tw<LOG_N1, LOG_B, false, FUSE_MODDOWN><<<gt, NTT_THREADS, smem, st>>>(c, data, rm, fz, npoly, R);
+                else
+                    k_ntt_rows_tw<LOG_N1, LOG_B, false, FUSE_NONE><<<gt, NTT_THREADS, smem, st>>>(c, data, rm, fz, npoly, R);
+            } else {
+                k_ntt_rows_tw<LOG_N1, LOG_B, true, FUSE_NONE><<<gt, NTT_THREADS, smem, st>>>(c, data, rm, fz, npoly, R);
+                k_ntt_cols<LOG_N1, LOG_B, C, true><<<ga, NTT_THREADS, 0, st>>>(c, data, rm);
+            }
+            note_launch(2);
+            return;
+        }
     }
     // rows in chunks whose intermediate (column pass -> row pass) stays in L2
     const int chunk = FHE_NTT_CHUNK > 0 ? std::max(1, (int)(((size_t)FHE_NTT_CHUNK << 20) / ((size_t)c.N * 8))) : nrows;
