@@ -863,10 +863,14 @@ __global__ void __launch_bounds__(256) k_bconv_moddown(DevCtx c, uint64_t* conv,
                 y0 = y0 >= r * qt ? y0 - r * qt : y0;
                 y1 = y1 >= r * qt ? y1 - r * qt : y1;
             }
+            // centred correction n [P]_{q_t}, n <= KA: predicated subtractions instead of a product
             const uint64_t pm = md->pmod[t];
-            const uint64_t c0 = n0 ? mul_shoup((uint64_t)n0, pm, md->pmod_sh[t], qt) : 0;
-            const uint64_t c1 = n1 ? mul_shoup((uint64_t)n1, pm, md->pmod_sh[t], qt) : 0;
-            *reinterpret_cast<ulonglong2*>(out + (size_t)t * c.N) = make_ulonglong2(sub_mod(y0, c0, qt), sub_mod(y1, c1, qt));
+#pragma unroll
+            for (int r = 1; r <= KA; ++r) {
+                y0 = n0 >= r ? sub_mod(y0, pm, qt) : y0;
+                y1 = n1 >= r ? sub_mod(y1, pm, qt) : y1;
+            }
+            *reinterpret_cast<ulonglong2*>(out + (size_t)t * c.N) = make_ulonglong2(y0, y1);
         }
     }
 }
