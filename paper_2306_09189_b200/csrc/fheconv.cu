@@ -1560,7 +1560,6 @@ void conv_paper_batch(fhe_ctx* c, const fhe_ct* const* cts, int S, const fhe_con
         TmaMaps tm{};
         tma_rows(c, level, tm);
         const uint32_t sg = (uint32_t)tma_sources(S), P2 = 256u / sg;
-        const size_t keyw = (size_t)c->dnum * 2 * c->np * N;
         uint64_t nkeys = 0;
         for (int v : PK.kidx) nkeys += v >= 0;
         const uint64_t dk[4] = {N, (uint64_t)c->np, 2ull * c->dnum, std::max<uint64_t>(1, nkeys)};
