@@ -2838,8 +2838,10 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
         const size_t SC = std::max<size_t>(1, std::min<size_t>({n, (size_t)256, ((size_t)4 << 30) / per_src}));
         uint64_t *buf = nullptr, *dig = nullptr, *XT = nullptr;
         uint64_t** outp = nullptr;  // device table of the keyed outputs' residue buffers (ModDown writes there)
-        std::vector<uint64_t*> hostp;
+        uint64_t** inp = nullptr;   // device table of the chunk's input residue buffers (one gather launch)
+        std::vector<uint64_t*> hostp, hostin;
         if (KK) {
+            inp = (uint64_t**)c->alloc(SC);
             buf = c->alloc(SC * ctw);
             dig = c->alloc(SC * dw);
             XT = c->alloc(SC * KK * 2 * extw);
@@ -2848,9 +2850,17 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
         for (size_t s0 = 0; s0 < n; s0 += SC) {
             const size_t sn = std::min(SC, n - s0);
             if (KK) {
-                for (size_t s = 0; s < sn; ++s)
-                    ck(cudaMemcpyAsync(buf + s * ctw, cts[s0 + s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st),
+                if (sn >= 32) {  // many inputs: one gather launch instead of a copy per ciphertext (~4 us each)
+                    hostin.resize(sn);
+                    for (size_t s = 0; s < sn; ++s) hostin[s] = cts[s0 + s]->d;
+                    ck(cudaMemcpyAsync(inp, hostin.data(), sn * sizeof(uint64_t*), cudaMemcpyHostToDevice, c->st),
                        "memcpy");
+                    gather_ptrs(buf, inp, ctw, (int)sn, c->st);
+                } else {
+                    for (size_t s = 0; s < sn; ++s)
+                        ck(cudaMemcpyAsync(buf + s * ctw, cts[s0 + s]->d, ctw * 8, cudaMemcpyDeviceToDevice, c->st),
+                           "memcpy");
+                }
                 // operand-form digits and P-scaled ciphertexts (k_ks_hoist_opf: FP64 products on
                 // the rows q < 2^50); buf then holds [P c]_q in operand form
                 modup_batch(c, buf + (size_t)nr * N, ctw, (int)sn, level, dig, 1);
@@ -2944,6 +2954,7 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
         c->release(XT);
         c->release(dig);
         c->release(buf);
+        c->release(inp);
     }
 }
 

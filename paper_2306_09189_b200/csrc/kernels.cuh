@@ -368,6 +368,8 @@ struct GiantSel {
 };
 // yc[s][g] = Y(s, idx[g]).c1 rows and (yc0 != null) yc0[s][g] = to_opf(Y(s, idx[g]).c0 rows),
 // Y(s, j) = Y + s * ys + j * 2 ne N ([2][ne][N] QP accumulators), one launch
+// dst[s][words] = *srcp[s] for a device table of nsrc source pointers (words even), one launch
+void gather_ptrs(uint64_t* dst, const uint64_t* const* srcp, size_t words, int nsrc, cudaStream_t st);
 void giant_gather(const DevCtx& c, uint64_t* yc, uint64_t* yc0, const uint64_t* Y, size_t ys, int sc, const GiantSel& gs,
                   int level, cudaStream_t st);
 void rows_to_limb(const DevCtx& c, uint64_t* dst, const uint64_t* src, size_t nrows, const RowMap& rm,
