@@ -136,6 +136,27 @@ def test_cfg3_hoisted_rotation_batch16_bit_exact(oracle):
         assert np.abs(p.ctx.decrypt(outs[i * len(ks)]) - np.roll(zs[i], -ks[0])).max() < TOL
 
 
+def test_cfg2_hoisted_rotation_batch40_gathered_inputs_bit_exact(oracle):
+    """batches of >= 32 ciphertexts gather their inputs through a device pointer table
+    (k_gather_ptrs, one launch): BASELINE cfg2's building block (one batched keyed rotation of all
+    ciphertexts, power-of-two keys) plus an identity amount, members 0 / 17 / 39 vs the golden model"""
+    p = pair(oracle, "cfg2")
+    ks = [4, 0, -16]
+    p.ctx.gen_galois_keys([k for k in ks if k])
+    rng = np.random.default_rng(47)
+    n = 40
+    zs = [rng.uniform(-1, 1, p.ctx.slots) for _ in range(n)]
+    cts = [p.ctx.encrypt(p.ctx.encode(z), ENC_SEED + 700 + i) for i, z in enumerate(zs)]
+    outs = [p.ctx.encrypt(p.ctx.encode(np.zeros(8)), 1) for _ in range(n * len(ks))]
+    p.ctx.rotate_hoisted_batch_into(cts, ks, outs)
+    for i in (0, 17, 39):
+        ctr = p.ck.encrypt(p.ck.encode(zs[i], p.ck.scale, p.top), p.top, ENC_SEED + 700 + i)
+        ref = p.ck.rotate_hoisted(ctr, p.top, ks)
+        for j, kk in enumerate(ks):
+            assert np.array_equal(outs[i * len(ks) + j].residues(), ref[j]), (i, kk)
+        assert np.abs(p.ctx.decrypt(outs[i * len(ks)]) - np.roll(zs[i], -ks[0])).max() < TOL
+
+
 # ------------------------------------------------------------------ bias / output_scale
 
 def bias_case(oracle, gb, name):
