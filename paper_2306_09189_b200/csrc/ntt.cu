@@ -113,6 +113,9 @@ __device__ __forceinline__ void tw_ld(const double2* p, double2* o, int cnt) {
 #ifndef FHE_NTTF_MINB
 #define FHE_NTTF_MINB 1  // CTAs per SM the single-launch kernel is compiled for
 #endif
+#ifndef FHE_NTTPF_MINB
+#define FHE_NTTPF_MINB 4  // CTAs per SM the prefetching row phase is compiled for
+#endif
 #ifndef FHE_NTT_CHUNK
 #define FHE_NTT_CHUNK 0  // MB of rows per NTT launch pair (0: all rows in one pair)
 #endif
@@ -463,10 +466,11 @@ __device__ __forceinline__ uint32_t perm_index_n(uint32_t k, uint32_t g, int log
 // TWS (k_ntt_rows_tw): the twiddles of the CTA's BPC blocks are read from the shared-memory
 // table `twsm` (entry ((BPC + bi) << sigma) + x of stage sigma: the global table's index
 // with N1 + blk replaced by BPC + bi), filled once per CTA and reused for several rows.
-template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE, int XCH, bool TWS = false>
+// PRE (k_ntt_rows_pf, forward): the thread's 16 input residues were loaded by the caller (`pre`).
+template <int LOG_N1, int LOG_B, bool INVERSE, int FUSE, int XCH, bool TWS = false, bool PRE = false>
 __device__ __forceinline__ void rows_phase(const DevCtx& c, uint64_t* data, const RowMap& rm, const NttFuse& fz, int row,
                                            int u, int bx, uint64_t* sm, uint64_t* stage,
-                                           const uint64_t* twsm = nullptr) {
+                                           const uint64_t* twsm = nullptr, const uint64_t* pre = nullptr) {
     constexpr int N1 = 1 << LOG_N1;
     constexpr int C = NTT_THREADS / (N1 / EPT);
     constexpr int B = 1 << LOG_B;
@@ -491,7 +495,10 @@ __device__ __forceinline__ void rows_phase(const DevCtx& c, uint64_t* data, cons
     uint64_t w[EPT];
     // input: forward stride-TPB residues (pass 1 positions lt + k TPB), inverse 16
     // contiguous residues lt 16 + e
-    if (XCH && !INVERSE) {
+    if (PRE) {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) w[e] = pre[e];
+    } else if (XCH && !INVERSE) {
         const uint32_t sb = (uint32_t)__cvta_generic_to_shared(stage) + (uint32_t)(blk * C) * 8u;
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
@@ -657,6 +664,49 @@ __global__ void __launch_bounds__(NTT_THREADS, 4) k_ntt_rows_tw(DevCtx c, uint64
         if (!skip_row(rm, row, u))
             rows_phase<LOG_N1, LOG_B, INVERSE, FUSE, 0, true>(c, data, rm, fz, row, u, blockIdx.x, sm, nullptr, twsm);
         __syncwarp();  // the next row reuses the exchange buffer
+    }
+}
+
+// Forward row phase with a software prefetch: a CTA transforms the same blocks of R rows of one
+// prime and loads the 16 residues of the next row into registers before it transforms the current
+// one, so the global-load latency (the row phase's first stall) overlaps the butterflies; the
+// rows' common twiddles stay in L1. Opt-in (FHE_NTT_PF=R).
+template <int LOG_N1, int LOG_B, int FUSE>
+__global__ void __launch_bounds__(NTT_THREADS, FHE_NTTPF_MINB) k_ntt_rows_pf(DevCtx c, uint64_t* data, RowMap rm, NttFuse fz, int npoly,
+                                                                int R) {
+    constexpr int B = 1 << LOG_B;
+    constexpr int TPB = B / EPT;
+    constexpr int BPC = NTT_THREADS / TPB;
+    using PP = PassPlan<LOG_B, false>;
+    __shared__ uint64_t sm[BPC * (B + (B >> 4))];
+    const int u = blockIdx.y % rm.rows_per_poly, g = blockIdx.y / rm.rows_per_poly;
+    const int bi = threadIdx.x / TPB, lt = threadIdx.x % TPB;
+    const size_t off = (size_t)(blockIdx.x * BPC + bi) * B;
+    const int pend = min(npoly, (g + 1) * R);
+    auto next_row = [&](int pp) {  // first row >= pp of the group that is not skipped, or -1
+        for (; pp < pend; ++pp) {
+            const int row = pp * rm.rows_per_poly + u;
+            if (!skip_row(rm, row, u)) return row;
+        }
+        return -1;
+    };
+    auto load = [&](int row, uint64_t (&w)[EPT]) {
+        const uint64_t* a = data + (size_t)row * c.N + off;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) w[e] = __ldcs(a + PP::pos1(lt, e));
+    };
+    int row = next_row(g * R);
+    if (row < 0) return;
+    uint64_t w[EPT], wn[EPT];
+    load(row, w);
+    while (row >= 0) {
+        const int nxt = next_row(row / rm.rows_per_poly + 1);
+        if (nxt >= 0) load(nxt, wn);
+        rows_phase<LOG_N1, LOG_B, false, FUSE, 0, false, true>(c, data, rm, fz, row, u, blockIdx.x, sm, nullptr, nullptr, w);
+        __syncwarp();  // the next row reuses the exchange buffer
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) w[e] = wn[e];
+        row = nxt;
     }
 }
 
@@ -981,6 +1031,12 @@ static int ntt_tw_rows() {  // read per launch: tests switch it between contexts
     return v < 0 ? 0 : v > 64 ? 64 : v;
 }
 
+static int ntt_pf_rows() {  // read per launch: tests switch it between contexts
+    const char* e = getenv("FHE_NTT_PF");
+    const int v = e ? atoi(e) : 0;
+    return v < 0 ? 0 : v > 64 ? 64 : v;
+}
+
 template <int LOG_N1, int LOG_B>
 void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, bool inverse, int fuse,
                   const NttFuse& fz, cudaStream_t st) {
@@ -1044,6 +1100,24 @@ void ntt_dispatch(const DevCtx& c, uint64_t* data, int nrows, const RowMap& rm, 
                 k_ntt_rows_tw<LOG_N1, LOG_B, true, FUSE_NONE><<<gt, NTT_THREADS, smem, st>>>(c, data, rm, fz, npoly, R);
                 k_ntt_cols<LOG_N1, LOG_B, C, true><<<ga, NTT_THREADS, 0, st>>>(c, data, rm);
             }
+            note_launch(2);
+            return;
+        }
+    }
+    // Opt-in (FHE_NTT_PF=R > 1): forward row phase with the next row's residues prefetched
+    // (k_ntt_rows_pf). Off by default: 1-2 % slower on the B200 at R = 2 / 4 / 8 and at 3 or 4 CTAs
+    // per SM (the second register set spills at 128 registers; profiles/ab_r02_ntt_prefetch.txt).
+    if (!inverse && rm.row0 == 0 && FHE_NTT_CHUNK == 0 && nrows % rm.rows_per_poly == 0) {
+        const int npoly = nrows / rm.rows_per_poly;
+        int R = std::min(ntt_pf_rows(), npoly);
+        while (R > 1 && (size_t)(N1 / BPC) * rm.rows_per_poly * ((npoly + R - 1) / R) < (size_t)148 * 4 * 2) R /= 2;
+        if (R >= 2) {
+            const dim3 ga(B / C, nrows), gt(N1 / BPC, rm.rows_per_poly * ((npoly + R - 1) / R));
+            k_ntt_cols<LOG_N1, LOG_B, C, false><<<ga, NTT_THREADS, 0, st>>>(c, data, rm);
+            if (fuse == FUSE_MODDOWN)
+                k_ntt_rows_pf<LOG_N1, LOG_B, FUSE_MODDOWN><<<gt, NTT_THREADS, 0, st>>>(c, data, rm, fz, npoly, R);
+            else
+                k_ntt_rows_pf<LOG_N1, LOG_B, FUSE_NONE><<<gt, NTT_THREADS, 0, st>>>(c, data, rm, fz, npoly, R);
             note_launch(2);
             return;
         }

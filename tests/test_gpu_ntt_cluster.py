@@ -3,12 +3,14 @@
 * the single-launch cluster NTT (k_ntt_fused: one thread-block cluster per residue row, the
   column -> row intermediate exchanged through distributed shared memory; FHE_NTT_FUSED=1),
   at every ring size with a cluster form (N = 2^13 cfg1, 2^14 cfg2, 2^15 cfg3);
-* the row phase with shared-memory twiddles reused over R rows (k_ntt_rows_tw; FHE_NTT_TWR=R).
+* the row phase with shared-memory twiddles reused over R rows (k_ntt_rows_tw; FHE_NTT_TWR=R);
+* the forward row phase that prefetches the next row's residues (k_ntt_rows_pf; FHE_NTT_PF=R).
 
 Covered: encryption (forward NTT), batched convs (ModUp forward transforms, inverse
 transforms, the fused ModDown + rescale epilogue) and hoisted rotations (ModDown epilogue
-through output pointer tables). Both kernels were measured slower than the default on the
-B200 (profiles/ab_r02_ntt_cluster.txt, profiles/ab_r02_ntt_twiddles.txt) and stay opt-in.
+through output pointer tables). All three were measured slower than the default on the
+B200 (profiles/ab_r02_ntt_cluster.txt, profiles/ab_r02_ntt_twiddles.txt,
+profiles/ab_r02_ntt_prefetch.txt) and stay opt-in.
 
 The transform itself is pinned to the golden model by tests/test_gpu_parity.py (default
 path); this test pins the opt-in kernel to the default one."""
@@ -71,3 +73,7 @@ def test_cluster_ntt_matches_two_launch_transform(cfg, geo):
 def test_shared_twiddle_row_phase_matches_default(cfg, geo, nct, r):
     # batches of 16: enough rows per prime for the R-row groups to be used (two waves of CTAs)
     _ab("FHE_NTT_TWR", r, cfg, geo, nct)
+
+
+def test_prefetching_row_phase_matches_default():
+    _ab("FHE_NTT_PF", "4", "cfg3", (16, 32, 3), 16)
