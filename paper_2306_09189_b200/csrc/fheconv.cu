@@ -112,6 +112,16 @@ struct fhe_ctx {
     std::vector<GraphEntry> graphs;
     // device plaintexts of the pooling stages, keyed by (stage, m, level)
     std::map<std::string, uint64_t*> lt_cache;
+    // encoded plaintexts of the linear head (weight masks, selection masks, bias) in the order
+    // linear_impl uses them, keyed by a hash of (weights, bias, slot -> feature map, level,
+    // scale): a served network re-encodes nothing (<= 4 heads kept, least recently used out)
+    struct LinearEntry {
+        uint64_t key = 0;
+        uint64_t last_use = 0;
+        std::vector<fhe_pt*> pts;
+    };
+    std::vector<LinearEntry> linear_cache;
+    uint64_t linear_clock = 0;
     bool use_graphs = true;
     uint64_t graph_clock = 0;
     struct ProfRec {
@@ -2460,6 +2470,12 @@ void fhe_ctx_destroy(fhe_ctx* c) {
         }
     host_pipe_free(c);
     for (auto& kv : c->lt_cache) cudaFree(kv.second);
+    for (auto& le : c->linear_cache)
+        for (fhe_pt* pt : le.pts)
+            if (pt) {
+                cudaFree(pt->d);
+                delete pt;
+            }
     for (auto& g : c->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     for (int b = 0; b < 2; ++b)
@@ -3715,6 +3731,35 @@ static void linear_impl(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const
     const int level = shards[0]->level;
     if (level < 2) fail(FHE_E_RUNTIME, "depth exhausted");
     auto feat = [&](size_t u, size_t i) -> long { return (long)featmap[u * s + i]; };
+    // plaintext cache (fhe_ctx::linear_cache): the encodes below are host FFTs + uploads,
+    // most of a small network's inference time when repeated per call
+    auto mix = [](uint64_t h, uint64_t v) {
+        h ^= v + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2);
+        return h * 0xff51afd7ed558ccdULL;
+    };
+    uint64_t hk = mix(mix(mix(mix(0x6c696e656172ULL, (uint64_t)level), t), nin), (uint64_t)out_features);
+    {
+        uint64_t sb;
+        memcpy(&sb, &shards[0]->scale, 8);
+        hk = mix(hk, sb);
+        for (size_t i = 0; i < t * s; ++i) hk = mix(hk, (uint64_t)featmap[i]);
+        const uint64_t* wp = reinterpret_cast<const uint64_t*>(w);
+        for (size_t i = 0; i < (size_t)out_features * nin; ++i) hk = mix(hk, wp[i]);
+        const uint64_t* bp = reinterpret_cast<const uint64_t*>(b);
+        for (int i = 0; i < out_features; ++i) hk = mix(hk, bp[i]);
+    }
+    fhe_ctx::LinearEntry* hit = nullptr;
+    for (auto& le : c->linear_cache)
+        if (le.key == hk) hit = &le;
+    std::vector<fhe_pt*> fresh;  // plaintexts encoded by this call (cached on success)
+    size_t next_pt = 0;
+    auto plain = [&](const double* z, int lv, double scale) -> fhe_pt* {
+        if (hit) return hit->pts.at(next_pt++);
+        fhe_pt* pt = nullptr;
+        okc(c, fhe_encode(c, z, s, lv, scale, 0, &pt));
+        fresh.push_back(pt);
+        return pt;
+    };
     std::vector<fhe_ct*> prods, sums;  // freed on any error (e.g. a missing slot-sum key)
     try {
         // products W_o . x_u for every output feature and shard, one level
@@ -3731,12 +3776,10 @@ static void linear_impl(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const
                     any = any || wt[i] != 0.0;
                 }
                 if (!any && started) continue;
-                fhe_pt* pt = nullptr;
+                fhe_pt* pt = plain(wt.data(), level, ql);
                 fhe_ct *pr = nullptr, *rs = nullptr;
-                okc(c, fhe_encode(c, wt.data(), s, level, ql, 0, &pt));
                 okc(c, fhe_mul_plain(c, shards[u], pt, &pr));
                 okc(c, fhe_rescale(c, pr, &rs));
-                fhe_pt_free(pt);
                 fhe_ct_free(pr);
                 prods.push_back(rs);
                 prod_o.push_back(o);
@@ -3767,12 +3810,10 @@ static void linear_impl(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const
             }
             std::fill(sel.begin(), sel.end(), 0.0);
             sel[(size_t)o] = 1.0;
-            fhe_pt* pt = nullptr;
+            fhe_pt* pt = plain(sel.data(), total->level, (double)c->primes[total->level]);
             fhe_ct *pr = nullptr, *rs = nullptr;
-            okc(c, fhe_encode(c, sel.data(), s, total->level, (double)c->primes[total->level], 0, &pt));
             okc(c, fhe_mul_plain(c, total, pt, &pr));
             okc(c, fhe_rescale(c, pr, &rs));
-            fhe_pt_free(pt);
             fhe_ct_free(pr);
             fhe_ct_free(total);
             if (!acc) {
@@ -3787,11 +3828,9 @@ static void linear_impl(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const
         }
         std::vector<double> bias(s, 0.0);
         for (int o = 0; o < out_features; ++o) bias[(size_t)o] = b[o];
-        fhe_pt* bp = nullptr;
-        okc(c, fhe_encode(c, bias.data(), s, acc->level, acc->scale, 0, &bp));
+        fhe_pt* bp = plain(bias.data(), acc->level, acc->scale);
         fhe_ct* res = nullptr;
         okc(c, fhe_add_plain(c, acc, bp, &res));
-        fhe_pt_free(bp);
         fhe_ct_free(acc);
         *out = res;
     } catch (...) {
@@ -3799,7 +3838,24 @@ static void linear_impl(fhe_ctx* c, const fhe_ct* const* shards, size_t t, const
             if (x) fhe_ct_free(x);
         for (fhe_ct* x : sums)
             if (x) fhe_ct_free(x);
+        for (fhe_pt* x : fresh) fhe_pt_free(x);
         throw;
+    }
+    if (hit) {
+        hit->last_use = ++c->linear_clock;
+    } else {
+        if (c->linear_cache.size() >= 4) {  // evict the least recently used head
+            size_t lru = 0;
+            for (size_t i = 1; i < c->linear_cache.size(); ++i)
+                if (c->linear_cache[i].last_use < c->linear_cache[lru].last_use) lru = i;
+            for (fhe_pt* x : c->linear_cache[lru].pts) fhe_pt_free(x);
+            c->linear_cache.erase(c->linear_cache.begin() + (long)lru);
+        }
+        fhe_ctx::LinearEntry le;
+        le.key = hk;
+        le.last_use = ++c->linear_clock;
+        le.pts = std::move(fresh);
+        c->linear_cache.push_back(std::move(le));
     }
 }
 

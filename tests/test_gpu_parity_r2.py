@@ -286,3 +286,35 @@ def test_keygen_after_captured_conv_graph(oracle, golden):
     ctr = ck.encrypt(ck.encode(img, ck.scale, top), top, ENC_SEED + 1)
     ref, _ = ck.conv(ctr, top, c, m, k, co, filt, 5)
     assert np.array_equal(outs[1].residues(), ref)
+
+
+def test_linear_head_plaintext_cache(oracle):
+    """fhe_linear keeps the encoded weight / selection / bias plaintexts of a head (keyed by a hash
+    of weights, bias, feature map, level and scale): a second call with the same head reuses them and
+    gives identical residues; other weights, another bias or another input level miss the cache and
+    give their own results (reference linear() dense.cpp:34-75 has no state to get stale)."""
+    p = pair(oracle, "cfg1")
+    rng = np.random.default_rng(91)
+    c, m, no = 4, 32, 3
+    p.ctx.gen_galois_keys([1 << i for i in range(12)])
+    x = rng.uniform(-1, 1, p.ctx.slots)
+    ct = p.ctx.encrypt(p.ctx.encode(x), ENC_SEED + 900)
+    w1, b1 = rng.uniform(-1, 1, no * c * m * m), rng.uniform(-1, 1, no)
+    w2, b2 = rng.uniform(-1, 1, no * c * m * m), rng.uniform(-1, 1, no)
+
+    def want(w, b):
+        return w.reshape(no, -1) @ x + b
+
+    first = p.ctx.linear([ct], c, m, w1, b1)
+    other = p.ctx.linear([ct], c, m, w2, b1)       # miss: other weights
+    biased = p.ctx.linear([ct], c, m, w1, b2)      # miss: other bias
+    again = p.ctx.linear([ct], c, m, w1, b1)       # hit
+    assert np.array_equal(first.residues(), again.residues())
+    for out, (w, b) in ((first, (w1, b1)), (other, (w2, b1)), (biased, (w1, b2)), (again, (w1, b1))):
+        y = want(w, b)
+        assert (np.abs(p.ctx.decrypt(out)[:no] - y) / np.maximum(1.0, np.abs(y))).max() < TOL
+    # five more heads evict the first (4 kept); it is re-encoded and still right
+    for i in range(5):
+        p.ctx.linear([ct], c, m, rng.uniform(-1, 1, no * c * m * m), b1)
+    back = p.ctx.linear([ct], c, m, w1, b1)
+    assert np.array_equal(first.residues(), back.residues())
