@@ -2866,7 +2866,11 @@ static void rotate_hoisted_batch_impl(fhe_ctx* c, const fhe_ct* const* cts, size
         for (size_t s0 = 0; s0 < n; s0 += SC) {
             const size_t sn = std::min(SC, n - s0);
             if (KK) {
-                if (sn >= 32) {  // many inputs: one gather launch instead of a copy per ciphertext (~4 us each)
+                static const size_t gather_min = [] {  // FHECONV_GATHER_MIN: batch size from which inputs are gathered
+                    const char* e = getenv("FHECONV_GATHER_MIN");
+                    return (size_t)(e ? std::max(1, atoi(e)) : 8);  // A/B at cfg3 batch 16: 8 is 1.5-4 % faster than 32
+                }();
+                if (sn >= gather_min) {  // many inputs: one gather launch instead of a copy per ciphertext (~4 us each)
                     hostin.resize(sn);
                     for (size_t s = 0; s < sn; ++s) hostin[s] = cts[s0 + s]->d;
                     ck(cudaMemcpyAsync(inp, hostin.data(), sn * sizeof(uint64_t*), cudaMemcpyHostToDevice, c->st),
