@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfheconv.so")
-SOURCES = ["ntt.cu", "kernels.cu", "fheconv.cu"]
+SOURCES = ["ntt.cu", "kernels.cu", "matvec.cu", "fheconv.cu"]
 HEADERS = ["kernels.cuh", "modarith.cuh", "host_math.hpp", "cdt_table.h"]
 
 NVCC_FLAGS = [
@@ -23,6 +23,9 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
     "-Xptxas", "-O3",
+    # no -split-compile: it halves the build time but makes code generation depend on how a
+    # translation unit's kernels are partitioned (k_pt_matvec2 a third slower, k_bsgs_tma +-2 %
+    # as kernels move between files; profiles/ab_r02_split_compile.txt)
     "-I", os.path.join(ROOT, "include"),
 ]
 
@@ -46,20 +49,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     objs = []
+    jobs = []  # the translation units compile side by side (kernels.cu alone is ~2 minutes)
     hdr = [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(ROOT, "include", "fheconv.h")]
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         deps = [os.path.join(CSRC, src)] + hdr
+        objs.append(obj)
         if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps
                                                      if os.path.exists(d)):
-            objs.append(obj)
             continue
         cmd = [_nvcc(), *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        jobs.append((cmd, subprocess.Popen(cmd)))
+    failed = [cmd for cmd, pr in jobs if pr.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     tmp = LIB + ".tmp"
     subprocess.run([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs],
                    check=True)
